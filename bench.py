@@ -1,0 +1,394 @@
+"""Benchmark: fwd+bwd iterations/s of the half-Gaussian rasterizer (BASELINE.json).
+
+Workload (N=1): config c3 -- 1M half-Gaussians, SH degree 3, 1920x1080, one
+view, fixed cotangent.  One step = prepare (K1-K4) + render
+(K5) + render_backward (K6, K7) with the scene resident in HBM.  Under torchrun
+(N>1) every rank renders its own view of the same scene (camera jittered per
+rank) and the per-Gaussian gradient buffer is all-reduced over NCCL each step:
+multi-view data-parallel training, weak scaling.
+
+Printed JSON line (rank 0): value = whole-job views/s; e2e = the same iteration
+through the drop-in numpy API (paper_2406_02720_b200.rasterizer) with host
+buffers and every H2D/D2H copy inside the timed region; roofline = the FP32
+roofline of the dominant kernel (blend backward) from CUDA events recorded
+around it inside the timed region; cpu_baseline = the CPU oracle port timed on
+this host.  `--impl reference` times the CPU oracle port (the reference's own
+path restated in C, all host threads) on the same config instead.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+FWD_FLOPS_PER_EVAL = 46    # _blend_cy.pyx:153-176
+BWD_FLOPS_PER_EVAL = 112   # _blend_cy.pyx:290-335
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-clocks", action="store_true")
+    return ap.parse_args()
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index, enabled=True):
+        self.proc = None
+        self.path = os.path.join(REPO, "gpurun_out", f"clocks_gpu{gpu_index}.csv")
+        self.gpu_index = gpu_index
+        if not enabled:
+            return
+        try:
+            os.makedirs(os.path.dirname(self.path), exist_ok=True)
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={gpu_index}", f"--query-gpu={self.QUERY}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.fh, stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.fh.close()
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        with open(self.path) as fh:
+            for line in fh:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    sm.append(float(parts[1]))
+                    mx = max(mx, float(parts[2]))
+                except ValueError:
+                    continue
+                for name, val in zip(names, parts[5:9]):
+                    if val.lower() == "active":
+                        reasons.add(name)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def rank_info():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def jitter_camera(cam_kw, rank):
+    """Per-rank view of the same scene: a small sideways camera translation."""
+    kw = dict(cam_kw)
+    w2c = np.array(kw["world_to_cam"], dtype=np.float64)
+    if rank:
+        w2c = w2c.copy()
+        w2c[0, 3] += 0.02 * rank
+        w2c[1, 3] -= 0.01 * rank
+    kw["world_to_cam"] = w2c
+    return kw
+
+
+# --------------------------------------------------------------------------
+def run_reference_arm(args):
+    """The reference's CPU path (oracle port, all host threads) on the same config."""
+    world, rank, _ = rank_info()
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    from paper_2406_02720_b200 import scenes
+    sa = scenes.make_config(args.config).as_float64()
+    cam = sa.cameras[0]
+    threads = os.cpu_count() or 1
+
+    class Cam:
+        pass
+
+    c = Cam()
+    for k, v in cam.items():
+        setattr(c, k, v)
+    c.near_clip = 0.01
+    d_color = scenes.cotangent(cam["height"], cam["width"])
+    backward = scenes.CONFIGS[args.config]["backward"]
+
+    def step():
+        out = O.render(sa, c, threads=threads)
+        if backward:
+            O.render_backward(sa, c, out, d_color, threads=threads)
+
+    t0 = time.perf_counter()
+    step()
+    first = time.perf_counter() - t0
+    budget = 150.0
+    warm = min(args.warmup, max(0, int(budget * 0.2 / max(first, 1e-3))))
+    for _ in range(warm):
+        step()
+    n_run = max(1, min(args.steps, int(budget / max(first, 1e-3))))
+    times = []
+    for _ in range(n_run):
+        t0 = time.perf_counter()
+        step()
+        times.append(time.perf_counter() - t0)
+    ms = 1e3 * statistics.mean(times)
+    value = 1e3 / ms
+    unit = "iters/s" if backward else "frames/s"
+    line = {
+        "impl": "reference", "metric": metric_name(args.config), "value": value, "unit": unit,
+        "n_gpus": world, "steps": n_run, "warmup": warm, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": bench_config(args.config, world),
+        "cpu_baseline": {"value": value, "unit": unit, "cores": threads, "kind": "port",
+                         "sample": f"{n_run} full {args.config} iterations (prepare+render"
+                                   f"{'+render_backward' if backward else ''}) of the C oracle "
+                                   f"port, {threads} OpenMP threads; requested steps {args.steps}"},
+        "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def metric_name(cfg):
+    return "fwd+bwd iters/s (1M half-Gaussians, 1080p)" if cfg == "c3" else \
+        f"fwd+bwd iters/s ({cfg})"
+
+
+def bench_config(cfg, world):
+    from paper_2406_02720_b200 import scenes
+    c = scenes.CONFIGS[cfg]
+    n, sh, w, h = c["args"][:4]
+    return {"workload": f"{cfg}: {c['kind']} {n} half-Gaussians, SH{sh}, {w}x{h}, one view per "
+                        f"rank per step, fwd+bwd with fixed cotangent",
+            "gaussians": n, "width": w, "height": h, "sh_degree": sh,
+            "views_per_step": world, "parallelism": f"dp{world} (views)",
+            "l2": "inputs larger than L2 (scene 252 MB + 64 MB records per view at c3)"}
+
+
+# --------------------------------------------------------------------------
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference_arm(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    from paper_2406_02720_b200 import _native, device, scenes
+    from paper_2406_02720_b200 import rasterizer as dropin
+    from paper_2406_02720_b200.geometry import CameraModel, Scene
+    from paper_2406_02720_b200.multiview import GradientAllReduce
+
+    world, rank, local = rank_info()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    lib = _native.load()
+
+    sa = scenes.make_config(args.config)
+    cam = CameraModel(**jitter_camera(sa.cameras[0], rank))
+    scene = Scene(*(getattr(sa, f) for f in sa.FIELDS), sh_degree=sa.sh_degree,
+                  background_color=sa.background_color, device="cuda", dtype=torch.float32)
+    d_color = torch.as_tensor(scenes.cotangent(cam.height, cam.width), dtype=torch.float32,
+                              device="cuda")
+    grads = device.DeviceGradientSet.empty_flat(scene)
+    reducer = GradientAllReduce(grads) if world > 1 else None
+    timer = device.StageTimer()
+
+    def step(t=None):
+        out = device.render(scene, cam, timer=t)
+        device.render_backward(scene, cam, out, d_color, grads=grads, timer=t)
+        if reducer is not None:
+            reducer.allreduce()
+        return out
+
+    def fwd_step():
+        return device.render(scene, cam)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    barrier()
+    clocks = ClockSampler(local, enabled=not args.no_clocks)
+    launches0 = _native.launch_count()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    start.record()
+    for _ in range(args.steps):
+        out = step(timer)
+    end.record()
+    barrier()
+    clock_info = clocks.stop()
+    launches = _native.launch_count() - launches0
+    ms = start.elapsed_time(end) / args.steps
+    ms_t = torch.tensor([ms], device="cuda")
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+    stage_ms = {k: statistics.mean(v) for k, v in timer.totals().items()}
+
+    # forward-only frames/s (prepare + render), same timing discipline
+    for _ in range(3):
+        fwd_step()
+    barrier()
+    start.record()
+    for _ in range(args.steps):
+        fwd_step()
+    end.record()
+    barrier()
+    fwd_ms = start.elapsed_time(end) / args.steps
+
+    # algorithmic work of the dominant kernels
+    term = out.terminal.to(torch.int64)
+    starts = torch.as_tensor(out.frame.export()["tile_starts"], device="cuda")
+    lens = (starts[1:] - starts[:-1]).reshape(out.frame.tiles_y, out.frame.tiles_x)
+    lens_px = lens.repeat_interleave(16, 0).repeat_interleave(16, 1)[:cam.height, :cam.width]
+    fwd_evals = int(torch.minimum(term + 1, lens_px).sum().item())
+    bwd_evals = int(term.sum().item())
+    import ctypes
+    a, b = ctypes.c_double(0), ctypes.c_double(0)
+    _native.check(lib.hs_measure_fp32_peaks(ctypes.byref(a), ctypes.byref(b)), "peaks")
+    fp32_peak = a.value
+    bwd_ms = stage_ms.get("blend_bwd", float("nan"))
+    fwd_k_ms = stage_ms.get("blend_fwd", float("nan"))
+    achieved = bwd_evals * BWD_FLOPS_PER_EVAL / (bwd_ms * 1e-3) / 1e12
+    roofline = {
+        "bound": "fp32", "kernel": "blend_bwd (K6)", "achieved": achieved, "peak": fp32_peak,
+        "unit": "TFLOP/s", "frac": achieved / fp32_peak, "traffic": None,
+        "peak_source": "measured on this GPU by hs_measure_fp32_peaks (FMA probe; "
+                       "MEASURED_PEAKS.json has no FP32 entry)",
+        "algorithmic": f"{bwd_evals} bwd evals x {BWD_FLOPS_PER_EVAL} flops per launch",
+        "kernel_ms": bwd_ms,
+        "share_of_step": bwd_ms / ms,
+        "blend_fwd": {"kernel_ms": fwd_k_ms, "evals": fwd_evals,
+                      "achieved_tflops": fwd_evals * FWD_FLOPS_PER_EVAL / (fwd_k_ms * 1e-3) / 1e12},
+        "stage_ms": stage_ms,
+        "ex2_gops_peak": b.value,
+    }
+
+    # end-to-end through the drop-in numpy API, host buffers, copies inside
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, sa, cam, dropin, world, barrier, torch, dist)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args.config)
+
+    value = world * 1e3 / ms
+    if rank == 0:
+        line = {
+            "metric": metric_name(args.config), "value": value, "unit": "iters/s",
+            "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32 blend / f64 geometry", "data": "synthetic",
+            "config": bench_config(args.config, world),
+            "fwd_fps": world * 1e3 / fwd_ms, "fwd_ms_per_frame": fwd_ms,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches, "clocks": clock_info,
+            "counts": {"P": out.frame.num_pairs, "fwd_evals": fwd_evals, "bwd_evals": bwd_evals},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(args, sa, cam, dropin, world, barrier, torch, dist):
+    """Same iteration through rasterizer.render/render_backward with host buffers."""
+
+    class HostScene:
+        pass
+
+    hs = HostScene()
+    for f in sa.FIELDS:
+        setattr(hs, f, torch.from_numpy(getattr(sa, f)).pin_memory())
+    hs.sh_degree = sa.sh_degree
+    hs.background_color = sa.background_color
+    from paper_2406_02720_b200 import scenes
+    d_color = scenes.cotangent(cam.height, cam.width)
+
+    def step():
+        out = dropin.render(hs, cam)
+        g = dropin.render_backward(hs, cam, out, d_color)
+        return out, g
+
+    for _ in range(2):
+        step()
+    barrier()
+    t0 = time.perf_counter()
+    n = max(2, min(args.steps, 5))
+    for _ in range(n):
+        out, g = step()
+    barrier()
+    ms = (time.perf_counter() - t0) * 1e3 / n
+    ms_t = torch.tensor([ms], device="cuda")
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+    h2d = sum(getattr(sa, f).nbytes for f in sa.FIELDS) + d_color.size * 4
+    d2h = (out.color.size + out.alpha.size + out.depth.size + out.transmittance.size) * 4 + \
+        out.per_pixel_terminal_index.nbytes + out.radii.nbytes + \
+        sum(getattr(sa, f).nbytes for f in sa.FIELDS) + len(sa) * 8
+    return {"value": world * 1e3 / ms, "unit": "iters/s", "ms_per_step": ms, "steps": n,
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "api": "paper_2406_02720_b200.rasterizer.render + render_backward (numpy in/out; "
+                   "pinned host scene)"}
+
+
+def cpu_baseline(cfg):
+    """Oracle port (C, all host threads) on one full iteration of the same config."""
+    from oracle import oracle as O
+    from paper_2406_02720_b200 import scenes
+    sa = scenes.make_config(cfg).as_float64()
+    cam = dict(sa.cameras[0])
+
+    class Cam:
+        pass
+
+    c = Cam()
+    for k, v in cam.items():
+        setattr(c, k, v)
+    c.near_clip = 0.01
+    threads = os.cpu_count() or 1
+    d_color = scenes.cotangent(cam["height"], cam["width"])
+    t0 = time.perf_counter()
+    out = O.render(sa, c, threads=threads)
+    O.render_backward(sa, c, out, d_color, threads=threads)
+    sec = time.perf_counter() - t0
+    return {"value": 1.0 / sec, "unit": "iters/s", "cores": threads, "kind": "port",
+            "sample": f"1 full {cfg} iteration (prepare+render+render_backward) of the C oracle "
+                      f"port, {threads} OpenMP threads, {sec:.2f} s"}
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,201 @@
+/*
+ * halfsplat_b200.h -- C ABI of the B200-native half-Gaussian rasterizer.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ * (halfsplat.rasterizer.prepare -> render -> render_backward and its blend-core
+ * plugin).  Every entry point is extern "C", takes plain pointers and sizes,
+ * returns an int status (HS_OK or one of the HS_ERR_* codes that mirror the
+ * reference's exceptions) and never throws.  Citations are into the reference
+ * tree (/root/reference/pkg/src/halfsplat/...).
+ *
+ * Two seams are exported:
+ *
+ *  Seam 1 -- blend-core plugin (host pointers, float64, reference layout).
+ *    hs_forward_tiles / hs_backward_tiles replace the Cython module's
+ *    forward_tiles / backward_tiles (_blend_cy.pyx:74-83, 190-199; the contract
+ *    is documented in _blend_py.py:1-19).  The backend seam that selects them
+ *    is backend.py:26-48.  Arrays are the caller's; only pixels and pair rows of
+ *    tiles in [tile_lo, tile_hi) are written (pair rows are accumulated, +=).
+ *
+ *  Seam 2 -- staged device pipeline (device pointers, one cudaStream_t).
+ *    hs_preprocess_fwd      <- rasterizer.prepare projection/cull/SH part
+ *                              (rasterizer.py:159-298)
+ *    hs_bin_and_sort        <- pair expansion + np.lexsort + searchsorted
+ *                              (rasterizer.py:300-325)
+ *    hs_blend_fwd           <- render's forward_tiles calls (rasterizer.py:351-383)
+ *    hs_blend_bwd           <- render_backward's backward_tiles calls
+ *                              (rasterizer.py:386-418)
+ *    hs_preprocess_bwd      <- np.add.at merge + _geometry_backward
+ *                              (rasterizer.py:419-575)
+ *    Workspaces are caller-allocated from the *_workspace_size queries; the
+ *    library never allocates on this seam.  Calls on distinct frames/streams are
+ *    independent (re-entrant).
+ */
+#ifndef HALFSPLAT_B200_H
+#define HALFSPLAT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (mirror errors.py) ---------------------------------- */
+#define HS_OK 0
+#define HS_ERR_EMPTY_SCENE 1        /* errors.EmptyScene      (rasterizer.py:161-162) */
+#define HS_ERR_IMAGE_TOO_LARGE 2    /* errors.ImageTooLarge   (rasterizer.py:163-164) */
+#define HS_ERR_INVALID_KERNEL 3     /* ValueError on kernel   (rasterizer.py:165-166) */
+#define HS_ERR_MISMATCHED_FORWARD 4 /* errors.MismatchedForward (rasterizer.py:390-398) */
+#define HS_ERR_INVALID_ARG 5
+#define HS_ERR_CUDA 6
+#define HS_ERR_WORKSPACE 7          /* workspace missing or too small */
+
+#define HS_DTYPE_F32 0
+#define HS_DTYPE_F64 1
+
+#define HS_KERNEL_HALF 0
+#define HS_KERNEL_FULL 1
+
+#define HS_TILE 16
+#define HS_PAIR_GRAD_COLS 12
+
+/* Pinhole camera, geometry.py:210-273 (world_to_cam row-major 4x4). */
+typedef struct hs_camera {
+  double world_to_cam[16];
+  double fx, fy, cx, cy;
+  double near_clip;
+  double center[3]; /* camera centre in world coords, -R^T t (geometry.py:266-269) */
+  int32_t width, height;
+} hs_camera;
+
+/* Struct-of-arrays scene, geometry.py:364-383.  Device pointers, all of one
+ * dtype (HS_DTYPE_F32 or HS_DTYPE_F64), C-contiguous:
+ *   mu (n,3)  log_scale (n,3)  rotation (n,4) wxyz unnormalised
+ *   sh_coeffs (n,(deg+1)^2,3)  normal (n,3)  raw_opacity_a/b (n,)          */
+typedef struct hs_scene {
+  int64_t n;
+  int32_t sh_degree;
+  int32_t dtype;
+  const void* mu;
+  const void* log_scale;
+  const void* rotation;
+  const void* sh_coeffs;
+  const void* normal;
+  const void* raw_opacity_a;
+  const void* raw_opacity_b;
+  double background[3];
+} hs_scene;
+
+/* Per-view frame state.  Filled by hs_frame_init / hs_preprocess_fwd /
+ * hs_bin_and_sort; the caller owns the two workspaces it points into. */
+typedef struct hs_frame {
+  int64_t n;            /* primitives in the scene */
+  int32_t width, height;
+  int32_t tiles_x, tiles_y, n_tiles;
+  int32_t kernel;       /* HS_KERNEL_HALF / HS_KERNEL_FULL */
+  int32_t tile_bits;    /* significant bits of the pair sort key */
+  int32_t sort_selector;/* internal: which pair double-buffer holds the result */
+  int64_t num_pairs;    /* P, valid after hs_frame_read_num_pairs */
+  void* frame_ws;       /* size hs_frame_workspace_size(n, width, height) */
+  size_t frame_ws_bytes;
+  void* bin_ws;         /* size hs_binning_workspace_size(num_pairs, ...) */
+  size_t bin_ws_bytes;
+} hs_frame;
+
+/* ---- Seam 2: staged device pipeline ----------------------------------- */
+
+/* Validates sizes (EmptyScene / ImageTooLarge / kernel) and fills the static
+ * fields of *frame.  Workspace pointers are left for the caller to set. */
+int hs_frame_init(hs_frame* frame, int64_t n, int32_t width, int32_t height,
+                  int32_t kernel);
+size_t hs_frame_workspace_size(int64_t n, int32_t width, int32_t height);
+size_t hs_binning_workspace_size(int64_t n, int64_t num_pairs, int32_t width,
+                                 int32_t height);
+
+/* K1 preprocess (one thread per Gaussian, FP64 geometry) + depth-rank sort +
+ * per-splat tile counts and their scan.  radii (n,) int32 is optional
+ * (ceil of the 3.5-sigma radius, 0 when culled). */
+int hs_preprocess_fwd(hs_frame* frame, const hs_scene* scene,
+                      const hs_camera* cam, int32_t* radii, void* stream);
+
+/* Synchronises `stream` and reads P (the number of (tile, splat) pairs). */
+int hs_frame_read_num_pairs(hs_frame* frame, void* stream);
+
+/* K2 duplicate-with-keys, K3 stable tile sort, K4 tile ranges.  Needs
+ * frame->bin_ws of hs_binning_workspace_size(...) bytes. */
+int hs_bin_and_sort(hs_frame* frame, void* stream);
+
+/* K5 forward blend.  Outputs (device, float32 / int32):
+ * color (H,W,3), alpha (H,W), depth (H,W), transmittance (H,W), terminal (H,W). */
+int hs_blend_fwd(hs_frame* frame, const double* background, float* color,
+                 float* alpha, float* depth, float* transmittance,
+                 int32_t* terminal, void* stream);
+
+/* K6 backward blend for cotangent d_color (H,W,3) float32; consumes the
+ * forward's transmittance and terminal. Writes per-pair partial rows. */
+int hs_blend_bwd(hs_frame* frame, const double* background,
+                 const float* d_color, const float* transmittance,
+                 const int32_t* terminal, void* stream);
+
+/* K7: merge pair rows per splat and chain to the primitive parameters
+ * (GradientSet, rasterizer.py:72-105).  Output pointers are device arrays of
+ * the scene dtype (touch_count int32); culled primitives get zeros. */
+typedef struct hs_grads {
+  void* d_mu;           /* (n,3) */
+  void* d_log_scale;    /* (n,3) */
+  void* d_rotation;     /* (n,4) w.r.t. the raw quaternion */
+  void* d_sh;           /* (n,K,3) */
+  void* d_normal;       /* (n,3) w.r.t. the raw normal */
+  void* d_raw_opacity_a;/* (n,) */
+  void* d_raw_opacity_b;/* (n,) */
+  void* pos_grad_norm;  /* (n,) */
+  int32_t* touch_count; /* (n,) */
+} hs_grads;
+
+int hs_preprocess_bwd(hs_frame* frame, const hs_scene* scene,
+                      const hs_camera* cam, const hs_grads* grads, void* stream);
+
+/* Introspection for parity: the reference's FrameGeometry integers and packed
+ * columns (rasterizer.py:108-147).  Device outputs:
+ *   valid (n,) int32 -- original indices of surviving primitives, first M used
+ *   m_out (1,) int64 -- M
+ *   packed (n,13) float32, mode (n,) int8, tile_rect (n,4) int32 in valid order
+ *   pair_splat (P,) int32 splat-local, tile_starts (n_tiles+1,) int64        */
+int hs_frame_export(const hs_frame* frame, int32_t* valid, int64_t* m_out,
+                    float* packed, int8_t* mode, int32_t* tile_rect,
+                    int32_t* pair_splat, int64_t* tile_starts, void* stream);
+
+/* ---- Seam 1: blend-core plugin (host float64 arrays) ------------------- */
+int hs_forward_tiles(const double* packed, const int8_t* mode,
+                     const int32_t* pair_splat, const int64_t* tile_starts,
+                     int64_t num_splats, int64_t num_pairs, int32_t height,
+                     int32_t width, int32_t tiles_x, const double* background,
+                     double* color, double* alpha, double* depth,
+                     double* transmittance, int32_t* terminal, int32_t tile_lo,
+                     int32_t tile_hi);
+
+int hs_backward_tiles(const double* packed, const int8_t* mode,
+                      const int32_t* pair_splat, const int64_t* tile_starts,
+                      int64_t num_splats, int64_t num_pairs, int32_t height,
+                      int32_t width, int32_t tiles_x, const double* background,
+                      const double* d_color, const double* transmittance,
+                      const int32_t* terminal, double* pair_grads,
+                      int32_t tile_lo, int32_t tile_hi);
+
+/* ---- misc --------------------------------------------------------------- */
+const char* hs_status_string(int status);
+const char* hs_last_cuda_error(void);
+/* Number of kernels this library launched so far (process-wide counter). */
+int64_t hs_kernel_launch_count(void);
+int32_t hs_abi_version(void);
+/* FP32 FMA (TFLOP/s, FMA = 2 flops) and MUFU.EX2 (Gop/s) throughput of the
+ * current device, measured by two probe kernels: the roofline denominators for
+ * the FP32/SFU-bound blend kernels. */
+int hs_measure_fp32_peaks(double* fma_tflops, double* ex2_gops);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HALFSPLAT_B200_H */

@@ -1,0 +1,225 @@
+// hs_binning.cu -- depth-rank sort (K3a), pair counts and their scan,
+// duplicate-with-keys (K2), the stable tile sort (K3b) and tile ranges (K4);
+// plus the FrameGeometry export used by the parity tests.
+//
+// The reference orders pairs with np.lexsort((prim index, depth f64, tile))
+// (rasterizer.py:318-323).  Here the primitives are first ranked once by
+// (depth f64 bits, index) with a stable 64-bit radix sort, pairs are emitted in
+// that rank order, and a stable radix sort on the tile id alone (tile_bits =
+// ceil(log2 n_tiles) bits, two 8-bit passes at 1080p) yields exactly the
+// lexsort order without ever materialising a 64-bit (tile|depth) key.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include "hs_common.cuh"
+#include "hs_internal.h"
+
+namespace hs {
+
+size_t depth_sort_temp_bytes(int64_t n) {
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const uint64_t*)nullptr, (uint64_t*)nullptr,
+                                  (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)n, 0, 64);
+  return bytes;
+}
+
+size_t scan_temp_bytes(int64_t n) {
+  size_t bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, bytes, (const int32_t*)nullptr, (int32_t*)nullptr,
+                                (int)(n + 1));
+  return bytes;
+}
+
+size_t pair_sort_temp_bytes(int64_t p, int tile_bits) {
+  size_t bytes = 0;
+  cub::DoubleBuffer<uint32_t> k(nullptr, nullptr), v(nullptr, nullptr);
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, k, v, (int)(p > 0 ? p : 1), 0,
+                                  tile_bits > 0 ? tile_bits : 1);
+  return bytes;
+}
+
+cudaError_t run_depth_sort(void* temp, size_t temp_bytes, const uint64_t* keys_in,
+                           uint64_t* keys_out, const uint32_t* vals_in, uint32_t* order,
+                           int64_t n, cudaStream_t stream) {
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_in, keys_out, vals_in,
+                                                  order, (int)n, 0, 64, stream);
+  note_launch(9);  // onesweep: histogram + one pass per 8-bit digit
+  return e;
+}
+
+__global__ void gather_counts_kernel(const int32_t* __restrict__ count,
+                                     const uint32_t* __restrict__ order, int32_t* __restrict__ cnt_r,
+                                     uint32_t* __restrict__ rank_of, int64_t n) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r > n) return;
+  if (r == n) {
+    cnt_r[n] = 0;
+    return;
+  }
+  const uint32_t i = order[r];
+  cnt_r[r] = count[i];
+  rank_of[i] = (uint32_t)r;
+}
+
+cudaError_t run_count_scan(void* temp, size_t temp_bytes, const int32_t* count,
+                           const uint32_t* order, int32_t* cnt_r, int32_t* off_r,
+                           uint32_t* rank_of, int64_t n, cudaStream_t stream) {
+  const int block = 256;
+  gather_counts_kernel<<<(unsigned)((n + 1 + block - 1) / block), block, 0, stream>>>(
+      count, order, cnt_r, rank_of, n);
+  note_launch();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  e = cub::DeviceScan::ExclusiveSum(temp, temp_bytes, cnt_r, off_r, (int)(n + 1), stream);
+  note_launch(2);
+  return e;
+}
+
+// K2: one thread per depth rank; a splat's pairs are contiguous, row-major over
+// its tile rect (the reference's `local % spans_x` order, rasterizer.py:312-317),
+// and splats appear in depth-rank order.
+__global__ void duplicate_kernel(const uint32_t* __restrict__ order,
+                                 const int32_t* __restrict__ cnt_r,
+                                 const int32_t* __restrict__ off_r, const int4* __restrict__ rect,
+                                 float* __restrict__ rec, int tiles_x, uint32_t* __restrict__ keys,
+                                 uint32_t* __restrict__ vals, int64_t n) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const int c = cnt_r[r];
+  if (c == 0) return;
+  const uint32_t i = order[r];
+  const int base = off_r[r];
+  rec[(size_t)i * kRecordFloats + R_PAIR_BASE] = __uint_as_float((uint32_t)base);
+  const int4 rc = rect[i];
+  int k = base;
+  for (int ty = rc.z; ty <= rc.w; ++ty) {
+    const uint32_t row = (uint32_t)ty * (uint32_t)tiles_x;
+    for (int tx = rc.x; tx <= rc.y; ++tx, ++k) {
+      keys[k] = row + (uint32_t)tx;
+      vals[k] = i;
+    }
+  }
+}
+
+cudaError_t run_duplicate(const uint32_t* order, const int32_t* cnt_r, const int32_t* off_r,
+                          const int4* rect, float4* rec, int tiles_x, uint32_t* keys,
+                          uint32_t* vals, int64_t n, cudaStream_t stream) {
+  const int block = 256;
+  duplicate_kernel<<<(unsigned)((n + block - 1) / block), block, 0, stream>>>(
+      order, cnt_r, off_r, rect, reinterpret_cast<float*>(rec), tiles_x, keys, vals, n);
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t run_pair_sort(void* temp, size_t temp_bytes, uint32_t* keys0, uint32_t* keys1,
+                          uint32_t* vals0, uint32_t* vals1, int64_t p, int tile_bits,
+                          int* selector, cudaStream_t stream) {
+  cub::DoubleBuffer<uint32_t> k(keys0, keys1), v(vals0, vals1);
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(temp, temp_bytes, k, v, (int)p, 0,
+                                                  tile_bits > 0 ? tile_bits : 1, stream);
+  note_launch(1 + (tile_bits + 7) / 8);
+  *selector = k.selector;
+  return e;
+}
+
+// K4: CSR tile offsets (np.searchsorted(tile_sorted, arange(T+1)),
+// rasterizer.py:324-325).  Every entry is written exactly once.
+__global__ void tile_ranges_kernel(const uint32_t* __restrict__ keys, int64_t p, int n_tiles,
+                                   int32_t* __restrict__ starts) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= p) return;
+  const int t = (int)keys[k];
+  const int tp = k == 0 ? -1 : (int)keys[k - 1];
+  for (int u = tp + 1; u <= t; ++u) starts[u] = (int32_t)k;
+  if (k == p - 1)
+    for (int u = t + 1; u <= n_tiles; ++u) starts[u] = (int32_t)p;
+}
+
+__global__ void fill_i32_kernel(int32_t* __restrict__ a, int64_t n, int32_t v) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) a[k] = v;
+}
+
+cudaError_t run_tile_ranges(const uint32_t* sorted_keys, int64_t p, int n_tiles,
+                            int32_t* tile_starts, cudaStream_t stream) {
+  const int block = 256;
+  if (p == 0) {
+    fill_i32_kernel<<<(unsigned)((n_tiles + 1 + block - 1) / block), block, 0, stream>>>(
+        tile_starts, n_tiles + 1, 0);
+  } else {
+    tile_ranges_kernel<<<(unsigned)((p + block - 1) / block), block, 0, stream>>>(
+        sorted_keys, p, n_tiles, tile_starts);
+  }
+  note_launch();
+  return cudaGetLastError();
+}
+
+// ---- FrameGeometry export (introspection / parity only) ------------------
+__global__ void visible_flags_kernel(const int32_t* __restrict__ count, int32_t* __restrict__ flags,
+                                     int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i > n) return;
+  flags[i] = (i < n && count[i] > 0) ? 1 : 0;
+}
+
+__global__ void export_splats_kernel(const int32_t* __restrict__ count,
+                                     const int32_t* __restrict__ local_of,
+                                     const float4* __restrict__ rec, const int4* __restrict__ rect,
+                                     int64_t n, int32_t* __restrict__ valid,
+                                     int64_t* __restrict__ m_out, float* __restrict__ packed,
+                                     int8_t* __restrict__ mode, int32_t* __restrict__ tile_rect) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (i == n - 1) *m_out = (int64_t)local_of[n];
+  if (count[i] == 0) return;
+  const int64_t l = local_of[i];
+  if (valid) valid[l] = (int32_t)i;
+  const float* r = reinterpret_cast<const float*>(rec + 4 * i);
+  if (packed)
+    for (int c = 0; c < 13; ++c) packed[l * 13 + c] = r[c];
+  if (mode) mode[l] = (int8_t)(__float_as_uint(r[R_MODE_SPANX]) & 3u);
+  if (tile_rect) {
+    const int4 rc = rect[i];
+    tile_rect[4 * l + 0] = rc.x;
+    tile_rect[4 * l + 1] = rc.y;
+    tile_rect[4 * l + 2] = rc.z;
+    tile_rect[4 * l + 3] = rc.w;
+  }
+}
+
+__global__ void export_pairs_kernel(const uint32_t* __restrict__ pair_src,
+                                    const int32_t* __restrict__ local_of, int64_t p,
+                                    int32_t* __restrict__ pair_splat) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < p) pair_splat[k] = local_of[pair_src[k]];
+}
+
+__global__ void widen_kernel(const int32_t* __restrict__ a, int64_t* __restrict__ b, int64_t n) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) b[k] = a[k];
+}
+
+cudaError_t run_export(void* temp, size_t temp_bytes, const int32_t* count, const float4* rec,
+                       const int4* rect, const uint32_t* pair_src, const int32_t* tile_starts32,
+                       int64_t n, int64_t p, int n_tiles, int32_t* local_of, int32_t* flags,
+                       int32_t* valid, int64_t* m_out, float* packed, int8_t* mode, int32_t* tile_rect,
+                       int32_t* pair_splat, int64_t* tile_starts, cudaStream_t stream) {
+  const int block = 256;
+  visible_flags_kernel<<<(unsigned)((n + 1 + block - 1) / block), block, 0, stream>>>(count, flags,
+                                                                                      n);
+  cudaError_t e = cub::DeviceScan::ExclusiveSum(temp, temp_bytes, flags, local_of, (int)(n + 1),
+                                                stream);
+  if (e != cudaSuccess) return e;
+  export_splats_kernel<<<(unsigned)((n + block - 1) / block), block, 0, stream>>>(
+      count, local_of, rec, rect, n, valid, m_out, packed, mode, tile_rect);
+  if (pair_splat && p > 0)
+    export_pairs_kernel<<<(unsigned)((p + block - 1) / block), block, 0, stream>>>(
+        pair_src, local_of, p, pair_splat);
+  if (tile_starts)
+    widen_kernel<<<(unsigned)((n_tiles + 1 + block - 1) / block), block, 0, stream>>>(
+        tile_starts32, tile_starts, n_tiles + 1);
+  note_launch(5);
+  return cudaGetLastError();
+}
+
+}  // namespace hs

@@ -1,0 +1,448 @@
+// hs_blend.cu -- K5 forward blend and K6 backward blend.
+//
+// Semantics follow the reference blend core exactly (_blend_cy.pyx:86-187 and
+// 202-347): every pair in a tile list is evaluated until the pixel terminates
+// (no alpha skip), w = min((c1 + c2*E) * g, 0.99), termination *before*
+// compositing when T*(1-w) < 1e-4, terminal = committed count, depth = sum of
+// w*T*z, gradient gating on w_raw <= 0.99, pixel centres at +0.5.
+//
+// Mapping (B200): one warp owns one 16x16 tile; lane l owns column l&15 and the
+// eight rows (l>>4) + 2i.  Because the column is shared, every per-splat term
+// that depends only on dx (A*dx^2, B*dx, za*dx) is hoisted out of the 8-pixel
+// loop, leaving ~2 FMAs of Gaussian power per pixel.  Splat records (64 B) are
+// gathered 32 at a time with cp.async into a per-warp double buffer and read back
+// as broadcast LDS.128.  Warps pull tiles from a global counter (persistent
+// grid), so long tile lists do not stall a whole CTA.
+#include <cstdint>
+
+#include "hs_common.cuh"
+#include "hs_internal.h"
+
+namespace hs {
+
+constexpr int kWarpsPerCta = 4;
+constexpr int kBatch = 32;
+constexpr int kPx = 8;  // pixels per lane
+constexpr float kNegHalfLog2e = -0.5f * kLog2e;
+constexpr float kNegLog2e = -kLog2e;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+struct WarpStage {
+  float4 rec[2][kBatch][4];
+};
+
+// Gather the records of pairs [first, first+count) (count <= 32) into `dst`,
+// one record per lane, in the order given by pos(j).
+template <typename PosFn>
+__device__ __forceinline__ void issue_batch(const BlendGeom& g, int k0, int count, PosFn pos,
+                                            float4 (*dst)[4], int lane) {
+  if (lane < count) {
+    const uint32_t idx = g.pair_src[k0 + pos(lane)];
+    const float4* src = g.rec + 4 * (size_t)idx;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) cp_async16(&dst[lane][c], src + c);
+  }
+  cp_async_commit();
+}
+
+__device__ __forceinline__ int next_tile(const BlendGeom& g, int lane) {
+  int t = 0;
+  if (lane == 0) t = atomicAdd(g.work_counter, 1);
+  t = __shfl_sync(0xffffffffu, t, 0);
+  if (t >= g.n_work) return -1;
+  return g.tile_order ? g.tile_order[t] : g.tile_lo + t;
+}
+
+// ---------------------------------------------------------------------------
+// K5 forward
+template <int MODE>
+__device__ __forceinline__ void fwd_splat(const float4 (&q)[4], float px, float py0, float (&T)[kPx],
+                                          float (&ar)[kPx], float (&ag)[kPx], float (&ab)[kPx],
+                                          float (&ad)[kPx], int (&cnt)[kPx], unsigned& alive) {
+  const float mux = q[0].x, muy = q[0].y;
+  const float A = q[0].z * kNegHalfLog2e, B = q[0].w * kNegLog2e, C = q[1].x * kNegHalfLog2e;
+  const float za = q[1].y, zb = q[1].z, c1 = q[1].w, c2 = q[2].x;
+  const float cr = q[2].y, cg = q[2].z, cb = q[2].w, z = q[3].x;
+  const float dx = px - mux;
+  const float P0 = A * dx * dx, Bx = B * dx, Z0 = za * dx;
+#pragma unroll
+  for (int i = 0; i < kPx; ++i) {
+    if (alive & (1u << i)) {
+      const float dy = (py0 + 2.0f * i) - muy;
+      const float g = ex2_approx(fmaf(fmaf(C, dy, Bx), dy, P0));
+      float w;
+      if (MODE == kModeErf) {
+        w = fmaf(c2, erf32(fmaf(zb, dy, Z0)), c1) * g;
+      } else if (MODE == kModeSign) {
+        w = fmaf(c2, sign32(fmaf(zb, dy, Z0)), c1) * g;
+      } else {
+        w = c1 * g;
+      }
+      w = fminf(w, kWeightClamp);
+      const float tn = T[i] * (1.0f - w);
+      if (tn < kTerminationT) {
+        alive &= ~(1u << i);
+      } else {
+        const float wt = w * T[i];
+        ar[i] = fmaf(wt, cr, ar[i]);
+        ag[i] = fmaf(wt, cg, ag[i]);
+        ab[i] = fmaf(wt, cb, ab[i]);
+        ad[i] = fmaf(wt, z, ad[i]);
+        cnt[i] += 1;
+        T[i] = tn;
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kWarpsPerCta * 32) blend_fwd_kernel(
+    BlendGeom g, float bg0, float bg1, float bg2, float* __restrict__ color,
+    float* __restrict__ alpha, float* __restrict__ depth, float* __restrict__ trans,
+    int32_t* __restrict__ terminal) {
+  __shared__ WarpStage stage_all[kWarpsPerCta];
+  const int lane = threadIdx.x & 31;
+  WarpStage& st = stage_all[threadIdx.x >> 5];
+  for (;;) {
+    const int tile = next_tile(g, lane);
+    if (tile < 0) break;
+    const int ty = tile / g.tiles_x, tx = tile - ty * g.tiles_x;
+    const int col = tx * kTile + (lane & 15);
+    const int row0 = ty * kTile + (lane >> 4);
+    const float px = (float)col + 0.5f;
+    const float py0 = (float)row0 + 0.5f;
+    float T[kPx], ar[kPx], ag[kPx], ab[kPx], ad[kPx];
+    int cnt[kPx];
+    unsigned alive = 0;
+#pragma unroll
+    for (int i = 0; i < kPx; ++i) {
+      T[i] = 1.f; ar[i] = 0.f; ag[i] = 0.f; ab[i] = 0.f; ad[i] = 0.f; cnt[i] = 0;
+      if (col < g.width && row0 + 2 * i < g.height) alive |= 1u << i;
+    }
+    const int k0 = g.tile_starts[tile];
+    const int nk = g.tile_starts[tile + 1] - k0;
+    auto fwd_pos = [](int j) { return j; };
+    if (nk > 0) issue_batch(g, k0, min(kBatch, nk), fwd_pos, st.rec[0], lane);
+    for (int b = 0; b * kBatch < nk; ++b) {
+      const int nb = min(kBatch, nk - b * kBatch);
+      if ((b + 1) * kBatch < nk)
+        issue_batch(g, k0 + (b + 1) * kBatch, min(kBatch, nk - (b + 1) * kBatch), fwd_pos,
+                    st.rec[(b + 1) & 1], lane);
+      else
+        cp_async_commit();
+      cp_async_wait<1>();
+      __syncwarp();
+      const float4(*buf)[4] = st.rec[b & 1];
+      bool any = true;
+      for (int j = 0; j < nb; ++j) {
+        any = __any_sync(0xffffffffu, alive != 0);
+        if (!any) break;
+        const float4 q[4] = {buf[j][0], buf[j][1], buf[j][2], buf[j][3]};
+        const int mode = (int)(__float_as_uint(q[3].y) & 3u);
+        if (mode == kModeErf)
+          fwd_splat<kModeErf>(q, px, py0, T, ar, ag, ab, ad, cnt, alive);
+        else if (mode == kModeSign)
+          fwd_splat<kModeSign>(q, px, py0, T, ar, ag, ab, ad, cnt, alive);
+        else
+          fwd_splat<kModePlain>(q, px, py0, T, ar, ag, ab, ad, cnt, alive);
+      }
+      __syncwarp();
+      if (!any) break;
+    }
+    cp_async_wait<0>();
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < kPx; ++i) {
+      const int row = row0 + 2 * i;
+      if (col < g.width && row < g.height) {
+        const size_t p = (size_t)row * g.width + col;
+        color[3 * p + 0] = fmaf(T[i], bg0, ar[i]);
+        color[3 * p + 1] = fmaf(T[i], bg1, ag[i]);
+        color[3 * p + 2] = fmaf(T[i], bg2, ab[i]);
+        alpha[p] = 1.0f - T[i];
+        depth[p] = ad[i];
+        trans[p] = T[i];
+        terminal[p] = cnt[i];
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K6 backward
+struct BwdAcc {
+  float s0, s1, s2, q0, q1, c1, c2, r, g, b;
+};
+
+template <int MODE>
+__device__ __forceinline__ void bwd_splat(const float4 (&q)[4], int pos, float px, float py0,
+                                          float (&T)[kPx], float (&D)[kPx], const float (&dr)[kPx],
+                                          const float (&dg)[kPx], const float (&db)[kPx],
+                                          const int (&cnt)[kPx], BwdAcc& a) {
+  const float mux = q[0].x, muy = q[0].y;
+  const float A = q[0].z * kNegHalfLog2e, B = q[0].w * kNegLog2e, C = q[1].x * kNegHalfLog2e;
+  const float za = q[1].y, zb = q[1].z, c1 = q[1].w, c2 = q[2].x;
+  const float cr = q[2].y, cg = q[2].z, cb = q[2].w;
+  const float c2k = c2 * (2.0f * kInvSqrtPi);
+  const float dx = px - mux;
+  const float P0 = A * dx * dx, Bx = B * dx, Z0 = za * dx;
+#pragma unroll
+  for (int i = 0; i < kPx; ++i) {
+    if (pos < cnt[i]) {
+      const float dy = (py0 + 2.0f * i) - muy;
+      const float gg = ex2_approx(fmaf(fmaf(C, dy, Bx), dy, P0));
+      float e = 0.f, zz = 0.f, u;
+      if (MODE == kModeErf) {
+        zz = fmaf(zb, dy, Z0);
+        e = erf32(zz);
+        u = fmaf(c2, e, c1);
+      } else if (MODE == kModeSign) {
+        e = sign32(fmaf(zb, dy, Z0));
+        u = fmaf(c2, e, c1);
+      } else {
+        u = c1;
+      }
+      const float w_raw = u * gg;
+      const float w = fminf(w_raw, kWeightClamp);
+      const float inv = __frcp_rn(1.0f - w);
+      const float Tp = T[i] * inv;
+      const float wt = w * Tp;
+      const float dcr = fmaf(dr[i], cr, fmaf(dg[i], cg, db[i] * cb));
+      a.r = fmaf(dr[i], wt, a.r);
+      a.g = fmaf(dg[i], wt, a.g);
+      a.b = fmaf(db[i], wt, a.b);
+      if (w_raw <= kWeightClamp) {
+        const float d_w = fmaf(Tp, dcr, -inv * D[i]);
+        const float dwg = d_w * gg;
+        const float d_pow = dwg * u;
+        a.s0 += d_pow;
+        a.s1 = fmaf(d_pow, dy, a.s1);
+        a.s2 = fmaf(d_pow * dy, dy, a.s2);
+        a.c1 += dwg;
+        a.c2 = fmaf(dwg, e, a.c2);
+        if (MODE == kModeErf) {
+          const float d_z = dwg * c2k * ex2_approx(-(zz * zz) * kLog2e);
+          a.q0 += d_z;
+          a.q1 = fmaf(d_z, dy, a.q1);
+        }
+      }
+      D[i] = fmaf(wt, dcr, D[i]);
+      T[i] = Tp;
+    }
+  }
+}
+
+// Sum 16 per-lane values over the warp with 16 shuffles (recursive halving):
+// afterwards lanes 2m and 2m+1 both hold the warp total of value m.
+__device__ __forceinline__ float warp_transpose_reduce16(float (&v)[16], int lane) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const bool h = lane & 16;
+    const float keep = h ? v[8 + j] : v[j];
+    const float send = h ? v[j] : v[8 + j];
+    v[j] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const bool h = lane & 8;
+    const float keep = h ? v[4 + j] : v[j];
+    const float send = h ? v[j] : v[4 + j];
+    v[j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const bool h = lane & 4;
+    const float keep = h ? v[2 + j] : v[j];
+    const float send = h ? v[j] : v[2 + j];
+    v[j] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+  {
+    const bool h = lane & 2;
+    const float keep = h ? v[1] : v[0];
+    const float send = h ? v[0] : v[1];
+    v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+  }
+  return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
+}
+
+template <bool kRowsBySortedPos>
+__global__ void __launch_bounds__(kWarpsPerCta * 32) blend_bwd_kernel(
+    BlendGeom g, float bg0, float bg1, float bg2, const float* __restrict__ d_color,
+    const float* __restrict__ trans, const int32_t* __restrict__ terminal,
+    float* __restrict__ rows, int32_t* __restrict__ last_rank,
+    const uint32_t* __restrict__ rank_of) {
+  __shared__ WarpStage stage_all[kWarpsPerCta];
+  const int lane = threadIdx.x & 31;
+  WarpStage& st = stage_all[threadIdx.x >> 5];
+  for (;;) {
+    const int tile = next_tile(g, lane);
+    if (tile < 0) break;
+    const int ty = tile / g.tiles_x, tx = tile - ty * g.tiles_x;
+    const int col = tx * kTile + (lane & 15);
+    const int row0 = ty * kTile + (lane >> 4);
+    const float px = (float)col + 0.5f;
+    const float py0 = (float)row0 + 0.5f;
+    float T[kPx], D[kPx], dr[kPx], dg[kPx], db[kPx];
+    int cnt[kPx];
+    int maxc = 0;
+#pragma unroll
+    for (int i = 0; i < kPx; ++i) {
+      const int row = row0 + 2 * i;
+      if (col < g.width && row < g.height) {
+        const size_t p = (size_t)row * g.width + col;
+        T[i] = trans[p];
+        cnt[i] = terminal[p];
+        dr[i] = d_color[3 * p + 0];
+        dg[i] = d_color[3 * p + 1];
+        db[i] = d_color[3 * p + 2];
+        D[i] = T[i] * fmaf(dr[i], bg0, fmaf(dg[i], bg1, db[i] * bg2));
+      } else {
+        T[i] = 1.f; cnt[i] = 0; dr[i] = 0.f; dg[i] = 0.f; db[i] = 0.f; D[i] = 0.f;
+      }
+      maxc = max(maxc, cnt[i]);
+    }
+    maxc = __reduce_max_sync(0xffffffffu, maxc);
+    const int k0 = g.tile_starts[tile];
+    if (!kRowsBySortedPos && lane == 0)
+      last_rank[tile] = maxc > 0 ? (int32_t)rank_of[g.pair_src[k0 + maxc - 1]] : -1;
+    if (maxc == 0) continue;
+    // positions maxc-1 .. 0, batch b holds positions hi_b - j for j < nb
+    auto batch_hi = [&](int b) { return maxc - 1 - b * kBatch; };
+    {
+      const int hi = batch_hi(0);
+      issue_batch(g, k0, min(kBatch, hi + 1), [hi](int j) { return hi - j; }, st.rec[0], lane);
+    }
+    const int ty0_tile = ty, tx0_tile = tx;
+    for (int b = 0; b * kBatch < maxc; ++b) {
+      const int hi = batch_hi(b);
+      const int nb = min(kBatch, hi + 1);
+      if ((b + 1) * kBatch < maxc) {
+        const int hi2 = batch_hi(b + 1);
+        issue_batch(g, k0, min(kBatch, hi2 + 1), [hi2](int j) { return hi2 - j; },
+                    st.rec[(b + 1) & 1], lane);
+      } else {
+        cp_async_commit();
+      }
+      cp_async_wait<1>();
+      __syncwarp();
+      const float4(*buf)[4] = st.rec[b & 1];
+      for (int j = 0; j < nb; ++j) {
+        const int pos = hi - j;
+        const float4 q[4] = {buf[j][0], buf[j][1], buf[j][2], buf[j][3]};
+        const uint32_t ms = __float_as_uint(q[3].y);
+        const int mode = (int)(ms & 3u);
+        BwdAcc a = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        if (mode == kModeErf)
+          bwd_splat<kModeErf>(q, pos, px, py0, T, D, dr, dg, db, cnt, a);
+        else if (mode == kModeSign)
+          bwd_splat<kModeSign>(q, pos, px, py0, T, D, dr, dg, db, cnt, a);
+        else
+          bwd_splat<kModePlain>(q, pos, px, py0, T, D, dr, dg, db, cnt, a);
+        // per-lane partials -> the 12 pair-row columns (_blend_py.py:16-18)
+        const float ca = q[0].z, cb = q[0].w, cc = q[1].x, za = q[1].y, zb = q[1].z;
+        const float dx = px - q[0].x;
+        float v[16];
+        v[0] = fmaf(ca * dx, a.s0, fmaf(cb, a.s1, -za * a.q0));
+        v[1] = fmaf(cc, a.s1, fmaf(cb * dx, a.s0, -zb * a.q0));
+        v[2] = -0.5f * dx * dx * a.s0;
+        v[3] = -dx * a.s1;
+        v[4] = -0.5f * a.s2;
+        v[5] = dx * a.q0;
+        v[6] = a.q1;
+        v[7] = a.c1;
+        v[8] = a.c2;
+        v[9] = a.r;
+        v[10] = a.g;
+        v[11] = a.b;
+        v[12] = v[13] = v[14] = v[15] = 0.f;
+        const float total = warp_transpose_reduce16(v, lane);
+        size_t row;
+        if (kRowsBySortedPos) {
+          row = (size_t)(k0 + pos);
+        } else {
+          const uint32_t txy = __float_as_uint(q[3].w);
+          const int spans_x = (int)(ms >> 2);
+          row = (size_t)__float_as_uint(q[3].z) +
+                (size_t)((ty0_tile - (int)(txy >> 16)) * spans_x + (tx0_tile - (int)(txy & 0xffffu)));
+        }
+        const int vi = lane >> 1;
+        if (!(lane & 1) && vi < 12) rows[row * 12 + vi] = total;
+      }
+      __syncwarp();
+    }
+    cp_async_wait<0>();
+    __syncwarp();
+  }
+}
+
+// Seam 1: reference packed (M,13) float64 + mode int8 -> 64-B records.
+__global__ void pack_records_kernel(const double* __restrict__ packed,
+                                    const int8_t* __restrict__ mode, int64_t m,
+                                    float* __restrict__ rec) {
+  const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= m) return;
+  float* r = rec + l * kRecordFloats;
+  for (int c = 0; c < 13; ++c) r[c] = (float)packed[l * 13 + c];
+  r[R_MODE_SPANX] = __uint_as_float(pack_mode_spanx(mode[l] & 3, 0));
+  r[R_PAIR_BASE] = __uint_as_float(0u);
+  r[R_TXY] = __uint_as_float(0u);
+}
+
+static int blend_grid(int n_work) {
+  int dev = 0, sms = 148, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, blend_bwd_kernel<false>,
+                                                kWarpsPerCta * 32, 0);
+  if (per_sm < 1) per_sm = 1;
+  const int want = (n_work + kWarpsPerCta - 1) / kWarpsPerCta;
+  const int cap = sms * per_sm;
+  return want < cap ? (want > 0 ? want : 1) : cap;
+}
+
+cudaError_t launch_blend_fwd(const BlendGeom& g, float bg0, float bg1, float bg2, float* color,
+                             float* alpha, float* depth, float* trans, int32_t* terminal,
+                             cudaStream_t stream) {
+  cudaError_t e = cudaMemsetAsync(g.work_counter, 0, sizeof(int), stream);
+  if (e != cudaSuccess) return e;
+  blend_fwd_kernel<<<blend_grid(g.n_work), kWarpsPerCta * 32, 0, stream>>>(
+      g, bg0, bg1, bg2, color, alpha, depth, trans, terminal);
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_blend_bwd(const BlendGeom& g, float bg0, float bg1, float bg2,
+                             const float* d_color, const float* trans, const int32_t* terminal,
+                             float* rows, int32_t* last_rank, const uint32_t* rank_of,
+                             bool rows_by_sorted_pos, cudaStream_t stream) {
+  cudaError_t e = cudaMemsetAsync(g.work_counter, 0, sizeof(int), stream);
+  if (e != cudaSuccess) return e;
+  if (rows_by_sorted_pos)
+    blend_bwd_kernel<true><<<blend_grid(g.n_work), kWarpsPerCta * 32, 0, stream>>>(
+        g, bg0, bg1, bg2, d_color, trans, terminal, rows, last_rank, rank_of);
+  else
+    blend_bwd_kernel<false><<<blend_grid(g.n_work), kWarpsPerCta * 32, 0, stream>>>(
+        g, bg0, bg1, bg2, d_color, trans, terminal, rows, last_rank, rank_of);
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack_records(const double* packed, const int8_t* mode, int64_t m, float4* rec,
+                                cudaStream_t stream) {
+  if (m == 0) return cudaSuccess;
+  const int block = 256;
+  pack_records_kernel<<<(unsigned)((m + block - 1) / block), block, 0, stream>>>(
+      packed, mode, m, reinterpret_cast<float*>(rec));
+  note_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace hs

@@ -1,0 +1,562 @@
+// hs_capi.cu -- extern "C" entry points of libhalfsplat_b200.so
+// (declared in include/halfsplat_b200.h).
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "../../include/halfsplat_b200.h"
+#include "hs_common.cuh"
+#include "hs_internal.h"
+
+namespace hs {
+
+static std::atomic<int64_t> g_launches{0};
+void note_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+static thread_local char g_err[256] = "";
+
+static int cuda_status(cudaError_t e) {
+  if (e == cudaSuccess) return HS_OK;
+  snprintf(g_err, sizeof(g_err), "%s: %s", cudaGetErrorName(e), cudaGetErrorString(e));
+  return HS_ERR_CUDA;
+}
+
+#define HS_CUDA(expr)                          \
+  do {                                         \
+    cudaError_t _e = (expr);                   \
+    if (_e != cudaSuccess) return cuda_status(_e); \
+  } while (0)
+
+static size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+// Carves a workspace into typed sub-buffers; the same walk computes the size.
+struct Carver {
+  char* base;
+  size_t off = 0;
+  explicit Carver(void* b) : base(static_cast<char*>(b)) {}
+  template <typename T>
+  T* take(size_t count) {
+    T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off = align_up(off + count * sizeof(T));
+    return p;
+  }
+};
+
+struct FrameBufs {
+  float4* rec;
+  int4* rect;
+  int32_t* count;
+  uint64_t* dkey_in;
+  uint64_t* dkey_out;
+  uint32_t* dval;
+  uint32_t* order;
+  int32_t* cnt_r;
+  int32_t* off_r;
+  uint32_t* rank_of;
+  int32_t* tile_starts;
+  int32_t* last_rank;
+  int* counters;
+  int32_t* xflags;
+  int32_t* xlocal;
+  void* temp;
+  size_t temp_bytes;
+};
+
+static size_t frame_temp_bytes(int64_t n) {
+  const size_t a = depth_sort_temp_bytes(n), b = scan_temp_bytes(n);
+  return a > b ? a : b;
+}
+
+static FrameBufs carve_frame(void* ws, int64_t n, int n_tiles, size_t* total) {
+  Carver c(ws);
+  FrameBufs f;
+  f.rec = c.take<float4>(4 * (size_t)n);
+  f.rect = c.take<int4>(n);
+  f.count = c.take<int32_t>(n);
+  f.dkey_in = c.take<uint64_t>(n);
+  f.dkey_out = c.take<uint64_t>(n);
+  f.dval = c.take<uint32_t>(n);
+  f.order = c.take<uint32_t>(n);
+  f.cnt_r = c.take<int32_t>(n + 1);
+  f.off_r = c.take<int32_t>(n + 1);
+  f.rank_of = c.take<uint32_t>(n);
+  f.tile_starts = c.take<int32_t>(n_tiles + 1);
+  f.last_rank = c.take<int32_t>(n_tiles);
+  f.counters = c.take<int>(64);
+  f.xflags = c.take<int32_t>(n + 1);
+  f.xlocal = c.take<int32_t>(n + 1);
+  f.temp_bytes = frame_temp_bytes(n);
+  f.temp = c.take<char>(f.temp_bytes);
+  if (total) *total = c.off;
+  return f;
+}
+
+struct BinBufs {
+  uint32_t* keys[2];
+  uint32_t* vals[2];
+  float* rows;
+  void* temp;
+  size_t temp_bytes;
+};
+
+static BinBufs carve_bin(void* ws, int64_t p, int tile_bits, size_t* total) {
+  Carver c(ws);
+  BinBufs b;
+  const size_t pp = p > 0 ? (size_t)p : 1;
+  b.keys[0] = c.take<uint32_t>(pp);
+  b.keys[1] = c.take<uint32_t>(pp);
+  b.vals[0] = c.take<uint32_t>(pp);
+  b.vals[1] = c.take<uint32_t>(pp);
+  b.rows = c.take<float>(pp * HS_PAIR_GRAD_COLS);
+  b.temp_bytes = pair_sort_temp_bytes(p, tile_bits);
+  b.temp = c.take<char>(b.temp_bytes);
+  if (total) *total = c.off;
+  return b;
+}
+
+static int tiles_of(int32_t px) { return (px + kTile - 1) / kTile; }
+
+static int bits_for(int n_tiles) {
+  int b = 0;
+  while ((1ll << b) < (long long)n_tiles) ++b;
+  return b;
+}
+
+static CamArgs cam_args(const hs_camera* cam) {
+  CamArgs c;
+  for (int r = 0; r < 3; ++r) {
+    for (int k = 0; k < 3; ++k) c.R[3 * r + k] = cam->world_to_cam[4 * r + k];
+    c.tr[r] = cam->world_to_cam[4 * r + 3];
+    c.center[r] = cam->center[r];
+  }
+  c.fx = cam->fx;
+  c.fy = cam->fy;
+  c.cx = cam->cx;
+  c.cy = cam->cy;
+  c.near_clip = cam->near_clip;
+  c.width = cam->width;
+  c.height = cam->height;
+  return c;
+}
+
+template <typename T>
+static SceneArgs<T> scene_args(const hs_scene* s) {
+  SceneArgs<T> a;
+  a.mu = static_cast<const T*>(s->mu);
+  a.ls = static_cast<const T*>(s->log_scale);
+  a.rot = static_cast<const T*>(s->rotation);
+  a.sh = static_cast<const T*>(s->sh_coeffs);
+  a.nrm = static_cast<const T*>(s->normal);
+  a.ra = static_cast<const T*>(s->raw_opacity_a);
+  a.rb = static_cast<const T*>(s->raw_opacity_b);
+  a.deg = s->sh_degree;
+  a.K = (s->sh_degree + 1) * (s->sh_degree + 1);
+  return a;
+}
+
+template <typename T>
+static GradArgs<T> grad_args(const hs_grads* g) {
+  GradArgs<T> a;
+  a.d_mu = static_cast<T*>(g->d_mu);
+  a.d_log_scale = static_cast<T*>(g->d_log_scale);
+  a.d_rotation = static_cast<T*>(g->d_rotation);
+  a.d_sh = static_cast<T*>(g->d_sh);
+  a.d_normal = static_cast<T*>(g->d_normal);
+  a.d_ra = static_cast<T*>(g->d_raw_opacity_a);
+  a.d_rb = static_cast<T*>(g->d_raw_opacity_b);
+  a.pos_grad_norm = static_cast<T*>(g->pos_grad_norm);
+  a.touch = g->touch_count;
+  return a;
+}
+
+static int check_frame_ws(const hs_frame* f) {
+  if (!f || !f->frame_ws) return HS_ERR_WORKSPACE;
+  if (f->frame_ws_bytes < hs_frame_workspace_size(f->n, f->width, f->height))
+    return HS_ERR_WORKSPACE;
+  return HS_OK;
+}
+
+static int check_bin_ws(const hs_frame* f) {
+  if (!f->bin_ws) return HS_ERR_WORKSPACE;
+  if (f->bin_ws_bytes < hs_binning_workspace_size(f->n, f->num_pairs, f->width, f->height))
+    return HS_ERR_WORKSPACE;
+  return HS_OK;
+}
+
+static int check_scene(const hs_scene* s, const hs_frame* f) {
+  if (!s || s->n != f->n) return HS_ERR_MISMATCHED_FORWARD;
+  if (s->sh_degree < 0 || s->sh_degree > 3) return HS_ERR_INVALID_ARG;
+  if (s->dtype != HS_DTYPE_F32 && s->dtype != HS_DTYPE_F64) return HS_ERR_INVALID_ARG;
+  if (!s->mu || !s->log_scale || !s->rotation || !s->sh_coeffs || !s->normal ||
+      !s->raw_opacity_a || !s->raw_opacity_b)
+    return HS_ERR_INVALID_ARG;
+  return HS_OK;
+}
+
+}  // namespace hs
+
+using namespace hs;
+
+extern "C" {
+
+int32_t hs_abi_version(void) { return 1; }
+
+int64_t hs_kernel_launch_count(void) { return g_launches.load(); }
+
+const char* hs_last_cuda_error(void) { return g_err; }
+
+const char* hs_status_string(int status) {
+  switch (status) {
+    case HS_OK: return "ok";
+    case HS_ERR_EMPTY_SCENE: return "EmptyScene: cannot render an empty scene";
+    case HS_ERR_IMAGE_TOO_LARGE: return "ImageTooLarge: render target exceeds the supported size";
+    case HS_ERR_INVALID_KERNEL: return "ValueError: kernel must be 'half' or 'full'";
+    case HS_ERR_MISMATCHED_FORWARD: return "MismatchedForward: forward bookkeeping does not match";
+    case HS_ERR_INVALID_ARG: return "invalid argument";
+    case HS_ERR_CUDA: return "CUDA error";
+    case HS_ERR_WORKSPACE: return "workspace missing or too small";
+    default: return "unknown status";
+  }
+}
+
+int hs_frame_init(hs_frame* frame, int64_t n, int32_t width, int32_t height, int32_t kernel) {
+  if (!frame) return HS_ERR_INVALID_ARG;
+  memset(frame, 0, sizeof(*frame));
+  if (n <= 0) return HS_ERR_EMPTY_SCENE;
+  if ((int64_t)width * (int64_t)height > (int64_t)1 << 31) return HS_ERR_IMAGE_TOO_LARGE;
+  if (kernel != HS_KERNEL_HALF && kernel != HS_KERNEL_FULL) return HS_ERR_INVALID_KERNEL;
+  if (width <= 0 || height <= 0) return HS_ERR_INVALID_ARG;
+  if (n > 0x7fffffffll) return HS_ERR_INVALID_ARG;
+  const int tx = tiles_of(width), ty = tiles_of(height);
+  // tx0/ty0 are packed into 16 bits of the splat record
+  if (tx > 0xffff || ty > 0xffff) return HS_ERR_IMAGE_TOO_LARGE;
+  frame->n = n;
+  frame->width = width;
+  frame->height = height;
+  frame->tiles_x = tx;
+  frame->tiles_y = ty;
+  frame->n_tiles = tx * ty;
+  frame->kernel = kernel;
+  frame->tile_bits = bits_for(tx * ty);
+  frame->num_pairs = -1;
+  return HS_OK;
+}
+
+size_t hs_frame_workspace_size(int64_t n, int32_t width, int32_t height) {
+  size_t total = 0;
+  carve_frame(nullptr, n, tiles_of(width) * tiles_of(height), &total);
+  return total;
+}
+
+size_t hs_binning_workspace_size(int64_t n, int64_t num_pairs, int32_t width, int32_t height) {
+  (void)n;
+  size_t total = 0;
+  carve_bin(nullptr, num_pairs, bits_for(tiles_of(width) * tiles_of(height)), &total);
+  return total;
+}
+
+int hs_preprocess_fwd(hs_frame* frame, const hs_scene* scene, const hs_camera* cam,
+                      int32_t* radii, void* stream_) {
+  int st = check_frame_ws(frame);
+  if (st) return st;
+  if ((st = check_scene(scene, frame))) return st;
+  if (!cam || cam->width != frame->width || cam->height != frame->height) return HS_ERR_INVALID_ARG;
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  FrameBufs f = carve_frame(frame->frame_ws, frame->n, frame->n_tiles, nullptr);
+  const CamArgs ca = cam_args(cam);
+  if (scene->dtype == HS_DTYPE_F32) {
+    HS_CUDA(launch_preprocess_fwd_t<float>(scene_args<float>(scene), ca, frame->kernel, frame->n,
+                                           f.rec, f.rect, f.count, f.dkey_in, f.dval, radii,
+                                           stream));
+  } else {
+    HS_CUDA(launch_preprocess_fwd_t<double>(scene_args<double>(scene), ca, frame->kernel,
+                                            frame->n, f.rec, f.rect, f.count, f.dkey_in, f.dval,
+                                            radii, stream));
+  }
+  HS_CUDA(run_depth_sort(f.temp, f.temp_bytes, f.dkey_in, f.dkey_out, f.dval, f.order, frame->n,
+                         stream));
+  HS_CUDA(run_count_scan(f.temp, f.temp_bytes, f.count, f.order, f.cnt_r, f.off_r, f.rank_of,
+                         frame->n, stream));
+  frame->num_pairs = -1;
+  return HS_OK;
+}
+
+int hs_frame_read_num_pairs(hs_frame* frame, void* stream_) {
+  int st = check_frame_ws(frame);
+  if (st) return st;
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  FrameBufs f = carve_frame(frame->frame_ws, frame->n, frame->n_tiles, nullptr);
+  int32_t p = 0;
+  HS_CUDA(cudaMemcpyAsync(&p, f.off_r + frame->n, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
+  HS_CUDA(cudaStreamSynchronize(stream));
+  if (p < 0) return HS_ERR_INVALID_ARG;  // overflowed int32
+  frame->num_pairs = p;
+  return HS_OK;
+}
+
+int hs_bin_and_sort(hs_frame* frame, void* stream_) {
+  int st = check_frame_ws(frame);
+  if (st) return st;
+  if (frame->num_pairs < 0) return HS_ERR_INVALID_ARG;
+  if ((st = check_bin_ws(frame))) return st;
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  FrameBufs f = carve_frame(frame->frame_ws, frame->n, frame->n_tiles, nullptr);
+  BinBufs b = carve_bin(frame->bin_ws, frame->num_pairs, frame->tile_bits, nullptr);
+  const int64_t p = frame->num_pairs;
+  int sel = 0;
+  if (p > 0) {
+    HS_CUDA(run_duplicate(f.order, f.cnt_r, f.off_r, f.rect, f.rec, frame->tiles_x, b.keys[0],
+                          b.vals[0], frame->n, stream));
+    HS_CUDA(run_pair_sort(b.temp, b.temp_bytes, b.keys[0], b.keys[1], b.vals[0], b.vals[1], p,
+                          frame->tile_bits, &sel, stream));
+  }
+  frame->sort_selector = sel;
+  HS_CUDA(run_tile_ranges(b.keys[sel], p, frame->n_tiles, f.tile_starts, stream));
+  return HS_OK;
+}
+
+static BlendGeom frame_geom(const hs_frame* frame, const FrameBufs& f, const BinBufs& b) {
+  BlendGeom g;
+  g.tile_starts = f.tile_starts;
+  g.pair_src = b.vals[frame->sort_selector];
+  g.rec = f.rec;
+  g.width = frame->width;
+  g.height = frame->height;
+  g.tiles_x = frame->tiles_x;
+  g.tile_lo = 0;
+  g.n_work = frame->n_tiles;
+  g.tile_order = nullptr;
+  g.work_counter = f.counters;
+  return g;
+}
+
+int hs_blend_fwd(hs_frame* frame, const double* bg, float* color, float* alpha, float* depth,
+                 float* transmittance, int32_t* terminal, void* stream_) {
+  int st = check_frame_ws(frame);
+  if (st) return st;
+  if ((st = check_bin_ws(frame))) return st;
+  if (!bg || !color || !alpha || !depth || !transmittance || !terminal) return HS_ERR_INVALID_ARG;
+  FrameBufs f = carve_frame(frame->frame_ws, frame->n, frame->n_tiles, nullptr);
+  BinBufs b = carve_bin(frame->bin_ws, frame->num_pairs, frame->tile_bits, nullptr);
+  BlendGeom g = frame_geom(frame, f, b);
+  HS_CUDA(launch_blend_fwd(g, (float)bg[0], (float)bg[1], (float)bg[2], color, alpha, depth,
+                           transmittance, terminal, static_cast<cudaStream_t>(stream_)));
+  return HS_OK;
+}
+
+int hs_blend_bwd(hs_frame* frame, const double* bg, const float* d_color,
+                 const float* transmittance, const int32_t* terminal, void* stream_) {
+  int st = check_frame_ws(frame);
+  if (st) return st;
+  if ((st = check_bin_ws(frame))) return st;
+  if (!bg || !d_color || !transmittance || !terminal) return HS_ERR_INVALID_ARG;
+  FrameBufs f = carve_frame(frame->frame_ws, frame->n, frame->n_tiles, nullptr);
+  BinBufs b = carve_bin(frame->bin_ws, frame->num_pairs, frame->tile_bits, nullptr);
+  BlendGeom g = frame_geom(frame, f, b);
+  g.work_counter = f.counters + 32;
+  HS_CUDA(launch_blend_bwd(g, (float)bg[0], (float)bg[1], (float)bg[2], d_color, transmittance,
+                           terminal, b.rows, f.last_rank, f.rank_of, false,
+                           static_cast<cudaStream_t>(stream_)));
+  return HS_OK;
+}
+
+int hs_preprocess_bwd(hs_frame* frame, const hs_scene* scene, const hs_camera* cam,
+                      const hs_grads* grads, void* stream_) {
+  int st = check_frame_ws(frame);
+  if (st) return st;
+  if ((st = check_bin_ws(frame))) return st;
+  if ((st = check_scene(scene, frame))) return st;
+  if (!cam || !grads || !grads->d_mu || !grads->d_log_scale || !grads->d_rotation ||
+      !grads->d_sh || !grads->d_normal || !grads->d_raw_opacity_a || !grads->d_raw_opacity_b ||
+      !grads->pos_grad_norm || !grads->touch_count)
+    return HS_ERR_INVALID_ARG;
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  FrameBufs f = carve_frame(frame->frame_ws, frame->n, frame->n_tiles, nullptr);
+  BinBufs b = carve_bin(frame->bin_ws, frame->num_pairs, frame->tile_bits, nullptr);
+  const CamArgs ca = cam_args(cam);
+  if (scene->dtype == HS_DTYPE_F32) {
+    HS_CUDA(launch_preprocess_bwd_t<float>(scene_args<float>(scene), ca, frame->kernel, frame->n,
+                                           frame->tiles_x, f.rec, f.rect, f.count, f.rank_of,
+                                           f.last_rank, b.rows, grad_args<float>(grads), stream));
+  } else {
+    HS_CUDA(launch_preprocess_bwd_t<double>(scene_args<double>(scene), ca, frame->kernel,
+                                            frame->n, frame->tiles_x, f.rec, f.rect, f.count,
+                                            f.rank_of, f.last_rank, b.rows,
+                                            grad_args<double>(grads), stream));
+  }
+  return HS_OK;
+}
+
+int hs_frame_export(const hs_frame* frame, int32_t* valid, int64_t* m_out, float* packed,
+                    int8_t* mode, int32_t* tile_rect, int32_t* pair_splat, int64_t* tile_starts,
+                    void* stream_) {
+  int st = check_frame_ws(frame);
+  if (st) return st;
+  if (!m_out) return HS_ERR_INVALID_ARG;
+  const bool binned = frame->bin_ws && frame->num_pairs >= 0;
+  if ((pair_splat || tile_starts) && !binned) return HS_ERR_INVALID_ARG;
+  FrameBufs f = carve_frame(frame->frame_ws, frame->n, frame->n_tiles, nullptr);
+  const uint32_t* pair_src = nullptr;
+  if (binned) {
+    BinBufs b = carve_bin(frame->bin_ws, frame->num_pairs, frame->tile_bits, nullptr);
+    pair_src = b.vals[frame->sort_selector];
+  }
+  HS_CUDA(run_export(f.temp, f.temp_bytes, f.count, f.rec, f.rect, pair_src, f.tile_starts,
+                     frame->n, binned ? frame->num_pairs : 0, frame->n_tiles, f.xlocal, f.xflags,
+                     valid, m_out, packed, mode, tile_rect, pair_splat, tile_starts,
+                     static_cast<cudaStream_t>(stream_)));
+  return HS_OK;
+}
+
+// ---- Seam 1 ----------------------------------------------------------------
+namespace {
+struct DevBuf {
+  void* p = nullptr;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  cudaError_t alloc(size_t bytes) { return cudaMalloc(&p, bytes > 0 ? bytes : 16); }
+};
+
+int seam1_validate(const int64_t* tile_starts, int64_t num_pairs, int32_t height, int32_t width,
+                   int32_t tiles_x, int32_t tile_lo, int32_t tile_hi) {
+  if (height <= 0 || width <= 0 || tiles_x != tiles_of(width)) return HS_ERR_INVALID_ARG;
+  const int n_tiles = tiles_x * tiles_of(height);
+  if (tile_lo < 0 || tile_hi > n_tiles || tile_lo > tile_hi) return HS_ERR_INVALID_ARG;
+  if (!tile_starts || tile_starts[n_tiles] != num_pairs) return HS_ERR_INVALID_ARG;
+  if (num_pairs > 0x7fffffffll) return HS_ERR_INVALID_ARG;
+  return HS_OK;
+}
+}  // namespace
+
+int hs_forward_tiles(const double* packed, const int8_t* mode, const int32_t* pair_splat,
+                     const int64_t* tile_starts, int64_t m, int64_t p, int32_t height,
+                     int32_t width, int32_t tiles_x, const double* bg, double* color, double* alpha,
+                     double* depth, double* transmittance, int32_t* terminal, int32_t tile_lo,
+                     int32_t tile_hi) {
+  int st = seam1_validate(tile_starts, p, height, width, tiles_x, tile_lo, tile_hi);
+  if (st) return st;
+  if (tile_hi == tile_lo) return HS_OK;
+  const int n_tiles = tiles_x * tiles_of(height);
+  const size_t npx = (size_t)height * width;
+  std::vector<int32_t> ts32(n_tiles + 1);
+  for (int t = 0; t <= n_tiles; ++t) ts32[t] = (int32_t)tile_starts[t];
+  cudaStream_t s;
+  HS_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  struct StreamGuard { cudaStream_t s; ~StreamGuard() { cudaStreamDestroy(s); } } sg{s};
+  DevBuf d_packed, d_mode, d_rec, d_pairs, d_ts, d_out, d_term, d_ctr;
+  HS_CUDA(d_packed.alloc(m * 13 * sizeof(double)));
+  HS_CUDA(d_mode.alloc(m));
+  HS_CUDA(d_rec.alloc(m * 64));
+  HS_CUDA(d_pairs.alloc(p * 4));
+  HS_CUDA(d_ts.alloc((n_tiles + 1) * 4));
+  HS_CUDA(d_out.alloc(npx * 6 * sizeof(float)));
+  HS_CUDA(d_term.alloc(npx * 4));
+  HS_CUDA(d_ctr.alloc(256));
+  if (m > 0) {
+    HS_CUDA(cudaMemcpyAsync(d_packed.p, packed, m * 13 * sizeof(double), cudaMemcpyHostToDevice, s));
+    HS_CUDA(cudaMemcpyAsync(d_mode.p, mode, m, cudaMemcpyHostToDevice, s));
+  }
+  if (p > 0) HS_CUDA(cudaMemcpyAsync(d_pairs.p, pair_splat, p * 4, cudaMemcpyHostToDevice, s));
+  HS_CUDA(cudaMemcpyAsync(d_ts.p, ts32.data(), (n_tiles + 1) * 4, cudaMemcpyHostToDevice, s));
+  HS_CUDA(launch_pack_records((const double*)d_packed.p, (const int8_t*)d_mode.p, m,
+                              (float4*)d_rec.p, s));
+  BlendGeom g;
+  g.tile_starts = (const int32_t*)d_ts.p;
+  g.pair_src = (const uint32_t*)d_pairs.p;
+  g.rec = (const float4*)d_rec.p;
+  g.width = width;
+  g.height = height;
+  g.tiles_x = tiles_x;
+  g.tile_lo = tile_lo;
+  g.n_work = tile_hi - tile_lo;
+  g.tile_order = nullptr;
+  g.work_counter = (int*)d_ctr.p;
+  float* o = (float*)d_out.p;
+  HS_CUDA(launch_blend_fwd(g, (float)bg[0], (float)bg[1], (float)bg[2], o, o + 3 * npx,
+                           o + 4 * npx, o + 5 * npx, (int32_t*)d_term.p, s));
+  std::vector<float> h(npx * 6);
+  std::vector<int32_t> ht(npx);
+  HS_CUDA(cudaMemcpyAsync(h.data(), o, npx * 6 * sizeof(float), cudaMemcpyDeviceToHost, s));
+  HS_CUDA(cudaMemcpyAsync(ht.data(), d_term.p, npx * 4, cudaMemcpyDeviceToHost, s));
+  HS_CUDA(cudaStreamSynchronize(s));
+  for (int t = tile_lo; t < tile_hi; ++t) {
+    const int ty = t / tiles_x, tx = t - ty * tiles_x;
+    for (int r = ty * kTile; r < ty * kTile + kTile && r < height; ++r)
+      for (int c = tx * kTile; c < tx * kTile + kTile && c < width; ++c) {
+        const size_t q = (size_t)r * width + c;
+        for (int ch = 0; ch < 3; ++ch) color[3 * q + ch] = h[3 * q + ch];
+        alpha[q] = h[3 * npx + q];
+        depth[q] = h[4 * npx + q];
+        transmittance[q] = h[5 * npx + q];
+        terminal[q] = ht[q];
+      }
+  }
+  return HS_OK;
+}
+
+int hs_backward_tiles(const double* packed, const int8_t* mode, const int32_t* pair_splat,
+                      const int64_t* tile_starts, int64_t m, int64_t p, int32_t height,
+                      int32_t width, int32_t tiles_x, const double* bg, const double* d_color,
+                      const double* transmittance, const int32_t* terminal, double* pair_grads,
+                      int32_t tile_lo, int32_t tile_hi) {
+  int st = seam1_validate(tile_starts, p, height, width, tiles_x, tile_lo, tile_hi);
+  if (st) return st;
+  if (tile_hi == tile_lo || p == 0) return HS_OK;
+  const int n_tiles = tiles_x * tiles_of(height);
+  const size_t npx = (size_t)height * width;
+  std::vector<int32_t> ts32(n_tiles + 1);
+  for (int t = 0; t <= n_tiles; ++t) ts32[t] = (int32_t)tile_starts[t];
+  std::vector<float> hin(npx * 4);
+  for (size_t q = 0; q < npx * 3; ++q) hin[q] = (float)d_color[q];
+  for (size_t q = 0; q < npx; ++q) hin[3 * npx + q] = (float)transmittance[q];
+  cudaStream_t s;
+  HS_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  struct StreamGuard { cudaStream_t s; ~StreamGuard() { cudaStreamDestroy(s); } } sg{s};
+  DevBuf d_packed, d_mode, d_rec, d_pairs, d_ts, d_in, d_term, d_rows, d_ctr;
+  HS_CUDA(d_packed.alloc(m * 13 * sizeof(double)));
+  HS_CUDA(d_mode.alloc(m));
+  HS_CUDA(d_rec.alloc(m * 64));
+  HS_CUDA(d_pairs.alloc(p * 4));
+  HS_CUDA(d_ts.alloc((n_tiles + 1) * 4));
+  HS_CUDA(d_in.alloc(npx * 4 * sizeof(float)));
+  HS_CUDA(d_term.alloc(npx * 4));
+  HS_CUDA(d_rows.alloc(p * 12 * sizeof(float)));
+  HS_CUDA(d_ctr.alloc(256));
+  HS_CUDA(cudaMemcpyAsync(d_packed.p, packed, m * 13 * sizeof(double), cudaMemcpyHostToDevice, s));
+  HS_CUDA(cudaMemcpyAsync(d_mode.p, mode, m, cudaMemcpyHostToDevice, s));
+  HS_CUDA(cudaMemcpyAsync(d_pairs.p, pair_splat, p * 4, cudaMemcpyHostToDevice, s));
+  HS_CUDA(cudaMemcpyAsync(d_ts.p, ts32.data(), (n_tiles + 1) * 4, cudaMemcpyHostToDevice, s));
+  HS_CUDA(cudaMemcpyAsync(d_in.p, hin.data(), npx * 4 * sizeof(float), cudaMemcpyHostToDevice, s));
+  HS_CUDA(cudaMemcpyAsync(d_term.p, terminal, npx * 4, cudaMemcpyHostToDevice, s));
+  HS_CUDA(cudaMemsetAsync(d_rows.p, 0, p * 12 * sizeof(float), s));
+  HS_CUDA(launch_pack_records((const double*)d_packed.p, (const int8_t*)d_mode.p, m,
+                              (float4*)d_rec.p, s));
+  BlendGeom g;
+  g.tile_starts = (const int32_t*)d_ts.p;
+  g.pair_src = (const uint32_t*)d_pairs.p;
+  g.rec = (const float4*)d_rec.p;
+  g.width = width;
+  g.height = height;
+  g.tiles_x = tiles_x;
+  g.tile_lo = tile_lo;
+  g.n_work = tile_hi - tile_lo;
+  g.tile_order = nullptr;
+  g.work_counter = (int*)d_ctr.p;
+  const float* in = (const float*)d_in.p;
+  HS_CUDA(launch_blend_bwd(g, (float)bg[0], (float)bg[1], (float)bg[2], in, in + 3 * npx,
+                           (const int32_t*)d_term.p, (float*)d_rows.p, nullptr, nullptr, true, s));
+  const int64_t r0 = tile_starts[tile_lo], r1 = tile_starts[tile_hi];
+  std::vector<float> rows((size_t)(r1 - r0) * 12);
+  if (r1 > r0)
+    HS_CUDA(cudaMemcpyAsync(rows.data(), (float*)d_rows.p + r0 * 12, (r1 - r0) * 12 * sizeof(float),
+                            cudaMemcpyDeviceToHost, s));
+  HS_CUDA(cudaStreamSynchronize(s));
+  for (int64_t k = r0; k < r1; ++k)
+    for (int c = 0; c < 12; ++c) pair_grads[k * 12 + c] += rows[(k - r0) * 12 + c];
+  return HS_OK;
+}
+
+}  // extern "C"

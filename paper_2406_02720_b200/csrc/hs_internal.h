@@ -1,0 +1,108 @@
+// hs_internal.h -- kernel argument structs and launcher prototypes shared by
+// the translation units of libhalfsplat_b200.so (not part of the public ABI).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace hs {
+
+template <typename T>
+struct SceneArgs {
+  const T* mu;
+  const T* ls;
+  const T* rot;
+  const T* sh;
+  const T* nrm;
+  const T* ra;
+  const T* rb;
+  int K;    // SH coefficients per channel, (deg+1)^2
+  int deg;  // SH degree 0..3
+};
+
+struct CamArgs {
+  double R[9];   // world_to_cam rotation, row-major
+  double tr[3];  // world_to_cam translation
+  double center[3];
+  double fx, fy, cx, cy, near_clip;
+  int width, height;
+};
+
+template <typename T>
+struct GradArgs {
+  T* d_mu;
+  T* d_log_scale;
+  T* d_rotation;
+  T* d_sh;
+  T* d_normal;
+  T* d_ra;
+  T* d_rb;
+  T* pos_grad_norm;
+  int32_t* touch;
+};
+
+// ---- hs_preprocess.cu -----------------------------------------------------
+template <typename T>
+cudaError_t launch_preprocess_fwd_t(const SceneArgs<T>& sc, const CamArgs& cam, int kernel,
+                                    int64_t n, float4* rec, int4* rect, int32_t* count,
+                                    uint64_t* dkey, uint32_t* dval, int32_t* radii,
+                                    cudaStream_t stream);
+template <typename T>
+cudaError_t launch_preprocess_bwd_t(const SceneArgs<T>& sc, const CamArgs& cam, int kernel,
+                                    int64_t n, int tiles_x, const float4* rec, const int4* rect,
+                                    const int32_t* count, const uint32_t* rank_of,
+                                    const int32_t* last_rank, const float* rows,
+                                    const GradArgs<T>& out, cudaStream_t stream);
+
+// ---- hs_blend.cu ------------------------------------------------------------
+struct BlendGeom {
+  const int32_t* tile_starts;  // (n_tiles+1) CSR offsets into pair_src
+  const uint32_t* pair_src;    // sorted pair -> record index
+  const float4* rec;           // 4 float4 per record
+  int width, height, tiles_x;
+  int tile_lo, n_work;         // tiles [tile_lo, tile_lo + n_work)
+  const int32_t* tile_order;   // optional work order (nullptr = natural)
+  int* work_counter;           // zeroed before launch
+};
+
+cudaError_t launch_blend_fwd(const BlendGeom& g, float bg0, float bg1, float bg2, float* color,
+                             float* alpha, float* depth, float* trans, int32_t* terminal,
+                             cudaStream_t stream);
+// rows_by_sorted_pos: write pair row at the sorted position (reference layout,
+// Seam 1) instead of at the generation-order index from the record.
+cudaError_t launch_blend_bwd(const BlendGeom& g, float bg0, float bg1, float bg2,
+                             const float* d_color, const float* trans, const int32_t* terminal,
+                             float* rows, int32_t* last_rank, const uint32_t* rank_of,
+                             bool rows_by_sorted_pos, cudaStream_t stream);
+cudaError_t launch_pack_records(const double* packed, const int8_t* mode, int64_t m,
+                                float4* rec, cudaStream_t stream);
+
+// ---- hs_binning.cu --------------------------------------------------------
+size_t depth_sort_temp_bytes(int64_t n);
+size_t scan_temp_bytes(int64_t n);
+size_t pair_sort_temp_bytes(int64_t p, int tile_bits);
+
+cudaError_t run_depth_sort(void* temp, size_t temp_bytes, const uint64_t* keys_in,
+                           uint64_t* keys_out, const uint32_t* vals_in, uint32_t* order,
+                           int64_t n, cudaStream_t stream);
+// cnt_r[r] = count[order[r]], off_r = exclusive scan (n+1 entries), rank_of[order[r]] = r
+cudaError_t run_count_scan(void* temp, size_t temp_bytes, const int32_t* count,
+                           const uint32_t* order, int32_t* cnt_r, int32_t* off_r,
+                           uint32_t* rank_of, int64_t n, cudaStream_t stream);
+cudaError_t run_duplicate(const uint32_t* order, const int32_t* cnt_r, const int32_t* off_r,
+                          const int4* rect, float4* rec, int tiles_x, uint32_t* keys,
+                          uint32_t* vals, int64_t n, cudaStream_t stream);
+// returns selector (0/1) of the buffer holding the sorted result
+cudaError_t run_pair_sort(void* temp, size_t temp_bytes, uint32_t* keys0, uint32_t* keys1,
+                          uint32_t* vals0, uint32_t* vals1, int64_t p, int tile_bits,
+                          int* selector, cudaStream_t stream);
+cudaError_t run_tile_ranges(const uint32_t* sorted_keys, int64_t p, int n_tiles,
+                            int32_t* tile_starts, cudaStream_t stream);
+cudaError_t run_export(void* temp, size_t temp_bytes, const int32_t* count, const float4* rec,
+                       const int4* rect, const uint32_t* pair_src, const int32_t* tile_starts32,
+                       int64_t n, int64_t p, int n_tiles, int32_t* local_of, int32_t* flags,
+                       int32_t* valid, int64_t* m_out, float* packed, int8_t* mode, int32_t* tile_rect,
+                       int32_t* pair_splat, int64_t* tile_starts, cudaStream_t stream);
+
+}  // namespace hs

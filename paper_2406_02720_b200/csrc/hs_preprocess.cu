@@ -1,0 +1,665 @@
+// hs_preprocess.cu -- K1 (per-Gaussian preprocess) and K7 (per-Gaussian
+// geometry backward), one thread per primitive, FP64 geometry.
+//
+// This translation unit is compiled with -fmad=false: every floating-point
+// operation below rounds exactly where the reference's numpy expression rounds,
+// and fma() appears only where numpy's own kernels fuse (the (N,3)@(3,3) and
+// batched 3x3 matmuls go through OpenBLAS FMA chains; the einsum reductions do
+// not).  With the same inputs this reproduces prepare()'s FP64 intermediates
+// bit for bit except where libm/numpy `exp` differ by an ulp, which is what makes
+// `valid`, `tile_rect`, `mode` and the sort order exact.
+#include <cmath>
+#include <cstdint>
+
+#include "hs_common.cuh"
+#include "hs_internal.h"
+
+namespace hs {
+
+// numpy float64 -> int64 cast of ceil/floor results (x86 cvttsd2si: values out
+// of range and NaN become INT64_MIN, which the on-screen test then rejects).
+__device__ __forceinline__ long long to_i64_numpy(double x) {
+  if (!(x > -9.2233720368547758e18 && x < 9.2233720368547758e18)) return LLONG_MIN;
+  return (long long)x;
+}
+
+template <typename T>
+__device__ __forceinline__ double ld(const T* p, int64_t i) { return (double)p[i]; }
+
+// Forward state of one primitive for one view: the subset of FrameGeometry
+// (rasterizer.py:108-147) that K1 emits and K7 needs.  Recomputed by K7 rather
+// than stored (about 1 KB per splat in the reference).
+struct FwdState {
+  double t[3];
+  double qu[4], qnorm;
+  double R[9], s[3], cov[9];
+  double ccam[9], J[9], cray[9];
+  double mux, muy;
+  double a, b, c, det, radius;
+  long long px0, px1, py0, py1;  // clipped pixel rect
+  bool in_front, visible;
+  double L[9];
+  bool bad;
+  double v00, v10, v11;
+  double nnorm, nu[3];
+  double hc[3], hr[3];
+  double y[3], ynorm;
+  double nray[3];
+  double a1, a2, c1, c2, za, zb;
+  int mode;
+  double vdir[3], vdist;
+  double basis[16];
+  double rgbu[3];
+};
+
+// sigmoid, geometry.py:349-352
+__device__ __forceinline__ double sigmoid_ref(double x) {
+  return x >= 0.0 ? 1.0 / (1.0 + exp(-x)) : exp(x) / (1.0 + exp(x));
+}
+
+// eval_sh_basis, sh.py:32-61 (left-to-right evaluation of each product)
+__device__ __forceinline__ void sh_basis(const double d[3], int deg, double* out) {
+  const double SH_C0 = 0.28209479177387814, SH_C1 = 0.4886025119029199;
+  const double x = d[0], y = d[1], z = d[2];
+  out[0] = SH_C0;
+  if (deg >= 1) {
+    out[1] = -SH_C1 * y;
+    out[2] = SH_C1 * z;
+    out[3] = -SH_C1 * x;
+  }
+  if (deg >= 2) {
+    const double xx = x * x, yy = y * y, zz = z * z;
+    out[4] = 1.0925484305920792 * x * y;
+    out[5] = -1.0925484305920792 * y * z;
+    out[6] = 0.31539156525252005 * (2.0 * zz - xx - yy);
+    out[7] = -1.0925484305920792 * x * z;
+    out[8] = 0.5462742152960396 * (xx - yy);
+    if (deg >= 3) {
+      out[9] = -0.5900435899266435 * y * (3.0 * xx - yy);
+      out[10] = 2.890611442640554 * x * y * z;
+      out[11] = -0.4570457994644658 * y * (4.0 * zz - xx - yy);
+      out[12] = 0.3731763325901154 * z * (2.0 * zz - 3.0 * xx - 3.0 * yy);
+      out[13] = -0.4570457994644658 * x * (4.0 * zz - xx - yy);
+      out[14] = 1.445305721320277 * z * (xx - yy);
+      out[15] = -0.5900435899266435 * x * (xx - 3.0 * yy);
+    }
+  }
+}
+
+// d basis / d direction, sh.py:64-98; g is (K,3) row-major.
+__device__ __forceinline__ void sh_basis_grad(const double d[3], int deg, double* g) {
+  const double SH_C1 = 0.4886025119029199;
+  const double x = d[0], y = d[1], z = d[2];
+  const int k = (deg + 1) * (deg + 1);
+  for (int i = 0; i < 3 * k; ++i) g[i] = 0.0;
+  if (deg >= 1) {
+    g[1 * 3 + 1] = -SH_C1;
+    g[2 * 3 + 2] = SH_C1;
+    g[3 * 3 + 0] = -SH_C1;
+  }
+  if (deg >= 2) {
+    const double c0 = 1.0925484305920792, c1 = -1.0925484305920792, c2 = 0.31539156525252005,
+                 c3 = -1.0925484305920792, c4 = 0.5462742152960396;
+    g[12] = c0 * y; g[13] = c0 * x; g[14] = 0.0;
+    g[15] = 0.0; g[16] = c1 * z; g[17] = c1 * y;
+    g[18] = c2 * (-2 * x); g[19] = c2 * (-2 * y); g[20] = c2 * (4 * z);
+    g[21] = c3 * z; g[22] = 0.0; g[23] = c3 * x;
+    g[24] = c4 * (2 * x); g[25] = c4 * (-2 * y); g[26] = 0.0;
+  }
+  if (deg >= 3) {
+    const double xx = x * x, yy = y * y, zz = z * z;
+    const double e0 = -0.5900435899266435, e1 = 2.890611442640554, e2 = -0.4570457994644658,
+                 e3 = 0.3731763325901154, e4 = -0.4570457994644658, e5 = 1.445305721320277,
+                 e6 = -0.5900435899266435;
+    g[27] = e0 * (6 * x * y); g[28] = e0 * (3 * xx - 3 * yy); g[29] = 0.0;
+    g[30] = e1 * (y * z); g[31] = e1 * (x * z); g[32] = e1 * (x * y);
+    g[33] = e2 * (-2 * x * y); g[34] = e2 * (4 * zz - xx - 3 * yy); g[35] = e2 * (8 * y * z);
+    g[36] = e3 * (-6 * x * z); g[37] = e3 * (-6 * y * z); g[38] = e3 * (6 * zz - 3 * xx - 3 * yy);
+    g[39] = e4 * (4 * zz - 3 * xx - yy); g[40] = e4 * (-2 * x * y); g[41] = e4 * (8 * x * z);
+    g[42] = e5 * (2 * x * z); g[43] = e5 * (-2 * y * z); g[44] = e5 * (xx - yy);
+    g[45] = e6 * (3 * xx - 3 * yy); g[46] = e6 * (-6 * x * y); g[47] = 0.0;
+  }
+}
+
+// quat_to_rot, geometry.py:27-49 (normalises its input again, as the reference
+// calls it on the already-normalised quaternion, rasterizer.py:174-176).
+__device__ __forceinline__ void quat_to_rot_ref(const double q_in[4], double R[9]) {
+  double ss = 0.0;
+  for (int k = 0; k < 4; ++k) ss += q_in[k] * q_in[k];
+  const double n = sqrt(ss);
+  const double w = q_in[0] / n, x = q_in[1] / n, y = q_in[2] / n, z = q_in[3] / n;
+  R[0] = 1 - 2 * (y * y + z * z);
+  R[1] = 2 * (x * y - w * z);
+  R[2] = 2 * (x * z + w * y);
+  R[3] = 2 * (x * y + w * z);
+  R[4] = 1 - 2 * (x * x + z * z);
+  R[5] = 2 * (y * z - w * x);
+  R[6] = 2 * (x * z - w * y);
+  R[7] = 2 * (y * z + w * x);
+  R[8] = 1 - 2 * (x * x + y * y);
+}
+
+// einsum("ab,nbc,dc->nad") / ("nab,nbc,ndc->nad"): sequential over b then c,
+// each term ((A[a,b] * C[b,c]) * A[d,c]), accumulated from 0.
+__device__ __forceinline__ void sandwich(const double A[9], const double C[9], double out[9]) {
+  for (int a = 0; a < 3; ++a)
+    for (int d = 0; d < 3; ++d) {
+      double s = 0.0;
+      for (int b = 0; b < 3; ++b)
+        for (int c = 0; c < 3; ++c) s += A[3 * a + b] * C[3 * b + c] * A[3 * d + c];
+      out[3 * a + d] = s;
+    }
+}
+
+// einsum("nab,nb->na"): numpy pairs the 3-term reduction as (x0 + x2) + x1.
+__device__ __forceinline__ void matvec_einsum(const double M[9], const double v[3], double out[3]) {
+  for (int a = 0; a < 3; ++a) {
+    const double x0 = M[3 * a] * v[0], x1 = M[3 * a + 1] * v[1], x2 = M[3 * a + 2] * v[2];
+    out[a] = (x0 + x2) + x1;
+  }
+}
+
+// (N,3) @ (3,3)^T through OpenBLAS: fma(v2, M[a,2], fma(v1, M[a,1], v0 * M[a,0])).
+__device__ __forceinline__ void matvec_blas(const double M[9], const double v[3], double out[3]) {
+  for (int a = 0; a < 3; ++a)
+    out[a] = fma(v[2], M[3 * a + 2], fma(v[1], M[3 * a + 1], v[0] * M[3 * a]));
+}
+
+template <typename T>
+__device__ void forward_state(const SceneArgs<T>& sc, const CamArgs& cam, int kernel,
+                              int64_t i, FwdState& st) {
+  const double m0 = ld(sc.mu, 3 * i), m1 = ld(sc.mu, 3 * i + 1), m2 = ld(sc.mu, 3 * i + 2);
+  // t_all = mu @ rot.T + translation (rasterizer.py:170)
+  {
+    const double mv[3] = {m0, m1, m2};
+    double tt[3];
+    matvec_blas(cam.R, mv, tt);
+    for (int a = 0; a < 3; ++a) st.t[a] = tt[a] + cam.tr[a];
+  }
+  st.in_front = st.t[2] > cam.near_clip;
+  // covariance build (rasterizer.py:174-179)
+  double q[4];
+  for (int k = 0; k < 4; ++k) q[k] = ld(sc.rot, 4 * i + k);
+  {
+    double ss = 0.0;
+    for (int k = 0; k < 4; ++k) ss += q[k] * q[k];
+    st.qnorm = sqrt(ss);
+  }
+  for (int k = 0; k < 4; ++k) st.qu[k] = q[k] / st.qnorm;
+  quat_to_rot_ref(st.qu, st.R);
+  for (int k = 0; k < 3; ++k) st.s[k] = exp(ld(sc.ls, 3 * i + k));
+  double M[9];
+  for (int r = 0; r < 3; ++r)
+    for (int k = 0; k < 3; ++k) M[3 * r + k] = st.R[3 * r + k] * st.s[k];
+  for (int a = 0; a < 3; ++a)
+    for (int d = 0; d < 3; ++d)
+      st.cov[3 * a + d] = fma(M[3 * a + 2], M[3 * d + 2],
+                              fma(M[3 * a + 1], M[3 * d + 1], M[3 * a] * M[3 * d]));
+  st.visible = false;
+  if (!st.in_front) return;
+  // cov_cam, Jacobian, ray covariance (rasterizer.py:183-185; geometry.py:189-207)
+  sandwich(cam.R, st.cov, st.ccam);
+  const double tx = st.t[0], ty = st.t[1], tz = st.t[2];
+  const double invz = 1.0 / tz;
+  const double ell = sqrt(tx * tx + ty * ty + tz * tz);
+  st.J[0] = cam.fx * invz; st.J[1] = 0.0; st.J[2] = -cam.fx * tx * invz * invz;
+  st.J[3] = 0.0; st.J[4] = cam.fy * invz; st.J[5] = -cam.fy * ty * invz * invz;
+  st.J[6] = tx / ell; st.J[7] = ty / ell; st.J[8] = tz / ell;
+  sandwich(st.J, st.ccam, st.cray);
+  st.mux = cam.fx * tx * invz + cam.cx;  // rasterizer.py:188-191
+  st.muy = cam.fy * ty * invz + cam.cy;
+  // dilated conic, radius, pixel rect, on-screen test (rasterizer.py:194-210)
+  st.a = st.cray[0] + kLowpass;
+  st.b = st.cray[1];
+  st.c = st.cray[4] + kLowpass;
+  st.det = st.a * st.c - st.b * st.b;
+  const double mid = 0.5 * (st.a + st.c);
+  const double lam = mid + sqrt(fmax(mid * mid - st.det, 0.0));
+  st.radius = kRadiusSigmas * sqrt(fmax(lam, 0.0));
+  long long x0 = to_i64_numpy(ceil(st.mux - st.radius - 0.5));
+  long long x1 = to_i64_numpy(floor(st.mux + st.radius - 0.5));
+  long long y0 = to_i64_numpy(ceil(st.muy - st.radius - 0.5));
+  long long y1 = to_i64_numpy(floor(st.muy + st.radius - 0.5));
+  const long long W1 = cam.width - 1, H1 = cam.height - 1;
+  st.visible = (x1 >= 0) && (x0 <= W1) && (y1 >= 0) && (y0 <= H1) && (x1 >= x0) &&
+               (y1 >= y0) && (st.det > 0.0);
+  if (!st.visible) return;
+  st.px0 = x0 < 0 ? 0 : (x0 > W1 ? W1 : x0);  // np.clip, rasterizer.py:225-228
+  st.px1 = x1 < 0 ? 0 : (x1 > W1 ? W1 : x1);
+  st.py0 = y0 < 0 ? 0 : (y0 > H1 ? H1 : y0);
+  st.py1 = y1 < 0 ? 0 : (y1 > H1 ? H1 : y1);
+  // whitening: chol3_batch on the undilated ray covariance (geometry.py:126-160)
+  {
+    const double* A = st.cray;
+    const double d0 = A[0];
+    const double l00 = sqrt(fmax(d0, 0.0));
+    const double l10 = A[3] / l00;
+    const double l20 = A[6] / l00;
+    const double d1 = A[4] - l10 * l10;
+    const double l11 = sqrt(fmax(d1, 0.0));
+    const double l21 = (A[7] - l20 * l10) / l11;
+    const double d2 = A[8] - l20 * l20 - l21 * l21;
+    const double l22 = sqrt(fmax(d2, 0.0));
+    const double dmin = fmin(fmin(l00, l11), l22), dmax = fmax(fmax(l00, l11), l22);
+    const bool finite = isfinite(l00) && isfinite(l11) && isfinite(l22);
+    // numpy min/max propagate NaN; any NaN diag already fails `finite`.
+    st.bad = (d0 <= 0.0) || (d1 <= 0.0) || (d2 <= 0.0) || !finite || (dmin * kCondLimit < dmax);
+    for (int k = 0; k < 9; ++k) st.L[k] = 0.0;
+    if (st.bad) {
+      st.L[0] = st.L[4] = st.L[8] = 1.0;
+    } else {
+      st.L[0] = l00; st.L[3] = l10; st.L[4] = l11; st.L[6] = l20; st.L[7] = l21; st.L[8] = l22;
+    }
+  }
+  st.v00 = 1.0 / st.L[0];  // rasterizer.py:236-238
+  st.v11 = 1.0 / st.L[4];
+  st.v10 = -st.L[3] * st.v00 * st.v11;
+  // ray-space splitting normal (rasterizer.py:241-254)
+  double nrm[3];
+  for (int k = 0; k < 3; ++k) nrm[k] = ld(sc.nrm, 3 * i + k);
+  st.nnorm = sqrt(nrm[0] * nrm[0] + nrm[1] * nrm[1] + nrm[2] * nrm[2]);
+  for (int k = 0; k < 3; ++k) st.nu[k] = nrm[k] / st.nnorm;
+  double hw[3];
+  matvec_einsum(st.cov, st.nu, hw);
+  matvec_blas(cam.R, hw, st.hc);
+  matvec_einsum(st.J, st.hc, st.hr);
+  st.y[0] = st.hr[0] * st.v00;
+  st.y[1] = (st.hr[1] - st.L[3] * st.y[0]) / st.L[4];
+  st.y[2] = (st.hr[2] - st.L[6] * st.y[0] - st.L[7] * st.y[1]) / st.L[8];
+  const double yn = sqrt(st.y[0] * st.y[0] + st.y[1] * st.y[1] + st.y[2] * st.y[2]);
+  st.bad = st.bad || (yn < 1e-12) || !isfinite(yn);
+  st.ynorm = st.bad ? 1.0 : yn;
+  if (st.bad) {
+    st.nray[0] = 0.0; st.nray[1] = 0.0; st.nray[2] = 1.0;
+  } else {
+    for (int k = 0; k < 3; ++k) st.nray[k] = st.y[k] / st.ynorm;
+  }
+  // opacities, blend mode, erf coefficients (rasterizer.py:256-277)
+  st.a1 = sigmoid_ref(ld(sc.ra, i));
+  st.a2 = sigmoid_ref(ld(sc.rb, i));
+  st.c1 = 0.5 * (st.a1 + st.a2);
+  if (kernel == 1) {
+    st.c2 = 0.0;
+    st.mode = kModePlain;
+  } else {
+    st.c2 = 0.5 * (st.a1 - st.a2);
+    st.mode = st.bad ? kModePlain : (fabs(st.nray[2]) < kNormalEps ? kModeSign : kModeErf);
+  }
+  st.za = 0.0;
+  st.zb = 0.0;
+  if (st.mode == kModeErf) {
+    const double inv = 1.0 / (1.4142135623730951 * fabs(st.nray[2]));
+    st.za = inv * (st.nray[0] * st.v00 + st.nray[1] * st.v10);
+    st.zb = inv * (st.nray[1] * st.v11);
+  } else if (st.mode == kModeSign) {
+    st.za = st.nray[0] * st.v00 + st.nray[1] * st.v10;
+    st.zb = st.nray[1] * st.v11;
+  }
+  // view-dependent colour (rasterizer.py:280-285)
+  double vv[3] = {m0 - cam.center[0], m1 - cam.center[1], m2 - cam.center[2]};
+  st.vdist = sqrt(vv[0] * vv[0] + vv[1] * vv[1] + vv[2] * vv[2]);
+  for (int k = 0; k < 3; ++k) st.vdir[k] = vv[k] / st.vdist;
+  sh_basis(st.vdir, sc.deg, st.basis);
+  for (int ch = 0; ch < 3; ++ch) {
+    double acc = 0.0;
+    for (int k = 0; k < sc.K; ++k) acc += st.basis[k] * ld(sc.sh, (i * sc.K + k) * 3 + ch);
+    st.rgbu[ch] = acc + 0.5;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K1: preprocess forward.  Writes the 64-B record, tile rect, pair count and
+// the depth-rank sort key of each primitive (culled: count 0, key ~0).
+template <typename T>
+__global__ void __launch_bounds__(128) preprocess_fwd_kernel(
+    SceneArgs<T> sc, CamArgs cam, int kernel, int64_t n, float4* __restrict__ rec,
+    int4* __restrict__ rect, int32_t* __restrict__ count, uint64_t* __restrict__ dkey,
+    uint32_t* __restrict__ dval, int32_t* __restrict__ radii) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  FwdState st;
+  forward_state(sc, cam, kernel, i, st);
+  dval[i] = (uint32_t)i;
+  if (!st.visible) {
+    count[i] = 0;
+    dkey[i] = ~0ull;
+    if (radii) radii[i] = 0;
+    return;
+  }
+  const int tx0 = (int)(st.px0 / kTile), tx1 = (int)(st.px1 / kTile);
+  const int ty0 = (int)(st.py0 / kTile), ty1 = (int)(st.py1 / kTile);
+  const int spans_x = tx1 - tx0 + 1, spans_y = ty1 - ty0 + 1;
+  rect[i] = make_int4(tx0, tx1, ty0, ty1);
+  count[i] = spans_x * spans_y;
+  // positive depths order like their IEEE bit patterns; the stable radix sort
+  // then breaks exact ties by primitive index, as np.lexsort does.
+  dkey[i] = (uint64_t)__double_as_longlong(st.t[2]);
+  if (radii) radii[i] = (int32_t)ceil(st.radius);
+  float4 r0 = make_float4((float)st.mux, (float)st.muy, (float)(st.c / st.det),
+                          (float)(-st.b / st.det));
+  float4 r1 = make_float4((float)(st.a / st.det), (float)st.za, (float)st.zb, (float)st.c1);
+  float4 r2 = make_float4((float)st.c2, (float)fmax(st.rgbu[0], 0.0), (float)fmax(st.rgbu[1], 0.0),
+                          (float)fmax(st.rgbu[2], 0.0));
+  float4 r3 = make_float4((float)st.t[2], __uint_as_float(pack_mode_spanx(st.mode, spans_x)),
+                          __uint_as_float(0u), __uint_as_float((uint32_t)tx0 | ((uint32_t)ty0 << 16)));
+  float4* dst = rec + 4 * i;
+  dst[0] = r0;
+  dst[1] = r1;
+  dst[2] = r2;
+  dst[3] = r3;
+}
+
+// ---------------------------------------------------------------------------
+// K7: merge the splat's pair rows (np.add.at, rasterizer.py:419-420) and chain
+// them through the projection to the primitive parameters
+// (_geometry_backward, rasterizer.py:424-575).  FP64 throughout.
+template <typename T>
+__global__ void __launch_bounds__(128) preprocess_bwd_kernel(
+    SceneArgs<T> sc, CamArgs cam, int kernel, int64_t n, int tiles_x,
+    const float4* __restrict__ rec, const int4* __restrict__ rect,
+    const int32_t* __restrict__ count, const uint32_t* __restrict__ rank_of,
+    const int32_t* __restrict__ last_rank, const float* __restrict__ rows,
+    GradArgs<T> out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int K = sc.K;
+  const int cnt = count[i];
+  if (cnt == 0) {
+    for (int k = 0; k < 3; ++k) {
+      out.d_mu[3 * i + k] = T(0);
+      out.d_log_scale[3 * i + k] = T(0);
+      out.d_normal[3 * i + k] = T(0);
+    }
+    for (int k = 0; k < 4; ++k) out.d_rotation[4 * i + k] = T(0);
+    for (int k = 0; k < 3 * K; ++k) out.d_sh[3 * K * i + k] = T(0);
+    out.d_ra[i] = T(0);
+    out.d_rb[i] = T(0);
+    out.pos_grad_norm[i] = T(0);
+    out.touch[i] = 0;
+    return;
+  }
+  // ---- merge pair rows: tiles of the rect in row-major (= sorted k) order,
+  // skipping pairs past the tile's last composited position (never written).
+  double m[12];
+  for (int k = 0; k < 12; ++k) m[k] = 0.0;
+  {
+    const float4 q3 = rec[4 * i + 3];
+    const uint32_t base = __float_as_uint(q3.z);
+    const int4 rc = rect[i];
+    const int spans_x = rc.y - rc.x + 1;
+    const int r = (int)rank_of[i];
+    for (int l = 0; l < cnt; ++l) {
+      const int ly = l / spans_x, lx = l - ly * spans_x;
+      const int tile = (rc.z + ly) * tiles_x + rc.x + lx;
+      if (r > last_rank[tile]) continue;
+      const float4* row = reinterpret_cast<const float4*>(rows + (size_t)(base + l) * 12);
+      const float4 u0 = row[0], u1 = row[1], u2 = row[2];
+      m[0] += u0.x; m[1] += u0.y; m[2] += u0.z; m[3] += u0.w;
+      m[4] += u1.x; m[5] += u1.y; m[6] += u1.z; m[7] += u1.w;
+      m[8] += u2.x; m[9] += u2.y; m[10] += u2.z; m[11] += u2.w;
+    }
+  }
+  FwdState st;
+  forward_state(sc, cam, kernel, i, st);
+
+  const double d_mux = m[0], d_muy = m[1];
+  const double d_ca = m[2], d_cb = m[3], d_cc = m[4];
+  const double d_za = m[5], d_zb = m[6], d_c1 = m[7], d_c2 = m[8];
+  const double d_rgb[3] = {m[9], m[10], m[11]};
+
+  // opacities (rasterizer.py:446-450)
+  {
+    const double d_a1 = 0.5 * (d_c1 + d_c2), d_a2 = 0.5 * (d_c1 - d_c2);
+    out.d_ra[i] = T(d_a1 * st.a1 * (1.0 - st.a1));
+    out.d_rb[i] = T(d_a2 * st.a2 * (1.0 - st.a2));
+  }
+  // erf coefficients -> n_ray and whitening (rasterizer.py:452-466)
+  const bool mode0 = st.mode == kModeErf;
+  const double n1 = st.nray[0], n2 = st.nray[1], n3 = st.nray[2];
+  const double inv = mode0 ? 1.0 / (1.4142135623730951 * fabs(n3)) : 0.0;
+  const double d_za0 = mode0 ? d_za : 0.0, d_zb0 = mode0 ? d_zb : 0.0;
+  const double d_inv = d_za0 * (n1 * st.v00 + n2 * st.v10) + d_zb0 * (n2 * st.v11);
+  double d_nray[3];
+  d_nray[0] = d_za0 * inv * st.v00;
+  d_nray[1] = d_za0 * inv * st.v10 + d_zb0 * inv * st.v11;
+  {
+    const double sg = n3 > 0.0 ? 1.0 : (n3 < 0.0 ? -1.0 : 0.0);
+    d_nray[2] = mode0 ? -d_inv * sg / (1.4142135623730951 * n3 * n3) : 0.0;
+  }
+  const double d_v00 = d_za0 * inv * n1, d_v10 = d_za0 * inv * n2, d_v11 = d_zb0 * inv * n2;
+  // n_ray = y/|y| (rasterizer.py:469)
+  double d_y[3];
+  {
+    const double dot = d_nray[0] * n1 + d_nray[1] * n2 + d_nray[2] * n3;
+    for (int k = 0; k < 3; ++k) d_y[k] = (d_nray[k] - dot * st.nray[k]) / st.ynorm;
+  }
+  // y = L^-1 h_ray (rasterizer.py:470-473; tri_inv3_batch geometry.py:176-186)
+  const double* L = st.L;
+  double Li[9];
+  {
+    const double a = L[0], b = L[4], c = L[8];
+    Li[0] = 1.0 / a; Li[1] = 0.0; Li[2] = 0.0;
+    Li[3] = -L[3] / (a * b); Li[4] = 1.0 / b; Li[5] = 0.0;
+    Li[6] = (L[3] * L[7] - L[6] * b) / (a * b * c); Li[7] = -L[7] / (b * c); Li[8] = 1.0 / c;
+  }
+  double d_hr[3];
+  for (int a = 0; a < 3; ++a) d_hr[a] = Li[a] * d_y[0] + Li[3 + a] * d_y[1] + Li[6 + a] * d_y[2];
+  double dL[9];
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) dL[3 * a + b] = -d_hr[a] * st.y[b];
+  // whiten2d = inv(L[:2,:2]): d_L2 -= V^T dV V^T (rasterizer.py:475-484)
+  {
+    const double V00 = st.v00, V10 = st.v10, V11 = st.v11;
+    // X = V^T dV with V^T = [[V00, V10],[0, V11]], dV = [[d_v00, 0],[d_v10, d_v11]]
+    const double X00 = V00 * d_v00 + V10 * d_v10, X01 = V10 * d_v11;
+    const double X10 = V11 * d_v10, X11 = V11 * d_v11;
+    // Y = X V^T
+    dL[0] -= X00 * V00;
+    dL[1] -= X00 * V10 + X01 * V11;
+    dL[3] -= X10 * V00;
+    dL[4] -= X10 * V10 + X11 * V11;
+  }
+  dL[1] = 0.0; dL[2] = 0.0; dL[5] = 0.0;  // np.tril
+  // chol3_vjp (geometry.py:163-173)
+  double dC[9];
+  {
+    double P[9];
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b)
+        P[3 * a + b] = L[a] * dL[b] + L[3 + a] * dL[3 + b] + L[6 + a] * dL[6 + b];
+    double phi[9];
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) phi[3 * a + b] = b < a ? P[3 * a + b] : (a == b ? 0.5 * P[3 * a + b] : 0.0);
+    double S[9];
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) S[3 * a + b] = phi[3 * a + b] + phi[3 * b + a];
+    double tmp[9];  // S @ Li
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b)
+        tmp[3 * a + b] = S[3 * a] * Li[b] + S[3 * a + 1] * Li[3 + b] + S[3 * a + 2] * Li[6 + b];
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b)
+        dC[3 * a + b] = 0.5 * (Li[a] * tmp[b] + Li[3 + a] * tmp[3 + b] + Li[6 + a] * tmp[6 + b]);
+  }
+  // conic = inverse of the dilated 2x2 (rasterizer.py:489-500)
+  {
+    const double a = st.a, b = st.b, c = st.c, det = st.det, det2 = det * det;
+    dC[0] += (-d_ca * c * c + d_cb * b * c - d_cc * b * b) / det2;
+    dC[1] += (2.0 * d_ca * b * c - d_cb * (det + 2.0 * b * b) + 2.0 * d_cc * a * b) / det2;
+    dC[4] += (-d_ca * b * b + d_cb * a * b - d_cc * a * a) / det2;
+  }
+  // cov_ray = J cov_cam J^T, h_ray = J h_cam (rasterizer.py:503-507)
+  const double* J = st.J;
+  double dJ[9], dCc[9], d_hc[3];
+  {
+    double S[9];
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) S[3 * a + b] = dC[3 * a + b] + dC[3 * b + a];
+    double SJ[9];
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b)
+        SJ[3 * a + b] = S[3 * a] * J[b] + S[3 * a + 1] * J[3 + b] + S[3 * a + 2] * J[6 + b];
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b)
+        dJ[3 * a + b] = SJ[3 * a] * st.ccam[b] + SJ[3 * a + 1] * st.ccam[3 + b] +
+                        SJ[3 * a + 2] * st.ccam[6 + b] + d_hr[a] * st.hc[b];
+    double tmp[9];  // dC @ J
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b)
+        tmp[3 * a + b] = dC[3 * a] * J[b] + dC[3 * a + 1] * J[3 + b] + dC[3 * a + 2] * J[6 + b];
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b)
+        dCc[3 * a + b] = J[a] * tmp[b] + J[3 + a] * tmp[3 + b] + J[6 + a] * tmp[6 + b];
+    for (int a = 0; a < 3; ++a) d_hc[a] = J[a] * d_hr[0] + J[3 + a] * d_hr[1] + J[6 + a] * d_hr[2];
+  }
+  // cov_cam = W cov W^T, h_cam = W h (rasterizer.py:510-511)
+  const double* Wr = cam.R;
+  double dS[9], d_h[3];
+  {
+    double tmp[9];  // dCc @ W
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b)
+        tmp[3 * a + b] = dCc[3 * a] * Wr[b] + dCc[3 * a + 1] * Wr[3 + b] + dCc[3 * a + 2] * Wr[6 + b];
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b)
+        dS[3 * a + b] = Wr[a] * tmp[b] + Wr[3 + a] * tmp[3 + b] + Wr[6 + a] * tmp[6 + b];
+    for (int a = 0; a < 3; ++a) d_h[a] = d_hc[0] * Wr[a] + d_hc[1] * Wr[3 + a] + d_hc[2] * Wr[6 + a];
+  }
+  // h = cov n_unit (rasterizer.py:514-515)
+  double d_nu[3];
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) dS[3 * a + b] += d_h[a] * st.nu[b];
+  for (int a = 0; a < 3; ++a)
+    d_nu[a] = st.cov[a] * d_h[0] + st.cov[3 + a] * d_h[1] + st.cov[6 + a] * d_h[2];
+  // projected mean and Jacobian w.r.t. the camera-space centre (rasterizer.py:518-538)
+  double d_t[3];
+  {
+    const double tx = st.t[0], ty = st.t[1], tz = st.t[2];
+    const double invz = 1.0 / tz;
+    d_t[0] = d_mux * cam.fx * invz;
+    d_t[1] = d_muy * cam.fy * invz;
+    d_t[2] = -d_mux * cam.fx * tx * invz * invz - d_muy * cam.fy * ty * invz * invz;
+    const double ell = sqrt(tx * tx + ty * ty + tz * tz);
+    d_t[2] += dJ[0] * (-cam.fx * invz * invz);
+    d_t[0] += dJ[2] * (-cam.fx * invz * invz);
+    d_t[2] += dJ[2] * (2.0 * cam.fx * tx * invz * invz * invz);
+    d_t[2] += dJ[4] * (-cam.fy * invz * invz);
+    d_t[1] += dJ[5] * (-cam.fy * invz * invz);
+    d_t[2] += dJ[5] * (2.0 * cam.fy * ty * invz * invz * invz);
+    const double rh[3] = {tx / ell, ty / ell, tz / ell};
+    const double dot = dJ[6] * rh[0] + dJ[7] * rh[1] + dJ[8] * rh[2];
+    for (int k = 0; k < 3; ++k) d_t[k] += (dJ[6 + k] - dot * rh[k]) / ell;
+  }
+  double d_mu[3];
+  for (int a = 0; a < 3; ++a) d_mu[a] = d_t[0] * Wr[a] + d_t[1] * Wr[3 + a] + d_t[2] * Wr[6 + a];
+  // spherical harmonics colour, clamped at zero (rasterizer.py:543-552)
+  {
+    double dpre[3];
+    for (int ch = 0; ch < 3; ++ch) dpre[ch] = st.rgbu[ch] > 0.0 ? d_rgb[ch] : 0.0;
+    for (int k = 0; k < K; ++k)
+      for (int ch = 0; ch < 3; ++ch) out.d_sh[3 * K * i + 3 * k + ch] = T(st.basis[k] * dpre[ch]);
+    if (sc.deg > 0) {
+      double g[48];
+      sh_basis_grad(st.vdir, sc.deg, g);
+      double d_dir[3] = {0.0, 0.0, 0.0};
+      for (int k = 0; k < K; ++k) {
+        double db = 0.0;
+        for (int ch = 0; ch < 3; ++ch) db += ld(sc.sh, (i * K + k) * 3 + ch) * dpre[ch];
+        for (int d = 0; d < 3; ++d) d_dir[d] += db * g[3 * k + d];
+      }
+      const double dot = d_dir[0] * st.vdir[0] + d_dir[1] * st.vdir[1] + d_dir[2] * st.vdir[2];
+      for (int d = 0; d < 3; ++d) d_mu[d] += (d_dir[d] - dot * st.vdir[d]) / st.vdist;
+    }
+  }
+  // covariance build: cov = M M^T, M = R diag(s) (rasterizer.py:555-562)
+  {
+    double Mf[9];
+    for (int r = 0; r < 3; ++r)
+      for (int k = 0; k < 3; ++k) Mf[3 * r + k] = st.R[3 * r + k] * st.s[k];
+    double dM[9];
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) {
+        double acc = 0.0;
+        for (int c = 0; c < 3; ++c) acc += (dS[3 * a + c] + dS[3 * c + a]) * Mf[3 * c + b];
+        dM[3 * a + b] = acc;
+      }
+    double dR[9], d_s[3];
+    for (int k = 0; k < 3; ++k) d_s[k] = 0.0;
+    for (int r = 0; r < 3; ++r)
+      for (int k = 0; k < 3; ++k) {
+        dR[3 * r + k] = dM[3 * r + k] * st.s[k];
+        d_s[k] += dM[3 * r + k] * st.R[3 * r + k];
+      }
+    for (int k = 0; k < 3; ++k) out.d_log_scale[3 * i + k] = T(d_s[k] * st.s[k]);
+    // quat_rot_vjp (geometry.py:76-107) at the unit quaternion
+    const double w = st.qu[0], x = st.qu[1], y = st.qu[2], z = st.qu[3];
+    const double Dw[9] = {0, -z, y, z, 0, -x, -y, x, 0};
+    const double Dx[9] = {0, y, z, y, -2 * x, -w, z, w, -2 * x};
+    const double Dy[9] = {-2 * y, x, w, x, 0, z, -w, z, -2 * y};
+    const double Dz[9] = {-2 * z, -w, x, w, -2 * z, y, x, y, 0};
+    double dq[4] = {0, 0, 0, 0};
+    for (int k = 0; k < 9; ++k) {
+      dq[0] += 2 * Dw[k] * dR[k];
+      dq[1] += 2 * Dx[k] * dR[k];
+      dq[2] += 2 * Dy[k] * dR[k];
+      dq[3] += 2 * Dz[k] * dR[k];
+    }
+    const double dot = dq[0] * w + dq[1] * x + dq[2] * y + dq[3] * z;
+    for (int k = 0; k < 4; ++k) out.d_rotation[4 * i + k] = T((dq[k] - dot * st.qu[k]) / st.qnorm);
+  }
+  // splitting normal through its normalisation (rasterizer.py:565-566)
+  {
+    const double dot = d_nu[0] * st.nu[0] + d_nu[1] * st.nu[1] + d_nu[2] * st.nu[2];
+    for (int k = 0; k < 3; ++k) out.d_normal[3 * i + k] = T((d_nu[k] - dot * st.nu[k]) / st.nnorm);
+  }
+  for (int k = 0; k < 3; ++k) out.d_mu[3 * i + k] = T(d_mu[k]);
+  out.pos_grad_norm[i] = T(sqrt(d_mux * d_mux + d_muy * d_muy));
+  out.touch[i] = 1;
+}
+
+// ---------------------------------------------------------------------------
+template <typename T>
+cudaError_t launch_preprocess_fwd_t(const SceneArgs<T>& sc, const CamArgs& cam, int kernel,
+                                    int64_t n, float4* rec, int4* rect, int32_t* count,
+                                    uint64_t* dkey, uint32_t* dval, int32_t* radii,
+                                    cudaStream_t stream) {
+  const int block = 128;
+  const int64_t grid = (n + block - 1) / block;
+  preprocess_fwd_kernel<T><<<(unsigned)grid, block, 0, stream>>>(sc, cam, kernel, n, rec, rect,
+                                                                count, dkey, dval, radii);
+  note_launch();
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_preprocess_bwd_t(const SceneArgs<T>& sc, const CamArgs& cam, int kernel,
+                                    int64_t n, int tiles_x, const float4* rec, const int4* rect,
+                                    const int32_t* count, const uint32_t* rank_of,
+                                    const int32_t* last_rank, const float* rows,
+                                    const GradArgs<T>& out, cudaStream_t stream) {
+  const int block = 128;
+  const int64_t grid = (n + block - 1) / block;
+  preprocess_bwd_kernel<T><<<(unsigned)grid, block, 0, stream>>>(
+      sc, cam, kernel, n, tiles_x, rec, rect, count, rank_of, last_rank, rows, out);
+  note_launch();
+  return cudaGetLastError();
+}
+
+template cudaError_t launch_preprocess_fwd_t<float>(const SceneArgs<float>&, const CamArgs&, int,
+                                                    int64_t, float4*, int4*, int32_t*, uint64_t*,
+                                                    uint32_t*, int32_t*, cudaStream_t);
+template cudaError_t launch_preprocess_fwd_t<double>(const SceneArgs<double>&, const CamArgs&, int,
+                                                     int64_t, float4*, int4*, int32_t*, uint64_t*,
+                                                     uint32_t*, int32_t*, cudaStream_t);
+template cudaError_t launch_preprocess_bwd_t<float>(const SceneArgs<float>&, const CamArgs&, int,
+                                                    int64_t, int, const float4*, const int4*,
+                                                    const int32_t*, const uint32_t*, const int32_t*,
+                                                    const float*, const GradArgs<float>&,
+                                                    cudaStream_t);
+template cudaError_t launch_preprocess_bwd_t<double>(const SceneArgs<double>&, const CamArgs&, int,
+                                                     int64_t, int, const float4*, const int4*,
+                                                     const int32_t*, const uint32_t*,
+                                                     const int32_t*, const float*,
+                                                     const GradArgs<double>&, cudaStream_t);
+
+}  // namespace hs

@@ -1,0 +1,349 @@
+"""Device-resident rasterizer: the staged C-ABI pipeline driven from PyTorch.
+
+prepare -> render -> render_backward here mirror rasterizer.py:159-421 of the
+reference, but every tensor stays in HBM and every stage is one or more
+sm_100a kernels of libhalfsplat_b200.so:
+
+    prepare          hs_preprocess_fwd (K1 + depth-rank sort + count scan),
+                     hs_frame_read_num_pairs (the one host sync: P),
+                     hs_bin_and_sort (K2 duplicate, K3 stable tile sort, K4 ranges)
+    render           hs_blend_fwd (K5)
+    render_backward  hs_blend_bwd (K6) + hs_preprocess_bwd (K7)
+
+PyTorch only provides device memory (caching allocator) and the stream.
+"""
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native
+from .errors import EmptyScene, ImageTooLarge, MismatchedForward
+from .geometry import CameraModel, Scene
+
+MAX_PIXELS = 2**31  # rasterizer.py:40
+TILE = 16
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def camera_struct(cam):
+    c = _native.HsCamera()
+    w2c = np.ascontiguousarray(cam.world_to_cam, dtype=np.float64).reshape(16)
+    for k in range(16):
+        c.world_to_cam[k] = float(w2c[k])
+    c.fx, c.fy, c.cx, c.cy = cam.fx, cam.fy, cam.cx, cam.cy
+    c.near_clip = cam.near_clip
+    center = -cam.rotation.T @ cam.translation  # geometry.py:266-269
+    for k in range(3):
+        c.center[k] = float(center[k])
+    c.width, c.height = cam.width, cam.height
+    return c
+
+
+def scene_struct(scene):
+    s = _native.HsScene()
+    s.n = len(scene)
+    s.sh_degree = scene.sh_degree
+    if scene.dtype == torch.float32:
+        s.dtype = _native.HS_DTYPE_F32
+    elif scene.dtype == torch.float64:
+        s.dtype = _native.HS_DTYPE_F64
+    else:
+        raise TypeError(f"unsupported scene dtype {scene.dtype}")
+    for f in Scene.FIELDS:
+        setattr(s, f, getattr(scene, f).data_ptr())
+    for k in range(3):
+        s.background[k] = float(scene.background_color[k])
+    return s
+
+
+class DeviceFrame:
+    """One view's binned splats (the device counterpart of FrameGeometry)."""
+
+    def __init__(self, scene, cam, kernel):
+        lib = _native.load()
+        self.lib = lib
+        self.kernel = kernel
+        self.camera = cam
+        self.st = _native.HsFrame()
+        kcode = {"half": _native.HS_KERNEL_HALF, "full": _native.HS_KERNEL_FULL}[kernel]
+        _native.check(lib.hs_frame_init(ctypes.byref(self.st), len(scene), cam.width,
+                                        cam.height, kcode), "hs_frame_init")
+        dev = scene.device
+        nbytes = lib.hs_frame_workspace_size(len(scene), cam.width, cam.height)
+        self.frame_ws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+        self.st.frame_ws = self.frame_ws.data_ptr()
+        self.st.frame_ws_bytes = nbytes
+        self.bin_ws = None
+        self.radii = torch.empty(len(scene), dtype=torch.int32, device=dev)
+        self.device = dev
+
+    @property
+    def n_total(self):
+        return int(self.st.n)
+
+    @property
+    def num_pairs(self):
+        return int(self.st.num_pairs)
+
+    @property
+    def tiles_x(self):
+        return int(self.st.tiles_x)
+
+    @property
+    def tiles_y(self):
+        return int(self.st.tiles_y)
+
+    def alloc_binning(self):
+        lib = self.lib
+        nbytes = lib.hs_binning_workspace_size(self.st.n, self.st.num_pairs, self.st.width,
+                                               self.st.height)
+        if self.bin_ws is None or self.bin_ws.numel() < nbytes:
+            self.bin_ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        self.st.bin_ws = self.bin_ws.data_ptr()
+        self.st.bin_ws_bytes = self.bin_ws.numel()
+
+    def export(self):
+        """FrameGeometry integers/packed columns as host numpy arrays (parity)."""
+        n, p, t = self.n_total, self.num_pairs, int(self.st.n_tiles)
+        dev = self.device
+        valid = torch.empty(n, dtype=torch.int32, device=dev)
+        m_out = torch.zeros(1, dtype=torch.int64, device=dev)
+        packed = torch.empty((n, 13), dtype=torch.float32, device=dev)
+        mode = torch.empty(n, dtype=torch.int8, device=dev)
+        rect = torch.empty((n, 4), dtype=torch.int32, device=dev)
+        pair_splat = torch.empty(max(p, 1), dtype=torch.int32, device=dev)
+        tile_starts = torch.empty(t + 1, dtype=torch.int64, device=dev)
+        _native.check(self.lib.hs_frame_export(
+            ctypes.byref(self.st), _ptr(valid), _ptr(m_out), _ptr(packed), _ptr(mode),
+            _ptr(rect), _ptr(pair_splat), _ptr(tile_starts), _stream()), "hs_frame_export")
+        m = int(m_out.item())
+        return {
+            "valid": valid[:m].cpu().numpy().astype(np.int64),
+            "packed": packed[:m].cpu().numpy(),
+            "mode": mode[:m].cpu().numpy(),
+            "tile_rect": rect[:m].cpu().numpy(),
+            "pair_splat": pair_splat[:p].cpu().numpy(),
+            "tile_starts": tile_starts.cpu().numpy(),
+            "radii": self.radii.cpu().numpy(),
+        }
+
+
+def _validate(scene, cam, kernel):
+    if len(scene) == 0:
+        raise EmptyScene("cannot render an empty scene")
+    if cam.width * cam.height > MAX_PIXELS:
+        raise ImageTooLarge(f"{cam.width}x{cam.height} exceeds {MAX_PIXELS} pixels")
+    if kernel not in ("half", "full"):
+        raise ValueError("kernel must be 'half' or 'full'")
+
+
+def prepare(scene, cam, kernel="half", timer=None):
+    """Project + bin one view on the GPU (rasterizer.py:159-341)."""
+    timer = timer or _NO_TIMER
+    scene = Scene.from_any(scene)
+    cam = CameraModel.from_any(cam)
+    _validate(scene, cam, kernel)
+    frame = DeviceFrame(scene, cam, kernel)
+    lib = frame.lib
+    s = _stream()
+    sc = scene_struct(scene)
+    cs = camera_struct(cam)
+    with timer.span("preprocess_fwd"):
+        st = lib.hs_preprocess_fwd(ctypes.byref(frame.st), ctypes.byref(sc), ctypes.byref(cs),
+                                   _ptr(frame.radii), s)
+    _native.check(st, "hs_preprocess_fwd")
+    _native.check(lib.hs_frame_read_num_pairs(ctypes.byref(frame.st), s), "read_num_pairs")
+    frame.alloc_binning()
+    with timer.span("bin_and_sort"):
+        st = lib.hs_bin_and_sort(ctypes.byref(frame.st), s)
+    _native.check(st, "hs_bin_and_sort")
+    return frame
+
+
+@dataclass
+class DeviceRenderOutput:
+    """Forward result on the device (RenderOutput, rasterizer.py:59-69)."""
+
+    color: torch.Tensor          # (H, W, 3) float32
+    alpha: torch.Tensor          # (H, W)
+    depth: torch.Tensor          # (H, W)
+    transmittance: torch.Tensor  # (H, W)
+    terminal: torch.Tensor       # (H, W) int32, per_pixel_terminal_index
+    radii: torch.Tensor          # (N,) int32, ceil of the 3.5-sigma radius, 0 if culled
+    frame: DeviceFrame = None
+    camera: object = None
+
+    @property
+    def per_pixel_terminal_index(self):
+        return self.terminal
+
+
+class StageTimer:
+    """CUDA-event brackets around individual library calls on the current stream.
+
+    ``timer.span(name)`` is a context manager; durations (ms) accumulate per name
+    and are read after a synchronize with ``timer.totals()``."""
+
+    def __init__(self):
+        self.events = {}
+
+    def span(self, name):
+        timer = self
+
+        class _Span:
+            def __enter__(self_):
+                self_.a = torch.cuda.Event(enable_timing=True)
+                self_.b = torch.cuda.Event(enable_timing=True)
+                self_.a.record()
+
+            def __exit__(self_, *exc):
+                self_.b.record()
+                timer.events.setdefault(name, []).append((self_.a, self_.b))
+
+        return _Span()
+
+    def totals(self):
+        return {k: [a.elapsed_time(b) for a, b in v] for k, v in self.events.items()}
+
+    def reset(self):
+        self.events = {}
+
+
+class _NoTimer:
+    def span(self, name):
+        import contextlib
+        return contextlib.nullcontext()
+
+
+_NO_TIMER = _NoTimer()
+
+
+def render(scene, cam, kernel="half", frame=None, out=None, timer=None):
+    """Render one view (rasterizer.py:351-383); outputs stay on the device."""
+    timer = timer or _NO_TIMER
+    scene = Scene.from_any(scene)
+    cam = CameraModel.from_any(cam)
+    if frame is None:
+        frame = prepare(scene, cam, kernel, timer=timer)
+    h, w = cam.height, cam.width
+    dev = scene.device
+    if out is None:
+        out = DeviceRenderOutput(
+            color=torch.empty((h, w, 3), dtype=torch.float32, device=dev),
+            alpha=torch.empty((h, w), dtype=torch.float32, device=dev),
+            depth=torch.empty((h, w), dtype=torch.float32, device=dev),
+            transmittance=torch.empty((h, w), dtype=torch.float32, device=dev),
+            terminal=torch.empty((h, w), dtype=torch.int32, device=dev),
+            radii=frame.radii, frame=frame, camera=cam)
+    else:
+        out.frame, out.radii, out.camera = frame, frame.radii, cam
+    bg = (ctypes.c_double * 3)(*scene.background_color.tolist())
+    with timer.span("blend_fwd"):
+        st = frame.lib.hs_blend_fwd(
+            ctypes.byref(frame.st), bg, _ptr(out.color), _ptr(out.alpha), _ptr(out.depth),
+            _ptr(out.transmittance), _ptr(out.terminal), _stream())
+    _native.check(st, "hs_blend_fwd")
+    return out
+
+
+@dataclass
+class DeviceGradientSet:
+    """Per-primitive gradients on the device (GradientSet, rasterizer.py:72-105)."""
+
+    d_mu: torch.Tensor
+    d_log_scale: torch.Tensor
+    d_rotation: torch.Tensor
+    d_sh: torch.Tensor
+    d_normal: torch.Tensor
+    d_raw_opacity_a: torch.Tensor
+    d_raw_opacity_b: torch.Tensor
+    pos_grad_norm: torch.Tensor
+    touch_count: torch.Tensor
+
+    NAMES = ("d_mu", "d_log_scale", "d_rotation", "d_sh", "d_normal", "d_raw_opacity_a",
+             "d_raw_opacity_b", "pos_grad_norm", "touch_count")
+
+    @classmethod
+    def empty_like_scene(cls, scene):
+        n, k, dev, dt = len(scene), scene.sh_coeffs.shape[1], scene.device, scene.dtype
+        return cls(
+            d_mu=torch.empty((n, 3), dtype=dt, device=dev),
+            d_log_scale=torch.empty((n, 3), dtype=dt, device=dev),
+            d_rotation=torch.empty((n, 4), dtype=dt, device=dev),
+            d_sh=torch.empty((n, k, 3), dtype=dt, device=dev),
+            d_normal=torch.empty((n, 3), dtype=dt, device=dev),
+            d_raw_opacity_a=torch.empty(n, dtype=dt, device=dev),
+            d_raw_opacity_b=torch.empty(n, dtype=dt, device=dev),
+            pos_grad_norm=torch.empty(n, dtype=dt, device=dev),
+            touch_count=torch.empty(n, dtype=torch.int32, device=dev))
+
+    @classmethod
+    def empty_flat(cls, scene):
+        """All float groups as views of one flat buffer (one all-reduce per step)."""
+        n, k, dev, dt = len(scene), scene.sh_coeffs.shape[1], scene.device, scene.dtype
+        sizes = [3 * n, 3 * n, 4 * n, 3 * k * n, 3 * n, n, n, n]
+        flat = torch.empty(sum(sizes), dtype=dt, device=dev)
+        parts = list(torch.split(flat, sizes))
+        g = cls(d_mu=parts[0].view(n, 3), d_log_scale=parts[1].view(n, 3),
+                d_rotation=parts[2].view(n, 4), d_sh=parts[3].view(n, k, 3),
+                d_normal=parts[4].view(n, 3), d_raw_opacity_a=parts[5], d_raw_opacity_b=parts[6],
+                pos_grad_norm=parts[7],
+                touch_count=torch.empty(n, dtype=torch.int32, device=dev))
+        g.flat = flat
+        return g
+
+    def add_(self, other):
+        """Accumulate another view's gradients (GradientSet.add, rasterizer.py:100-105)."""
+        for name in self.NAMES:
+            getattr(self, name).add_(getattr(other, name))
+        return self
+
+    def flat_views(self):
+        return [getattr(self, name) for name in self.NAMES]
+
+
+def render_backward(scene, cam, out, d_color, grads=None, timer=None):
+    """Gradients of sum(d_color * color) for every parameter (rasterizer.py:386-421)."""
+    scene = Scene.from_any(scene)
+    cam = CameraModel.from_any(cam)
+    frame = out.frame
+    if frame is None or frame.n_total != len(scene):
+        raise MismatchedForward("forward bookkeeping does not match the scene")
+    if tuple(d_color.shape) != (cam.height, cam.width, 3):
+        raise MismatchedForward(
+            f"cotangent shape {tuple(d_color.shape)} != {(cam.height, cam.width, 3)}")
+    if tuple(out.terminal.shape) != (cam.height, cam.width):
+        raise MismatchedForward("terminal-index shape mismatch")
+    if not isinstance(d_color, torch.Tensor):
+        d_color = torch.as_tensor(np.asarray(d_color))
+    d_color = d_color.to(device=scene.device, dtype=torch.float32).contiguous()
+    timer = timer or _NO_TIMER
+    lib = frame.lib
+    s = _stream()
+    bg = (ctypes.c_double * 3)(*scene.background_color.tolist())
+    with timer.span("blend_bwd"):
+        st = lib.hs_blend_bwd(ctypes.byref(frame.st), bg, _ptr(d_color),
+                              _ptr(out.transmittance), _ptr(out.terminal), s)
+    _native.check(st, "hs_blend_bwd")
+    if grads is None:
+        grads = DeviceGradientSet.empty_like_scene(scene)
+    g = _native.HsGrads()
+    for name in DeviceGradientSet.NAMES:
+        setattr(g, name, getattr(grads, name).data_ptr())
+    sc = scene_struct(scene)
+    cs = camera_struct(cam)
+    with timer.span("preprocess_bwd"):
+        st = lib.hs_preprocess_bwd(ctypes.byref(frame.st), ctypes.byref(sc), ctypes.byref(cs),
+                                   ctypes.byref(g), s)
+    _native.check(st, "hs_preprocess_bwd")
+    return grads

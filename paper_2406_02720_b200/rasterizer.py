@@ -1,0 +1,252 @@
+"""Drop-in replacement for ``halfsplat.rasterizer`` running on the B200.
+
+Same functions, argument meaning, return types and exceptions as the reference
+module (rasterizer.py:43-642): host numpy in, host numpy out.  Every call goes
+through the device pipeline in ``device.py`` (libhalfsplat_b200.so); host
+buffers are copied to HBM on entry and results copied back on exit, so this is
+the end-to-end path a reference caller gets by switching imports.
+
+float64 reference scenes are uploaded as float64 (the FP64 preprocess then sees
+exactly the reference's inputs); float32 scenes stay float32.  The blend runs in
+FP32; see DESIGN.md for the parity contract.
+"""
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import device as _dev
+from .errors import EmptyScene, ImageTooLarge, MismatchedForward  # noqa: F401  (re-export)
+from .geometry import CameraModel, Scene
+
+TILE = 16
+RADIUS_SIGMAS = 3.5
+MAX_PIXELS = 2**31
+
+
+@dataclass
+class ScreenSplat:
+    """One primitive projected into one view (rasterizer.py:43-56)."""
+
+    prim_index: int
+    mu_hat: np.ndarray
+    conic: np.ndarray
+    mode: int
+    za: float
+    zb: float
+    c1: float
+    c2: float
+    rgb: np.ndarray
+    depth: float
+    tile_span: tuple
+
+
+@dataclass
+class RenderOutput:
+    """Forward-pass result (rasterizer.py:59-69)."""
+
+    color: np.ndarray
+    alpha: np.ndarray
+    depth: np.ndarray
+    per_pixel_terminal_index: np.ndarray
+    camera: object = None
+    transmittance: np.ndarray = None
+    frame: object = None
+    radii: np.ndarray = None
+
+
+@dataclass
+class GradientSet:
+    """Per-primitive gradients, index-aligned with the scene (rasterizer.py:72-105)."""
+
+    d_mu: np.ndarray
+    d_log_scale: np.ndarray
+    d_rotation: np.ndarray
+    d_sh: np.ndarray
+    d_normal: np.ndarray
+    d_raw_opacity_a: np.ndarray
+    d_raw_opacity_b: np.ndarray
+    pos_grad_norm: np.ndarray
+    touch_count: np.ndarray
+
+    NAMES = ("d_mu", "d_log_scale", "d_rotation", "d_sh", "d_normal", "d_raw_opacity_a",
+             "d_raw_opacity_b", "pos_grad_norm", "touch_count")
+
+    @classmethod
+    def zeros(cls, n, sh_k):
+        return cls(d_mu=np.zeros((n, 3)), d_log_scale=np.zeros((n, 3)),
+                   d_rotation=np.zeros((n, 4)), d_sh=np.zeros((n, sh_k, 3)),
+                   d_normal=np.zeros((n, 3)), d_raw_opacity_a=np.zeros(n),
+                   d_raw_opacity_b=np.zeros(n), pos_grad_norm=np.zeros(n),
+                   touch_count=np.zeros(n, dtype=np.int64))
+
+    def add(self, other):
+        for name in self.NAMES:
+            getattr(self, name).__iadd__(getattr(other, name))
+        return self
+
+
+class FrameGeometry:
+    """Binned view (rasterizer.py:108-147).  The device frame does the work; the
+    reference's integer arrays and packed columns are materialised on first
+    access (they are parity observables, not needed to render)."""
+
+    def __init__(self, dframe, dscene, kernel):
+        self._device = dframe
+        self._scene = dscene
+        self.kernel = kernel
+        self.n_total = dframe.n_total
+        self.tiles_x = dframe.tiles_x
+        self.tiles_y = dframe.tiles_y
+        self._export = None
+
+    def _exported(self):
+        if self._export is None:
+            self._export = self._device.export()
+        return self._export
+
+    @property
+    def valid(self):
+        return self._exported()["valid"]
+
+    @property
+    def packed(self):
+        return self._exported()["packed"].astype(np.float64)
+
+    @property
+    def mode(self):
+        return self._exported()["mode"]
+
+    @property
+    def pair_splat(self):
+        return self._exported()["pair_splat"]
+
+    @property
+    def tile_starts(self):
+        return self._exported()["tile_starts"]
+
+    @property
+    def tile_rect(self):
+        return self._exported()["tile_rect"]
+
+    @property
+    def radii(self):
+        return self._exported()["radii"]
+
+
+def resolve_threads(threads):
+    """Accepted for signature compatibility (rasterizer.py:150-156); the GPU ignores it."""
+    return 1 if threads is None else max(1, int(threads))
+
+
+def prepare(scene, cam, kernel="half"):
+    """Project a scene into one view; returns FrameGeometry (rasterizer.py:159)."""
+    dscene = Scene.from_any(scene)
+    dframe = _dev.prepare(dscene, cam, kernel)
+    return FrameGeometry(dframe, dscene, kernel)
+
+
+def render(scene, cam, kernel="half", threads=None, frame=None):
+    """Render one view (rasterizer.py:351).  Deterministic for any launch config."""
+    resolve_threads(threads)
+    cam = CameraModel.from_any(cam)
+    if frame is None:
+        frame = prepare(scene, cam, kernel)
+    dscene = frame._scene
+    dout = _dev.render(dscene, cam, kernel, frame=frame._device)
+    host = lambda t: t.detach().cpu().numpy()  # noqa: E731
+    out = RenderOutput(
+        color=host(dout.color).astype(np.float64),
+        alpha=host(dout.alpha).astype(np.float64),
+        depth=host(dout.depth).astype(np.float64),
+        per_pixel_terminal_index=host(dout.terminal),
+        camera=cam,
+        transmittance=host(dout.transmittance).astype(np.float64),
+        frame=frame,
+        radii=host(dout.radii),
+    )
+    out._device_out = dout
+    out._host_scene = scene
+    return out
+
+
+def render_backward(scene, cam, out, d_color, threads=None):
+    """Gradients of sum(d_color * rendered color) for every parameter (rasterizer.py:386)."""
+    resolve_threads(threads)
+    cam = CameraModel.from_any(cam)
+    frame = out.frame
+    if frame is None or frame.n_total != len(scene):
+        raise MismatchedForward("forward bookkeeping does not match the scene")
+    d_color = np.asarray(d_color)
+    if d_color.shape != (cam.height, cam.width, 3):
+        raise MismatchedForward(f"cotangent shape {d_color.shape} != {(cam.height, cam.width, 3)}")
+    if np.shape(out.per_pixel_terminal_index) != (cam.height, cam.width):
+        raise MismatchedForward("terminal-index shape mismatch")
+    dout = getattr(out, "_device_out", None)
+    dscene = frame._scene if getattr(out, "_host_scene", None) is scene else Scene.from_any(scene)
+    if dout is None:
+        # a RenderOutput assembled by the caller: upload its bookkeeping
+        dev = dscene.device
+        dout = _dev.DeviceRenderOutput(
+            color=None, alpha=None, depth=None,
+            transmittance=torch.as_tensor(np.asarray(out.transmittance, np.float32), device=dev),
+            terminal=torch.as_tensor(np.asarray(out.per_pixel_terminal_index, np.int32),
+                                     device=dev),
+            radii=frame._device.radii, frame=frame._device, camera=cam)
+    dc = torch.as_tensor(np.ascontiguousarray(d_color, dtype=np.float32)).to(dscene.device)
+    g = _dev.render_backward(dscene, cam, dout, dc)
+    host = lambda t: t.detach().cpu().numpy().astype(np.float64)  # noqa: E731
+    return GradientSet(
+        d_mu=host(g.d_mu), d_log_scale=host(g.d_log_scale), d_rotation=host(g.d_rotation),
+        d_sh=host(g.d_sh), d_normal=host(g.d_normal), d_raw_opacity_a=host(g.d_raw_opacity_a),
+        d_raw_opacity_b=host(g.d_raw_opacity_b), pos_grad_norm=host(g.pos_grad_norm),
+        touch_count=g.touch_count.cpu().numpy().astype(np.int64))
+
+
+def screen_splats(scene, cam, kernel="half"):
+    """Per-primitive projected splats for one view (rasterizer.py:578-603)."""
+    frame = prepare(scene, cam, kernel)
+    ex = frame._exported()
+    out = []
+    for i in range(ex["valid"].shape[0]):
+        row = ex["packed"][i].astype(np.float64)
+        out.append(ScreenSplat(
+            prim_index=int(ex["valid"][i]), mu_hat=row[0:2].copy(),
+            conic=np.array([[row[2], row[3]], [row[3], row[4]]]), mode=int(ex["mode"][i]),
+            za=float(row[5]), zb=float(row[6]), c1=float(row[7]), c2=float(row[8]),
+            rgb=row[9:12].copy(), depth=float(row[12]),
+            tile_span=tuple(int(x) for x in ex["tile_rect"][i])))
+    return out
+
+
+def render_depth_normalmap(out, alpha_threshold=0.5):
+    """Per-pixel normals from screen-space depth differences (rasterizer.py:606-642).
+
+    Post-processing of a rendered depth map, evaluated with torch ops on the
+    render's device."""
+    cam = out.camera
+    dev = torch.device("cuda") if torch.cuda.is_available() else torch.device("cpu")
+    depth = torch.as_tensor(np.asarray(out.depth, dtype=np.float64), device=dev)
+    alpha = torch.as_tensor(np.asarray(out.alpha, dtype=np.float64), device=dev)
+    h, w = depth.shape
+    ys, xs = torch.meshgrid(torch.arange(h, device=dev, dtype=torch.float64),
+                            torch.arange(w, device=dev, dtype=torch.float64), indexing="ij")
+    pts = torch.stack([depth * (xs + 0.5 - cam.cx) / cam.fx,
+                       depth * (ys + 0.5 - cam.cy) / cam.fy, depth], dim=-1)
+    valid = alpha >= alpha_threshold
+    normals = torch.zeros((h, w, 3), dtype=torch.float64, device=dev)
+    if h >= 3 and w >= 3:
+        dx = pts[1:-1, 2:] - pts[1:-1, :-2]
+        dy = pts[2:, 1:-1] - pts[:-2, 1:-1]
+        ok = (valid[1:-1, 1:-1] & valid[1:-1, 2:] & valid[1:-1, :-2] & valid[2:, 1:-1]
+              & valid[:-2, 1:-1])
+        cross = torch.linalg.cross(dx, dy, dim=-1)
+        norm = torch.linalg.norm(cross, dim=-1)
+        ok &= norm > 1e-12
+        safe = torch.where(norm > 1e-12, norm, torch.ones_like(norm))
+        cross = torch.where(ok[..., None], cross / safe[..., None], torch.zeros_like(cross))
+        flip = cross[..., 2] > 0
+        cross = torch.where(flip[..., None], -cross, cross)
+        normals[1:-1, 1:-1] = cross
+    return normals.cpu().numpy()

@@ -1,0 +1,192 @@
+"""Generate the golden fixtures in tests/golden/ from the reference itself.
+
+Runs only in the build container (needs /root/reference): copies the reference
+package to a scratch dir, builds its Cython blend core exactly as its setup.py
+does, imports `halfsplat` from there and records its outputs on the canonical
+synthetic scenes (paper_2406_02720_b200/scenes.py).  Nothing here is imported at
+test time; the fixtures are plain .npz files.
+
+    python tests/golden/make_golden.py [--build-dir /tmp/hs_refbuild] [--only c1,mini,...]
+
+Fixture kinds
+  full     every FrameGeometry integer array, packed, images, terminal and (if
+           backward) the d_color and GradientSet -- small scenes only
+  summary  full-size configs: sha256 of each integer array, counts, a seeded
+           sample of pixels and of gradient rows, per-group gradient norms
+"""
+
+import argparse
+import hashlib
+import os
+import shutil
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, REPO)
+
+from paper_2406_02720_b200 import scenes  # noqa: E402
+
+REF_PKG = "/root/reference/pkg"
+GRAD_GROUPS = ("d_mu", "d_log_scale", "d_rotation", "d_sh", "d_normal", "d_raw_opacity_a",
+               "d_raw_opacity_b", "pos_grad_norm", "touch_count")
+INT_ARRAYS = {"valid": np.int64, "mode": np.int8, "tile_rect": np.int32,
+              "pair_splat": np.int32, "tile_starts": np.int64}
+
+
+def sha(a, dtype):
+    return hashlib.sha256(np.ascontiguousarray(a, dtype=dtype).tobytes()).hexdigest()
+
+
+def scene_sha(sa):
+    h = hashlib.sha256()
+    for f in sa.FIELDS:
+        h.update(np.ascontiguousarray(getattr(sa, f), dtype=np.float32).tobytes())
+    return h.hexdigest()
+
+
+def build_reference(build_dir):
+    if not os.path.exists(os.path.join(build_dir, "src", "halfsplat")):
+        shutil.rmtree(build_dir, ignore_errors=True)
+        shutil.copytree(REF_PKG, build_dir)
+        subprocess.run(["chmod", "-R", "u+w", build_dir], check=True)
+        subprocess.run([sys.executable, "setup.py", "build_ext", "--inplace"], cwd=build_dir,
+                       check=True, capture_output=True)
+    sys.path.insert(0, os.path.join(build_dir, "src"))
+    import halfsplat.backend as backend
+    backend.set_backend("cython")
+    return backend
+
+
+def ref_scene(sa):
+    from halfsplat.geometry import Scene
+    s64 = sa.as_float64()
+    return Scene(**{f: getattr(s64, f) for f in s64.FIELDS}, sh_degree=s64.sh_degree,
+                 background_color=s64.background_color)
+
+
+def ref_camera(c):
+    from halfsplat.geometry import CameraModel
+    return CameraModel(**c)
+
+
+def run_reference(sa, cam_idx, backward, threads, kernel="half"):
+    from halfsplat.rasterizer import prepare, render, render_backward
+    sc = ref_scene(sa)
+    cam = ref_camera(sa.cameras[cam_idx])
+    t0 = time.time()
+    frame = prepare(sc, cam, kernel)
+    out = render(sc, cam, kernel=kernel, threads=threads, frame=frame)
+    t1 = time.time()
+    grads, d_color = None, None
+    if backward:
+        d_color = scenes.cotangent(cam.height, cam.width)
+        grads = render_backward(sc, cam, out, d_color, threads=threads)
+    t2 = time.time()
+    return frame, out, grads, d_color, (t1 - t0, t2 - t1)
+
+
+def full_fixture(name, sa, cam_idx, backward, threads, kernel="half"):
+    frame, out, grads, d_color, secs = run_reference(sa, cam_idx, backward, threads, kernel)
+    d = dict(scene_sha=scene_sha(sa), cam_idx=cam_idx, kernel=kernel,
+             packed=frame.packed, color=out.color, alpha=out.alpha, depth=out.depth,
+             transmittance=out.transmittance, terminal=out.per_pixel_terminal_index,
+             tiles_x=frame.tiles_x, tiles_y=frame.tiles_y)
+    for k, dt in INT_ARRAYS.items():
+        d[k] = np.asarray(getattr(frame, k), dtype=dt)
+    if backward:
+        d["d_color"] = d_color
+        for g in GRAD_GROUPS:
+            d[g] = getattr(grads, g)
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **d)
+    print(f"{name}: M={frame.valid.shape[0]} P={frame.pair_splat.shape[0]} "
+          f"ref fwd {secs[0]:.2f}s bwd {secs[1]:.2f}s")
+
+
+def summary_fixture(name, sa, cam_idx, backward, threads, n_px=4096, n_rows=2048):
+    frame, out, grads, d_color, secs = run_reference(sa, cam_idx, backward, threads)
+    cam = sa.cameras[cam_idx]
+    h, w = cam["height"], cam["width"]
+    rng = np.random.default_rng(12345)
+    px = rng.choice(h * w, size=min(n_px, h * w), replace=False)
+    d = dict(scene_sha=scene_sha(sa), cam_idx=cam_idx, M=frame.valid.shape[0],
+             P=frame.pair_splat.shape[0], tiles_x=frame.tiles_x, tiles_y=frame.tiles_y,
+             mode_counts=np.bincount(frame.mode, minlength=3), px_index=px,
+             px_color=out.color.reshape(-1, 3)[px], px_alpha=out.alpha.reshape(-1)[px],
+             px_depth=out.depth.reshape(-1)[px],
+             px_transmittance=out.transmittance.reshape(-1)[px],
+             px_terminal=out.per_pixel_terminal_index.reshape(-1)[px],
+             terminal_sha=sha(out.per_pixel_terminal_index, np.int32),
+             terminal_sum=int(out.per_pixel_terminal_index.astype(np.int64).sum()),
+             color_sum=out.color.sum(axis=(0, 1)), alpha_sum=float(out.alpha.sum()),
+             fwd_evals=int(np.minimum(out.per_pixel_terminal_index.astype(np.int64) + 1,
+                                      _list_len_per_px(frame, h, w)).sum()),
+             ref_seconds=np.array(secs))
+    for k, dt in INT_ARRAYS.items():
+        d[f"sha_{k}"] = sha(getattr(frame, k), dt)
+    d["packed_sample_rows"] = rng.choice(frame.valid.shape[0], size=min(n_rows, frame.valid.shape[0]),
+                                         replace=False)
+    d["packed_sample"] = frame.packed[d["packed_sample_rows"]]
+    if backward:
+        n = len(sa)
+        rows = rng.choice(n, size=min(n_rows, n), replace=False)
+        d["grad_rows"] = rows
+        for g in GRAD_GROUPS:
+            arr = getattr(grads, g)
+            d[f"norm_{g}"] = float(np.linalg.norm(arr.astype(np.float64)))
+            d[f"sample_{g}"] = arr[rows]
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **d)
+    print(f"{name}: M={d['M']} P={d['P']} ref fwd {secs[0]:.1f}s bwd {secs[1]:.1f}s")
+
+
+def _list_len_per_px(frame, h, w):
+    lens = np.diff(frame.tile_starts).reshape(frame.tiles_y, frame.tiles_x)
+    full = np.repeat(np.repeat(lens, 16, axis=0), 16, axis=1)
+    return full[:h, :w].astype(np.int64)
+
+
+def erf_fixture():
+    from halfsplat.kernels import fast_erf
+    rng = np.random.default_rng(7)
+    z = np.concatenate([np.linspace(-6, 6, 4001), rng.normal(0, 2, 4000),
+                        np.array([0.0, -0.0, 1.0, -1.0, 2.4, -2.4, 4.5, -4.5, 1e-300, 50.0])])
+    np.savez_compressed(os.path.join(HERE, "erf.npz"), z=z, erf=fast_erf(z))
+    print("erf: ", z.shape[0], "points")
+
+
+JOBS = {
+    "erf": lambda t: erf_fixture(),
+    # small scenes, every array
+    "c1": lambda t: full_fixture("c1", scenes.make_config("c1"), 0, True, t),
+    "mini": lambda t: full_fixture("mini", scenes.frustum(300, 2, 64, 48, seed=3), 0, True, t),
+    "mini_full": lambda t: full_fixture("mini_full", scenes.frustum(300, 2, 64, 48, seed=3), 0,
+                                        True, t, kernel="full"),
+    "ball_small": lambda t: full_fixture("ball_small", scenes.ball(3000, 3, 96, 72, views=4, seed=9),
+                                         1, True, t),
+    "ties": lambda t: full_fixture("ties", scenes.frustum(2000, 1, 96, 80, seed=5, clustered=True,
+                                                          dup=0.3), 0, True, t),
+    # full-size configs, summaries
+    "c2": lambda t: summary_fixture("c2", scenes.make_config("c2"), 0, True, t),
+    "c3": lambda t: summary_fixture("c3", scenes.make_config("c3"), 0, True, t),
+    "c5": lambda t: summary_fixture("c5", scenes.make_config("c5"), 0, True, t),
+    "c4v0": lambda t: summary_fixture("c4v0", scenes.make_config("c4"), 0, True, t),
+}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--build-dir", default="/tmp/hs_refbuild")
+    ap.add_argument("--only", default=",".join(JOBS))
+    ap.add_argument("--threads", type=int, default=os.cpu_count())
+    args = ap.parse_args()
+    build_reference(args.build_dir)
+    for name in args.only.split(","):
+        JOBS[name](args.threads)
+
+
+if __name__ == "__main__":
+    main()

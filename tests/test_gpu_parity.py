@@ -1,0 +1,187 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the reference's own
+outputs (golden fixtures) and against the live CPU oracle.
+
+Every call below goes through libhalfsplat_b200.so; the oracle is only the
+checker.  Tolerances: tests/parity.py.
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import load_golden
+from parity import (GRAD_GROUPS, PACKED_RTOL, assert_grads, assert_images, grad_report,
+                    image_report)
+from paper_2406_02720_b200 import device, scenes
+from paper_2406_02720_b200.geometry import CameraModel, Scene
+
+pytestmark = pytest.mark.gpu
+
+FULL_FIXTURES = {
+    "c1": (lambda: scenes.make_config("c1"), "half"),
+    "mini": (lambda: scenes.frustum(300, 2, 64, 48, seed=3), "half"),
+    "mini_full": (lambda: scenes.frustum(300, 2, 64, 48, seed=3), "full"),
+    "ball_small": (lambda: scenes.ball(3000, 3, 96, 72, views=4, seed=9), "half"),
+    "ties": (lambda: scenes.frustum(2000, 1, 96, 80, seed=5, clustered=True, dup=0.3), "half"),
+}
+SUMMARY_FIXTURES = ("c2", "c3", "c5", "c4v0")
+INT_DTYPES = {"valid": np.int64, "mode": np.int8, "tile_rect": np.int32, "pair_splat": np.int32,
+              "tile_starts": np.int64}
+
+
+def scene_sha(sa):
+    h = hashlib.sha256()
+    for f in sa.FIELDS:
+        h.update(np.ascontiguousarray(getattr(sa, f), dtype=np.float32).tobytes())
+    return h.hexdigest()
+
+
+def device_scene(sa, dtype=torch.float32):
+    return Scene(*(getattr(sa, f) for f in sa.FIELDS), sh_degree=sa.sh_degree,
+                 background_color=sa.background_color, device="cuda", dtype=dtype)
+
+
+def run_gpu(sa, cam_idx, kernel="half", dtype=torch.float32, d_color=None):
+    sc = device_scene(sa, dtype)
+    cam = CameraModel(**sa.cameras[cam_idx])
+    out = device.render(sc, cam, kernel)
+    res = {
+        "color": out.color.cpu().numpy(), "alpha": out.alpha.cpu().numpy(),
+        "depth": out.depth.cpu().numpy(), "transmittance": out.transmittance.cpu().numpy(),
+        "terminal": out.terminal.cpu().numpy(),
+    }
+    res.update(out.frame.export())
+    if d_color is not None:
+        g = device.render_backward(sc, cam, out, torch.as_tensor(d_color, dtype=torch.float32))
+        for name in GRAD_GROUPS + ("touch_count",):
+            res[name] = getattr(g, name).double().cpu().numpy()
+    return res
+
+
+@pytest.mark.parametrize("name", list(FULL_FIXTURES))
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_full_fixture_parity(cuda, name, dtype):
+    gold = load_golden(name)
+    gen, kernel = FULL_FIXTURES[name]
+    sa = gen()
+    assert scene_sha(sa) == str(gold["scene_sha"]), "scene generator drifted"
+    d_color = gold["d_color"] if "d_color" in gold else None
+    got = run_gpu(sa, int(gold["cam_idx"]), kernel, dtype, d_color)
+    # integers: bit-exact
+    for k, dt in INT_DTYPES.items():
+        assert np.array_equal(np.asarray(got[k], dtype=dt), gold[k]), k
+    # packed: FP64 value rounded to FP32
+    ref32 = gold["packed"].astype(np.float32).astype(np.float64)
+    np.testing.assert_allclose(got["packed"].astype(np.float64), ref32, rtol=PACKED_RTOL,
+                               atol=1e-30)
+    assert_images(got, gold)
+    if d_color is not None:
+        assert_grads(got, gold)
+        assert np.array_equal(got["touch_count"], gold["touch_count"])
+
+
+@pytest.mark.parametrize("name", SUMMARY_FIXTURES)
+def test_full_size_summary_parity(cuda, name):
+    gold = load_golden(name)
+    cfg = {"c4v0": "c4"}.get(name, name)
+    sa = scenes.make_config(cfg)
+    assert scene_sha(sa) == str(gold["scene_sha"]), "scene generator drifted"
+    cam = CameraModel(**sa.cameras[int(gold["cam_idx"])])
+    d_color = scenes.cotangent(cam.height, cam.width) if "grad_rows" in gold else None
+    got = run_gpu(sa, int(gold["cam_idx"]), "half", torch.float32, d_color)
+    for k, dt in INT_DTYPES.items():
+        h = hashlib.sha256(np.ascontiguousarray(got[k], dtype=dt).tobytes()).hexdigest()
+        assert h == str(gold[f"sha_{k}"]), f"{k} differs from the reference"
+    assert got["valid"].shape[0] == int(gold["M"])
+    assert got["pair_splat"].shape[0] == int(gold["P"])
+    rows = gold["packed_sample_rows"]
+    np.testing.assert_allclose(got["packed"][rows].astype(np.float64),
+                               gold["packed_sample"].astype(np.float32).astype(np.float64),
+                               rtol=PACKED_RTOL, atol=1e-30)
+    # terminal: mismatch fraction over the whole frame from the sampled pixels
+    px = gold["px_index"]
+    sample_got = {
+        "color": got["color"].reshape(-1, 3)[px], "alpha": got["alpha"].reshape(-1)[px],
+        "depth": got["depth"].reshape(-1)[px],
+        "transmittance": got["transmittance"].reshape(-1)[px],
+        "terminal": got["terminal"].reshape(-1)[px],
+    }
+    sample_ref = {"color": gold["px_color"], "alpha": gold["px_alpha"], "depth": gold["px_depth"],
+                  "transmittance": gold["px_transmittance"], "terminal": gold["px_terminal"]}
+    assert_images(sample_got, sample_ref)
+    rep = image_report({"terminal": got["terminal"]},
+                       {"terminal": got["terminal"]})  # shape sanity
+    assert rep["pixels"] == got["terminal"].size
+    if d_color is not None:
+        rows = gold["grad_rows"]
+        for g in GRAD_GROUPS:
+            ref_norm = float(gold[f"norm_{g}"])
+            got_norm = float(np.linalg.norm(got[g]))
+            assert abs(got_norm - ref_norm) <= 1e-3 * ref_norm, (g, got_norm, ref_norm)
+        sample = {g: got[g][rows] for g in GRAD_GROUPS}
+        ref = {g: gold[f"sample_{g}"] for g in GRAD_GROUPS}
+        assert_grads(sample, ref)
+
+
+def _oracle():
+    from oracle import oracle
+    return oracle
+
+
+@pytest.mark.parametrize("kernel", ["half", "full"])
+def test_live_oracle_medium(cuda, kernel):
+    """Unseen scene, both kernels: GPU vs the CPU oracle run on this host."""
+    O = _oracle()
+    sa = scenes.frustum(20_000, 3, 320, 240, seed=11, sig_lo=0.8, sig_hi=6.0)
+    s64 = sa.as_float64()
+    cam = CameraModel(**sa.cameras[0])
+    d_color = scenes.cotangent(cam.height, cam.width, seed=4)
+    ref_out = O.render(s64, cam, kernel=kernel)
+    ref_g = O.render_backward(s64, cam, ref_out, d_color)
+    got = run_gpu(sa, 0, kernel, torch.float32, d_color)
+    f = ref_out.frame
+    assert np.array_equal(got["valid"], f.valid)
+    assert np.array_equal(got["pair_splat"], f.pair_splat)
+    assert np.array_equal(got["tile_starts"], f.tile_starts)
+    assert np.array_equal(got["tile_rect"], f.tile_rect)
+    assert np.array_equal(got["mode"], f.mode)
+    ref = {"color": ref_out.color, "alpha": ref_out.alpha, "depth": ref_out.depth,
+           "transmittance": ref_out.transmittance, "terminal": ref_out.per_pixel_terminal_index}
+    assert_images(got, ref)
+    assert_grads(got, ref_g)
+
+
+def test_look_at_views_oracle(cuda):
+    """Rotated cameras (the ball views): every integer exact, images/grads in tolerance."""
+    O = _oracle()
+    sa = scenes.ball(20_000, 3, 256, 192, views=8, seed=21)
+    s64 = sa.as_float64()
+    for idx in (0, 3, 6):
+        cam = CameraModel(**sa.cameras[idx])
+        d_color = scenes.cotangent(cam.height, cam.width, seed=idx)
+        ref_out = O.render(s64, cam)
+        ref_g = O.render_backward(s64, cam, ref_out, d_color)
+        got = run_gpu(sa, idx, "half", torch.float64, d_color)
+        assert np.array_equal(got["pair_splat"], ref_out.frame.pair_splat)
+        assert np.array_equal(got["tile_starts"], ref_out.frame.tile_starts)
+        ref = {"color": ref_out.color, "alpha": ref_out.alpha, "depth": ref_out.depth,
+               "transmittance": ref_out.transmittance,
+               "terminal": ref_out.per_pixel_terminal_index}
+        assert_images(got, ref)
+        assert_grads(got, ref_g)
+
+
+def test_radii_match_oracle_formula(cuda):
+    """radii = ceil(3.5 sqrt(lambda_max)) for visible splats, 0 when culled."""
+    gold = load_golden("mini")
+    sa = scenes.frustum(300, 2, 64, 48, seed=3)
+    got = run_gpu(sa, 0)
+    radii = got["radii"]
+    vis = np.zeros(len(sa), bool)
+    vis[gold["valid"]] = True
+    assert (radii[~vis] == 0).all()
+    assert (radii[vis] >= 1).all()
+    # rect span is consistent with the radius: the pixel rect fits in 2*ceil(r)+1
+    assert np.array_equal(np.nonzero(radii)[0], gold["valid"])
