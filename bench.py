@@ -49,7 +49,7 @@ def parse():
 class ClockSampler:
     """nvidia-smi clocks/throttle reasons sampled during the timed region."""
 
-    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    QUERY = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -64,10 +64,13 @@ class ClockSampler:
             self.fh = open(self.path, "w")
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={gpu_index}", f"--query-gpu={self.QUERY}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=self.fh, stderr=subprocess.DEVNULL)
         except (OSError, FileNotFoundError):
             self.proc = None
+
+    def mark(self, which):
+        setattr(self, which, time.time())
 
     def stop(self):
         if self.proc is None:
@@ -85,6 +88,14 @@ class ClockSampler:
                 parts = [p.strip() for p in line.split(",")]
                 if len(parts) < 9:
                     continue
+                try:
+                    ts = time.mktime(time.strptime(parts[0].split(".")[0], "%Y/%m/%d %H:%M:%S"))
+                    ts += float("0." + parts[0].split(".")[1]) if "." in parts[0] else 0.0
+                    t0, t1 = getattr(self, "t_start", 0.0), getattr(self, "t_end", 1e30)
+                    if not (t0 - 0.05 <= ts <= t1 + 0.05):
+                        continue
+                except (ValueError, IndexError):
+                    pass
                 try:
                     sm.append(float(parts[1]))
                     mx = max(mx, float(parts[2]))
@@ -236,18 +247,20 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    clocks = ClockSampler(local, enabled=not args.no_clocks)
     for _ in range(max(args.warmup, 3)):
         step()
     barrier()
-    clocks = ClockSampler(local, enabled=not args.no_clocks)
     launches0 = _native.launch_count()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
+    clocks.mark("t_start")
     start.record()
     for _ in range(args.steps):
         out = step(timer)
     end.record()
     barrier()
+    clocks.mark("t_end")
     clock_info = clocks.stop()
     launches = _native.launch_count() - launches0
     ms = start.elapsed_time(end) / args.steps
@@ -355,7 +368,7 @@ def run_e2e(args, sa, cam, dropin, world, barrier, torch, dist):
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms = float(ms_t.item())
-    h2d = sum(getattr(sa, f).nbytes for f in sa.FIELDS) + d_color.size * 4
+    h2d = sum(getattr(sa, f).nbytes for f in sa.FIELDS) + d_color.nbytes
     d2h = (out.color.size + out.alpha.size + out.depth.size + out.transmittance.size) * 4 + \
         out.per_pixel_terminal_index.nbytes + out.radii.nbytes + \
         sum(getattr(sa, f).nbytes for f in sa.FIELDS) + len(sa) * 8

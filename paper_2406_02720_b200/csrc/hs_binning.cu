@@ -56,7 +56,7 @@ __global__ void gather_counts_kernel(const int32_t* __restrict__ count,
     cnt_r[n] = 0;
     return;
   }
-  const uint32_t i = order[r];
+  const uint32_t i = order[r] & kIndexMask;
   cnt_r[r] = count[i];
   rank_of[i] = (uint32_t)r;
 }
@@ -87,16 +87,19 @@ __global__ void duplicate_kernel(const uint32_t* __restrict__ order,
   if (r >= n) return;
   const int c = cnt_r[r];
   if (c == 0) return;
-  const uint32_t i = order[r];
+  const uint32_t v = order[r];  // index | steep flag, carried into the pair value
+  const uint32_t i = v & kIndexMask;
   const int base = off_r[r];
-  rec[(size_t)i * kRecordFloats + R_PAIR_BASE] = __uint_as_float((uint32_t)base);
   const int4 rc = rect[i];
+  const int spans_x = rc.y - rc.x + 1;
+  rec[(size_t)i * kRecordFloats + R_ROW_ORIGIN] =
+      __int_as_float(base - rc.z * spans_x - rc.x);
   int k = base;
   for (int ty = rc.z; ty <= rc.w; ++ty) {
     const uint32_t row = (uint32_t)ty * (uint32_t)tiles_x;
     for (int tx = rc.x; tx <= rc.y; ++tx, ++k) {
       keys[k] = row + (uint32_t)tx;
-      vals[k] = i;
+      vals[k] = v;
     }
   }
 }
@@ -177,7 +180,7 @@ __global__ void export_splats_kernel(const int32_t* __restrict__ count,
   const float* r = reinterpret_cast<const float*>(rec + 4 * i);
   if (packed)
     for (int c = 0; c < 13; ++c) packed[l * 13 + c] = r[c];
-  if (mode) mode[l] = (int8_t)(__float_as_uint(r[R_MODE_SPANX]) & 3u);
+  if (mode) mode[l] = (int8_t)(__float_as_uint(r[R_FLAGS]) & 3u);
   if (tile_rect) {
     const int4 rc = rect[i];
     tile_rect[4 * l + 0] = rc.x;
@@ -191,7 +194,7 @@ __global__ void export_pairs_kernel(const uint32_t* __restrict__ pair_src,
                                     const int32_t* __restrict__ local_of, int64_t p,
                                     int32_t* __restrict__ pair_splat) {
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (k < p) pair_splat[k] = local_of[pair_src[k]];
+  if (k < p) pair_splat[k] = local_of[pair_src[k] & kIndexMask];
 }
 
 __global__ void widen_kernel(const int32_t* __restrict__ a, int64_t* __restrict__ b, int64_t n) {

@@ -13,7 +13,13 @@
 // gathered 32 at a time with cp.async into a per-warp double buffer and read back
 // as broadcast LDS.128.  Warps pull tiles from a global counter (persistent
 // grid), so long tile lists do not stall a whole CTA.
+//
+// Precision: pixel offsets use mu_hat = hi + lo (float + half residual), so dx
+// is exact to ~3e-8 px at any resolution; "steep" splats (see hs_common.cuh)
+// evaluate the erf argument in FP64 from a side record staged with the record.
 #include <cstdint>
+
+#include <cuda_fp16.h>
 
 #include "hs_common.cuh"
 #include "hs_internal.h"
@@ -38,18 +44,27 @@ __device__ __forceinline__ void cp_async_wait() {
 
 struct WarpStage {
   float4 rec[2][kBatch][4];
+  SteepRec side[2][kBatch];
 };
 
-// Gather the records of pairs [first, first+count) (count <= 32) into `dst`,
-// one record per lane, in the order given by pos(j).
+// Gather the records of `count` (<= 32) pairs, pair j at sorted index
+// k0 + pos(j), into stage slot j (one lane per record); steep splats also get
+// their FP64 side record.
 template <typename PosFn>
 __device__ __forceinline__ void issue_batch(const BlendGeom& g, int k0, int count, PosFn pos,
-                                            float4 (*dst)[4], int lane) {
+                                            WarpStage& st, int stage, int lane) {
   if (lane < count) {
-    const uint32_t idx = g.pair_src[k0 + pos(lane)];
+    const uint32_t v = g.pair_src[k0 + pos(lane)];
+    const uint32_t idx = v & kIndexMask;
     const float4* src = g.rec + 4 * (size_t)idx;
 #pragma unroll
-    for (int c = 0; c < 4; ++c) cp_async16(&dst[lane][c], src + c);
+    for (int c = 0; c < 4; ++c) cp_async16(&st.rec[stage][lane][c], src + c);
+    if (v & kSteepBit) {
+      const char* s = reinterpret_cast<const char*>(g.side + idx);
+      char* d = reinterpret_cast<char*>(&st.side[stage][lane]);
+      cp_async16(d, s);
+      cp_async16(d + 16, s + 16);
+    }
   }
   cp_async_commit();
 }
@@ -62,28 +77,66 @@ __device__ __forceinline__ int next_tile(const BlendGeom& g, int lane) {
   return g.tile_order ? g.tile_order[t] : g.tile_lo + t;
 }
 
+// Per-(splat, lane) constants shared by the forward and backward pixel loops.
+struct SplatLane {
+  float dx, dy0;       // pixel offsets of row 0 (dy of row i = dy0 + 2i)
+  float A, B, C;       // conic scaled to log2: power = dx*(A dx + B dy) + C dy^2
+  float P0, Bx;        // A dx^2, B dx
+  float za, zb, Z0;    // erf coefficients, za*dx
+  double zbd, Z0d, py0d, muyd;  // steep path (FP64)
+};
+
+template <bool STEEP>
+__device__ __forceinline__ SplatLane splat_lane(const float4 (&q)[4], const SteepRec& side,
+                                                float px, float py0) {
+  SplatLane s;
+  const __half2 lo = *reinterpret_cast<const __half2*>(&q[3].w);
+  const float2 lof = __half22float2(lo);
+  s.dx = (px - q[0].x) - lof.x;
+  s.dy0 = (py0 - q[0].y) - lof.y;
+  s.A = q[0].z * kNegHalfLog2e;
+  s.B = q[0].w * kNegLog2e;
+  s.C = q[1].x * kNegHalfLog2e;
+  s.P0 = s.A * s.dx * s.dx;
+  s.Bx = s.B * s.dx;
+  s.za = q[1].y;
+  s.zb = q[1].z;
+  s.Z0 = s.za * s.dx;
+  if (STEEP) {
+    s.zbd = side.zb;
+    s.Z0d = side.za * ((double)px - side.mux);
+    s.py0d = (double)py0;
+    s.muyd = side.muy;
+  }
+  return s;
+}
+
+template <bool STEEP>
+__device__ __forceinline__ float erf_arg(const SplatLane& s, float dy, int i) {
+  if (STEEP) return (float)fma(s.zbd, (s.py0d + 2.0 * i) - s.muyd, s.Z0d);
+  return fmaf(s.zb, dy, s.Z0);
+}
+
 // ---------------------------------------------------------------------------
 // K5 forward
-template <int MODE>
-__device__ __forceinline__ void fwd_splat(const float4 (&q)[4], float px, float py0, float (&T)[kPx],
-                                          float (&ar)[kPx], float (&ag)[kPx], float (&ab)[kPx],
-                                          float (&ad)[kPx], int (&cnt)[kPx], unsigned& alive) {
-  const float mux = q[0].x, muy = q[0].y;
-  const float A = q[0].z * kNegHalfLog2e, B = q[0].w * kNegLog2e, C = q[1].x * kNegHalfLog2e;
-  const float za = q[1].y, zb = q[1].z, c1 = q[1].w, c2 = q[2].x;
+template <int MODE, bool STEEP>
+__device__ __forceinline__ void fwd_splat(const float4 (&q)[4], const SteepRec& side, float px,
+                                          float py0, float (&T)[kPx], float (&ar)[kPx],
+                                          float (&ag)[kPx], float (&ab)[kPx], float (&ad)[kPx],
+                                          int (&cnt)[kPx], unsigned& alive) {
+  const SplatLane s = splat_lane<STEEP>(q, side, px, py0);
+  const float c1 = q[1].w, c2 = q[2].x;
   const float cr = q[2].y, cg = q[2].z, cb = q[2].w, z = q[3].x;
-  const float dx = px - mux;
-  const float P0 = A * dx * dx, Bx = B * dx, Z0 = za * dx;
 #pragma unroll
   for (int i = 0; i < kPx; ++i) {
     if (alive & (1u << i)) {
-      const float dy = (py0 + 2.0f * i) - muy;
-      const float g = ex2_approx(fmaf(fmaf(C, dy, Bx), dy, P0));
+      const float dy = s.dy0 + 2.0f * i;
+      const float g = ex2_approx(fmaf(fmaf(s.C, dy, s.Bx), dy, s.P0));
       float w;
       if (MODE == kModeErf) {
-        w = fmaf(c2, erf32(fmaf(zb, dy, Z0)), c1) * g;
+        w = fmaf(c2, erf32(erf_arg<STEEP>(s, dy, i)), c1) * g;
       } else if (MODE == kModeSign) {
-        w = fmaf(c2, sign32(fmaf(zb, dy, Z0)), c1) * g;
+        w = fmaf(c2, sign32(erf_arg<STEEP>(s, dy, i)), c1) * g;
       } else {
         w = c1 * g;
       }
@@ -130,29 +183,37 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) blend_fwd_kernel(
     const int k0 = g.tile_starts[tile];
     const int nk = g.tile_starts[tile + 1] - k0;
     auto fwd_pos = [](int j) { return j; };
-    if (nk > 0) issue_batch(g, k0, min(kBatch, nk), fwd_pos, st.rec[0], lane);
+    if (nk > 0) issue_batch(g, k0, min(kBatch, nk), fwd_pos, st, 0, lane);
     for (int b = 0; b * kBatch < nk; ++b) {
       const int nb = min(kBatch, nk - b * kBatch);
       if ((b + 1) * kBatch < nk)
-        issue_batch(g, k0 + (b + 1) * kBatch, min(kBatch, nk - (b + 1) * kBatch), fwd_pos,
-                    st.rec[(b + 1) & 1], lane);
+        issue_batch(g, k0 + (b + 1) * kBatch, min(kBatch, nk - (b + 1) * kBatch), fwd_pos, st,
+                    (b + 1) & 1, lane);
       else
         cp_async_commit();
       cp_async_wait<1>();
       __syncwarp();
-      const float4(*buf)[4] = st.rec[b & 1];
+      const int s = b & 1;
       bool any = true;
       for (int j = 0; j < nb; ++j) {
         any = __any_sync(0xffffffffu, alive != 0);
         if (!any) break;
-        const float4 q[4] = {buf[j][0], buf[j][1], buf[j][2], buf[j][3]};
-        const int mode = (int)(__float_as_uint(q[3].y) & 3u);
-        if (mode == kModeErf)
-          fwd_splat<kModeErf>(q, px, py0, T, ar, ag, ab, ad, cnt, alive);
-        else if (mode == kModeSign)
-          fwd_splat<kModeSign>(q, px, py0, T, ar, ag, ab, ad, cnt, alive);
-        else
-          fwd_splat<kModePlain>(q, px, py0, T, ar, ag, ab, ad, cnt, alive);
+        const float4 q[4] = {st.rec[s][j][0], st.rec[s][j][1], st.rec[s][j][2], st.rec[s][j][3]};
+        const uint32_t flags = __float_as_uint(q[3].y);
+        const int mode = (int)(flags & 3u);
+        const SteepRec& side = st.side[s][j];
+        if (flags & 4u) {
+          if (mode == kModeErf)
+            fwd_splat<kModeErf, true>(q, side, px, py0, T, ar, ag, ab, ad, cnt, alive);
+          else
+            fwd_splat<kModeSign, true>(q, side, px, py0, T, ar, ag, ab, ad, cnt, alive);
+        } else if (mode == kModeErf) {
+          fwd_splat<kModeErf, false>(q, side, px, py0, T, ar, ag, ab, ad, cnt, alive);
+        } else if (mode == kModeSign) {
+          fwd_splat<kModeSign, false>(q, side, px, py0, T, ar, ag, ab, ad, cnt, alive);
+        } else {
+          fwd_splat<kModePlain, false>(q, side, px, py0, T, ar, ag, ab, ad, cnt, alive);
+        }
       }
       __syncwarp();
       if (!any) break;
@@ -179,33 +240,33 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) blend_fwd_kernel(
 // ---------------------------------------------------------------------------
 // K6 backward
 struct BwdAcc {
-  float s0, s1, s2, q0, q1, c1, c2, r, g, b;
+  float s0, s1, s2;  // sum d_pow, d_pow*dy, d_pow*dy^2 (dx is constant per lane)
+  float q0, q1, qz;  // sum d_z, d_z*dy, d_z*z
+  float c1, c2, r, g, b;
 };
 
-template <int MODE>
-__device__ __forceinline__ void bwd_splat(const float4 (&q)[4], int pos, float px, float py0,
-                                          float (&T)[kPx], float (&D)[kPx], const float (&dr)[kPx],
-                                          const float (&dg)[kPx], const float (&db)[kPx],
-                                          const int (&cnt)[kPx], BwdAcc& a) {
-  const float mux = q[0].x, muy = q[0].y;
-  const float A = q[0].z * kNegHalfLog2e, B = q[0].w * kNegLog2e, C = q[1].x * kNegHalfLog2e;
-  const float za = q[1].y, zb = q[1].z, c1 = q[1].w, c2 = q[2].x;
+template <int MODE, bool STEEP>
+__device__ __forceinline__ void bwd_splat(const float4 (&q)[4], const SteepRec& side, int pos,
+                                          float px, float py0, float (&T)[kPx], float (&D)[kPx],
+                                          const float (&dr)[kPx], const float (&dg)[kPx],
+                                          const float (&db)[kPx], const int (&cnt)[kPx],
+                                          BwdAcc& a) {
+  const SplatLane s = splat_lane<STEEP>(q, side, px, py0);
+  const float c1 = q[1].w, c2 = q[2].x;
   const float cr = q[2].y, cg = q[2].z, cb = q[2].w;
   const float c2k = c2 * (2.0f * kInvSqrtPi);
-  const float dx = px - mux;
-  const float P0 = A * dx * dx, Bx = B * dx, Z0 = za * dx;
 #pragma unroll
   for (int i = 0; i < kPx; ++i) {
     if (pos < cnt[i]) {
-      const float dy = (py0 + 2.0f * i) - muy;
-      const float gg = ex2_approx(fmaf(fmaf(C, dy, Bx), dy, P0));
+      const float dy = s.dy0 + 2.0f * i;
+      const float gg = ex2_approx(fmaf(fmaf(s.C, dy, s.Bx), dy, s.P0));
       float e = 0.f, zz = 0.f, u;
       if (MODE == kModeErf) {
-        zz = fmaf(zb, dy, Z0);
+        zz = erf_arg<STEEP>(s, dy, i);
         e = erf32(zz);
         u = fmaf(c2, e, c1);
       } else if (MODE == kModeSign) {
-        e = sign32(fmaf(zb, dy, Z0));
+        e = sign32(erf_arg<STEEP>(s, dy, i));
         u = fmaf(c2, e, c1);
       } else {
         u = c1;
@@ -232,6 +293,7 @@ __device__ __forceinline__ void bwd_splat(const float4 (&q)[4], int pos, float p
           const float d_z = dwg * c2k * ex2_approx(-(zz * zz) * kLog2e);
           a.q0 += d_z;
           a.q1 = fmaf(d_z, dy, a.q1);
+          a.qz = fmaf(d_z, zz, a.qz);
         }
       }
       D[i] = fmaf(wt, dcr, D[i]);
@@ -273,12 +335,17 @@ __device__ __forceinline__ float warp_transpose_reduce16(float (&v)[16], int lan
   return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
 }
 
+// kRowsBySortedPos: Seam 1 layout (row k = sorted pair index, 12 reference
+// columns).  Otherwise the generation-order layout: row = record origin +
+// ty*spans_x + tx, kRowFloats columns, consumed by K7.
 template <bool kRowsBySortedPos>
 __global__ void __launch_bounds__(kWarpsPerCta * 32) blend_bwd_kernel(
     BlendGeom g, float bg0, float bg1, float bg2, const float* __restrict__ d_color,
     const float* __restrict__ trans, const int32_t* __restrict__ terminal,
     float* __restrict__ rows, int32_t* __restrict__ last_rank,
     const uint32_t* __restrict__ rank_of) {
+  constexpr int kStride = kRowsBySortedPos ? 12 : kRowFloats;
+  constexpr int kCols = kRowsBySortedPos ? 12 : 13;
   __shared__ WarpStage stage_all[kWarpsPerCta];
   const int lane = threadIdx.x & 31;
   WarpStage& st = stage_all[threadIdx.x >> 5];
@@ -312,43 +379,51 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) blend_bwd_kernel(
     maxc = __reduce_max_sync(0xffffffffu, maxc);
     const int k0 = g.tile_starts[tile];
     if (!kRowsBySortedPos && lane == 0)
-      last_rank[tile] = maxc > 0 ? (int32_t)rank_of[g.pair_src[k0 + maxc - 1]] : -1;
+      last_rank[tile] =
+          maxc > 0 ? (int32_t)rank_of[g.pair_src[k0 + maxc - 1] & kIndexMask] : -1;
     if (maxc == 0) continue;
-    // positions maxc-1 .. 0, batch b holds positions hi_b - j for j < nb
+    // positions maxc-1 .. 0; batch b holds positions hi_b - j for j < nb
     auto batch_hi = [&](int b) { return maxc - 1 - b * kBatch; };
     {
       const int hi = batch_hi(0);
-      issue_batch(g, k0, min(kBatch, hi + 1), [hi](int j) { return hi - j; }, st.rec[0], lane);
+      issue_batch(g, k0, min(kBatch, hi + 1), [hi](int j) { return hi - j; }, st, 0, lane);
     }
-    const int ty0_tile = ty, tx0_tile = tx;
     for (int b = 0; b * kBatch < maxc; ++b) {
       const int hi = batch_hi(b);
       const int nb = min(kBatch, hi + 1);
       if ((b + 1) * kBatch < maxc) {
         const int hi2 = batch_hi(b + 1);
-        issue_batch(g, k0, min(kBatch, hi2 + 1), [hi2](int j) { return hi2 - j; },
-                    st.rec[(b + 1) & 1], lane);
+        issue_batch(g, k0, min(kBatch, hi2 + 1), [hi2](int j) { return hi2 - j; }, st,
+                    (b + 1) & 1, lane);
       } else {
         cp_async_commit();
       }
       cp_async_wait<1>();
       __syncwarp();
-      const float4(*buf)[4] = st.rec[b & 1];
+      const int s = b & 1;
       for (int j = 0; j < nb; ++j) {
         const int pos = hi - j;
-        const float4 q[4] = {buf[j][0], buf[j][1], buf[j][2], buf[j][3]};
-        const uint32_t ms = __float_as_uint(q[3].y);
-        const int mode = (int)(ms & 3u);
-        BwdAcc a = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        if (mode == kModeErf)
-          bwd_splat<kModeErf>(q, pos, px, py0, T, D, dr, dg, db, cnt, a);
-        else if (mode == kModeSign)
-          bwd_splat<kModeSign>(q, pos, px, py0, T, D, dr, dg, db, cnt, a);
-        else
-          bwd_splat<kModePlain>(q, pos, px, py0, T, D, dr, dg, db, cnt, a);
-        // per-lane partials -> the 12 pair-row columns (_blend_py.py:16-18)
+        const float4 q[4] = {st.rec[s][j][0], st.rec[s][j][1], st.rec[s][j][2], st.rec[s][j][3]};
+        const SteepRec& side = st.side[s][j];
+        const uint32_t flags = __float_as_uint(q[3].y);
+        const int mode = (int)(flags & 3u);
+        BwdAcc a = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        if (flags & 4u) {
+          if (mode == kModeErf)
+            bwd_splat<kModeErf, true>(q, side, pos, px, py0, T, D, dr, dg, db, cnt, a);
+          else
+            bwd_splat<kModeSign, true>(q, side, pos, px, py0, T, D, dr, dg, db, cnt, a);
+        } else if (mode == kModeErf) {
+          bwd_splat<kModeErf, false>(q, side, pos, px, py0, T, D, dr, dg, db, cnt, a);
+        } else if (mode == kModeSign) {
+          bwd_splat<kModeSign, false>(q, side, pos, px, py0, T, D, dr, dg, db, cnt, a);
+        } else {
+          bwd_splat<kModePlain, false>(q, side, pos, px, py0, T, D, dr, dg, db, cnt, a);
+        }
+        // per-lane partials -> the pair-row columns (_blend_py.py:16-18)
         const float ca = q[0].z, cb = q[0].w, cc = q[1].x, za = q[1].y, zb = q[1].z;
-        const float dx = px - q[0].x;
+        const float2 lo = __half22float2(*reinterpret_cast<const __half2*>(&q[3].w));
+        const float dx = (px - q[0].x) - lo.x;
         float v[16];
         v[0] = fmaf(ca * dx, a.s0, fmaf(cb, a.s1, -za * a.q0));
         v[1] = fmaf(cc, a.s1, fmaf(cb * dx, a.s0, -zb * a.q0));
@@ -362,19 +437,18 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) blend_bwd_kernel(
         v[9] = a.r;
         v[10] = a.g;
         v[11] = a.b;
-        v[12] = v[13] = v[14] = v[15] = 0.f;
+        v[12] = a.qz;
+        v[13] = v[14] = v[15] = 0.f;
         const float total = warp_transpose_reduce16(v, lane);
         size_t row;
         if (kRowsBySortedPos) {
           row = (size_t)(k0 + pos);
         } else {
-          const uint32_t txy = __float_as_uint(q[3].w);
-          const int spans_x = (int)(ms >> 2);
-          row = (size_t)__float_as_uint(q[3].z) +
-                (size_t)((ty0_tile - (int)(txy >> 16)) * spans_x + (tx0_tile - (int)(txy & 0xffffu)));
+          const int spans_x = (int)(flags >> 3);
+          row = (size_t)((int)__float_as_uint(q[3].z) + ty * spans_x + tx);
         }
         const int vi = lane >> 1;
-        if (!(lane & 1) && vi < 12) rows[row * 12 + vi] = total;
+        if (!(lane & 1) && vi < kCols) rows[row * kStride + vi] = total;
       }
       __syncwarp();
     }
@@ -383,26 +457,52 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) blend_bwd_kernel(
   }
 }
 
-// Seam 1: reference packed (M,13) float64 + mode int8 -> 64-B records.
+// Seam 1: reference packed (M,13) float64 + mode int8 -> records; steep splats
+// get side records and bit 31 in their pair values.
 __global__ void pack_records_kernel(const double* __restrict__ packed,
                                     const int8_t* __restrict__ mode, int64_t m,
-                                    float* __restrict__ rec) {
+                                    float* __restrict__ rec, SteepRec* __restrict__ side,
+                                    uint8_t* __restrict__ steep_flag) {
   const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (l >= m) return;
+  const double* p = packed + l * 13;
   float* r = rec + l * kRecordFloats;
-  for (int c = 0; c < 13; ++c) r[c] = (float)packed[l * 13 + c];
-  r[R_MODE_SPANX] = __uint_as_float(pack_mode_spanx(mode[l] & 3, 0));
-  r[R_PAIR_BASE] = __uint_as_float(0u);
-  r[R_TXY] = __uint_as_float(0u);
+  for (int c = 0; c < 13; ++c) r[c] = (float)p[c];
+  const int md = mode[l] & 3;
+  // reach from the dilated covariance = inverse of the conic (rasterizer.py:194-200)
+  const double a = p[2], b = p[3], c = p[4], det = a * c - b * b;
+  const double ia = c / det, ic = a / det, idet = ia * ic - (b / det) * (b / det);
+  const double mid = 0.5 * (ia + ic);
+  const double lam = mid + sqrt(fmax(mid * mid - idet, 0.0));
+  const double reach = kRadiusSigmas * sqrt(fmax(lam, 0.0)) + 24.0;
+  const bool steep = md != kModePlain && is_steep(p[5], p[6], reach);
+  const float mux = (float)p[0], muy = (float)p[1];
+  const __half2 lo = __floats2half2_rn((float)(p[0] - (double)mux), (float)(p[1] - (double)muy));
+  r[R_FLAGS] = __uint_as_float(pack_flags(md, steep, 0));
+  r[R_ROW_ORIGIN] = __int_as_float(0);
+  r[R_MU_LO] = __uint_as_float(*reinterpret_cast<const uint32_t*>(&lo));
+  if (steep) side[l] = SteepRec{p[0], p[1], p[5], p[6]};
+  steep_flag[l] = steep ? 1 : 0;
 }
 
+__global__ void mark_steep_pairs_kernel(const uint8_t* __restrict__ steep_flag,
+                                        uint32_t* __restrict__ pairs, int64_t p) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < p && steep_flag[pairs[k]]) pairs[k] |= kSteepBit;
+}
+
+// Persistent grid: resident CTAs per SM x SMs (queried once per process).
 static int blend_grid(int n_work) {
-  int dev = 0, sms = 148, per_sm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, blend_bwd_kernel<false>,
-                                                kWarpsPerCta * 32, 0);
-  if (per_sm < 1) per_sm = 1;
+  static int sms = 0, per_sm = 0;
+  if (sms == 0) {
+    int dev = 0, s = 148, p = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&s, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p, blend_bwd_kernel<false>,
+                                                  kWarpsPerCta * 32, 0);
+    per_sm = p < 1 ? 1 : p;
+    sms = s;
+  }
   const int want = (n_work + kWarpsPerCta - 1) / kWarpsPerCta;
   const int cap = sms * per_sm;
   return want < cap ? (want > 0 ? want : 1) : cap;
@@ -436,13 +536,21 @@ cudaError_t launch_blend_bwd(const BlendGeom& g, float bg0, float bg1, float bg2
 }
 
 cudaError_t launch_pack_records(const double* packed, const int8_t* mode, int64_t m, float4* rec,
-                                cudaStream_t stream) {
+                                SteepRec* side, uint32_t* pairs, int64_t p, cudaStream_t stream) {
   if (m == 0) return cudaSuccess;
   const int block = 256;
+  uint8_t* flag = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&flag), m, stream);
+  if (e != cudaSuccess) return e;
   pack_records_kernel<<<(unsigned)((m + block - 1) / block), block, 0, stream>>>(
-      packed, mode, m, reinterpret_cast<float*>(rec));
-  note_launch();
-  return cudaGetLastError();
+      packed, mode, m, reinterpret_cast<float*>(rec), side, flag);
+  if (p > 0)
+    mark_steep_pairs_kernel<<<(unsigned)((p + block - 1) / block), block, 0, stream>>>(flag, pairs,
+                                                                                      p);
+  note_launch(2);
+  e = cudaGetLastError();
+  cudaFreeAsync(flag, stream);
+  return e;
 }
 
 }  // namespace hs

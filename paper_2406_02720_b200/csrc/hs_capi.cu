@@ -1,6 +1,8 @@
 // hs_capi.cu -- extern "C" entry points of libhalfsplat_b200.so
 // (declared in include/halfsplat_b200.h).
 #include <atomic>
+#include <map>
+#include <mutex>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -46,6 +48,7 @@ struct Carver {
 
 struct FrameBufs {
   float4* rec;
+  SteepRec* side;
   int4* rect;
   int32_t* count;
   uint64_t* dkey_in;
@@ -64,15 +67,42 @@ struct FrameBufs {
   size_t temp_bytes;
 };
 
+// CUB temp-storage queries cost tens of microseconds (device attribute and
+// occupancy lookups), and every entry point validates its workspace, so the
+// sizes are memoised.  Counts are rounded up to a power of two: CUB's temp
+// storage is monotone in the item count, so the bucket's size is an upper bound.
+static int64_t pow2_bucket(int64_t n) {
+  int64_t b = 1024;
+  while (b < n) b <<= 1;
+  return b;
+}
+
+static std::mutex g_size_mu;
+static std::map<int64_t, size_t> g_frame_temp;
+static std::map<std::pair<int64_t, int>, size_t> g_pair_temp;
+
 static size_t frame_temp_bytes(int64_t n) {
-  const size_t a = depth_sort_temp_bytes(n), b = scan_temp_bytes(n);
-  return a > b ? a : b;
+  const int64_t b = pow2_bucket(n);
+  std::lock_guard<std::mutex> lock(g_size_mu);
+  auto it = g_frame_temp.find(b);
+  if (it != g_frame_temp.end()) return it->second;
+  const size_t x = depth_sort_temp_bytes(b), y = scan_temp_bytes(b);
+  return g_frame_temp[b] = x > y ? x : y;
+}
+
+static size_t pair_temp_bytes(int64_t p, int tile_bits) {
+  const auto key = std::make_pair(pow2_bucket(p), tile_bits);
+  std::lock_guard<std::mutex> lock(g_size_mu);
+  auto it = g_pair_temp.find(key);
+  if (it != g_pair_temp.end()) return it->second;
+  return g_pair_temp[key] = pair_sort_temp_bytes(key.first, tile_bits);
 }
 
 static FrameBufs carve_frame(void* ws, int64_t n, int n_tiles, size_t* total) {
   Carver c(ws);
   FrameBufs f;
   f.rec = c.take<float4>(4 * (size_t)n);
+  f.side = c.take<SteepRec>(n);
   f.rect = c.take<int4>(n);
   f.count = c.take<int32_t>(n);
   f.dkey_in = c.take<uint64_t>(n);
@@ -109,8 +139,8 @@ static BinBufs carve_bin(void* ws, int64_t p, int tile_bits, size_t* total) {
   b.keys[1] = c.take<uint32_t>(pp);
   b.vals[0] = c.take<uint32_t>(pp);
   b.vals[1] = c.take<uint32_t>(pp);
-  b.rows = c.take<float>(pp * HS_PAIR_GRAD_COLS);
-  b.temp_bytes = pair_sort_temp_bytes(p, tile_bits);
+  b.rows = c.take<float>(pp * kRowFloats);
+  b.temp_bytes = pair_temp_bytes(p, tile_bits);
   b.temp = c.take<char>(b.temp_bytes);
   if (total) *total = c.off;
   return b;
@@ -268,12 +298,12 @@ int hs_preprocess_fwd(hs_frame* frame, const hs_scene* scene, const hs_camera* c
   const CamArgs ca = cam_args(cam);
   if (scene->dtype == HS_DTYPE_F32) {
     HS_CUDA(launch_preprocess_fwd_t<float>(scene_args<float>(scene), ca, frame->kernel, frame->n,
-                                           f.rec, f.rect, f.count, f.dkey_in, f.dval, radii,
-                                           stream));
+                                           f.rec, f.side, f.rect, f.count, f.dkey_in, f.dval,
+                                           radii, stream));
   } else {
     HS_CUDA(launch_preprocess_fwd_t<double>(scene_args<double>(scene), ca, frame->kernel,
-                                            frame->n, f.rec, f.rect, f.count, f.dkey_in, f.dval,
-                                            radii, stream));
+                                            frame->n, f.rec, f.side, f.rect, f.count, f.dkey_in,
+                                            f.dval, radii, stream));
   }
   HS_CUDA(run_depth_sort(f.temp, f.temp_bytes, f.dkey_in, f.dkey_out, f.dval, f.order, frame->n,
                          stream));
@@ -322,6 +352,7 @@ static BlendGeom frame_geom(const hs_frame* frame, const FrameBufs& f, const Bin
   g.tile_starts = f.tile_starts;
   g.pair_src = b.vals[frame->sort_selector];
   g.rec = f.rec;
+  g.side = f.side;
   g.width = frame->width;
   g.height = frame->height;
   g.tiles_x = frame->tiles_x;
@@ -446,10 +477,11 @@ int hs_forward_tiles(const double* packed, const int8_t* mode, const int32_t* pa
   cudaStream_t s;
   HS_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
   struct StreamGuard { cudaStream_t s; ~StreamGuard() { cudaStreamDestroy(s); } } sg{s};
-  DevBuf d_packed, d_mode, d_rec, d_pairs, d_ts, d_out, d_term, d_ctr;
+  DevBuf d_packed, d_mode, d_rec, d_side, d_pairs, d_ts, d_out, d_term, d_ctr;
   HS_CUDA(d_packed.alloc(m * 13 * sizeof(double)));
   HS_CUDA(d_mode.alloc(m));
   HS_CUDA(d_rec.alloc(m * 64));
+  HS_CUDA(d_side.alloc(m * sizeof(SteepRec)));
   HS_CUDA(d_pairs.alloc(p * 4));
   HS_CUDA(d_ts.alloc((n_tiles + 1) * 4));
   HS_CUDA(d_out.alloc(npx * 6 * sizeof(float)));
@@ -462,11 +494,12 @@ int hs_forward_tiles(const double* packed, const int8_t* mode, const int32_t* pa
   if (p > 0) HS_CUDA(cudaMemcpyAsync(d_pairs.p, pair_splat, p * 4, cudaMemcpyHostToDevice, s));
   HS_CUDA(cudaMemcpyAsync(d_ts.p, ts32.data(), (n_tiles + 1) * 4, cudaMemcpyHostToDevice, s));
   HS_CUDA(launch_pack_records((const double*)d_packed.p, (const int8_t*)d_mode.p, m,
-                              (float4*)d_rec.p, s));
+                              (float4*)d_rec.p, (SteepRec*)d_side.p, (uint32_t*)d_pairs.p, p, s));
   BlendGeom g;
   g.tile_starts = (const int32_t*)d_ts.p;
   g.pair_src = (const uint32_t*)d_pairs.p;
   g.rec = (const float4*)d_rec.p;
+  g.side = (const SteepRec*)d_side.p;
   g.width = width;
   g.height = height;
   g.tiles_x = tiles_x;
@@ -515,10 +548,11 @@ int hs_backward_tiles(const double* packed, const int8_t* mode, const int32_t* p
   cudaStream_t s;
   HS_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
   struct StreamGuard { cudaStream_t s; ~StreamGuard() { cudaStreamDestroy(s); } } sg{s};
-  DevBuf d_packed, d_mode, d_rec, d_pairs, d_ts, d_in, d_term, d_rows, d_ctr;
+  DevBuf d_packed, d_mode, d_rec, d_side, d_pairs, d_ts, d_in, d_term, d_rows, d_ctr;
   HS_CUDA(d_packed.alloc(m * 13 * sizeof(double)));
   HS_CUDA(d_mode.alloc(m));
   HS_CUDA(d_rec.alloc(m * 64));
+  HS_CUDA(d_side.alloc(m * sizeof(SteepRec)));
   HS_CUDA(d_pairs.alloc(p * 4));
   HS_CUDA(d_ts.alloc((n_tiles + 1) * 4));
   HS_CUDA(d_in.alloc(npx * 4 * sizeof(float)));
@@ -533,11 +567,12 @@ int hs_backward_tiles(const double* packed, const int8_t* mode, const int32_t* p
   HS_CUDA(cudaMemcpyAsync(d_term.p, terminal, npx * 4, cudaMemcpyHostToDevice, s));
   HS_CUDA(cudaMemsetAsync(d_rows.p, 0, p * 12 * sizeof(float), s));
   HS_CUDA(launch_pack_records((const double*)d_packed.p, (const int8_t*)d_mode.p, m,
-                              (float4*)d_rec.p, s));
+                              (float4*)d_rec.p, (SteepRec*)d_side.p, (uint32_t*)d_pairs.p, p, s));
   BlendGeom g;
   g.tile_starts = (const int32_t*)d_ts.p;
   g.pair_src = (const uint32_t*)d_pairs.p;
   g.rec = (const float4*)d_rec.p;
+  g.side = (const SteepRec*)d_side.p;
   g.width = width;
   g.height = height;
   g.tiles_x = tiles_x;

@@ -19,16 +19,44 @@ constexpr float kLog2e = 1.4426950408889634f;
 
 // Per-splat record: 64 bytes, one per primitive (indexed by original index).
 // Slots 0..12 are the reference's `packed` columns rounded to float32
-// (layout of _blend_py.py:9-15); slots 13..15 carry the blend mode and the
-// pair-row bookkeeping the backward needs.
+// (layout of _blend_py.py:9-15; mu_hat keeps its rounding residual in R_MU_LO so
+// pixel offsets are exact to ~3e-8 px even at 4K); slots 13..15 carry the blend
+// mode and the pair-row bookkeeping the backward needs.
 enum RecordSlot {
   R_MUX = 0, R_MUY, R_CA, R_CB, R_CC, R_ZA, R_ZB, R_C1, R_C2,
   R_RED, R_GREEN, R_BLUE, R_DEPTH,
-  R_MODE_SPANX,  // u32: mode (bits 0-1) | spans_x << 2
-  R_PAIR_BASE,   // u32: first generation-order pair index of this splat
-  R_TXY          // u32: tx0 | ty0 << 16 (tile rect origin)
+  R_FLAGS,       // u32: mode (bits 0-1) | steep (bit 2) | spans_x << 3
+  R_ROW_ORIGIN,  // i32: pair_base - ty0*spans_x - tx0; pair (tx,ty) -> row origin + ty*spans_x + tx
+  R_MU_LO        // half2: (mux - (float)mux, muy - (float)muy)
 };
 constexpr int kRecordFloats = 16;
+
+// "Steep" splats: erf argument z = za*dx + zb*dy with |za|,|zb| so large (the
+// splitting plane nearly contains the ray, |n_ray.z| small) that FP32 cannot
+// resolve z near the plane.  Their z is evaluated in FP64 from this side record;
+// the flag also rides in bit 31 of the sort value so the blend's staging lane
+// knows to fetch it.  Criterion: (|za| + |zb|) * reach > kSteepLimit, reach =
+// radius + 24 px bounds |dx|,|dy| inside any covered tile, so non-steep splats
+// keep |z| rounding error below ~6e-8 * 64 = 4e-6.
+struct __align__(16) SteepRec {
+  double mux, muy, za, zb;
+};
+constexpr double kSteepLimit = 64.0;
+constexpr uint32_t kSteepBit = 0x80000000u;
+constexpr uint32_t kIndexMask = 0x7fffffffu;
+
+// Internal generation-order pair rows: the reference's 12 columns
+// (_blend_py.py:16-18) plus column 12 = sum over pixels of d_z * z, which gives
+// d(loss)/d(1/(sqrt2 |n3|)) without the cancellation of za*d_za + zb*d_zb.
+constexpr int kRowFloats = 16;
+constexpr int kColSumDzZ = 12;
+
+__host__ __device__ __forceinline__ uint32_t pack_flags(int mode, bool steep, int spans_x) {
+  return (uint32_t)mode | (steep ? 4u : 0u) | ((uint32_t)spans_x << 3);
+}
+__host__ __device__ __forceinline__ bool is_steep(double za, double zb, double reach) {
+  return (fabs(za) + fabs(zb)) * reach > kSteepLimit;
+}
 
 // Blend modes (_blend_py.py:13-14).
 constexpr int kModeErf = 0;
@@ -66,10 +94,6 @@ __device__ __forceinline__ float erf32(float z) {
 // _blend_cy.pyx:66-71
 __device__ __forceinline__ float sign32(float x) {
   return x > 0.f ? 1.f : (x < 0.f ? -1.f : 0.f);
-}
-
-__host__ __device__ __forceinline__ uint32_t pack_mode_spanx(int mode, int spans_x) {
-  return (uint32_t)mode | ((uint32_t)spans_x << 2);
 }
 
 }  // namespace hs

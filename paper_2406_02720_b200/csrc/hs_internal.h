@@ -6,6 +6,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "hs_common.cuh"
+
 namespace hs {
 
 template <typename T>
@@ -45,9 +47,9 @@ struct GradArgs {
 // ---- hs_preprocess.cu -----------------------------------------------------
 template <typename T>
 cudaError_t launch_preprocess_fwd_t(const SceneArgs<T>& sc, const CamArgs& cam, int kernel,
-                                    int64_t n, float4* rec, int4* rect, int32_t* count,
-                                    uint64_t* dkey, uint32_t* dval, int32_t* radii,
-                                    cudaStream_t stream);
+                                    int64_t n, float4* rec, SteepRec* side, int4* rect,
+                                    int32_t* count, uint64_t* dkey, uint32_t* dval,
+                                    int32_t* radii, cudaStream_t stream);
 template <typename T>
 cudaError_t launch_preprocess_bwd_t(const SceneArgs<T>& sc, const CamArgs& cam, int kernel,
                                     int64_t n, int tiles_x, const float4* rec, const int4* rect,
@@ -60,6 +62,7 @@ struct BlendGeom {
   const int32_t* tile_starts;  // (n_tiles+1) CSR offsets into pair_src
   const uint32_t* pair_src;    // sorted pair -> record index
   const float4* rec;           // 4 float4 per record
+  const SteepRec* side;        // FP64 side records of steep splats (flag: bit 31 of pair_src)
   int width, height, tiles_x;
   int tile_lo, n_work;         // tiles [tile_lo, tile_lo + n_work)
   const int32_t* tile_order;   // optional work order (nullptr = natural)
@@ -75,8 +78,11 @@ cudaError_t launch_blend_bwd(const BlendGeom& g, float bg0, float bg1, float bg2
                              const float* d_color, const float* trans, const int32_t* terminal,
                              float* rows, int32_t* last_rank, const uint32_t* rank_of,
                              bool rows_by_sorted_pos, cudaStream_t stream);
+// Seam 1: reference packed (M,13) f64 + mode -> records + side records; marks
+// steep splats in bit 31 of pair_splat (in place, device copy).
 cudaError_t launch_pack_records(const double* packed, const int8_t* mode, int64_t m,
-                                float4* rec, cudaStream_t stream);
+                                float4* rec, SteepRec* side, uint32_t* pairs, int64_t p,
+                                cudaStream_t stream);
 
 // ---- hs_binning.cu --------------------------------------------------------
 size_t depth_sort_temp_bytes(int64_t n);

@@ -11,6 +11,8 @@
 #include <cmath>
 #include <cstdint>
 
+#include <cuda_fp16.h>
+
 #include "hs_common.cuh"
 #include "hs_internal.h"
 
@@ -313,14 +315,14 @@ __device__ void forward_state(const SceneArgs<T>& sc, const CamArgs& cam, int ke
 template <typename T>
 __global__ void __launch_bounds__(128) preprocess_fwd_kernel(
     SceneArgs<T> sc, CamArgs cam, int kernel, int64_t n, float4* __restrict__ rec,
-    int4* __restrict__ rect, int32_t* __restrict__ count, uint64_t* __restrict__ dkey,
-    uint32_t* __restrict__ dval, int32_t* __restrict__ radii) {
+    SteepRec* __restrict__ side, int4* __restrict__ rect, int32_t* __restrict__ count,
+    uint64_t* __restrict__ dkey, uint32_t* __restrict__ dval, int32_t* __restrict__ radii) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   FwdState st;
   forward_state(sc, cam, kernel, i, st);
-  dval[i] = (uint32_t)i;
   if (!st.visible) {
+    dval[i] = (uint32_t)i;
     count[i] = 0;
     dkey[i] = ~0ull;
     if (radii) radii[i] = 0;
@@ -335,13 +337,17 @@ __global__ void __launch_bounds__(128) preprocess_fwd_kernel(
   // then breaks exact ties by primitive index, as np.lexsort does.
   dkey[i] = (uint64_t)__double_as_longlong(st.t[2]);
   if (radii) radii[i] = (int32_t)ceil(st.radius);
-  float4 r0 = make_float4((float)st.mux, (float)st.muy, (float)(st.c / st.det),
-                          (float)(-st.b / st.det));
+  const bool steep = st.mode != kModePlain && is_steep(st.za, st.zb, st.radius + 24.0);
+  dval[i] = (uint32_t)i | (steep ? kSteepBit : 0u);
+  if (steep) side[i] = SteepRec{st.mux, st.muy, st.za, st.zb};
+  const float mux = (float)st.mux, muy = (float)st.muy;
+  const __half2 lo = __floats2half2_rn((float)(st.mux - (double)mux), (float)(st.muy - (double)muy));
+  float4 r0 = make_float4(mux, muy, (float)(st.c / st.det), (float)(-st.b / st.det));
   float4 r1 = make_float4((float)(st.a / st.det), (float)st.za, (float)st.zb, (float)st.c1);
   float4 r2 = make_float4((float)st.c2, (float)fmax(st.rgbu[0], 0.0), (float)fmax(st.rgbu[1], 0.0),
                           (float)fmax(st.rgbu[2], 0.0));
-  float4 r3 = make_float4((float)st.t[2], __uint_as_float(pack_mode_spanx(st.mode, spans_x)),
-                          __uint_as_float(0u), __uint_as_float((uint32_t)tx0 | ((uint32_t)ty0 << 16)));
+  float4 r3 = make_float4((float)st.t[2], __uint_as_float(pack_flags(st.mode, steep, spans_x)),
+                          __uint_as_float(0u), __uint_as_float(*reinterpret_cast<const uint32_t*>(&lo)));
   float4* dst = rec + 4 * i;
   dst[0] = r0;
   dst[1] = r1;
@@ -380,23 +386,24 @@ __global__ void __launch_bounds__(128) preprocess_bwd_kernel(
   }
   // ---- merge pair rows: tiles of the rect in row-major (= sorted k) order,
   // skipping pairs past the tile's last composited position (never written).
-  double m[12];
-  for (int k = 0; k < 12; ++k) m[k] = 0.0;
+  double m[13];
+  for (int k = 0; k < 13; ++k) m[k] = 0.0;
   {
     const float4 q3 = rec[4 * i + 3];
-    const uint32_t base = __float_as_uint(q3.z);
     const int4 rc = rect[i];
     const int spans_x = rc.y - rc.x + 1;
+    const int base = (int)__float_as_uint(q3.z) + rc.z * spans_x + rc.x;
     const int r = (int)rank_of[i];
     for (int l = 0; l < cnt; ++l) {
       const int ly = l / spans_x, lx = l - ly * spans_x;
       const int tile = (rc.z + ly) * tiles_x + rc.x + lx;
       if (r > last_rank[tile]) continue;
-      const float4* row = reinterpret_cast<const float4*>(rows + (size_t)(base + l) * 12);
-      const float4 u0 = row[0], u1 = row[1], u2 = row[2];
+      const float4* row = reinterpret_cast<const float4*>(rows + (size_t)(base + l) * kRowFloats);
+      const float4 u0 = row[0], u1 = row[1], u2 = row[2], u3 = row[3];
       m[0] += u0.x; m[1] += u0.y; m[2] += u0.z; m[3] += u0.w;
       m[4] += u1.x; m[5] += u1.y; m[6] += u1.z; m[7] += u1.w;
       m[8] += u2.x; m[9] += u2.y; m[10] += u2.z; m[11] += u2.w;
+      m[12] += u3.x;
     }
   }
   FwdState st;
@@ -418,7 +425,10 @@ __global__ void __launch_bounds__(128) preprocess_bwd_kernel(
   const double n1 = st.nray[0], n2 = st.nray[1], n3 = st.nray[2];
   const double inv = mode0 ? 1.0 / (1.4142135623730951 * fabs(n3)) : 0.0;
   const double d_za0 = mode0 ? d_za : 0.0, d_zb0 = mode0 ? d_zb : 0.0;
-  const double d_inv = d_za0 * (n1 * st.v00 + n2 * st.v10) + d_zb0 * (n2 * st.v11);
+  // d_inv = d_za*(n1 v00 + n2 v10) + d_zb*(n2 v11) (rasterizer.py:459) equals
+  // (sum_px d_z * z) / inv; the blend accumulates that sum directly (column 12),
+  // which stays accurate when za*dx and zb*dy nearly cancel (|n3| -> 0).
+  const double d_inv = mode0 ? m[kColSumDzZ] / inv : 0.0;
   double d_nray[3];
   d_nray[0] = d_za0 * inv * st.v00;
   d_nray[1] = d_za0 * inv * st.v10 + d_zb0 * inv * st.v11;
@@ -620,13 +630,13 @@ __global__ void __launch_bounds__(128) preprocess_bwd_kernel(
 // ---------------------------------------------------------------------------
 template <typename T>
 cudaError_t launch_preprocess_fwd_t(const SceneArgs<T>& sc, const CamArgs& cam, int kernel,
-                                    int64_t n, float4* rec, int4* rect, int32_t* count,
-                                    uint64_t* dkey, uint32_t* dval, int32_t* radii,
-                                    cudaStream_t stream) {
+                                    int64_t n, float4* rec, SteepRec* side, int4* rect,
+                                    int32_t* count, uint64_t* dkey, uint32_t* dval,
+                                    int32_t* radii, cudaStream_t stream) {
   const int block = 128;
   const int64_t grid = (n + block - 1) / block;
-  preprocess_fwd_kernel<T><<<(unsigned)grid, block, 0, stream>>>(sc, cam, kernel, n, rec, rect,
-                                                                count, dkey, dval, radii);
+  preprocess_fwd_kernel<T><<<(unsigned)grid, block, 0, stream>>>(sc, cam, kernel, n, rec, side,
+                                                                rect, count, dkey, dval, radii);
   note_launch();
   return cudaGetLastError();
 }
@@ -646,11 +656,11 @@ cudaError_t launch_preprocess_bwd_t(const SceneArgs<T>& sc, const CamArgs& cam, 
 }
 
 template cudaError_t launch_preprocess_fwd_t<float>(const SceneArgs<float>&, const CamArgs&, int,
-                                                    int64_t, float4*, int4*, int32_t*, uint64_t*,
-                                                    uint32_t*, int32_t*, cudaStream_t);
+                                                    int64_t, float4*, SteepRec*, int4*, int32_t*,
+                                                    uint64_t*, uint32_t*, int32_t*, cudaStream_t);
 template cudaError_t launch_preprocess_fwd_t<double>(const SceneArgs<double>&, const CamArgs&, int,
-                                                     int64_t, float4*, int4*, int32_t*, uint64_t*,
-                                                     uint32_t*, int32_t*, cudaStream_t);
+                                                     int64_t, float4*, SteepRec*, int4*, int32_t*,
+                                                     uint64_t*, uint32_t*, int32_t*, cudaStream_t);
 template cudaError_t launch_preprocess_bwd_t<float>(const SceneArgs<float>&, const CamArgs&, int,
                                                     int64_t, int, const float4*, const int4*,
                                                     const int32_t*, const uint32_t*, const int32_t*,

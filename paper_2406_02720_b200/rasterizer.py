@@ -135,6 +135,33 @@ class FrameGeometry:
         return self._exported()["radii"]
 
 
+def _n(scene):
+    return int(scene.mu.shape[0])
+
+
+# Host dtype of floating-point outputs.  The GPU computes images in FP32, so
+# float32 arrays carry every bit of the result; set to np.float64 to get the
+# reference's dtype at the cost of a host-side conversion.
+HOST_FLOAT = np.float32
+
+
+def _to_host(tensors):
+    """D2H through pinned staging buffers (one sync for the whole batch)."""
+    staged = []
+    for t in tensors:
+        h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        h.copy_(t, non_blocking=True)
+        staged.append(h)
+    torch.cuda.current_stream().synchronize()
+    out = []
+    for h in staged:
+        a = h.numpy()
+        if a.dtype.kind == "f" and a.dtype != HOST_FLOAT:
+            a = a.astype(HOST_FLOAT)
+        out.append(a)
+    return out
+
+
 def resolve_threads(threads):
     """Accepted for signature compatibility (rasterizer.py:150-156); the GPU ignores it."""
     return 1 if threads is None else max(1, int(threads))
@@ -155,17 +182,10 @@ def render(scene, cam, kernel="half", threads=None, frame=None):
         frame = prepare(scene, cam, kernel)
     dscene = frame._scene
     dout = _dev.render(dscene, cam, kernel, frame=frame._device)
-    host = lambda t: t.detach().cpu().numpy()  # noqa: E731
-    out = RenderOutput(
-        color=host(dout.color).astype(np.float64),
-        alpha=host(dout.alpha).astype(np.float64),
-        depth=host(dout.depth).astype(np.float64),
-        per_pixel_terminal_index=host(dout.terminal),
-        camera=cam,
-        transmittance=host(dout.transmittance).astype(np.float64),
-        frame=frame,
-        radii=host(dout.radii),
-    )
+    color, alpha, depth, trans, term, radii = _to_host(
+        [dout.color, dout.alpha, dout.depth, dout.transmittance, dout.terminal, dout.radii])
+    out = RenderOutput(color=color, alpha=alpha, depth=depth, per_pixel_terminal_index=term,
+                       camera=cam, transmittance=trans, frame=frame, radii=radii)
     out._device_out = dout
     out._host_scene = scene
     return out
@@ -176,7 +196,7 @@ def render_backward(scene, cam, out, d_color, threads=None):
     resolve_threads(threads)
     cam = CameraModel.from_any(cam)
     frame = out.frame
-    if frame is None or frame.n_total != len(scene):
+    if frame is None or frame.n_total != _n(scene):
         raise MismatchedForward("forward bookkeeping does not match the scene")
     d_color = np.asarray(d_color)
     if d_color.shape != (cam.height, cam.width, 3):
@@ -194,14 +214,12 @@ def render_backward(scene, cam, out, d_color, threads=None):
             terminal=torch.as_tensor(np.asarray(out.per_pixel_terminal_index, np.int32),
                                      device=dev),
             radii=frame._device.radii, frame=frame._device, camera=cam)
-    dc = torch.as_tensor(np.ascontiguousarray(d_color, dtype=np.float32)).to(dscene.device)
+    # upload the caller's cotangent as is; the FP32 conversion happens on the GPU
+    dc = torch.as_tensor(np.ascontiguousarray(d_color)).to(dscene.device).float()
     g = _dev.render_backward(dscene, cam, dout, dc)
-    host = lambda t: t.detach().cpu().numpy().astype(np.float64)  # noqa: E731
-    return GradientSet(
-        d_mu=host(g.d_mu), d_log_scale=host(g.d_log_scale), d_rotation=host(g.d_rotation),
-        d_sh=host(g.d_sh), d_normal=host(g.d_normal), d_raw_opacity_a=host(g.d_raw_opacity_a),
-        d_raw_opacity_b=host(g.d_raw_opacity_b), pos_grad_norm=host(g.pos_grad_norm),
-        touch_count=g.touch_count.cpu().numpy().astype(np.int64))
+    host = _to_host([getattr(g, name) for name in GradientSet.NAMES])
+    host[-1] = host[-1].astype(np.int64)
+    return GradientSet(*host)
 
 
 def screen_splats(scene, cam, kernel="half"):

@@ -12,8 +12,7 @@ import pytest
 import torch
 
 from conftest import load_golden
-from parity import (GRAD_GROUPS, PACKED_RTOL, assert_grads, assert_images, grad_report,
-                    image_report)
+from parity import GRAD_GROUPS, PACKED_RTOL, assert_grads, assert_images
 from paper_2406_02720_b200 import device, scenes
 from paper_2406_02720_b200.geometry import CameraModel, Scene
 
@@ -111,9 +110,7 @@ def test_full_size_summary_parity(cuda, name):
     sample_ref = {"color": gold["px_color"], "alpha": gold["px_alpha"], "depth": gold["px_depth"],
                   "transmittance": gold["px_transmittance"], "terminal": gold["px_terminal"]}
     assert_images(sample_got, sample_ref)
-    rep = image_report({"terminal": got["terminal"]},
-                       {"terminal": got["terminal"]})  # shape sanity
-    assert rep["pixels"] == got["terminal"].size
+    assert int(got["terminal"].astype(np.int64).sum()) > 0
     if d_color is not None:
         rows = gold["grad_rows"]
         for g in GRAD_GROUPS:
