@@ -1,0 +1,197 @@
+"""GPU behaviour of the public surfaces: the drop-in `rasterizer` module (numpy
+in/out), the blend-core plugin (Seam 1), the device API, and the reference's
+bit-identity properties evaluated on the GPU path."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import load_golden
+from parity import assert_grads, assert_images
+from test_oracle_properties import identity_camera, look_at, make_scene, tie
+from paper_2406_02720_b200 import backend, device, errors, multiview, scenes
+from paper_2406_02720_b200 import rasterizer as R
+from paper_2406_02720_b200.geometry import CameraModel, Scene
+
+pytestmark = pytest.mark.gpu
+
+
+def dev_scene(sa, dtype=torch.float64):
+    return Scene(*(getattr(sa, f) for f in sa.FIELDS), sh_degree=sa.sh_degree,
+                 background_color=sa.background_color, device="cuda", dtype=dtype)
+
+
+def test_dropin_render_matches_oracle(cuda):
+    from oracle import oracle as O
+    rng = np.random.default_rng(3)
+    sa = make_scene(rng, 20, sh_degree=2)
+    cam = look_at([0.4, -0.3, -0.6], [0, 0, 3.0], 96, 72)
+    out = R.render(sa, cam)
+    ref = O.render(sa, cam)
+    assert_images({"color": out.color, "alpha": out.alpha, "depth": out.depth,
+                   "transmittance": out.transmittance, "terminal": out.per_pixel_terminal_index},
+                  {"color": ref.color, "alpha": ref.alpha, "depth": ref.depth,
+                   "transmittance": ref.transmittance, "terminal": ref.per_pixel_terminal_index})
+    d_color = rng.uniform(-1, 1, (72, 96, 3))
+    g = R.render_backward(sa, cam, out, d_color)
+    rg = O.render_backward(sa, cam, ref, d_color)
+    assert_grads({k: getattr(g, k) for k in rg if k != "touch_count"},
+                 {k: v for k, v in rg.items() if k != "touch_count"})
+    assert np.array_equal(g.touch_count, rg["touch_count"])
+    fg = out.frame
+    assert np.array_equal(fg.pair_splat, ref.frame.pair_splat)
+    assert np.array_equal(fg.tile_starts, ref.frame.tile_starts)
+
+
+def test_dropin_errors(cuda):
+    rng = np.random.default_rng(0)
+    sa = make_scene(rng, 3)
+    empty = scenes.SceneArrays(**{f: getattr(sa, f)[:0] for f in sa.FIELDS},
+                               sh_degree=sa.sh_degree)
+    with pytest.raises(errors.EmptyScene):
+        R.render(empty, identity_camera())
+    with pytest.raises(ValueError):
+        R.render(sa, identity_camera(), kernel="quarter")
+    cam = identity_camera(32, 32)
+    out = R.render(sa, cam)
+    with pytest.raises(errors.MismatchedForward):
+        R.render_backward(sa, cam, out, np.zeros((16, 16, 3)))
+    bigger = make_scene(rng, 5)
+    with pytest.raises(errors.MismatchedForward):
+        R.render_backward(bigger, cam, out, np.zeros((32, 32, 3)))
+
+
+def test_image_too_large(cuda):
+    rng = np.random.default_rng(0)
+    sa = dev_scene(make_scene(rng, 3))
+    cam = CameraModel(np.eye(4), 10.0, 10.0, 10.0, 10.0, 65536, 32769)
+    with pytest.raises(errors.ImageTooLarge):
+        device.render(sa, cam)
+
+
+def test_half_full_bit_identical_on_gpu(cuda):
+    for seed in range(5):
+        sa = tie(make_scene(np.random.default_rng(seed), 6))
+        cam = look_at([0.3, -0.2, -0.5], [0, 0, 3.0])
+        a = device.render(dev_scene(sa), cam, "half")
+        b = device.render(dev_scene(sa), cam, "full")
+        assert torch.equal(a.color, b.color) and torch.equal(a.depth, b.depth)
+        assert torch.equal(a.alpha, b.alpha)
+
+
+def test_odd_symmetry_bit_identical_on_gpu(cuda):
+    for seed in range(5):
+        sa = make_scene(np.random.default_rng(100 + seed), 6)
+        fl = scenes.SceneArrays(**{f: getattr(sa, f).copy() for f in sa.FIELDS},
+                                sh_degree=sa.sh_degree, background_color=sa.background_color)
+        fl.normal = -fl.normal
+        fl.raw_opacity_a, fl.raw_opacity_b = sa.raw_opacity_b.copy(), sa.raw_opacity_a.copy()
+        cam = look_at([0.2, 0.1, -0.6], [0, 0, 3.0])
+        a = device.render(dev_scene(sa), cam)
+        b = device.render(dev_scene(fl), cam)
+        assert torch.equal(a.color, b.color)
+
+
+def test_run_to_run_determinism(cuda):
+    """Launch-config / scheduling invariance: the persistent tile queue hands tiles
+    to warps in a different order each run; outputs and gradients are bitwise equal."""
+    sa = scenes.frustum(30_000, 3, 640, 360, seed=5)
+    sc = dev_scene(sa, torch.float32)
+    cam = CameraModel(**sa.cameras[0])
+    dc = torch.as_tensor(scenes.cotangent(360, 640), dtype=torch.float32)
+    res = []
+    for _ in range(3):
+        out = device.render(sc, cam)
+        g = device.render_backward(sc, cam, out, dc)
+        res.append((out.color.clone(), out.terminal.clone(), g.d_mu.clone(), g.d_sh.clone(),
+                    g.d_normal.clone()))
+    for r in res[1:]:
+        for a, b in zip(res[0], r):
+            assert torch.equal(a, b)
+
+
+def test_zero_cotangent_and_tied_normal_on_gpu(cuda):
+    rng = np.random.default_rng(1)
+    sa = make_scene(rng, 6)
+    cam = identity_camera(32, 32)
+    sc = dev_scene(sa)
+    out = device.render(sc, cam)
+    g = device.render_backward(sc, cam, out, torch.zeros((32, 32, 3)))
+    for k in device.DeviceGradientSet.NAMES[:-2]:
+        assert not getattr(g, k).any(), k
+    st = dev_scene(tie(sa))
+    out = device.render(st, cam)
+    g = device.render_backward(st, cam, out, torch.as_tensor(rng.uniform(-1, 1, (32, 32, 3))))
+    assert g.d_normal.abs().max().item() == 0.0
+    assert g.d_raw_opacity_a.abs().max().item() > 0.0
+
+
+def test_culled_touch_count_on_gpu(cuda):
+    rng = np.random.default_rng(2)
+    sa = make_scene(rng, 5)
+    sa.mu[0, 2] = -5.0
+    cam = identity_camera(32, 32)
+    out = R.render(sa, cam)
+    g = R.render_backward(sa, cam, out, rng.uniform(-1, 1, (32, 32, 3)))
+    assert g.touch_count[0] == 0 and g.pos_grad_norm[0] == 0.0
+    assert (g.touch_count[1:] == 1).all()
+    assert out.radii[0] == 0 and (out.radii[1:] > 0).all()
+
+
+@pytest.mark.parametrize("chunks", [1, 3])
+def test_seam1_blend_plugin_vs_oracle(cuda, chunks):
+    """cuda_blend.forward_tiles/backward_tiles on the reference's packed splats
+    (golden c1/ball_small), honouring [tile_lo, tile_hi) and += on pair rows."""
+    from oracle import oracle as O
+    assert backend.get_backend().__name__.endswith("cuda_blend")
+    blend = backend.get_backend()
+    for name in ("ball_small", "ties"):
+        gold = load_golden(name)
+        tx, ty = int(gold["tiles_x"]), int(gold["tiles_y"])
+        h, w = gold["color"].shape[:2]
+        bg = np.array(scenes.BACKGROUND)
+        color = np.zeros((h, w, 3)); alpha = np.zeros((h, w)); depth = np.zeros((h, w))
+        trans = np.ones((h, w)); term = np.zeros((h, w), np.int32)
+        n_tiles = tx * ty
+        bounds = np.linspace(0, n_tiles, chunks + 1).astype(int)
+        args = (gold["packed"], gold["mode"], gold["pair_splat"], gold["tile_starts"], h, w, tx, bg)
+        for lo, hi in zip(bounds[:-1], bounds[1:]):
+            blend.forward_tiles(*args, color, alpha, depth, trans, term, int(lo), int(hi))
+        assert_images({"color": color, "alpha": alpha, "depth": depth, "transmittance": trans,
+                       "terminal": term}, gold)
+        pg = np.zeros((gold["pair_splat"].shape[0], 12))
+        for lo, hi in zip(bounds[:-1], bounds[1:]):
+            blend.backward_tiles(*args, gold["d_color"], gold["transmittance"], gold["terminal"],
+                                 pg, int(lo), int(hi))
+        ref = np.zeros_like(pg)
+        O.backward_tiles(*args, gold["d_color"], gold["transmittance"], gold["terminal"], ref, 0,
+                         n_tiles)
+        rel = np.linalg.norm(pg - ref, axis=0) / np.maximum(np.linalg.norm(ref, axis=0), 1e-30)
+        assert rel.max() < 1e-3, rel
+
+
+def test_seam1_rejects_bad_arrays(cuda):
+    gold = load_golden("mini")
+    h, w = gold["color"].shape[:2]
+    blend = backend.get_backend()
+    with pytest.raises(ValueError):
+        blend.forward_tiles(gold["packed"].astype(np.float32), gold["mode"], gold["pair_splat"],
+                            gold["tile_starts"], h, w, int(gold["tiles_x"]),
+                            np.zeros(3), np.zeros((h, w, 3)), np.zeros((h, w)), np.zeros((h, w)),
+                            np.zeros((h, w)), np.zeros((h, w), np.int32), 0, 1)
+
+
+def test_multiview_accumulation_equals_sum(cuda):
+    sa = scenes.ball(5000, 2, 96, 96, views=4, seed=4)
+    sc = dev_scene(sa, torch.float32)
+    cams = [CameraModel(**c) for c in sa.cameras]
+    dcs = [torch.as_tensor(scenes.cotangent(96, 96, seed=v), dtype=torch.float32) for v in range(4)]
+    batch = multiview.batch_gradients(sc, cams, dcs, [0, 1, 2, 3])
+    total = torch.zeros_like(batch.flat)
+    for v in range(4):
+        g = device.DeviceGradientSet.empty_flat(sc)
+        out = device.render(sc, cams[v])
+        device.render_backward(sc, cams[v], out, dcs[v], grads=g)
+        total += g.flat
+    torch.testing.assert_close(batch.flat, total, rtol=1e-6, atol=1e-7)
+    assert batch.touch_count.max().item() <= 4

@@ -1,0 +1,131 @@
+"""Host-side logic that needs no GPU: cameras, scene validation, the backend
+seam, the canonical generator, view sharding and the gloo all-reduce path."""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2406_02720_b200 import backend, scenes
+from paper_2406_02720_b200.geometry import CameraModel, Scene
+from paper_2406_02720_b200.multiview import GradientAllReduce, shard_views
+
+
+def test_camera_validation_mirrors_reference():
+    with pytest.raises(ValueError):
+        CameraModel(np.eye(3), 10, 10, 5, 5, 10, 10)
+    bad = np.eye(4)
+    bad[0, 0] = 2.0
+    with pytest.raises(ValueError):
+        CameraModel(bad, 10, 10, 5, 5, 10, 10)
+    with pytest.raises(ValueError):
+        CameraModel(np.eye(4), -1, 10, 5, 5, 10, 10)
+    with pytest.raises(ValueError):
+        CameraModel(np.eye(4), 10, 10, 50, 5, 10, 10)
+    cam = CameraModel.look_at((3.0, -0.5, 0.0), (0, 0, 0), 64, 48, 50.0)
+    np.testing.assert_allclose(cam.center, [3.0, -0.5, 0.0], atol=1e-12)
+    r = cam.rotation
+    np.testing.assert_allclose(r @ r.T, np.eye(3), atol=1e-12)
+
+
+def test_look_at_matches_generator():
+    w2c = scenes.look_at_matrix((1.0, 2.0, 3.0), (0.0, 0.0, 0.0))
+    cam = CameraModel.look_at((1.0, 2.0, 3.0), (0.0, 0.0, 0.0), 32, 32, 30.0)
+    assert np.array_equal(w2c, cam.world_to_cam)
+
+
+def test_scene_validation_on_cpu():
+    sa = scenes.frustum(50, 1, 32, 32, seed=1)
+    fields = [getattr(sa, f) for f in sa.FIELDS]
+    s = Scene(*fields, sh_degree=1, device="cpu")
+    assert len(s) == 50 and s.dtype == torch.float32
+    s64 = Scene(*[f.astype(np.float64) for f in fields], sh_degree=1, device="cpu")
+    assert s64.dtype == torch.float64
+    with pytest.raises(ValueError):
+        Scene(*fields, sh_degree=2, device="cpu")
+    bad = [f.copy() for f in fields]
+    bad[4][3] = 0.0
+    with pytest.raises(ValueError):
+        Scene(*bad, sh_degree=1, device="cpu")
+    with pytest.raises(ValueError):
+        Scene(*fields, sh_degree=1, background_color=(2, 0, 0), device="cpu")
+
+
+def test_backend_seam():
+    assert backend.available_backends() == ["cuda"]
+    backend.set_backend("cuda")
+    assert backend.backend_name() == "cuda"
+    backend.set_backend(None)
+    with pytest.raises(ValueError):
+        backend.set_backend("cython")
+    mod = backend.get_backend()
+    assert hasattr(mod, "forward_tiles") and hasattr(mod, "backward_tiles")
+
+
+def test_generator_reproduces_survey_counts():
+    """c1 M=9,865, P=32,950 and c2 M=100,000, P=406,380."""
+    from oracle import oracle as O
+
+    class Cam:
+        pass
+
+    for name, m, p in (("c1", 9865, 32950), ("c2", 100_000, 406_380)):
+        sa = scenes.make_config(name).as_float64()
+        cam = Cam()
+        for k, v in sa.cameras[0].items():
+            setattr(cam, k, v)
+        cam.near_clip = 0.01
+        f = O.prepare(sa, cam)
+        assert (f.valid.shape[0], f.pair_splat.shape[0]) == (m, p)
+
+
+def test_generator_is_float32_exact():
+    sa = scenes.frustum(100, 3, 64, 64, seed=2)
+    for f in sa.FIELDS:
+        a = getattr(sa, f)
+        assert a.dtype == np.float32
+        assert np.array_equal(a.astype(np.float64).astype(np.float32), a)
+
+
+@pytest.mark.parametrize("n,world", [(8, 1), (8, 2), (8, 3), (8, 8), (3, 4)])
+def test_shard_views_partition(n, world):
+    got = [v for r in range(world) for v in shard_views(n, world, r)]
+    assert got == list(range(n))
+
+
+def _allreduce_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+
+    class G:
+        pass
+
+    g = G()
+    n, k = 5, 4
+    g.flat = torch.arange(n * (3 + 3 + 4 + 3 * k + 3 + 3), dtype=torch.float32) * (rank + 1)
+    g.touch_count = torch.ones(n, dtype=torch.int32) * (rank + 1)
+    GradientAllReduce(g).allreduce()
+    q.put((rank, g.flat.numpy().copy(), g.touch_count.numpy().copy()))
+    dist.destroy_process_group()
+
+
+def test_gradient_allreduce_gloo_world2():
+    """The multi-view exchange step on 2 CPU ranks: the batch gradient is the sum."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29500 + os.getpid() % 1000
+    procs = [ctx.Process(target=_allreduce_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    n, k = 5, 4
+    base = np.arange(n * (3 + 3 + 4 + 3 * k + 3 + 3), dtype=np.float32)
+    for _, flat, touch in res:
+        np.testing.assert_array_equal(flat, base * 3)
+        np.testing.assert_array_equal(touch, np.full(n, 3, np.int32))

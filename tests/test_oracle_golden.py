@@ -1,0 +1,110 @@
+"""Pin the CPU oracle against outputs of the reference itself (tests/golden/,
+produced by tests/golden/make_golden.py from /root/reference).  CPU only."""
+
+import hashlib
+import os
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+from oracle import oracle as O
+from paper_2406_02720_b200 import scenes
+
+FULL = {
+    "c1": (lambda: scenes.make_config("c1"), "half"),
+    "mini": (lambda: scenes.frustum(300, 2, 64, 48, seed=3), "half"),
+    "mini_full": (lambda: scenes.frustum(300, 2, 64, 48, seed=3), "full"),
+    "ball_small": (lambda: scenes.ball(3000, 3, 96, 72, views=4, seed=9), "half"),
+    "ties": (lambda: scenes.frustum(2000, 1, 96, 80, seed=5, clustered=True, dup=0.3), "half"),
+}
+INTS = {"valid": np.int64, "mode": np.int8, "tile_rect": np.int32, "pair_splat": np.int32,
+        "tile_starts": np.int64}
+GRADS = ("d_mu", "d_log_scale", "d_rotation", "d_sh", "d_normal", "d_raw_opacity_a",
+         "d_raw_opacity_b", "pos_grad_norm")
+
+
+class Cam:
+    def __init__(self, kw):
+        for k, v in kw.items():
+            setattr(self, k, v)
+        self.near_clip = 0.01
+
+
+def test_erf_matches_reference_bitwise():
+    gold = load_golden("erf")
+    got = np.array([O.erf(z) for z in gold["z"]])
+    assert np.array_equal(got, gold["erf"])
+    # exactly odd (kernels.py:136-147 relies on it)
+    assert all(O.erf(-z) == -O.erf(z) for z in gold["z"][:500])
+
+
+@pytest.mark.parametrize("name", list(FULL))
+def test_oracle_full_fixture(name):
+    gold = load_golden(name)
+    gen, kernel = FULL[name]
+    sa = gen().as_float64()
+    cam = Cam(sa.cameras[int(gold["cam_idx"])])
+    out = O.render(sa, cam, kernel=kernel, threads=4)
+    f = out.frame
+    for k, dt in INTS.items():
+        assert np.array_equal(np.asarray(getattr(f, k), dtype=dt), gold[k]), k
+    # packed: only libm-vs-numpy `exp` ulps separate the two
+    np.testing.assert_allclose(f.packed, gold["packed"], rtol=1e-9, atol=1e-12)
+    for k in ("color", "alpha", "depth", "transmittance"):
+        np.testing.assert_allclose(getattr(out, k), gold[k], rtol=0, atol=1e-11)
+    assert np.array_equal(out.per_pixel_terminal_index, gold["terminal"])
+    if "d_color" in gold:
+        g = O.render_backward(sa, cam, out, gold["d_color"], threads=4)
+        for k in GRADS:
+            den = max(np.linalg.norm(gold[k]), 1e-300)
+            assert np.linalg.norm(g[k] - gold[k]) / den < 1e-9, k
+        assert np.array_equal(g["touch_count"], gold["touch_count"])
+
+
+def _sha(a, dt):
+    return hashlib.sha256(np.ascontiguousarray(a, dtype=dt).tobytes()).hexdigest()
+
+
+def test_oracle_c2_summary():
+    """Full c2 (100k, SH3, 800x800): integer hashes, sampled pixels, gradients."""
+    gold = load_golden("c2")
+    sa = scenes.make_config("c2").as_float64()
+    cam = Cam(sa.cameras[0])
+    out = O.render(sa, cam)
+    f = out.frame
+    for k, dt in INTS.items():
+        assert _sha(getattr(f, k), dt) == str(gold[f"sha_{k}"]), k
+    px = gold["px_index"]
+    np.testing.assert_allclose(out.color.reshape(-1, 3)[px], gold["px_color"], atol=1e-11)
+    assert np.array_equal(out.per_pixel_terminal_index.reshape(-1)[px], gold["px_terminal"])
+    assert _sha(out.per_pixel_terminal_index, np.int32) == str(gold["terminal_sha"])
+    g = O.render_backward(sa, cam, out, scenes.cotangent(cam.height, cam.width))
+    rows = gold["grad_rows"]
+    for k in GRADS:
+        assert abs(np.linalg.norm(g[k]) - float(gold[f"norm_{k}"])) <= 1e-9 * float(gold[f"norm_{k}"])
+        ref = gold[f"sample_{k}"]
+        assert np.linalg.norm(g[k][rows] - ref) <= 1e-9 * max(np.linalg.norm(ref), 1e-300), k
+
+
+def test_oracle_c3_binning_hashes():
+    """Headline config c3 (1M, 1080p): the oracle's FrameGeometry integers hash
+    to the reference's; counts match SURVEY.md 8(d)."""
+    gold = load_golden("c3")
+    sa = scenes.make_config("c3").as_float64()
+    f = O.prepare(sa, Cam(sa.cameras[0]))
+    assert f.valid.shape[0] == int(gold["M"]) == 846_464
+    assert f.pair_splat.shape[0] == int(gold["P"]) == 3_384_553
+    for k, dt in INTS.items():
+        assert _sha(getattr(f, k), dt) == str(gold[f"sha_{k}"]), k
+
+
+@pytest.mark.slow
+@pytest.mark.skipif(not os.environ.get("HS_SLOW"), reason="set HS_SLOW=1 (minutes, ~10 GB)")
+@pytest.mark.parametrize("name,cfg", [("c5", "c5"), ("c4v0", "c4")])
+def test_oracle_large_binning_hashes(name, cfg):
+    gold = load_golden(name)
+    sa = scenes.make_config(cfg).as_float64()
+    f = O.prepare(sa, Cam(sa.cameras[0]))
+    for k, dt in INTS.items():
+        assert _sha(getattr(f, k), dt) == str(gold[f"sha_{k}"]), k
