@@ -231,16 +231,17 @@ def main():
     grads = device.DeviceGradientSet.empty_flat(scene)
     reducer = GradientAllReduce(grads) if world > 1 else None
     timer = device.StageTimer()
+    rast = device.Rasterizer("cuda", slots=1)
 
     def step(t=None):
-        out = device.render(scene, cam, timer=t)
-        device.render_backward(scene, cam, out, d_color, grads=grads, timer=t)
+        out = rast.render(scene, cam, timer=t)
+        rast.render_backward(scene, cam, out, d_color, grads=grads, timer=t)
         if reducer is not None:
             reducer.allreduce()
         return out
 
     def fwd_step():
-        return device.render(scene, cam)
+        return rast.render(scene, cam)
 
     def barrier():
         if world > 1:

@@ -127,33 +127,33 @@ __device__ __forceinline__ void fwd_splat(const float4 (&q)[4], const SteepRec& 
   const SplatLane s = splat_lane<STEEP>(q, side, px, py0);
   const float c1 = q[1].w, c2 = q[2].x;
   const float cr = q[2].y, cg = q[2].z, cb = q[2].w, z = q[3].x;
+  // Branch-free over the 8 pixels (selects, no per-pixel basic blocks) so the
+  // compiler interleaves the eight independent chains; dead pixels compute and
+  // discard.
 #pragma unroll
   for (int i = 0; i < kPx; ++i) {
-    if (alive & (1u << i)) {
-      const float dy = s.dy0 + 2.0f * i;
-      const float g = ex2_approx(fmaf(fmaf(s.C, dy, s.Bx), dy, s.P0));
-      float w;
-      if (MODE == kModeErf) {
-        w = fmaf(c2, erf32(erf_arg<STEEP>(s, dy, i)), c1) * g;
-      } else if (MODE == kModeSign) {
-        w = fmaf(c2, sign32(erf_arg<STEEP>(s, dy, i)), c1) * g;
-      } else {
-        w = c1 * g;
-      }
-      w = fminf(w, kWeightClamp);
-      const float tn = T[i] * (1.0f - w);
-      if (tn < kTerminationT) {
-        alive &= ~(1u << i);
-      } else {
-        const float wt = w * T[i];
-        ar[i] = fmaf(wt, cr, ar[i]);
-        ag[i] = fmaf(wt, cg, ag[i]);
-        ab[i] = fmaf(wt, cb, ab[i]);
-        ad[i] = fmaf(wt, z, ad[i]);
-        cnt[i] += 1;
-        T[i] = tn;
-      }
+    const float dy = s.dy0 + 2.0f * i;
+    const float g = ex2_approx(fmaf(fmaf(s.C, dy, s.Bx), dy, s.P0));
+    float w;
+    if (MODE == kModeErf) {
+      w = fmaf(c2, erf32(erf_arg<STEEP>(s, dy, i)), c1) * g;
+    } else if (MODE == kModeSign) {
+      w = fmaf(c2, sign32(erf_arg<STEEP>(s, dy, i)), c1) * g;
+    } else {
+      w = c1 * g;
     }
+    w = fminf(w, kWeightClamp);
+    const float tn = T[i] * (1.0f - w);
+    // the pixel terminates *before* compositing this splat (_blend_cy.pyx:165-169)
+    const bool commit = ((alive >> i) & 1u) && !(tn < kTerminationT);
+    alive &= commit ? 0xffffffffu : ~(1u << i);
+    const float wt = commit ? w * T[i] : 0.0f;
+    ar[i] = fmaf(wt, cr, ar[i]);
+    ag[i] = fmaf(wt, cg, ag[i]);
+    ab[i] = fmaf(wt, cb, ab[i]);
+    ad[i] = fmaf(wt, z, ad[i]);
+    cnt[i] += commit ? 1 : 0;
+    T[i] = commit ? tn : T[i];
   }
 }
 
@@ -255,50 +255,50 @@ __device__ __forceinline__ void bwd_splat(const float4 (&q)[4], const SteepRec& 
   const float c1 = q[1].w, c2 = q[2].x;
   const float cr = q[2].y, cg = q[2].z, cb = q[2].w;
   const float c2k = c2 * (2.0f * kInvSqrtPi);
+  // Branch-free over the 8 pixels: inactive pixels (pos >= terminal count)
+  // compute and contribute exact zeros, so the eight chains interleave.
 #pragma unroll
   for (int i = 0; i < kPx; ++i) {
-    if (pos < cnt[i]) {
-      const float dy = s.dy0 + 2.0f * i;
-      const float gg = ex2_approx(fmaf(fmaf(s.C, dy, s.Bx), dy, s.P0));
-      float e = 0.f, zz = 0.f, u;
-      if (MODE == kModeErf) {
-        zz = erf_arg<STEEP>(s, dy, i);
-        e = erf32(zz);
-        u = fmaf(c2, e, c1);
-      } else if (MODE == kModeSign) {
-        e = sign32(erf_arg<STEEP>(s, dy, i));
-        u = fmaf(c2, e, c1);
-      } else {
-        u = c1;
-      }
-      const float w_raw = u * gg;
-      const float w = fminf(w_raw, kWeightClamp);
-      const float inv = __frcp_rn(1.0f - w);
-      const float Tp = T[i] * inv;
-      const float wt = w * Tp;
-      const float dcr = fmaf(dr[i], cr, fmaf(dg[i], cg, db[i] * cb));
-      a.r = fmaf(dr[i], wt, a.r);
-      a.g = fmaf(dg[i], wt, a.g);
-      a.b = fmaf(db[i], wt, a.b);
-      if (w_raw <= kWeightClamp) {
-        const float d_w = fmaf(Tp, dcr, -inv * D[i]);
-        const float dwg = d_w * gg;
-        const float d_pow = dwg * u;
-        a.s0 += d_pow;
-        a.s1 = fmaf(d_pow, dy, a.s1);
-        a.s2 = fmaf(d_pow * dy, dy, a.s2);
-        a.c1 += dwg;
-        a.c2 = fmaf(dwg, e, a.c2);
-        if (MODE == kModeErf) {
-          const float d_z = dwg * c2k * ex2_approx(-(zz * zz) * kLog2e);
-          a.q0 += d_z;
-          a.q1 = fmaf(d_z, dy, a.q1);
-          a.qz = fmaf(d_z, zz, a.qz);
-        }
-      }
-      D[i] = fmaf(wt, dcr, D[i]);
-      T[i] = Tp;
+    const bool active = pos < cnt[i];
+    const float dy = s.dy0 + 2.0f * i;
+    const float gg = ex2_approx(fmaf(fmaf(s.C, dy, s.Bx), dy, s.P0));
+    float e = 0.f, zz = 0.f, u;
+    if (MODE == kModeErf) {
+      zz = erf_arg<STEEP>(s, dy, i);
+      e = erf32(zz);
+      u = fmaf(c2, e, c1);
+    } else if (MODE == kModeSign) {
+      e = sign32(erf_arg<STEEP>(s, dy, i));
+      u = fmaf(c2, e, c1);
+    } else {
+      u = c1;
     }
+    const float w_raw = u * gg;
+    const float w = fminf(w_raw, kWeightClamp);
+    const float inv = rcp_approx(1.0f - w);  // 1 - w >= 0.01
+    const float Tp = T[i] * inv;
+    const float wt = active ? w * Tp : 0.0f;
+    const float dcr = fmaf(dr[i], cr, fmaf(dg[i], cg, db[i] * cb));
+    a.r = fmaf(dr[i], wt, a.r);
+    a.g = fmaf(dg[i], wt, a.g);
+    a.b = fmaf(db[i], wt, a.b);
+    // gradient gating on the unclamped weight (_blend_cy.pyx:309)
+    const float d_w = (active && w_raw <= kWeightClamp) ? fmaf(Tp, dcr, -inv * D[i]) : 0.0f;
+    const float dwg = d_w * gg;
+    const float d_pow = dwg * u;
+    a.s0 += d_pow;
+    a.s1 = fmaf(d_pow, dy, a.s1);
+    a.s2 = fmaf(d_pow * dy, dy, a.s2);
+    a.c1 += dwg;
+    a.c2 = fmaf(dwg, e, a.c2);
+    if (MODE == kModeErf) {
+      const float d_z = dwg * c2k * ex2_approx(-(zz * zz) * kLog2e);
+      a.q0 += d_z;
+      a.q1 = fmaf(d_z, dy, a.q1);
+      a.qz = fmaf(d_z, zz, a.qz);
+    }
+    D[i] = fmaf(wt, dcr, D[i]);
+    T[i] = active ? Tp : T[i];
   }
 }
 

@@ -69,6 +69,12 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // Branch-free FP32 erf: erf(z) = sign(z) * (1 - 2^Q(|z|)), Q(x) = x*R(x) with
 // R a degree-8 minimax fit of log2(erfc(x))/x on [0, 3.92] (erfc(3.92) is
 // below half an ulp of 1.0f).  Max abs error 8.4e-8 including FP32 rounding

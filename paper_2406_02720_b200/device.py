@@ -66,10 +66,32 @@ def scene_struct(scene):
     return s
 
 
+class Workspace:
+    """Persistent device buffers for one in-flight view: the frame and binning
+    workspaces, the image outputs and radii.  Reused across calls (grown when a
+    larger scene/image/pair count needs it), so a steady training or benchmark
+    loop performs no device allocation at all."""
+
+    def __init__(self, device="cuda"):
+        self.device = torch.device(device)
+        self._bufs = {}
+
+    def tensor(self, name, shape, dtype):
+        t = self._bufs.get(name)
+        numel = int(np.prod(shape)) if len(shape) else 1
+        if t is None or t.dtype != dtype or t.numel() < numel:
+            t = torch.empty(numel, dtype=dtype, device=self.device)
+            self._bufs[name] = t
+        return t[:numel].view(shape)
+
+    def bytes(self, name, nbytes):
+        return self.tensor(name, (nbytes,), torch.uint8)
+
+
 class DeviceFrame:
     """One view's binned splats (the device counterpart of FrameGeometry)."""
 
-    def __init__(self, scene, cam, kernel):
+    def __init__(self, scene, cam, kernel, ws=None):
         lib = _native.load()
         self.lib = lib
         self.kernel = kernel
@@ -79,12 +101,17 @@ class DeviceFrame:
         _native.check(lib.hs_frame_init(ctypes.byref(self.st), len(scene), cam.width,
                                         cam.height, kcode), "hs_frame_init")
         dev = scene.device
+        self.ws = ws
         nbytes = lib.hs_frame_workspace_size(len(scene), cam.width, cam.height)
-        self.frame_ws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+        if ws is not None:
+            self.frame_ws = ws.bytes("frame_ws", nbytes)
+            self.radii = ws.tensor("radii", (len(scene),), torch.int32)
+        else:
+            self.frame_ws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+            self.radii = torch.empty(len(scene), dtype=torch.int32, device=dev)
         self.st.frame_ws = self.frame_ws.data_ptr()
         self.st.frame_ws_bytes = nbytes
         self.bin_ws = None
-        self.radii = torch.empty(len(scene), dtype=torch.int32, device=dev)
         self.device = dev
 
     @property
@@ -107,7 +134,9 @@ class DeviceFrame:
         lib = self.lib
         nbytes = lib.hs_binning_workspace_size(self.st.n, self.st.num_pairs, self.st.width,
                                                self.st.height)
-        if self.bin_ws is None or self.bin_ws.numel() < nbytes:
+        if self.ws is not None:
+            self.bin_ws = self.ws.bytes("bin_ws", nbytes)
+        elif self.bin_ws is None or self.bin_ws.numel() < nbytes:
             self.bin_ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
         self.st.bin_ws = self.bin_ws.data_ptr()
         self.st.bin_ws_bytes = self.bin_ws.numel()
@@ -147,13 +176,13 @@ def _validate(scene, cam, kernel):
         raise ValueError("kernel must be 'half' or 'full'")
 
 
-def prepare(scene, cam, kernel="half", timer=None):
+def prepare(scene, cam, kernel="half", timer=None, ws=None):
     """Project + bin one view on the GPU (rasterizer.py:159-341)."""
     timer = timer or _NO_TIMER
     scene = Scene.from_any(scene)
     cam = CameraModel.from_any(cam)
     _validate(scene, cam, kernel)
-    frame = DeviceFrame(scene, cam, kernel)
+    frame = DeviceFrame(scene, cam, kernel, ws)
     lib = frame.lib
     s = _stream()
     sc = scene_struct(scene)
@@ -228,15 +257,25 @@ class _NoTimer:
 _NO_TIMER = _NoTimer()
 
 
-def render(scene, cam, kernel="half", frame=None, out=None, timer=None):
-    """Render one view (rasterizer.py:351-383); outputs stay on the device."""
+def render(scene, cam, kernel="half", frame=None, out=None, timer=None, ws=None):
+    """Render one view (rasterizer.py:351-383); outputs stay on the device.
+
+    With a Workspace `ws`, every buffer (frame, binning, outputs) is reused."""
     timer = timer or _NO_TIMER
     scene = Scene.from_any(scene)
     cam = CameraModel.from_any(cam)
     if frame is None:
-        frame = prepare(scene, cam, kernel, timer=timer)
+        frame = prepare(scene, cam, kernel, timer=timer, ws=ws)
     h, w = cam.height, cam.width
     dev = scene.device
+    if out is None and ws is not None:
+        out = DeviceRenderOutput(
+            color=ws.tensor("color", (h, w, 3), torch.float32),
+            alpha=ws.tensor("alpha", (h, w), torch.float32),
+            depth=ws.tensor("depth", (h, w), torch.float32),
+            transmittance=ws.tensor("transmittance", (h, w), torch.float32),
+            terminal=ws.tensor("terminal", (h, w), torch.int32),
+            radii=frame.radii, frame=frame, camera=cam)
     if out is None:
         out = DeviceRenderOutput(
             color=torch.empty((h, w, 3), dtype=torch.float32, device=dev),
@@ -310,6 +349,25 @@ class DeviceGradientSet:
 
     def flat_views(self):
         return [getattr(self, name) for name in self.NAMES]
+
+
+class Rasterizer:
+    """Allocation-free rendering loop: `slots` persistent workspaces used round
+    robin.  An output stays valid until its slot is reused `slots` renders later
+    (slots=1 suits render -> render_backward -> next render)."""
+
+    def __init__(self, device="cuda", slots=1, kernel="half"):
+        self.slots = [Workspace(device) for _ in range(slots)]
+        self.next = 0
+        self.kernel = kernel
+
+    def render(self, scene, cam, timer=None):
+        ws = self.slots[self.next]
+        self.next = (self.next + 1) % len(self.slots)
+        return render(scene, cam, self.kernel, timer=timer, ws=ws)
+
+    def render_backward(self, scene, cam, out, d_color, grads=None, timer=None):
+        return render_backward(scene, cam, out, d_color, grads=grads, timer=timer)
 
 
 def render_backward(scene, cam, out, d_color, grads=None, timer=None):
