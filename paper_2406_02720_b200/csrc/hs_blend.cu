@@ -119,11 +119,15 @@ __device__ __forceinline__ float erf_arg(const SplatLane& s, float dy, int i) {
 
 // ---------------------------------------------------------------------------
 // K5 forward
+// Live pixels hold T > 0.  A pixel that terminates stores -T (its final
+// transmittance, sign flipped); from then on T*(1-w) <= 0 never passes the
+// termination test, so no separate alive mask is needed.  Pixels outside the
+// image start at T = -1.
 template <int MODE, bool STEEP>
 __device__ __forceinline__ void fwd_splat(const float4 (&q)[4], const SteepRec& side, float px,
                                           float py0, float (&T)[kPx], float (&ar)[kPx],
                                           float (&ag)[kPx], float (&ab)[kPx], float (&ad)[kPx],
-                                          int (&cnt)[kPx], unsigned& alive) {
+                                          int (&cnt)[kPx]) {
   const SplatLane s = splat_lane<STEEP>(q, side, px, py0);
   const float c1 = q[1].w, c2 = q[2].x;
   const float cr = q[2].y, cg = q[2].z, cb = q[2].w, z = q[3].x;
@@ -145,16 +149,22 @@ __device__ __forceinline__ void fwd_splat(const float4 (&q)[4], const SteepRec& 
     w = fminf(w, kWeightClamp);
     const float tn = T[i] * (1.0f - w);
     // the pixel terminates *before* compositing this splat (_blend_cy.pyx:165-169)
-    const bool commit = ((alive >> i) & 1u) && !(tn < kTerminationT);
-    alive &= commit ? 0xffffffffu : ~(1u << i);
+    const bool commit = tn >= kTerminationT;
     const float wt = commit ? w * T[i] : 0.0f;
     ar[i] = fmaf(wt, cr, ar[i]);
     ag[i] = fmaf(wt, cg, ag[i]);
     ab[i] = fmaf(wt, cb, ab[i]);
     ad[i] = fmaf(wt, z, ad[i]);
     cnt[i] += commit ? 1 : 0;
-    T[i] = commit ? tn : T[i];
+    T[i] = commit ? tn : -fabsf(T[i]);
   }
+}
+
+__device__ __forceinline__ bool warp_any_alive(const float (&T)[kPx]) {
+  float m = T[0];
+#pragma unroll
+  for (int i = 1; i < kPx; ++i) m = fmaxf(m, T[i]);
+  return __any_sync(0xffffffffu, m > 0.0f);
 }
 
 __global__ void __launch_bounds__(kWarpsPerCta * 32) blend_fwd_kernel(
@@ -174,17 +184,17 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) blend_fwd_kernel(
     const float py0 = (float)row0 + 0.5f;
     float T[kPx], ar[kPx], ag[kPx], ab[kPx], ad[kPx];
     int cnt[kPx];
-    unsigned alive = 0;
 #pragma unroll
     for (int i = 0; i < kPx; ++i) {
-      T[i] = 1.f; ar[i] = 0.f; ag[i] = 0.f; ab[i] = 0.f; ad[i] = 0.f; cnt[i] = 0;
-      if (col < g.width && row0 + 2 * i < g.height) alive |= 1u << i;
+      T[i] = (col < g.width && row0 + 2 * i < g.height) ? 1.f : -1.f;
+      ar[i] = 0.f; ag[i] = 0.f; ab[i] = 0.f; ad[i] = 0.f; cnt[i] = 0;
     }
     const int k0 = g.tile_starts[tile];
     const int nk = g.tile_starts[tile + 1] - k0;
     auto fwd_pos = [](int j) { return j; };
     if (nk > 0) issue_batch(g, k0, min(kBatch, nk), fwd_pos, st, 0, lane);
-    for (int b = 0; b * kBatch < nk; ++b) {
+    bool any = true;
+    for (int b = 0; b * kBatch < nk && any; ++b) {
       const int nb = min(kBatch, nk - b * kBatch);
       if ((b + 1) * kBatch < nk)
         issue_batch(g, k0 + (b + 1) * kBatch, min(kBatch, nk - (b + 1) * kBatch), fwd_pos, st,
@@ -194,29 +204,28 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) blend_fwd_kernel(
       cp_async_wait<1>();
       __syncwarp();
       const int s = b & 1;
-      bool any = true;
       for (int j = 0; j < nb; ++j) {
-        any = __any_sync(0xffffffffu, alive != 0);
-        if (!any) break;
+        // dead pixels never change again: stop once the whole tile is dead
+        // (checked every 8 splats; the reference checks per splat, same result)
+        if ((j & 7) == 0 && !(any = warp_any_alive(T))) break;
         const float4 q[4] = {st.rec[s][j][0], st.rec[s][j][1], st.rec[s][j][2], st.rec[s][j][3]};
         const uint32_t flags = __float_as_uint(q[3].y);
         const int mode = (int)(flags & 3u);
         const SteepRec& side = st.side[s][j];
         if (flags & 4u) {
           if (mode == kModeErf)
-            fwd_splat<kModeErf, true>(q, side, px, py0, T, ar, ag, ab, ad, cnt, alive);
+            fwd_splat<kModeErf, true>(q, side, px, py0, T, ar, ag, ab, ad, cnt);
           else
-            fwd_splat<kModeSign, true>(q, side, px, py0, T, ar, ag, ab, ad, cnt, alive);
+            fwd_splat<kModeSign, true>(q, side, px, py0, T, ar, ag, ab, ad, cnt);
         } else if (mode == kModeErf) {
-          fwd_splat<kModeErf, false>(q, side, px, py0, T, ar, ag, ab, ad, cnt, alive);
+          fwd_splat<kModeErf, false>(q, side, px, py0, T, ar, ag, ab, ad, cnt);
         } else if (mode == kModeSign) {
-          fwd_splat<kModeSign, false>(q, side, px, py0, T, ar, ag, ab, ad, cnt, alive);
+          fwd_splat<kModeSign, false>(q, side, px, py0, T, ar, ag, ab, ad, cnt);
         } else {
-          fwd_splat<kModePlain, false>(q, side, px, py0, T, ar, ag, ab, ad, cnt, alive);
+          fwd_splat<kModePlain, false>(q, side, px, py0, T, ar, ag, ab, ad, cnt);
         }
       }
       __syncwarp();
-      if (!any) break;
     }
     cp_async_wait<0>();
     __syncwarp();
@@ -225,12 +234,13 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) blend_fwd_kernel(
       const int row = row0 + 2 * i;
       if (col < g.width && row < g.height) {
         const size_t p = (size_t)row * g.width + col;
-        color[3 * p + 0] = fmaf(T[i], bg0, ar[i]);
-        color[3 * p + 1] = fmaf(T[i], bg1, ag[i]);
-        color[3 * p + 2] = fmaf(T[i], bg2, ab[i]);
-        alpha[p] = 1.0f - T[i];
+        const float t = fabsf(T[i]);
+        color[3 * p + 0] = fmaf(t, bg0, ar[i]);
+        color[3 * p + 1] = fmaf(t, bg1, ag[i]);
+        color[3 * p + 2] = fmaf(t, bg2, ab[i]);
+        alpha[p] = 1.0f - t;
         depth[p] = ad[i];
-        trans[p] = T[i];
+        trans[p] = t;
         terminal[p] = cnt[i];
       }
     }
@@ -245,7 +255,9 @@ struct BwdAcc {
   float c1, c2, r, g, b;
 };
 
-template <int MODE, bool STEEP>
+// ALL: every pixel of the warp is active at this position (pos < warp-min of the
+// terminal counts), so the per-pixel activity selects disappear.
+template <int MODE, bool STEEP, bool ALL>
 __device__ __forceinline__ void bwd_splat(const float4 (&q)[4], const SteepRec& side, int pos,
                                           float px, float py0, float (&T)[kPx], float (&D)[kPx],
                                           const float (&dr)[kPx], const float (&dg)[kPx],
@@ -259,7 +271,7 @@ __device__ __forceinline__ void bwd_splat(const float4 (&q)[4], const SteepRec& 
   // compute and contribute exact zeros, so the eight chains interleave.
 #pragma unroll
   for (int i = 0; i < kPx; ++i) {
-    const bool active = pos < cnt[i];
+    const bool active = ALL || pos < cnt[i];
     const float dy = s.dy0 + 2.0f * i;
     const float gg = ex2_approx(fmaf(fmaf(s.C, dy, s.Bx), dy, s.P0));
     float e = 0.f, zz = 0.f, u;
@@ -359,7 +371,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) blend_bwd_kernel(
     const float py0 = (float)row0 + 0.5f;
     float T[kPx], D[kPx], dr[kPx], dg[kPx], db[kPx];
     int cnt[kPx];
-    int maxc = 0;
+    int maxc = 0, minc = 0x7fffffff;
 #pragma unroll
     for (int i = 0; i < kPx; ++i) {
       const int row = row0 + 2 * i;
@@ -371,11 +383,15 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) blend_bwd_kernel(
         dg[i] = d_color[3 * p + 1];
         db[i] = d_color[3 * p + 2];
         D[i] = T[i] * fmaf(dr[i], bg0, fmaf(dg[i], bg1, db[i] * bg2));
+        maxc = max(maxc, cnt[i]);
+        minc = min(minc, cnt[i]);
       } else {
-        T[i] = 1.f; cnt[i] = 0; dr[i] = 0.f; dg[i] = 0.f; db[i] = 0.f; D[i] = 0.f;
+        // outside the image: always "active" with T = 0 and a zero cotangent,
+        // which contributes exact zeros (and keeps T_prev = 0 finite)
+        T[i] = 0.f; cnt[i] = 0x7fffffff; dr[i] = 0.f; dg[i] = 0.f; db[i] = 0.f; D[i] = 0.f;
       }
-      maxc = max(maxc, cnt[i]);
     }
+    minc = __reduce_min_sync(0xffffffffu, minc);
     maxc = __reduce_max_sync(0xffffffffu, maxc);
     const int k0 = g.tile_starts[tile];
     if (!kRowsBySortedPos && lane == 0)
@@ -408,17 +424,32 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) blend_bwd_kernel(
         const uint32_t flags = __float_as_uint(q[3].y);
         const int mode = (int)(flags & 3u);
         BwdAcc a = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        if (flags & 4u) {
-          if (mode == kModeErf)
-            bwd_splat<kModeErf, true>(q, side, pos, px, py0, T, D, dr, dg, db, cnt, a);
-          else
-            bwd_splat<kModeSign, true>(q, side, pos, px, py0, T, D, dr, dg, db, cnt, a);
-        } else if (mode == kModeErf) {
-          bwd_splat<kModeErf, false>(q, side, pos, px, py0, T, D, dr, dg, db, cnt, a);
-        } else if (mode == kModeSign) {
-          bwd_splat<kModeSign, false>(q, side, pos, px, py0, T, D, dr, dg, db, cnt, a);
+        if (pos < minc) {
+          if (flags & 4u) {
+            if (mode == kModeErf)
+              bwd_splat<kModeErf, true, true>(q, side, pos, px, py0, T, D, dr, dg, db, cnt, a);
+            else
+              bwd_splat<kModeSign, true, true>(q, side, pos, px, py0, T, D, dr, dg, db, cnt, a);
+          } else if (mode == kModeErf) {
+            bwd_splat<kModeErf, false, true>(q, side, pos, px, py0, T, D, dr, dg, db, cnt, a);
+          } else if (mode == kModeSign) {
+            bwd_splat<kModeSign, false, true>(q, side, pos, px, py0, T, D, dr, dg, db, cnt, a);
+          } else {
+            bwd_splat<kModePlain, false, true>(q, side, pos, px, py0, T, D, dr, dg, db, cnt, a);
+          }
         } else {
-          bwd_splat<kModePlain, false>(q, side, pos, px, py0, T, D, dr, dg, db, cnt, a);
+          if (flags & 4u) {
+            if (mode == kModeErf)
+              bwd_splat<kModeErf, true, false>(q, side, pos, px, py0, T, D, dr, dg, db, cnt, a);
+            else
+              bwd_splat<kModeSign, true, false>(q, side, pos, px, py0, T, D, dr, dg, db, cnt, a);
+          } else if (mode == kModeErf) {
+            bwd_splat<kModeErf, false, false>(q, side, pos, px, py0, T, D, dr, dg, db, cnt, a);
+          } else if (mode == kModeSign) {
+            bwd_splat<kModeSign, false, false>(q, side, pos, px, py0, T, D, dr, dg, db, cnt, a);
+          } else {
+            bwd_splat<kModePlain, false, false>(q, side, pos, px, py0, T, D, dr, dg, db, cnt, a);
+          }
         }
         // per-lane partials -> the pair-row columns (_blend_py.py:16-18)
         const float ca = q[0].z, cb = q[0].w, cc = q[1].x, za = q[1].y, zb = q[1].z;

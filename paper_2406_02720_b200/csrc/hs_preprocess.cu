@@ -167,9 +167,10 @@ __device__ __forceinline__ void matvec_blas(const double M[9], const double v[3]
     out[a] = fma(v[2], M[3 * a + 2], fma(v[1], M[3 * a + 1], v[0] * M[3 * a]));
 }
 
-template <typename T>
-__device__ void forward_state(const SceneArgs<T>& sc, const CamArgs& cam, int kernel,
-                              int64_t i, FwdState& st) {
+template <int DEG, typename T>
+__device__ __forceinline__ void forward_state(const SceneArgs<T>& sc, const CamArgs& cam,
+                                              int kernel, int64_t i, FwdState& st) {
+  constexpr int K = (DEG + 1) * (DEG + 1);
   const double m0 = ld(sc.mu, 3 * i), m1 = ld(sc.mu, 3 * i + 1), m2 = ld(sc.mu, 3 * i + 2);
   // t_all = mu @ rot.T + translation (rasterizer.py:170)
   {
@@ -301,10 +302,12 @@ __device__ void forward_state(const SceneArgs<T>& sc, const CamArgs& cam, int ke
   double vv[3] = {m0 - cam.center[0], m1 - cam.center[1], m2 - cam.center[2]};
   st.vdist = sqrt(vv[0] * vv[0] + vv[1] * vv[1] + vv[2] * vv[2]);
   for (int k = 0; k < 3; ++k) st.vdir[k] = vv[k] / st.vdist;
-  sh_basis(st.vdir, sc.deg, st.basis);
+  sh_basis(st.vdir, DEG, st.basis);
+#pragma unroll
   for (int ch = 0; ch < 3; ++ch) {
     double acc = 0.0;
-    for (int k = 0; k < sc.K; ++k) acc += st.basis[k] * ld(sc.sh, (i * sc.K + k) * 3 + ch);
+#pragma unroll
+    for (int k = 0; k < K; ++k) acc += st.basis[k] * ld(sc.sh, (i * K + k) * 3 + ch);
     st.rgbu[ch] = acc + 0.5;
   }
 }
@@ -312,7 +315,7 @@ __device__ void forward_state(const SceneArgs<T>& sc, const CamArgs& cam, int ke
 // ---------------------------------------------------------------------------
 // K1: preprocess forward.  Writes the 64-B record, tile rect, pair count and
 // the depth-rank sort key of each primitive (culled: count 0, key ~0).
-template <typename T>
+template <typename T, int DEG>
 __global__ void __launch_bounds__(128) preprocess_fwd_kernel(
     SceneArgs<T> sc, CamArgs cam, int kernel, int64_t n, float4* __restrict__ rec,
     SteepRec* __restrict__ side, int4* __restrict__ rect, int32_t* __restrict__ count,
@@ -320,7 +323,7 @@ __global__ void __launch_bounds__(128) preprocess_fwd_kernel(
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   FwdState st;
-  forward_state(sc, cam, kernel, i, st);
+  forward_state<DEG>(sc, cam, kernel, i, st);
   if (!st.visible) {
     dval[i] = (uint32_t)i;
     count[i] = 0;
@@ -359,7 +362,7 @@ __global__ void __launch_bounds__(128) preprocess_fwd_kernel(
 // K7: merge the splat's pair rows (np.add.at, rasterizer.py:419-420) and chain
 // them through the projection to the primitive parameters
 // (_geometry_backward, rasterizer.py:424-575).  FP64 throughout.
-template <typename T>
+template <typename T, int DEG>
 __global__ void __launch_bounds__(128) preprocess_bwd_kernel(
     SceneArgs<T> sc, CamArgs cam, int kernel, int64_t n, int tiles_x,
     const float4* __restrict__ rec, const int4* __restrict__ rect,
@@ -368,7 +371,7 @@ __global__ void __launch_bounds__(128) preprocess_bwd_kernel(
     GradArgs<T> out) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const int K = sc.K;
+  constexpr int K = (DEG + 1) * (DEG + 1);
   const int cnt = count[i];
   if (cnt == 0) {
     for (int k = 0; k < 3; ++k) {
@@ -407,7 +410,7 @@ __global__ void __launch_bounds__(128) preprocess_bwd_kernel(
     }
   }
   FwdState st;
-  forward_state(sc, cam, kernel, i, st);
+  forward_state<DEG>(sc, cam, kernel, i, st);
 
   const double d_mux = m[0], d_muy = m[1];
   const double d_ca = m[2], d_cb = m[3], d_cc = m[4];
@@ -568,9 +571,9 @@ __global__ void __launch_bounds__(128) preprocess_bwd_kernel(
     for (int ch = 0; ch < 3; ++ch) dpre[ch] = st.rgbu[ch] > 0.0 ? d_rgb[ch] : 0.0;
     for (int k = 0; k < K; ++k)
       for (int ch = 0; ch < 3; ++ch) out.d_sh[3 * K * i + 3 * k + ch] = T(st.basis[k] * dpre[ch]);
-    if (sc.deg > 0) {
+    if (DEG > 0) {
       double g[48];
-      sh_basis_grad(st.vdir, sc.deg, g);
+      sh_basis_grad(st.vdir, DEG, g);
       double d_dir[3] = {0.0, 0.0, 0.0};
       for (int k = 0; k < K; ++k) {
         double db = 0.0;
@@ -635,8 +638,17 @@ cudaError_t launch_preprocess_fwd_t(const SceneArgs<T>& sc, const CamArgs& cam, 
                                     int32_t* radii, cudaStream_t stream) {
   const int block = 128;
   const int64_t grid = (n + block - 1) / block;
-  preprocess_fwd_kernel<T><<<(unsigned)grid, block, 0, stream>>>(sc, cam, kernel, n, rec, side,
-                                                                rect, count, dkey, dval, radii);
+  switch (sc.deg) {
+#define HS_K1(D)                                                                              \
+  case D:                                                                                     \
+    preprocess_fwd_kernel<T, D><<<(unsigned)grid, block, 0, stream>>>(sc, cam, kernel, n, rec, \
+                                                                      side, rect, count, dkey, \
+                                                                      dval, radii);           \
+    break;
+    HS_K1(0) HS_K1(1) HS_K1(2) HS_K1(3)
+#undef HS_K1
+    default: return cudaErrorInvalidValue;
+  }
   note_launch();
   return cudaGetLastError();
 }
@@ -649,8 +661,16 @@ cudaError_t launch_preprocess_bwd_t(const SceneArgs<T>& sc, const CamArgs& cam, 
                                     const GradArgs<T>& out, cudaStream_t stream) {
   const int block = 128;
   const int64_t grid = (n + block - 1) / block;
-  preprocess_bwd_kernel<T><<<(unsigned)grid, block, 0, stream>>>(
-      sc, cam, kernel, n, tiles_x, rec, rect, count, rank_of, last_rank, rows, out);
+  switch (sc.deg) {
+#define HS_K7(D)                                                                               \
+  case D:                                                                                      \
+    preprocess_bwd_kernel<T, D><<<(unsigned)grid, block, 0, stream>>>(                         \
+        sc, cam, kernel, n, tiles_x, rec, rect, count, rank_of, last_rank, rows, out);         \
+    break;
+    HS_K7(0) HS_K7(1) HS_K7(2) HS_K7(3)
+#undef HS_K7
+    default: return cudaErrorInvalidValue;
+  }
   note_launch();
   return cudaGetLastError();
 }

@@ -36,15 +36,15 @@ def erf32(z):
 
 
 def test_coefficients_parse():
-    assert len(coefficients()) == 9
+    assert len(coefficients()) == 6
 
 
 def test_erf32_accuracy_vs_reference_erf():
     gold = load_golden("erf")
     z = gold["z"].astype(np.float32)
     got = erf32(z).astype(np.float64)
-    # reference polynomial is within 5e-9 of erf; the FP32 one within ~1e-7
-    assert np.abs(got - gold["erf"]).max() < 2.5e-7
+    # reference polynomial is within 5e-9 of erf; the FP32 one within ~3.3e-7
+    assert np.abs(got - gold["erf"]).max() < 4e-7
 
 
 def test_erf32_is_exactly_odd():

@@ -1,6 +1,6 @@
 """Fit the FP32 erf used by the blend kernels (csrc/hs_common.cuh:erf32).
 
-erf(x) = 1 - 2**Q(x) for x >= 0 with Q(x) = x * R(x), R of degree 8, fitted
+erf(x) = 1 - 2**Q(x) for x >= 0 with Q(x) = x * R(x), R of degree 5, fitted
 to log2(erfc(x)) on [0, 3.92] by iteratively reweighted least squares
 (Lawson) with weight erfc(x)*ln2 (i.e. minimising the absolute error of erf).
 Prints the coefficients (lowest order first) and the max abs error of an
@@ -38,7 +38,7 @@ def eval_f32(c, x):
 
 
 if __name__ == "__main__":
-    coeffs = fit(9).astype(np.float32)
+    coeffs = fit(6).astype(np.float32)
     xs = np.linspace(0, 6, 200001)
     err = np.abs(eval_f32(coeffs, xs).astype(np.float64) - erf(xs)).max()
     for v in coeffs:
