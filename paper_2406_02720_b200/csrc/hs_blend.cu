@@ -111,46 +111,60 @@ __device__ __forceinline__ SplatLane splat_lane(const float4 (&q)[4], const Stee
   return s;
 }
 
-template <bool STEEP>
-__device__ __forceinline__ float erf_arg(const SplatLane& s, float dy, int i) {
-  if (STEEP) return (float)fma(s.zbd, (s.py0d + 2.0 * i) - s.muyd, s.Z0d);
-  return fmaf(s.zb, dy, s.Z0);
+// erf argument z for the 8 pixels of a lane: FP32 for ordinary splats, FP64
+// (side record) for steep ones.
+__device__ __forceinline__ void erf_args(const SplatLane& s, bool steep, float (&z)[kPx]) {
+  if (steep) {
+#pragma unroll
+    for (int i = 0; i < kPx; ++i) z[i] = (float)fma(s.zbd, (s.py0d + 2.0 * i) - s.muyd, s.Z0d);
+  } else {
+#pragma unroll
+    for (int i = 0; i < kPx; ++i) z[i] = fmaf(s.zb, s.dy0 + 2.0f * i, s.Z0);
+  }
+}
+
+// Blend factor E of the three modes (_blend_cy.pyx:156-161); mode 2 records
+// carry za = zb = 0, so erf32(0) = 0 serves it too.
+__device__ __forceinline__ float mode_factor(int mode, float z) {
+  return mode == kModeSign ? sign32(z) : erf32(z);
 }
 
 // ---------------------------------------------------------------------------
-// K5 forward
-// Live pixels hold T > 0.  A pixel that terminates stores -T (its final
-// transmittance, sign flipped); from then on T*(1-w) <= 0 never passes the
+// K5 forward.  Live pixels hold T > 0.  A pixel that terminates stores -T (its
+// final transmittance, sign flipped); from then on T*(1-w) <= 0 never passes the
 // termination test, so no separate alive mask is needed.  Pixels outside the
-// image start at T = -1.
-template <int MODE, bool STEEP>
-__device__ __forceinline__ void fwd_splat(const float4 (&q)[4], const SteepRec& side, float px,
-                                          float py0, float (&T)[kPx], float (&ar)[kPx],
-                                          float (&ag)[kPx], float (&ab)[kPx], float (&ad)[kPx],
-                                          int (&cnt)[kPx]) {
-  const SplatLane s = splat_lane<STEEP>(q, side, px, py0);
+// image start at T = -1.  Branch-free over the 8 pixels (selects only) so the
+// compiler interleaves the eight independent chains; dead pixels compute and
+// discard.
+//
+// FAST: mode 0 or 2, FP32 erf argument, weight provably below the 0.99 clamp
+// (the common case); otherwise every feature is resolved from `flags` at run
+// time.
+template <bool FAST>
+__device__ __forceinline__ void fwd_splat(const float4 (&q)[4], const SteepRec& side,
+                                          uint32_t flags, float px, float py0, float (&T)[kPx],
+                                          float (&ar)[kPx], float (&ag)[kPx], float (&ab)[kPx],
+                                          float (&ad)[kPx], int (&cnt)[kPx]) {
+  const bool steep = !FAST && (flags & kFlagSteep);
+  const SplatLane s = steep ? splat_lane<true>(q, side, px, py0)
+                            : splat_lane<false>(q, side, px, py0);
+  const int mode = (int)(flags & 3u);
   const float c1 = q[1].w, c2 = q[2].x;
   const float cr = q[2].y, cg = q[2].z, cb = q[2].w, z = q[3].x;
-  // Branch-free over the 8 pixels (selects, no per-pixel basic blocks) so the
-  // compiler interleaves the eight independent chains; dead pixels compute and
-  // discard.
+  float zz[kPx];
+  erf_args(s, steep, zz);
 #pragma unroll
   for (int i = 0; i < kPx; ++i) {
     const float dy = s.dy0 + 2.0f * i;
     const float g = ex2_approx(fmaf(fmaf(s.C, dy, s.Bx), dy, s.P0));
-    float w;
-    if (MODE == kModeErf) {
-      w = fmaf(c2, erf32(erf_arg<STEEP>(s, dy, i)), c1) * g;
-    } else if (MODE == kModeSign) {
-      w = fmaf(c2, sign32(erf_arg<STEEP>(s, dy, i)), c1) * g;
-    } else {
-      w = c1 * g;
-    }
-    w = fminf(w, kWeightClamp);
-    const float tn = T[i] * (1.0f - w);
+    const float e = FAST ? erf32(zz[i]) : mode_factor(mode, zz[i]);
+    float w = fmaf(c2, e, c1) * g;
+    if (!FAST) w = fminf(w, kWeightClamp);
+    const float wT = w * T[i];
+    const float tn = T[i] - wT;  // T * (1 - w)
     // the pixel terminates *before* compositing this splat (_blend_cy.pyx:165-169)
     const bool commit = tn >= kTerminationT;
-    const float wt = commit ? w * T[i] : 0.0f;
+    const float wt = commit ? wT : 0.0f;
     ar[i] = fmaf(wt, cr, ar[i]);
     ag[i] = fmaf(wt, cg, ag[i]);
     ab[i] = fmaf(wt, cb, ab[i]);
@@ -165,6 +179,10 @@ __device__ __forceinline__ bool warp_any_alive(const float (&T)[kPx]) {
 #pragma unroll
   for (int i = 1; i < kPx; ++i) m = fmaxf(m, T[i]);
   return __any_sync(0xffffffffu, m > 0.0f);
+}
+
+__device__ __forceinline__ bool fast_flags(uint32_t flags) {
+  return (flags & (kFlagSteep | kFlagClamp)) == 0 && (flags & 3u) != (uint32_t)kModeSign;
 }
 
 __global__ void __launch_bounds__(kWarpsPerCta * 32) blend_fwd_kernel(
@@ -210,20 +228,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) blend_fwd_kernel(
         if ((j & 7) == 0 && !(any = warp_any_alive(T))) break;
         const float4 q[4] = {st.rec[s][j][0], st.rec[s][j][1], st.rec[s][j][2], st.rec[s][j][3]};
         const uint32_t flags = __float_as_uint(q[3].y);
-        const int mode = (int)(flags & 3u);
-        const SteepRec& side = st.side[s][j];
-        if (flags & 4u) {
-          if (mode == kModeErf)
-            fwd_splat<kModeErf, true>(q, side, px, py0, T, ar, ag, ab, ad, cnt);
-          else
-            fwd_splat<kModeSign, true>(q, side, px, py0, T, ar, ag, ab, ad, cnt);
-        } else if (mode == kModeErf) {
-          fwd_splat<kModeErf, false>(q, side, px, py0, T, ar, ag, ab, ad, cnt);
-        } else if (mode == kModeSign) {
-          fwd_splat<kModeSign, false>(q, side, px, py0, T, ar, ag, ab, ad, cnt);
-        } else {
-          fwd_splat<kModePlain, false>(q, side, px, py0, T, ar, ag, ab, ad, cnt);
-        }
+        if (fast_flags(flags))
+          fwd_splat<true>(q, st.side[s][j], flags, px, py0, T, ar, ag, ab, ad, cnt);
+        else
+          fwd_splat<false>(q, st.side[s][j], flags, px, py0, T, ar, ag, ab, ad, cnt);
       }
       __syncwarp();
     }
@@ -255,38 +263,35 @@ struct BwdAcc {
   float c1, c2, r, g, b;
 };
 
-// ALL: every pixel of the warp is active at this position (pos < warp-min of the
-// terminal counts), so the per-pixel activity selects disappear.
-template <int MODE, bool STEEP, bool ALL>
-__device__ __forceinline__ void bwd_splat(const float4 (&q)[4], const SteepRec& side, int pos,
-                                          float px, float py0, float (&T)[kPx], float (&D)[kPx],
+// FAST: as in the forward, plus every pixel of the warp active at this position
+// (pos < warp-min of the terminal counts), so the activity selects vanish.
+// Inactive pixels (generic path) compute and contribute exact zeros.
+template <bool FAST>
+__device__ __forceinline__ void bwd_splat(const float4 (&q)[4], const SteepRec& side,
+                                          uint32_t flags, int pos, float px, float py0,
+                                          float (&T)[kPx], float (&D)[kPx],
                                           const float (&dr)[kPx], const float (&dg)[kPx],
                                           const float (&db)[kPx], const int (&cnt)[kPx],
                                           BwdAcc& a) {
-  const SplatLane s = splat_lane<STEEP>(q, side, px, py0);
+  const bool steep = !FAST && (flags & kFlagSteep);
+  const SplatLane s = steep ? splat_lane<true>(q, side, px, py0)
+                            : splat_lane<false>(q, side, px, py0);
+  const int mode = (int)(flags & 3u);
   const float c1 = q[1].w, c2 = q[2].x;
   const float cr = q[2].y, cg = q[2].z, cb = q[2].w;
-  const float c2k = c2 * (2.0f * kInvSqrtPi);
-  // Branch-free over the 8 pixels: inactive pixels (pos >= terminal count)
-  // compute and contribute exact zeros, so the eight chains interleave.
+  // d erf/dz = 2/sqrt(pi) exp(-z^2); only the erf mode has a z derivative
+  const float c2k = (FAST || mode == kModeErf) ? c2 * (2.0f * kInvSqrtPi) : 0.0f;
+  float zz[kPx];
+  erf_args(s, steep, zz);
 #pragma unroll
   for (int i = 0; i < kPx; ++i) {
-    const bool active = ALL || pos < cnt[i];
+    const bool active = FAST || pos < cnt[i];
     const float dy = s.dy0 + 2.0f * i;
     const float gg = ex2_approx(fmaf(fmaf(s.C, dy, s.Bx), dy, s.P0));
-    float e = 0.f, zz = 0.f, u;
-    if (MODE == kModeErf) {
-      zz = erf_arg<STEEP>(s, dy, i);
-      e = erf32(zz);
-      u = fmaf(c2, e, c1);
-    } else if (MODE == kModeSign) {
-      e = sign32(erf_arg<STEEP>(s, dy, i));
-      u = fmaf(c2, e, c1);
-    } else {
-      u = c1;
-    }
+    const float e = FAST ? erf32(zz[i]) : mode_factor(mode, zz[i]);
+    const float u = fmaf(c2, e, c1);
     const float w_raw = u * gg;
-    const float w = fminf(w_raw, kWeightClamp);
+    const float w = FAST ? w_raw : fminf(w_raw, kWeightClamp);
     const float inv = rcp_approx(1.0f - w);  // 1 - w >= 0.01
     const float Tp = T[i] * inv;
     const float wt = active ? w * Tp : 0.0f;
@@ -294,8 +299,10 @@ __device__ __forceinline__ void bwd_splat(const float4 (&q)[4], const SteepRec& 
     a.r = fmaf(dr[i], wt, a.r);
     a.g = fmaf(dg[i], wt, a.g);
     a.b = fmaf(db[i], wt, a.b);
-    // gradient gating on the unclamped weight (_blend_cy.pyx:309)
-    const float d_w = (active && w_raw <= kWeightClamp) ? fmaf(Tp, dcr, -inv * D[i]) : 0.0f;
+    // d_w = T_prev*(dC.rgb) - (dC.S)/(1-w) = inv*(T*dcr - D); gated on the
+    // unclamped weight (_blend_cy.pyx:309-312)
+    float d_w = inv * fmaf(T[i], dcr, -D[i]);
+    if (!FAST) d_w = (active && w_raw <= kWeightClamp) ? d_w : 0.0f;
     const float dwg = d_w * gg;
     const float d_pow = dwg * u;
     a.s0 += d_pow;
@@ -303,12 +310,10 @@ __device__ __forceinline__ void bwd_splat(const float4 (&q)[4], const SteepRec& 
     a.s2 = fmaf(d_pow * dy, dy, a.s2);
     a.c1 += dwg;
     a.c2 = fmaf(dwg, e, a.c2);
-    if (MODE == kModeErf) {
-      const float d_z = dwg * c2k * ex2_approx(-(zz * zz) * kLog2e);
-      a.q0 += d_z;
-      a.q1 = fmaf(d_z, dy, a.q1);
-      a.qz = fmaf(d_z, zz, a.qz);
-    }
+    const float d_z = dwg * c2k * ex2_approx(-(zz[i] * zz[i]) * kLog2e);
+    a.q0 += d_z;
+    a.q1 = fmaf(d_z, dy, a.q1);
+    a.qz = fmaf(d_z, zz[i], a.qz);
     D[i] = fmaf(wt, dcr, D[i]);
     T[i] = active ? Tp : T[i];
   }
@@ -424,33 +429,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) blend_bwd_kernel(
         const uint32_t flags = __float_as_uint(q[3].y);
         const int mode = (int)(flags & 3u);
         BwdAcc a = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        if (pos < minc) {
-          if (flags & 4u) {
-            if (mode == kModeErf)
-              bwd_splat<kModeErf, true, true>(q, side, pos, px, py0, T, D, dr, dg, db, cnt, a);
-            else
-              bwd_splat<kModeSign, true, true>(q, side, pos, px, py0, T, D, dr, dg, db, cnt, a);
-          } else if (mode == kModeErf) {
-            bwd_splat<kModeErf, false, true>(q, side, pos, px, py0, T, D, dr, dg, db, cnt, a);
-          } else if (mode == kModeSign) {
-            bwd_splat<kModeSign, false, true>(q, side, pos, px, py0, T, D, dr, dg, db, cnt, a);
-          } else {
-            bwd_splat<kModePlain, false, true>(q, side, pos, px, py0, T, D, dr, dg, db, cnt, a);
-          }
-        } else {
-          if (flags & 4u) {
-            if (mode == kModeErf)
-              bwd_splat<kModeErf, true, false>(q, side, pos, px, py0, T, D, dr, dg, db, cnt, a);
-            else
-              bwd_splat<kModeSign, true, false>(q, side, pos, px, py0, T, D, dr, dg, db, cnt, a);
-          } else if (mode == kModeErf) {
-            bwd_splat<kModeErf, false, false>(q, side, pos, px, py0, T, D, dr, dg, db, cnt, a);
-          } else if (mode == kModeSign) {
-            bwd_splat<kModeSign, false, false>(q, side, pos, px, py0, T, D, dr, dg, db, cnt, a);
-          } else {
-            bwd_splat<kModePlain, false, false>(q, side, pos, px, py0, T, D, dr, dg, db, cnt, a);
-          }
-        }
+        if (pos < minc && fast_flags(flags))
+          bwd_splat<true>(q, side, flags, pos, px, py0, T, D, dr, dg, db, cnt, a);
+        else
+          bwd_splat<false>(q, side, flags, pos, px, py0, T, D, dr, dg, db, cnt, a);
         // per-lane partials -> the pair-row columns (_blend_py.py:16-18)
         const float ca = q[0].z, cb = q[0].w, cc = q[1].x, za = q[1].y, zb = q[1].z;
         const float2 lo = __half22float2(*reinterpret_cast<const __half2*>(&q[3].w));
@@ -461,21 +443,23 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) blend_bwd_kernel(
         v[2] = -0.5f * dx * dx * a.s0;
         v[3] = -dx * a.s1;
         v[4] = -0.5f * a.s2;
-        v[5] = dx * a.q0;
-        v[6] = a.q1;
+        // za/zb gradients exist only in the erf mode (_blend_cy.pyx:322-329)
+        const bool erf_mode = (flags & 3u) == (uint32_t)kModeErf;
+        v[5] = erf_mode ? dx * a.q0 : 0.f;
+        v[6] = erf_mode ? a.q1 : 0.f;
         v[7] = a.c1;
         v[8] = a.c2;
         v[9] = a.r;
         v[10] = a.g;
         v[11] = a.b;
-        v[12] = a.qz;
+        v[12] = erf_mode ? a.qz : 0.f;
         v[13] = v[14] = v[15] = 0.f;
         const float total = warp_transpose_reduce16(v, lane);
         size_t row;
         if (kRowsBySortedPos) {
           row = (size_t)(k0 + pos);
         } else {
-          const int spans_x = (int)(flags >> 3);
+          const int spans_x = (int)(flags >> kFlagSpanShift);
           row = (size_t)((int)__float_as_uint(q[3].z) + ty * spans_x + tx);
         }
         const int vi = lane >> 1;
@@ -509,7 +493,7 @@ __global__ void pack_records_kernel(const double* __restrict__ packed,
   const bool steep = md != kModePlain && is_steep(p[5], p[6], reach);
   const float mux = (float)p[0], muy = (float)p[1];
   const __half2 lo = __floats2half2_rn((float)(p[0] - (double)mux), (float)(p[1] - (double)muy));
-  r[R_FLAGS] = __uint_as_float(pack_flags(md, steep, 0));
+  r[R_FLAGS] = __uint_as_float(pack_flags(md, steep, may_clamp(p[7], p[8]), 0));
   r[R_ROW_ORIGIN] = __int_as_float(0);
   r[R_MU_LO] = __uint_as_float(*reinterpret_cast<const uint32_t*>(&lo));
   if (steep) side[l] = SteepRec{p[0], p[1], p[5], p[6]};

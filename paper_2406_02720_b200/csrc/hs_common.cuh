@@ -25,7 +25,7 @@ constexpr float kLog2e = 1.4426950408889634f;
 enum RecordSlot {
   R_MUX = 0, R_MUY, R_CA, R_CB, R_CC, R_ZA, R_ZB, R_C1, R_C2,
   R_RED, R_GREEN, R_BLUE, R_DEPTH,
-  R_FLAGS,       // u32: mode (bits 0-1) | steep (bit 2) | spans_x << 3
+  R_FLAGS,       // u32: mode (bits 0-1) | steep (bit 2) | may-clamp (bit 3) | spans_x << 4
   R_ROW_ORIGIN,  // i32: pair_base - ty0*spans_x - tx0; pair (tx,ty) -> row origin + ty*spans_x + tx
   R_MU_LO        // half2: (mux - (float)mux, muy - (float)muy)
 };
@@ -37,11 +37,12 @@ constexpr int kRecordFloats = 16;
 // the flag also rides in bit 31 of the sort value so the blend's staging lane
 // knows to fetch it.  Criterion: (|za| + |zb|) * reach > kSteepLimit, reach =
 // radius + 24 px bounds |dx|,|dy| inside any covered tile, so non-steep splats
-// keep |z| rounding error below ~6e-8 * 64 = 4e-6.
+// keep |z| rounding error below ~6e-8 * 256 = 1.5e-5 (a weight error below
+// 0.56 * 1.5e-5 = 9e-6).  About 10% of the c3 pairs are steep.
 struct __align__(16) SteepRec {
   double mux, muy, za, zb;
 };
-constexpr double kSteepLimit = 64.0;
+constexpr double kSteepLimit = 256.0;
 constexpr uint32_t kSteepBit = 0x80000000u;
 constexpr uint32_t kIndexMask = 0x7fffffffu;
 
@@ -51,8 +52,19 @@ constexpr uint32_t kIndexMask = 0x7fffffffu;
 constexpr int kRowFloats = 16;
 constexpr int kColSumDzZ = 12;
 
-__host__ __device__ __forceinline__ uint32_t pack_flags(int mode, bool steep, int spans_x) {
-  return (uint32_t)mode | (steep ? 4u : 0u) | ((uint32_t)spans_x << 3);
+constexpr uint32_t kFlagSteep = 4u;
+constexpr uint32_t kFlagClamp = 8u;
+constexpr int kFlagSpanShift = 4;
+// Splats whose weight can never reach the 0.99 clamp (c1 + |c2| bounds
+// (c1 + c2 E) g; 0.989 leaves room for FP32 rounding) skip the clamp and the
+// backward's gating test.
+__host__ __device__ __forceinline__ bool may_clamp(double c1, double c2) {
+  return c1 + fabs(c2) > 0.989;
+}
+__host__ __device__ __forceinline__ uint32_t pack_flags(int mode, bool steep, bool clamp,
+                                                        int spans_x) {
+  return (uint32_t)mode | (steep ? kFlagSteep : 0u) | (clamp ? kFlagClamp : 0u) |
+         ((uint32_t)spans_x << kFlagSpanShift);
 }
 __host__ __device__ __forceinline__ bool is_steep(double za, double zb, double reach) {
   return (fabs(za) + fabs(zb)) * reach > kSteepLimit;

@@ -167,11 +167,63 @@ __device__ __forceinline__ void matvec_blas(const double M[9], const double v[3]
     out[a] = fma(v[2], M[3 * a + 2], fma(v[1], M[3 * a + 1], v[0] * M[3 * a]));
 }
 
-template <int DEG, typename T>
-__device__ __forceinline__ void forward_state(const SceneArgs<T>& sc, const CamArgs& cam,
-                                              int kernel, int64_t i, FwdState& st) {
+// ---------------------------------------------------------------------------
+// Shared-memory staging of one CTA's primitives.  The scene is array-of-structs
+// per field ((N,3), (N,K,3), ...); a thread reading its own primitive would issue
+// ~60 scalar loads with 12..192-byte strides.  Instead the CTA copies its NT
+// primitives field by field with consecutive threads on consecutive elements
+// (fully coalesced), and every thread reads its own from shared memory.  SH rows
+// are padded to an odd stride (3K+1) so the per-thread reads are conflict-free.
+// K7 reuses the same slots to stage its gradient outputs for coalesced stores.
+template <typename T, int K, int NT>
+struct Staged {
+  static constexpr int SHS = 3 * K + 1;
+  T mu[NT * 3], ls[NT * 3], rot[NT * 4], nrm[NT * 3], ra[NT], rb[NT];
+  T sh[NT * SHS];
+};
+
+template <typename T, int K, int NT>
+__device__ __forceinline__ void stage_in(Staged<T, K, NT>& s, const SceneArgs<T>& sc,
+                                         int64_t base, int cnt) {
+  const int tid = threadIdx.x;
+  for (int e = tid; e < cnt * 3; e += NT) {
+    s.mu[e] = sc.mu[base * 3 + e];
+    s.ls[e] = sc.ls[base * 3 + e];
+    s.nrm[e] = sc.nrm[base * 3 + e];
+  }
+  for (int e = tid; e < cnt * 4; e += NT) s.rot[e] = sc.rot[base * 4 + e];
+  for (int e = tid; e < cnt; e += NT) {
+    s.ra[e] = sc.ra[base + e];
+    s.rb[e] = sc.rb[base + e];
+  }
+  for (int e = tid; e < cnt * 3 * K; e += NT) {
+    const int t = e / (3 * K), c = e - t * (3 * K);
+    s.sh[t * Staged<T, K, NT>::SHS + c] = sc.sh[base * 3 * K + e];
+  }
+  __syncthreads();
+}
+
+// One thread's view of its staged primitive (the inputs of forward_state).
+template <typename T, int K, int NT>
+struct StagedView {
+  const Staged<T, K, NT>& s;
+  int t;
+  __device__ __forceinline__ double mu(int k) const { return (double)s.mu[3 * t + k]; }
+  __device__ __forceinline__ double ls(int k) const { return (double)s.ls[3 * t + k]; }
+  __device__ __forceinline__ double rot(int k) const { return (double)s.rot[4 * t + k]; }
+  __device__ __forceinline__ double nrm(int k) const { return (double)s.nrm[3 * t + k]; }
+  __device__ __forceinline__ double ra() const { return (double)s.ra[t]; }
+  __device__ __forceinline__ double rb() const { return (double)s.rb[t]; }
+  __device__ __forceinline__ double sh(int k, int ch) const {
+    return (double)s.sh[t * Staged<T, K, NT>::SHS + 3 * k + ch];
+  }
+};
+
+template <int DEG, typename Src>
+__device__ __forceinline__ void forward_state(const Src& src, const CamArgs& cam, int kernel,
+                                              FwdState& st) {
   constexpr int K = (DEG + 1) * (DEG + 1);
-  const double m0 = ld(sc.mu, 3 * i), m1 = ld(sc.mu, 3 * i + 1), m2 = ld(sc.mu, 3 * i + 2);
+  const double m0 = src.mu(0), m1 = src.mu(1), m2 = src.mu(2);
   // t_all = mu @ rot.T + translation (rasterizer.py:170)
   {
     const double mv[3] = {m0, m1, m2};
@@ -182,7 +234,7 @@ __device__ __forceinline__ void forward_state(const SceneArgs<T>& sc, const CamA
   st.in_front = st.t[2] > cam.near_clip;
   // covariance build (rasterizer.py:174-179)
   double q[4];
-  for (int k = 0; k < 4; ++k) q[k] = ld(sc.rot, 4 * i + k);
+  for (int k = 0; k < 4; ++k) q[k] = src.rot(k);
   {
     double ss = 0.0;
     for (int k = 0; k < 4; ++k) ss += q[k] * q[k];
@@ -190,7 +242,7 @@ __device__ __forceinline__ void forward_state(const SceneArgs<T>& sc, const CamA
   }
   for (int k = 0; k < 4; ++k) st.qu[k] = q[k] / st.qnorm;
   quat_to_rot_ref(st.qu, st.R);
-  for (int k = 0; k < 3; ++k) st.s[k] = exp(ld(sc.ls, 3 * i + k));
+  for (int k = 0; k < 3; ++k) st.s[k] = exp(src.ls(k));
   double M[9];
   for (int r = 0; r < 3; ++r)
     for (int k = 0; k < 3; ++k) M[3 * r + k] = st.R[3 * r + k] * st.s[k];
@@ -259,7 +311,7 @@ __device__ __forceinline__ void forward_state(const SceneArgs<T>& sc, const CamA
   st.v10 = -st.L[3] * st.v00 * st.v11;
   // ray-space splitting normal (rasterizer.py:241-254)
   double nrm[3];
-  for (int k = 0; k < 3; ++k) nrm[k] = ld(sc.nrm, 3 * i + k);
+  for (int k = 0; k < 3; ++k) nrm[k] = src.nrm(k);
   st.nnorm = sqrt(nrm[0] * nrm[0] + nrm[1] * nrm[1] + nrm[2] * nrm[2]);
   for (int k = 0; k < 3; ++k) st.nu[k] = nrm[k] / st.nnorm;
   double hw[3];
@@ -278,8 +330,8 @@ __device__ __forceinline__ void forward_state(const SceneArgs<T>& sc, const CamA
     for (int k = 0; k < 3; ++k) st.nray[k] = st.y[k] / st.ynorm;
   }
   // opacities, blend mode, erf coefficients (rasterizer.py:256-277)
-  st.a1 = sigmoid_ref(ld(sc.ra, i));
-  st.a2 = sigmoid_ref(ld(sc.rb, i));
+  st.a1 = sigmoid_ref(src.ra());
+  st.a2 = sigmoid_ref(src.rb());
   st.c1 = 0.5 * (st.a1 + st.a2);
   if (kernel == 1) {
     st.c2 = 0.0;
@@ -307,7 +359,7 @@ __device__ __forceinline__ void forward_state(const SceneArgs<T>& sc, const CamA
   for (int ch = 0; ch < 3; ++ch) {
     double acc = 0.0;
 #pragma unroll
-    for (int k = 0; k < K; ++k) acc += st.basis[k] * ld(sc.sh, (i * K + k) * 3 + ch);
+    for (int k = 0; k < K; ++k) acc += st.basis[k] * src.sh(k, ch);
     st.rgbu[ch] = acc + 0.5;
   }
 }
@@ -315,15 +367,21 @@ __device__ __forceinline__ void forward_state(const SceneArgs<T>& sc, const CamA
 // ---------------------------------------------------------------------------
 // K1: preprocess forward.  Writes the 64-B record, tile rect, pair count and
 // the depth-rank sort key of each primitive (culled: count 0, key ~0).
-template <typename T, int DEG>
-__global__ void __launch_bounds__(128) preprocess_fwd_kernel(
+template <typename T, int DEG, int NT>
+__global__ void __launch_bounds__(NT) preprocess_fwd_kernel(
     SceneArgs<T> sc, CamArgs cam, int kernel, int64_t n, float4* __restrict__ rec,
     SteepRec* __restrict__ side, int4* __restrict__ rect, int32_t* __restrict__ count,
     uint64_t* __restrict__ dkey, uint32_t* __restrict__ dval, int32_t* __restrict__ radii) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+  constexpr int K = (DEG + 1) * (DEG + 1);
+  __shared__ Staged<T, K, NT> sm;
+  const int64_t base = (int64_t)blockIdx.x * NT;
+  const int cnt = (int)(n - base < NT ? n - base : NT);
+  stage_in(sm, sc, base, cnt);
+  const int t = threadIdx.x;
+  if (t >= cnt) return;
+  const int64_t i = base + t;
   FwdState st;
-  forward_state<DEG>(sc, cam, kernel, i, st);
+  forward_state<DEG>(StagedView<T, K, NT>{sm, t}, cam, kernel, st);
   if (!st.visible) {
     dval[i] = (uint32_t)i;
     count[i] = 0;
@@ -349,7 +407,7 @@ __global__ void __launch_bounds__(128) preprocess_fwd_kernel(
   float4 r1 = make_float4((float)(st.a / st.det), (float)st.za, (float)st.zb, (float)st.c1);
   float4 r2 = make_float4((float)st.c2, (float)fmax(st.rgbu[0], 0.0), (float)fmax(st.rgbu[1], 0.0),
                           (float)fmax(st.rgbu[2], 0.0));
-  float4 r3 = make_float4((float)st.t[2], __uint_as_float(pack_flags(st.mode, steep, spans_x)),
+  float4 r3 = make_float4((float)st.t[2], __uint_as_float(pack_flags(st.mode, steep, may_clamp(st.c1, st.c2), spans_x)),
                           __uint_as_float(0u), __uint_as_float(*reinterpret_cast<const uint32_t*>(&lo)));
   float4* dst = rec + 4 * i;
   dst[0] = r0;
@@ -362,29 +420,25 @@ __global__ void __launch_bounds__(128) preprocess_fwd_kernel(
 // K7: merge the splat's pair rows (np.add.at, rasterizer.py:419-420) and chain
 // them through the projection to the primitive parameters
 // (_geometry_backward, rasterizer.py:424-575).  FP64 throughout.
-template <typename T, int DEG>
-__global__ void __launch_bounds__(128) preprocess_bwd_kernel(
-    SceneArgs<T> sc, CamArgs cam, int kernel, int64_t n, int tiles_x,
-    const float4* __restrict__ rec, const int4* __restrict__ rect,
-    const int32_t* __restrict__ count, const uint32_t* __restrict__ rank_of,
-    const int32_t* __restrict__ last_rank, const float* __restrict__ rows,
-    GradArgs<T> out) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+// K7 body for one primitive: reads its staged inputs, overwrites the same
+// slots with its gradients (each thread touches only its own slots).
+template <typename T, int DEG, int NT>
+__device__ __forceinline__ void preprocess_bwd_one(
+    Staged<T, (DEG + 1) * (DEG + 1), NT>& sm, T* pgn_s, int32_t* touch_s, int t, int64_t i,
+    const CamArgs& cam, int kernel, int tiles_x, const float4* __restrict__ rec,
+    const int4* __restrict__ rect, const int32_t* __restrict__ count,
+    const uint32_t* __restrict__ rank_of, const int32_t* __restrict__ last_rank,
+    const float* __restrict__ rows) {
   constexpr int K = (DEG + 1) * (DEG + 1);
+  using St = Staged<T, K, NT>;
   const int cnt = count[i];
   if (cnt == 0) {
-    for (int k = 0; k < 3; ++k) {
-      out.d_mu[3 * i + k] = T(0);
-      out.d_log_scale[3 * i + k] = T(0);
-      out.d_normal[3 * i + k] = T(0);
-    }
-    for (int k = 0; k < 4; ++k) out.d_rotation[4 * i + k] = T(0);
-    for (int k = 0; k < 3 * K; ++k) out.d_sh[3 * K * i + k] = T(0);
-    out.d_ra[i] = T(0);
-    out.d_rb[i] = T(0);
-    out.pos_grad_norm[i] = T(0);
-    out.touch[i] = 0;
+    for (int k = 0; k < 3; ++k) sm.mu[3 * t + k] = sm.ls[3 * t + k] = sm.nrm[3 * t + k] = T(0);
+    for (int k = 0; k < 4; ++k) sm.rot[4 * t + k] = T(0);
+    for (int k = 0; k < 3 * K; ++k) sm.sh[t * St::SHS + k] = T(0);
+    sm.ra[t] = sm.rb[t] = T(0);
+    pgn_s[t] = T(0);
+    touch_s[t] = 0;
     return;
   }
   // ---- merge pair rows: tiles of the rect in row-major (= sorted k) order,
@@ -410,7 +464,7 @@ __global__ void __launch_bounds__(128) preprocess_bwd_kernel(
     }
   }
   FwdState st;
-  forward_state<DEG>(sc, cam, kernel, i, st);
+  forward_state<DEG>(StagedView<T, K, NT>{sm, t}, cam, kernel, st);
 
   const double d_mux = m[0], d_muy = m[1];
   const double d_ca = m[2], d_cb = m[3], d_cc = m[4];
@@ -420,8 +474,8 @@ __global__ void __launch_bounds__(128) preprocess_bwd_kernel(
   // opacities (rasterizer.py:446-450)
   {
     const double d_a1 = 0.5 * (d_c1 + d_c2), d_a2 = 0.5 * (d_c1 - d_c2);
-    out.d_ra[i] = T(d_a1 * st.a1 * (1.0 - st.a1));
-    out.d_rb[i] = T(d_a2 * st.a2 * (1.0 - st.a2));
+    sm.ra[t] = T(d_a1 * st.a1 * (1.0 - st.a1));
+    sm.rb[t] = T(d_a2 * st.a2 * (1.0 - st.a2));
   }
   // erf coefficients -> n_ray and whitening (rasterizer.py:452-466)
   const bool mode0 = st.mode == kModeErf;
@@ -569,20 +623,21 @@ __global__ void __launch_bounds__(128) preprocess_bwd_kernel(
   {
     double dpre[3];
     for (int ch = 0; ch < 3; ++ch) dpre[ch] = st.rgbu[ch] > 0.0 ? d_rgb[ch] : 0.0;
-    for (int k = 0; k < K; ++k)
-      for (int ch = 0; ch < 3; ++ch) out.d_sh[3 * K * i + 3 * k + ch] = T(st.basis[k] * dpre[ch]);
     if (DEG > 0) {
       double g[48];
       sh_basis_grad(st.vdir, DEG, g);
       double d_dir[3] = {0.0, 0.0, 0.0};
       for (int k = 0; k < K; ++k) {
         double db = 0.0;
-        for (int ch = 0; ch < 3; ++ch) db += ld(sc.sh, (i * K + k) * 3 + ch) * dpre[ch];
+        for (int ch = 0; ch < 3; ++ch) db += (double)sm.sh[t * St::SHS + 3 * k + ch] * dpre[ch];
         for (int d = 0; d < 3; ++d) d_dir[d] += db * g[3 * k + d];
       }
       const double dot = d_dir[0] * st.vdir[0] + d_dir[1] * st.vdir[1] + d_dir[2] * st.vdir[2];
       for (int d = 0; d < 3; ++d) d_mu[d] += (d_dir[d] - dot * st.vdir[d]) / st.vdist;
     }
+    // d_sh overwrites this thread's staged SH row (read above for d_basis)
+    for (int k = 0; k < K; ++k)
+      for (int ch = 0; ch < 3; ++ch) sm.sh[t * St::SHS + 3 * k + ch] = T(st.basis[k] * dpre[ch]);
   }
   // covariance build: cov = M M^T, M = R diag(s) (rasterizer.py:555-562)
   {
@@ -603,7 +658,7 @@ __global__ void __launch_bounds__(128) preprocess_bwd_kernel(
         dR[3 * r + k] = dM[3 * r + k] * st.s[k];
         d_s[k] += dM[3 * r + k] * st.R[3 * r + k];
       }
-    for (int k = 0; k < 3; ++k) out.d_log_scale[3 * i + k] = T(d_s[k] * st.s[k]);
+    for (int k = 0; k < 3; ++k) sm.ls[3 * t + k] = T(d_s[k] * st.s[k]);
     // quat_rot_vjp (geometry.py:76-107) at the unit quaternion
     const double w = st.qu[0], x = st.qu[1], y = st.qu[2], z = st.qu[3];
     const double Dw[9] = {0, -z, y, z, 0, -x, -y, x, 0};
@@ -618,17 +673,58 @@ __global__ void __launch_bounds__(128) preprocess_bwd_kernel(
       dq[3] += 2 * Dz[k] * dR[k];
     }
     const double dot = dq[0] * w + dq[1] * x + dq[2] * y + dq[3] * z;
-    for (int k = 0; k < 4; ++k) out.d_rotation[4 * i + k] = T((dq[k] - dot * st.qu[k]) / st.qnorm);
+    for (int k = 0; k < 4; ++k) sm.rot[4 * t + k] = T((dq[k] - dot * st.qu[k]) / st.qnorm);
   }
   // splitting normal through its normalisation (rasterizer.py:565-566)
   {
     const double dot = d_nu[0] * st.nu[0] + d_nu[1] * st.nu[1] + d_nu[2] * st.nu[2];
-    for (int k = 0; k < 3; ++k) out.d_normal[3 * i + k] = T((d_nu[k] - dot * st.nu[k]) / st.nnorm);
+    for (int k = 0; k < 3; ++k) sm.nrm[3 * t + k] = T((d_nu[k] - dot * st.nu[k]) / st.nnorm);
   }
-  for (int k = 0; k < 3; ++k) out.d_mu[3 * i + k] = T(d_mu[k]);
-  out.pos_grad_norm[i] = T(sqrt(d_mux * d_mux + d_muy * d_muy));
-  out.touch[i] = 1;
+  for (int k = 0; k < 3; ++k) sm.mu[3 * t + k] = T(d_mu[k]);
+  pgn_s[t] = T(sqrt(d_mux * d_mux + d_muy * d_muy));
+  touch_s[t] = 1;
 }
+
+template <typename T, int DEG, int NT>
+__global__ void __launch_bounds__(NT) preprocess_bwd_kernel(
+    SceneArgs<T> sc, CamArgs cam, int kernel, int64_t n, int tiles_x,
+    const float4* __restrict__ rec, const int4* __restrict__ rect,
+    const int32_t* __restrict__ count, const uint32_t* __restrict__ rank_of,
+    const int32_t* __restrict__ last_rank, const float* __restrict__ rows,
+    GradArgs<T> out) {
+  constexpr int K = (DEG + 1) * (DEG + 1);
+  using St = Staged<T, K, NT>;
+  __shared__ St sm;
+  __shared__ T pgn_s[NT];
+  __shared__ int32_t touch_s[NT];
+  const int64_t base = (int64_t)blockIdx.x * NT;
+  const int ncta = (int)(n - base < NT ? n - base : NT);
+  stage_in(sm, sc, base, ncta);
+  const int t = threadIdx.x;
+  if (t < ncta) preprocess_bwd_one<T, DEG, NT>(sm, pgn_s, touch_s, t, base + t, cam, kernel,
+                                               tiles_x, rec, rect, count, rank_of, last_rank,
+                                               rows);
+  __syncthreads();
+  // coalesced stores of the staged gradients
+  for (int e = t; e < ncta * 3; e += NT) {
+    out.d_mu[base * 3 + e] = sm.mu[e];
+    out.d_log_scale[base * 3 + e] = sm.ls[e];
+    out.d_normal[base * 3 + e] = sm.nrm[e];
+  }
+  for (int e = t; e < ncta * 4; e += NT) out.d_rotation[base * 4 + e] = sm.rot[e];
+  for (int e = t; e < ncta; e += NT) {
+    out.d_ra[base + e] = sm.ra[e];
+    out.d_rb[base + e] = sm.rb[e];
+    out.pos_grad_norm[base + e] = pgn_s[e];
+    out.touch[base + e] = touch_s[e];
+  }
+  for (int e = t; e < ncta * 3 * K; e += NT) {
+    const int tt = e / (3 * K), c = e - tt * (3 * K);
+    out.d_sh[base * 3 * K + e] = sm.sh[tt * St::SHS + c];
+  }
+}
+
+
 
 // ---------------------------------------------------------------------------
 template <typename T>
@@ -636,14 +732,15 @@ cudaError_t launch_preprocess_fwd_t(const SceneArgs<T>& sc, const CamArgs& cam, 
                                     int64_t n, float4* rec, SteepRec* side, int4* rect,
                                     int32_t* count, uint64_t* dkey, uint32_t* dval,
                                     int32_t* radii, cudaStream_t stream) {
-  const int block = 128;
-  const int64_t grid = (n + block - 1) / block;
+  // staging holds NT primitives in shared memory: 128 float or 64 double ones
+  constexpr int NT = sizeof(T) == 4 ? 128 : 64;
+  const int64_t grid = (n + NT - 1) / NT;
   switch (sc.deg) {
-#define HS_K1(D)                                                                              \
-  case D:                                                                                     \
-    preprocess_fwd_kernel<T, D><<<(unsigned)grid, block, 0, stream>>>(sc, cam, kernel, n, rec, \
-                                                                      side, rect, count, dkey, \
-                                                                      dval, radii);           \
+#define HS_K1(D)                                                                               \
+  case D:                                                                                      \
+    preprocess_fwd_kernel<T, D, NT><<<(unsigned)grid, NT, 0, stream>>>(sc, cam, kernel, n, rec, \
+                                                                       side, rect, count, dkey, \
+                                                                       dval, radii);           \
     break;
     HS_K1(0) HS_K1(1) HS_K1(2) HS_K1(3)
 #undef HS_K1
@@ -659,12 +756,12 @@ cudaError_t launch_preprocess_bwd_t(const SceneArgs<T>& sc, const CamArgs& cam, 
                                     const int32_t* count, const uint32_t* rank_of,
                                     const int32_t* last_rank, const float* rows,
                                     const GradArgs<T>& out, cudaStream_t stream) {
-  const int block = 128;
-  const int64_t grid = (n + block - 1) / block;
+  constexpr int NT = sizeof(T) == 4 ? 128 : 64;
+  const int64_t grid = (n + NT - 1) / NT;
   switch (sc.deg) {
 #define HS_K7(D)                                                                               \
   case D:                                                                                      \
-    preprocess_bwd_kernel<T, D><<<(unsigned)grid, block, 0, stream>>>(                         \
+    preprocess_bwd_kernel<T, D, NT><<<(unsigned)grid, NT, 0, stream>>>(                        \
         sc, cam, kernel, n, tiles_x, rec, rect, count, rank_of, last_rank, rows, out);         \
     break;
     HS_K7(0) HS_K7(1) HS_K7(2) HS_K7(3)
