@@ -308,6 +308,7 @@ def main():
                       "achieved_tflops": fwd_evals * FWD_FLOPS_PER_EVAL / (fwd_k_ms * 1e-3) / 1e12},
         "stage_ms": stage_ms,
         "ex2_gops_peak": b.value,
+        "fma2_tflops_peak": lib.hs_last_fma2_tflops(),
     }
 
     # end-to-end through the drop-in numpy API, host buffers, copies inside

@@ -193,6 +193,9 @@ int32_t hs_abi_version(void);
  * current device, measured by two probe kernels: the roofline denominators for
  * the FP32/SFU-bound blend kernels. */
 int hs_measure_fp32_peaks(double* fma_tflops, double* ex2_gops);
+/* Packed FP32 (fma.rn.f32x2) throughput measured by the last
+ * hs_measure_fp32_peaks call, TFLOP/s. */
+double hs_last_fma2_tflops(void);
 
 #ifdef __cplusplus
 }

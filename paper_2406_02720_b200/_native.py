@@ -103,6 +103,7 @@ _SIGNATURES = {
     "hs_abi_version": (c_int32, []),
     "hs_measure_fp32_peaks": (c_int32, [ctypes.POINTER(ctypes.c_double),
                                         ctypes.POINTER(ctypes.c_double)]),
+    "hs_last_fma2_tflops": (ctypes.c_double, []),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGNATURES)

@@ -111,16 +111,47 @@ __device__ __forceinline__ SplatLane splat_lane(const float4 (&q)[4], const Stee
   return s;
 }
 
-// erf argument z for the 8 pixels of a lane: FP32 for ordinary splats, FP64
-// (side record) for steep ones.
-__device__ __forceinline__ void erf_args(const SplatLane& s, bool steep, float (&z)[kPx]) {
-  if (steep) {
-#pragma unroll
-    for (int i = 0; i < kPx; ++i) z[i] = (float)fma(s.zbd, (s.py0d + 2.0 * i) - s.muyd, s.Z0d);
-  } else {
-#pragma unroll
-    for (int i = 0; i < kPx; ++i) z[i] = fmaf(s.zb, s.dy0 + 2.0f * i, s.Z0);
-  }
+// Pixel pairs.  Lane pixel i (row offset 2i) lives in pair i>>1, slot i&1, so
+// every per-pixel quantity is a float2 and the fast paths run on the packed
+// FP32 pipe instructions of sm_100 (FFMA2/FMUL2/FADD2: one issue slot for two
+// pixels; negated, broadcast-scalar and immediate operands fold into the
+// instruction).  The MUFU ops (ex2, rcp) stay scalar.
+constexpr int kPairs = kPx / 2;
+__device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
+__device__ __forceinline__ float2 neg2(float2 a) { return make_float2(-a.x, -a.y); }
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 ex2x2(float2 x) {
+  return make_float2(ex2_approx(x.x), ex2_approx(x.y));
+}
+__device__ __forceinline__ float& slot(float2& v, int h) { return h ? v.y : v.x; }
+__device__ __forceinline__ float slot(const float2& v, int h) { return h ? v.y : v.x; }
+
+// erf32 on a pixel pair: same arithmetic as erf32 (fma.rn per lane), so the
+// packed and scalar paths agree bit for bit.
+__device__ __forceinline__ float2 erf32x2(float2 z) {
+  const float2 a = make_float2(fminf(fabsf(z.x), 3.92f), fminf(fabsf(z.y), 3.92f));
+  float2 r = ffma2(f2(1.420475164e-04f), a, f2(-3.664300777e-03f));
+  r = ffma2(r, a, f2(3.089622408e-02f));
+  r = ffma2(r, a, f2(-1.496994644e-01f));
+  r = ffma2(r, a, f2(-9.181654453e-01f));
+  r = ffma2(r, a, f2(-1.627925038e+00f));
+  r = fmul2(r, a);
+  const float2 om = fadd2(f2(1.0f), neg2(ex2x2(r)));
+  return make_float2(copysignf(om.x, z.x), copysignf(om.y, z.y));
+}
+
+// dy of pair p: rows (row0 + 4p, row0 + 4p + 2)
+__device__ __forceinline__ float2 pair_dy(float dy0, int p) {
+  return fadd2(f2(dy0), make_float2(4.0f * p, 4.0f * p + 2.0f));
+}
+
+// erf argument z of pixel i: FP32 for ordinary splats, FP64 (side record) for
+// steep ones.
+__device__ __forceinline__ float erf_arg(const SplatLane& s, bool steep, int i) {
+  if (steep) return (float)fma(s.zbd, (s.py0d + 2.0 * i) - s.muyd, s.Z0d);
+  return fmaf(s.zb, s.dy0 + 2.0f * i, s.Z0);
 }
 
 // Blend factor E of the three modes (_blend_cy.pyx:156-161); mode 2 records
@@ -129,60 +160,91 @@ __device__ __forceinline__ float mode_factor(int mode, float z) {
   return mode == kModeSign ? sign32(z) : erf32(z);
 }
 
+__device__ __forceinline__ bool fast_flags(uint32_t flags) {
+  return (flags & (kFlagSteep | kFlagClamp)) == 0 && (flags & 3u) != (uint32_t)kModeSign;
+}
+
 // ---------------------------------------------------------------------------
 // K5 forward.  Live pixels hold T > 0.  A pixel that terminates stores -T (its
 // final transmittance, sign flipped); from then on T*(1-w) <= 0 never passes the
 // termination test, so no separate alive mask is needed.  Pixels outside the
-// image start at T = -1.  Branch-free over the 8 pixels (selects only) so the
-// compiler interleaves the eight independent chains; dead pixels compute and
-// discard.
-//
-// FAST: mode 0 or 2, FP32 erf argument, weight provably below the 0.99 clamp
-// (the common case); otherwise every feature is resolved from `flags` at run
-// time.
-template <bool FAST>
-__device__ __forceinline__ void fwd_splat(const float4 (&q)[4], const SteepRec& side,
-                                          uint32_t flags, float px, float py0, float (&T)[kPx],
-                                          float (&ar)[kPx], float (&ag)[kPx], float (&ab)[kPx],
-                                          float (&ad)[kPx], int (&cnt)[kPx]) {
-  const bool steep = !FAST && (flags & kFlagSteep);
+// image start at T = -1.  The colour/depth accumulators hold the NEGATED sums
+// (T - w*T = fma(-w, T, T) needs -w; the sign is restored at the store).
+// Branch-free over the pixels (selects only); dead pixels compute and discard.
+struct FwdPix {
+  float2 T[kPairs], ar[kPairs], ag[kPairs], ab[kPairs], ad[kPairs];
+  int cnt[kPx];
+};
+
+// one pixel: the termination rule and compositing of _blend_cy.pyx:162-176
+__device__ __forceinline__ void fwd_commit(float nw, float& T, float& ar, float& ag, float& ab,
+                                           float& ad, int& cnt, float cr, float cg, float cb,
+                                           float z) {
+  const float tn = fmaf(nw, T, T);  // T * (1 - w)
+  const bool commit = tn >= kTerminationT;
+  const float nwt = commit ? nw * T : 0.0f;
+  ar = fmaf(nwt, cr, ar);
+  ag = fmaf(nwt, cg, ag);
+  ab = fmaf(nwt, cb, ab);
+  ad = fmaf(nwt, z, ad);
+  cnt += commit ? 1 : 0;
+  T = commit ? tn : -fabsf(T);
+}
+
+// FAST: mode 0 or 2, FP32 erf argument, weight provably below the 0.99 clamp.
+__device__ __forceinline__ void fwd_splat_fast(const float4 (&q)[4], float px, float py0,
+                                               FwdPix& P) {
+  const SteepRec none{};
+  const SplatLane s = splat_lane<false>(q, none, px, py0);
+  const float nc1 = -q[1].w, nc2 = -q[2].x;
+  const float cr = q[2].y, cg = q[2].z, cb = q[2].w, z = q[3].x;
+#pragma unroll
+  for (int p = 0; p < kPairs; ++p) {
+    const float2 dy = pair_dy(s.dy0, p);
+    const float2 g = ex2x2(ffma2(ffma2(f2(s.C), dy, f2(s.Bx)), dy, f2(s.P0)));
+    const float2 e = erf32x2(ffma2(f2(s.zb), dy, f2(s.Z0)));
+    const float2 nw = fmul2(ffma2(f2(nc2), e, f2(nc1)), g);  // -w
+    const float2 tn = ffma2(nw, P.T[p], P.T[p]);              // T * (1 - w)
+    const float2 nwT = fmul2(nw, P.T[p]);
+    const bool cx = tn.x >= kTerminationT, cy = tn.y >= kTerminationT;
+    const float2 nwt = make_float2(cx ? nwT.x : 0.0f, cy ? nwT.y : 0.0f);
+    P.ar[p] = ffma2(nwt, f2(cr), P.ar[p]);
+    P.ag[p] = ffma2(nwt, f2(cg), P.ag[p]);
+    P.ab[p] = ffma2(nwt, f2(cb), P.ab[p]);
+    P.ad[p] = ffma2(nwt, f2(z), P.ad[p]);
+    P.cnt[2 * p] += cx ? 1 : 0;
+    P.cnt[2 * p + 1] += cy ? 1 : 0;
+    P.T[p] = make_float2(cx ? tn.x : -fabsf(P.T[p].x), cy ? tn.y : -fabsf(P.T[p].y));
+  }
+}
+
+// Generic: steep (FP64 z), sign mode, clamped weights; scalar per pixel.
+__device__ __forceinline__ void fwd_splat_generic(const float4 (&q)[4], const SteepRec& side,
+                                                  uint32_t flags, float px, float py0,
+                                                  FwdPix& P) {
+  const bool steep = flags & kFlagSteep;
   const SplatLane s = steep ? splat_lane<true>(q, side, px, py0)
                             : splat_lane<false>(q, side, px, py0);
   const int mode = (int)(flags & 3u);
   const float c1 = q[1].w, c2 = q[2].x;
   const float cr = q[2].y, cg = q[2].z, cb = q[2].w, z = q[3].x;
-  float zz[kPx];
-  erf_args(s, steep, zz);
 #pragma unroll
   for (int i = 0; i < kPx; ++i) {
+    const int p = i >> 1, h = i & 1;
     const float dy = s.dy0 + 2.0f * i;
     const float g = ex2_approx(fmaf(fmaf(s.C, dy, s.Bx), dy, s.P0));
-    const float e = FAST ? erf32(zz[i]) : mode_factor(mode, zz[i]);
-    float w = fmaf(c2, e, c1) * g;
-    if (!FAST) w = fminf(w, kWeightClamp);
-    const float wT = w * T[i];
-    const float tn = T[i] - wT;  // T * (1 - w)
-    // the pixel terminates *before* compositing this splat (_blend_cy.pyx:165-169)
-    const bool commit = tn >= kTerminationT;
-    const float wt = commit ? wT : 0.0f;
-    ar[i] = fmaf(wt, cr, ar[i]);
-    ag[i] = fmaf(wt, cg, ag[i]);
-    ab[i] = fmaf(wt, cb, ab[i]);
-    ad[i] = fmaf(wt, z, ad[i]);
-    cnt[i] += commit ? 1 : 0;
-    T[i] = commit ? tn : -fabsf(T[i]);
+    const float e = mode_factor(mode, erf_arg(s, steep, i));
+    const float w = fminf(fmaf(c2, e, c1) * g, kWeightClamp);
+    fwd_commit(-w, slot(P.T[p], h), slot(P.ar[p], h), slot(P.ag[p], h), slot(P.ab[p], h),
+               slot(P.ad[p], h), P.cnt[i], cr, cg, cb, z);
   }
 }
 
-__device__ __forceinline__ bool warp_any_alive(const float (&T)[kPx]) {
-  float m = T[0];
+__device__ __forceinline__ bool warp_any_alive(const FwdPix& P) {
+  float m = fmaxf(P.T[0].x, P.T[0].y);
 #pragma unroll
-  for (int i = 1; i < kPx; ++i) m = fmaxf(m, T[i]);
+  for (int p = 1; p < kPairs; ++p) m = fmaxf(m, fmaxf(P.T[p].x, P.T[p].y));
   return __any_sync(0xffffffffu, m > 0.0f);
-}
-
-__device__ __forceinline__ bool fast_flags(uint32_t flags) {
-  return (flags & (kFlagSteep | kFlagClamp)) == 0 && (flags & 3u) != (uint32_t)kModeSign;
 }
 
 __global__ void __launch_bounds__(kWarpsPerCta * 32) blend_fwd_kernel(
@@ -200,12 +262,14 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) blend_fwd_kernel(
     const int row0 = ty * kTile + (lane >> 4);
     const float px = (float)col + 0.5f;
     const float py0 = (float)row0 + 0.5f;
-    float T[kPx], ar[kPx], ag[kPx], ab[kPx], ad[kPx];
-    int cnt[kPx];
+    FwdPix P;
 #pragma unroll
     for (int i = 0; i < kPx; ++i) {
-      T[i] = (col < g.width && row0 + 2 * i < g.height) ? 1.f : -1.f;
-      ar[i] = 0.f; ag[i] = 0.f; ab[i] = 0.f; ad[i] = 0.f; cnt[i] = 0;
+      const int p = i >> 1, h = i & 1;
+      slot(P.T[p], h) = (col < g.width && row0 + 2 * i < g.height) ? 1.f : -1.f;
+      slot(P.ar[p], h) = 0.f; slot(P.ag[p], h) = 0.f; slot(P.ab[p], h) = 0.f;
+      slot(P.ad[p], h) = 0.f;
+      P.cnt[i] = 0;
     }
     const int k0 = g.tile_starts[tile];
     const int nk = g.tile_starts[tile + 1] - k0;
@@ -225,13 +289,13 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) blend_fwd_kernel(
       for (int j = 0; j < nb; ++j) {
         // dead pixels never change again: stop once the whole tile is dead
         // (checked every 8 splats; the reference checks per splat, same result)
-        if ((j & 7) == 0 && !(any = warp_any_alive(T))) break;
+        if ((j & 7) == 0 && !(any = warp_any_alive(P))) break;
         const float4 q[4] = {st.rec[s][j][0], st.rec[s][j][1], st.rec[s][j][2], st.rec[s][j][3]};
         const uint32_t flags = __float_as_uint(q[3].y);
         if (fast_flags(flags))
-          fwd_splat<true>(q, st.side[s][j], flags, px, py0, T, ar, ag, ab, ad, cnt);
+          fwd_splat_fast(q, px, py0, P);
         else
-          fwd_splat<false>(q, st.side[s][j], flags, px, py0, T, ar, ag, ab, ad, cnt);
+          fwd_splat_generic(q, st.side[s][j], flags, px, py0, P);
       }
       __syncwarp();
     }
@@ -239,17 +303,18 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) blend_fwd_kernel(
     __syncwarp();
 #pragma unroll
     for (int i = 0; i < kPx; ++i) {
+      const int p = i >> 1, h = i & 1;
       const int row = row0 + 2 * i;
       if (col < g.width && row < g.height) {
-        const size_t p = (size_t)row * g.width + col;
-        const float t = fabsf(T[i]);
-        color[3 * p + 0] = fmaf(t, bg0, ar[i]);
-        color[3 * p + 1] = fmaf(t, bg1, ag[i]);
-        color[3 * p + 2] = fmaf(t, bg2, ab[i]);
-        alpha[p] = 1.0f - t;
-        depth[p] = ad[i];
-        trans[p] = t;
-        terminal[p] = cnt[i];
+        const size_t o = (size_t)row * g.width + col;
+        const float t = fabsf(slot(P.T[p], h));
+        color[3 * o + 0] = fmaf(t, bg0, -slot(P.ar[p], h));
+        color[3 * o + 1] = fmaf(t, bg1, -slot(P.ag[p], h));
+        color[3 * o + 2] = fmaf(t, bg2, -slot(P.ab[p], h));
+        alpha[o] = 1.0f - t;
+        depth[o] = -slot(P.ad[p], h);
+        trans[o] = t;
+        terminal[o] = P.cnt[i];
       }
     }
   }
@@ -263,46 +328,99 @@ struct BwdAcc {
   float c1, c2, r, g, b;
 };
 
-// FAST: as in the forward, plus every pixel of the warp active at this position
-// (pos < warp-min of the terminal counts), so the activity selects vanish.
-// Inactive pixels (generic path) compute and contribute exact zeros.
-template <bool FAST>
-__device__ __forceinline__ void bwd_splat(const float4 (&q)[4], const SteepRec& side,
-                                          uint32_t flags, int pos, float px, float py0,
-                                          float (&T)[kPx], float (&D)[kPx],
-                                          const float (&dr)[kPx], const float (&dg)[kPx],
-                                          const float (&db)[kPx], const int (&cnt)[kPx],
-                                          BwdAcc& a) {
-  const bool steep = !FAST && (flags & kFlagSteep);
+struct BwdPix {
+  float2 T[kPairs], D[kPairs], dr[kPairs], dg[kPairs], db[kPairs];
+  int cnt[kPx];
+};
+
+// FAST: mode 0 or 2, FP32 z, no clamp, and every pixel of the warp active at
+// this position (pos < warp-min of the terminal counts).  Packed pixel pairs.
+__device__ __forceinline__ void bwd_splat_fast(const float4 (&q)[4], float px, float py0,
+                                               BwdPix& P, BwdAcc& out) {
+  const SteepRec none{};
+  const SplatLane s = splat_lane<false>(q, none, px, py0);
+  const float c1 = q[1].w, c2 = q[2].x;
+  const float cr = q[2].y, cg = q[2].z, cb = q[2].w;
+  float2 s0 = f2(0.f), s1 = f2(0.f), s2 = f2(0.f), q0 = f2(0.f), q1 = f2(0.f), qz = f2(0.f);
+  float2 a1 = f2(0.f), a2 = f2(0.f), ar = f2(0.f), ag = f2(0.f), ab = f2(0.f);
+#pragma unroll
+  for (int p = 0; p < kPairs; ++p) {
+    const float2 dy = pair_dy(s.dy0, p);
+    const float2 gg = ex2x2(ffma2(ffma2(f2(s.C), dy, f2(s.Bx)), dy, f2(s.P0)));
+    const float2 zz = ffma2(f2(s.zb), dy, f2(s.Z0));
+    const float2 e = erf32x2(zz);
+    const float2 u = ffma2(f2(c2), e, f2(c1));
+    const float2 w = fmul2(u, gg);
+    const float2 om = fadd2(f2(1.0f), neg2(w));
+    const float2 inv = make_float2(rcp_approx(om.x), rcp_approx(om.y));  // 1 - w >= 0.01
+    const float2 Tp = fmul2(P.T[p], inv);
+    const float2 wt = fmul2(w, Tp);
+    const float2 dcr = ffma2(P.dr[p], f2(cr), ffma2(P.dg[p], f2(cg), fmul2(P.db[p], f2(cb))));
+    ar = ffma2(P.dr[p], wt, ar);
+    ag = ffma2(P.dg[p], wt, ag);
+    ab = ffma2(P.db[p], wt, ab);
+    // d_w = T_prev*(dC.rgb) - (dC.S)/(1-w) = inv*(T*dcr - D) (_blend_cy.pyx:310-312)
+    const float2 d_w = fmul2(inv, ffma2(P.T[p], dcr, neg2(P.D[p])));
+    const float2 dwg = fmul2(d_w, gg);
+    const float2 d_pow = fmul2(dwg, u);
+    s0 = fadd2(s0, d_pow);
+    s1 = ffma2(d_pow, dy, s1);
+    s2 = ffma2(fmul2(d_pow, dy), dy, s2);
+    a1 = fadd2(a1, dwg);
+    a2 = ffma2(dwg, e, a2);
+    // d_z / c2k (the constant factor is applied once per splat below)
+    const float2 ez = ex2x2(fmul2(fmul2(zz, zz), f2(-kLog2e)));
+    const float2 dz = fmul2(dwg, ez);
+    q0 = fadd2(q0, dz);
+    q1 = ffma2(dz, dy, q1);
+    qz = ffma2(dz, zz, qz);
+    P.D[p] = ffma2(wt, dcr, P.D[p]);
+    P.T[p] = Tp;
+  }
+  const float c2k = c2 * (2.0f * kInvSqrtPi);
+  out.s0 = s0.x + s0.y; out.s1 = s1.x + s1.y; out.s2 = s2.x + s2.y;
+  out.q0 = c2k * (q0.x + q0.y); out.q1 = c2k * (q1.x + q1.y); out.qz = c2k * (qz.x + qz.y);
+  out.c1 = a1.x + a1.y; out.c2 = a2.x + a2.y;
+  out.r = ar.x + ar.y; out.g = ag.x + ag.y; out.b = ab.x + ab.y;
+}
+
+// Generic: steep, sign mode, clamped weights, partially active warps.  Scalar;
+// inactive pixels compute and contribute exact zeros.
+__device__ __forceinline__ void bwd_splat_generic(const float4 (&q)[4], const SteepRec& side,
+                                                  uint32_t flags, int pos, float px, float py0,
+                                                  BwdPix& P, BwdAcc& a) {
+  const bool steep = flags & kFlagSteep;
   const SplatLane s = steep ? splat_lane<true>(q, side, px, py0)
                             : splat_lane<false>(q, side, px, py0);
   const int mode = (int)(flags & 3u);
   const float c1 = q[1].w, c2 = q[2].x;
   const float cr = q[2].y, cg = q[2].z, cb = q[2].w;
   // d erf/dz = 2/sqrt(pi) exp(-z^2); only the erf mode has a z derivative
-  const float c2k = (FAST || mode == kModeErf) ? c2 * (2.0f * kInvSqrtPi) : 0.0f;
-  float zz[kPx];
-  erf_args(s, steep, zz);
+  const float c2k = mode == kModeErf ? c2 * (2.0f * kInvSqrtPi) : 0.0f;
+  a = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
   for (int i = 0; i < kPx; ++i) {
-    const bool active = FAST || pos < cnt[i];
+    const int p = i >> 1, h = i & 1;
+    float& T = slot(P.T[p], h);
+    float& D = slot(P.D[p], h);
+    const float dr = slot(P.dr[p], h), dg = slot(P.dg[p], h), db = slot(P.db[p], h);
+    const bool active = pos < P.cnt[i];
     const float dy = s.dy0 + 2.0f * i;
     const float gg = ex2_approx(fmaf(fmaf(s.C, dy, s.Bx), dy, s.P0));
-    const float e = FAST ? erf32(zz[i]) : mode_factor(mode, zz[i]);
+    const float zz = erf_arg(s, steep, i);
+    const float e = mode_factor(mode, zz);
     const float u = fmaf(c2, e, c1);
     const float w_raw = u * gg;
-    const float w = FAST ? w_raw : fminf(w_raw, kWeightClamp);
-    const float inv = rcp_approx(1.0f - w);  // 1 - w >= 0.01
-    const float Tp = T[i] * inv;
+    const float w = fminf(w_raw, kWeightClamp);
+    const float inv = rcp_approx(1.0f - w);
+    const float Tp = T * inv;
     const float wt = active ? w * Tp : 0.0f;
-    const float dcr = fmaf(dr[i], cr, fmaf(dg[i], cg, db[i] * cb));
-    a.r = fmaf(dr[i], wt, a.r);
-    a.g = fmaf(dg[i], wt, a.g);
-    a.b = fmaf(db[i], wt, a.b);
-    // d_w = T_prev*(dC.rgb) - (dC.S)/(1-w) = inv*(T*dcr - D); gated on the
-    // unclamped weight (_blend_cy.pyx:309-312)
-    float d_w = inv * fmaf(T[i], dcr, -D[i]);
-    if (!FAST) d_w = (active && w_raw <= kWeightClamp) ? d_w : 0.0f;
+    const float dcr = fmaf(dr, cr, fmaf(dg, cg, db * cb));
+    a.r = fmaf(dr, wt, a.r);
+    a.g = fmaf(dg, wt, a.g);
+    a.b = fmaf(db, wt, a.b);
+    // gated on the unclamped weight (_blend_cy.pyx:309)
+    const float d_w = (active && w_raw <= kWeightClamp) ? inv * fmaf(T, dcr, -D) : 0.0f;
     const float dwg = d_w * gg;
     const float d_pow = dwg * u;
     a.s0 += d_pow;
@@ -310,12 +428,12 @@ __device__ __forceinline__ void bwd_splat(const float4 (&q)[4], const SteepRec& 
     a.s2 = fmaf(d_pow * dy, dy, a.s2);
     a.c1 += dwg;
     a.c2 = fmaf(dwg, e, a.c2);
-    const float d_z = dwg * c2k * ex2_approx(-(zz[i] * zz[i]) * kLog2e);
+    const float d_z = dwg * c2k * ex2_approx(-(zz * zz) * kLog2e);
     a.q0 += d_z;
     a.q1 = fmaf(d_z, dy, a.q1);
-    a.qz = fmaf(d_z, zz[i], a.qz);
-    D[i] = fmaf(wt, dcr, D[i]);
-    T[i] = active ? Tp : T[i];
+    a.qz = fmaf(d_z, zz, a.qz);
+    D = fmaf(wt, dcr, D);
+    T = active ? Tp : T;
   }
 }
 
@@ -374,26 +492,30 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) blend_bwd_kernel(
     const int row0 = ty * kTile + (lane >> 4);
     const float px = (float)col + 0.5f;
     const float py0 = (float)row0 + 0.5f;
-    float T[kPx], D[kPx], dr[kPx], dg[kPx], db[kPx];
-    int cnt[kPx];
+    BwdPix P;
     int maxc = 0, minc = 0x7fffffff;
 #pragma unroll
     for (int i = 0; i < kPx; ++i) {
+      const int p = i >> 1, h = i & 1;
       const int row = row0 + 2 * i;
       if (col < g.width && row < g.height) {
-        const size_t p = (size_t)row * g.width + col;
-        T[i] = trans[p];
-        cnt[i] = terminal[p];
-        dr[i] = d_color[3 * p + 0];
-        dg[i] = d_color[3 * p + 1];
-        db[i] = d_color[3 * p + 2];
-        D[i] = T[i] * fmaf(dr[i], bg0, fmaf(dg[i], bg1, db[i] * bg2));
-        maxc = max(maxc, cnt[i]);
-        minc = min(minc, cnt[i]);
+        const size_t o = (size_t)row * g.width + col;
+        const float t = trans[o];
+        const float dr = d_color[3 * o + 0], dg = d_color[3 * o + 1], db = d_color[3 * o + 2];
+        slot(P.T[p], h) = t;
+        P.cnt[i] = terminal[o];
+        slot(P.dr[p], h) = dr;
+        slot(P.dg[p], h) = dg;
+        slot(P.db[p], h) = db;
+        // suffix S starts at T_final * background; only dC.S is needed
+        slot(P.D[p], h) = t * fmaf(dr, bg0, fmaf(dg, bg1, db * bg2));
+        maxc = max(maxc, P.cnt[i]);
+        minc = min(minc, P.cnt[i]);
       } else {
         // outside the image: always "active" with T = 0 and a zero cotangent,
         // which contributes exact zeros (and keeps T_prev = 0 finite)
-        T[i] = 0.f; cnt[i] = 0x7fffffff; dr[i] = 0.f; dg[i] = 0.f; db[i] = 0.f; D[i] = 0.f;
+        slot(P.T[p], h) = 0.f; P.cnt[i] = 0x7fffffff; slot(P.dr[p], h) = 0.f;
+        slot(P.dg[p], h) = 0.f; slot(P.db[p], h) = 0.f; slot(P.D[p], h) = 0.f;
       }
     }
     minc = __reduce_min_sync(0xffffffffu, minc);
@@ -428,11 +550,11 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) blend_bwd_kernel(
         const SteepRec& side = st.side[s][j];
         const uint32_t flags = __float_as_uint(q[3].y);
         const int mode = (int)(flags & 3u);
-        BwdAcc a = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        BwdAcc a;
         if (pos < minc && fast_flags(flags))
-          bwd_splat<true>(q, side, flags, pos, px, py0, T, D, dr, dg, db, cnt, a);
+          bwd_splat_fast(q, px, py0, P, a);
         else
-          bwd_splat<false>(q, side, flags, pos, px, py0, T, D, dr, dg, db, cnt, a);
+          bwd_splat_generic(q, side, flags, pos, px, py0, P, a);
         // per-lane partials -> the pair-row columns (_blend_py.py:16-18)
         const float ca = q[0].z, cb = q[0].w, cc = q[1].x, za = q[1].y, zb = q[1].z;
         const float2 lo = __half22float2(*reinterpret_cast<const __half2*>(&q[3].w));

@@ -24,6 +24,31 @@ __global__ void __launch_bounds__(256) fma_probe_kernel(float* out, int iters, f
   if (s == 12345.678f) out[0] = s;  // keep the chains alive
 }
 
+__device__ __forceinline__ float2 ffma2_probe(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{\n .reg .b64 ra, rb, rc, rd;\n mov.b64 ra, {%2,%3};\n mov.b64 rb, {%4,%5};\n"
+      " mov.b64 rc, {%6,%7};\n fma.rn.f32x2 rd, ra, rb, rc;\n mov.b64 {%0,%1}, rd;\n}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+
+// packed FP32 (FFMA2, sm_100): 2 FMAs per lane per instruction
+__global__ void __launch_bounds__(256) fma2_probe_kernel(float* out, int iters, float m, float a) {
+  float2 x[kChains];
+#pragma unroll
+  for (int c = 0; c < kChains; ++c) x[c] = make_float2(threadIdx.x * 1e-3f + c, c * 0.5f);
+  const float2 mm = make_float2(m, m), aa = make_float2(a, a);
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) x[c] = ffma2_probe(x[c], mm, aa);
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int c = 0; c < kChains; ++c) s += x[c].x + x[c].y;
+  if (s == 12345.678f) out[0] = s;
+}
+
 __global__ void __launch_bounds__(256) ex2_probe_kernel(float* out, int iters) {
   float x[kChains];
 #pragma unroll
@@ -40,6 +65,9 @@ __global__ void __launch_bounds__(256) ex2_probe_kernel(float* out, int iters) {
 
 }  // namespace hs
 
+static double g_fma2_tflops = 0.0;
+extern "C" double hs_last_fma2_tflops(void) { return g_fma2_tflops; }
+
 extern "C" int hs_measure_fp32_peaks(double* fma_tflops, double* ex2_gops) {
   using namespace hs;
   int dev = 0, sms = 0;
@@ -51,7 +79,7 @@ extern "C" int hs_measure_fp32_peaks(double* fma_tflops, double* ex2_gops) {
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   const int blocks = sms * 8, threads = 256, iters = 4096;
-  float best_fma = 1e30f, best_ex2 = 1e30f, ms = 0.f;
+  float best_fma = 1e30f, best_ex2 = 1e30f, best_fma2 = 1e30f, ms = 0.f;
   for (int rep = 0; rep < 5; ++rep) {
     cudaEventRecord(a);
     fma_probe_kernel<<<blocks, threads>>>(out, iters, 0.9999f, 1e-3f);
@@ -60,16 +88,23 @@ extern "C" int hs_measure_fp32_peaks(double* fma_tflops, double* ex2_gops) {
     cudaEventElapsedTime(&ms, a, b);
     if (ms < best_fma) best_fma = ms;
     cudaEventRecord(a);
+    fma2_probe_kernel<<<blocks, threads>>>(out, iters, 0.9999f, 1e-3f);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    cudaEventElapsedTime(&ms, a, b);
+    if (ms < best_fma2) best_fma2 = ms;
+    cudaEventRecord(a);
     ex2_probe_kernel<<<blocks, threads>>>(out, iters / 4);
     cudaEventRecord(b);
     cudaEventSynchronize(b);
     cudaEventElapsedTime(&ms, a, b);
     if (ms < best_ex2) best_ex2 = ms;
   }
-  note_launch(10);
+  note_launch(15);
   const double n = (double)blocks * threads * kChains;
   if (fma_tflops) *fma_tflops = 2.0 * n * iters / (best_fma * 1e-3) / 1e12;
   if (ex2_gops) *ex2_gops = n * (iters / 4) / (best_ex2 * 1e-3) / 1e9;
+  g_fma2_tflops = 4.0 * n * iters / (best_fma2 * 1e-3) / 1e12;
   cudaEventDestroy(a);
   cudaEventDestroy(b);
   cudaFree(out);
