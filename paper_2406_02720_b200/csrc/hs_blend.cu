@@ -628,29 +628,28 @@ __global__ void mark_steep_pairs_kernel(const uint8_t* __restrict__ steep_flag,
   if (k < p && steep_flag[pairs[k]]) pairs[k] |= kSteepBit;
 }
 
-// Persistent grid: resident CTAs per SM x SMs (queried once per process).
-static int blend_grid(int n_work) {
-  static int sms = 0, per_sm = 0;
-  if (sms == 0) {
-    int dev = 0, s = 148, p = 0;
+// Persistent grid: resident CTAs per SM x SMs of that kernel (queried once).
+template <typename Kernel>
+static int blend_grid(Kernel kernel, int n_work, int* cache) {
+  if (*cache == 0) {
+    int dev = 0, sms = 148, per_sm = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&s, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p, blend_bwd_kernel<false>,
-                                                  kWarpsPerCta * 32, 0);
-    per_sm = p < 1 ? 1 : p;
-    sms = s;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kWarpsPerCta * 32, 0);
+    *cache = sms * (per_sm < 1 ? 1 : per_sm);
   }
   const int want = (n_work + kWarpsPerCta - 1) / kWarpsPerCta;
-  const int cap = sms * per_sm;
-  return want < cap ? (want > 0 ? want : 1) : cap;
+  return want < *cache ? (want > 0 ? want : 1) : *cache;
 }
+static int g_fwd_grid = 0, g_bwd_grid[2] = {0, 0};
 
 cudaError_t launch_blend_fwd(const BlendGeom& g, float bg0, float bg1, float bg2, float* color,
                              float* alpha, float* depth, float* trans, int32_t* terminal,
                              cudaStream_t stream) {
   cudaError_t e = cudaMemsetAsync(g.work_counter, 0, sizeof(int), stream);
   if (e != cudaSuccess) return e;
-  blend_fwd_kernel<<<blend_grid(g.n_work), kWarpsPerCta * 32, 0, stream>>>(
+  blend_fwd_kernel<<<blend_grid(blend_fwd_kernel, g.n_work, &g_fwd_grid), kWarpsPerCta * 32, 0,
+                     stream>>>(
       g, bg0, bg1, bg2, color, alpha, depth, trans, terminal);
   note_launch();
   return cudaGetLastError();
@@ -663,10 +662,12 @@ cudaError_t launch_blend_bwd(const BlendGeom& g, float bg0, float bg1, float bg2
   cudaError_t e = cudaMemsetAsync(g.work_counter, 0, sizeof(int), stream);
   if (e != cudaSuccess) return e;
   if (rows_by_sorted_pos)
-    blend_bwd_kernel<true><<<blend_grid(g.n_work), kWarpsPerCta * 32, 0, stream>>>(
+    blend_bwd_kernel<true><<<blend_grid(blend_bwd_kernel<true>, g.n_work, &g_bwd_grid[1]),
+                             kWarpsPerCta * 32, 0, stream>>>(
         g, bg0, bg1, bg2, d_color, trans, terminal, rows, last_rank, rank_of);
   else
-    blend_bwd_kernel<false><<<blend_grid(g.n_work), kWarpsPerCta * 32, 0, stream>>>(
+    blend_bwd_kernel<false><<<blend_grid(blend_bwd_kernel<false>, g.n_work, &g_bwd_grid[0]),
+                              kWarpsPerCta * 32, 0, stream>>>(
         g, bg0, bg1, bg2, d_color, trans, terminal, rows, last_rank, rank_of);
   note_launch();
   return cudaGetLastError();
