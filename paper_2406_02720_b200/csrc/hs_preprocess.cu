@@ -451,9 +451,13 @@ __device__ __forceinline__ void preprocess_bwd_one(
     const int spans_x = rc.y - rc.x + 1;
     const int base = (int)__float_as_uint(q3.z) + rc.z * spans_x + rc.x;
     const int r = (int)rank_of[i];
+    int lx = 0, ly = 0;
     for (int l = 0; l < cnt; ++l) {
-      const int ly = l / spans_x, lx = l - ly * spans_x;
       const int tile = (rc.z + ly) * tiles_x + rc.x + lx;
+      if (++lx == spans_x) {
+        lx = 0;
+        ++ly;
+      }
       if (r > last_rank[tile]) continue;
       const float4* row = reinterpret_cast<const float4*>(rows + (size_t)(base + l) * kRowFloats);
       const float4 u0 = row[0], u1 = row[1], u2 = row[2], u3 = row[3];
@@ -485,29 +489,32 @@ __device__ __forceinline__ void preprocess_bwd_one(
   // d_inv = d_za*(n1 v00 + n2 v10) + d_zb*(n2 v11) (rasterizer.py:459) equals
   // (sum_px d_z * z) / inv; the blend accumulates that sum directly (column 12),
   // which stays accurate when za*dx and zb*dy nearly cancel (|n3| -> 0).
-  const double d_inv = mode0 ? m[kColSumDzZ] / inv : 0.0;
+  const double d_inv = mode0 ? m[kColSumDzZ] * (1.4142135623730951 * fabs(n3)) : 0.0;
   double d_nray[3];
   d_nray[0] = d_za0 * inv * st.v00;
   d_nray[1] = d_za0 * inv * st.v10 + d_zb0 * inv * st.v11;
   {
     const double sg = n3 > 0.0 ? 1.0 : (n3 < 0.0 ? -1.0 : 0.0);
-    d_nray[2] = mode0 ? -d_inv * sg / (1.4142135623730951 * n3 * n3) : 0.0;
+    // 1 / (sqrt2 n3^2) = sqrt2 * inv^2
+    d_nray[2] = mode0 ? -d_inv * sg * (1.4142135623730951 * inv * inv) : 0.0;
   }
   const double d_v00 = d_za0 * inv * n1, d_v10 = d_za0 * inv * n2, d_v11 = d_zb0 * inv * n2;
   // n_ray = y/|y| (rasterizer.py:469)
   double d_y[3];
   {
     const double dot = d_nray[0] * n1 + d_nray[1] * n2 + d_nray[2] * n3;
-    for (int k = 0; k < 3; ++k) d_y[k] = (d_nray[k] - dot * st.nray[k]) / st.ynorm;
+    const double rn = 1.0 / st.ynorm;
+    for (int k = 0; k < 3; ++k) d_y[k] = (d_nray[k] - dot * st.nray[k]) * rn;
   }
   // y = L^-1 h_ray (rasterizer.py:470-473; tri_inv3_batch geometry.py:176-186)
   const double* L = st.L;
   double Li[9];
   {
     const double a = L[0], b = L[4], c = L[8];
-    Li[0] = 1.0 / a; Li[1] = 0.0; Li[2] = 0.0;
-    Li[3] = -L[3] / (a * b); Li[4] = 1.0 / b; Li[5] = 0.0;
-    Li[6] = (L[3] * L[7] - L[6] * b) / (a * b * c); Li[7] = -L[7] / (b * c); Li[8] = 1.0 / c;
+    const double ra = 1.0 / a, rb = 1.0 / b, rc = 1.0 / c;
+    Li[0] = ra; Li[1] = 0.0; Li[2] = 0.0;
+    Li[3] = -L[3] * (ra * rb); Li[4] = rb; Li[5] = 0.0;
+    Li[6] = (L[3] * L[7] - L[6] * b) * (ra * rb * rc); Li[7] = -L[7] * (rb * rc); Li[8] = rc;
   }
   double d_hr[3];
   for (int a = 0; a < 3; ++a) d_hr[a] = Li[a] * d_y[0] + Li[3 + a] * d_y[1] + Li[6 + a] * d_y[2];
@@ -551,9 +558,10 @@ __device__ __forceinline__ void preprocess_bwd_one(
   // conic = inverse of the dilated 2x2 (rasterizer.py:489-500)
   {
     const double a = st.a, b = st.b, c = st.c, det = st.det, det2 = det * det;
-    dC[0] += (-d_ca * c * c + d_cb * b * c - d_cc * b * b) / det2;
-    dC[1] += (2.0 * d_ca * b * c - d_cb * (det + 2.0 * b * b) + 2.0 * d_cc * a * b) / det2;
-    dC[4] += (-d_ca * b * b + d_cb * a * b - d_cc * a * a) / det2;
+    const double rd2 = 1.0 / det2;
+    dC[0] += (-d_ca * c * c + d_cb * b * c - d_cc * b * b) * rd2;
+    dC[1] += (2.0 * d_ca * b * c - d_cb * (det + 2.0 * b * b) + 2.0 * d_cc * a * b) * rd2;
+    dC[4] += (-d_ca * b * b + d_cb * a * b - d_cc * a * a) * rd2;
   }
   // cov_ray = J cov_cam J^T, h_ray = J h_cam (rasterizer.py:503-507)
   const double* J = st.J;
@@ -613,9 +621,10 @@ __device__ __forceinline__ void preprocess_bwd_one(
     d_t[2] += dJ[4] * (-cam.fy * invz * invz);
     d_t[1] += dJ[5] * (-cam.fy * invz * invz);
     d_t[2] += dJ[5] * (2.0 * cam.fy * ty * invz * invz * invz);
-    const double rh[3] = {tx / ell, ty / ell, tz / ell};
+    const double rell = 1.0 / ell;
+    const double rh[3] = {tx * rell, ty * rell, tz * rell};
     const double dot = dJ[6] * rh[0] + dJ[7] * rh[1] + dJ[8] * rh[2];
-    for (int k = 0; k < 3; ++k) d_t[k] += (dJ[6 + k] - dot * rh[k]) / ell;
+    for (int k = 0; k < 3; ++k) d_t[k] += (dJ[6 + k] - dot * rh[k]) * rell;
   }
   double d_mu[3];
   for (int a = 0; a < 3; ++a) d_mu[a] = d_t[0] * Wr[a] + d_t[1] * Wr[3 + a] + d_t[2] * Wr[6 + a];
@@ -633,7 +642,8 @@ __device__ __forceinline__ void preprocess_bwd_one(
         for (int d = 0; d < 3; ++d) d_dir[d] += db * g[3 * k + d];
       }
       const double dot = d_dir[0] * st.vdir[0] + d_dir[1] * st.vdir[1] + d_dir[2] * st.vdir[2];
-      for (int d = 0; d < 3; ++d) d_mu[d] += (d_dir[d] - dot * st.vdir[d]) / st.vdist;
+      const double rv = 1.0 / st.vdist;
+      for (int d = 0; d < 3; ++d) d_mu[d] += (d_dir[d] - dot * st.vdir[d]) * rv;
     }
     // d_sh overwrites this thread's staged SH row (read above for d_basis)
     for (int k = 0; k < K; ++k)
@@ -673,12 +683,14 @@ __device__ __forceinline__ void preprocess_bwd_one(
       dq[3] += 2 * Dz[k] * dR[k];
     }
     const double dot = dq[0] * w + dq[1] * x + dq[2] * y + dq[3] * z;
-    for (int k = 0; k < 4; ++k) sm.rot[4 * t + k] = T((dq[k] - dot * st.qu[k]) / st.qnorm);
+    const double rq = 1.0 / st.qnorm;
+    for (int k = 0; k < 4; ++k) sm.rot[4 * t + k] = T((dq[k] - dot * st.qu[k]) * rq);
   }
   // splitting normal through its normalisation (rasterizer.py:565-566)
   {
     const double dot = d_nu[0] * st.nu[0] + d_nu[1] * st.nu[1] + d_nu[2] * st.nu[2];
-    for (int k = 0; k < 3; ++k) sm.nrm[3 * t + k] = T((d_nu[k] - dot * st.nu[k]) / st.nnorm);
+    const double rnn = 1.0 / st.nnorm;
+    for (int k = 0; k < 3; ++k) sm.nrm[3 * t + k] = T((d_nu[k] - dot * st.nu[k]) * rnn);
   }
   for (int k = 0; k < 3; ++k) sm.mu[3 * t + k] = T(d_mu[k]);
   pgn_s[t] = T(sqrt(d_mux * d_mux + d_muy * d_muy));
