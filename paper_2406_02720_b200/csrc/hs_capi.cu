@@ -63,6 +63,7 @@ struct FrameBufs {
   int* counters;
   int32_t* xflags;
   int32_t* xlocal;
+  float4* merged;
   void* temp;
   size_t temp_bytes;
 };
@@ -117,6 +118,7 @@ static FrameBufs carve_frame(void* ws, int64_t n, int n_tiles, size_t* total) {
   f.counters = c.take<int>(64);
   f.xflags = c.take<int32_t>(n + 1);
   f.xlocal = c.take<int32_t>(n + 1);
+  f.merged = c.take<float4>(4 * (size_t)n);
   f.temp_bytes = frame_temp_bytes(n);
   f.temp = c.take<char>(f.temp_bytes);
   if (total) *total = c.off;
@@ -410,11 +412,12 @@ int hs_preprocess_bwd(hs_frame* frame, const hs_scene* scene, const hs_camera* c
   if (scene->dtype == HS_DTYPE_F32) {
     HS_CUDA(launch_preprocess_bwd_t<float>(scene_args<float>(scene), ca, frame->kernel, frame->n,
                                            frame->tiles_x, f.rec, f.rect, f.count, f.rank_of,
-                                           f.last_rank, b.rows, grad_args<float>(grads), stream));
+                                           f.last_rank, b.rows, f.merged, grad_args<float>(grads),
+                                           stream));
   } else {
     HS_CUDA(launch_preprocess_bwd_t<double>(scene_args<double>(scene), ca, frame->kernel,
                                             frame->n, frame->tiles_x, f.rec, f.rect, f.count,
-                                            f.rank_of, f.last_rank, b.rows,
+                                            f.rank_of, f.last_rank, b.rows, f.merged,
                                             grad_args<double>(grads), stream));
   }
   return HS_OK;

@@ -182,24 +182,33 @@ struct Staged {
   T sh[NT * SHS];
 };
 
+// One element global -> shared without a register round trip (LDGSTS), so a
+// thread's whole share of the staging is in flight at once.
+template <typename T>
+__device__ __forceinline__ void cp_async_elem(T* smem, const T* gmem) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(d), "l"(gmem), "n"(sizeof(T)));
+}
+
 template <typename T, int K, int NT>
 __device__ __forceinline__ void stage_in(Staged<T, K, NT>& s, const SceneArgs<T>& sc,
                                          int64_t base, int cnt) {
   const int tid = threadIdx.x;
   for (int e = tid; e < cnt * 3; e += NT) {
-    s.mu[e] = sc.mu[base * 3 + e];
-    s.ls[e] = sc.ls[base * 3 + e];
-    s.nrm[e] = sc.nrm[base * 3 + e];
+    cp_async_elem(&s.mu[e], &sc.mu[base * 3 + e]);
+    cp_async_elem(&s.ls[e], &sc.ls[base * 3 + e]);
+    cp_async_elem(&s.nrm[e], &sc.nrm[base * 3 + e]);
   }
-  for (int e = tid; e < cnt * 4; e += NT) s.rot[e] = sc.rot[base * 4 + e];
+  for (int e = tid; e < cnt * 4; e += NT) cp_async_elem(&s.rot[e], &sc.rot[base * 4 + e]);
   for (int e = tid; e < cnt; e += NT) {
-    s.ra[e] = sc.ra[base + e];
-    s.rb[e] = sc.rb[base + e];
+    cp_async_elem(&s.ra[e], &sc.ra[base + e]);
+    cp_async_elem(&s.rb[e], &sc.rb[base + e]);
   }
   for (int e = tid; e < cnt * 3 * K; e += NT) {
     const int t = e / (3 * K), c = e - t * (3 * K);
-    s.sh[t * Staged<T, K, NT>::SHS + c] = sc.sh[base * 3 * K + e];
+    cp_async_elem(&s.sh[t * Staged<T, K, NT>::SHS + c], &sc.sh[base * 3 * K + e]);
   }
+  asm volatile("cp.async.wait_all;\n" ::);
   __syncthreads();
 }
 
@@ -422,13 +431,53 @@ __global__ void __launch_bounds__(NT) preprocess_fwd_kernel(
 // (_geometry_backward, rasterizer.py:424-575).  FP64 throughout.
 // K7 body for one primitive: reads its staged inputs, overwrites the same
 // slots with its gradients (each thread touches only its own slots).
+// K7a: merge each visible splat's pair rows (np.add.at, rasterizer.py:419-420):
+// the tiles of its rect in row-major (= sorted k) order, skipping pairs past
+// the tile's last composited position (never written by K6).  A separate,
+// register-light kernel so the dependent gathers are hidden by occupancy.
+__global__ void __launch_bounds__(256) merge_rows_kernel(
+    int64_t n, int tiles_x, const float4* __restrict__ rec, const int4* __restrict__ rect,
+    const int32_t* __restrict__ count, const uint32_t* __restrict__ rank_of,
+    const int32_t* __restrict__ last_rank, const float* __restrict__ rows,
+    float4* __restrict__ merged) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int cnt = count[i];
+  if (cnt == 0) return;
+  double m[13];
+#pragma unroll
+  for (int k = 0; k < 13; ++k) m[k] = 0.0;
+  const int4 rc = rect[i];
+  const int spans_x = rc.y - rc.x + 1;
+  const int base = __float_as_int(rec[4 * i + 3].z) + rc.z * spans_x + rc.x;
+  const int r = (int)rank_of[i];
+  int lx = 0, ly = 0;
+  for (int l = 0; l < cnt; ++l) {
+    const int tile = (rc.z + ly) * tiles_x + rc.x + lx;
+    if (++lx == spans_x) {
+      lx = 0;
+      ++ly;
+    }
+    const float4* row = reinterpret_cast<const float4*>(rows + (size_t)(base + l) * kRowFloats);
+    const float4 u0 = row[0], u1 = row[1], u2 = row[2], u3 = row[3];
+    if (r > last_rank[tile]) continue;
+    m[0] += u0.x; m[1] += u0.y; m[2] += u0.z; m[3] += u0.w;
+    m[4] += u1.x; m[5] += u1.y; m[6] += u1.z; m[7] += u1.w;
+    m[8] += u2.x; m[9] += u2.y; m[10] += u2.z; m[11] += u2.w;
+    m[12] += u3.x;
+  }
+  float4* dst = merged + 4 * i;
+  dst[0] = make_float4((float)m[0], (float)m[1], (float)m[2], (float)m[3]);
+  dst[1] = make_float4((float)m[4], (float)m[5], (float)m[6], (float)m[7]);
+  dst[2] = make_float4((float)m[8], (float)m[9], (float)m[10], (float)m[11]);
+  dst[3] = make_float4((float)m[12], 0.f, 0.f, 0.f);
+}
+
 template <typename T, int DEG, int NT>
 __device__ __forceinline__ void preprocess_bwd_one(
     Staged<T, (DEG + 1) * (DEG + 1), NT>& sm, T* pgn_s, int32_t* touch_s, int t, int64_t i,
-    const CamArgs& cam, int kernel, int tiles_x, const float4* __restrict__ rec,
-    const int4* __restrict__ rect, const int32_t* __restrict__ count,
-    const uint32_t* __restrict__ rank_of, const int32_t* __restrict__ last_rank,
-    const float* __restrict__ rows) {
+    const CamArgs& cam, int kernel, const int32_t* __restrict__ count,
+    const float4* __restrict__ merged) {
   constexpr int K = (DEG + 1) * (DEG + 1);
   using St = Staged<T, K, NT>;
   const int cnt = count[i];
@@ -441,31 +490,14 @@ __device__ __forceinline__ void preprocess_bwd_one(
     touch_s[t] = 0;
     return;
   }
-  // ---- merge pair rows: tiles of the rect in row-major (= sorted k) order,
-  // skipping pairs past the tile's last composited position (never written).
   double m[13];
-  for (int k = 0; k < 13; ++k) m[k] = 0.0;
   {
-    const float4 q3 = rec[4 * i + 3];
-    const int4 rc = rect[i];
-    const int spans_x = rc.y - rc.x + 1;
-    const int base = (int)__float_as_uint(q3.z) + rc.z * spans_x + rc.x;
-    const int r = (int)rank_of[i];
-    int lx = 0, ly = 0;
-    for (int l = 0; l < cnt; ++l) {
-      const int tile = (rc.z + ly) * tiles_x + rc.x + lx;
-      if (++lx == spans_x) {
-        lx = 0;
-        ++ly;
-      }
-      if (r > last_rank[tile]) continue;
-      const float4* row = reinterpret_cast<const float4*>(rows + (size_t)(base + l) * kRowFloats);
-      const float4 u0 = row[0], u1 = row[1], u2 = row[2], u3 = row[3];
-      m[0] += u0.x; m[1] += u0.y; m[2] += u0.z; m[3] += u0.w;
-      m[4] += u1.x; m[5] += u1.y; m[6] += u1.z; m[7] += u1.w;
-      m[8] += u2.x; m[9] += u2.y; m[10] += u2.z; m[11] += u2.w;
-      m[12] += u3.x;
-    }
+    const float4* src = merged + 4 * i;
+    const float4 u0 = src[0], u1 = src[1], u2 = src[2], u3 = src[3];
+    m[0] = u0.x; m[1] = u0.y; m[2] = u0.z; m[3] = u0.w;
+    m[4] = u1.x; m[5] = u1.y; m[6] = u1.z; m[7] = u1.w;
+    m[8] = u2.x; m[9] = u2.y; m[10] = u2.z; m[11] = u2.w;
+    m[12] = u3.x;
   }
   FwdState st;
   forward_state<DEG>(StagedView<T, K, NT>{sm, t}, cam, kernel, st);
@@ -699,11 +731,8 @@ __device__ __forceinline__ void preprocess_bwd_one(
 
 template <typename T, int DEG, int NT>
 __global__ void __launch_bounds__(NT) preprocess_bwd_kernel(
-    SceneArgs<T> sc, CamArgs cam, int kernel, int64_t n, int tiles_x,
-    const float4* __restrict__ rec, const int4* __restrict__ rect,
-    const int32_t* __restrict__ count, const uint32_t* __restrict__ rank_of,
-    const int32_t* __restrict__ last_rank, const float* __restrict__ rows,
-    GradArgs<T> out) {
+    SceneArgs<T> sc, CamArgs cam, int kernel, int64_t n, const int32_t* __restrict__ count,
+    const float4* __restrict__ merged, GradArgs<T> out) {
   constexpr int K = (DEG + 1) * (DEG + 1);
   using St = Staged<T, K, NT>;
   __shared__ St sm;
@@ -713,9 +742,8 @@ __global__ void __launch_bounds__(NT) preprocess_bwd_kernel(
   const int ncta = (int)(n - base < NT ? n - base : NT);
   stage_in(sm, sc, base, ncta);
   const int t = threadIdx.x;
-  if (t < ncta) preprocess_bwd_one<T, DEG, NT>(sm, pgn_s, touch_s, t, base + t, cam, kernel,
-                                               tiles_x, rec, rect, count, rank_of, last_rank,
-                                               rows);
+  if (t < ncta)
+    preprocess_bwd_one<T, DEG, NT>(sm, pgn_s, touch_s, t, base + t, cam, kernel, count, merged);
   __syncthreads();
   // coalesced stores of the staged gradients
   for (int e = t; e < ncta * 3; e += NT) {
@@ -766,15 +794,18 @@ template <typename T>
 cudaError_t launch_preprocess_bwd_t(const SceneArgs<T>& sc, const CamArgs& cam, int kernel,
                                     int64_t n, int tiles_x, const float4* rec, const int4* rect,
                                     const int32_t* count, const uint32_t* rank_of,
-                                    const int32_t* last_rank, const float* rows,
+                                    const int32_t* last_rank, const float* rows, float4* merged,
                                     const GradArgs<T>& out, cudaStream_t stream) {
+  merge_rows_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(
+      n, tiles_x, rec, rect, count, rank_of, last_rank, rows, merged);
+  note_launch();
   constexpr int NT = sizeof(T) == 4 ? 128 : 64;
   const int64_t grid = (n + NT - 1) / NT;
   switch (sc.deg) {
 #define HS_K7(D)                                                                               \
   case D:                                                                                      \
     preprocess_bwd_kernel<T, D, NT><<<(unsigned)grid, NT, 0, stream>>>(                        \
-        sc, cam, kernel, n, tiles_x, rec, rect, count, rank_of, last_rank, rows, out);         \
+        sc, cam, kernel, n, count, merged, out);                                               \
     break;
     HS_K7(0) HS_K7(1) HS_K7(2) HS_K7(3)
 #undef HS_K7
@@ -793,12 +824,12 @@ template cudaError_t launch_preprocess_fwd_t<double>(const SceneArgs<double>&, c
 template cudaError_t launch_preprocess_bwd_t<float>(const SceneArgs<float>&, const CamArgs&, int,
                                                     int64_t, int, const float4*, const int4*,
                                                     const int32_t*, const uint32_t*, const int32_t*,
-                                                    const float*, const GradArgs<float>&,
+                                                    const float*, float4*, const GradArgs<float>&,
                                                     cudaStream_t);
 template cudaError_t launch_preprocess_bwd_t<double>(const SceneArgs<double>&, const CamArgs&, int,
                                                      int64_t, int, const float4*, const int4*,
                                                      const int32_t*, const uint32_t*,
-                                                     const int32_t*, const float*,
+                                                     const int32_t*, const float*, float4*,
                                                      const GradArgs<double>&, cudaStream_t);
 
 }  // namespace hs
