@@ -187,18 +187,26 @@ def run_reference_arm(args):
 
 
 def metric_name(cfg):
-    return "fwd+bwd iters/s (1M half-Gaussians, 1080p)" if cfg == "c3" else \
-        f"fwd+bwd iters/s ({cfg})"
+    if cfg == "c3":
+        return "fwd+bwd iters/s (1M half-Gaussians, 1080p)"
+    if cfg == "c4":
+        return "fwd+bwd views/s (3M half-Gaussians, 1297x840, 8-view batch)"
+    return f"fwd+bwd iters/s ({cfg})"
 
 
-def bench_config(cfg, world):
+def bench_config(cfg, world, views_per_step=None):
     from paper_2406_02720_b200 import scenes
     c = scenes.CONFIGS[cfg]
     n, sh, w, h = c["args"][:4]
-    return {"workload": f"{cfg}: {c['kind']} {n} half-Gaussians, SH{sh}, {w}x{h}, one view per "
-                        f"rank per step, fwd+bwd with fixed cotangent",
+    multi = c["kind"] == "ball"
+    views = views_per_step or (c["kw"].get("views", 8) if multi else world)
+    per = (f"a batch of {views} views sharded over {world} rank(s)" if multi
+           else "one view per rank per step")
+    return {"workload": f"{cfg}: {c['kind']} {n} half-Gaussians, SH{sh}, {w}x{h}, {per}, "
+                        f"fwd+bwd with fixed cotangents, gradients summed over the batch"
+                        + (" and all-reduced (NCCL)" if world > 1 else ""),
             "gaussians": n, "width": w, "height": h, "sh_degree": sh,
-            "views_per_step": world, "parallelism": f"dp{world} (views)",
+            "views_per_step": views, "parallelism": f"dp{world} (views)",
             "l2": "inputs larger than L2 (scene 252 MB + 64 MB records per view at c3)"}
 
 
@@ -214,7 +222,7 @@ def main():
     from paper_2406_02720_b200 import _native, device, scenes
     from paper_2406_02720_b200 import rasterizer as dropin
     from paper_2406_02720_b200.geometry import CameraModel, Scene
-    from paper_2406_02720_b200.multiview import GradientAllReduce
+    from paper_2406_02720_b200.multiview import GradientAllReduce, shard_views
 
     world, rank, local = rank_info()
     torch.cuda.set_device(local)
@@ -223,25 +231,38 @@ def main():
     lib = _native.load()
 
     sa = scenes.make_config(args.config)
-    cam = CameraModel(**jitter_camera(sa.cameras[0], rank))
+    multi = len(sa.cameras) > 1
+    if multi:
+        # c4: a batch of views sharded over the ranks (strong scaling)
+        cams = [CameraModel(**c) for c in sa.cameras]
+        views = shard_views(len(cams), world, rank)
+    else:
+        # one view per rank of the same scene (weak scaling)
+        cams = [CameraModel(**jitter_camera(sa.cameras[0], rank))]
+        views = [0]
+    cam = cams[views[0]] if views else cams[0]
     scene = Scene(*(getattr(sa, f) for f in sa.FIELDS), sh_degree=sa.sh_degree,
                   background_color=sa.background_color, device="cuda", dtype=torch.float32)
-    d_color = torch.as_tensor(scenes.cotangent(cam.height, cam.width), dtype=torch.float32,
-                              device="cuda")
+    d_colors = [torch.as_tensor(scenes.cotangent(c.height, c.width, seed=1 + v),
+                                dtype=torch.float32, device="cuda") for v, c in enumerate(cams)]
     grads = device.DeviceGradientSet.empty_flat(scene)
     reducer = GradientAllReduce(grads) if world > 1 else None
     timer = device.StageTimer()
     rast = device.Rasterizer("cuda", slots=1)
 
     def step(t=None):
-        out = rast.render(scene, cam, timer=t)
-        rast.render_backward(scene, cam, out, d_color, grads=grads, timer=t)
+        out = None
+        for j, v in enumerate(views):
+            out = rast.render(scene, cams[v], timer=t)
+            rast.render_backward(scene, cams[v], out, d_colors[v], grads=grads, timer=t,
+                                 accumulate=j > 0)
         if reducer is not None:
             reducer.allreduce()
         return out
 
     def fwd_step():
-        return rast.render(scene, cam)
+        for v in views:
+            rast.render(scene, cams[v])
 
     def barrier():
         if world > 1:
@@ -320,15 +341,17 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args.config)
 
-    value = world * 1e3 / ms
+    views_per_step = len(cams) if multi else world
+    value = views_per_step * 1e3 / ms
     if rank == 0:
         line = {
-            "metric": metric_name(args.config), "value": value, "unit": "iters/s",
+            "metric": metric_name(args.config), "value": value,
+            "unit": "views/s" if multi else "iters/s",
             "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
-            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong" if multi else "weak",
             "vs_baseline": None, "dtype": "f32 blend / f64 geometry", "data": "synthetic",
-            "config": bench_config(args.config, world),
-            "fwd_fps": world * 1e3 / fwd_ms, "fwd_ms_per_frame": fwd_ms,
+            "config": bench_config(args.config, world, views_per_step),
+            "fwd_fps": views_per_step * 1e3 / fwd_ms, "fwd_ms_per_step": fwd_ms,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clock_info,
             "counts": {"P": out.frame.num_pairs, "fwd_evals": fwd_evals, "bwd_evals": bwd_evals},

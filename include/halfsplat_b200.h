@@ -151,6 +151,8 @@ typedef struct hs_grads {
   void* d_raw_opacity_b;/* (n,) */
   void* pos_grad_norm;  /* (n,) */
   int32_t* touch_count; /* (n,) */
+  int32_t accumulate;   /* 0: overwrite; 1: add into the buffers (multi-view
+                           batches, GradientSet.add rasterizer.py:100-105) */
 } hs_grads;
 
 int hs_preprocess_bwd(hs_frame* frame, const hs_scene* scene,

@@ -70,7 +70,7 @@ class HsGrads(ctypes.Structure):
         ("d_mu", c_void_p), ("d_log_scale", c_void_p), ("d_rotation", c_void_p),
         ("d_sh", c_void_p), ("d_normal", c_void_p),
         ("d_raw_opacity_a", c_void_p), ("d_raw_opacity_b", c_void_p),
-        ("pos_grad_norm", c_void_p), ("touch_count", c_void_p),
+        ("pos_grad_norm", c_void_p), ("touch_count", c_void_p), ("accumulate", c_int32),
     ]
 
 

@@ -200,6 +200,7 @@ static GradArgs<T> grad_args(const hs_grads* g) {
   a.d_rb = static_cast<T*>(g->d_raw_opacity_b);
   a.pos_grad_norm = static_cast<T*>(g->pos_grad_norm);
   a.touch = g->touch_count;
+  a.accumulate = g->accumulate;
   return a;
 }
 

@@ -42,6 +42,7 @@ struct GradArgs {
   T* d_rb;
   T* pos_grad_norm;
   int32_t* touch;
+  int accumulate;
 };
 
 // ---- hs_preprocess.cu -----------------------------------------------------

@@ -745,26 +745,25 @@ __global__ void __launch_bounds__(NT) preprocess_bwd_kernel(
   if (t < ncta)
     preprocess_bwd_one<T, DEG, NT>(sm, pgn_s, touch_s, t, base + t, cam, kernel, count, merged);
   __syncthreads();
-  // coalesced stores of the staged gradients
+  // coalesced stores of the staged gradients (or accumulation into them)
+  auto put = [&](T* dst, int64_t k, T v) { dst[k] = out.accumulate ? dst[k] + v : v; };
   for (int e = t; e < ncta * 3; e += NT) {
-    out.d_mu[base * 3 + e] = sm.mu[e];
-    out.d_log_scale[base * 3 + e] = sm.ls[e];
-    out.d_normal[base * 3 + e] = sm.nrm[e];
+    put(out.d_mu, base * 3 + e, sm.mu[e]);
+    put(out.d_log_scale, base * 3 + e, sm.ls[e]);
+    put(out.d_normal, base * 3 + e, sm.nrm[e]);
   }
-  for (int e = t; e < ncta * 4; e += NT) out.d_rotation[base * 4 + e] = sm.rot[e];
+  for (int e = t; e < ncta * 4; e += NT) put(out.d_rotation, base * 4 + e, sm.rot[e]);
   for (int e = t; e < ncta; e += NT) {
-    out.d_ra[base + e] = sm.ra[e];
-    out.d_rb[base + e] = sm.rb[e];
-    out.pos_grad_norm[base + e] = pgn_s[e];
-    out.touch[base + e] = touch_s[e];
+    put(out.d_ra, base + e, sm.ra[e]);
+    put(out.d_rb, base + e, sm.rb[e]);
+    put(out.pos_grad_norm, base + e, pgn_s[e]);
+    out.touch[base + e] = out.accumulate ? out.touch[base + e] + touch_s[e] : touch_s[e];
   }
   for (int e = t; e < ncta * 3 * K; e += NT) {
     const int tt = e / (3 * K), c = e - tt * (3 * K);
-    out.d_sh[base * 3 * K + e] = sm.sh[tt * St::SHS + c];
+    put(out.d_sh, base * 3 * K + e, sm.sh[tt * St::SHS + c]);
   }
 }
-
-
 
 // ---------------------------------------------------------------------------
 template <typename T>

@@ -366,12 +366,16 @@ class Rasterizer:
         self.next = (self.next + 1) % len(self.slots)
         return render(scene, cam, self.kernel, timer=timer, ws=ws)
 
-    def render_backward(self, scene, cam, out, d_color, grads=None, timer=None):
-        return render_backward(scene, cam, out, d_color, grads=grads, timer=timer)
+    def render_backward(self, scene, cam, out, d_color, grads=None, timer=None, accumulate=False):
+        return render_backward(scene, cam, out, d_color, grads=grads, timer=timer,
+                               accumulate=accumulate)
 
 
-def render_backward(scene, cam, out, d_color, grads=None, timer=None):
-    """Gradients of sum(d_color * color) for every parameter (rasterizer.py:386-421)."""
+def render_backward(scene, cam, out, d_color, grads=None, timer=None, accumulate=False):
+    """Gradients of sum(d_color * color) for every parameter (rasterizer.py:386-421).
+
+    accumulate=True adds this view's gradients into `grads` (GradientSet.add,
+    rasterizer.py:100-105) inside the K7 kernel instead of overwriting them."""
     scene = Scene.from_any(scene)
     cam = CameraModel.from_any(cam)
     frame = out.frame
@@ -398,6 +402,7 @@ def render_backward(scene, cam, out, d_color, grads=None, timer=None):
     g = _native.HsGrads()
     for name in DeviceGradientSet.NAMES:
         setattr(g, name, getattr(grads, name).data_ptr())
+    g.accumulate = 1 if accumulate else 0
     sc = scene_struct(scene)
     cs = camera_struct(cam)
     with timer.span("preprocess_bwd"):

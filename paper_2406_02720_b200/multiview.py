@@ -38,28 +38,31 @@ class GradientAllReduce:
         return self.grads
 
 
-def batch_gradients(scene, cams, d_colors, view_ids, out=None, tmp=None):
-    """Accumulate render_backward over this rank's views into `out` (flat buffer)."""
+def batch_gradients(scene, cams, d_colors, view_ids, out=None, rast=None, timer=None):
+    """Sum render_backward over this rank's views into `out` (flat buffer).
+
+    The first view overwrites, later ones accumulate inside the K7 kernel, so a
+    batch costs no extra gradient-sized passes."""
     from . import device
     if out is None:
         out = device.DeviceGradientSet.empty_flat(scene)
-    out.flat.zero_()
-    out.touch_count.zero_()
-    if tmp is None:
-        tmp = device.DeviceGradientSet.empty_flat(scene)
-    for v in view_ids:
-        r = device.render(scene, cams[v])
-        device.render_backward(scene, cams[v], r, d_colors[v], grads=tmp)
-        out.flat.add_(tmp.flat)
-        out.touch_count.add_(tmp.touch_count)
+    if rast is None:
+        rast = device.Rasterizer(scene.device)
+    if not view_ids:
+        out.flat.zero_()
+        out.touch_count.zero_()
+    for j, v in enumerate(view_ids):
+        r = rast.render(scene, cams[v], timer=timer)
+        rast.render_backward(scene, cams[v], r, d_colors[v], grads=out, timer=timer,
+                             accumulate=j > 0)
     return out
 
 
-def multiview_step(scene, cams, d_colors, grads=None, tmp=None):
+def multiview_step(scene, cams, d_colors, grads=None, rast=None):
     """One data-parallel step: local views, then the all-reduce. Returns the batch gradient."""
     world = dist.get_world_size() if dist.is_available() and dist.is_initialized() else 1
     rank = dist.get_rank() if world > 1 else 0
     views = shard_views(len(cams), world, rank)
-    grads = batch_gradients(scene, cams, d_colors, views, grads, tmp)
+    grads = batch_gradients(scene, cams, d_colors, views, grads, rast)
     GradientAllReduce(grads).allreduce()
     return grads

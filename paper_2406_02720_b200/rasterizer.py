@@ -11,6 +11,7 @@ exactly the reference's inputs); float32 scenes stay float32.  The blend runs in
 FP32; see DESIGN.md for the parity contract.
 """
 
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -167,11 +168,39 @@ def resolve_threads(threads):
     return 1 if threads is None else max(1, int(threads))
 
 
+class _WorkspacePool:
+    """Device workspaces recycled across calls.  A FrameGeometry owns one until it
+    is garbage collected, so a frame kept for a later render_backward is never
+    overwritten, while a plain render -> render_backward loop reuses the same
+    buffers every iteration (no cudaMalloc/cudaFree in steady state)."""
+
+    def __init__(self, keep=2):
+        self.keep = keep
+        self.free = {}
+
+    def acquire(self, device):
+        lst = self.free.setdefault(str(device), [])
+        return lst.pop() if lst else _dev.Workspace(device)
+
+    def release(self, device, ws):
+        lst = self.free.setdefault(str(device), [])
+        if len(lst) < self.keep:
+            lst.append(ws)
+
+
+_POOL = _WorkspacePool()
+
+
 def prepare(scene, cam, kernel="half"):
     """Project a scene into one view; returns FrameGeometry (rasterizer.py:159)."""
     dscene = Scene.from_any(scene)
-    dframe = _dev.prepare(dscene, cam, kernel)
-    return FrameGeometry(dframe, dscene, kernel)
+    ws = _POOL.acquire(dscene.device)
+    dframe = _dev.prepare(dscene, cam, kernel, ws=ws)
+    fg = FrameGeometry(dframe, dscene, kernel)
+    fg._ws = ws
+    fg._ws_gen = [0]  # renders issued into this workspace
+    weakref.finalize(fg, _POOL.release, dscene.device, ws)
+    return fg
 
 
 def render(scene, cam, kernel="half", threads=None, frame=None):
@@ -181,12 +210,14 @@ def render(scene, cam, kernel="half", threads=None, frame=None):
     if frame is None:
         frame = prepare(scene, cam, kernel)
     dscene = frame._scene
-    dout = _dev.render(dscene, cam, kernel, frame=frame._device)
+    dout = _dev.render(dscene, cam, kernel, frame=frame._device, ws=frame._ws)
+    frame._ws_gen[0] += 1
     color, alpha, depth, trans, term, radii = _to_host(
         [dout.color, dout.alpha, dout.depth, dout.transmittance, dout.terminal, dout.radii])
     out = RenderOutput(color=color, alpha=alpha, depth=depth, per_pixel_terminal_index=term,
                        camera=cam, transmittance=trans, frame=frame, radii=radii)
     out._device_out = dout
+    out._gen = frame._ws_gen[0]
     out._host_scene = scene
     return out
 
@@ -204,6 +235,8 @@ def render_backward(scene, cam, out, d_color, threads=None):
     if np.shape(out.per_pixel_terminal_index) != (cam.height, cam.width):
         raise MismatchedForward("terminal-index shape mismatch")
     dout = getattr(out, "_device_out", None)
+    if dout is not None and getattr(out, "_gen", None) != frame._ws_gen[0]:
+        dout = None  # the frame was rendered again since: its device buffers moved on
     dscene = frame._scene if getattr(out, "_host_scene", None) is scene else Scene.from_any(scene)
     if dout is None:
         # a RenderOutput assembled by the caller: upload its bookkeeping

@@ -77,5 +77,5 @@ def test_struct_layouts_match_header():
     # field order/size of the ctypes mirrors (the C compiler's layout for x86-64)
     assert ctypes.sizeof(_native.HsCamera) == 16 * 8 + 5 * 8 + 3 * 8 + 2 * 4
     assert ctypes.sizeof(_native.HsScene) == 8 + 4 + 4 + 7 * 8 + 3 * 8
-    assert ctypes.sizeof(_native.HsGrads) == 9 * 8
+    assert ctypes.sizeof(_native.HsGrads) == 9 * 8 + 8  # + int32 accumulate, padded
     assert _native.HsFrame.num_pairs.offset == 40

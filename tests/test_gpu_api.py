@@ -195,3 +195,36 @@ def test_multiview_accumulation_equals_sum(cuda):
         total += g.flat
     torch.testing.assert_close(batch.flat, total, rtol=1e-6, atol=1e-7)
     assert batch.touch_count.max().item() <= 4
+
+
+def test_torch_autograd_matches_oracle(cuda):
+    """rasterize_half_gaussians: loss.backward() gives the oracle's GradientSet."""
+    from oracle import oracle as O
+    from paper_2406_02720_b200.torch_api import (HalfGaussianRasterizationSettings,
+                                                 HalfGaussianRasterizer)
+    sa = scenes.frustum(3000, 2, 160, 120, seed=12)
+    cam = sa.cameras[0]
+    settings = HalfGaussianRasterizationSettings(
+        image_height=cam["height"], image_width=cam["width"], world_to_cam=cam["world_to_cam"],
+        fx=cam["fx"], fy=cam["fy"], cx=cam["cx"], cy=cam["cy"], sh_degree=sa.sh_degree,
+        background=tuple(sa.background_color))
+    params = {f: torch.tensor(getattr(sa, f), device="cuda", requires_grad=True)
+              for f in sa.FIELDS}
+    rast = HalfGaussianRasterizer(settings)
+    color, radii = rast(params["mu"], params["normal"], params["raw_opacity_a"],
+                        params["raw_opacity_b"], params["log_scale"], params["rotation"],
+                        params["sh_coeffs"])
+    d_color = scenes.cotangent(cam["height"], cam["width"], seed=3)
+    loss = (color * torch.as_tensor(d_color, dtype=torch.float32, device="cuda")).sum()
+    loss.backward()
+    s64 = sa.as_float64()
+    ref = O.render(s64, CameraModel(**cam))
+    rg = O.render_backward(s64, CameraModel(**cam), ref, d_color)
+    assert abs(loss.item() - float((ref.color * d_color).sum())) < 1e-3 * abs(loss.item()) + 1e-2
+    got = {"d_mu": params["mu"].grad, "d_log_scale": params["log_scale"].grad,
+           "d_rotation": params["rotation"].grad, "d_sh": params["sh_coeffs"].grad,
+           "d_normal": params["normal"].grad, "d_raw_opacity_a": params["raw_opacity_a"].grad,
+           "d_raw_opacity_b": params["raw_opacity_b"].grad}
+    assert_grads({k: v.double().cpu().numpy() for k, v in got.items()},
+                 {k: rg[k] for k in got}, groups=tuple(got))
+    assert (radii.cpu().numpy() > 0).sum() == ref.frame.valid.shape[0]
