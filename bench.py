@@ -186,6 +186,27 @@ def run_reference_arm(args):
     print(json.dumps(line), flush=True)
 
 
+def committed_traffic(kernel):
+    """dram read+write bytes per launch of `kernel` from the committed ncu --set full
+    summary (profiles/round*/ncu_<kernel>.txt, c3), or None."""
+    import glob
+    import re
+    files = sorted(glob.glob(os.path.join(REPO, "profiles", "round*", f"ncu_{kernel}.txt")))
+    if not files:
+        return None
+    text = open(files[-1]).read()
+    tot = 0.0
+    for key in ("dram read", "dram write"):
+        m = re.search(rf"{key}\s+([0-9.]+)\s+(\w+)", text)
+        if not m:
+            return None
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(m.group(2), None)
+        if scale is None:
+            return None
+        tot += float(m.group(1)) * scale
+    return {"bytes_per_launch": tot, "source": os.path.relpath(files[-1], REPO)}
+
+
 def metric_name(cfg):
     if cfg == "c3":
         return "fwd+bwd iters/s (1M half-Gaussians, 1080p)"
@@ -319,7 +340,7 @@ def main():
     achieved = bwd_evals * BWD_FLOPS_PER_EVAL / (bwd_ms * 1e-3) / 1e12
     roofline = {
         "bound": "fp32", "kernel": "blend_bwd (K6)", "achieved": achieved, "peak": fp32_peak,
-        "unit": "TFLOP/s", "frac": achieved / fp32_peak, "traffic": None,
+        "unit": "TFLOP/s", "frac": achieved / fp32_peak, "traffic": committed_traffic("blend_bwd"),
         "peak_source": "measured on this GPU by hs_measure_fp32_peaks (FMA probe; "
                        "MEASURED_PEAKS.json has no FP32 entry)",
         "algorithmic": f"{bwd_evals} bwd evals x {BWD_FLOPS_PER_EVAL} flops per launch",
