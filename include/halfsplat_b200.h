@@ -168,6 +168,13 @@ int hs_frame_export(const hs_frame* frame, int32_t* valid, int64_t* m_out,
                     float* packed, int8_t* mode, int32_t* tile_rect,
                     int32_t* pair_splat, int64_t* tile_starts, void* stream);
 
+/* ScreenSplat export (rasterizer.py:578-603): for every primitive 20 doubles
+ * (zeros when culled): mu_hat x,y; conic a,b,c; whiten2d v00,v10,v11;
+ * n_ray x,y,z; alpha1, alpha2; rgb (3); depth; radius; za, zb.  `out` is a
+ * device array of n*20 doubles. */
+int hs_screen_splats(const hs_scene* scene, const hs_camera* cam, int32_t kernel, double* out,
+                     void* stream);
+
 /* ---- Seam 1: blend-core plugin (host float64 arrays) ------------------- */
 int hs_forward_tiles(const double* packed, const int8_t* mode,
                      const int32_t* pair_splat, const int64_t* tile_starts,

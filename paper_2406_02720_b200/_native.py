@@ -91,6 +91,8 @@ _SIGNATURES = {
                                     ctypes.POINTER(HsCamera), ctypes.POINTER(HsGrads), c_void_p]),
     "hs_frame_export": (c_int32, [ctypes.POINTER(HsFrame), c_void_p, c_void_p, c_void_p,
                                   c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "hs_screen_splats": (c_int32, [ctypes.POINTER(HsScene), ctypes.POINTER(HsCamera), c_int32,
+                                   c_void_p, c_void_p]),
     "hs_forward_tiles": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int64,
                                    c_int32, c_int32, c_int32, c_void_p, c_void_p, c_void_p,
                                    c_void_p, c_void_p, c_void_p, c_int32, c_int32]),

@@ -445,6 +445,22 @@ int hs_frame_export(const hs_frame* frame, int32_t* valid, int64_t* m_out, float
   return HS_OK;
 }
 
+int hs_screen_splats(const hs_scene* scene, const hs_camera* cam, int32_t kernel, double* out,
+                     void* stream_) {
+  if (!scene || !cam || !out) return HS_ERR_INVALID_ARG;
+  if (scene->n <= 0) return HS_ERR_EMPTY_SCENE;
+  if (kernel != HS_KERNEL_HALF && kernel != HS_KERNEL_FULL) return HS_ERR_INVALID_KERNEL;
+  const CamArgs ca = cam_args(cam);
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  if (scene->dtype == HS_DTYPE_F32)
+    HS_CUDA(launch_screen_splats_t<float>(scene_args<float>(scene), ca, kernel, scene->n, out,
+                                          stream));
+  else
+    HS_CUDA(launch_screen_splats_t<double>(scene_args<double>(scene), ca, kernel, scene->n, out,
+                                           stream));
+  return HS_OK;
+}
+
 // ---- Seam 1 ----------------------------------------------------------------
 namespace {
 struct DevBuf {

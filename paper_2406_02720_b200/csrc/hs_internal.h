@@ -58,6 +58,10 @@ cudaError_t launch_preprocess_bwd_t(const SceneArgs<T>& sc, const CamArgs& cam, 
                                     const int32_t* last_rank, const float* rows, float4* merged,
                                     const GradArgs<T>& out, cudaStream_t stream);
 
+template <typename T>
+cudaError_t launch_screen_splats_t(const SceneArgs<T>& sc, const CamArgs& cam, int kernel,
+                                   int64_t n, double* out, cudaStream_t stream);
+
 // ---- hs_blend.cu ------------------------------------------------------------
 struct BlendGeom {
   const int32_t* tile_starts;  // (n_tiles+1) CSR offsets into pair_src

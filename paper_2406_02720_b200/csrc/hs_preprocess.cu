@@ -426,11 +426,67 @@ __global__ void __launch_bounds__(NT) preprocess_fwd_kernel(
 }
 
 // ---------------------------------------------------------------------------
+// ScreenSplat export (rasterizer.py:578-603): the FP64 projected quantities of
+// every visible primitive (introspection only; reads the scene directly).
+template <typename T, int K>
+struct GlobalView {
+  const SceneArgs<T>& sc;
+  int64_t i;
+  __device__ __forceinline__ double mu(int k) const { return (double)sc.mu[3 * i + k]; }
+  __device__ __forceinline__ double ls(int k) const { return (double)sc.ls[3 * i + k]; }
+  __device__ __forceinline__ double rot(int k) const { return (double)sc.rot[4 * i + k]; }
+  __device__ __forceinline__ double nrm(int k) const { return (double)sc.nrm[3 * i + k]; }
+  __device__ __forceinline__ double ra() const { return (double)sc.ra[i]; }
+  __device__ __forceinline__ double rb() const { return (double)sc.rb[i]; }
+  __device__ __forceinline__ double sh(int k, int ch) const {
+    return (double)sc.sh[(i * K + k) * 3 + ch];
+  }
+};
+
+template <typename T, int DEG>
+__global__ void __launch_bounds__(128) screen_splats_kernel(SceneArgs<T> sc, CamArgs cam,
+                                                            int kernel, int64_t n,
+                                                            double* __restrict__ out) {
+  constexpr int K = (DEG + 1) * (DEG + 1);
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  FwdState st;
+  forward_state<DEG>(GlobalView<T, K>{sc, i}, cam, kernel, st);
+  double* o = out + 20 * i;
+  if (!st.visible) {
+    for (int k = 0; k < 20; ++k) o[k] = 0.0;
+    return;
+  }
+  const double v[20] = {st.mux, st.muy, st.c / st.det, -st.b / st.det, st.a / st.det,
+                        st.v00, st.v10, st.v11, st.nray[0], st.nray[1], st.nray[2],
+                        st.a1, st.a2, fmax(st.rgbu[0], 0.0), fmax(st.rgbu[1], 0.0),
+                        fmax(st.rgbu[2], 0.0), st.t[2], st.radius, st.za, st.zb};
+  for (int k = 0; k < 20; ++k) o[k] = v[k];
+}
+
+template <typename T>
+cudaError_t launch_screen_splats_t(const SceneArgs<T>& sc, const CamArgs& cam, int kernel,
+                                   int64_t n, double* out, cudaStream_t stream) {
+  const int64_t grid = (n + 127) / 128;
+  switch (sc.deg) {
+    case 0: screen_splats_kernel<T, 0><<<(unsigned)grid, 128, 0, stream>>>(sc, cam, kernel, n, out); break;
+    case 1: screen_splats_kernel<T, 1><<<(unsigned)grid, 128, 0, stream>>>(sc, cam, kernel, n, out); break;
+    case 2: screen_splats_kernel<T, 2><<<(unsigned)grid, 128, 0, stream>>>(sc, cam, kernel, n, out); break;
+    case 3: screen_splats_kernel<T, 3><<<(unsigned)grid, 128, 0, stream>>>(sc, cam, kernel, n, out); break;
+    default: return cudaErrorInvalidValue;
+  }
+  note_launch();
+  return cudaGetLastError();
+}
+template cudaError_t launch_screen_splats_t<float>(const SceneArgs<float>&, const CamArgs&, int,
+                                                   int64_t, double*, cudaStream_t);
+template cudaError_t launch_screen_splats_t<double>(const SceneArgs<double>&, const CamArgs&, int,
+                                                    int64_t, double*, cudaStream_t);
+
+// ---------------------------------------------------------------------------
 // K7: merge the splat's pair rows (np.add.at, rasterizer.py:419-420) and chain
 // them through the projection to the primitive parameters
 // (_geometry_backward, rasterizer.py:424-575).  FP64 throughout.
-// K7 body for one primitive: reads its staged inputs, overwrites the same
-// slots with its gradients (each thread touches only its own slots).
 // K7a: merge each visible splat's pair rows (np.add.at, rasterizer.py:419-420):
 // the tiles of its rect in row-major (= sorted k) order, skipping pairs past
 // the tile's last composited position (never written by K6).  A separate,

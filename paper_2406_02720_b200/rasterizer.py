@@ -11,6 +11,7 @@ exactly the reference's inputs); float32 scenes stay float32.  The blend runs in
 FP32; see DESIGN.md for the parity contract.
 """
 
+import ctypes
 import weakref
 from dataclasses import dataclass
 
@@ -33,14 +34,13 @@ class ScreenSplat:
     prim_index: int
     mu_hat: np.ndarray
     conic: np.ndarray
-    mode: int
-    za: float
-    zb: float
-    c1: float
-    c2: float
+    whiten2d: np.ndarray
+    n_ray: np.ndarray
+    alpha1: float
+    alpha2: float
     rgb: np.ndarray
     depth: float
-    tile_span: tuple
+    tile_span: tuple  # (tx0, tx1, ty0, ty1), inclusive
 
 
 @dataclass
@@ -257,16 +257,24 @@ def render_backward(scene, cam, out, d_color, threads=None):
 
 def screen_splats(scene, cam, kernel="half"):
     """Per-primitive projected splats for one view (rasterizer.py:578-603)."""
+    cam = CameraModel.from_any(cam)
     frame = prepare(scene, cam, kernel)
     ex = frame._exported()
+    dscene = frame._scene
+    vals = torch.empty((len(dscene), 20), dtype=torch.float64, device=dscene.device)
+    lib = _dev._native.load()
+    _dev._native.check(lib.hs_screen_splats(
+        ctypes.byref(_dev.scene_struct(dscene)), ctypes.byref(_dev.camera_struct(cam)),
+        0 if kernel == "half" else 1, _dev._ptr(vals), _dev._stream()), "hs_screen_splats")
+    vals = vals.cpu().numpy()
     out = []
-    for i in range(ex["valid"].shape[0]):
-        row = ex["packed"][i].astype(np.float64)
+    for i, prim in enumerate(ex["valid"]):
+        v = vals[prim]
         out.append(ScreenSplat(
-            prim_index=int(ex["valid"][i]), mu_hat=row[0:2].copy(),
-            conic=np.array([[row[2], row[3]], [row[3], row[4]]]), mode=int(ex["mode"][i]),
-            za=float(row[5]), zb=float(row[6]), c1=float(row[7]), c2=float(row[8]),
-            rgb=row[9:12].copy(), depth=float(row[12]),
+            prim_index=int(prim), mu_hat=v[0:2].copy(),
+            conic=np.array([[v[2], v[3]], [v[3], v[4]]]),
+            whiten2d=np.array([[v[5], 0.0], [v[6], v[7]]]), n_ray=v[8:11].copy(),
+            alpha1=float(v[11]), alpha2=float(v[12]), rgb=v[13:16].copy(), depth=float(v[16]),
             tile_span=tuple(int(x) for x in ex["tile_rect"][i])))
     return out
 
