@@ -333,10 +333,13 @@ struct BwdPix {
   int cnt[kPx];
 };
 
-// FAST: mode 0 or 2, FP32 z, no clamp, and every pixel of the warp active at
-// this position (pos < warp-min of the terminal counts).  Packed pixel pairs.
-__device__ __forceinline__ void bwd_splat_fast(const float4 (&q)[4], float px, float py0,
-                                               BwdPix& P, BwdAcc& out) {
+// FAST: mode 0 or 2, FP32 z, no clamp.  Packed pixel pairs.  ALL: every pixel
+// of the warp is active at this position (pos < warp-min of the terminal
+// counts); otherwise inactive pixels are masked with selects and contribute
+// exact zeros (pixels terminated early, as in heavily occluded views).
+template <bool ALL>
+__device__ __forceinline__ void bwd_splat_fast(const float4 (&q)[4], int pos, float px,
+                                               float py0, BwdPix& P, BwdAcc& out) {
   const SteepRec none{};
   const SplatLane s = splat_lane<false>(q, none, px, py0);
   const float c1 = q[1].w, c2 = q[2].x;
@@ -354,13 +357,16 @@ __device__ __forceinline__ void bwd_splat_fast(const float4 (&q)[4], float px, f
     const float2 om = fadd2(f2(1.0f), neg2(w));
     const float2 inv = make_float2(rcp_approx(om.x), rcp_approx(om.y));  // 1 - w >= 0.01
     const float2 Tp = fmul2(P.T[p], inv);
-    const float2 wt = fmul2(w, Tp);
+    const bool ax = ALL || pos < P.cnt[2 * p], ay = ALL || pos < P.cnt[2 * p + 1];
+    float2 wt = fmul2(w, Tp);
+    if (!ALL) wt = make_float2(ax ? wt.x : 0.f, ay ? wt.y : 0.f);
     const float2 dcr = ffma2(P.dr[p], f2(cr), ffma2(P.dg[p], f2(cg), fmul2(P.db[p], f2(cb))));
     ar = ffma2(P.dr[p], wt, ar);
     ag = ffma2(P.dg[p], wt, ag);
     ab = ffma2(P.db[p], wt, ab);
     // d_w = T_prev*(dC.rgb) - (dC.S)/(1-w) = inv*(T*dcr - D) (_blend_cy.pyx:310-312)
-    const float2 d_w = fmul2(inv, ffma2(P.T[p], dcr, neg2(P.D[p])));
+    float2 d_w = fmul2(inv, ffma2(P.T[p], dcr, neg2(P.D[p])));
+    if (!ALL) d_w = make_float2(ax ? d_w.x : 0.f, ay ? d_w.y : 0.f);
     const float2 dwg = fmul2(d_w, gg);
     const float2 d_pow = fmul2(dwg, u);
     s0 = fadd2(s0, d_pow);
@@ -375,7 +381,7 @@ __device__ __forceinline__ void bwd_splat_fast(const float4 (&q)[4], float px, f
     q1 = ffma2(dz, dy, q1);
     qz = ffma2(dz, zz, qz);
     P.D[p] = ffma2(wt, dcr, P.D[p]);
-    P.T[p] = Tp;
+    P.T[p] = ALL ? Tp : make_float2(ax ? Tp.x : P.T[p].x, ay ? Tp.y : P.T[p].y);
   }
   const float c2k = c2 * (2.0f * kInvSqrtPi);
   out.s0 = s0.x + s0.y; out.s1 = s1.x + s1.y; out.s2 = s2.x + s2.y;
@@ -551,10 +557,14 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) blend_bwd_kernel(
         const uint32_t flags = __float_as_uint(q[3].y);
         const int mode = (int)(flags & 3u);
         BwdAcc a;
-        if (pos < minc && fast_flags(flags))
-          bwd_splat_fast(q, px, py0, P, a);
-        else
+        if (fast_flags(flags)) {
+          if (pos < minc)
+            bwd_splat_fast<true>(q, pos, px, py0, P, a);
+          else
+            bwd_splat_fast<false>(q, pos, px, py0, P, a);
+        } else {
           bwd_splat_generic(q, side, flags, pos, px, py0, P, a);
+        }
         // per-lane partials -> the pair-row columns (_blend_py.py:16-18)
         const float ca = q[0].z, cb = q[0].w, cc = q[1].x, za = q[1].y, zb = q[1].z;
         const float2 lo = __half22float2(*reinterpret_cast<const __half2*>(&q[3].w));
