@@ -28,6 +28,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", CSRC, "
           "--expt-relaxed-constexpr", "-Xptxas", "-v"]
 SOURCES = {
     "hs_preprocess.cu": ["-fmad=false"],
+    "hs_geometry_bwd.cu": [],
     "hs_binning.cu": [],
     "hs_blend.cu": [],
     "hs_capi.cu": [],

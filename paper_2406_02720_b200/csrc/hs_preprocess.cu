@@ -1,13 +1,18 @@
 // hs_preprocess.cu -- K1 (per-Gaussian preprocess) and K7 (per-Gaussian
 // geometry backward), one thread per primitive, FP64 geometry.
 //
-// This translation unit is compiled with -fmad=false: every floating-point
+// K1 is compiled with -fmad=false: every floating-point
 // operation below rounds exactly where the reference's numpy expression rounds,
 // and fma() appears only where numpy's own kernels fuse (the (N,3)@(3,3) and
 // batched 3x3 matmuls go through OpenBLAS FMA chains; the einsum reductions do
 // not).  With the same inputs this reproduces prepare()'s FP64 intermediates
 // bit for bit except where libm/numpy `exp` differ by an ulp, which is what makes
 // `valid`, `tile_rect`, `mode` and the sort order exact.
+//
+// K7 needs no such exactness (its outputs are gradients under a 1e-3 contract),
+// so hs_geometry_bwd.cu compiles this same file with HS_GEOMETRY_BWD_TU defined
+// and FMA contraction on; it replays K1's discrete decisions from the record
+// flags (forward_state<..., kReplay>).
 #include <cmath>
 #include <cstdint>
 
@@ -192,7 +197,7 @@ __device__ __forceinline__ void cp_async_elem(T* smem, const T* gmem) {
 
 template <typename T, int K, int NT>
 __device__ __forceinline__ void stage_in(Staged<T, K, NT>& s, const SceneArgs<T>& sc,
-                                         int64_t base, int cnt) {
+                                         int64_t base, int cnt, bool wait = true) {
   const int tid = threadIdx.x;
   for (int e = tid; e < cnt * 3; e += NT) {
     cp_async_elem(&s.mu[e], &sc.mu[base * 3 + e]);
@@ -208,8 +213,11 @@ __device__ __forceinline__ void stage_in(Staged<T, K, NT>& s, const SceneArgs<T>
     const int t = e / (3 * K), c = e - t * (3 * K);
     cp_async_elem(&s.sh[t * Staged<T, K, NT>::SHS + c], &sc.sh[base * 3 * K + e]);
   }
-  asm volatile("cp.async.wait_all;\n" ::);
-  __syncthreads();
+  asm volatile("cp.async.commit_group;\n" ::);
+  if (wait) {
+    asm volatile("cp.async.wait_all;\n" ::);
+    __syncthreads();
+  }
 }
 
 // One thread's view of its staged primitive (the inputs of forward_state).
@@ -228,9 +236,12 @@ struct StagedView {
   }
 };
 
-template <int DEG, typename Src>
+// kReplay (K7): the primitive is known visible and K1's discrete decisions --
+// the identity-whitening fallback and the blend mode -- are taken from its
+// record flags, so a K7 build with different rounding cannot branch otherwise.
+template <int DEG, bool kReplay = false, typename Src>
 __device__ __forceinline__ void forward_state(const Src& src, const CamArgs& cam, int kernel,
-                                              FwdState& st) {
+                                              FwdState& st, uint32_t flags = 0) {
   constexpr int K = (DEG + 1) * (DEG + 1);
   const double m0 = src.mu(0), m1 = src.mu(1), m2 = src.mu(2);
   // t_all = mu @ rot.T + translation (rasterizer.py:170)
@@ -260,7 +271,7 @@ __device__ __forceinline__ void forward_state(const Src& src, const CamArgs& cam
       st.cov[3 * a + d] = fma(M[3 * a + 2], M[3 * d + 2],
                               fma(M[3 * a + 1], M[3 * d + 1], M[3 * a] * M[3 * d]));
   st.visible = false;
-  if (!st.in_front) return;
+  if (!kReplay && !st.in_front) return;
   // cov_cam, Jacobian, ray covariance (rasterizer.py:183-185; geometry.py:189-207)
   sandwich(cam.R, st.cov, st.ccam);
   const double tx = st.t[0], ty = st.t[1], tz = st.t[2];
@@ -285,8 +296,8 @@ __device__ __forceinline__ void forward_state(const Src& src, const CamArgs& cam
   long long y0 = to_i64_numpy(ceil(st.muy - st.radius - 0.5));
   long long y1 = to_i64_numpy(floor(st.muy + st.radius - 0.5));
   const long long W1 = cam.width - 1, H1 = cam.height - 1;
-  st.visible = (x1 >= 0) && (x0 <= W1) && (y1 >= 0) && (y0 <= H1) && (x1 >= x0) &&
-               (y1 >= y0) && (st.det > 0.0);
+  st.visible = kReplay || ((x1 >= 0) && (x0 <= W1) && (y1 >= 0) && (y0 <= H1) && (x1 >= x0) &&
+                           (y1 >= y0) && (st.det > 0.0));
   if (!st.visible) return;
   st.px0 = x0 < 0 ? 0 : (x0 > W1 ? W1 : x0);  // np.clip, rasterizer.py:225-228
   st.px1 = x1 < 0 ? 0 : (x1 > W1 ? W1 : x1);
@@ -307,7 +318,9 @@ __device__ __forceinline__ void forward_state(const Src& src, const CamArgs& cam
     const double dmin = fmin(fmin(l00, l11), l22), dmax = fmax(fmax(l00, l11), l22);
     const bool finite = isfinite(l00) && isfinite(l11) && isfinite(l22);
     // numpy min/max propagate NaN; any NaN diag already fails `finite`.
-    st.bad = (d0 <= 0.0) || (d1 <= 0.0) || (d2 <= 0.0) || !finite || (dmin * kCondLimit < dmax);
+    st.bad = kReplay ? (flags & kFlagBad) != 0
+                     : (d0 <= 0.0) || (d1 <= 0.0) || (d2 <= 0.0) || !finite ||
+                           (dmin * kCondLimit < dmax);
     for (int k = 0; k < 9; ++k) st.L[k] = 0.0;
     if (st.bad) {
       st.L[0] = st.L[4] = st.L[8] = 1.0;
@@ -331,7 +344,7 @@ __device__ __forceinline__ void forward_state(const Src& src, const CamArgs& cam
   st.y[1] = (st.hr[1] - st.L[3] * st.y[0]) / st.L[4];
   st.y[2] = (st.hr[2] - st.L[6] * st.y[0] - st.L[7] * st.y[1]) / st.L[8];
   const double yn = sqrt(st.y[0] * st.y[0] + st.y[1] * st.y[1] + st.y[2] * st.y[2]);
-  st.bad = st.bad || (yn < 1e-12) || !isfinite(yn);
+  if (!kReplay) st.bad = st.bad || (yn < 1e-12) || !isfinite(yn);
   st.ynorm = st.bad ? 1.0 : yn;
   if (st.bad) {
     st.nray[0] = 0.0; st.nray[1] = 0.0; st.nray[2] = 1.0;
@@ -347,7 +360,9 @@ __device__ __forceinline__ void forward_state(const Src& src, const CamArgs& cam
     st.mode = kModePlain;
   } else {
     st.c2 = 0.5 * (st.a1 - st.a2);
-    st.mode = st.bad ? kModePlain : (fabs(st.nray[2]) < kNormalEps ? kModeSign : kModeErf);
+    st.mode = kReplay ? (int)(flags & 3u)
+                      : st.bad ? kModePlain
+                               : (fabs(st.nray[2]) < kNormalEps ? kModeSign : kModeErf);
   }
   st.za = 0.0;
   st.zb = 0.0;
@@ -373,6 +388,7 @@ __device__ __forceinline__ void forward_state(const Src& src, const CamArgs& cam
   }
 }
 
+#ifndef HS_GEOMETRY_BWD_TU
 // ---------------------------------------------------------------------------
 // K1: preprocess forward.  Writes the 64-B record, tile rect, pair count and
 // the depth-rank sort key of each primitive (culled: count 0, key ~0).
@@ -416,7 +432,7 @@ __global__ void __launch_bounds__(NT) preprocess_fwd_kernel(
   float4 r1 = make_float4((float)(st.a / st.det), (float)st.za, (float)st.zb, (float)st.c1);
   float4 r2 = make_float4((float)st.c2, (float)fmax(st.rgbu[0], 0.0), (float)fmax(st.rgbu[1], 0.0),
                           (float)fmax(st.rgbu[2], 0.0));
-  float4 r3 = make_float4((float)st.t[2], __uint_as_float(pack_flags(st.mode, steep, may_clamp(st.c1, st.c2), spans_x)),
+  float4 r3 = make_float4((float)st.t[2], __uint_as_float(pack_flags(st.mode, steep, may_clamp(st.c1, st.c2), spans_x, st.bad)),
                           __uint_as_float(0u), __uint_as_float(*reinterpret_cast<const uint32_t*>(&lo)));
   float4* dst = rec + 4 * i;
   dst[0] = r0;
@@ -483,6 +499,9 @@ template cudaError_t launch_screen_splats_t<float>(const SceneArgs<float>&, cons
 template cudaError_t launch_screen_splats_t<double>(const SceneArgs<double>&, const CamArgs&, int,
                                                     int64_t, double*, cudaStream_t);
 
+#endif  // !HS_GEOMETRY_BWD_TU
+
+#ifdef HS_GEOMETRY_BWD_TU
 // ---------------------------------------------------------------------------
 // K7: merge the splat's pair rows (np.add.at, rasterizer.py:419-420) and chain
 // them through the projection to the primitive parameters
@@ -505,7 +524,8 @@ __global__ void __launch_bounds__(256) merge_rows_kernel(
   for (int k = 0; k < 13; ++k) m[k] = 0.0;
   const int4 rc = rect[i];
   const int spans_x = rc.y - rc.x + 1;
-  const int base = __float_as_int(rec[4 * i + 3].z) + rc.z * spans_x + rc.x;
+  const float4 r3 = rec[4 * i + 3];
+  const int base = __float_as_int(r3.z) + rc.z * spans_x + rc.x;
   const int r = (int)rank_of[i];
   int lx = 0, ly = 0;
   for (int l = 0; l < cnt; ++l) {
@@ -526,7 +546,7 @@ __global__ void __launch_bounds__(256) merge_rows_kernel(
   dst[0] = make_float4((float)m[0], (float)m[1], (float)m[2], (float)m[3]);
   dst[1] = make_float4((float)m[4], (float)m[5], (float)m[6], (float)m[7]);
   dst[2] = make_float4((float)m[8], (float)m[9], (float)m[10], (float)m[11]);
-  dst[3] = make_float4((float)m[12], 0.f, 0.f, 0.f);
+  dst[3] = make_float4((float)m[12], r3.y, 0.f, 0.f);  // .y: K1's record flags for K7
 }
 
 template <typename T, int DEG, int NT>
@@ -547,6 +567,7 @@ __device__ __forceinline__ void preprocess_bwd_one(
     return;
   }
   double m[13];
+  uint32_t flags;
   {
     const float4* src = merged + 4 * i;
     const float4 u0 = src[0], u1 = src[1], u2 = src[2], u3 = src[3];
@@ -554,9 +575,10 @@ __device__ __forceinline__ void preprocess_bwd_one(
     m[4] = u1.x; m[5] = u1.y; m[6] = u1.z; m[7] = u1.w;
     m[8] = u2.x; m[9] = u2.y; m[10] = u2.z; m[11] = u2.w;
     m[12] = u3.x;
+    flags = __float_as_uint(u3.y);
   }
   FwdState st;
-  forward_state<DEG>(StagedView<T, K, NT>{sm, t}, cam, kernel, st);
+  forward_state<DEG, true>(StagedView<T, K, NT>{sm, t}, cam, kernel, st, flags);
 
   const double d_mux = m[0], d_muy = m[1];
   const double d_ca = m[2], d_cb = m[3], d_cc = m[4];
@@ -785,43 +807,148 @@ __device__ __forceinline__ void preprocess_bwd_one(
   touch_s[t] = 1;
 }
 
+template <typename E> struct Vec16;
+template <> struct Vec16<float> { using type = float4; };
+template <> struct Vec16<double> { using type = double2; };
+template <> struct Vec16<int32_t> { using type = int4; };
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem));
+}
+
+// Does any primitive of elements [e0, e0 + len) (S elements per primitive) have
+// a non-zero flag?
+template <int S>
+__device__ __forceinline__ bool any_live(const int32_t* live, int e0, int len) {
+  bool any = false;
+  for (int p = e0 / S; p <= (e0 + len - 1) / S; ++p) any |= live[p] != 0;
+  return any;
+}
+
+// Accumulation targets of one CTA, prefetched into shared memory while the
+// geometry backward runs (field order and layout as in global memory, so both
+// copies move in 16-B pieces).
+template <typename T, int K, int NT>
+struct GradStage {
+  T mu[NT * 3], ls[NT * 3], nrm[NT * 3], rot[NT * 4], ra[NT], rb[NT], pgn[NT];
+  int32_t touch[NT];
+  T sh[NT * 3 * K];
+};
+
+// One field of the CTA's `cnt` primitives (S elements each, contiguous from
+// `src`): global -> shared with cp.async, skipping primitives this view does
+// not touch.  16-B copies when `src` is 16-B aligned, element copies otherwise.
+template <int NT, int S, typename E>
+__device__ __forceinline__ void prefetch_block(E* smem, const E* src, int cnt,
+                                               const int32_t* live) {
+  constexpr int kV = 16 / sizeof(E);
+  const int n = cnt * S;
+  const int nv = ((uintptr_t)src & 15) ? 0 : n / kV;
+  for (int v = threadIdx.x; v < nv; v += NT)
+    if (any_live<S>(live, v * kV, kV)) cp_async16(smem + v * kV, src + v * kV);
+  for (int e = nv * kV + threadIdx.x; e < n; e += NT)
+    if (live[e / S]) cp_async_elem(smem + e, src + e);
+}
+
+// Write one field of the CTA's primitives from `get(e)`, or with `old` (the
+// prefetched targets) add into it, skipping primitives this view did not touch
+// (their gradient is zero).  16-B stores when `dst` is 16-B aligned.
+template <int NT, int S, typename E, typename Get>
+__device__ __forceinline__ void store_block(E* __restrict__ dst, int cnt, const E* old,
+                                            const int32_t* live, Get get) {
+  using V = typename Vec16<E>::type;
+  constexpr int kV = 16 / sizeof(E);
+  const int n = cnt * S;
+  const int nv = ((uintptr_t)dst & 15) ? 0 : n / kV;
+  V* dv = reinterpret_cast<V*>(dst);
+  for (int v = threadIdx.x; v < nv; v += NT) {
+    if (old && !any_live<S>(live, v * kV, kV)) continue;
+    V nw;
+    E* ne = reinterpret_cast<E*>(&nw);
+#pragma unroll
+    for (int j = 0; j < kV; ++j) ne[j] = get(v * kV + j) + (old ? old[v * kV + j] : E(0));
+    dv[v] = nw;
+  }
+  for (int e = nv * kV + threadIdx.x; e < n; e += NT) {
+    if (old && !live[e / S]) continue;
+    dst[e] = get(e) + (old ? old[e] : E(0));
+  }
+}
+
+template <typename T, int K, int NT>
+constexpr size_t k7_dynamic_smem() { return sizeof(GradStage<T, K, NT>); }
+
 template <typename T, int DEG, int NT>
-__global__ void __launch_bounds__(NT) preprocess_bwd_kernel(
+__global__ void __launch_bounds__(NT, 3) preprocess_bwd_kernel(
     SceneArgs<T> sc, CamArgs cam, int kernel, int64_t n, const int32_t* __restrict__ count,
     const float4* __restrict__ merged, GradArgs<T> out) {
   constexpr int K = (DEG + 1) * (DEG + 1);
   using St = Staged<T, K, NT>;
+  using Gs = GradStage<T, K, NT>;
   __shared__ St sm;
   __shared__ T pgn_s[NT];
   __shared__ int32_t touch_s[NT];
+  extern __shared__ __align__(16) unsigned char dyn_smem[];
   const int64_t base = (int64_t)blockIdx.x * NT;
   const int ncta = (int)(n - base < NT ? n - base : NT);
-  stage_in(sm, sc, base, ncta);
   const int t = threadIdx.x;
+  const bool acc = out.accumulate != 0;
+  stage_in(sm, sc, base, ncta, /*wait=*/false);
+  Gs* g = acc ? reinterpret_cast<Gs*>(dyn_smem) : nullptr;
+  if (acc) {
+    // touch_s = visible in this view (count > 0); preprocess_bwd_one rewrites
+    // the same value.  The targets of visible primitives stream in behind the
+    // scene staging and are waited for only before the final stores.
+    touch_s[t] = t < ncta ? (count[base + t] != 0) : 0;
+    __syncthreads();
+    prefetch_block<NT, 3>(g->mu, out.d_mu + base * 3, ncta, touch_s);
+    prefetch_block<NT, 3>(g->ls, out.d_log_scale + base * 3, ncta, touch_s);
+    prefetch_block<NT, 3>(g->nrm, out.d_normal + base * 3, ncta, touch_s);
+    prefetch_block<NT, 4>(g->rot, out.d_rotation + base * 4, ncta, touch_s);
+    prefetch_block<NT, 1>(g->ra, out.d_ra + base, ncta, touch_s);
+    prefetch_block<NT, 1>(g->rb, out.d_rb + base, ncta, touch_s);
+    prefetch_block<NT, 1>(g->pgn, out.pos_grad_norm + base, ncta, touch_s);
+    prefetch_block<NT, 1>(g->touch, out.touch + base, ncta, touch_s);
+    prefetch_block<NT, 3 * K>(g->sh, out.d_sh + base * 3 * K, ncta, touch_s);
+    asm volatile("cp.async.commit_group;\n" ::);
+    asm volatile("cp.async.wait_group 1;\n" ::);
+  } else {
+    asm volatile("cp.async.wait_all;\n" ::);
+  }
+  __syncthreads();
   if (t < ncta)
     preprocess_bwd_one<T, DEG, NT>(sm, pgn_s, touch_s, t, base + t, cam, kernel, count, merged);
+  asm volatile("cp.async.wait_all;\n" ::);
   __syncthreads();
-  // coalesced stores of the staged gradients (or accumulation into them)
-  auto put = [&](T* dst, int64_t k, T v) { dst[k] = out.accumulate ? dst[k] + v : v; };
-  for (int e = t; e < ncta * 3; e += NT) {
-    put(out.d_mu, base * 3 + e, sm.mu[e]);
-    put(out.d_log_scale, base * 3 + e, sm.ls[e]);
-    put(out.d_normal, base * 3 + e, sm.nrm[e]);
-  }
-  for (int e = t; e < ncta * 4; e += NT) put(out.d_rotation, base * 4 + e, sm.rot[e]);
-  for (int e = t; e < ncta; e += NT) {
-    put(out.d_ra, base + e, sm.ra[e]);
-    put(out.d_rb, base + e, sm.rb[e]);
-    put(out.pos_grad_norm, base + e, pgn_s[e]);
-    out.touch[base + e] = out.accumulate ? out.touch[base + e] + touch_s[e] : touch_s[e];
-  }
-  for (int e = t; e < ncta * 3 * K; e += NT) {
-    const int tt = e / (3 * K), c = e - tt * (3 * K);
-    put(out.d_sh, base * 3 * K + e, sm.sh[tt * St::SHS + c]);
-  }
+  store_block<NT, 3>(out.d_mu + base * 3, ncta, acc ? g->mu : nullptr, touch_s,
+                     [&](int e) { return sm.mu[e]; });
+  store_block<NT, 3>(out.d_log_scale + base * 3, ncta, acc ? g->ls : nullptr, touch_s,
+                     [&](int e) { return sm.ls[e]; });
+  store_block<NT, 3>(out.d_normal + base * 3, ncta, acc ? g->nrm : nullptr, touch_s,
+                     [&](int e) { return sm.nrm[e]; });
+  store_block<NT, 4>(out.d_rotation + base * 4, ncta, acc ? g->rot : nullptr, touch_s,
+                     [&](int e) { return sm.rot[e]; });
+  store_block<NT, 1>(out.d_ra + base, ncta, acc ? g->ra : nullptr, touch_s,
+                     [&](int e) { return sm.ra[e]; });
+  store_block<NT, 1>(out.d_rb + base, ncta, acc ? g->rb : nullptr, touch_s,
+                     [&](int e) { return sm.rb[e]; });
+  store_block<NT, 1>(out.pos_grad_norm + base, ncta, acc ? g->pgn : nullptr, touch_s,
+                     [&](int e) { return pgn_s[e]; });
+  store_block<NT, 1>(out.touch + base, ncta, acc ? g->touch : nullptr, touch_s,
+                     [&](int e) { return touch_s[e]; });
+  store_block<NT, 3 * K>(out.d_sh + base * 3 * K, ncta, acc ? g->sh : nullptr, touch_s,
+                         [&](int e) {
+                           const int tt = e / (3 * K);
+                           return sm.sh[tt * St::SHS + (e - tt * 3 * K)];
+                         });
 }
 
+
+#endif  // HS_GEOMETRY_BWD_TU
+
 // ---------------------------------------------------------------------------
+#ifndef HS_GEOMETRY_BWD_TU
 template <typename T>
 cudaError_t launch_preprocess_fwd_t(const SceneArgs<T>& sc, const CamArgs& cam, int kernel,
                                     int64_t n, float4* rec, SteepRec* side, int4* rect,
@@ -845,6 +972,13 @@ cudaError_t launch_preprocess_fwd_t(const SceneArgs<T>& sc, const CamArgs& cam, 
   return cudaGetLastError();
 }
 
+template cudaError_t launch_preprocess_fwd_t<float>(const SceneArgs<float>&, const CamArgs&, int,
+                                                    int64_t, float4*, SteepRec*, int4*, int32_t*,
+                                                    uint64_t*, uint32_t*, int32_t*, cudaStream_t);
+template cudaError_t launch_preprocess_fwd_t<double>(const SceneArgs<double>&, const CamArgs&, int,
+                                                     int64_t, float4*, SteepRec*, int4*, int32_t*,
+                                                     uint64_t*, uint32_t*, int32_t*, cudaStream_t);
+#else
 template <typename T>
 cudaError_t launch_preprocess_bwd_t(const SceneArgs<T>& sc, const CamArgs& cam, int kernel,
                                     int64_t n, int tiles_x, const float4* rec, const int4* rect,
@@ -858,10 +992,15 @@ cudaError_t launch_preprocess_bwd_t(const SceneArgs<T>& sc, const CamArgs& cam, 
   const int64_t grid = (n + NT - 1) / NT;
   switch (sc.deg) {
 #define HS_K7(D)                                                                               \
-  case D:                                                                                      \
-    preprocess_bwd_kernel<T, D, NT><<<(unsigned)grid, NT, 0, stream>>>(                        \
+  case D: {                                                                                    \
+    constexpr size_t dyn = k7_dynamic_smem<T, (D + 1) * (D + 1), NT>();                        \
+    static const cudaError_t attr = cudaFuncSetAttribute(                                      \
+        preprocess_bwd_kernel<T, D, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn); \
+    if (attr != cudaSuccess) return attr;                                                      \
+    preprocess_bwd_kernel<T, D, NT><<<(unsigned)grid, NT, out.accumulate ? dyn : 0, stream>>>( \
         sc, cam, kernel, n, count, merged, out);                                               \
-    break;
+    break;                                                                                     \
+  }
     HS_K7(0) HS_K7(1) HS_K7(2) HS_K7(3)
 #undef HS_K7
     default: return cudaErrorInvalidValue;
@@ -870,12 +1009,6 @@ cudaError_t launch_preprocess_bwd_t(const SceneArgs<T>& sc, const CamArgs& cam, 
   return cudaGetLastError();
 }
 
-template cudaError_t launch_preprocess_fwd_t<float>(const SceneArgs<float>&, const CamArgs&, int,
-                                                    int64_t, float4*, SteepRec*, int4*, int32_t*,
-                                                    uint64_t*, uint32_t*, int32_t*, cudaStream_t);
-template cudaError_t launch_preprocess_fwd_t<double>(const SceneArgs<double>&, const CamArgs&, int,
-                                                     int64_t, float4*, SteepRec*, int4*, int32_t*,
-                                                     uint64_t*, uint32_t*, int32_t*, cudaStream_t);
 template cudaError_t launch_preprocess_bwd_t<float>(const SceneArgs<float>&, const CamArgs&, int,
                                                     int64_t, int, const float4*, const int4*,
                                                     const int32_t*, const uint32_t*, const int32_t*,
@@ -886,5 +1019,6 @@ template cudaError_t launch_preprocess_bwd_t<double>(const SceneArgs<double>&, c
                                                      const int32_t*, const uint32_t*,
                                                      const int32_t*, const float*, float4*,
                                                      const GradArgs<double>&, cudaStream_t);
+#endif  // HS_GEOMETRY_BWD_TU
 
 }  // namespace hs

@@ -331,8 +331,10 @@ class DeviceGradientSet:
         """All float groups as views of one flat buffer (one all-reduce per step)."""
         n, k, dev, dt = len(scene), scene.sh_coeffs.shape[1], scene.device, scene.dtype
         sizes = [3 * n, 3 * n, 4 * n, 3 * k * n, 3 * n, n, n, n]
-        flat = torch.empty(sum(sizes), dtype=dt, device=dev)
-        parts = list(torch.split(flat, sizes))
+        # each group starts 16-B aligned so K7 stores it with vector accesses
+        padded = [(sz + 3) // 4 * 4 for sz in sizes]
+        flat = torch.empty(sum(padded), dtype=dt, device=dev)
+        parts = [p[:sz] for p, sz in zip(torch.split(flat, padded), sizes)]
         g = cls(d_mu=parts[0].view(n, 3), d_log_scale=parts[1].view(n, 3),
                 d_rotation=parts[2].view(n, 4), d_sh=parts[3].view(n, k, 3),
                 d_normal=parts[4].view(n, 3), d_raw_opacity_a=parts[5], d_raw_opacity_b=parts[6],
