@@ -17,6 +17,7 @@ path restated in C, all host threads) on the same config instead.
 """
 
 import argparse
+import contextlib
 import json
 import os
 import statistics
@@ -215,6 +216,10 @@ def metric_name(cfg):
     return f"fwd+bwd iters/s ({cfg})"
 
 
+def metric_unit(multi):
+    return "views/s" if multi else "iters/s"
+
+
 def bench_config(cfg, world, views_per_step=None):
     from paper_2406_02720_b200 import scenes
     c = scenes.CONFIGS[cfg]
@@ -324,6 +329,34 @@ def main():
     barrier()
     fwd_ms = start.elapsed_time(end) / args.steps
 
+    # training iteration with the loss on the device (render -> hs_loss -> backward), the
+    # reference trainer's step minus the optimizer (trainer.py:179-226): synthetic targets
+    from paper_2406_02720_b200.loss import DeviceLoss
+    gen = torch.Generator(device="cuda").manual_seed(7)
+    targets = [torch.rand((c.height, c.width, 3), generator=gen, device="cuda") for c in cams]
+    dloss = DeviceLoss(0.2)
+    loss_timer = device.StageTimer()
+
+    def train_step(t=None):
+        for j, v in enumerate(views):
+            o = rast.render(scene, cams[v])
+            with (t.span("loss") if t is not None else contextlib.nullcontext()):
+                _, d = dloss(o.color, targets[v])
+            rast.render_backward(scene, cams[v], o, d, grads=grads, accumulate=j > 0)
+        if reducer is not None:
+            reducer.allreduce()
+
+    for _ in range(3):
+        train_step()
+    barrier()
+    start.record()
+    for _ in range(args.steps):
+        train_step(loss_timer)
+    end.record()
+    barrier()
+    train_ms = start.elapsed_time(end) / args.steps
+    loss_ms = statistics.mean(loss_timer.totals().get("loss", [float("nan")]))
+
     # algorithmic work of the dominant kernels
     term = out.terminal.to(torch.int64)
     starts = torch.as_tensor(out.frame.export()["tile_starts"], device="cuda")
@@ -367,12 +400,16 @@ def main():
     if rank == 0:
         line = {
             "metric": metric_name(args.config), "value": value,
-            "unit": "views/s" if multi else "iters/s",
+            "unit": metric_unit(multi),
             "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
             "ms_per_step": ms, "higher_is_better": True, "scaling": "strong" if multi else "weak",
             "vs_baseline": None, "dtype": "f32 blend / f64 geometry", "data": "synthetic",
             "config": bench_config(args.config, world, views_per_step),
             "fwd_fps": views_per_step * 1e3 / fwd_ms, "fwd_ms_per_step": fwd_ms,
+            "train_step": {"value": views_per_step * 1e3 / train_ms, "unit": metric_unit(multi),
+                           "ms_per_step": train_ms, "loss_kernel_ms": loss_ms,
+                           "what": "render -> L1+SSIM loss and cotangent on device (hs_loss, "
+                                   "lambda 0.2) -> render_backward, synthetic targets"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clock_info,
             "counts": {"P": out.frame.num_pairs, "fwd_evals": fwd_evals, "bwd_evals": bwd_evals},

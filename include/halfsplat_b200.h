@@ -50,6 +50,8 @@ extern "C" {
 #define HS_ERR_INVALID_ARG 5
 #define HS_ERR_CUDA 6
 #define HS_ERR_WORKSPACE 7          /* workspace missing or too small */
+#define HS_ERR_IMAGE_TOO_SMALL 8    /* errors.ImageTooSmall   (loss.py:52-53) */
+#define HS_ERR_INVALID_LAMBDA 9     /* ValueError on lambda_ssim (loss.py:91-92) */
 
 #define HS_DTYPE_F32 0
 #define HS_DTYPE_F64 1
@@ -191,6 +193,24 @@ int hs_backward_tiles(const double* packed, const int8_t* mode,
                       const double* d_color, const double* transmittance,
                       const int32_t* terminal, double* pair_grads,
                       int32_t tile_lo, int32_t tile_hi);
+
+/* ---- training loss: the cotangent producer between K5 and K6 ---------- */
+
+/* Device workspace for hs_loss on an (height, width, channels) image. */
+size_t hs_loss_workspace_size(int32_t height, int32_t width, int32_t channels);
+
+/* compute_loss (loss.py:88-106): (1 - lambda) L1 + lambda (1 - SSIM) of
+ * `rendered` against `target`, both device float32 (H,W,C) C-contiguous, and
+ * its exact gradient w.r.t. `rendered` (ssim_with_grad, loss.py:48-79).
+ * loss3 (device, 3 doubles) receives [loss, L1, mean SSIM]; the gradient goes
+ * to d_rendered (float32, the cotangent hs_blend_bwd takes) and/or
+ * d_rendered_f64 (float64); either may be NULL.  FP64 arithmetic.  lambda 0
+ * skips SSIM as the reference does (and then accepts images under 11 px).
+ * Errors: HS_ERR_INVALID_LAMBDA outside [0, 1]; HS_ERR_IMAGE_TOO_SMALL when
+ * lambda > 0 and min(H, W) < 11; HS_ERR_WORKSPACE.  Asynchronous on `stream`. */
+int hs_loss(const float* rendered, const float* target, int32_t height, int32_t width,
+            int32_t channels, double lambda_ssim, double* loss3, float* d_rendered,
+            double* d_rendered_f64, void* ws, size_t ws_bytes, void* stream);
 
 /* ---- misc --------------------------------------------------------------- */
 const char* hs_status_string(int status);

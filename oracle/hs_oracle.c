@@ -907,3 +907,105 @@ void oracle_backward(const oracle_frame* f, const double* bg, const double* d_co
   free(start);
   free(rows);
 }
+
+/* ---- training loss, loss.py:1-106 ------------------------------------------
+ * compute_loss / ssim_with_grad restated in plain C on float64 (H,W,C) images.
+ * The blur is scipy.ndimage.correlate1d (scipy, the reference's dependency;
+ * its NI_Correlate1D symmetric-kernel branch: centre tap, then the pairs
+ * (i-r, i+r) ... (i-1, i+1) summed before scaling) with mode="constant",
+ * cval 0, along axis 0 and then axis 1 (loss.py:29-32). */
+static void loss_window(double w[11]) { /* loss.py:19-23 */
+  for (int k = 0; k < 11; ++k) {
+    const double t = (double)(k - 5) / 1.5;
+    w[k] = exp(-0.5 * (t * t));
+  }
+  /* numpy pairwise-sum order for 11 elements */
+  double s = ((w[0] + w[1]) + (w[2] + w[3])) + ((w[4] + w[5]) + (w[6] + w[7]));
+  s += w[8];
+  s += w[9];
+  s += w[10];
+  for (int k = 0; k < 11; ++k) w[k] /= s;
+}
+
+static void corr1d(const double* in, double* out, int h, int wd, int axis, const double w[11]) {
+  for (int y = 0; y < h; ++y)
+    for (int x = 0; x < wd; ++x) {
+      const int64_t stride = axis == 0 ? wd : 1;
+      const int pos = axis == 0 ? y : x, len = axis == 0 ? h : wd;
+      const double* c = in + (int64_t)y * wd + x;
+      double s = c[0] * w[5];
+      for (int j = 5; j >= 1; --j) {
+        const double lo = pos - j >= 0 ? c[-j * stride] : 0.0;
+        const double hi = pos + j < len ? c[j * stride] : 0.0;
+        s += (lo + hi) * w[5 - j];
+      }
+      out[(int64_t)y * wd + x] = s;
+    }
+}
+
+static void filt(const double* in, double* out, double* tmp, int h, int wd, const double w[11]) {
+  corr1d(in, tmp, h, wd, 0, w);
+  corr1d(tmp, out, h, wd, 1, w);
+}
+
+/* out3 = [loss, l1, mean ssim]; grad = d loss / d a.  lambda 0 skips SSIM
+ * (loss.py:97-99). */
+void oracle_loss(const double* a, const double* b, int h, int wd, int ch, double lam,
+                 double* out3, double* grad) {
+  const int64_t hw = (int64_t)h * wd, n = hw * ch;
+  double win[11];
+  loss_window(win);
+  double l1 = 0.0;
+  for (int64_t i = 0; i < n; ++i) l1 += fabs(a[i] - b[i]);
+  l1 /= (double)n;
+  for (int64_t i = 0; i < n; ++i) grad[i] = (1.0 - lam) * (sgn(a[i] - b[i]) / (double)n);
+  out3[1] = l1;
+  out3[2] = 0.0;
+  out3[0] = l1;
+  if (lam == 0.0) return;
+  double* buf = (double*)malloc(sizeof(double) * hw * 14);
+  double *x = buf, *y = buf + hw, *t = buf + 2 * hw, *m1 = buf + 3 * hw, *m2 = buf + 4 * hw,
+         *fxx = buf + 5 * hw, *fyy = buf + 6 * hw, *fxy = buf + 7 * hw, *p = buf + 8 * hw,
+         *q = buf + 9 * hw, *r = buf + 10 * hw, *g1 = buf + 11 * hw, *g2 = buf + 12 * hw,
+         *g3 = buf + 13 * hw;
+  double total = 0.0;
+  for (int c = 0; c < ch; ++c) {
+    for (int64_t i = 0; i < hw; ++i) {
+      x[i] = a[i * ch + c];
+      y[i] = b[i * ch + c];
+    }
+    filt(x, m1, t, h, wd, win);
+    filt(y, m2, t, h, wd, win);
+    for (int64_t i = 0; i < hw; ++i) p[i] = x[i] * x[i];
+    filt(p, fxx, t, h, wd, win);
+    for (int64_t i = 0; i < hw; ++i) p[i] = y[i] * y[i];
+    filt(p, fyy, t, h, wd, win);
+    for (int64_t i = 0; i < hw; ++i) p[i] = x[i] * y[i];
+    filt(p, fxy, t, h, wd, win);
+    for (int64_t i = 0; i < hw; ++i) { /* loss.py:62-75 */
+      const double s1 = fxx[i] - m1[i] * m1[i], s2 = fyy[i] - m2[i] * m2[i];
+      const double s12 = fxy[i] - m1[i] * m2[i];
+      const double a1 = 2.0 * m1[i] * m2[i] + 0.01 * 0.01, a2 = 2.0 * s12 + 0.03 * 0.03;
+      const double b1 = m1[i] * m1[i] + m2[i] * m2[i] + 0.01 * 0.01, b2 = s1 + s2 + 0.03 * 0.03;
+      total += (a1 * a2) / (b1 * b2);
+      const double d_m1 =
+          (2.0 * m2[i] * a2 / (b1 * b2) - 2.0 * m1[i] * a1 * a2 / (b1 * b1 * b2)) / (double)n;
+      const double d_s1 = (-a1 * a2 / (b1 * b2 * b2)) / (double)n;
+      const double d_s12 = (2.0 * a1 / (b1 * b2)) / (double)n;
+      p[i] = d_m1 - 2.0 * m1[i] * d_s1 - m2[i] * d_s12;
+      q[i] = d_s1;
+      r[i] = d_s12;
+    }
+    filt(p, g1, t, h, wd, win);
+    filt(q, g2, t, h, wd, win);
+    filt(r, g3, t, h, wd, win);
+    for (int64_t i = 0; i < hw; ++i) { /* loss.py:74-78, 103 */
+      const double s_grad = g1[i] + 2.0 * x[i] * g2[i] + y[i] * g3[i];
+      grad[i * ch + c] = grad[i * ch + c] - lam * s_grad;
+    }
+  }
+  free(buf);
+  const double s_val = total / (double)n;
+  out3[2] = s_val;
+  out3[0] = (1.0 - lam) * l1 + lam * (1.0 - s_val);
+}

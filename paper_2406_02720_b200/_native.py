@@ -20,6 +20,8 @@ HS_ERR_MISMATCHED_FORWARD = 4
 HS_ERR_INVALID_ARG = 5
 HS_ERR_CUDA = 6
 HS_ERR_WORKSPACE = 7
+HS_ERR_IMAGE_TOO_SMALL = 8
+HS_ERR_INVALID_LAMBDA = 9
 
 HS_DTYPE_F32 = 0
 HS_DTYPE_F64 = 1
@@ -99,6 +101,9 @@ _SIGNATURES = {
     "hs_backward_tiles": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int64,
                                     c_int32, c_int32, c_int32, c_void_p, c_void_p, c_void_p,
                                     c_void_p, c_void_p, c_int32, c_int32]),
+    "hs_loss_workspace_size": (c_size_t, [c_int32, c_int32, c_int32]),
+    "hs_loss": (c_int32, [c_void_p, c_void_p, c_int32, c_int32, c_int32, ctypes.c_double,
+                          c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
     "hs_status_string": (ctypes.c_char_p, [c_int32]),
     "hs_last_cuda_error": (ctypes.c_char_p, []),
     "hs_kernel_launch_count": (c_int64, []),
@@ -143,6 +148,8 @@ _STATUS_ERRORS = {
     HS_ERR_MISMATCHED_FORWARD: errors.MismatchedForward,
     HS_ERR_INVALID_ARG: ValueError,
     HS_ERR_WORKSPACE: errors.WorkspaceError,
+    HS_ERR_IMAGE_TOO_SMALL: errors.ImageTooSmall,
+    HS_ERR_INVALID_LAMBDA: ValueError,
 }
 
 

@@ -29,6 +29,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", CSRC, "
 SOURCES = {
     "hs_preprocess.cu": ["-fmad=false"],
     "hs_geometry_bwd.cu": [],
+    "hs_loss.cu": [],
     "hs_binning.cu": [],
     "hs_blend.cu": [],
     "hs_capi.cu": [],

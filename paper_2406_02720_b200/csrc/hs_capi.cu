@@ -250,6 +250,8 @@ const char* hs_status_string(int status) {
     case HS_ERR_INVALID_ARG: return "invalid argument";
     case HS_ERR_CUDA: return "CUDA error";
     case HS_ERR_WORKSPACE: return "workspace missing or too small";
+    case HS_ERR_IMAGE_TOO_SMALL: return "ImageTooSmall: needs at least 11 pixels on each side";
+    case HS_ERR_INVALID_LAMBDA: return "ValueError: lambda_ssim must lie in [0, 1]";
     default: return "unknown status";
   }
 }
@@ -615,3 +617,78 @@ int hs_backward_tiles(const double* packed, const int8_t* mode, const int32_t* p
 }
 
 }  // extern "C"
+
+// ---- training loss (loss.py:48-106) -----------------------------------------
+namespace {
+struct LossBufs {
+  double* adj_m;
+  double* adj_s1;
+  double* adj_s12;
+  double* partial;
+};
+LossBufs carve_loss(void* ws, int32_t height, int32_t width, int32_t channels, size_t* bytes) {
+  Carver c(ws);
+  const size_t n = (size_t)height * width * channels;
+  LossBufs b;
+  b.adj_m = c.take<double>(n);
+  b.adj_s1 = c.take<double>(n);
+  b.adj_s12 = c.take<double>(n);
+  b.partial = c.take<double>(2 * (size_t)hs::loss_partials(width, height, channels));
+  *bytes = c.off;
+  return b;
+}
+}  // namespace
+
+extern "C" size_t hs_loss_workspace_size(int32_t height, int32_t width, int32_t channels) {
+  if (height <= 0 || width <= 0 || channels <= 0) return 0;
+  size_t bytes = 0;
+  carve_loss(nullptr, height, width, channels, &bytes);
+  return bytes;
+}
+
+extern "C" int hs_loss(const float* rendered, const float* target, int32_t height, int32_t width,
+                       int32_t channels, double lambda_ssim, double* loss3, float* d_rendered,
+                       double* d_rendered_f64, void* ws, size_t ws_bytes, void* stream_) {
+  if (!rendered || !target || !loss3 || height <= 0 || width <= 0 || channels <= 0)
+    return HS_ERR_INVALID_ARG;
+  if (!(lambda_ssim >= 0.0 && lambda_ssim <= 1.0)) return HS_ERR_INVALID_LAMBDA;
+  const bool ssim = lambda_ssim != 0.0;  // loss.py:97-103: lambda 0 skips SSIM
+  if (ssim && (height < 11 || width < 11)) return HS_ERR_IMAGE_TOO_SMALL;
+  size_t need = 0;
+  carve_loss(nullptr, height, width, channels, &need);
+  if (!ws || ws_bytes < need) return HS_ERR_WORKSPACE;
+  const LossBufs b = carve_loss(ws, height, width, channels, &need);
+  hs::LossArgs a;
+  a.x = rendered;
+  a.y = target;
+  a.width = width;
+  a.height = height;
+  a.channels = channels;
+  a.lambda = lambda_ssim;
+  a.n = (double)height * width * channels;
+  a.inv_n = 1.0 / a.n;
+  a.adj_m = b.adj_m;
+  a.adj_s1 = b.adj_s1;
+  a.adj_s12 = b.adj_s12;
+  a.partial = b.partial;
+  a.n_partials = (int)hs::loss_partials(width, height, channels);
+  a.loss = loss3;
+  a.d_f32 = d_rendered;
+  a.d_f64 = d_rendered_f64;
+  a.ssim = ssim;
+  a.group0 = 0;
+  // _window(), loss.py:19-23
+  for (int k = 0; k < 11; ++k) {
+    const double t = (double)(k - 5) / 1.5;
+    a.win[k] = std::exp(-0.5 * (t * t));
+  }
+  // numpy's pairwise sum order for 11 elements: 8 lanes, tree, then the tail
+  const double* w = a.win;
+  double sum = ((w[0] + w[1]) + (w[2] + w[3])) + ((w[4] + w[5]) + (w[6] + w[7]));
+  sum += w[8];
+  sum += w[9];
+  sum += w[10];
+  for (int k = 0; k < 11; ++k) a.win[k] /= sum;
+  HS_CUDA(hs::launch_loss(a, static_cast<cudaStream_t>(stream_)));
+  return HS_OK;
+}

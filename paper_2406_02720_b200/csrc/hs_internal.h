@@ -116,4 +116,27 @@ cudaError_t run_export(void* temp, size_t temp_bytes, const int32_t* count, cons
                        int32_t* valid, int64_t* m_out, float* packed, int8_t* mode, int32_t* tile_rect,
                        int32_t* pair_splat, int64_t* tile_starts, cudaStream_t stream);
 
+// ---- hs_loss.cu -------------------------------------------------------------
+struct LossArgs {
+  const float* x;  // rendered (H,W,C) float32
+  const float* y;  // target   (H,W,C) float32
+  int width, height, channels;
+  double lambda;   // lambda_ssim
+  double n;        // H*W*C
+  double inv_n;    // 1 / n
+  double* adj_m;   // ssim_with_grad adjoint maps, (C,H,W) float64 each
+  double* adj_s1;
+  double* adj_s12;
+  double* partial;  // 2 per CTA: sum |x-y|, sum SSIM map
+  int n_partials;
+  double* loss;     // [loss, l1, mean ssim]
+  float* d_f32;     // d loss / d rendered (nullable)
+  double* d_f64;    // same in float64 (nullable)
+  int ssim;         // lambda > 0
+  int group0;       // first channel group of a launch (internal)
+  double win[11];   // Gaussian window, loss.py:19-23 (kernel parameter space)
+};
+cudaError_t launch_loss(const LossArgs& a, cudaStream_t stream);
+int64_t loss_partials(int width, int height, int channels);
+
 }  // namespace hs

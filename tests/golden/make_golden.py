@@ -158,8 +158,43 @@ def erf_fixture():
     print("erf: ", z.shape[0], "points")
 
 
+def loss_fixture():
+    """compute_loss / ssim_with_grad (loss.py:48-106) on float32-representable
+    images: ragged sizes against the 32x16 tiles, 1/3/4 channels and 2-D images,
+    lambda 0 / 0.2 / 1, identical images and exact ties (sign 0)."""
+    from halfsplat import loss as ref_loss
+    rng = np.random.default_rng(21)
+    f32 = lambda a: np.asarray(a, dtype=np.float32)  # noqa: E731
+    x = f32(rng.random((37, 53, 3)))
+    y = f32(np.clip(x + rng.normal(0, 0.1, x.shape), 0, 1))
+    y[::3, ::4] = x[::3, ::4]  # exact ties: sign(0) = 0
+    g2 = f32(rng.random((64, 48)))
+    cases = {
+        "rgb_l02": (x, y, 0.2),
+        "rgb_l0": (x, y, 0.0),
+        "rgb_l1": (x, y, 1.0),
+        "small_l0": (f32(rng.random((7, 9, 3))), f32(rng.random((7, 9, 3))), 0.0),
+        "gray2d_l05": (g2, f32(np.roll(g2, 3, axis=1)), 0.5),
+        "rgba_l02": (f32(rng.random((24, 40, 4))), f32(rng.random((24, 40, 4))), 0.2),
+        "same_l02": (x, x.copy(), 0.2),
+        "edge_11": (f32(rng.random((11, 11, 3))), f32(rng.random((11, 11, 3))), 0.2),
+    }
+    d = {}
+    for name, (a, b, lam) in cases.items():
+        loss, grad = ref_loss.compute_loss(a.astype(np.float64), b.astype(np.float64), lam)
+        d[f"{name}_a"], d[f"{name}_b"], d[f"{name}_lambda"] = a, b, np.float64(lam)
+        d[f"{name}_loss"], d[f"{name}_grad"] = np.float64(loss), grad
+        if lam > 0:
+            s, sg = ref_loss.ssim_with_grad(a.astype(np.float64), b.astype(np.float64))
+            d[f"{name}_ssim"], d[f"{name}_ssim_grad"] = np.float64(s), sg
+    d["cases"] = np.array(list(cases))
+    np.savez_compressed(os.path.join(HERE, "loss.npz"), **d)
+    print("loss:", len(cases), "cases")
+
+
 JOBS = {
     "erf": lambda t: erf_fixture(),
+    "loss": lambda t: loss_fixture(),
     # small scenes, every array
     "c1": lambda t: full_fixture("c1", scenes.make_config("c1"), 0, True, t),
     "mini": lambda t: full_fixture("mini", scenes.frustum(300, 2, 64, 48, seed=3), 0, True, t),

@@ -108,3 +108,23 @@ def test_oracle_large_binning_hashes(name, cfg):
     f = O.prepare(sa, Cam(sa.cameras[0]))
     for k, dt in INTS.items():
         assert _sha(getattr(f, k), dt) == str(gold[f"sha_{k}"]), k
+
+
+def test_loss_oracle_matches_reference():
+    """compute_loss / ssim_with_grad (loss.py:48-106): the oracle's gradients
+    are bit-identical to the reference's; the scalars differ only by the
+    summation order of the means (numpy pairwise vs sequential)."""
+    gold = load_golden("loss")
+    for c in gold["cases"]:
+        a, b, lam = gold[f"{c}_a"], gold[f"{c}_b"], float(gold[f"{c}_lambda"])
+        loss, grad = O.compute_loss(a, b, lam)
+        assert grad.shape == gold[f"{c}_grad"].shape, c
+        assert np.array_equal(grad, gold[f"{c}_grad"]), c
+        assert loss == pytest.approx(float(gold[f"{c}_loss"]), rel=1e-12, abs=1e-15), c
+        if lam > 0:
+            s, sg = O.ssim_with_grad(a, b)
+            assert sg.shape == gold[f"{c}_ssim_grad"].shape, c
+            assert np.array_equal(sg, gold[f"{c}_ssim_grad"]), c
+            assert s == pytest.approx(float(gold[f"{c}_ssim"]), rel=1e-12), c
+    s, _ = O.ssim_with_grad(gold["same_l02_a"], gold["same_l02_a"])
+    assert s == 1.0

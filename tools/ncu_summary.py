@@ -29,7 +29,11 @@ def summarize(path):
     raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
-    hdr, units, vals = rows[0], rows[1], rows[2]
+    hdr, units = rows[0], rows[1]
+    return "\n".join(_one(hdr, units, vals) for vals in rows[2:])
+
+
+def _one(hdr, units, vals):
     idx = {h: i for i, h in enumerate(hdr)}
     out = [f"kernel: {vals[idx['Kernel Name']][:100]}"]
     for key, label in WANT:
