@@ -34,6 +34,17 @@ FWD_FLOPS_PER_EVAL = 46    # _blend_cy.pyx:153-176
 BWD_FLOPS_PER_EVAL = 112   # _blend_cy.pyx:290-335
 
 
+def _hbm_peak():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"])
+    except (OSError, KeyError, ValueError):
+        return 7700.0  # B200_PROFILING.md fallback
+
+
+HBM_PEAK_GBS = _hbm_peak()
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -329,13 +340,18 @@ def main():
     barrier()
     fwd_ms = start.elapsed_time(end) / args.steps
 
-    # training iteration with the loss on the device (render -> hs_loss -> backward), the
-    # reference trainer's step minus the optimizer (trainer.py:179-226): synthetic targets
+    # full training iteration on the device, the reference trainer's step (trainer.py:179-226):
+    # render -> hs_loss (L1 + SSIM, cotangent) -> backward -> [all-reduce] -> hs_adam_step,
+    # synthetic targets.  Runs last: Adam moves the scene.
+    from paper_2406_02720_b200 import trainer as T
     from paper_2406_02720_b200.loss import DeviceLoss
     gen = torch.Generator(device="cuda").manual_seed(7)
     targets = [torch.rand((c.height, c.width, 3), generator=gen, device="cuda") for c in cams]
     dloss = DeviceLoss(0.2)
     loss_timer = device.StageTimer()
+    tcfg = T.TrainConfig()
+    adam = T.AdamState(scene)
+    it_counter = [0]
 
     def train_step(t=None):
         for j, v in enumerate(views):
@@ -345,6 +361,9 @@ def main():
             rast.render_backward(scene, cams[v], o, d, grads=grads, accumulate=j > 0)
         if reducer is not None:
             reducer.allreduce()
+        with (t.span("adam") if t is not None else contextlib.nullcontext()):
+            T.adam_step(scene, grads, tcfg, adam, it_counter[0])
+        it_counter[0] += 1
 
     for _ in range(3):
         train_step()
@@ -356,6 +375,9 @@ def main():
     barrier()
     train_ms = start.elapsed_time(end) / args.steps
     loss_ms = statistics.mean(loss_timer.totals().get("loss", [float("nan")]))
+    adam_ms = statistics.mean(loss_timer.totals().get("adam", [float("nan")]))
+    # Adam moves param, m, v (read+write) and reads grad: 28 B per float32 element
+    adam_bytes = sum(getattr(scene, f).numel() for f in scene.FIELDS) * 7 * scene.mu.element_size()
 
     # algorithmic work of the dominant kernels
     term = out.terminal.to(torch.int64)
@@ -408,8 +430,14 @@ def main():
             "fwd_fps": views_per_step * 1e3 / fwd_ms, "fwd_ms_per_step": fwd_ms,
             "train_step": {"value": views_per_step * 1e3 / train_ms, "unit": metric_unit(multi),
                            "ms_per_step": train_ms, "loss_kernel_ms": loss_ms,
+                           "adam_kernel_ms": adam_ms,
+                           "adam_hbm": {"bytes": adam_bytes,
+                                        "achieved_gbs": adam_bytes / (adam_ms * 1e-3) / 1e9,
+                                        "frac_of_peak": adam_bytes / (adam_ms * 1e-3) / 1e9
+                                        / HBM_PEAK_GBS},
                            "what": "render -> L1+SSIM loss and cotangent on device (hs_loss, "
-                                   "lambda 0.2) -> render_backward, synthetic targets"},
+                                   "lambda 0.2) -> render_backward -> Adam on all 8 groups "
+                                   "(hs_adam_step), synthetic targets"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clock_info,
             "counts": {"P": out.frame.num_pairs, "fwd_evals": fwd_evals, "bwd_evals": bwd_evals},

@@ -212,6 +212,42 @@ int hs_loss(const float* rendered, const float* target, int32_t height, int32_t 
             int32_t channels, double lambda_ssim, double* loss3, float* d_rendered,
             double* d_rendered_f64, void* ws, size_t ws_bytes, void* stream);
 
+/* ---- optimizer: per-group Adam, the step after K7 ----------------------- */
+
+/* Parameter groups in the reference's order (trainer.py:81-82). */
+#define HS_ADAM_GROUPS 8
+#define HS_GROUP_MU 0
+#define HS_GROUP_LOG_SCALE 1
+#define HS_GROUP_ROTATION 2
+#define HS_GROUP_SH_DC 3
+#define HS_GROUP_SH_REST 4
+#define HS_GROUP_NORMAL 5
+#define HS_GROUP_OPACITY_A 6
+#define HS_GROUP_OPACITY_B 7
+
+/* AdamState (trainer.py:110-136).  m / v: device arrays of the scene's dtype
+ * and shapes, in scene-field order mu, log_scale, rotation, sh_coeffs (both SH
+ * groups), normal, raw_opacity_a, raw_opacity_b.  t: per-group step counts,
+ * advanced by hs_adam_step for every group it updates. */
+typedef struct hs_adam_state {
+  void* m[7];
+  void* v[7];
+  int64_t t[HS_ADAM_GROUPS];
+} hs_adam_state;
+
+/* The Adam part of trainer.step (trainer.py:192-224): for every group g with
+ * lr[g] > 0 (the caller passes 0 for groups its mode freezes, active_groups
+ * trainer.py:161-168), t[g] += 1 and
+ *   m = b1 m + (1-b1) grad;  v = b2 v + (1-b2) grad^2;
+ *   param -= lr m/(1-b1^t) / (sqrt(v/(1-b2^t)) + 1e-15)
+ * with b1 0.9, b2 0.999; normals whose update is non-zero are renormalised;
+ * tie_opacities (the 'full' kernel) then sets raw_opacity_b = raw_opacity_a.
+ * The SCENE'S PARAMETER ARRAYS ARE UPDATED IN PLACE (the const in hs_scene is
+ * the renderer's view).  grads: the hs_grads buffers of the same scene/dtype.
+ * One kernel launch; a float64 scene steps bit-identically to the reference. */
+int hs_adam_step(const hs_scene* scene, const hs_grads* grads, hs_adam_state* state,
+                 const double lr[HS_ADAM_GROUPS], int32_t tie_opacities, void* stream);
+
 /* ---- misc --------------------------------------------------------------- */
 const char* hs_status_string(int status);
 const char* hs_last_cuda_error(void);

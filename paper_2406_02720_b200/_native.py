@@ -76,6 +76,10 @@ class HsGrads(ctypes.Structure):
     ]
 
 
+class HsAdamState(ctypes.Structure):
+    _fields_ = [("m", c_void_p * 7), ("v", c_void_p * 7), ("t", c_int64 * 8)]
+
+
 # name -> (restype, argtypes); every symbol declared in include/halfsplat_b200.h
 _SIGNATURES = {
     "hs_frame_init": (c_int32, [ctypes.POINTER(HsFrame), c_int64, c_int32, c_int32, c_int32]),
@@ -104,6 +108,9 @@ _SIGNATURES = {
     "hs_loss_workspace_size": (c_size_t, [c_int32, c_int32, c_int32]),
     "hs_loss": (c_int32, [c_void_p, c_void_p, c_int32, c_int32, c_int32, ctypes.c_double,
                           c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
+    "hs_adam_step": (c_int32, [ctypes.POINTER(HsScene), ctypes.POINTER(HsGrads),
+                               ctypes.POINTER(HsAdamState), ctypes.POINTER(ctypes.c_double),
+                               c_int32, c_void_p]),
     "hs_status_string": (ctypes.c_char_p, [c_int32]),
     "hs_last_cuda_error": (ctypes.c_char_p, []),
     "hs_kernel_launch_count": (c_int64, []),

@@ -692,3 +692,83 @@ extern "C" int hs_loss(const float* rendered, const float* target, int32_t heigh
   HS_CUDA(hs::launch_loss(a, static_cast<cudaStream_t>(stream_)));
   return HS_OK;
 }
+
+// ---- optimizer (trainer.py:192-224) -------------------------------------------
+extern "C" int hs_adam_step(const hs_scene* scene, const hs_grads* grads, hs_adam_state* state,
+                            const double lr[HS_ADAM_GROUPS], int32_t tie_opacities,
+                            void* stream_) {
+  if (!scene || !grads || !state || !lr) return HS_ERR_INVALID_ARG;
+  if (scene->n <= 0) return HS_ERR_EMPTY_SCENE;
+  if (scene->sh_degree < 0 || scene->sh_degree > 3) return HS_ERR_INVALID_ARG;
+  for (int g = 0; g < HS_ADAM_GROUPS; ++g)
+    if (!(lr[g] >= 0.0)) return HS_ERR_INVALID_ARG;
+  const int64_t n = scene->n;
+  const int K = (scene->sh_degree + 1) * (scene->sh_degree + 1);
+  bool on[HS_ADAM_GROUPS];
+  double bc1[HS_ADAM_GROUPS], bc2[HS_ADAM_GROUPS];
+  for (int g = 0; g < HS_ADAM_GROUPS; ++g) {
+    on[g] = lr[g] != 0.0;
+    // sh_rest has no coefficients at degree 0: the reference still counts its step
+    const int64_t t = state->t[g] + (on[g] ? 1 : 0);
+    bc1[g] = 1.0 - std::pow(0.9, (double)t);  // 1 - ADAM_BETA1**t (trainer.py:210)
+    bc2[g] = 1.0 - std::pow(0.999, (double)t);
+  }
+  hs::AdamArgs a;
+  memset(&a, 0, sizeof(a));
+  int s = 0;
+  auto add = [&](int kind, int field, int64_t count, int g0, int g1, const void* p1, void* m1,
+                 void* v1, const void* gr1, void* grad0) {
+    hs::AdamSeg& sg = a.seg[s];
+    const void* params[7] = {scene->mu, scene->log_scale, scene->rotation, scene->sh_coeffs,
+                             scene->normal, scene->raw_opacity_a, scene->raw_opacity_b};
+    sg.kind = kind;
+    sg.K = K;
+    sg.param[0] = const_cast<void*>(params[field]);
+    sg.m[0] = state->m[field];
+    sg.v[0] = state->v[field];
+    sg.grad[0] = grad0;
+    sg.param[1] = const_cast<void*>(p1);
+    sg.m[1] = m1;
+    sg.v[1] = v1;
+    sg.grad[1] = gr1;
+    const int gs[2] = {g0, g1};
+    for (int j = 0; j < 2; ++j) {
+      if (gs[j] < 0) continue;
+      sg.lr[j] = lr[gs[j]];
+      sg.bc1[j] = bc1[gs[j]];
+      sg.bc2[j] = bc2[gs[j]];
+      sg.active[j] = on[gs[j]];
+    }
+    // elementwise segments move in 16-B vectors when every array allows it
+    const int esz = scene->dtype == HS_DTYPE_F64 ? 8 : 4, per = 16 / esz;
+    auto al = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
+    sg.vec = (kind == hs::kAdamPlain || kind == hs::kAdamSh) && count % per == 0 &&
+             al(sg.param[0]) && al(sg.m[0]) && al(sg.v[0]) && al(sg.grad[0]);
+    if (sg.vec) count /= per;
+    sg.units = count;
+    ++s;
+  };
+  if (on[HS_GROUP_MU]) add(hs::kAdamPlain, 0, 3 * n, HS_GROUP_MU, -1, nullptr, nullptr, nullptr, nullptr, grads->d_mu);
+  if (on[HS_GROUP_LOG_SCALE])
+    add(hs::kAdamPlain, 1, 3 * n, HS_GROUP_LOG_SCALE, -1, nullptr, nullptr, nullptr, nullptr,
+        grads->d_log_scale);
+  if (on[HS_GROUP_ROTATION])
+    add(hs::kAdamPlain, 2, 4 * n, HS_GROUP_ROTATION, -1, nullptr, nullptr, nullptr, nullptr,
+        grads->d_rotation);
+  if (on[HS_GROUP_SH_DC] || on[HS_GROUP_SH_REST])
+    add(hs::kAdamSh, 3, 3 * (int64_t)K * n, HS_GROUP_SH_DC, HS_GROUP_SH_REST, nullptr, nullptr,
+        nullptr, nullptr, grads->d_sh);
+  if (on[HS_GROUP_NORMAL])
+    add(hs::kAdamNormal, 4, n, HS_GROUP_NORMAL, -1, nullptr, nullptr, nullptr, nullptr,
+        grads->d_normal);
+  if (on[HS_GROUP_OPACITY_A] || on[HS_GROUP_OPACITY_B] || tie_opacities)
+    add(hs::kAdamOpacity, 5, n, HS_GROUP_OPACITY_A, HS_GROUP_OPACITY_B, scene->raw_opacity_b,
+        state->m[6], state->v[6], grads->d_raw_opacity_b, grads->d_raw_opacity_a);
+  a.nseg = s;
+  a.tie_opacities = tie_opacities != 0;
+  HS_CUDA(hs::launch_adam(a, scene->dtype == HS_DTYPE_F64 ? 1 : 0,
+                          static_cast<cudaStream_t>(stream_)));
+  for (int g = 0; g < HS_ADAM_GROUPS; ++g)
+    if (on[g]) state->t[g] += 1;
+  return HS_OK;
+}

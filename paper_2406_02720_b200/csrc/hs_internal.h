@@ -139,4 +139,29 @@ struct LossArgs {
 cudaError_t launch_loss(const LossArgs& a, cudaStream_t stream);
 int64_t loss_partials(int width, int height, int channels);
 
+// ---- hs_adam.cu -------------------------------------------------------------
+enum AdamKind { kAdamPlain = 0, kAdamSh = 1, kAdamNormal = 2, kAdamOpacity = 3 };
+struct AdamSeg {
+  void* param[2];  // [1] used by kAdamOpacity (raw_opacity_b)
+  void* m[2];
+  void* v[2];
+  const void* grad[2];
+  double lr[2];    // kAdamSh: [0] sh_dc, [1] sh_rest
+  double bc1[2];   // 1 - beta1^t of the group
+  double bc2[2];   // 1 - beta2^t
+  int active[2];
+  int kind;
+  int K;           // SH coefficients per channel (kAdamSh)
+  int vec;         // units are 16-B vectors (plain / sh segments, aligned, divisible)
+  int64_t units;   // work units of the segment
+};
+constexpr int kAdamMaxSeg = 6;
+struct AdamArgs {
+  AdamSeg seg[kAdamMaxSeg];
+  int cta_start[kAdamMaxSeg + 1];  // CTA prefix over segments (set by launch_adam)
+  int nseg;
+  int tie_opacities;
+};
+cudaError_t launch_adam(AdamArgs a, int dtype, cudaStream_t stream);
+
 }  // namespace hs

@@ -1,0 +1,239 @@
+"""Device-resident training step: render -> loss -> backward -> Adam, all on the GPU.
+
+Mirror of the reference's optimizer path (trainer.py:22-226): the same names
+(`TrainConfig`, `GROUPS`, `AdamState`, `mu_learning_rate`, `learning_rates`,
+`active_groups`, `camera_extent`, `step`) with the same argument meaning, but
+the scene, its gradients and the Adam moments are CUDA tensors and the update is
+one `hs_adam_step` launch (csrc/hs_adam.cu).  The learning-rate schedule is
+scalar host arithmetic, evaluated exactly as the reference does.
+
+Densification (trainer.py:229-350) and the run loop / checkpoints are not part of
+this module (scope).
+"""
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native, device
+from .errors import NonFiniteLoss
+from .loss import DeviceLoss
+
+ADAM_BETA1 = 0.9    # trainer.py:23
+ADAM_BETA2 = 0.999  # trainer.py:24
+ADAM_EPS = 1e-15    # trainer.py:25
+
+MODES = ("from_scratch", "finetune_all", "finetune_all_with_densify",
+         "finetune_normals_opacities")
+
+# parameter groups (trainer.py:81-82) and the scene field each lives in
+GROUPS = ("mu", "log_scale", "rotation", "sh_dc", "sh_rest", "normal",
+          "opacity_a", "opacity_b")
+_STATE_FIELDS = ("mu", "log_scale", "rotation", "sh_coeffs", "normal", "raw_opacity_a",
+                 "raw_opacity_b")
+_GROUP_FIELD = {"mu": 0, "log_scale": 1, "rotation": 2, "sh_dc": 3, "sh_rest": 3, "normal": 4,
+                "opacity_a": 5, "opacity_b": 6}
+
+
+@dataclass
+class TrainConfig:
+    """trainer.py:31-76 (same fields, defaults and validation)."""
+
+    total_iters: int = 30000
+    densify_until: int = 20000
+    densify_interval: int = 100
+    opacity_reset_start: int = 3000
+    opacity_reset_interval: int = 3000
+    opacity_reset_until: int = 20000
+    opacity_reset_ceiling: float = 0.01
+    lambda_ssim: float = 0.2
+    lr_normal: float = 0.003
+    lr_mu_init: float = 1.6e-4
+    lr_mu_final: float = 1.6e-6
+    lr_scale: float = 5e-3
+    lr_rotation: float = 1e-3
+    lr_sh_dc: float = 2.5e-3
+    sh_rest_divisor: float = 20.0
+    lr_opacity: float = 5e-2
+    densify_grad_threshold: float = 2e-4
+    prune_opacity_threshold: float = 0.005
+    percent_dense: float = 0.01
+    prune_extent_factor: float = 0.1
+    split_scale_factor: float = 1.6
+    max_primitives: int = 0
+    mode: str = "from_scratch"
+    kernel: str = "half"
+    seed: int = 0
+    threads: int = 0
+    checkpoint_interval: int = 0
+
+    def __post_init__(self):
+        if not (0 < self.densify_until <= self.total_iters):
+            raise ValueError("require 0 < densify_until <= total_iters")
+        if not (0.0 <= self.lambda_ssim <= 1.0):
+            raise ValueError("lambda_ssim must lie in [0, 1]")
+        for name in ("lr_mu_init", "lr_mu_final", "lr_scale", "lr_rotation",
+                     "lr_sh_dc", "lr_opacity"):
+            if getattr(self, name) <= 0:
+                raise ValueError(f"{name} must be positive")
+        if self.lr_normal < 0:
+            raise ValueError("lr_normal must be >= 0")
+        if self.mode not in MODES:
+            raise ValueError(f"mode must be one of {MODES}")
+        if self.kernel not in ("half", "full"):
+            raise ValueError("kernel must be 'half' or 'full'")
+
+
+class AdamState:
+    """First/second moments per parameter group, row-aligned with the scene
+    (trainer.py:110-136).  Moments are device tensors shaped like the scene
+    fields; `m[name]` / `v[name]` give the group's view (sh_dc / sh_rest are
+    slices of the sh_coeffs moments)."""
+
+    def __init__(self, scene):
+        self._m = [torch.zeros_like(getattr(scene, f)) for f in _STATE_FIELDS]
+        self._v = [torch.zeros_like(getattr(scene, f)) for f in _STATE_FIELDS]
+        self.t = {name: 0 for name in GROUPS}
+
+    @staticmethod
+    def _view(arrays, name):
+        a = arrays[_GROUP_FIELD[name]]
+        if name == "sh_dc":
+            return a[:, :1, :]
+        if name == "sh_rest":
+            return a[:, 1:, :]
+        return a
+
+    @property
+    def m(self):
+        return {name: self._view(self._m, name) for name in GROUPS}
+
+    @property
+    def v(self):
+        return {name: self._view(self._v, name) for name in GROUPS}
+
+    def select(self, keep):
+        keep = torch.as_tensor(keep, device=self._m[0].device)
+        self._m = [a[keep].contiguous() for a in self._m]
+        self._v = [a[keep].contiguous() for a in self._v]
+
+    def append_zeros(self, count):
+        self._m = [torch.cat([a, a.new_zeros((count,) + a.shape[1:])]) for a in self._m]
+        self._v = [torch.cat([a, a.new_zeros((count,) + a.shape[1:])]) for a in self._v]
+
+    def zero_group(self, name):
+        self._view(self._m, name).zero_()
+        self._view(self._v, name).zero_()
+        self.t[name] = 0
+
+    def struct(self):
+        s = _native.HsAdamState()
+        for k in range(7):
+            s.m[k] = self._m[k].data_ptr()
+            s.v[k] = self._v[k].data_ptr()
+        for k, name in enumerate(GROUPS):
+            s.t[k] = self.t[name]
+        return s
+
+
+def mu_learning_rate(config, iteration, spatial_scale):
+    """Exponential decay from lr_mu_init to lr_mu_final (trainer.py:139-143)."""
+    frac = min(max(iteration / config.total_iters, 0.0), 1.0)
+    lr = config.lr_mu_init * (config.lr_mu_final / config.lr_mu_init) ** frac
+    return lr * spatial_scale
+
+
+def learning_rates(config, iteration, spatial_scale):
+    """trainer.py:146-156."""
+    return {
+        "mu": mu_learning_rate(config, iteration, spatial_scale),
+        "log_scale": config.lr_scale,
+        "rotation": config.lr_rotation,
+        "sh_dc": config.lr_sh_dc,
+        "sh_rest": config.lr_sh_dc / config.sh_rest_divisor,
+        "normal": config.lr_normal,
+        "opacity_a": config.lr_opacity,
+        "opacity_b": config.lr_opacity,
+    }
+
+
+def active_groups(config):
+    """trainer.py:159-166."""
+    if config.mode == "finetune_normals_opacities":
+        groups = {"normal", "opacity_a", "opacity_b"}
+    else:
+        groups = set(GROUPS)
+    if config.kernel == "full":
+        groups.discard("normal")
+    return groups
+
+
+def camera_extent(cameras):
+    """Radius of the camera-centre bounding sphere (trainer.py:169-176)."""
+    centers = np.stack([np.asarray(cam.center, dtype=np.float64) for cam in cameras])
+    if centers.shape[0] < 2:
+        return 1.0
+    centroid = centers.mean(axis=0)
+    radius = np.linalg.norm(centers - centroid, axis=1).max()
+    return float(radius) if radius > 0 else 1.0
+
+
+def adam_step(scene, grads, config, opt_state, iteration, spatial_scale=1.0):
+    """The Adam part of step() (trainer.py:192-224) as one device launch."""
+    lrs = learning_rates(config, iteration, spatial_scale)
+    enabled = active_groups(config)
+    lr = (ctypes.c_double * 8)(*[(lrs[g] if g in enabled else 0.0) for g in GROUPS])
+    g = _native.HsGrads()
+    for name in device.DeviceGradientSet.NAMES:
+        setattr(g, name, getattr(grads, name).data_ptr())
+    st = opt_state.struct()
+    sc = device.scene_struct(scene)
+    lib = _native.load()
+    _native.check(lib.hs_adam_step(ctypes.byref(sc), ctypes.byref(g), ctypes.byref(st), lr,
+                                   1 if config.kernel == "full" else 0, device._stream()),
+                  "hs_adam_step")
+    for k, name in enumerate(GROUPS):
+        opt_state.t[name] = int(st.t[k])
+
+
+class Trainer:
+    """Persistent buffers for repeated steps: one rasterizer workspace, one
+    gradient set, one loss workspace (no allocation per step)."""
+
+    def __init__(self, scene, config):
+        self.config = config
+        self.rast = device.Rasterizer(scene.device, slots=1, kernel=config.kernel)
+        self.grads = device.DeviceGradientSet.empty_flat(scene)
+        self.loss = DeviceLoss(config.lambda_ssim)
+
+    def step(self, scene, batch_view, opt_state, iteration, spatial_scale=1.0,
+             check_finite=True):
+        cam, target = batch_view
+        if not isinstance(target, torch.Tensor):
+            target = torch.as_tensor(np.asarray(target, dtype=np.float32))
+        target = target.to(device=scene.device, dtype=torch.float32)
+        out = self.rast.render(scene, cam)
+        stats, d_color = self.loss(out.color, target)
+        loss = stats[0]
+        if check_finite:
+            loss = float(loss)  # trainer.py:189-190 (one 8-byte read)
+            if not math.isfinite(loss):
+                raise NonFiniteLoss(iteration, loss)
+        self.rast.render_backward(scene, cam, out, d_color, grads=self.grads)
+        adam_step(scene, self.grads, self.config, opt_state, iteration, spatial_scale)
+        return loss, self.grads, out
+
+
+def step(scene, batch_view, config, opt_state, iteration, spatial_scale=1.0, threads=None):
+    """One optimisation step on a (camera, target image) pair (trainer.py:179-226).
+
+    Returns (loss, grads, out) like the reference; grads/out are device objects.
+    `threads` is accepted and ignored.  Repeated callers should hold a Trainer."""
+    trainer = getattr(opt_state, "_trainer", None)
+    if trainer is None or trainer.config is not config:
+        trainer = Trainer(scene, config)
+        opt_state._trainer = trainer
+    return trainer.step(scene, batch_view, opt_state, iteration, spatial_scale)

@@ -192,8 +192,73 @@ def loss_fixture():
     print("loss:", len(cases), "cases")
 
 
+def adam_fixture():
+    """The optimizer part of trainer.step (trainer.py:179-226), driven through the
+    reference's own step() with render / compute_loss / render_backward replaced
+    by stubs that hand it preset gradients, so only its Adam / normal / tie code
+    runs.  Cases: modes, 'full' kernel, frozen normal (lr 0), SH degree 0 and 3,
+    rows with all-zero gradients (must stay bit-identical), 3 steps each."""
+    from halfsplat import geometry, rasterizer
+    from halfsplat import trainer as T
+    d = {}
+    cases = {
+        "half_sh3": dict(kw={}, deg=3),
+        "full_sh1": dict(kw={"kernel": "full"}, deg=1),
+        "finetune_no": dict(kw={"mode": "finetune_normals_opacities"}, deg=2),
+        "frozen_normal_sh0": dict(kw={"lr_normal": 0.0}, deg=0),
+    }
+    for ci, (name, c) in enumerate(cases.items()):
+        rng = np.random.default_rng(100 + ci)
+        n, k = 97, (c["deg"] + 1) ** 2
+        f32 = lambda a: np.asarray(a, dtype=np.float32).astype(np.float64)  # noqa: E731
+        nrm = rng.normal(size=(n, 3))
+        nrm /= np.linalg.norm(nrm, axis=1, keepdims=True)
+        sc = geometry.Scene(mu=f32(rng.uniform(-1, 1, (n, 3))),
+                            log_scale=f32(rng.uniform(-4, -2, (n, 3))),
+                            rotation=f32(rng.normal(size=(n, 4))),
+                            sh_coeffs=f32(rng.normal(0, 0.3, (n, k, 3))),
+                            normal=f32(nrm), raw_opacity_a=f32(rng.normal(size=n)),
+                            raw_opacity_b=f32(rng.normal(size=n)), sh_degree=c["deg"])
+        cfg = T.TrainConfig(total_iters=100, densify_until=50, **c["kw"])
+        state = T.AdamState(sc)
+        d[f"{name}_init"] = np.concatenate([getattr(sc, f).reshape(n, -1) for f in SCENE_FIELDS],
+                                           axis=1)
+        for it in range(3):
+            g = rasterizer.GradientSet.zeros(n, k)
+            for gname in ("d_mu", "d_log_scale", "d_rotation", "d_sh", "d_normal",
+                          "d_raw_opacity_a", "d_raw_opacity_b"):
+                arr = getattr(g, gname)
+                arr[...] = f32(rng.normal(0, 1e-3, arr.shape))
+                arr[: 8 + it] = 0.0  # untouched rows
+            d[f"{name}_grad{it}"] = np.concatenate(
+                [getattr(g, gn).reshape(n, -1) for gn in ("d_mu", "d_log_scale", "d_rotation",
+                                                          "d_sh", "d_normal", "d_raw_opacity_a",
+                                                          "d_raw_opacity_b")], axis=1)
+            saved = (T.render, T.compute_loss, T.render_backward)
+            T.render = lambda scene, cam, kernel="half", threads=None: rasterizer.RenderOutput(
+                color=None, alpha=None, depth=None, per_pixel_terminal_index=None)
+            T.compute_loss = lambda color, target, lam: (0.5, None)
+            T.render_backward = lambda scene, cam, out, d_color, threads=None, _g=g: _g
+            try:
+                T.step(sc, (None, None), cfg, state, iteration=10 * it + 5, spatial_scale=2.5)
+            finally:
+                T.render, T.compute_loss, T.render_backward = saved
+            d[f"{name}_after{it}"] = np.concatenate(
+                [getattr(sc, f).reshape(n, -1) for f in SCENE_FIELDS], axis=1)
+        d[f"{name}_t"] = np.array([state.t[gname] for gname in T.GROUPS])
+        d[f"{name}_deg"] = np.int64(c["deg"])
+        d[f"{name}_kw"] = np.array(repr(c["kw"]))
+    d["cases"] = np.array(list(cases))
+    np.savez_compressed(os.path.join(HERE, "adam.npz"), **d)
+    print("adam:", len(cases), "cases")
+
+
+SCENE_FIELDS = ("mu", "log_scale", "rotation", "sh_coeffs", "normal", "raw_opacity_a",
+                "raw_opacity_b")
+
 JOBS = {
     "erf": lambda t: erf_fixture(),
+    "adam": lambda t: adam_fixture(),
     "loss": lambda t: loss_fixture(),
     # small scenes, every array
     "c1": lambda t: full_fixture("c1", scenes.make_config("c1"), 0, True, t),

@@ -128,3 +128,24 @@ def test_loss_oracle_matches_reference():
             assert s == pytest.approx(float(gold[f"{c}_ssim"]), rel=1e-12), c
     s, _ = O.ssim_with_grad(gold["same_l02_a"], gold["same_l02_a"])
     assert s == 1.0
+
+
+def test_adam_oracle_matches_reference():
+    """OracleAdam (trainer.py:192-224 restated) steps the reference's scenes
+    bit-identically, including frozen groups, the 'full' tie, zero-gradient
+    rows and the normal renormalisation."""
+    import adam_cases as A
+    from paper_2406_02720_b200 import trainer as T
+    gold = load_golden("adam")
+    for name in gold["cases"]:
+        deg, kw, params, steps, t_ref = A.case(gold, name)
+        cfg = A.config(kw)
+        opt = O.OracleAdam(params)
+        for it, (iteration, grads, after) in enumerate(steps):
+            lrs = T.learning_rates(cfg, iteration, A.SPATIAL_SCALE)
+            enabled = T.active_groups(cfg)
+            lrs = {g: (lr if g in enabled else 0.0) for g, lr in lrs.items()}
+            opt.step(params, grads, lrs, cfg.kernel == "full")
+            for f in A.FIELDS:
+                assert np.array_equal(params[f], after[f]), (name, it, f)
+        assert [opt.t[g] for g in O.ADAM_GROUPS] == list(t_ref), name
