@@ -248,6 +248,67 @@ typedef struct hs_adam_state {
 int hs_adam_step(const hs_scene* scene, const hs_grads* grads, hs_adam_state* state,
                  const double lr[HS_ADAM_GROUPS], int32_t tie_opacities, void* stream);
 
+/* ---- density control (trainer.py:229-350) ------------------------------- */
+
+/* DensifyStats (trainer.py:229-244): device float64 / int64 accumulators. */
+typedef struct hs_densify_stats {
+  double* grad_sum;     /* (n,)   sum of pos_grad_norm */
+  double* mu_grad_sum;  /* (n,3)  sum of d_mu */
+  int64_t* count;       /* (n,)   sum of touch_count */
+} hs_densify_stats;
+
+/* TrainConfig's density fields (trainer.py:47-53) plus the scene extent. */
+typedef struct hs_densify_config {
+  double densify_grad_threshold;
+  double prune_opacity_threshold;
+  double percent_dense;
+  double prune_extent_factor;
+  double scene_extent;
+  double log_split_scale;  /* log(split_scale_factor), as numpy computes it */
+  int64_t max_primitives;  /* 0 = unlimited */
+} hs_densify_config;
+
+/* Filled by hs_densify_plan; read by hs_densify_apply. */
+typedef struct hs_densify_plan {
+  int64_t n_in, n_out;
+  int64_t kept;    /* survivors, including over-budget split parents */
+  int64_t cloned;  /* report["cloned"] */
+  int64_t split;   /* report["split"] (parents; 2 children each) */
+  int64_t pruned;  /* report["pruned"] */
+} hs_densify_plan;
+
+/* DensifyStats.update (trainer.py:241-244) from one step's gradients. */
+int hs_densify_stats_update(const hs_densify_stats* stats, const hs_grads* grads, int64_t n,
+                            int32_t dtype, void* stream);
+
+size_t hs_densify_workspace_size(int64_t n);
+
+/* First half of densify_and_prune (trainer.py:254-288): classify every
+ * primitive, rank the candidates, apply the max_primitives budget.  Fills
+ * `plan` (so the caller can allocate n_out rows); SYNCHRONISES `stream`.
+ * The workspace carries the classification to hs_densify_apply. */
+int hs_densify_plan_compute(const hs_scene* scene, const hs_densify_stats* stats,
+                            const hs_densify_config* cfg, hs_densify_plan* plan, void* ws,
+                            size_t ws_bytes, void* stream);
+
+/* Second half (trainer.py:290-340): write the new scene into `out` (device
+ * arrays of plan->n_out rows, same dtype/degree; the const in hs_scene is the
+ * renderer's view, these ARE WRITTEN) and the re-aligned Adam moments into
+ * state_out (survivor rows copied, new rows zero; NULL entries skipped).
+ * split_offsets: device float64 (2, plan->split, 3) standard normals, the
+ * reference's two rng.normal draws; NULL draws them on the device (Philox,
+ * keyed by `seed`). */
+int hs_densify_apply(const hs_scene* scene, const hs_densify_stats* stats,
+                     const hs_densify_config* cfg, const hs_densify_plan* plan, const void* ws,
+                     size_t ws_bytes, const double* split_offsets, uint64_t seed,
+                     const hs_adam_state* state_in, hs_scene* out, hs_adam_state* state_out,
+                     void* stream);
+
+/* reset_opacity (trainer.py:343-350): raw opacities = min(raw, cap) with
+ * cap = logit(ceiling); zeroes the opacity groups' moments and steps when
+ * `state` is given.  Writes the scene's opacity arrays. */
+int hs_reset_opacity(const hs_scene* scene, double cap, hs_adam_state* state, void* stream);
+
 /* ---- misc --------------------------------------------------------------- */
 const char* hs_status_string(int status);
 const char* hs_last_cuda_error(void);

@@ -80,6 +80,23 @@ class HsAdamState(ctypes.Structure):
     _fields_ = [("m", c_void_p * 7), ("v", c_void_p * 7), ("t", c_int64 * 8)]
 
 
+class HsDensifyStats(ctypes.Structure):
+    _fields_ = [("grad_sum", c_void_p), ("mu_grad_sum", c_void_p), ("count", c_void_p)]
+
+
+class HsDensifyConfig(ctypes.Structure):
+    _fields_ = [("densify_grad_threshold", ctypes.c_double),
+                ("prune_opacity_threshold", ctypes.c_double),
+                ("percent_dense", ctypes.c_double), ("prune_extent_factor", ctypes.c_double),
+                ("scene_extent", ctypes.c_double), ("log_split_scale", ctypes.c_double),
+                ("max_primitives", c_int64)]
+
+
+class HsDensifyPlan(ctypes.Structure):
+    _fields_ = [("n_in", c_int64), ("n_out", c_int64), ("kept", c_int64), ("cloned", c_int64),
+                ("split", c_int64), ("pruned", c_int64)]
+
+
 # name -> (restype, argtypes); every symbol declared in include/halfsplat_b200.h
 _SIGNATURES = {
     "hs_frame_init": (c_int32, [ctypes.POINTER(HsFrame), c_int64, c_int32, c_int32, c_int32]),
@@ -111,6 +128,20 @@ _SIGNATURES = {
     "hs_adam_step": (c_int32, [ctypes.POINTER(HsScene), ctypes.POINTER(HsGrads),
                                ctypes.POINTER(HsAdamState), ctypes.POINTER(ctypes.c_double),
                                c_int32, c_void_p]),
+    "hs_densify_stats_update": (c_int32, [ctypes.POINTER(HsDensifyStats),
+                                          ctypes.POINTER(HsGrads), c_int64, c_int32, c_void_p]),
+    "hs_densify_workspace_size": (c_size_t, [c_int64]),
+    "hs_densify_plan_compute": (c_int32, [ctypes.POINTER(HsScene), ctypes.POINTER(HsDensifyStats),
+                                          ctypes.POINTER(HsDensifyConfig),
+                                          ctypes.POINTER(HsDensifyPlan), c_void_p, c_size_t,
+                                          c_void_p]),
+    "hs_densify_apply": (c_int32, [ctypes.POINTER(HsScene), ctypes.POINTER(HsDensifyStats),
+                                   ctypes.POINTER(HsDensifyConfig), ctypes.POINTER(HsDensifyPlan),
+                                   c_void_p, c_size_t, c_void_p, ctypes.c_uint64,
+                                   ctypes.POINTER(HsAdamState), ctypes.POINTER(HsScene),
+                                   ctypes.POINTER(HsAdamState), c_void_p]),
+    "hs_reset_opacity": (c_int32, [ctypes.POINTER(HsScene), ctypes.c_double,
+                                   ctypes.POINTER(HsAdamState), c_void_p]),
     "hs_status_string": (ctypes.c_char_p, [c_int32]),
     "hs_last_cuda_error": (ctypes.c_char_p, []),
     "hs_kernel_launch_count": (c_int64, []),

@@ -31,6 +31,7 @@ SOURCES = {
     "hs_geometry_bwd.cu": [],
     "hs_loss.cu": [],
     "hs_adam.cu": ["-fmad=false"],
+    "hs_densify.cu": ["-fmad=false"],
     "hs_binning.cu": [],
     "hs_blend.cu": [],
     "hs_capi.cu": [],

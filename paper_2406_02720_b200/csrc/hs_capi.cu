@@ -772,3 +772,163 @@ extern "C" int hs_adam_step(const hs_scene* scene, const hs_grads* grads, hs_ada
     if (on[g]) state->t[g] += 1;
   return HS_OK;
 }
+
+// ---- density control (trainer.py:229-350) --------------------------------------
+namespace {
+hs::DensifyStatsArgs stats_args(const hs_densify_stats* s) {
+  return {s->grad_sum, s->mu_grad_sum, s->count};
+}
+hs::DensifyBufs carve_densify(void* ws, int64_t n, size_t* bytes) {
+  Carver c(ws);
+  hs::DensifyBufs b;
+  b.flags = c.take<uint8_t>(n + 1);
+  b.f_surv = c.take<int32_t>(n + 1);
+  b.f_clone = c.take<int32_t>(n + 1);
+  b.f_split = c.take<int32_t>(n + 1);
+  b.surv_rank = c.take<int32_t>(n + 1);
+  b.clone_rank = c.take<int32_t>(n + 1);
+  b.split_rank = c.take<int32_t>(n + 1);
+  b.temp_bytes = hs::densify_scan_temp_bytes(n);
+  b.temp = c.take<char>(b.temp_bytes);
+  *bytes = c.off;
+  return b;
+}
+}  // namespace
+
+extern "C" int hs_densify_stats_update(const hs_densify_stats* stats, const hs_grads* grads,
+                                       int64_t n, int32_t dtype, void* stream_) {
+  if (!stats || !grads || n < 0) return HS_ERR_INVALID_ARG;
+  if (n == 0) return HS_OK;
+  HS_CUDA(hs::launch_densify_stats(stats_args(stats), grads->pos_grad_norm, grads->d_mu,
+                                   grads->touch_count, n, dtype == HS_DTYPE_F64 ? 1 : 0,
+                                   static_cast<cudaStream_t>(stream_)));
+  return HS_OK;
+}
+
+extern "C" size_t hs_densify_workspace_size(int64_t n) {
+  if (n < 0 || n >= ((int64_t)1 << 31) - 1) return 0;
+  size_t bytes = 0;
+  carve_densify(nullptr, n, &bytes);
+  return bytes;
+}
+
+extern "C" int hs_densify_plan_compute(const hs_scene* scene, const hs_densify_stats* stats,
+                                       const hs_densify_config* cfg, hs_densify_plan* plan,
+                                       void* ws, size_t ws_bytes, void* stream_) {
+  if (!scene || !stats || !cfg || !plan) return HS_ERR_INVALID_ARG;
+  const int64_t n = scene->n;
+  if (n < 0 || n >= ((int64_t)1 << 31) - 1) return HS_ERR_INVALID_ARG;
+  size_t need = 0;
+  carve_densify(nullptr, n, &need);
+  if (!ws || ws_bytes < need) return HS_ERR_WORKSPACE;
+  hs::DensifyBufs b = carve_densify(ws, n, &need);
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  memset(plan, 0, sizeof(*plan));
+  plan->n_in = n;
+  if (n == 0) return HS_OK;
+  const hs::DensifyParams p{cfg->densify_grad_threshold, cfg->prune_opacity_threshold,
+                            cfg->percent_dense, cfg->prune_extent_factor, cfg->scene_extent};
+  HS_CUDA(hs::launch_densify_classify(stats_args(stats), scene->log_scale, scene->raw_opacity_a,
+                                      scene->raw_opacity_b, n,
+                                      scene->dtype == HS_DTYPE_F64 ? 1 : 0, p, b, stream));
+  int32_t tot[3];
+  HS_CUDA(cudaMemcpyAsync(&tot[0], b.surv_rank + n, 4, cudaMemcpyDeviceToHost, stream));
+  HS_CUDA(cudaMemcpyAsync(&tot[1], b.clone_rank + n, 4, cudaMemcpyDeviceToHost, stream));
+  HS_CUDA(cudaMemcpyAsync(&tot[2], b.split_rank + n, 4, cudaMemcpyDeviceToHost, stream));
+  HS_CUDA(cudaStreamSynchronize(stream));
+  const int64_t surv0 = tot[0], nc = tot[1], ns = tot[2];
+  // the reference's budget loops (trainer.py:268-288): clones first, then splits,
+  // each in index order; over-budget split parents are kept unsplit
+  int64_t acc_c = nc, acc_s = ns;
+  if (cfg->max_primitives > 0) {
+    const int64_t base = surv0 + ns;
+    int64_t budget = cfg->max_primitives - base;
+    if (budget < 0) budget = 0;
+    acc_c = nc < budget ? nc : budget;
+    budget -= acc_c;
+    acc_s = ns < budget ? ns : budget;
+  }
+  plan->kept = surv0 + (ns - acc_s);
+  plan->cloned = acc_c;
+  plan->split = acc_s;
+  plan->pruned = n - surv0 - ns;
+  plan->n_out = plan->kept + acc_c + 2 * acc_s;
+  return HS_OK;
+}
+
+namespace {
+template <typename T>
+int densify_apply_t(const hs_scene* scene, const hs_densify_stats* stats,
+                    const hs_densify_config* cfg, const hs_densify_plan* plan,
+                    const hs::DensifyBufs& b, const double* offsets, uint64_t seed,
+                    const hs_adam_state* sin, hs_scene* out, hs_adam_state* sout,
+                    cudaStream_t stream) {
+  hs::DensifyEmitArgs<T> a;
+  memset(&a, 0, sizeof(a));
+  a.n = scene->n;
+  a.K = (scene->sh_degree + 1) * (scene->sh_degree + 1);
+  a.flags = b.flags;
+  a.surv_rank = b.surv_rank;
+  a.clone_rank = b.clone_rank;
+  a.split_rank = b.split_rank;
+  a.acc_clone = plan->cloned;
+  a.acc_split = plan->split;
+  a.n_surv = plan->kept;
+  a.mu_grad_sum = stats->mu_grad_sum;
+  a.offsets = offsets;
+  a.seed = seed;
+  a.log_split_scale = cfg->log_split_scale;
+  a.in = {(const T*)scene->mu, (const T*)scene->log_scale, (const T*)scene->rotation,
+          (const T*)scene->sh_coeffs, (const T*)scene->normal, (const T*)scene->raw_opacity_a,
+          (const T*)scene->raw_opacity_b};
+  a.out = {(T*)out->mu, (T*)out->log_scale, (T*)out->rotation, (T*)out->sh_coeffs,
+           (T*)out->normal, (T*)out->raw_opacity_a, (T*)out->raw_opacity_b};
+  for (int f = 0; f < 7; ++f) {
+    const bool have = sin && sout && sin->m[f] && sin->v[f] && sout->m[f] && sout->v[f];
+    a.m_in[f] = have ? sin->m[f] : nullptr;
+    a.v_in[f] = have ? sin->v[f] : nullptr;
+    a.m_out[f] = have ? sout->m[f] : nullptr;
+    a.v_out[f] = have ? sout->v[f] : nullptr;
+  }
+  HS_CUDA(hs::launch_densify_emit_t<T>(a, stream));
+  return HS_OK;
+}
+}  // namespace
+
+extern "C" int hs_densify_apply(const hs_scene* scene, const hs_densify_stats* stats,
+                                const hs_densify_config* cfg, const hs_densify_plan* plan,
+                                const void* ws, size_t ws_bytes, const double* split_offsets,
+                                uint64_t seed, const hs_adam_state* state_in, hs_scene* out,
+                                hs_adam_state* state_out, void* stream_) {
+  if (!scene || !stats || !cfg || !plan || !out) return HS_ERR_INVALID_ARG;
+  if (plan->n_in != scene->n || out->n != plan->n_out || out->dtype != scene->dtype ||
+      out->sh_degree != scene->sh_degree)
+    return HS_ERR_INVALID_ARG;
+  size_t need = 0;
+  carve_densify(nullptr, scene->n, &need);
+  if (!ws || ws_bytes < need) return HS_ERR_WORKSPACE;
+  const hs::DensifyBufs b = carve_densify(const_cast<void*>(ws), scene->n, &need);
+  if (state_in && state_out)
+    for (int g = 0; g < HS_ADAM_GROUPS; ++g) state_out->t[g] = state_in->t[g];
+  if (scene->n == 0 || plan->n_out == 0) return HS_OK;
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  if (scene->dtype == HS_DTYPE_F64)
+    return densify_apply_t<double>(scene, stats, cfg, plan, b, split_offsets, seed, state_in, out,
+                                   state_out, stream);
+  return densify_apply_t<float>(scene, stats, cfg, plan, b, split_offsets, seed, state_in, out,
+                                state_out, stream);
+}
+
+extern "C" int hs_reset_opacity(const hs_scene* scene, double cap, hs_adam_state* state,
+                                void* stream_) {
+  if (!scene) return HS_ERR_INVALID_ARG;
+  if (scene->n == 0) return HS_OK;
+  HS_CUDA(hs::launch_reset_opacity(const_cast<void*>(scene->raw_opacity_a),
+                                   const_cast<void*>(scene->raw_opacity_b),
+                                   state ? state->m[5] : nullptr, state ? state->v[5] : nullptr,
+                                   state ? state->m[6] : nullptr, state ? state->v[6] : nullptr,
+                                   scene->n, cap, scene->dtype == HS_DTYPE_F64 ? 1 : 0,
+                                   static_cast<cudaStream_t>(stream_)));
+  if (state) state->t[HS_GROUP_OPACITY_A] = state->t[HS_GROUP_OPACITY_B] = 0;
+  return HS_OK;
+}

@@ -164,4 +164,50 @@ struct AdamArgs {
 };
 cudaError_t launch_adam(AdamArgs a, int dtype, cudaStream_t stream);
 
+// ---- hs_densify.cu ----------------------------------------------------------
+struct DensifyStatsArgs {
+  double* grad_sum;     // (n,)
+  double* mu_grad_sum;  // (n,3)
+  int64_t* count;       // (n,)
+};
+struct DensifyParams {
+  double densify_grad_threshold, prune_opacity_threshold, percent_dense, prune_extent_factor,
+      scene_extent;
+};
+struct DensifyBufs {
+  uint8_t* flags;
+  int32_t *f_surv, *f_clone, *f_split;           // n + 1 each
+  int32_t *surv_rank, *clone_rank, *split_rank;  // exclusive scans, n + 1 each
+  void* temp;
+  size_t temp_bytes;
+};
+template <typename T>
+struct DensifyEmitArgs {
+  int64_t n;
+  int K;
+  const uint8_t* flags;
+  const int32_t *surv_rank, *clone_rank, *split_rank;
+  int64_t acc_clone, acc_split, n_surv;
+  const double* mu_grad_sum;
+  const double* offsets;  // (2, acc_split, 3) standard normals or nullptr (Philox)
+  uint64_t seed;
+  double log_split_scale;
+  struct { const T *mu, *ls, *rot, *sh, *nrm, *ra, *rb; } in;
+  struct { T *mu, *ls, *rot, *sh, *nrm, *ra, *rb; } out;
+  const void* m_in[7];
+  const void* v_in[7];
+  void* m_out[7];
+  void* v_out[7];
+};
+cudaError_t launch_densify_stats(const DensifyStatsArgs& st, const void* pgn, const void* d_mu,
+                                 const int32_t* touch, int64_t n, int dtype, cudaStream_t s);
+size_t densify_scan_temp_bytes(int64_t n);
+cudaError_t launch_densify_classify(const DensifyStatsArgs& st, const void* log_scale,
+                                    const void* ra, const void* rb, int64_t n, int dtype,
+                                    const DensifyParams& p, DensifyBufs& b, cudaStream_t s);
+template <typename T>
+cudaError_t launch_densify_emit_t(const DensifyEmitArgs<T>& a, cudaStream_t s);
+cudaError_t launch_reset_opacity(void* ra, void* rb, void* ma, void* va, void* mb, void* vb,
+                                 int64_t n, double cap, int dtype, cudaStream_t s);
+
 }  // namespace hs

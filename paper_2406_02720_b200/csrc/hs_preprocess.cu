@@ -20,6 +20,7 @@
 
 #include "hs_common.cuh"
 #include "hs_internal.h"
+#include "hs_numpy_order.cuh"
 
 namespace hs {
 
@@ -58,11 +59,6 @@ struct FwdState {
   double basis[16];
   double rgbu[3];
 };
-
-// sigmoid, geometry.py:349-352
-__device__ __forceinline__ double sigmoid_ref(double x) {
-  return x >= 0.0 ? 1.0 / (1.0 + exp(-x)) : exp(x) / (1.0 + exp(x));
-}
 
 // eval_sh_basis, sh.py:32-61 (left-to-right evaluation of each product)
 __device__ __forceinline__ void sh_basis(const double d[3], int deg, double* out) {
@@ -128,24 +124,6 @@ __device__ __forceinline__ void sh_basis_grad(const double d[3], int deg, double
   }
 }
 
-// quat_to_rot, geometry.py:27-49 (normalises its input again, as the reference
-// calls it on the already-normalised quaternion, rasterizer.py:174-176).
-__device__ __forceinline__ void quat_to_rot_ref(const double q_in[4], double R[9]) {
-  double ss = 0.0;
-  for (int k = 0; k < 4; ++k) ss += q_in[k] * q_in[k];
-  const double n = sqrt(ss);
-  const double w = q_in[0] / n, x = q_in[1] / n, y = q_in[2] / n, z = q_in[3] / n;
-  R[0] = 1 - 2 * (y * y + z * z);
-  R[1] = 2 * (x * y - w * z);
-  R[2] = 2 * (x * z + w * y);
-  R[3] = 2 * (x * y + w * z);
-  R[4] = 1 - 2 * (x * x + z * z);
-  R[5] = 2 * (y * z - w * x);
-  R[6] = 2 * (x * z - w * y);
-  R[7] = 2 * (y * z + w * x);
-  R[8] = 1 - 2 * (x * x + y * y);
-}
-
 // einsum("ab,nbc,dc->nad") / ("nab,nbc,ndc->nad"): sequential over b then c,
 // each term ((A[a,b] * C[b,c]) * A[d,c]), accumulated from 0.
 __device__ __forceinline__ void sandwich(const double A[9], const double C[9], double out[9]) {
@@ -156,20 +134,6 @@ __device__ __forceinline__ void sandwich(const double A[9], const double C[9], d
         for (int c = 0; c < 3; ++c) s += A[3 * a + b] * C[3 * b + c] * A[3 * d + c];
       out[3 * a + d] = s;
     }
-}
-
-// einsum("nab,nb->na"): numpy pairs the 3-term reduction as (x0 + x2) + x1.
-__device__ __forceinline__ void matvec_einsum(const double M[9], const double v[3], double out[3]) {
-  for (int a = 0; a < 3; ++a) {
-    const double x0 = M[3 * a] * v[0], x1 = M[3 * a + 1] * v[1], x2 = M[3 * a + 2] * v[2];
-    out[a] = (x0 + x2) + x1;
-  }
-}
-
-// (N,3) @ (3,3)^T through OpenBLAS: fma(v2, M[a,2], fma(v1, M[a,1], v0 * M[a,0])).
-__device__ __forceinline__ void matvec_blas(const double M[9], const double v[3], double out[3]) {
-  for (int a = 0; a < 3; ++a)
-    out[a] = fma(v[2], M[3 * a + 2], fma(v[1], M[3 * a + 1], v[0] * M[3 * a]));
 }
 
 // ---------------------------------------------------------------------------

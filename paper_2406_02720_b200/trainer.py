@@ -7,8 +7,9 @@ the scene, its gradients and the Adam moments are CUDA tensors and the update is
 one `hs_adam_step` launch (csrc/hs_adam.cu).  The learning-rate schedule is
 scalar host arithmetic, evaluated exactly as the reference does.
 
-Densification (trainer.py:229-350) and the run loop / checkpoints are not part of
-this module (scope).
+Density control (trainer.py:229-350) runs on the device too: `DensifyStats`,
+`densify_and_prune` (hs_densify_plan_compute + hs_densify_apply) and
+`reset_opacity`.  The run loop / metrics / checkpoints are not part of this module.
 """
 
 import ctypes
@@ -186,9 +187,7 @@ def adam_step(scene, grads, config, opt_state, iteration, spatial_scale=1.0):
     lrs = learning_rates(config, iteration, spatial_scale)
     enabled = active_groups(config)
     lr = (ctypes.c_double * 8)(*[(lrs[g] if g in enabled else 0.0) for g in GROUPS])
-    g = _native.HsGrads()
-    for name in device.DeviceGradientSet.NAMES:
-        setattr(g, name, getattr(grads, name).data_ptr())
+    g = _grads_struct(grads)
     st = opt_state.struct()
     sc = device.scene_struct(scene)
     lib = _native.load()
@@ -197,6 +196,119 @@ def adam_step(scene, grads, config, opt_state, iteration, spatial_scale=1.0):
                   "hs_adam_step")
     for k, name in enumerate(GROUPS):
         opt_state.t[name] = int(st.t[k])
+
+
+def _grads_struct(grads):
+    g = _native.HsGrads()
+    for name in device.DeviceGradientSet.NAMES:
+        setattr(g, name, getattr(grads, name).data_ptr())
+    return g
+
+
+class DensifyStats:
+    """Screen-space gradient statistics between densify events (trainer.py:229-244),
+    float64 / int64 device tensors."""
+
+    def __init__(self, grad_sum, mu_grad_sum, count):
+        self.grad_sum, self.mu_grad_sum, self.count = grad_sum, mu_grad_sum, count
+
+    @classmethod
+    def zeros(cls, n, device="cuda"):
+        return cls(torch.zeros(n, dtype=torch.float64, device=device),
+                   torch.zeros((n, 3), dtype=torch.float64, device=device),
+                   torch.zeros(n, dtype=torch.int64, device=device))
+
+    def struct(self):
+        s = _native.HsDensifyStats()
+        s.grad_sum = self.grad_sum.data_ptr()
+        s.mu_grad_sum = self.mu_grad_sum.data_ptr()
+        s.count = self.count.data_ptr()
+        return s
+
+    def update(self, grads):
+        """DensifyStats.update (trainer.py:241-244), one launch."""
+        n = self.grad_sum.shape[0]
+        dt = _native.HS_DTYPE_F64 if grads.d_mu.dtype == torch.float64 else _native.HS_DTYPE_F32
+        st = self.struct()
+        _native.check(_native.load().hs_densify_stats_update(
+            ctypes.byref(st), ctypes.byref(_grads_struct(grads)), n, dt, device._stream()),
+            "hs_densify_stats_update")
+
+
+def densify_and_prune(scene, stats, config, opt_state, rng, scene_extent):
+    """Clone small / split large high-gradient primitives, prune weak ones
+    (trainer.py:247-340).  Returns (scene, stats, report); `opt_state` is re-aligned
+    with the new rows in place.
+
+    `rng`: a numpy Generator draws the split offsets exactly as the reference
+    does (two rng.normal((k, 3)) calls, only when k > 0), so a float64 scene
+    densifies bit-identically; an int (or None) seeds the device Philox draw."""
+    from .geometry import Scene
+    lib = _native.load()
+    n = len(scene)
+    ws = torch.empty(max(lib.hs_densify_workspace_size(n), 1), dtype=torch.uint8,
+                     device=scene.device)
+    cfg = _native.HsDensifyConfig(
+        config.densify_grad_threshold, config.prune_opacity_threshold, config.percent_dense,
+        config.prune_extent_factor, float(scene_extent),
+        float(np.log(config.split_scale_factor)), int(config.max_primitives))
+    sc = device.scene_struct(scene)
+    st = stats.struct()
+    plan = _native.HsDensifyPlan()
+    s = device._stream()
+    _native.check(lib.hs_densify_plan_compute(ctypes.byref(sc), ctypes.byref(st),
+                                              ctypes.byref(cfg), ctypes.byref(plan),
+                                              ws.data_ptr(), ws.numel(), s),
+                  "hs_densify_plan_compute")
+    m = int(plan.n_out)
+    k = (scene.sh_degree + 1) ** 2
+    new = Scene(torch.empty((m, 3)), torch.empty((m, 3)), torch.empty((m, 4)),
+                torch.empty((m, k, 3)), torch.empty((m, 3)), torch.empty(m), torch.empty(m),
+                sh_degree=scene.sh_degree, background_color=scene.background_color,
+                device=scene.device, dtype=scene.dtype, validate=False)
+    offsets, seed = None, 0
+    if isinstance(rng, np.random.Generator):
+        if plan.split:
+            draws = [rng.normal(size=(int(plan.split), 3)) for _ in range(2)]
+            offsets = torch.as_tensor(np.stack(draws), dtype=torch.float64, device=scene.device)
+    else:
+        seed = int(rng or 0)
+    new_state = None
+    sin = sout = None
+    if opt_state is not None:
+        new_m = [torch.empty((m,) + a.shape[1:], dtype=a.dtype, device=a.device)
+                 for a in opt_state._m]
+        new_v = [torch.empty_like(a) for a in new_m]
+        sin = opt_state.struct()
+        sout = _native.HsAdamState()
+        for f in range(7):
+            sout.m[f] = new_m[f].data_ptr()
+            sout.v[f] = new_v[f].data_ptr()
+        new_state = (new_m, new_v)
+    out = device.scene_struct(new)
+    _native.check(lib.hs_densify_apply(
+        ctypes.byref(sc), ctypes.byref(st), ctypes.byref(cfg), ctypes.byref(plan),
+        ws.data_ptr(), ws.numel(), offsets.data_ptr() if offsets is not None else None, seed,
+        ctypes.byref(sin) if sin is not None else None, ctypes.byref(out),
+        ctypes.byref(sout) if sout is not None else None, s), "hs_densify_apply")
+    if new_state is not None:
+        opt_state._m, opt_state._v = new_state
+    report = {"cloned": int(plan.cloned), "split": int(plan.split), "pruned": int(plan.pruned)}
+    return new, DensifyStats.zeros(m, scene.device), report
+
+
+def reset_opacity(scene, opt_state=None, ceiling=0.01):
+    """Clamp both opacity logits so sigmoid <= ceiling (trainer.py:343-350)."""
+    p = np.float64(ceiling)
+    cap = float(np.log(p) - np.log1p(-p))  # logit, geometry.py:355-358
+    st = opt_state.struct() if opt_state is not None else None
+    sc = device.scene_struct(scene)
+    _native.check(_native.load().hs_reset_opacity(
+        ctypes.byref(sc), cap, ctypes.byref(st) if st is not None else None, device._stream()),
+        "hs_reset_opacity")
+    if opt_state is not None:
+        opt_state.t["opacity_a"] = 0
+        opt_state.t["opacity_b"] = 0
 
 
 class Trainer:

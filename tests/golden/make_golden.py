@@ -253,12 +253,93 @@ def adam_fixture():
     print("adam:", len(cases), "cases")
 
 
+def densify_fixture():
+    """densify_and_prune + reset_opacity (trainer.py:229-350) of the reference on a
+    random float32-representable scene with random statistics and Adam moments:
+    unlimited, a budget that accepts some clones and no splits, a budget that
+    splits part of the candidates, and zero accumulated gradients (clone
+    direction 0).  The split offsets come from rng = default_rng(seed)."""
+    from halfsplat import geometry
+    from halfsplat import trainer as T
+    d = {}
+    cases = {"unlimited": 0, "budget_clones": 10**9, "budget_split": 10**9, "zero_grad": 0}
+    for ci, (name, maxp) in enumerate(cases.items()):
+        rng = np.random.default_rng(300 + ci)
+        f32 = lambda a: np.asarray(a, dtype=np.float32).astype(np.float64)  # noqa: E731
+        n, deg = 160, 2
+        k = (deg + 1) ** 2
+        nrm = rng.normal(size=(n, 3))
+        nrm /= np.linalg.norm(nrm, axis=1, keepdims=True)
+        ls = f32(rng.uniform(-5.0, -3.0, (n, 3)))
+        ls[:5] = f32(rng.uniform(-1.2, -1.0, (5, 3)))  # too large: pruned by extent
+        ra = f32(rng.normal(0, 3, n))
+        sc = geometry.Scene(mu=f32(rng.uniform(-1, 1, (n, 3))), log_scale=ls,
+                            rotation=f32(rng.normal(size=(n, 4))),
+                            sh_coeffs=f32(rng.normal(0, 0.3, (n, k, 3))), normal=f32(nrm),
+                            raw_opacity_a=ra, raw_opacity_b=f32(rng.normal(0, 3, n)),
+                            sh_degree=deg)
+        stats = T.DensifyStats.zeros(n)
+        stats.count[:] = rng.integers(0, 5, n)
+        stats.grad_sum[:] = f32(rng.uniform(0, 1.2e-3, n)) * stats.count
+        stats.mu_grad_sum[:] = f32(rng.normal(0, 1e-3, (n, 3)))
+        if name == "zero_grad":
+            stats.mu_grad_sum[:] = 0.0
+        opt = T.AdamState(sc)
+        for g in T.GROUPS:
+            opt.m[g][...] = f32(rng.normal(size=opt.m[g].shape))
+            opt.v[g][...] = f32(rng.uniform(0, 1, opt.v[g].shape))
+            opt.t[g] = 7
+        # budgets relative to this scene's counts
+        avg = np.where(stats.count > 0, stats.grad_sum / np.maximum(stats.count, 1), 0.0)
+        a1, a2 = sc.alphas()
+        mx = np.exp(sc.log_scale).max(axis=1)
+        extent = 2.0
+        prune = (np.maximum(a1, a2) < 0.005) | (mx > 0.1 * extent)
+        hot = (avg >= 2e-4) & ~prune
+        nclone = int((hot & (mx <= 0.01 * extent)).sum())
+        nsplit = int((hot & (mx > 0.01 * extent)).sum())
+        base = int((~prune & ~(hot & (mx > 0.01 * extent))).sum()) + nsplit
+        if name == "budget_clones":
+            maxp = base + nclone // 2
+        elif name == "budget_split":
+            maxp = base + nclone + nsplit // 3
+        cfg = T.TrainConfig(total_iters=100, densify_until=50, max_primitives=maxp)
+        # float32-representable inputs (and their copies) are stored as float32
+        d[f"{name}_scene"] = np.concatenate([getattr(sc, f).reshape(n, -1) for f in SCENE_FIELDS],
+                                            axis=1).astype(np.float32)
+        d[f"{name}_stats"] = np.concatenate([stats.grad_sum[:, None], stats.mu_grad_sum,
+                                             stats.count[:, None].astype(np.float64)], axis=1)
+        d[f"{name}_m"] = np.concatenate([opt.m[g].reshape(n, -1) for g in T.GROUPS],
+                                        axis=1).astype(np.float32)
+        d[f"{name}_v"] = np.concatenate([opt.v[g].reshape(n, -1) for g in T.GROUPS],
+                                        axis=1).astype(np.float32)
+        d[f"{name}_seed"] = np.int64(1000 + ci)
+        d[f"{name}_max_primitives"] = np.int64(maxp)
+        new, _, report = T.densify_and_prune(sc, stats, cfg, opt, np.random.default_rng(1000 + ci),
+                                             extent)
+        m = len(new)
+        d[f"{name}_out"] = np.concatenate([getattr(new, f).reshape(m, -1) for f in SCENE_FIELDS],
+                                          axis=1)
+        d[f"{name}_out_m"] = np.concatenate([opt.m[g].reshape(m, -1) for g in T.GROUPS],
+                                            axis=1).astype(np.float32)
+        d[f"{name}_out_v"] = np.concatenate([opt.v[g].reshape(m, -1) for g in T.GROUPS],
+                                            axis=1).astype(np.float32)
+        d[f"{name}_report"] = np.array([report["cloned"], report["split"], report["pruned"]])
+        T.reset_opacity(new, opt, 0.01)
+        d[f"{name}_reset"] = np.stack([new.raw_opacity_a, new.raw_opacity_b], axis=1)
+        print(f"densify {name}: n {n} -> {m}, report {report}, max_primitives {maxp}")
+    d["cases"] = np.array(list(cases))
+    d["extent"] = np.float64(2.0)
+    np.savez_compressed(os.path.join(HERE, "densify.npz"), **d)
+
+
 SCENE_FIELDS = ("mu", "log_scale", "rotation", "sh_coeffs", "normal", "raw_opacity_a",
                 "raw_opacity_b")
 
 JOBS = {
     "erf": lambda t: erf_fixture(),
     "adam": lambda t: adam_fixture(),
+    "densify": lambda t: densify_fixture(),
     "loss": lambda t: loss_fixture(),
     # small scenes, every array
     "c1": lambda t: full_fixture("c1", scenes.make_config("c1"), 0, True, t),

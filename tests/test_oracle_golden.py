@@ -149,3 +149,24 @@ def test_adam_oracle_matches_reference():
             for f in A.FIELDS:
                 assert np.array_equal(params[f], after[f]), (name, it, f)
         assert [opt.t[g] for g in O.ADAM_GROUPS] == list(t_ref), name
+
+
+def test_densify_oracle_matches_reference():
+    """densify_and_prune / reset_opacity restated in numpy reproduce the
+    reference's new scenes, re-aligned moments and reports bit for bit."""
+    import adam_cases as A
+    gold = load_golden("densify")
+    for name in gold["cases"]:
+        c = A.densify_case(gold, name)
+        cfg = dict(A.DENSIFY_CFG, max_primitives=c["max_primitives"])
+        new, nm, nv, report = O.densify_and_prune(
+            {f: a.copy() for f, a in c["params"].items()}, *c["stats"], c["m"], c["v"], cfg,
+            c["extent"], np.random.default_rng(c["seed"]))
+        assert report == c["report"], name
+        for f in A.FIELDS:
+            assert np.array_equal(new[f], c["out"][f]), (name, f)
+            assert np.array_equal(nm[f], c["out_m"][f]), (name, f)
+            assert np.array_equal(nv[f], c["out_v"][f]), (name, f)
+        O.reset_opacity(new, 0.01)
+        assert np.array_equal(np.stack([new["raw_opacity_a"], new["raw_opacity_b"]], 1),
+                              c["reset"]), name
