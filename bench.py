@@ -353,6 +353,8 @@ def main():
     adam = T.AdamState(scene)
     it_counter = [0]
 
+    dstats = T.DensifyStats.zeros(len(scene))
+
     def train_step(t=None):
         for j, v in enumerate(views):
             o = rast.render(scene, cams[v])
@@ -363,6 +365,7 @@ def main():
             reducer.allreduce()
         with (t.span("adam") if t is not None else contextlib.nullcontext()):
             T.adam_step(scene, grads, tcfg, adam, it_counter[0])
+        dstats.update(grads)
         it_counter[0] += 1
 
     for _ in range(3):
@@ -376,6 +379,23 @@ def main():
     train_ms = start.elapsed_time(end) / args.steps
     loss_ms = statistics.mean(loss_timer.totals().get("loss", [float("nan")]))
     adam_ms = statistics.mean(loss_timer.totals().get("adam", [float("nan")]))
+    # one density-control event on the accumulated statistics (plan + host sync + apply),
+    # device Philox split offsets; wall-clock bracketed by synchronizes (it syncs inside)
+    extent = T.camera_extent(cams) if len(cams) > 1 else 1.0
+    for rep in range(2):  # the second event runs with the allocator warm
+        adam_copy = T.AdamState.__new__(T.AdamState)
+        adam_copy._m, adam_copy._v, adam_copy.t = list(adam._m), list(adam._v), dict(adam.t)
+        barrier()
+        t0 = time.perf_counter()
+        dense_scene, _, dense_report = T.densify_and_prune(scene, dstats, tcfg, adam_copy, 1,
+                                                           extent)
+        torch.cuda.synchronize()
+        densify_ms = (time.perf_counter() - t0) * 1e3
+        if rep == 0:
+            del dense_scene, adam_copy
+    densify = {"ms": densify_ms, "n_in": len(scene), "n_out": len(dense_scene), **dense_report,
+               "what": "one densify_and_prune on the train steps' statistics, Philox offsets"}
+    del dense_scene
     # Adam moves param, m, v (read+write) and reads grad: 28 B per float32 element
     adam_bytes = sum(getattr(scene, f).numel() for f in scene.FIELDS) * 7 * scene.mu.element_size()
 
@@ -437,7 +457,8 @@ def main():
                                         / HBM_PEAK_GBS},
                            "what": "render -> L1+SSIM loss and cotangent on device (hs_loss, "
                                    "lambda 0.2) -> render_backward -> Adam on all 8 groups "
-                                   "(hs_adam_step), synthetic targets"},
+                                   "(hs_adam_step), synthetic targets",
+                           "densify": densify},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clock_info,
             "counts": {"P": out.frame.num_pairs, "fwd_evals": fwd_evals, "bwd_evals": bwd_evals},

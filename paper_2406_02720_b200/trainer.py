@@ -262,9 +262,11 @@ def densify_and_prune(scene, stats, config, opt_state, rng, scene_extent):
                   "hs_densify_plan_compute")
     m = int(plan.n_out)
     k = (scene.sh_degree + 1) ** 2
-    new = Scene(torch.empty((m, 3)), torch.empty((m, 3)), torch.empty((m, 4)),
-                torch.empty((m, k, 3)), torch.empty((m, 3)), torch.empty(m), torch.empty(m),
-                sh_degree=scene.sh_degree, background_color=scene.background_color,
+    def alloc(*shape):
+        return torch.empty(shape, dtype=scene.dtype, device=scene.device)
+
+    new = Scene(alloc(m, 3), alloc(m, 3), alloc(m, 4), alloc(m, k, 3), alloc(m, 3), alloc(m),
+                alloc(m), sh_degree=scene.sh_degree, background_color=scene.background_color,
                 device=scene.device, dtype=scene.dtype, validate=False)
     offsets, seed = None, 0
     if isinstance(rng, np.random.Generator):
