@@ -309,6 +309,47 @@ int hs_densify_apply(const hs_scene* scene, const hs_densify_stats* stats,
  * `state` is given.  Writes the scene's opacity arrays. */
 int hs_reset_opacity(const hs_scene* scene, double cap, hs_adam_state* state, void* stream);
 
+/* ---- scene I/O: PLY payload <-> device scene (scene_io.py:136-269) ----- */
+
+#define HS_PLY_FLOAT 0   /* property float / float32 */
+#define HS_PLY_DOUBLE 1  /* property double / float64 */
+#define HS_PLY_UCHAR 2   /* property uchar / uint8 */
+#define HS_PLY_INT 3     /* property int / int32 */
+#define HS_PLY_MAX_PROPS 128
+
+#define HS_PLY_NATIVE 0       /* save_scene: double, x y z nx ny nz f_dc f_rest opacity opacity_2 scale rot */
+#define HS_PLY_3DGS_MEAN 1    /* export_3dgs(opacity="mean"): float, zero normals, one opacity */
+#define HS_PLY_3DGS_FIRST 2   /* export_3dgs(opacity="first") */
+
+/* The vertex payload of a parsed PLY header: `n` rows of `stride` bytes.
+ * offset/type: byte offset and HS_PLY_* type of each property.  column: for each
+ * scene component in field order (mu 3, log_scale 3, rotation 4, sh 3K as
+ * (coefficient, channel), normal 3, raw_opacity_a, raw_opacity_b) the source
+ * property index, or -1 to leave that component untouched. */
+typedef struct hs_ply_layout {
+  int64_t n;
+  int32_t stride;
+  int32_t n_props;
+  int32_t sh_degree;
+  int16_t offset[HS_PLY_MAX_PROPS];
+  int8_t type[HS_PLY_MAX_PROPS];
+  int16_t column[66];
+} hs_ply_layout;
+
+/* load_scene / import_3dgs payload step: de-interleave the device payload into
+ * the scene's device arrays (`out`, n rows, written), converting types and
+ * transposing f_rest from channel-major.  One launch. */
+int hs_ply_unpack(const void* payload, const hs_ply_layout* layout, hs_scene* out,
+                  void* stream);
+
+/* Bytes per payload row of hs_ply_pack's output for a layout kind. */
+int32_t hs_ply_row_bytes(int32_t sh_degree, int32_t kind);
+
+/* save_scene / export_3dgs payload step: interleave the scene into `payload`
+ * (device, n * hs_ply_row_bytes bytes) in the reference's property order.
+ * HS_PLY_3DGS_MEAN writes logit(clip((a1 + a2) / 2, 1e-6, 1 - 1e-6)). */
+int hs_ply_pack(const hs_scene* scene, void* payload, int32_t kind, void* stream);
+
 /* ---- misc --------------------------------------------------------------- */
 const char* hs_status_string(int status);
 const char* hs_last_cuda_error(void);

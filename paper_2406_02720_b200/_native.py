@@ -97,6 +97,12 @@ class HsDensifyPlan(ctypes.Structure):
                 ("split", c_int64), ("pruned", c_int64)]
 
 
+class HsPlyLayout(ctypes.Structure):
+    _fields_ = [("n", c_int64), ("stride", c_int32), ("n_props", c_int32),
+                ("sh_degree", c_int32), ("offset", ctypes.c_int16 * 128),
+                ("type", ctypes.c_int8 * 128), ("column", ctypes.c_int16 * 66)]
+
+
 # name -> (restype, argtypes); every symbol declared in include/halfsplat_b200.h
 _SIGNATURES = {
     "hs_frame_init": (c_int32, [ctypes.POINTER(HsFrame), c_int64, c_int32, c_int32, c_int32]),
@@ -142,6 +148,10 @@ _SIGNATURES = {
                                    ctypes.POINTER(HsAdamState), c_void_p]),
     "hs_reset_opacity": (c_int32, [ctypes.POINTER(HsScene), ctypes.c_double,
                                    ctypes.POINTER(HsAdamState), c_void_p]),
+    "hs_ply_unpack": (c_int32, [c_void_p, ctypes.POINTER(HsPlyLayout), ctypes.POINTER(HsScene),
+                                c_void_p]),
+    "hs_ply_row_bytes": (c_int32, [c_int32, c_int32]),
+    "hs_ply_pack": (c_int32, [ctypes.POINTER(HsScene), c_void_p, c_int32, c_void_p]),
     "hs_status_string": (ctypes.c_char_p, [c_int32]),
     "hs_last_cuda_error": (ctypes.c_char_p, []),
     "hs_kernel_launch_count": (c_int64, []),

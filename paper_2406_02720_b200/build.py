@@ -32,6 +32,7 @@ SOURCES = {
     "hs_loss.cu": [],
     "hs_adam.cu": ["-fmad=false"],
     "hs_densify.cu": ["-fmad=false"],
+    "hs_io.cu": ["-fmad=false"],
     "hs_binning.cu": [],
     "hs_blend.cu": [],
     "hs_capi.cu": [],

@@ -932,3 +932,65 @@ extern "C" int hs_reset_opacity(const hs_scene* scene, double cap, hs_adam_state
   if (state) state->t[HS_GROUP_OPACITY_A] = state->t[HS_GROUP_OPACITY_B] = 0;
   return HS_OK;
 }
+
+// ---- scene I/O (scene_io.py:136-269) -------------------------------------------
+static_assert(HS_PLY_MAX_PROPS == hs::kPlyMaxProps, "PLY property table size");
+static_assert(66 >= hs::kPlyMaxComps, "PLY component table size");
+
+extern "C" int hs_ply_unpack(const void* payload, const hs_ply_layout* layout, hs_scene* out,
+                             void* stream_) {
+  if (!payload || !layout || !out) return HS_ERR_INVALID_ARG;
+  if (layout->n != out->n || layout->sh_degree != out->sh_degree || layout->stride <= 0 ||
+      layout->n_props <= 0 || layout->n_props > HS_PLY_MAX_PROPS)
+    return HS_ERR_INVALID_ARG;
+  if (out->sh_degree < 0 || out->sh_degree > 3) return HS_ERR_INVALID_ARG;
+  if (layout->n == 0) return HS_OK;
+  hs::PlyUnpackArgs a;
+  memset(&a, 0, sizeof(a));
+  a.payload = payload;
+  a.n = layout->n;
+  a.stride = layout->stride;
+  a.K = (out->sh_degree + 1) * (out->sh_degree + 1);
+  for (int p = 0; p < layout->n_props; ++p) {
+    if (layout->offset[p] < 0 || layout->type[p] < 0 || layout->type[p] > HS_PLY_INT)
+      return HS_ERR_INVALID_ARG;
+    a.offset[p] = layout->offset[p];
+    a.type[p] = layout->type[p];
+  }
+  const int ncomp = 3 + 3 + 4 + 3 * a.K + 3 + 1 + 1;
+  for (int c = 0; c < ncomp; ++c) {
+    if (layout->column[c] >= layout->n_props) return HS_ERR_INVALID_ARG;
+    a.column[c] = layout->column[c];
+  }
+  const void* fields[7] = {out->mu, out->log_scale, out->rotation, out->sh_coeffs, out->normal,
+                           out->raw_opacity_a, out->raw_opacity_b};
+  HS_CUDA(hs::launch_ply_unpack(a, fields, out->dtype == HS_DTYPE_F64 ? 1 : 0,
+                                static_cast<cudaStream_t>(stream_)));
+  return HS_OK;
+}
+
+extern "C" int32_t hs_ply_row_bytes(int32_t sh_degree, int32_t kind) {
+  if (sh_degree < 0 || sh_degree > 3 || kind < HS_PLY_NATIVE || kind > HS_PLY_3DGS_FIRST)
+    return 0;
+  const int K = (sh_degree + 1) * (sh_degree + 1);
+  const int ncol = 9 + 3 * (K - 1) + (kind == HS_PLY_NATIVE ? 2 : 1) + 7;
+  return ncol * (kind == HS_PLY_NATIVE ? 8 : 4);
+}
+
+extern "C" int hs_ply_pack(const hs_scene* scene, void* payload, int32_t kind, void* stream_) {
+  if (!scene || !payload) return HS_ERR_INVALID_ARG;
+  if (hs_ply_row_bytes(scene->sh_degree, kind) == 0) return HS_ERR_INVALID_ARG;
+  if (scene->n == 0) return HS_OK;
+  hs::PlyPackArgs a;
+  a.payload = payload;
+  a.n = scene->n;
+  a.K = (scene->sh_degree + 1) * (scene->sh_degree + 1);
+  a.gs3d = kind != HS_PLY_NATIVE;
+  a.opacity_first = kind == HS_PLY_3DGS_FIRST;
+  a.out_f64 = kind == HS_PLY_NATIVE;
+  const void* fields[7] = {scene->mu, scene->log_scale, scene->rotation, scene->sh_coeffs,
+                           scene->normal, scene->raw_opacity_a, scene->raw_opacity_b};
+  HS_CUDA(hs::launch_ply_pack(a, fields, scene->dtype == HS_DTYPE_F64 ? 1 : 0,
+                              static_cast<cudaStream_t>(stream_)));
+  return HS_OK;
+}

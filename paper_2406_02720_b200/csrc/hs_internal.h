@@ -210,4 +210,34 @@ cudaError_t launch_densify_emit_t(const DensifyEmitArgs<T>& a, cudaStream_t s);
 cudaError_t launch_reset_opacity(void* ra, void* rb, void* ma, void* va, void* mb, void* vb,
                                  int64_t n, double cap, int dtype, cudaStream_t s);
 
+// ---- hs_io.cu ----------------------------------------------------------------
+enum PlyType { kPlyF32 = 0, kPlyF64 = 1, kPlyU8 = 2, kPlyI32 = 3 };
+constexpr int kPlyMaxProps = 128;
+constexpr int kPlyMaxComps = 3 + 3 + 4 + 48 + 3 + 1 + 1;
+struct PlyUnpackArgs {
+  const void* payload;  // device, n rows of `stride` bytes
+  int64_t n;
+  int stride;
+  int K;                       // SH coefficients per channel
+  int16_t offset[kPlyMaxProps];  // byte offset of each property in a row
+  int8_t type[kPlyMaxProps];     // PlyType of each property
+  int16_t column[kPlyMaxComps];  // source property of each scene component, -1 = skip
+};
+struct PlyPackArgs {
+  void* payload;  // device, n rows
+  int64_t n;
+  int K;
+  int gs3d;           // export_3dgs layout (zero normals, one opacity)
+  int opacity_first;  // export_3dgs(opacity="first")
+  int out_f64;        // double properties (native) / float
+};
+template <typename T>
+struct SceneOut { T *mu, *ls, *rot, *sh, *nrm, *ra, *rb; };
+template <typename T>
+struct SceneIn { const T *mu, *ls, *rot, *sh, *nrm, *ra, *rb; };
+cudaError_t launch_ply_unpack(const PlyUnpackArgs& a, const void* const* fields, int dtype,
+                              cudaStream_t s);
+cudaError_t launch_ply_pack(const PlyPackArgs& a, const void* const* fields, int dtype,
+                            cudaStream_t s);
+
 }  // namespace hs

@@ -333,6 +333,65 @@ def densify_fixture():
     np.savez_compressed(os.path.join(HERE, "densify.npz"), **d)
 
 
+def io_fixture():
+    """scene_io.py:136-269 of the reference: native save/load, 3D-GS export
+    (mean / first) and import (both normal inits), and a mixed-type native file
+    (float / double / uchar / int properties) read by load_scene."""
+    import tempfile
+    from halfsplat import geometry, scene_io
+    rng = np.random.default_rng(77)
+    n, deg = 45, 3
+    k = (deg + 1) ** 2
+    nrm = rng.normal(size=(n, 3))
+    sc = geometry.Scene(mu=rng.uniform(-1, 1, (n, 3)), log_scale=rng.uniform(-5, -2, (n, 3)),
+                        rotation=rng.normal(size=(n, 4)), sh_coeffs=rng.normal(0, 0.3, (n, k, 3)),
+                        normal=nrm / np.linalg.norm(nrm, axis=1, keepdims=True),
+                        raw_opacity_a=rng.normal(0, 3, n), raw_opacity_b=rng.normal(0, 3, n),
+                        sh_degree=deg, background_color=np.array([0.1, 0.25, 0.5]))
+    d = {"scene": np.concatenate([getattr(sc, f).reshape(n, -1) for f in SCENE_FIELDS], 1)}
+    tmp = tempfile.mkdtemp()
+
+    def file_bytes(fn):
+        with open(fn, "rb") as fh:
+            return np.frombuffer(fh.read(), dtype=np.uint8)
+
+    scene_io.save_scene(sc, f"{tmp}/native.ply")
+    d["native_ply"] = file_bytes(f"{tmp}/native.ply")
+    for mode in ("mean", "first"):
+        scene_io.export_3dgs(sc, f"{tmp}/gs_{mode}.ply", opacity=mode)
+        d[f"gs_{mode}_ply"] = file_bytes(f"{tmp}/gs_{mode}.ply")
+    for init in ("zero_plus_jitter", "random_unit"):
+        imp = scene_io.import_3dgs(f"{tmp}/gs_mean.ply", normal_init=init, seed=5,
+                                   background_color=(0.2, 0.2, 0.2))
+        d[f"import_{init}"] = np.concatenate([getattr(imp, f).reshape(n, -1)
+                                              for f in SCENE_FIELDS], 1)
+    # mixed property types, degree 1
+    m = 20
+    props = [("x", "f4"), ("y", "f8"), ("z", "i4"), ("nx", "f8"), ("ny", "f4"), ("nz", "u1"),
+             ("f_dc_0", "f4"), ("f_dc_1", "f8"), ("f_dc_2", "f4")]
+    props += [(f"f_rest_{i}", "f8" if i % 2 else "f4") for i in range(9)]
+    props += [("opacity", "f4"), ("opacity_2", "f8"), ("scale_0", "f8"), ("scale_1", "f4"),
+              ("scale_2", "f8"), ("rot_0", "i4"), ("rot_1", "f4"), ("rot_2", "f8"), ("rot_3", "u1")]
+    arr = np.zeros(m, dtype=[(nm, "<" + t) for nm, t in props])
+    for nm, t in props:
+        if t in ("i4", "u1"):
+            arr[nm] = rng.integers(1, 5, m)
+        else:
+            arr[nm] = rng.normal(size=m)
+    tname = {"f4": "float", "f8": "double", "i4": "int", "u1": "uchar"}
+    header = ["ply", "format binary_little_endian 1.0", "comment sh_degree 1",
+              f"element vertex {m}"] + [f"property {tname[t]} {nm}" for nm, t in props]
+    header.append("end_header")
+    with open(f"{tmp}/mixed.ply", "wb") as fh:
+        fh.write(("\n".join(header) + "\n").encode("ascii"))
+        fh.write(arr.tobytes())
+    d["mixed_ply"] = file_bytes(f"{tmp}/mixed.ply")
+    mixed = scene_io.load_scene(f"{tmp}/mixed.ply")
+    d["mixed_scene"] = np.concatenate([getattr(mixed, f).reshape(m, -1) for f in SCENE_FIELDS], 1)
+    np.savez_compressed(os.path.join(HERE, "io.npz"), **d)
+    print("io: native", d["native_ply"].size, "bytes; mixed", d["mixed_ply"].size, "bytes")
+
+
 SCENE_FIELDS = ("mu", "log_scale", "rotation", "sh_coeffs", "normal", "raw_opacity_a",
                 "raw_opacity_b")
 
@@ -340,6 +399,7 @@ JOBS = {
     "erf": lambda t: erf_fixture(),
     "adam": lambda t: adam_fixture(),
     "densify": lambda t: densify_fixture(),
+    "io": lambda t: io_fixture(),
     "loss": lambda t: loss_fixture(),
     # small scenes, every array
     "c1": lambda t: full_fixture("c1", scenes.make_config("c1"), 0, True, t),

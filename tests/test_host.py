@@ -129,3 +129,34 @@ def test_gradient_allreduce_gloo_world2():
     for _, flat, touch in res:
         np.testing.assert_array_equal(flat, base * 3)
         np.testing.assert_array_equal(touch, np.full(n, 3, np.int32))
+
+
+def test_scene_io_header_errors(tmp_path):
+    """scene_io header validation mirrors the reference's errors (scene_io.py:49-111);
+    all raised on the host before any device work."""
+    import pytest
+    from paper_2406_02720_b200 import errors, scene_io
+
+    def write(name, text, payload=b""):
+        p = tmp_path / name
+        p.write_bytes(text.encode("ascii") + payload)
+        return str(p)
+
+    with pytest.raises(errors.MalformedHeader):
+        scene_io.load_scene(write("a.ply", "plx\n"))
+    with pytest.raises(errors.MalformedHeader):
+        scene_io.load_scene(write("b.ply", "ply\nformat ascii 1.0\nend_header\n"))
+    with pytest.raises(errors.MalformedHeader):
+        scene_io.load_scene(write("c.ply", "ply\nformat binary_little_endian 1.0\n"
+                                           "element vertex 1\nproperty list uchar int f\n"
+                                           "end_header\n"))
+    with pytest.raises(errors.MissingProperty):
+        scene_io.load_scene(write("d.ply", "ply\nformat binary_little_endian 1.0\n"
+                                           "element vertex 1\nproperty double x\nend_header\n",
+                                  b"\0" * 8))
+    with pytest.raises(errors.TruncatedPayload):
+        scene_io.load_scene(write("e.ply", "ply\nformat binary_little_endian 1.0\n"
+                                           "element vertex 2\nproperty double x\nend_header\n",
+                                  b"\0" * 8))
+    with pytest.raises(ValueError):
+        scene_io.import_3dgs(write("f.ply", "ply\n"), normal_init="bogus")
