@@ -83,7 +83,8 @@ struct SplatLane {
   float A, B, C;       // conic scaled to log2: power = dx*(A dx + B dy) + C dy^2
   float P0, Bx;        // A dx^2, B dx
   float za, zb, Z0;    // erf coefficients, za*dx
-  double zbd, Z0d, py0d, muyd;  // steep path (FP64)
+  // steep splats: z(row offset o) = zK * (fma(zt_hi, o, zc_hi) + zc_lo + zt_lo o)
+  float zK, zc_hi, zc_lo, zt_hi, zt_lo;
 };
 
 template <bool STEEP>
@@ -103,10 +104,15 @@ __device__ __forceinline__ SplatLane splat_lane(const float4 (&q)[4], const Stee
   s.zb = q[1].z;
   s.Z0 = s.za * s.dx;
   if (STEEP) {
-    s.zbd = side.zb;
-    s.Z0d = side.za * ((double)px - side.mux);
-    s.py0d = (double)py0;
-    s.muyd = side.muy;
+    // the bracket at this lane's column and first row, in FP64 (SteepRec)
+    const double dxd = (double)px - side.mux, dyd = (double)py0 - side.muy;
+    const double c = side.xform ? fma(side.r, dyd, dxd) : fma(side.r, dxd, dyd);
+    const double t = side.xform ? side.r : 1.0;
+    s.zK = side.K;
+    s.zc_hi = (float)c;
+    s.zc_lo = (float)(c - (double)s.zc_hi);
+    s.zt_hi = (float)t;
+    s.zt_lo = (float)(t - (double)s.zt_hi);
   }
   return s;
 }
@@ -147,10 +153,22 @@ __device__ __forceinline__ float2 pair_dy(float dy0, int p) {
   return fadd2(f2(dy0), make_float2(4.0f * p, 4.0f * p + 2.0f));
 }
 
-// erf argument z of pixel i: FP32 for ordinary splats, FP64 (side record) for
-// steep ones.
+// steep z of a pixel pair (row offsets o = 4p, 4p + 2) and of one pixel; the
+// same operation sequence, so packed and scalar paths agree bit for bit
+__device__ __forceinline__ float2 steep_z2(const SplatLane& s, int p) {
+  const float2 o = make_float2(4.0f * p, 4.0f * p + 2.0f);
+  float2 b = fadd2(ffma2(f2(s.zt_hi), o, f2(s.zc_hi)), f2(s.zc_lo));
+  b = ffma2(f2(s.zt_lo), o, b);
+  return fmul2(f2(s.zK), b);
+}
+
+// erf argument z of pixel i: FP32 for ordinary splats, the side-record form
+// for steep ones.
 __device__ __forceinline__ float erf_arg(const SplatLane& s, bool steep, int i) {
-  if (steep) return (float)fma(s.zbd, (s.py0d + 2.0 * i) - s.muyd, s.Z0d);
+  if (steep) {
+    const float o = 2.0f * i;
+    return s.zK * fmaf(s.zt_lo, o, fmaf(s.zt_hi, o, s.zc_hi) + s.zc_lo);
+  }
   return fmaf(s.zb, s.dy0 + 2.0f * i, s.Z0);
 }
 
@@ -160,8 +178,9 @@ __device__ __forceinline__ float mode_factor(int mode, float z) {
   return mode == kModeSign ? sign32(z) : erf32(z);
 }
 
+// packed fast paths: mode 0 or 2 and no clamp (steep or not)
 __device__ __forceinline__ bool fast_flags(uint32_t flags) {
-  return (flags & (kFlagSteep | kFlagClamp)) == 0 && (flags & 3u) != (uint32_t)kModeSign;
+  return (flags & kFlagClamp) == 0 && (flags & 3u) != (uint32_t)kModeSign;
 }
 
 // ---------------------------------------------------------------------------
@@ -191,18 +210,19 @@ __device__ __forceinline__ void fwd_commit(float nw, float& T, float& ar, float&
   T = commit ? tn : -fabsf(T);
 }
 
-// FAST: mode 0 or 2, FP32 erf argument, weight provably below the 0.99 clamp.
-__device__ __forceinline__ void fwd_splat_fast(const float4 (&q)[4], float px, float py0,
-                                               FwdPix& P) {
-  const SteepRec none{};
-  const SplatLane s = splat_lane<false>(q, none, px, py0);
+// FAST: mode 0 or 2, weight provably below the 0.99 clamp; STEEP takes z from
+// the side-record form.
+template <bool STEEP>
+__device__ __forceinline__ void fwd_splat_fast(const float4 (&q)[4], const SteepRec& side,
+                                               float px, float py0, FwdPix& P) {
+  const SplatLane s = splat_lane<STEEP>(q, side, px, py0);
   const float nc1 = -q[1].w, nc2 = -q[2].x;
   const float cr = q[2].y, cg = q[2].z, cb = q[2].w, z = q[3].x;
 #pragma unroll
   for (int p = 0; p < kPairs; ++p) {
     const float2 dy = pair_dy(s.dy0, p);
     const float2 g = ex2x2(ffma2(ffma2(f2(s.C), dy, f2(s.Bx)), dy, f2(s.P0)));
-    const float2 e = erf32x2(ffma2(f2(s.zb), dy, f2(s.Z0)));
+    const float2 e = erf32x2(STEEP ? steep_z2(s, p) : ffma2(f2(s.zb), dy, f2(s.Z0)));
     const float2 nw = fmul2(ffma2(f2(nc2), e, f2(nc1)), g);  // -w
     const float2 tn = ffma2(nw, P.T[p], P.T[p]);              // T * (1 - w)
     const float2 nwT = fmul2(nw, P.T[p]);
@@ -292,9 +312,12 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) blend_fwd_kernel(
         if ((j & 7) == 0 && !(any = warp_any_alive(P))) break;
         const float4 q[4] = {st.rec[s][j][0], st.rec[s][j][1], st.rec[s][j][2], st.rec[s][j][3]};
         const uint32_t flags = __float_as_uint(q[3].y);
-        if (fast_flags(flags))
-          fwd_splat_fast(q, px, py0, P);
-        else
+        if (fast_flags(flags)) {
+          if (flags & kFlagSteep)
+            fwd_splat_fast<true>(q, st.side[s][j], px, py0, P);
+          else
+            fwd_splat_fast<false>(q, st.side[s][j], px, py0, P);
+        } else
           fwd_splat_generic(q, st.side[s][j], flags, px, py0, P);
       }
       __syncwarp();
@@ -337,11 +360,11 @@ struct BwdPix {
 // of the warp is active at this position (pos < warp-min of the terminal
 // counts); otherwise inactive pixels are masked with selects and contribute
 // exact zeros (pixels terminated early, as in heavily occluded views).
-template <bool ALL>
-__device__ __forceinline__ void bwd_splat_fast(const float4 (&q)[4], int pos, float px,
-                                               float py0, BwdPix& P, BwdAcc& out) {
-  const SteepRec none{};
-  const SplatLane s = splat_lane<false>(q, none, px, py0);
+template <bool ALL, bool STEEP>
+__device__ __forceinline__ void bwd_splat_fast(const float4 (&q)[4], const SteepRec& side,
+                                               int pos, float px, float py0, BwdPix& P,
+                                               BwdAcc& out) {
+  const SplatLane s = splat_lane<STEEP>(q, side, px, py0);
   const float c1 = q[1].w, c2 = q[2].x;
   const float cr = q[2].y, cg = q[2].z, cb = q[2].w;
   float2 s0 = f2(0.f), s1 = f2(0.f), s2 = f2(0.f), q0 = f2(0.f), q1 = f2(0.f), qz = f2(0.f);
@@ -350,7 +373,7 @@ __device__ __forceinline__ void bwd_splat_fast(const float4 (&q)[4], int pos, fl
   for (int p = 0; p < kPairs; ++p) {
     const float2 dy = pair_dy(s.dy0, p);
     const float2 gg = ex2x2(ffma2(ffma2(f2(s.C), dy, f2(s.Bx)), dy, f2(s.P0)));
-    const float2 zz = ffma2(f2(s.zb), dy, f2(s.Z0));
+    const float2 zz = STEEP ? steep_z2(s, p) : ffma2(f2(s.zb), dy, f2(s.Z0));
     const float2 e = erf32x2(zz);
     const float2 u = ffma2(f2(c2), e, f2(c1));
     const float2 w = fmul2(u, gg);
@@ -558,10 +581,18 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) blend_bwd_kernel(
         const int mode = (int)(flags & 3u);
         BwdAcc a;
         if (fast_flags(flags)) {
-          if (pos < minc)
-            bwd_splat_fast<true>(q, pos, px, py0, P, a);
-          else
-            bwd_splat_fast<false>(q, pos, px, py0, P, a);
+          const bool steep = flags & kFlagSteep;
+          if (pos < minc) {
+            if (steep)
+              bwd_splat_fast<true, true>(q, side, pos, px, py0, P, a);
+            else
+              bwd_splat_fast<true, false>(q, side, pos, px, py0, P, a);
+          } else {
+            if (steep)
+              bwd_splat_fast<false, true>(q, side, pos, px, py0, P, a);
+            else
+              bwd_splat_fast<false, false>(q, side, pos, px, py0, P, a);
+          }
         } else {
           bwd_splat_generic(q, side, flags, pos, px, py0, P, a);
         }
@@ -628,7 +659,7 @@ __global__ void pack_records_kernel(const double* __restrict__ packed,
   r[R_FLAGS] = __uint_as_float(pack_flags(md, steep, may_clamp(p[7], p[8]), 0));
   r[R_ROW_ORIGIN] = __int_as_float(0);
   r[R_MU_LO] = __uint_as_float(*reinterpret_cast<const uint32_t*>(&lo));
-  if (steep) side[l] = SteepRec{p[0], p[1], p[5], p[6]};
+  if (steep) side[l] = make_steep(p[0], p[1], p[5], p[6]);
   steep_flag[l] = steep ? 1 : 0;
 }
 

@@ -40,9 +40,31 @@ constexpr int kRecordFloats = 16;
 // radius + 24 px bounds |dx|,|dy| inside any covered tile, so non-steep splats
 // keep |z| rounding error below ~6e-8 * 256 = 1.5e-5 (a weight error below
 // 0.56 * 1.5e-5 = 9e-6).  About 10% of the c3 pairs are steep.
+//
+// The side record holds the erf argument in a cancellation-free form.  With K
+// the larger of |za|, |zb| and r = (smaller / larger) coefficient:
+//   y-form (|zb| >= |za|):  z = zb * ((py - muy) + r (px - mux))
+//   x-form (|za| >  |zb|):  z = za * ((px - mux) + r (py - muy))
+// A lane evaluates the bracket at its column and first row in FP64, splits it
+// into float hi + lo, and steps down its rows in FP32 with one FMA per pixel
+// (exact product + single rounding), so z keeps ~1e-7 relative accuracy on the
+// packed FP32 path (steep_setup / steep_z in hs_blend.cu).
 struct __align__(16) SteepRec {
-  double mux, muy, za, zb;
+  double mux, muy;
+  double r;        // smaller / larger erf coefficient, |r| <= 1
+  float K;         // the larger coefficient (zb in the y-form, za in the x-form)
+  uint32_t xform;  // 1: x-form
 };
+__host__ __device__ __forceinline__ SteepRec make_steep(double mux, double muy, double za,
+                                                        double zb) {
+  SteepRec s;
+  s.mux = mux;
+  s.muy = muy;
+  s.xform = fabs(za) > fabs(zb) ? 1u : 0u;
+  s.r = s.xform ? zb / za : za / zb;
+  s.K = (float)(s.xform ? za : zb);
+  return s;
+}
 constexpr double kSteepLimit = 256.0;
 constexpr uint32_t kSteepBit = 0x80000000u;
 constexpr uint32_t kIndexMask = 0x7fffffffu;

@@ -389,7 +389,7 @@ __global__ void __launch_bounds__(NT) preprocess_fwd_kernel(
   if (radii) radii[i] = (int32_t)ceil(st.radius);
   const bool steep = st.mode != kModePlain && is_steep(st.za, st.zb, st.radius + 24.0);
   dval[i] = (uint32_t)i | (steep ? kSteepBit : 0u);
-  if (steep) side[i] = SteepRec{st.mux, st.muy, st.za, st.zb};
+  if (steep) side[i] = make_steep(st.mux, st.muy, st.za, st.zb);
   const float mux = (float)st.mux, muy = (float)st.muy;
   const __half2 lo = __floats2half2_rn((float)(st.mux - (double)mux), (float)(st.muy - (double)muy));
   float4 r0 = make_float4(mux, muy, (float)(st.c / st.det), (float)(-st.b / st.det));
