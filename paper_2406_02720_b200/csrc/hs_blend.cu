@@ -367,13 +367,20 @@ __device__ __forceinline__ void bwd_splat_fast(const float4 (&q)[4], const Steep
   const SplatLane s = splat_lane<STEEP>(q, side, px, py0);
   const float c1 = q[1].w, c2 = q[2].x;
   const float cr = q[2].y, cg = q[2].z, cb = q[2].w;
+  // Row-offset basis: pixel dy = dy0 + o with o = 2i the offset from row 0, so the
+  // exponent is (C o + Lg) o + Kg, z = zb o + Zc, and the dy-moments are kept as
+  // o-moments and shifted by dy0 once per splat (no per-pixel dy).
+  const float Lg = fmaf(2.0f * s.C, s.dy0, s.Bx);
+  const float Kg = fmaf(fmaf(s.C, s.dy0, s.Bx), s.dy0, s.P0);
+  const float Zc = fmaf(s.zb, s.dy0, s.Z0);
   float2 s0 = f2(0.f), s1 = f2(0.f), s2 = f2(0.f), q0 = f2(0.f), q1 = f2(0.f), qz = f2(0.f);
   float2 a1 = f2(0.f), a2 = f2(0.f), ar = f2(0.f), ag = f2(0.f), ab = f2(0.f);
 #pragma unroll
   for (int p = 0; p < kPairs; ++p) {
-    const float2 dy = pair_dy(s.dy0, p);
-    const float2 gg = ex2x2(ffma2(ffma2(f2(s.C), dy, f2(s.Bx)), dy, f2(s.P0)));
-    const float2 zz = STEEP ? steep_z2(s, p) : ffma2(f2(s.zb), dy, f2(s.Z0));
+    const float2 o = make_float2(4.0f * p, 4.0f * p + 2.0f);
+    const float2 o2 = make_float2(16.0f * p * p, (4.0f * p + 2.0f) * (4.0f * p + 2.0f));
+    const float2 gg = ex2x2(ffma2(ffma2(f2(s.C), o, f2(Lg)), o, f2(Kg)));
+    const float2 zz = STEEP ? steep_z2(s, p) : ffma2(f2(s.zb), o, f2(Zc));
     const float2 e = erf32x2(zz);
     const float2 u = ffma2(f2(c2), e, f2(c1));
     const float2 w = fmul2(u, gg);
@@ -393,22 +400,27 @@ __device__ __forceinline__ void bwd_splat_fast(const float4 (&q)[4], const Steep
     const float2 dwg = fmul2(d_w, gg);
     const float2 d_pow = fmul2(dwg, u);
     s0 = fadd2(s0, d_pow);
-    s1 = ffma2(d_pow, dy, s1);
-    s2 = ffma2(fmul2(d_pow, dy), dy, s2);
+    s1 = ffma2(d_pow, o, s1);
+    s2 = ffma2(d_pow, o2, s2);
     a1 = fadd2(a1, dwg);
     a2 = ffma2(dwg, e, a2);
     // d_z / c2k (the constant factor is applied once per splat below)
     const float2 ez = ex2x2(fmul2(fmul2(zz, zz), f2(-kLog2e)));
     const float2 dz = fmul2(dwg, ez);
     q0 = fadd2(q0, dz);
-    q1 = ffma2(dz, dy, q1);
+    q1 = ffma2(dz, o, q1);
     qz = ffma2(dz, zz, qz);
     P.D[p] = ffma2(wt, dcr, P.D[p]);
     P.T[p] = ALL ? Tp : make_float2(ax ? Tp.x : P.T[p].x, ay ? Tp.y : P.T[p].y);
   }
   const float c2k = c2 * (2.0f * kInvSqrtPi);
-  out.s0 = s0.x + s0.y; out.s1 = s1.x + s1.y; out.s2 = s2.x + s2.y;
-  out.q0 = c2k * (q0.x + q0.y); out.q1 = c2k * (q1.x + q1.y); out.qz = c2k * (qz.x + qz.y);
+  const float S0 = s0.x + s0.y, S1 = s1.x + s1.y, S2 = s2.x + s2.y;
+  const float Q0 = q0.x + q0.y, Q1 = q1.x + q1.y;
+  // back to dy-moments: sum d (dy0 + o) = dy0 S0 + S1; sum d (dy0 + o)^2 = dy0 (dy0 S0 + 2 S1) + S2
+  out.s0 = S0;
+  out.s1 = fmaf(s.dy0, S0, S1);
+  out.s2 = fmaf(s.dy0, fmaf(s.dy0, S0, 2.0f * S1), S2);
+  out.q0 = c2k * Q0; out.q1 = c2k * fmaf(s.dy0, Q0, Q1); out.qz = c2k * (qz.x + qz.y);
   out.c1 = a1.x + a1.y; out.c2 = a2.x + a2.y;
   out.r = ar.x + ar.y; out.g = ag.x + ag.y; out.b = ab.x + ab.y;
 }
