@@ -48,7 +48,7 @@ HBM_PEAK_GBS = _hbm_peak()
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5"])
@@ -340,6 +340,40 @@ def main():
     barrier()
     fwd_ms = start.elapsed_time(end) / args.steps
 
+    # algorithmic work of the dominant kernels (SURVEY.md 8(d))
+    term = out.terminal.to(torch.int64)
+    starts = torch.as_tensor(out.frame.export()["tile_starts"], device="cuda")
+    lens = (starts[1:] - starts[:-1]).reshape(out.frame.tiles_y, out.frame.tiles_x)
+    lens_px = lens.repeat_interleave(16, 0).repeat_interleave(16, 1)[:cam.height, :cam.width]
+    fwd_evals = int(torch.minimum(term + 1, lens_px).sum().item())
+    bwd_evals = int(term.sum().item())
+    import ctypes
+    a, b = ctypes.c_double(0), ctypes.c_double(0)
+    _native.check(lib.hs_measure_fp32_peaks(ctypes.byref(a), ctypes.byref(b)), "peaks")
+    fp32_peak = a.value
+    bwd_ms = stage_ms.get("blend_bwd", float("nan"))
+    fwd_k_ms = stage_ms.get("blend_fwd", float("nan"))
+    achieved = bwd_evals * BWD_FLOPS_PER_EVAL / (bwd_ms * 1e-3) / 1e12
+    roofline = {
+        "bound": "fp32", "kernel": "blend_bwd (K6)", "achieved": achieved, "peak": fp32_peak,
+        "unit": "TFLOP/s", "frac": achieved / fp32_peak, "traffic": committed_traffic("blend_bwd"),
+        "peak_source": "measured on this GPU by hs_measure_fp32_peaks (FMA probe; "
+                       "MEASURED_PEAKS.json has no FP32 entry)",
+        "algorithmic": f"{bwd_evals} bwd evals x {BWD_FLOPS_PER_EVAL} flops per launch",
+        "kernel_ms": bwd_ms,
+        "share_of_step": bwd_ms / ms,
+        "blend_fwd": {"kernel_ms": fwd_k_ms, "evals": fwd_evals,
+                      "achieved_tflops": fwd_evals * FWD_FLOPS_PER_EVAL / (fwd_k_ms * 1e-3) / 1e12},
+        "stage_ms": stage_ms,
+        "ex2_gops_peak": b.value,
+        "fma2_tflops_peak": lib.hs_last_fma2_tflops(),
+    }
+
+    # end-to-end through the drop-in numpy API, host buffers, copies inside
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, sa, cam, dropin, world, barrier, torch, dist)
+
     # full training iteration on the device, the reference trainer's step (trainer.py:179-226):
     # render -> hs_loss (L1 + SSIM, cotangent) -> backward -> [all-reduce] -> hs_adam_step,
     # synthetic targets.  Runs last: Adam moves the scene.
@@ -399,40 +433,6 @@ def main():
     # Adam moves param, m, v (read+write) and reads grad: 28 B per float32 element
     adam_bytes = sum(getattr(scene, f).numel() for f in scene.FIELDS) * 7 * scene.mu.element_size()
 
-    # algorithmic work of the dominant kernels (SURVEY.md 8(d))
-    term = out.terminal.to(torch.int64)
-    starts = torch.as_tensor(out.frame.export()["tile_starts"], device="cuda")
-    lens = (starts[1:] - starts[:-1]).reshape(out.frame.tiles_y, out.frame.tiles_x)
-    lens_px = lens.repeat_interleave(16, 0).repeat_interleave(16, 1)[:cam.height, :cam.width]
-    fwd_evals = int(torch.minimum(term + 1, lens_px).sum().item())
-    bwd_evals = int(term.sum().item())
-    import ctypes
-    a, b = ctypes.c_double(0), ctypes.c_double(0)
-    _native.check(lib.hs_measure_fp32_peaks(ctypes.byref(a), ctypes.byref(b)), "peaks")
-    fp32_peak = a.value
-    bwd_ms = stage_ms.get("blend_bwd", float("nan"))
-    fwd_k_ms = stage_ms.get("blend_fwd", float("nan"))
-    achieved = bwd_evals * BWD_FLOPS_PER_EVAL / (bwd_ms * 1e-3) / 1e12
-    roofline = {
-        "bound": "fp32", "kernel": "blend_bwd (K6)", "achieved": achieved, "peak": fp32_peak,
-        "unit": "TFLOP/s", "frac": achieved / fp32_peak, "traffic": committed_traffic("blend_bwd"),
-        "peak_source": "measured on this GPU by hs_measure_fp32_peaks (FMA probe; "
-                       "MEASURED_PEAKS.json has no FP32 entry)",
-        "algorithmic": f"{bwd_evals} bwd evals x {BWD_FLOPS_PER_EVAL} flops per launch",
-        "kernel_ms": bwd_ms,
-        "share_of_step": bwd_ms / ms,
-        "blend_fwd": {"kernel_ms": fwd_k_ms, "evals": fwd_evals,
-                      "achieved_tflops": fwd_evals * FWD_FLOPS_PER_EVAL / (fwd_k_ms * 1e-3) / 1e12},
-        "stage_ms": stage_ms,
-        "ex2_gops_peak": b.value,
-        "fma2_tflops_peak": lib.hs_last_fma2_tflops(),
-    }
-
-    # end-to-end through the drop-in numpy API, host buffers, copies inside
-    e2e = None
-    if not args.no_e2e:
-        e2e = run_e2e(args, sa, cam, dropin, world, barrier, torch, dist)
-
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args.config)
@@ -487,8 +487,11 @@ def run_e2e(args, sa, cam, dropin, world, barrier, torch, dist):
         g = dropin.render_backward(hs, cam, out, d_color)
         return out, g
 
-    for _ in range(2):
-        step()
+    # warm up exactly as the timed loop runs (the previous step's outputs stay alive while
+    # the next runs), so pinned staging buffers and workspaces reach steady state first
+    out = g = None
+    for _ in range(3):
+        out, g = step()
     barrier()
     t0 = time.perf_counter()
     n = max(2, min(args.steps, 5))
