@@ -202,14 +202,15 @@ size_t hs_loss_workspace_size(int32_t height, int32_t width, int32_t channels);
 /* compute_loss (loss.py:88-106): (1 - lambda) L1 + lambda (1 - SSIM) of
  * `rendered` against `target`, both device float32 (H,W,C) C-contiguous, and
  * its exact gradient w.r.t. `rendered` (ssim_with_grad, loss.py:48-79).
- * loss3 (device, 3 doubles) receives [loss, L1, mean SSIM]; the gradient goes
+ * loss4 (device, 4 doubles) receives [loss, L1, mean SSIM, MSE] (the MSE is
+ * metrics.psnr's, metrics.py:13-22); the gradient goes
  * to d_rendered (float32, the cotangent hs_blend_bwd takes) and/or
  * d_rendered_f64 (float64); either may be NULL.  FP64 arithmetic.  lambda 0
  * skips SSIM as the reference does (and then accepts images under 11 px).
  * Errors: HS_ERR_INVALID_LAMBDA outside [0, 1]; HS_ERR_IMAGE_TOO_SMALL when
  * lambda > 0 and min(H, W) < 11; HS_ERR_WORKSPACE.  Asynchronous on `stream`. */
 int hs_loss(const float* rendered, const float* target, int32_t height, int32_t width,
-            int32_t channels, double lambda_ssim, double* loss3, float* d_rendered,
+            int32_t channels, double lambda_ssim, double* loss4, float* d_rendered,
             double* d_rendered_f64, void* ws, size_t ws_bytes, void* stream);
 
 /* ---- optimizer: per-group Adam, the step after K7 ----------------------- */
@@ -308,6 +309,13 @@ int hs_densify_apply(const hs_scene* scene, const hs_densify_stats* stats,
  * cap = logit(ceiling); zeroes the opacity groups' moments and steps when
  * `state` is given.  Writes the scene's opacity arrays. */
 int hs_reset_opacity(const hs_scene* scene, double cap, hs_adam_state* state, void* stream);
+
+/* opacity_disparity (trainer.py:353-358): the SUM of |sigmoid(a) - sigmoid(b)|
+ * over the scene into *out_sum (device double; divide by n for the mean).
+ * Deterministic; EmptyScene for n == 0. */
+size_t hs_opacity_disparity_workspace_size(int64_t n);
+int hs_opacity_disparity(const hs_scene* scene, double* out_sum, void* ws, size_t ws_bytes,
+                         void* stream);
 
 /* ---- scene I/O: PLY payload <-> device scene (scene_io.py:136-269) ----- */
 

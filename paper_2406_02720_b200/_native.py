@@ -152,6 +152,9 @@ _SIGNATURES = {
                                 c_void_p]),
     "hs_ply_row_bytes": (c_int32, [c_int32, c_int32]),
     "hs_ply_pack": (c_int32, [ctypes.POINTER(HsScene), c_void_p, c_int32, c_void_p]),
+    "hs_opacity_disparity_workspace_size": (c_size_t, [c_int64]),
+    "hs_opacity_disparity": (c_int32, [ctypes.POINTER(HsScene), c_void_p, c_void_p, c_size_t,
+                                       c_void_p]),
     "hs_status_string": (ctypes.c_char_p, [c_int32]),
     "hs_last_cuda_error": (ctypes.c_char_p, []),
     "hs_kernel_launch_count": (c_int64, []),

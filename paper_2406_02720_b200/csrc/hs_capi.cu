@@ -633,7 +633,7 @@ LossBufs carve_loss(void* ws, int32_t height, int32_t width, int32_t channels, s
   b.adj_m = c.take<double>(n);
   b.adj_s1 = c.take<double>(n);
   b.adj_s12 = c.take<double>(n);
-  b.partial = c.take<double>(2 * (size_t)hs::loss_partials(width, height, channels));
+  b.partial = c.take<double>(3 * (size_t)hs::loss_partials(width, height, channels));
   *bytes = c.off;
   return b;
 }
@@ -647,9 +647,9 @@ extern "C" size_t hs_loss_workspace_size(int32_t height, int32_t width, int32_t 
 }
 
 extern "C" int hs_loss(const float* rendered, const float* target, int32_t height, int32_t width,
-                       int32_t channels, double lambda_ssim, double* loss3, float* d_rendered,
+                       int32_t channels, double lambda_ssim, double* loss4, float* d_rendered,
                        double* d_rendered_f64, void* ws, size_t ws_bytes, void* stream_) {
-  if (!rendered || !target || !loss3 || height <= 0 || width <= 0 || channels <= 0)
+  if (!rendered || !target || !loss4 || height <= 0 || width <= 0 || channels <= 0)
     return HS_ERR_INVALID_ARG;
   if (!(lambda_ssim >= 0.0 && lambda_ssim <= 1.0)) return HS_ERR_INVALID_LAMBDA;
   const bool ssim = lambda_ssim != 0.0;  // loss.py:97-103: lambda 0 skips SSIM
@@ -672,7 +672,7 @@ extern "C" int hs_loss(const float* rendered, const float* target, int32_t heigh
   a.adj_s12 = b.adj_s12;
   a.partial = b.partial;
   a.n_partials = (int)hs::loss_partials(width, height, channels);
-  a.loss = loss3;
+  a.loss = loss4;
   a.d_f32 = d_rendered;
   a.d_f64 = d_rendered_f64;
   a.ssim = ssim;
@@ -992,5 +992,27 @@ extern "C" int hs_ply_pack(const hs_scene* scene, void* payload, int32_t kind, v
                            scene->normal, scene->raw_opacity_a, scene->raw_opacity_b};
   HS_CUDA(hs::launch_ply_pack(a, fields, scene->dtype == HS_DTYPE_F64 ? 1 : 0,
                               static_cast<cudaStream_t>(stream_)));
+  return HS_OK;
+}
+
+extern "C" size_t hs_opacity_disparity_workspace_size(int64_t n) {
+  if (n <= 0 || n >= ((int64_t)1 << 31)) return 0;
+  size_t bytes = 0;
+  hs::opacity_disparity_sum(nullptr, nullptr, n, 0, nullptr, nullptr, &bytes, 0);
+  size_t b64 = 0;
+  hs::opacity_disparity_sum(nullptr, nullptr, n, 1, nullptr, nullptr, &b64, 0);
+  return bytes > b64 ? bytes : b64;
+}
+
+extern "C" int hs_opacity_disparity(const hs_scene* scene, double* out_sum, void* ws,
+                                    size_t ws_bytes, void* stream_) {
+  if (!scene || !out_sum) return HS_ERR_INVALID_ARG;
+  if (scene->n <= 0) return HS_ERR_EMPTY_SCENE;
+  if (scene->n >= ((int64_t)1 << 31)) return HS_ERR_INVALID_ARG;
+  if (!ws || ws_bytes < hs_opacity_disparity_workspace_size(scene->n)) return HS_ERR_WORKSPACE;
+  size_t bytes = ws_bytes;
+  HS_CUDA(hs::opacity_disparity_sum(scene->raw_opacity_a, scene->raw_opacity_b, scene->n,
+                                    scene->dtype == HS_DTYPE_F64 ? 1 : 0, out_sum, ws, &bytes,
+                                    static_cast<cudaStream_t>(stream_)));
   return HS_OK;
 }

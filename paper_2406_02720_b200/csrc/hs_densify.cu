@@ -263,3 +263,32 @@ cudaError_t launch_reset_opacity(void* ra, void* rb, void* ma, void* va, void* m
 }
 
 }  // namespace hs
+
+namespace hs {
+// opacity_disparity (trainer.py:353-358): mean |sigmoid(a) - sigmoid(b)|, one CUB
+// reduction over a transform iterator (deterministic for a given size).
+template <typename T>
+struct AlphaGap {
+  const T* ra;
+  const T* rb;
+  __device__ double operator()(int64_t i) const {
+    return fabs(sigmoid_ref((double)ra[i]) - sigmoid_ref((double)rb[i]));
+  }
+};
+
+template <typename T>
+static cudaError_t disparity_t(const void* ra, const void* rb, int64_t n, double* out, void* temp,
+                               size_t* temp_bytes, cudaStream_t s) {
+  auto it = cub::TransformInputIterator<double, AlphaGap<T>, cub::CountingInputIterator<int64_t>>(
+      cub::CountingInputIterator<int64_t>(0), AlphaGap<T>{(const T*)ra, (const T*)rb});
+  return cub::DeviceReduce::Sum(temp, *temp_bytes, it, out, (int)n, s);
+}
+
+cudaError_t opacity_disparity_sum(const void* ra, const void* rb, int64_t n, int dtype,
+                                  double* out, void* temp, size_t* temp_bytes, cudaStream_t s) {
+  cudaError_t e = dtype == 0 ? disparity_t<float>(ra, rb, n, out, temp, temp_bytes, s)
+                             : disparity_t<double>(ra, rb, n, out, temp, temp_bytes, s);
+  if (temp) note_launch();
+  return e;
+}
+}  // namespace hs

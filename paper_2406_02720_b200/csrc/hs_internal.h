@@ -127,9 +127,9 @@ struct LossArgs {
   double* adj_m;   // ssim_with_grad adjoint maps, (C,H,W) float64 each
   double* adj_s1;
   double* adj_s12;
-  double* partial;  // 2 per CTA: sum |x-y|, sum SSIM map
+  double* partial;  // 3 per CTA: sum |x-y|, sum SSIM map, sum (x-y)^2
   int n_partials;
-  double* loss;     // [loss, l1, mean ssim]
+  double* loss;     // [loss, l1, mean ssim, mse]
   float* d_f32;     // d loss / d rendered (nullable)
   double* d_f64;    // same in float64 (nullable)
   int ssim;         // lambda > 0
@@ -207,6 +207,8 @@ cudaError_t launch_densify_classify(const DensifyStatsArgs& st, const void* log_
                                     const DensifyParams& p, DensifyBufs& b, cudaStream_t s);
 template <typename T>
 cudaError_t launch_densify_emit_t(const DensifyEmitArgs<T>& a, cudaStream_t s);
+cudaError_t opacity_disparity_sum(const void* ra, const void* rb, int64_t n, int dtype,
+                                  double* out, void* temp, size_t* temp_bytes, cudaStream_t s);
 cudaError_t launch_reset_opacity(void* ra, void* rb, void* ma, void* va, void* mb, void* vb,
                                  int64_t n, double cap, int dtype, cudaStream_t s);
 

@@ -16,7 +16,7 @@
 //   L2 (loss_grad_kernel): filter the adjoint maps the same way (the window is
 //      symmetric, so the blur is self-adjoint), combine with the pixel values
 //      and the L1 term into d_color; CTA 0 also reduces the partials into the
-//      loss in a fixed order, so the result is deterministic.
+//      loss (and the MSE of metrics.psnr) in a fixed order: deterministic.
 // Arithmetic is FP64 on the FP32 images (their squares and products are exact
 // in FP64); the window taps are summed in scipy's symmetric order, centre
 // first, then the outer pairs inwards, with FMA contraction and one division
@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(kLossThreads, 3) loss_stats_kernel(LossArgs a)
   constexpr int rowf = kLHX * cg;  // floats per staged halo row
   float* xs = halo;
   float* ys = halo + kLHY * rowf;
-  double l1 = 0.0, ssum = 0.0;
+  double l1 = 0.0, ssum = 0.0, sq = 0.0;
   if (SSIM) {
     // the halo rows of all cg channels: contiguous runs of the HWC images
     for (int e = tid; e < kLHY * rowf; e += kLossThreads) {
@@ -177,6 +177,7 @@ __global__ void __launch_bounds__(kLossThreads, 3) loss_stats_kernel(LossArgs a)
         y = a.y[k];
       }
       l1 += fabs(x - y);
+      sq += (x - y) * (x - y);  // metrics.psnr's MSE (metrics.py:13-22)
       if (!SSIM) continue;
       const int64_t kp = ((int64_t)c * H + gy) * W + gx;  // planar adjoint maps
       // ssim_with_grad, loss.py:60-73 (one division: 1/b1 and 1/b2 from 1/(b1 b2))
@@ -197,10 +198,12 @@ __global__ void __launch_bounds__(kLossThreads, 3) loss_stats_kernel(LossArgs a)
   }
   l1 = block_sum(l1, red);
   ssum = block_sum(ssum, red);
+  sq = block_sum(sq, red);
   if (tid == 0) {
     const int cta = (group * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
-    a.partial[2 * cta] = l1;
-    a.partial[2 * cta + 1] = ssum;
+    a.partial[3 * cta] = l1;
+    a.partial[3 * cta + 1] = ssum;
+    a.partial[3 * cta + 2] = sq;
   }
 }
 
@@ -215,17 +218,20 @@ __global__ void __launch_bounds__(kLossThreads) loss_grad_kernel(LossArgs a) {
   const int cg = (int)(C - c0 < kMaxCG ? C - c0 : kMaxCG);
   if (cta_linear() == 0) {
     // loss.py:95 and 102: fixed-order reduction of the L1 partials
-    double l1 = 0.0, ss = 0.0;
+    double l1 = 0.0, ss = 0.0, sq = 0.0;
     for (int i = tid; i < a.n_partials; i += kLossThreads) {
-      l1 += a.partial[2 * i];
-      ss += a.partial[2 * i + 1];
+      l1 += a.partial[3 * i];
+      ss += a.partial[3 * i + 1];
+      sq += a.partial[3 * i + 2];
     }
     l1 = block_sum(l1, red) / a.n;
     ss = block_sum(ss, red) / a.n;
+    sq = block_sum(sq, red) / a.n;
     if (tid == 0) {
       a.loss[0] = SSIM ? (1.0 - a.lambda) * l1 + a.lambda * (1.0 - ss) : l1;
       a.loss[1] = l1;
       a.loss[2] = SSIM ? ss : 0.0;
+      a.loss[3] = sq;
     }
   }
   const double w_l1 = 1.0 - a.lambda;

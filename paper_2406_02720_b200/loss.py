@@ -37,8 +37,8 @@ class DeviceLoss:
     """compute_loss on device tensors with a persistent workspace.
 
     `__call__(rendered, target)` takes (H,W,C) or (H,W) float32 CUDA tensors and
-    returns `(stats, d_rendered)`: stats is a (3,) float64 device tensor
-    [loss, L1, mean SSIM] and d_rendered the float32 gradient, shaped like
+    returns `(stats, d_rendered)`: stats is a (4,) float64 device tensor
+    [loss, L1, mean SSIM, MSE] and d_rendered the float32 gradient, shaped like
     `rendered`.  Nothing is copied to the host.
     """
 
@@ -68,7 +68,7 @@ class DeviceLoss:
         h, w = x.shape[0], x.shape[1]
         c = x.shape[2] if x.dim() == 3 else 1
         if stats is None:
-            stats = torch.empty(3, dtype=torch.float64, device=x.device)
+            stats = torch.empty(4, dtype=torch.float64, device=x.device)
         if d_out is None and d_out_f64 is None:
             d_out = torch.empty_like(x)
         ws = self._workspace(h, w, c, x.device)

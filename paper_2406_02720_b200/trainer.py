@@ -313,15 +313,34 @@ def reset_opacity(scene, opt_state=None, ceiling=0.01):
         opt_state.t["opacity_b"] = 0
 
 
-class Trainer:
+def opacity_disparity(scene):
+    """Mean |alpha1 - alpha2| over the scene (trainer.py:353-358), one device reduction."""
+    from .errors import EmptyScene
+    n = len(scene)
+    if n == 0:
+        raise EmptyScene("opacity_disparity of an empty scene")
+    lib = _native.load()
+    ws = torch.empty(max(lib.hs_opacity_disparity_workspace_size(n), 1), dtype=torch.uint8,
+                     device=scene.device)
+    out = torch.empty(1, dtype=torch.float64, device=scene.device)
+    sc = device.scene_struct(scene)
+    _native.check(lib.hs_opacity_disparity(ctypes.byref(sc), ctypes.c_void_p(out.data_ptr()),
+                                           ctypes.c_void_p(ws.data_ptr()), ws.numel(),
+                                           device._stream()), "hs_opacity_disparity")
+    return float(out.item()) / n
+
+
+class StepRunner:
     """Persistent buffers for repeated steps: one rasterizer workspace, one
-    gradient set, one loss workspace (no allocation per step)."""
+    gradient set (re-allocated when density control changes N), one loss
+    workspace."""
 
     def __init__(self, scene, config):
         self.config = config
         self.rast = device.Rasterizer(scene.device, slots=1, kernel=config.kernel)
         self.grads = device.DeviceGradientSet.empty_flat(scene)
         self.loss = DeviceLoss(config.lambda_ssim)
+        self.last_stats = None  # [loss, L1, SSIM, MSE] of the last step (device)
 
     def step(self, scene, batch_view, opt_state, iteration, spatial_scale=1.0,
              check_finite=True):
@@ -329,8 +348,11 @@ class Trainer:
         if not isinstance(target, torch.Tensor):
             target = torch.as_tensor(np.asarray(target, dtype=np.float32))
         target = target.to(device=scene.device, dtype=torch.float32)
+        if self.grads.d_mu.shape[0] != len(scene):
+            self.grads = device.DeviceGradientSet.empty_flat(scene)
         out = self.rast.render(scene, cam)
         stats, d_color = self.loss(out.color, target)
+        self.last_stats = stats
         loss = stats[0]
         if check_finite:
             loss = float(loss)  # trainer.py:189-190 (one 8-byte read)
@@ -345,9 +367,105 @@ def step(scene, batch_view, config, opt_state, iteration, spatial_scale=1.0, thr
     """One optimisation step on a (camera, target image) pair (trainer.py:179-226).
 
     Returns (loss, grads, out) like the reference; grads/out are device objects.
-    `threads` is accepted and ignored.  Repeated callers should hold a Trainer."""
-    trainer = getattr(opt_state, "_trainer", None)
-    if trainer is None or trainer.config is not config:
-        trainer = Trainer(scene, config)
-        opt_state._trainer = trainer
-    return trainer.step(scene, batch_view, opt_state, iteration, spatial_scale)
+    `threads` is accepted and ignored.  Repeated callers should hold a StepRunner."""
+    runner = getattr(opt_state, "_runner", None)
+    if runner is None or runner.config is not config:
+        runner = StepRunner(scene, config)
+        opt_state._runner = runner
+    return runner.step(scene, batch_view, opt_state, iteration, spatial_scale)
+
+
+METRICS_FIELDS = ("iteration", "loss", "psnr", "num_primitives",
+                  "opacity_disparity", "cloned", "split", "pruned",
+                  "opacity_reset")
+
+
+class Trainer:
+    """Drives the full schedule over a fixed set of training views (trainer.py:365-449),
+    every tensor on the GPU.
+
+    Same constructor, `run`, `write_metrics` and `metrics_rows` as the reference.
+    The view order and the split offsets come from one numpy Generator seeded with
+    config.seed, consumed in the reference's order, so a run makes the same
+    density-control decisions as the reference would on the same gradients.
+    Targets are uploaded once."""
+
+    def __init__(self, scene, views, config, metrics_path=None, checkpoint_fn=None):
+        from .geometry import Scene
+        self.scene = Scene.from_any(scene)
+        self.views = list(views)  # (name, CameraModel, target image)
+        if not self.views:
+            raise ValueError("need at least one training view")
+        self.config = config
+        self.rng = np.random.default_rng(config.seed)
+        self.opt = AdamState(self.scene)
+        self.stats = DensifyStats.zeros(len(self.scene), self.scene.device)
+        self.spatial_scale = camera_extent([v[1] for v in self.views])
+        self.metrics_path = metrics_path
+        self.checkpoint_fn = checkpoint_fn
+        self._metrics_rows = []
+        self._order = []
+        self._targets = [torch.as_tensor(np.asarray(t, dtype=np.float32)).to(self.scene.device)
+                         for _, _, t in self.views]
+        self._runner = StepRunner(self.scene, config)
+
+    def _next_view(self):
+        if not self._order:
+            self._order = list(self.rng.permutation(len(self.views)))
+        return self._order.pop()
+
+    def densify_enabled(self):
+        return self.config.mode in ("from_scratch", "finetune_all_with_densify")
+
+    def run(self, progress=None):
+        cfg = self.config
+        for iteration in range(1, cfg.total_iters + 1):
+            v = self._next_view()
+            _, cam, _ = self.views[v]
+            loss, grads, out = self._runner.step(
+                self.scene, (cam, self._targets[v]), self.opt, iteration, self.spatial_scale)
+            self.stats.update(grads)
+            report = {"cloned": 0, "split": 0, "pruned": 0}
+            did_reset = 0
+            if (self.densify_enabled() and iteration % cfg.densify_interval == 0
+                    and iteration < cfg.densify_until):
+                self.scene, self.stats, report = densify_and_prune(
+                    self.scene, self.stats, cfg, self.opt, self.rng, self.spatial_scale)
+            if (cfg.opacity_reset_start <= iteration <= cfg.opacity_reset_until
+                    and iteration % cfg.opacity_reset_interval == 0):
+                reset_opacity(self.scene, self.opt, cfg.opacity_reset_ceiling)
+                did_reset = 1
+            mse = float(self._runner.last_stats[3])
+            row = {
+                "iteration": iteration,
+                "loss": loss,
+                "psnr": math.inf if mse == 0.0 else float(10.0 * np.log10(1.0 / mse)),
+                "num_primitives": len(self.scene),
+                "opacity_disparity": opacity_disparity(self.scene),
+                "cloned": report["cloned"],
+                "split": report["split"],
+                "pruned": report["pruned"],
+                "opacity_reset": did_reset,
+            }
+            self._metrics_rows.append(row)
+            if progress and iteration % progress == 0:
+                print(f"iter {iteration:>6}  loss {loss:.5f}  prims {len(self.scene)}")
+            if (self.checkpoint_fn and cfg.checkpoint_interval
+                    and iteration % cfg.checkpoint_interval == 0):
+                self.checkpoint_fn(self.scene, iteration)
+        if self.metrics_path:
+            self.write_metrics(self.metrics_path)
+        if self.checkpoint_fn:
+            self.checkpoint_fn(self.scene, cfg.total_iters)
+        return self.scene
+
+    def write_metrics(self, path):
+        import csv
+        with open(path, "w", newline="") as fh:
+            writer = csv.DictWriter(fh, fieldnames=METRICS_FIELDS)
+            writer.writeheader()
+            writer.writerows(self._metrics_rows)
+
+    @property
+    def metrics_rows(self):
+        return self._metrics_rows

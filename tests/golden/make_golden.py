@@ -392,6 +392,53 @@ def io_fixture():
     print("io: native", d["native_ply"].size, "bytes; mixed", d["mixed_ply"].size, "bytes")
 
 
+def train_fixture():
+    """A short Trainer.run of the reference (trainer.py:365-449): 40 iterations
+    over 3 views of a small scene towards targets rendered from a perturbed copy,
+    densify every 10 iterations, opacity reset at 30; the metrics rows."""
+    from halfsplat import geometry, rasterizer
+    from halfsplat import trainer as T
+    sa = scenes.frustum(400, 1, 48, 40, seed=11)
+    sc = geometry.Scene(**{f: getattr(sa, f).astype(np.float64) for f in SCENE_FIELDS},
+                        sh_degree=sa.sh_degree, background_color=sa.background_color)
+    base = sa.cameras[0]
+    views = []
+    rng = np.random.default_rng(5)
+    tgt_scene = geometry.Scene(**{f: getattr(sa, f).astype(np.float64) for f in SCENE_FIELDS},
+                               sh_degree=sa.sh_degree, background_color=sa.background_color)
+    tgt_scene.sh_coeffs[:, 0, :] += 0.4
+    cams = []
+    for v in range(3):
+        w2c = np.array(base["world_to_cam"], dtype=np.float64)
+        w2c[0, 3] += 0.5 * (v - 1)
+        cam = geometry.CameraModel(world_to_cam=w2c, fx=base["fx"], fy=base["fy"], cx=base["cx"],
+                                   cy=base["cy"], width=base["width"], height=base["height"])
+        target = rasterizer.render(tgt_scene, cam).color.astype(np.float32).astype(np.float64)
+        views.append((f"v{v}", cam, target))
+        cams.append(dict(world_to_cam=w2c, target=target))
+    cfg = T.TrainConfig(total_iters=40, densify_until=35, densify_interval=10,
+                        opacity_reset_start=30, opacity_reset_interval=30,
+                        opacity_reset_until=35, densify_grad_threshold=2e-5, seed=3,
+                        prune_extent_factor=5.0, percent_dense=0.02)
+    # the initial scene (the run updates it in place until the first densify)
+    d = {"scene": np.concatenate([getattr(sc, f).reshape(len(sc), -1) for f in SCENE_FIELDS], 1),
+         "deg": np.int64(sa.sh_degree), "background": np.asarray(sa.background_color)}
+    tr = T.Trainer(sc, views, cfg)
+    tr.run()
+    for v, c in enumerate(cams):
+        d[f"w2c{v}"] = c["world_to_cam"]
+        d[f"target{v}"] = c["target"].astype(np.float32)
+    d["cam"] = np.array([base["fx"], base["fy"], base["cx"], base["cy"], base["width"],
+                         base["height"]], dtype=np.float64)
+    fields = T.METRICS_FIELDS
+    d["fields"] = np.array(fields)
+    d["rows"] = np.array([[float(r[f]) for f in fields] for r in tr.metrics_rows])
+    np.savez_compressed(os.path.join(HERE, "train.npz"), **d)
+    print("train: final prims", len(tr.scene), "rows", len(tr.metrics_rows))
+    for r in tr.metrics_rows[::5]:
+        print({k: (round(v, 5) if isinstance(v, float) else v) for k, v in r.items()})
+
+
 SCENE_FIELDS = ("mu", "log_scale", "rotation", "sh_coeffs", "normal", "raw_opacity_a",
                 "raw_opacity_b")
 
@@ -400,6 +447,7 @@ JOBS = {
     "adam": lambda t: adam_fixture(),
     "densify": lambda t: densify_fixture(),
     "io": lambda t: io_fixture(),
+    "train": lambda t: train_fixture(),
     "loss": lambda t: loss_fixture(),
     # small scenes, every array
     "c1": lambda t: full_fixture("c1", scenes.make_config("c1"), 0, True, t),
