@@ -184,30 +184,35 @@ __device__ __forceinline__ bool fast_flags(uint32_t flags) {
 }
 
 // ---------------------------------------------------------------------------
-// K5 forward.  Live pixels hold T > 0.  A pixel that terminates stores -T (its
-// final transmittance, sign flipped); from then on T*(1-w) <= 0 never passes the
-// termination test, so no separate alive mask is needed.  Pixels outside the
-// image start at T = -1.  The colour/depth accumulators hold the NEGATED sums
-// (T - w*T = fma(-w, T, T) needs -w; the sign is restored at the store).
-// Branch-free over the pixels (selects only); dead pixels compute and discard.
+// K5 forward.  Each pixel carries T and a 0/1 float "alive" mask A; a splat
+// commits with m = A * [T (1 - w) >= 1e-4], and every update is an exact
+// multiply by m: nw m is -w or 0, so T <- fma(nw m, T, T) is T (1 - w) or T
+// unchanged, the colour term is (nw m) T, the count adds m, and A <- m (a pixel
+// that fails the test is dead for good).  No selects or integer ops per pixel;
+// pixels outside the image start dead.  The colour/depth accumulators hold the
+// NEGATED sums (T - w T = fma(-w, T, T) needs -w; the sign is restored at the
+// store).  Dead pixels compute and discard.
 struct FwdPix {
-  float2 T[kPairs], ar[kPairs], ag[kPairs], ab[kPairs], ad[kPairs];
-  int cnt[kPx];
+  float2 T[kPairs], A[kPairs], C[kPairs], ar[kPairs], ag[kPairs], ab[kPairs], ad[kPairs];
 };
 
+__device__ __forceinline__ float ge_mask(float v) { return v >= kTerminationT ? 1.0f : 0.0f; }
+
 // one pixel: the termination rule and compositing of _blend_cy.pyx:162-176
-__device__ __forceinline__ void fwd_commit(float nw, float& T, float& ar, float& ag, float& ab,
-                                           float& ad, int& cnt, float cr, float cg, float cb,
-                                           float z) {
+__device__ __forceinline__ void fwd_commit(float nw, float& T, float& A, float& C, float& ar,
+                                           float& ag, float& ab, float& ad, float cr, float cg,
+                                           float cb, float z) {
   const float tn = fmaf(nw, T, T);  // T * (1 - w)
-  const bool commit = tn >= kTerminationT;
-  const float nwt = commit ? nw * T : 0.0f;
+  const float m = A * ge_mask(tn);
+  const float nwm = nw * m;
+  const float nwt = nwm * T;
   ar = fmaf(nwt, cr, ar);
   ag = fmaf(nwt, cg, ag);
   ab = fmaf(nwt, cb, ab);
   ad = fmaf(nwt, z, ad);
-  cnt += commit ? 1 : 0;
-  T = commit ? tn : -fabsf(T);
+  C += m;
+  A = m;
+  T = fmaf(nwm, T, T);
 }
 
 // FAST: mode 0 or 2, weight provably below the 0.99 clamp; STEEP takes z from
@@ -225,16 +230,16 @@ __device__ __forceinline__ void fwd_splat_fast(const float4 (&q)[4], const Steep
     const float2 e = erf32x2(STEEP ? steep_z2(s, p) : ffma2(f2(s.zb), dy, f2(s.Z0)));
     const float2 nw = fmul2(ffma2(f2(nc2), e, f2(nc1)), g);  // -w
     const float2 tn = ffma2(nw, P.T[p], P.T[p]);              // T * (1 - w)
-    const float2 nwT = fmul2(nw, P.T[p]);
-    const bool cx = tn.x >= kTerminationT, cy = tn.y >= kTerminationT;
-    const float2 nwt = make_float2(cx ? nwT.x : 0.0f, cy ? nwT.y : 0.0f);
+    const float2 m = fmul2(P.A[p], make_float2(ge_mask(tn.x), ge_mask(tn.y)));
+    const float2 nwm = fmul2(nw, m);
+    const float2 nwt = fmul2(nwm, P.T[p]);
     P.ar[p] = ffma2(nwt, f2(cr), P.ar[p]);
     P.ag[p] = ffma2(nwt, f2(cg), P.ag[p]);
     P.ab[p] = ffma2(nwt, f2(cb), P.ab[p]);
     P.ad[p] = ffma2(nwt, f2(z), P.ad[p]);
-    P.cnt[2 * p] += cx ? 1 : 0;
-    P.cnt[2 * p + 1] += cy ? 1 : 0;
-    P.T[p] = make_float2(cx ? tn.x : -fabsf(P.T[p].x), cy ? tn.y : -fabsf(P.T[p].y));
+    P.C[p] = fadd2(P.C[p], m);
+    P.A[p] = m;
+    P.T[p] = ffma2(nwm, P.T[p], P.T[p]);
   }
 }
 
@@ -255,15 +260,15 @@ __device__ __forceinline__ void fwd_splat_generic(const float4 (&q)[4], const St
     const float g = ex2_approx(fmaf(fmaf(s.C, dy, s.Bx), dy, s.P0));
     const float e = mode_factor(mode, erf_arg(s, steep, i));
     const float w = fminf(fmaf(c2, e, c1) * g, kWeightClamp);
-    fwd_commit(-w, slot(P.T[p], h), slot(P.ar[p], h), slot(P.ag[p], h), slot(P.ab[p], h),
-               slot(P.ad[p], h), P.cnt[i], cr, cg, cb, z);
+    fwd_commit(-w, slot(P.T[p], h), slot(P.A[p], h), slot(P.C[p], h), slot(P.ar[p], h),
+               slot(P.ag[p], h), slot(P.ab[p], h), slot(P.ad[p], h), cr, cg, cb, z);
   }
 }
 
 __device__ __forceinline__ bool warp_any_alive(const FwdPix& P) {
-  float m = fmaxf(P.T[0].x, P.T[0].y);
+  float m = fmaxf(P.A[0].x, P.A[0].y);
 #pragma unroll
-  for (int p = 1; p < kPairs; ++p) m = fmaxf(m, fmaxf(P.T[p].x, P.T[p].y));
+  for (int p = 1; p < kPairs; ++p) m = fmaxf(m, fmaxf(P.A[p].x, P.A[p].y));
   return __any_sync(0xffffffffu, m > 0.0f);
 }
 
@@ -286,10 +291,11 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) blend_fwd_kernel(
 #pragma unroll
     for (int i = 0; i < kPx; ++i) {
       const int p = i >> 1, h = i & 1;
-      slot(P.T[p], h) = (col < g.width && row0 + 2 * i < g.height) ? 1.f : -1.f;
+      slot(P.T[p], h) = 1.f;
+      slot(P.A[p], h) = (col < g.width && row0 + 2 * i < g.height) ? 1.f : 0.f;
+      slot(P.C[p], h) = 0.f;
       slot(P.ar[p], h) = 0.f; slot(P.ag[p], h) = 0.f; slot(P.ab[p], h) = 0.f;
       slot(P.ad[p], h) = 0.f;
-      P.cnt[i] = 0;
     }
     const int k0 = g.tile_starts[tile];
     const int nk = g.tile_starts[tile + 1] - k0;
@@ -330,14 +336,14 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) blend_fwd_kernel(
       const int row = row0 + 2 * i;
       if (col < g.width && row < g.height) {
         const size_t o = (size_t)row * g.width + col;
-        const float t = fabsf(slot(P.T[p], h));
+        const float t = slot(P.T[p], h);
         color[3 * o + 0] = fmaf(t, bg0, -slot(P.ar[p], h));
         color[3 * o + 1] = fmaf(t, bg1, -slot(P.ag[p], h));
         color[3 * o + 2] = fmaf(t, bg2, -slot(P.ab[p], h));
         alpha[o] = 1.0f - t;
         depth[o] = -slot(P.ad[p], h);
         trans[o] = t;
-        terminal[o] = P.cnt[i];
+        terminal[o] = (int32_t)slot(P.C[p], h);
       }
     }
   }
