@@ -359,7 +359,8 @@ struct BwdAcc {
 
 struct BwdPix {
   float2 T[kPairs], D[kPairs], dr[kPairs], dg[kPairs], db[kPairs];
-  int cnt[kPx];
+  const int* cnt;  // this lane's terminal counts, cnt[i * 32] (shared memory: keeps
+                   // 8 registers free on the ALL path, which never reads them)
 };
 
 // FAST: mode 0 or 2, FP32 z, no clamp.  Packed pixel pairs.  ALL: every pixel
@@ -393,7 +394,7 @@ __device__ __forceinline__ void bwd_splat_fast(const float4 (&q)[4], const Steep
     const float2 om = fadd2(f2(1.0f), neg2(w));
     const float2 inv = make_float2(rcp_approx(om.x), rcp_approx(om.y));  // 1 - w >= 0.01
     const float2 Tp = fmul2(P.T[p], inv);
-    const bool ax = ALL || pos < P.cnt[2 * p], ay = ALL || pos < P.cnt[2 * p + 1];
+    const bool ax = ALL || pos < P.cnt[(2 * p) * 32], ay = ALL || pos < P.cnt[(2 * p + 1) * 32];
     float2 wt = fmul2(w, Tp);
     if (!ALL) wt = make_float2(ax ? wt.x : 0.f, ay ? wt.y : 0.f);
     const float2 dcr = ffma2(P.dr[p], f2(cr), ffma2(P.dg[p], f2(cg), fmul2(P.db[p], f2(cb))));
@@ -451,7 +452,7 @@ __device__ __forceinline__ void bwd_splat_generic(const float4 (&q)[4], const St
     float& T = slot(P.T[p], h);
     float& D = slot(P.D[p], h);
     const float dr = slot(P.dr[p], h), dg = slot(P.dg[p], h), db = slot(P.db[p], h);
-    const bool active = pos < P.cnt[i];
+    const bool active = pos < P.cnt[i * 32];
     const float dy = s.dy0 + 2.0f * i;
     const float gg = ex2_approx(fmaf(fmaf(s.C, dy, s.Bx), dy, s.P0));
     const float zz = erf_arg(s, steep, i);
@@ -529,8 +530,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) blend_bwd_kernel(
   constexpr int kStride = kRowsBySortedPos ? 12 : kRowFloats;
   constexpr int kCols = kRowsBySortedPos ? 12 : 13;
   __shared__ WarpStage stage_all[kWarpsPerCta];
+  __shared__ int cnt_all[kWarpsPerCta][kPx][32];
   const int lane = threadIdx.x & 31;
   WarpStage& st = stage_all[threadIdx.x >> 5];
+  int* cnt = &cnt_all[threadIdx.x >> 5][0][lane];
   for (;;) {
     const int tile = next_tile(g, lane);
     if (tile < 0) break;
@@ -540,6 +543,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) blend_bwd_kernel(
     const float px = (float)col + 0.5f;
     const float py0 = (float)row0 + 0.5f;
     BwdPix P;
+    P.cnt = cnt;
     int maxc = 0, minc = 0x7fffffff;
 #pragma unroll
     for (int i = 0; i < kPx; ++i) {
@@ -550,18 +554,18 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) blend_bwd_kernel(
         const float t = trans[o];
         const float dr = d_color[3 * o + 0], dg = d_color[3 * o + 1], db = d_color[3 * o + 2];
         slot(P.T[p], h) = t;
-        P.cnt[i] = terminal[o];
+        cnt[i * 32] = terminal[o];
         slot(P.dr[p], h) = dr;
         slot(P.dg[p], h) = dg;
         slot(P.db[p], h) = db;
         // suffix S starts at T_final * background; only dC.S is needed
         slot(P.D[p], h) = t * fmaf(dr, bg0, fmaf(dg, bg1, db * bg2));
-        maxc = max(maxc, P.cnt[i]);
-        minc = min(minc, P.cnt[i]);
+        maxc = max(maxc, cnt[i * 32]);
+        minc = min(minc, cnt[i * 32]);
       } else {
         // outside the image: always "active" with T = 0 and a zero cotangent,
         // which contributes exact zeros (and keeps T_prev = 0 finite)
-        slot(P.T[p], h) = 0.f; P.cnt[i] = 0x7fffffff; slot(P.dr[p], h) = 0.f;
+        slot(P.T[p], h) = 0.f; cnt[i * 32] = 0x7fffffff; slot(P.dr[p], h) = 0.f;
         slot(P.dg[p], h) = 0.f; slot(P.db[p], h) = 0.f; slot(P.D[p], h) = 0.f;
       }
     }
