@@ -78,28 +78,60 @@ cudaError_t run_count_scan(void* temp, size_t temp_bytes, const int32_t* count,
 // K2: one thread per depth rank; a splat's pairs are contiguous, row-major over
 // its tile rect (the reference's `local % spans_x` order, rasterizer.py:312-317),
 // and splats appear in depth-rank order.
-__global__ void duplicate_kernel(const uint32_t* __restrict__ order,
-                                 const int32_t* __restrict__ cnt_r,
-                                 const int32_t* __restrict__ off_r, const int4* __restrict__ rect,
-                                 float* __restrict__ rec, int tiles_x, uint32_t* __restrict__ keys,
-                                 uint32_t* __restrict__ vals, int64_t n) {
-  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= n) return;
-  const int c = cnt_r[r];
-  if (c == 0) return;
-  const uint32_t v = order[r];  // index | steep flag, carried into the pair value
-  const uint32_t i = v & kIndexMask;
-  const int base = off_r[r];
-  const int4 rc = rect[i];
-  const int spans_x = rc.y - rc.x + 1;
-  rec[(size_t)i * kRecordFloats + R_ROW_ORIGIN] =
-      __int_as_float(base - rc.z * spans_x - rc.x);
-  int k = base;
-  for (int ty = rc.z; ty <= rc.w; ++ty) {
-    const uint32_t row = (uint32_t)ty * (uint32_t)tiles_x;
-    for (int tx = rc.x; tx <= rc.y; ++tx, ++k) {
-      keys[k] = row + (uint32_t)tx;
-      vals[k] = v;
+// One warp per 32 consecutive depth ranks.  Their pairs form one contiguous run
+// of the output (off_r is the exclusive scan in rank order), so the warp writes
+// that run with consecutive lanes on consecutive pairs: each lane finds the
+// splat owning pair j by a binary search over the warp's exclusive counts
+// (shuffles) and the tile from the pair's index inside the splat's rect.
+__global__ void __launch_bounds__(256) duplicate_kernel(
+    const uint32_t* __restrict__ order, const int32_t* __restrict__ cnt_r,
+    const int32_t* __restrict__ off_r, const int4* __restrict__ rect, float* __restrict__ rec,
+    int tiles_x, uint32_t* __restrict__ keys, uint32_t* __restrict__ vals, int64_t n) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) - lane;
+  if (r0 >= n) return;  // whole warp
+  const int64_t r = r0 + lane;
+  const int c = r < n ? cnt_r[r] : 0;
+  uint32_t v = 0;
+  int4 rc = make_int4(0, 0, 0, 0);
+  int spans_x = 1;
+  if (c > 0) {
+    v = order[r];  // index | steep flag, carried into the pair value
+    const uint32_t i = v & kIndexMask;
+    rc = rect[i];
+    spans_x = rc.y - rc.x + 1;
+    rec[(size_t)i * kRecordFloats + R_ROW_ORIGIN] =
+        __int_as_float(off_r[r] - rc.z * spans_x - rc.x);
+  }
+  int incl = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  const int excl = incl - c;
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  const int64_t wbase = __shfl_sync(0xffffffffu, r < n ? (int64_t)off_r[r] : 0, 0);
+  for (int j0 = 0; j0 < total; j0 += 32) {
+    const int j = j0 + lane;
+    // largest s with excl[s] <= j (splats with c == 0 share their successor's
+    // excl and are skipped by taking the largest)
+    int sidx = 0;
+#pragma unroll
+    for (int step = 16; step > 0; step >>= 1) {
+      const int cand = sidx + step;
+      const int e = __shfl_sync(0xffffffffu, excl, cand & 31);
+      if (cand < 32 && e <= j) sidx = cand;
+    }
+    const int es = __shfl_sync(0xffffffffu, excl, sidx);
+    const int sx = __shfl_sync(0xffffffffu, spans_x, sidx);
+    const int x0 = __shfl_sync(0xffffffffu, rc.x, sidx);
+    const int y0 = __shfl_sync(0xffffffffu, rc.z, sidx);
+    const uint32_t vs = __shfl_sync(0xffffffffu, v, sidx);
+    if (j < total) {
+      const int l = j - es, ly = l / sx, lx = l - ly * sx;
+      keys[wbase + j] = (uint32_t)(y0 + ly) * (uint32_t)tiles_x + (uint32_t)(x0 + lx);
+      vals[wbase + j] = vs;
     }
   }
 }
