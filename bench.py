@@ -356,7 +356,10 @@ def main():
     achieved = bwd_evals * BWD_FLOPS_PER_EVAL / (bwd_ms * 1e-3) / 1e12
     roofline = {
         "bound": "fp32", "kernel": "blend_bwd (K6)", "achieved": achieved, "peak": fp32_peak,
-        "unit": "TFLOP/s", "frac": achieved / fp32_peak, "traffic": committed_traffic("blend_bwd"),
+        "unit": "TFLOP/s", "frac": achieved / fp32_peak,
+        "traffic": (tr := committed_traffic("blend_bwd")) and tr["bytes_per_launch"],
+        "traffic_source": tr and tr["source"],
+        "traffic_hbm_frac": tr and tr["bytes_per_launch"] / (bwd_ms * 1e-3) / 1e9 / HBM_PEAK_GBS,
         "peak_source": "measured on this GPU by hs_measure_fp32_peaks (FMA probe; "
                        "MEASURED_PEAKS.json has no FP32 entry)",
         "algorithmic": f"{bwd_evals} bwd evals x {BWD_FLOPS_PER_EVAL} flops per launch",
