@@ -2,10 +2,27 @@
 // half-Gaussian weight primitives used by every kernel of the rasterizer.
 #pragma once
 
+#include <atomic>
 #include <cstdint>
 #include <cuda_runtime.h>
 
 namespace hs {
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel and device
+// (a bit per device; the attribute is per-device state).
+template <auto Kernel>
+inline cudaError_t set_dynamic_smem(int bytes) {
+  static std::atomic<uint64_t> done{0};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = dev < 64 ? (1ull << dev) : 0ull;
+  if (bit && (done.load(std::memory_order_acquire) & bit)) return cudaSuccess;
+  e = cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess && bit) done.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
+}
+
 
 constexpr int kTile = 16;              // rasterizer.py:35
 constexpr double kRadiusSigmas = 3.5;  // rasterizer.py:39

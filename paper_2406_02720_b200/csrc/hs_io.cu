@@ -145,16 +145,19 @@ cudaError_t launch_ply_unpack(const PlyUnpackArgs& a, const void* const* fields,
                               cudaStream_t s) {
   const unsigned grid = (unsigned)((a.n + kIoRows - 1) / kIoRows);
   const size_t smem = (size_t)kIoRows * a.stride;
-  if (smem > 200 * 1024) return cudaErrorInvalidValue;
+  if (smem > 200 * 1024) return cudaErrorInvalidValue;  // rows wider than ~6 KB
+  constexpr int kMaxSmem = 200 * 1024;
   if (dtype == 0) {
     auto k = ply_unpack_kernel<float>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const cudaError_t e = set_dynamic_smem<ply_unpack_kernel<float>>(kMaxSmem);
+    if (e != cudaSuccess) return e;
     SceneOut<float> o{(float*)fields[0], (float*)fields[1], (float*)fields[2], (float*)fields[3],
                       (float*)fields[4], (float*)fields[5], (float*)fields[6]};
     k<<<grid, kIoThreads, smem, s>>>(a, o);
   } else {
     auto k = ply_unpack_kernel<double>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const cudaError_t e = set_dynamic_smem<ply_unpack_kernel<double>>(kMaxSmem);
+    if (e != cudaSuccess) return e;
     SceneOut<double> o{(double*)fields[0], (double*)fields[1], (double*)fields[2],
                        (double*)fields[3], (double*)fields[4], (double*)fields[5],
                        (double*)fields[6]};
@@ -173,12 +176,14 @@ static cudaError_t pack_t(const PlyPackArgs& a, const void* const* f, cudaStream
   if (a.out_f64) {
     const size_t smem = (size_t)kIoRows * ncol * 8;
     auto k = ply_pack_kernel<T, double>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const cudaError_t e = set_dynamic_smem<ply_pack_kernel<T, double>>((int)smem);
+    if (e != cudaSuccess) return e;
     k<<<grid, kIoThreads, smem, s>>>(a, in);
   } else {
     const size_t smem = (size_t)kIoRows * ncol * 4;
     auto k = ply_pack_kernel<T, float>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const cudaError_t e = set_dynamic_smem<ply_pack_kernel<T, float>>((int)smem);
+    if (e != cudaSuccess) return e;
     k<<<grid, kIoThreads, smem, s>>>(a, in);
   }
   note_launch();

@@ -282,9 +282,7 @@ static cudaError_t launch_stats(const LossArgs& a, dim3 grid, cudaStream_t strea
     loss_stats_kernel<false, CG><<<grid, kLossThreads, 0, stream>>>(a);
     return cudaGetLastError();
   }
-  static const cudaError_t attr = cudaFuncSetAttribute(
-      loss_stats_kernel<true, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-      (int)loss_stats_smem(CG));
+  const cudaError_t attr = set_dynamic_smem<loss_stats_kernel<true, CG>>((int)loss_stats_smem(CG));
   if (attr != cudaSuccess) return attr;
   loss_stats_kernel<true, CG><<<grid, kLossThreads, loss_stats_smem(CG), stream>>>(a);
   return cudaGetLastError();

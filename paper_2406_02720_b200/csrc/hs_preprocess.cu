@@ -958,8 +958,7 @@ cudaError_t launch_preprocess_bwd_t(const SceneArgs<T>& sc, const CamArgs& cam, 
 #define HS_K7(D)                                                                               \
   case D: {                                                                                    \
     constexpr size_t dyn = k7_dynamic_smem<T, (D + 1) * (D + 1), NT>();                        \
-    static const cudaError_t attr = cudaFuncSetAttribute(                                      \
-        preprocess_bwd_kernel<T, D, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn); \
+    const cudaError_t attr = set_dynamic_smem<preprocess_bwd_kernel<T, D, NT>>((int)dyn);     \
     if (attr != cudaSuccess) return attr;                                                      \
     preprocess_bwd_kernel<T, D, NT><<<(unsigned)grid, NT, out.accumulate ? dyn : 0, stream>>>( \
         sc, cam, kernel, n, count, merged, out);                                               \
