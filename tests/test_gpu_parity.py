@@ -182,3 +182,37 @@ def test_radii_match_oracle_formula(cuda):
     assert (radii[vis] >= 1).all()
     # rect span is consistent with the radius: the pixel rect fits in 2*ceil(r)+1
     assert np.array_equal(np.nonzero(radii)[0], gold["valid"])
+
+
+def test_steep_and_sign_mode_splats_oracle(cuda):
+    """Splitting planes that nearly contain the viewing ray: |n_ray.z| from ~1e-3 down
+    through the sign-mode threshold (1e-6), where |za|, |zb| reach 1e5+.  These take
+    the side-record (steep) form on the packed path or the sign mode; images and
+    gradients must still match the FP64 oracle under the same contract."""
+    O = _oracle()
+    sa = scenes.frustum(6000, 2, 256, 192, seed=23, sig_lo=1.0, sig_hi=8.0)
+    rng = np.random.default_rng(5)
+    # normals perpendicular to the ray through each centre, tilted by tiny angles
+    mu = sa.mu.astype(np.float64)
+    ray = mu / np.linalg.norm(mu, axis=1, keepdims=True)
+    perp = np.cross(ray, rng.normal(size=ray.shape))
+    perp /= np.linalg.norm(perp, axis=1, keepdims=True)
+    tilt = 10.0 ** rng.uniform(-7, -2, len(mu))
+    nrm = perp + tilt[:, None] * ray
+    sa.normal[:] = (nrm / np.linalg.norm(nrm, axis=1, keepdims=True)).astype(np.float32)
+    s64 = sa.as_float64()
+    cam = CameraModel(**sa.cameras[0])
+    d_color = scenes.cotangent(cam.height, cam.width, seed=8)
+    ref_out = O.render(s64, cam)
+    ref_g = O.render_backward(s64, cam, ref_out, d_color)
+    f = ref_out.frame
+    assert (f.mode == 1).sum() > 0 and (np.abs(f.packed[:, 5]) > 1e3).sum() > 100
+    for dtype in (torch.float32, torch.float64):
+        got = run_gpu(sa, 0, "half", dtype, d_color)
+        assert np.array_equal(got["pair_splat"], f.pair_splat)
+        assert np.array_equal(got["mode"], f.mode)
+        ref = {"color": ref_out.color, "alpha": ref_out.alpha, "depth": ref_out.depth,
+               "transmittance": ref_out.transmittance,
+               "terminal": ref_out.per_pixel_terminal_index}
+        assert_images(got, ref)
+        assert_grads(got, ref_g)
