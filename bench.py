@@ -243,7 +243,10 @@ def bench_config(cfg, world, views_per_step=None):
                         f"fwd+bwd with fixed cotangents, gradients summed over the batch"
                         + (" and all-reduced (NCCL)" if world > 1 else ""),
             "gaussians": n, "width": w, "height": h, "sh_degree": sh,
-            "views_per_step": views, "parallelism": f"dp{world} (views)",
+            "views_per_step": views,
+            "parallelism": f"dp{world} (views)" + (
+                ", all-reduce fused into K7 (NVLS multimem)"
+                if world > 1 and os.environ.get("HS_FUSED_ALLREDUCE") == "1" else ""),
             "l2": "inputs larger than L2 (scene 252 MB + 64 MB records per view at c3)"}
 
 
@@ -282,20 +285,43 @@ def main():
                   background_color=sa.background_color, device="cuda", dtype=torch.float32)
     d_colors = [torch.as_tensor(scenes.cotangent(c.height, c.width, seed=1 + v),
                                 dtype=torch.float32, device="cuda") for v, c in enumerate(cams)]
-    grads = device.DeviceGradientSet.empty_flat(scene)
-    reducer = GradientAllReduce(grads) if world > 1 else None
+    # HS_FUSED_ALLREDUCE=1 (N > 1, NVSwitch): the gradient all-reduce fused into K7
+    # through NVLS multicast (multiview.FusedGradientReduce); otherwise one NCCL
+    # all-reduce of the flat buffer after the last view.
+    fused = None
+    if world > 1 and os.environ.get("HS_FUSED_ALLREDUCE") == "1":
+        from paper_2406_02720_b200.multiview import FusedGradientReduce
+        fused = FusedGradientReduce(scene)
+        if not fused.multicast:
+            fused = None
+    grads = fused.grads if fused is not None else device.DeviceGradientSet.empty_flat(scene)
+    reducer = GradientAllReduce(grads) if world > 1 and fused is None else None
     timer = device.StageTimer()
     rast = device.Rasterizer("cuda", slots=1)
 
-    def step(t=None):
+    def backward_views(renderer, t=None):
+        """Every owned view: render, cotangent, backward; the batch gradient summed
+        over views and ranks.  Returns the last view's output."""
         out = None
+        if fused is not None:
+            fused.begin()
         for j, v in enumerate(views):
-            out = rast.render(scene, cams[v], timer=t)
-            rast.render_backward(scene, cams[v], out, d_colors[v], grads=grads, timer=t,
-                                 accumulate=j > 0)
-        if reducer is not None:
+            out, d = renderer(v, t)
+            if fused is not None:
+                rast.render_backward(scene, cams[v], out, d, grads=grads, timer=t,
+                                     reduce_ptrs=fused.ptrs)
+            else:
+                rast.render_backward(scene, cams[v], out, d, grads=grads, timer=t,
+                                     accumulate=j > 0)
+        if fused is not None:
+            fused.end()
+        elif reducer is not None:
             reducer.allreduce()
         return out
+
+    def step(t=None):
+        return backward_views(lambda v, tt: (rast.render(scene, cams[v], timer=tt), d_colors[v]),
+                              t)
 
     def fwd_step():
         for v in views:
@@ -393,13 +419,13 @@ def main():
     dstats = T.DensifyStats.zeros(len(scene))
 
     def train_step(t=None):
-        for j, v in enumerate(views):
+        def render_and_loss(v, _):
             o = rast.render(scene, cams[v])
             with (t.span("loss") if t is not None else contextlib.nullcontext()):
                 _, d = dloss(o.color, targets[v])
-            rast.render_backward(scene, cams[v], o, d, grads=grads, accumulate=j > 0)
-        if reducer is not None:
-            reducer.allreduce()
+            return o, d
+
+        backward_views(render_and_loss)
         with (t.span("adam") if t is not None else contextlib.nullcontext()):
             T.adam_step(scene, grads, tcfg, adam, it_counter[0])
         dstats.update(grads)

@@ -154,7 +154,15 @@ typedef struct hs_grads {
   void* pos_grad_norm;  /* (n,) */
   int32_t* touch_count; /* (n,) */
   int32_t accumulate;   /* 0: overwrite; 1: add into the buffers (multi-view
-                           batches, GradientSet.add rasterizer.py:100-105) */
+                           batches, GradientSet.add rasterizer.py:100-105);
+                           2: add with device atomics (red.global.add);
+                           3: the pointers are NVLS multicast addresses of a
+                           buffer every rank of a node maps (e.g. torch
+                           symmetric memory): K7 adds with multimem.red, so
+                           the switch sums all ranks' gradients into every
+                           rank's copy -- the all-reduce fused into K7.  With
+                           2 / 3 the caller zeroes the buffers first and, for
+                           3, brackets the batch with a cross-rank barrier. */
 } hs_grads;
 
 int hs_preprocess_bwd(hs_frame* frame, const hs_scene* scene,

@@ -406,7 +406,8 @@ int hs_preprocess_bwd(hs_frame* frame, const hs_scene* scene, const hs_camera* c
   if ((st = check_scene(scene, frame))) return st;
   if (!cam || !grads || !grads->d_mu || !grads->d_log_scale || !grads->d_rotation ||
       !grads->d_sh || !grads->d_normal || !grads->d_raw_opacity_a || !grads->d_raw_opacity_b ||
-      !grads->pos_grad_norm || !grads->touch_count)
+      !grads->pos_grad_norm || !grads->touch_count || grads->accumulate < 0 ||
+      grads->accumulate > 3)
     return HS_ERR_INVALID_ARG;
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
   FrameBufs f = carve_frame(frame->frame_ws, frame->n, frame->n_tiles, nullptr);

@@ -15,6 +15,7 @@
 // flags (forward_state<..., kReplay>).
 #include <cmath>
 #include <cstdint>
+#include <type_traits>
 
 #include <cuda_fp16.h>
 
@@ -843,6 +844,57 @@ __device__ __forceinline__ void store_block(E* __restrict__ dst, int cnt, const 
 template <typename T, int K, int NT>
 constexpr size_t k7_dynamic_smem() { return sizeof(GradStage<T, K, NT>); }
 
+// Reduction stores (hs_grads.accumulate 2 / 3): add into the destination with a
+// relaxed device-scope atomic, or -- when the destination is an NVLS multicast
+// address of a buffer shared by every rank -- with multimem.red, which the
+// NVSwitch reduces into every rank's copy: K7 then IS the cross-GPU all-reduce.
+__device__ __forceinline__ void red_add(float* p, float v, bool mc) {
+  if (mc)
+    asm volatile("multimem.red.relaxed.sys.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+  else
+    asm volatile("red.relaxed.gpu.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+__device__ __forceinline__ void red_add(double* p, double v, bool mc) {
+  if (mc)
+    asm volatile("multimem.red.relaxed.sys.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+  else
+    asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+__device__ __forceinline__ void red_add(int32_t* p, int32_t v, bool mc) {
+  if (mc)
+    asm volatile("multimem.red.relaxed.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+  else
+    asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_add4(float* p, float4 v, bool mc) {
+  if (mc)
+    asm volatile("multimem.red.relaxed.sys.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p),
+                 "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+  else
+    asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x),
+                 "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+}
+
+// One field of the CTA's primitives reduced into `dst` (only touched ones: the
+// others add zero).  float fields move in 16-B vector reductions when aligned.
+template <int NT, int S, typename E, typename Get>
+__device__ __forceinline__ void reduce_block(E* __restrict__ dst, int cnt, const int32_t* live,
+                                             bool mc, Get get) {
+  const int n = cnt * S;
+  int done = 0;
+  if constexpr (sizeof(E) == 4 && !std::is_same<E, int32_t>::value) {
+    const int nv = ((uintptr_t)dst & 15) ? 0 : n / 4;
+    for (int v = threadIdx.x; v < nv; v += NT) {
+      if (!any_live<S>(live, v * 4, 4)) continue;
+      red_add4(dst + 4 * v, make_float4(get(4 * v), get(4 * v + 1), get(4 * v + 2),
+                                        get(4 * v + 3)), mc);
+    }
+    done = nv * 4;
+  }
+  for (int e = done + threadIdx.x; e < n; e += NT)
+    if (live[e / S]) red_add(dst + e, get(e), mc);
+}
+
 template <typename T, int DEG, int NT>
 __global__ void __launch_bounds__(NT, 3) preprocess_bwd_kernel(
     SceneArgs<T> sc, CamArgs cam, int kernel, int64_t n, const int32_t* __restrict__ count,
@@ -857,7 +909,9 @@ __global__ void __launch_bounds__(NT, 3) preprocess_bwd_kernel(
   const int64_t base = (int64_t)blockIdx.x * NT;
   const int ncta = (int)(n - base < NT ? n - base : NT);
   const int t = threadIdx.x;
-  const bool acc = out.accumulate != 0;
+  // accumulate: 0 overwrite, 1 read-modify-write, 2 atomic add, 3 multimem add
+  const bool acc = out.accumulate == 1;
+  const bool red = out.accumulate >= 2, mc = out.accumulate == 3;
   stage_in(sm, sc, base, ncta, /*wait=*/false);
   Gs* g = acc ? reinterpret_cast<Gs*>(dyn_smem) : nullptr;
   if (acc) {
@@ -885,6 +939,25 @@ __global__ void __launch_bounds__(NT, 3) preprocess_bwd_kernel(
     preprocess_bwd_one<T, DEG, NT>(sm, pgn_s, touch_s, t, base + t, cam, kernel, count, merged);
   asm volatile("cp.async.wait_all;\n" ::);
   __syncthreads();
+  if (red) {
+    reduce_block<NT, 3>(out.d_mu + base * 3, ncta, touch_s, mc, [&](int e) { return sm.mu[e]; });
+    reduce_block<NT, 3>(out.d_log_scale + base * 3, ncta, touch_s, mc,
+                        [&](int e) { return sm.ls[e]; });
+    reduce_block<NT, 3>(out.d_normal + base * 3, ncta, touch_s, mc,
+                        [&](int e) { return sm.nrm[e]; });
+    reduce_block<NT, 4>(out.d_rotation + base * 4, ncta, touch_s, mc,
+                        [&](int e) { return sm.rot[e]; });
+    reduce_block<NT, 1>(out.d_ra + base, ncta, touch_s, mc, [&](int e) { return sm.ra[e]; });
+    reduce_block<NT, 1>(out.d_rb + base, ncta, touch_s, mc, [&](int e) { return sm.rb[e]; });
+    reduce_block<NT, 1>(out.pos_grad_norm + base, ncta, touch_s, mc,
+                        [&](int e) { return pgn_s[e]; });
+    reduce_block<NT, 1>(out.touch + base, ncta, touch_s, mc, [&](int e) { return touch_s[e]; });
+    reduce_block<NT, 3 * K>(out.d_sh + base * 3 * K, ncta, touch_s, mc, [&](int e) {
+      const int tt = e / (3 * K);
+      return sm.sh[tt * St::SHS + (e - tt * 3 * K)];
+    });
+    return;
+  }
   store_block<NT, 3>(out.d_mu + base * 3, ncta, acc ? g->mu : nullptr, touch_s,
                      [&](int e) { return sm.mu[e]; });
   store_block<NT, 3>(out.d_log_scale + base * 3, ncta, acc ? g->ls : nullptr, touch_s,
@@ -960,7 +1033,8 @@ cudaError_t launch_preprocess_bwd_t(const SceneArgs<T>& sc, const CamArgs& cam, 
     constexpr size_t dyn = k7_dynamic_smem<T, (D + 1) * (D + 1), NT>();                        \
     const cudaError_t attr = set_dynamic_smem<preprocess_bwd_kernel<T, D, NT>>((int)dyn);     \
     if (attr != cudaSuccess) return attr;                                                      \
-    preprocess_bwd_kernel<T, D, NT><<<(unsigned)grid, NT, out.accumulate ? dyn : 0, stream>>>( \
+    preprocess_bwd_kernel<T, D, NT><<<(unsigned)grid, NT, out.accumulate == 1 ? dyn : 0,       \
+                                      stream>>>(                                               \
         sc, cam, kernel, n, count, merged, out);                                               \
     break;                                                                                     \
   }

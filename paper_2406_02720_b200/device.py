@@ -368,12 +368,14 @@ class Rasterizer:
         self.next = (self.next + 1) % len(self.slots)
         return render(scene, cam, self.kernel, timer=timer, ws=ws)
 
-    def render_backward(self, scene, cam, out, d_color, grads=None, timer=None, accumulate=False):
+    def render_backward(self, scene, cam, out, d_color, grads=None, timer=None, accumulate=False,
+                        reduce_ptrs=None):
         return render_backward(scene, cam, out, d_color, grads=grads, timer=timer,
-                               accumulate=accumulate)
+                               accumulate=accumulate, reduce_ptrs=reduce_ptrs)
 
 
-def render_backward(scene, cam, out, d_color, grads=None, timer=None, accumulate=False):
+def render_backward(scene, cam, out, d_color, grads=None, timer=None, accumulate=False,
+                    reduce_ptrs=None):
     """Gradients of sum(d_color * color) for every parameter (rasterizer.py:386-421).
 
     accumulate=True adds this view's gradients into `grads` (GradientSet.add,
@@ -405,6 +407,12 @@ def render_backward(scene, cam, out, d_color, grads=None, timer=None, accumulate
     for name in DeviceGradientSet.NAMES:
         setattr(g, name, getattr(grads, name).data_ptr())
     g.accumulate = 1 if accumulate else 0
+    if reduce_ptrs is not None:
+        # reduction stores: {name: address} (NVLS multicast addresses -> mode 3, or the
+        # buffers' own addresses with reduce_ptrs["mode"] == 2 for device atomics)
+        for name in DeviceGradientSet.NAMES:
+            setattr(g, name, reduce_ptrs[name])
+        g.accumulate = reduce_ptrs.get("mode", 3)
     sc = scene_struct(scene)
     cs = camera_struct(cam)
     with timer.span("preprocess_bwd"):

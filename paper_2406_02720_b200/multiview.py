@@ -38,11 +38,85 @@ class GradientAllReduce:
         return self.grads
 
 
-def batch_gradients(scene, cams, d_colors, view_ids, out=None, rast=None, timer=None):
+class FusedGradientReduce:
+    """The gradient all-reduce fused into K7 (the multimem stretch).
+
+    The flat gradient buffer (and the touch counts) live in torch symmetric memory,
+    mapped by every rank of the node.  K7 adds its per-primitive results straight
+    into the buffer's NVLS multicast address with `multimem.red.add`
+    (hs_grads.accumulate = 3): the NVSwitch reduces every rank's contribution into
+    every rank's copy as K7 produces it, so there is no separate collective and the
+    reduction traffic overlaps the FP64 geometry backward tile by tile.
+
+    Protocol per batch: begin() zeroes the local copy and barriers (nobody may add
+    into a copy that is not zeroed yet), every view's K7 adds, end() barriers
+    (after it every copy holds the global sum).  Without multicast support (a
+    single GPU, no NVSwitch) the same protocol runs with device atomics into the
+    local copy (accumulate = 2), which is exact for one rank; multi-rank callers
+    should then use GradientAllReduce instead (`multicast` tells which).  Sums of
+    more than two ranks' contributions are reduced in switch order, so the result
+    is not bitwise reproducible run to run."""
+
+    def __init__(self, scene, group=None):
+        import torch.distributed._symmetric_memory as symm_mem
+        from . import device
+        n, k, dev, dt = len(scene), scene.sh_coeffs.shape[1], scene.device, scene.dtype
+        sizes = [3 * n, 3 * n, 4 * n, 3 * k * n, 3 * n, n, n, n]
+        padded = [(sz + 3) // 4 * 4 for sz in sizes]
+        self.flat = symm_mem.empty(sum(padded), dtype=dt, device=dev)
+        self.touch = symm_mem.empty(n, dtype=torch.int32, device=dev)
+        grp = group if group is not None else dist.group.WORLD
+        self.h_flat = symm_mem.rendezvous(self.flat, grp)
+        self.h_touch = symm_mem.rendezvous(self.touch, grp)
+        parts = [p[:sz] for p, sz in zip(torch.split(self.flat, padded), sizes)]
+        self.grads = device.DeviceGradientSet(
+            d_mu=parts[0].view(n, 3), d_log_scale=parts[1].view(n, 3),
+            d_rotation=parts[2].view(n, 4), d_sh=parts[3].view(n, k, 3),
+            d_normal=parts[4].view(n, 3), d_raw_opacity_a=parts[5], d_raw_opacity_b=parts[6],
+            pos_grad_norm=parts[7], touch_count=self.touch)
+        self.grads.flat = self.flat
+        mc_flat, mc_touch = self.h_flat.multicast_ptr, self.h_touch.multicast_ptr
+        self.multicast = bool(mc_flat) and bool(mc_touch)
+
+        def base(h, t, mc):
+            # the multicast address of t: the buffer's multicast base + t's offset in it
+            return mc + (t.data_ptr() - h.buffer_ptrs[h.rank]) if mc else t.data_ptr()
+
+        fb = base(self.h_flat, self.flat, mc_flat if self.multicast else 0)
+        self.ptrs = {name: fb + (getattr(self.grads, name).data_ptr() - self.flat.data_ptr())
+                     for name in device.DeviceGradientSet.NAMES if name != "touch_count"}
+        self.ptrs["touch_count"] = base(self.h_touch, self.touch,
+                                        mc_touch if self.multicast else 0)
+        self.ptrs["mode"] = 3 if self.multicast else 2
+
+    def begin(self):
+        self.flat.zero_()
+        self.touch.zero_()
+        self.h_flat.barrier(channel=0)
+
+    def end(self):
+        self.h_flat.barrier(channel=0)
+        return self.grads
+
+
+def batch_gradients(scene, cams, d_colors, view_ids, out=None, rast=None, timer=None,
+                    fused=None):
     """Sum render_backward over this rank's views into `out` (flat buffer).
 
     The first view overwrites, later ones accumulate inside the K7 kernel, so a
-    batch costs no extra gradient-sized passes."""
+    batch costs no extra gradient-sized passes.  With `fused` (a
+    FusedGradientReduce) every view's K7 adds into the shared buffer instead and
+    the result is already summed over all ranks."""
+    if fused is not None:
+        from . import device
+        if rast is None:
+            rast = device.Rasterizer(scene.device)
+        fused.begin()
+        for v in view_ids:
+            r = rast.render(scene, cams[v], timer=timer)
+            rast.render_backward(scene, cams[v], r, d_colors[v], grads=fused.grads, timer=timer,
+                                 reduce_ptrs=fused.ptrs)
+        return fused.end()
     from . import device
     if out is None:
         out = device.DeviceGradientSet.empty_flat(scene)

@@ -228,3 +228,67 @@ def test_torch_autograd_matches_oracle(cuda):
     assert_grads({k: v.double().cpu().numpy() for k, v in got.items()},
                  {k: rg[k] for k in got}, groups=tuple(got))
     assert (radii.cpu().numpy() > 0).sum() == ref.frame.valid.shape[0]
+
+
+def test_reduction_store_modes_match_accumulate(cuda):
+    """hs_grads.accumulate = 2 (device atomics into zeroed buffers) gives bit for bit
+    the gradients of the read-modify-write accumulation over the same two views,
+    up to subnormals (float atomics flush them); the multicast mode 3 differs only
+    in the store instruction."""
+    from paper_2406_02720_b200 import device
+    from paper_2406_02720_b200.geometry import CameraModel, Scene
+    sa = scenes.ball(4000, 2, 96, 72, views=4, seed=3)
+    scene = Scene(*(getattr(sa, f) for f in sa.FIELDS), sh_degree=sa.sh_degree,
+                  background_color=sa.background_color, device="cuda", dtype=torch.float32)
+    cams = [CameraModel(**c) for c in sa.cameras]
+    dcs = [torch.as_tensor(scenes.cotangent(c.height, c.width, seed=i), dtype=torch.float32,
+                           device="cuda") for i, c in enumerate(cams)]
+    ref = device.DeviceGradientSet.empty_flat(scene)
+    red = device.DeviceGradientSet.empty_flat(scene)
+    red.flat.zero_()
+    red.touch_count.zero_()
+    ptrs = {name: getattr(red, name).data_ptr() for name in device.DeviceGradientSet.NAMES}
+    ptrs["mode"] = 2
+    rast = device.Rasterizer("cuda")
+    for j, v in enumerate((0, 2)):
+        out = rast.render(scene, cams[v])
+        rast.render_backward(scene, cams[v], out, dcs[v], grads=ref, accumulate=j > 0)
+        out = rast.render(scene, cams[v])
+        rast.render_backward(scene, cams[v], out, dcs[v], grads=red, reduce_ptrs=ptrs)
+    torch.cuda.synchronize()
+    for name in device.DeviceGradientSet.NAMES:
+        assert _same_up_to_subnormals(getattr(ref, name), getattr(red, name)), name
+
+
+def _same_up_to_subnormals(a, b):
+    """Float atomics flush subnormal operands and results to zero, so values may
+    differ by subnormal amounts (< 2 * FLT_MIN) and by nothing else."""
+    if not a.is_floating_point():
+        return torch.equal(a, b)
+    return bool(((a.double() - b.double()).abs() <= 2 * torch.finfo(a.dtype).tiny).all())
+
+
+def test_fused_gradient_reduce_single_rank(cuda):
+    """FusedGradientReduce over a one-rank NCCL group (symmetric memory; without an
+    NVSwitch it runs the same protocol with device atomics): equals batch_gradients."""
+    import torch.distributed as dist
+    from paper_2406_02720_b200 import device, multiview
+    from paper_2406_02720_b200.geometry import CameraModel, Scene
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", init_method="tcp://127.0.0.1:29517", rank=0,
+                                world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        sa = scenes.ball(3000, 1, 80, 64, views=3, seed=8)
+        scene = Scene(*(getattr(sa, f) for f in sa.FIELDS), sh_degree=sa.sh_degree,
+                      background_color=sa.background_color, device="cuda", dtype=torch.float32)
+        cams = [CameraModel(**c) for c in sa.cameras]
+        dcs = [torch.as_tensor(scenes.cotangent(c.height, c.width, seed=i), dtype=torch.float32,
+                               device="cuda") for i, c in enumerate(cams)]
+        ref = multiview.batch_gradients(scene, cams, dcs, [0, 1, 2])
+        fused = multiview.FusedGradientReduce(scene)
+        got = multiview.batch_gradients(scene, cams, dcs, [0, 1, 2], fused=fused)
+        torch.cuda.synchronize()
+        for name in device.DeviceGradientSet.NAMES:
+            assert _same_up_to_subnormals(getattr(ref, name), getattr(got, name)), name
+    finally:
+        dist.destroy_process_group()
