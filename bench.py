@@ -372,6 +372,23 @@ def main():
     lens = (starts[1:] - starts[:-1]).reshape(out.frame.tiles_y, out.frame.tiles_x)
     lens_px = lens.repeat_interleave(16, 0).repeat_interleave(16, 1)[:cam.height, :cam.width]
     fwd_evals = int(torch.minimum(term + 1, lens_px).sum().item())
+    # %HBM of the HBM-bound stages from SURVEY.md 8(d)'s compulsory bytes per view
+    n_prim = len(scene)
+    k_sh = (scene.sh_degree + 1) ** 2
+    m_vis = int((out.radii > 0).sum().item())
+    p_pairs = out.frame.num_pairs
+    compulsory = {
+        "preprocess_fwd": n_prim * (15 + 3 * k_sh) * 4 + m_vis * 80,
+        "bin_and_sort": p_pairs * 44 + m_vis * 24,
+        "preprocess_bwd": n_prim * (15 + 3 * k_sh) * 4 * 2 + m_vis * 48 + n_prim * 8,
+    }
+    hbm_stages = {}
+    for name, nbytes in compulsory.items():
+        ms_stage = stage_ms.get(name)
+        if ms_stage:
+            gbs = nbytes / (ms_stage * 1e-3) / 1e9
+            hbm_stages[name] = {"bytes": nbytes, "ms": ms_stage, "gbs": gbs,
+                                "frac": gbs / HBM_PEAK_GBS}
     bwd_evals = int(term.sum().item())
     import ctypes
     a, b = ctypes.c_double(0), ctypes.c_double(0)
@@ -396,6 +413,7 @@ def main():
         "stage_ms": stage_ms,
         "ex2_gops_peak": b.value,
         "fma2_tflops_peak": lib.hs_last_fma2_tflops(),
+        "hbm_stages": hbm_stages,
     }
 
     # end-to-end through the drop-in numpy API, host buffers, copies inside
