@@ -1,3 +1,5 @@
+"""Per-iteration wall time of the drop-in numpy API (render + render_backward) at c3:
+shows the warm-up iterations that allocate pinned staging and workspaces."""
 import sys, time
 import numpy as np
 import torch
