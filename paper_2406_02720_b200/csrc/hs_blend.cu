@@ -87,7 +87,8 @@ struct SplatLane {
   float zK, zc_hi, zc_lo, zt_hi, zt_lo;
 };
 
-template <bool STEEP>
+// PRE: the staged record was already transformed by prescale_record (K5).
+template <bool STEEP, bool PRE = false>
 __device__ __forceinline__ SplatLane splat_lane(const float4 (&q)[4], const SteepRec& side,
                                                 float px, float py0) {
   SplatLane s;
@@ -95,9 +96,9 @@ __device__ __forceinline__ SplatLane splat_lane(const float4 (&q)[4], const Stee
   const float2 lof = __half22float2(lo);
   s.dx = (px - q[0].x) - lof.x;
   s.dy0 = (py0 - q[0].y) - lof.y;
-  s.A = q[0].z * kNegHalfLog2e;
-  s.B = q[0].w * kNegLog2e;
-  s.C = q[1].x * kNegHalfLog2e;
+  s.A = PRE ? q[0].z : q[0].z * kNegHalfLog2e;
+  s.B = PRE ? q[0].w : q[0].w * kNegLog2e;
+  s.C = PRE ? q[1].x : q[1].x * kNegHalfLog2e;
   s.P0 = s.A * s.dx * s.dx;
   s.Bx = s.B * s.dx;
   s.za = q[1].y;
@@ -220,8 +221,8 @@ __device__ __forceinline__ void fwd_commit(float nw, float& T, float& A, float& 
 template <bool STEEP>
 __device__ __forceinline__ void fwd_splat_fast(const float4 (&q)[4], const SteepRec& side,
                                                float px, float py0, FwdPix& P) {
-  const SplatLane s = splat_lane<STEEP>(q, side, px, py0);
-  const float nc1 = -q[1].w, nc2 = -q[2].x;
+  const SplatLane s = splat_lane<STEEP, true>(q, side, px, py0);
+  const float nc1 = q[1].w, nc2 = q[2].x;  // negated by prescale_record
   const float cr = q[2].y, cg = q[2].z, cb = q[2].w, z = q[3].x;
 #pragma unroll
   for (int p = 0; p < kPairs; ++p) {
@@ -248,10 +249,10 @@ __device__ __forceinline__ void fwd_splat_generic(const float4 (&q)[4], const St
                                                   uint32_t flags, float px, float py0,
                                                   FwdPix& P) {
   const bool steep = flags & kFlagSteep;
-  const SplatLane s = steep ? splat_lane<true>(q, side, px, py0)
-                            : splat_lane<false>(q, side, px, py0);
+  const SplatLane s = steep ? splat_lane<true, true>(q, side, px, py0)
+                            : splat_lane<false, true>(q, side, px, py0);
   const int mode = (int)(flags & 3u);
-  const float c1 = q[1].w, c2 = q[2].x;
+  const float c1 = -q[1].w, c2 = -q[2].x;  // prescale_record negated them
   const float cr = q[2].y, cg = q[2].z, cb = q[2].w, z = q[3].x;
 #pragma unroll
   for (int i = 0; i < kPx; ++i) {
@@ -263,6 +264,16 @@ __device__ __forceinline__ void fwd_splat_generic(const float4 (&q)[4], const St
     fwd_commit(-w, slot(P.T[p], h), slot(P.A[p], h), slot(P.C[p], h), slot(P.ar[p], h),
                slot(P.ag[p], h), slot(P.ab[p], h), slot(P.ad[p], h), cr, cg, cb, z);
   }
+}
+
+// K5 staging transform, once per splat instead of once per lane: conic to the
+// log2 scale of the exponent and -c1, -c2 (the forward composites with -w).
+__device__ __forceinline__ void prescale_record(float4 (&r)[4]) {
+  r[0].z *= kNegHalfLog2e;
+  r[0].w *= kNegLog2e;
+  r[1].x *= kNegHalfLog2e;
+  r[1].w = -r[1].w;
+  r[2].x = -r[2].x;
 }
 
 __device__ __forceinline__ bool warp_any_alive(const FwdPix& P) {
@@ -312,6 +323,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) blend_fwd_kernel(
       cp_async_wait<1>();
       __syncwarp();
       const int s = b & 1;
+      if (lane < nb) prescale_record(st.rec[s][lane]);
+      __syncwarp();
       for (int j = 0; j < nb; ++j) {
         // dead pixels never change again: stop once the whole tile is dead
         // (checked every 8 splats; the reference checks per splat, same result)
