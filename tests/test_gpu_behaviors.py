@@ -121,3 +121,37 @@ def test_depth_normalmap_planes_and_mask(cuda):
     sc.raw_opacity_a[:] = -50
     sc.raw_opacity_b[:] = -50
     assert not R.render_depth_normalmap(R.render(sc, _cam(32, 32))).any()
+
+
+@pytest.mark.parametrize("wh", [(1, 1), (15, 17), (33, 2)])
+def test_tiny_and_ragged_images_vs_oracle(cuda, wh):
+    """Images smaller than a tile and ragged edges: same integers, images and
+    gradients as the oracle."""
+    from oracle import oracle as O
+    from paper_2406_02720_b200 import rasterizer as R
+    w, h = wh
+    sc = _scene(np.random.default_rng(7), 12, spread=0.2)
+    cam = _cam(w, h, 20.0)
+    ref = O.render(sc, cam)
+    out = R.render(sc, cam)
+    np.testing.assert_allclose(out.color, ref.color, atol=1e-5)
+    assert np.array_equal(out.per_pixel_terminal_index, ref.per_pixel_terminal_index)
+    d = np.random.default_rng(1).uniform(-1, 1, (h, w, 3))
+    g = R.render_backward(sc, cam, out, d)
+    rg = O.render_backward(sc, cam, ref, d)
+    for name in ("d_mu", "d_log_scale", "d_rotation", "d_sh", "d_normal", "d_raw_opacity_a",
+                 "d_raw_opacity_b"):
+        a, b = getattr(g, name), rg[name]
+        assert np.linalg.norm(a - b) <= 1e-3 * max(np.linalg.norm(b), 1e-12), name
+
+
+def test_everything_culled(cuda):
+    """No pair at all (P = 0): background image, zero gradients, zero touch counts."""
+    from paper_2406_02720_b200 import rasterizer as R
+    sc = _scene(np.random.default_rng(8), 5)
+    sc.mu[:, 0] += 100.0  # far off screen
+    cam = _cam(40, 24)
+    out = R.render(sc, cam)
+    assert np.allclose(out.color, sc.background_color, atol=1e-7)
+    g = R.render_backward(sc, cam, out, np.ones((24, 40, 3)))
+    assert not g.d_mu.any() and not g.d_sh.any() and not g.touch_count.any()
