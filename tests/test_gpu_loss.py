@@ -98,3 +98,26 @@ def test_loss_many_channels_vs_oracle(cuda):
         val, grad = L.compute_loss(a, b, 0.3)
         assert val == pytest.approx(ref_loss, rel=1e-12)
         assert _grad_close(grad, ref_grad, 1e-12)
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_loss_random_shapes_vs_oracle(cuda, seed):
+    """Random sizes (ragged against the 32x16 tiles), channel counts, lambdas and
+    exact ties against the C oracle (itself bit-identical to the reference)."""
+    from oracle import oracle as O
+    from paper_2406_02720_b200 import loss as L
+    rng = np.random.default_rng(seed)
+    h, w = int(rng.integers(11, 90)), int(rng.integers(11, 120))
+    c = int(rng.choice([1, 2, 3, 4, 5]))
+    lam = float(rng.choice([0.0, 1.0, rng.uniform(0, 1)]))
+    a = rng.random((h, w, c)).astype(np.float32)
+    b = np.clip(a + rng.normal(0, 0.2, a.shape), 0, 1).astype(np.float32)
+    ties = rng.random(a.shape) < 0.1
+    b[ties] = a[ties]
+    if c == 1 and rng.random() < 0.5:
+        a, b = a[..., 0], b[..., 0]
+    ref_loss, ref_grad = O.compute_loss(a, b, lam)
+    val, grad = L.compute_loss(a, b, lam)
+    assert grad.shape == ref_grad.shape
+    assert val == pytest.approx(ref_loss, rel=1e-12, abs=1e-15)
+    assert _grad_close(grad, ref_grad, 1e-12)
