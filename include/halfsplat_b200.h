@@ -30,6 +30,17 @@
  *    Workspaces are caller-allocated from the *_workspace_size queries; the
  *    library never allocates on this seam.  Calls on distinct frames/streams are
  *    independent (re-entrant).
+ *
+ *  Training-iteration entry points around the path, same
+ *  conventions (device pointers, caller stream, caller workspaces):
+ *    hs_loss                 <- loss.compute_loss / ssim_with_grad (loss.py:48-106)
+ *    hs_adam_step            <- the Adam block of trainer.step (trainer.py:192-224)
+ *    hs_densify_*            <- DensifyStats / densify_and_prune (trainer.py:229-340)
+ *    hs_reset_opacity, hs_opacity_disparity (trainer.py:343-358)
+ *    hs_ply_pack / unpack    <- scene_io save/load/import/export payloads
+ *                               (scene_io.py:136-269)
+ *  hs_grads.accumulate = 3 lets K7 reduce its gradients straight into an NVLS
+ *  multicast buffer: the multi-GPU all-reduce fused into the kernel.
  */
 #ifndef HALFSPLAT_B200_H
 #define HALFSPLAT_B200_H
