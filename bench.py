@@ -246,7 +246,9 @@ def bench_config(cfg, world, views_per_step=None):
             "views_per_step": views,
             "parallelism": f"dp{world} (views)" + (
                 ", all-reduce fused into K7 (NVLS multimem)"
-                if world > 1 and os.environ.get("HS_FUSED_ALLREDUCE") == "1" else ""),
+                if world > 1 and os.environ.get("HS_FUSED_ALLREDUCE") == "1" else
+                ", NCCL all-reduce in 4 buckets overlapping K7"
+                if world > 1 and os.environ.get("HS_BUCKETED_ALLREDUCE", "1") == "1" else ""),
             "l2": "inputs larger than L2 (scene 252 MB + 64 MB records per view at c3)"}
 
 
@@ -296,6 +298,9 @@ def main():
             fused = None
     grads = fused.grads if fused is not None else device.DeviceGradientSet.empty_flat(scene)
     reducer = GradientAllReduce(grads) if world > 1 and fused is None else None
+    # HS_BUCKETED_ALLREDUCE=0 turns off the K7-bucketed overlap of the NCCL all-reduce
+    bucketed = reducer is not None and os.environ.get("HS_BUCKETED_ALLREDUCE", "1") == "1"
+    buckets = GradientAllReduce.bucket_ranges(len(scene)) if bucketed else None
     timer = device.StageTimer()
     rast = device.Rasterizer("cuda", slots=1)
 
@@ -310,11 +315,18 @@ def main():
             if fused is not None:
                 rast.render_backward(scene, cams[v], out, d, grads=grads, timer=t,
                                      reduce_ptrs=fused.ptrs)
+            elif bucketed and j == len(views) - 1:
+                # last view: K7 in buckets, each bucket's all-reduce overlapping the next
+                rast.render_backward(scene, cams[v], out, d, grads=grads, timer=t,
+                                     accumulate=j > 0, buckets=buckets,
+                                     on_bucket=reducer.start_range)
             else:
                 rast.render_backward(scene, cams[v], out, d, grads=grads, timer=t,
                                      accumulate=j > 0)
         if fused is not None:
             fused.end()
+        elif bucketed:
+            reducer.finish()
         elif reducer is not None:
             reducer.allreduce()
         return out

@@ -179,6 +179,12 @@ typedef struct hs_grads {
 int hs_preprocess_bwd(hs_frame* frame, const hs_scene* scene,
                       const hs_camera* cam, const hs_grads* grads, void* stream);
 
+/* hs_preprocess_bwd restricted to primitives [begin, end) (begin a multiple of
+ * 128; end clamped to n): K7 in buckets, so a bucket's gradients can be
+ * all-reduced while the next bucket computes. */
+int hs_preprocess_bwd_range(hs_frame* frame, const hs_scene* scene, const hs_camera* cam,
+                            const hs_grads* grads, int64_t begin, int64_t end, void* stream);
+
 /* Introspection for parity: the reference's FrameGeometry integers and packed
  * columns (rasterizer.py:108-147).  Device outputs:
  *   valid (n,) int32 -- original indices of surviving primitives, first M used

@@ -118,6 +118,9 @@ _SIGNATURES = {
                                c_void_p, c_void_p]),
     "hs_preprocess_bwd": (c_int32, [ctypes.POINTER(HsFrame), ctypes.POINTER(HsScene),
                                     ctypes.POINTER(HsCamera), ctypes.POINTER(HsGrads), c_void_p]),
+    "hs_preprocess_bwd_range": (c_int32, [ctypes.POINTER(HsFrame), ctypes.POINTER(HsScene),
+                                          ctypes.POINTER(HsCamera), ctypes.POINTER(HsGrads),
+                                          c_int64, c_int64, c_void_p]),
     "hs_frame_export": (c_int32, [ctypes.POINTER(HsFrame), c_void_p, c_void_p, c_void_p,
                                   c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "hs_screen_splats": (c_int32, [ctypes.POINTER(HsScene), ctypes.POINTER(HsCamera), c_int32,

@@ -201,8 +201,18 @@ static GradArgs<T> grad_args(const hs_grads* g) {
   a.pos_grad_norm = static_cast<T*>(g->pos_grad_norm);
   a.touch = g->touch_count;
   a.accumulate = g->accumulate;
+  a.begin = 0;
+  a.end = INT64_MAX;
   return a;
 }
+
+template <typename T>
+static GradArgs<T> ranged(GradArgs<T> a, int64_t begin, int64_t end) {
+  a.begin = begin;
+  a.end = end;
+  return a;
+}
+
 
 static int check_frame_ws(const hs_frame* f) {
   if (!f || !f->frame_ws) return HS_ERR_WORKSPACE;
@@ -400,6 +410,11 @@ int hs_blend_bwd(hs_frame* frame, const double* bg, const float* d_color,
 
 int hs_preprocess_bwd(hs_frame* frame, const hs_scene* scene, const hs_camera* cam,
                       const hs_grads* grads, void* stream_) {
+  return hs_preprocess_bwd_range(frame, scene, cam, grads, 0, INT64_MAX, stream_);
+}
+
+int hs_preprocess_bwd_range(hs_frame* frame, const hs_scene* scene, const hs_camera* cam,
+                            const hs_grads* grads, int64_t begin, int64_t end, void* stream_) {
   int st = check_frame_ws(frame);
   if (st) return st;
   if ((st = check_bin_ws(frame))) return st;
@@ -407,7 +422,7 @@ int hs_preprocess_bwd(hs_frame* frame, const hs_scene* scene, const hs_camera* c
   if (!cam || !grads || !grads->d_mu || !grads->d_log_scale || !grads->d_rotation ||
       !grads->d_sh || !grads->d_normal || !grads->d_raw_opacity_a || !grads->d_raw_opacity_b ||
       !grads->pos_grad_norm || !grads->touch_count || grads->accumulate < 0 ||
-      grads->accumulate > 3)
+      grads->accumulate > 3 || begin < 0 || begin % 128 != 0 || end < begin)
     return HS_ERR_INVALID_ARG;
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
   FrameBufs f = carve_frame(frame->frame_ws, frame->n, frame->n_tiles, nullptr);
@@ -416,13 +431,13 @@ int hs_preprocess_bwd(hs_frame* frame, const hs_scene* scene, const hs_camera* c
   if (scene->dtype == HS_DTYPE_F32) {
     HS_CUDA(launch_preprocess_bwd_t<float>(scene_args<float>(scene), ca, frame->kernel, frame->n,
                                            frame->tiles_x, f.rec, f.rect, f.count, f.rank_of,
-                                           f.last_rank, b.rows, f.merged, grad_args<float>(grads),
-                                           stream));
+                                           f.last_rank, b.rows, f.merged, ranged(grad_args<float>(grads), begin, end), stream));
   } else {
     HS_CUDA(launch_preprocess_bwd_t<double>(scene_args<double>(scene), ca, frame->kernel,
                                             frame->n, frame->tiles_x, f.rec, f.rect, f.count,
                                             f.rank_of, f.last_rank, b.rows, f.merged,
-                                            grad_args<double>(grads), stream));
+                                            ranged(grad_args<double>(grads), begin, end),
+                                            stream));
   }
   return HS_OK;
 }

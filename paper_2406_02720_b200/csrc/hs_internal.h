@@ -43,6 +43,7 @@ struct GradArgs {
   T* pos_grad_norm;
   int32_t* touch;
   int accumulate;
+  int64_t begin, end;  // primitive range [begin, end) of this launch (begin % 128 == 0)
 };
 
 // ---- hs_preprocess.cu -----------------------------------------------------

@@ -479,8 +479,8 @@ __global__ void __launch_bounds__(256) merge_rows_kernel(
     int64_t n, int tiles_x, const float4* __restrict__ rec, const int4* __restrict__ rect,
     const int32_t* __restrict__ count, const uint32_t* __restrict__ rank_of,
     const int32_t* __restrict__ last_rank, const float* __restrict__ rows,
-    float4* __restrict__ merged) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    float4* __restrict__ merged, int64_t begin) {
+  const int64_t i = begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int cnt = count[i];
   if (cnt == 0) return;
@@ -906,7 +906,7 @@ __global__ void __launch_bounds__(NT, 3) preprocess_bwd_kernel(
   __shared__ T pgn_s[NT];
   __shared__ int32_t touch_s[NT];
   extern __shared__ __align__(16) unsigned char dyn_smem[];
-  const int64_t base = (int64_t)blockIdx.x * NT;
+  const int64_t base = out.begin + (int64_t)blockIdx.x * NT;
   const int ncta = (int)(n - base < NT ? n - base : NT);
   const int t = threadIdx.x;
   // accumulate: 0 overwrite, 1 read-modify-write, 2 atomic add, 3 multimem add
@@ -1022,11 +1022,15 @@ cudaError_t launch_preprocess_bwd_t(const SceneArgs<T>& sc, const CamArgs& cam, 
                                     const int32_t* count, const uint32_t* rank_of,
                                     const int32_t* last_rank, const float* rows, float4* merged,
                                     const GradArgs<T>& out, cudaStream_t stream) {
-  merge_rows_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(
-      n, tiles_x, rec, rect, count, rank_of, last_rank, rows, merged);
+  // the launch covers primitives [out.begin, out.end): K7a and K7 over that range only
+  const int64_t end = out.end < n ? out.end : n;
+  if (end <= out.begin) return cudaSuccess;
+  const int64_t cnt = end - out.begin;
+  merge_rows_kernel<<<(unsigned)((cnt + 255) / 256), 256, 0, stream>>>(
+      end, tiles_x, rec, rect, count, rank_of, last_rank, rows, merged, out.begin);
   note_launch();
   constexpr int NT = sizeof(T) == 4 ? 128 : 64;
-  const int64_t grid = (n + NT - 1) / NT;
+  const int64_t grid = (cnt + NT - 1) / NT;
   switch (sc.deg) {
 #define HS_K7(D)                                                                               \
   case D: {                                                                                    \
@@ -1035,7 +1039,7 @@ cudaError_t launch_preprocess_bwd_t(const SceneArgs<T>& sc, const CamArgs& cam, 
     if (attr != cudaSuccess) return attr;                                                      \
     preprocess_bwd_kernel<T, D, NT><<<(unsigned)grid, NT, out.accumulate == 1 ? dyn : 0,       \
                                       stream>>>(                                               \
-        sc, cam, kernel, n, count, merged, out);                                               \
+        sc, cam, kernel, end, count, merged, out);                                             \
     break;                                                                                     \
   }
     HS_K7(0) HS_K7(1) HS_K7(2) HS_K7(3)

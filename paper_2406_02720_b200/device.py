@@ -369,13 +369,14 @@ class Rasterizer:
         return render(scene, cam, self.kernel, timer=timer, ws=ws)
 
     def render_backward(self, scene, cam, out, d_color, grads=None, timer=None, accumulate=False,
-                        reduce_ptrs=None):
+                        reduce_ptrs=None, buckets=None, on_bucket=None):
         return render_backward(scene, cam, out, d_color, grads=grads, timer=timer,
-                               accumulate=accumulate, reduce_ptrs=reduce_ptrs)
+                               accumulate=accumulate, reduce_ptrs=reduce_ptrs, buckets=buckets,
+                               on_bucket=on_bucket)
 
 
 def render_backward(scene, cam, out, d_color, grads=None, timer=None, accumulate=False,
-                    reduce_ptrs=None):
+                    reduce_ptrs=None, buckets=None, on_bucket=None):
     """Gradients of sum(d_color * color) for every parameter (rasterizer.py:386-421).
 
     accumulate=True adds this view's gradients into `grads` (GradientSet.add,
@@ -416,7 +417,17 @@ def render_backward(scene, cam, out, d_color, grads=None, timer=None, accumulate
     sc = scene_struct(scene)
     cs = camera_struct(cam)
     with timer.span("preprocess_bwd"):
-        st = lib.hs_preprocess_bwd(ctypes.byref(frame.st), ctypes.byref(sc), ctypes.byref(cs),
-                                   ctypes.byref(g), s)
-    _native.check(st, "hs_preprocess_bwd")
+        if buckets is None:
+            st = lib.hs_preprocess_bwd(ctypes.byref(frame.st), ctypes.byref(sc),
+                                       ctypes.byref(cs), ctypes.byref(g), s)
+            _native.check(st, "hs_preprocess_bwd")
+        else:
+            # K7 in primitive buckets; on_bucket(b, e) runs right after each launch (e.g.
+            # an async all-reduce of that bucket, overlapping the next bucket's K7)
+            for b, e in buckets:
+                st = lib.hs_preprocess_bwd_range(ctypes.byref(frame.st), ctypes.byref(sc),
+                                                 ctypes.byref(cs), ctypes.byref(g), b, e, s)
+                _native.check(st, "hs_preprocess_bwd_range")
+                if on_bucket is not None:
+                    on_bucket(b, e)
     return grads

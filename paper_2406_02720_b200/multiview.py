@@ -22,18 +22,68 @@ def shard_views(n_views, world, rank):
 
 
 class GradientAllReduce:
-    """Sums a flat gradient buffer (+ int touch counts) over the default group."""
+    """Sums a flat gradient buffer (+ int touch counts) over the default group.
+
+    allreduce() sums everything after the last K7.  The bucketed form overlaps the
+    exchange with K7: K7 runs over primitive buckets
+    (`bucket_ranges`), start_range(b, e) issues the bucket's all-reduce
+    asynchronously right after its K7 launch (NCCL orders it after that launch on
+    its own stream, so it runs under the next bucket's K7), and finish() waits
+    for all of them and sums the touch counts."""
 
     def __init__(self, grads, group=None):
         if not hasattr(grads, "flat"):
             raise ValueError("gradients must be allocated with DeviceGradientSet.empty_flat")
         self.grads = grads
         self.group = group
+        self._pending = []
+
+    @staticmethod
+    def _active():
+        return dist.is_available() and dist.is_initialized()
 
     def allreduce(self):
-        if not dist.is_available() or not dist.is_initialized() or dist.get_world_size(self.group) == 1:
+        if not self._active():
             return self.grads
         dist.all_reduce(self.grads.flat, op=dist.ReduceOp.SUM, group=self.group)
+        dist.all_reduce(self.grads.touch_count, op=dist.ReduceOp.SUM, group=self.group)
+        return self.grads
+
+    @staticmethod
+    def bucket_ranges(n, buckets=4, align=128):
+        """[(begin, end)] covering n primitives; begins are multiples of `align`
+        (K7's CTA size, hs_preprocess_bwd_range)."""
+        per = -(-n // (buckets * align)) * align
+        return [(b, min(b + per, n)) for b in range(0, n, per)] if n > 0 else []
+
+    def slices(self, b, e):
+        g = self.grads
+        return [g.d_mu[b:e], g.d_log_scale[b:e], g.d_rotation[b:e], g.d_sh[b:e],
+                g.d_normal[b:e], g.d_raw_opacity_a[b:e], g.d_raw_opacity_b[b:e],
+                g.pos_grad_norm[b:e]]
+
+    def start_range(self, b, e):
+        if not self._active():
+            return
+        tensors = self.slices(b, e)
+        if tensors[0].is_cuda and dist.get_backend(self.group) == "nccl":
+            from torch.distributed.distributed_c10d import _coalescing_manager
+            # one grouped NCCL launch for the bucket's eight field slices
+            with _coalescing_manager(group=self.group, device=tensors[0].device,
+                                     async_ops=True) as cm:
+                for t in tensors:
+                    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+            self._pending.append(cm)
+        else:
+            self._pending.extend(dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group,
+                                                 async_op=True) for t in tensors)
+
+    def finish(self):
+        if not self._active():
+            return self.grads
+        for w in self._pending:
+            w.wait()
+        self._pending = []
         dist.all_reduce(self.grads.touch_count, op=dist.ReduceOp.SUM, group=self.group)
         return self.grads
 

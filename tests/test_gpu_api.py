@@ -292,3 +292,41 @@ def test_fused_gradient_reduce_single_rank(cuda):
             assert _same_up_to_subnormals(getattr(ref, name), getattr(got, name)), name
     finally:
         dist.destroy_process_group()
+
+
+def test_bucketed_k7_and_allreduce_single_rank(cuda):
+    """K7 over primitive buckets (hs_preprocess_bwd_range) with each bucket's NCCL
+    all-reduce issued right after its launch (one-rank NCCL group: the exchange is
+    the identity): bit-identical to one K7 launch, for a fresh and an accumulating
+    view."""
+    import torch.distributed as dist
+    from paper_2406_02720_b200 import device, multiview
+    from paper_2406_02720_b200.geometry import CameraModel, Scene
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", init_method="tcp://127.0.0.1:29519", rank=0,
+                                world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        sa = scenes.ball(5000, 3, 96, 72, views=4, seed=12)
+        scene = Scene(*(getattr(sa, f) for f in sa.FIELDS), sh_degree=sa.sh_degree,
+                      background_color=sa.background_color, device="cuda", dtype=torch.float32)
+        cams = [CameraModel(**c) for c in sa.cameras]
+        dcs = [torch.as_tensor(scenes.cotangent(c.height, c.width, seed=i), dtype=torch.float32,
+                               device="cuda") for i, c in enumerate(cams)]
+        ref = device.DeviceGradientSet.empty_flat(scene)
+        got = device.DeviceGradientSet.empty_flat(scene)
+        red = multiview.GradientAllReduce(got)
+        buckets = multiview.GradientAllReduce.bucket_ranges(len(scene), buckets=3)
+        rast = device.Rasterizer("cuda")
+        for j, v in enumerate((1, 3)):
+            out = rast.render(scene, cams[v])
+            rast.render_backward(scene, cams[v], out, dcs[v], grads=ref, accumulate=j > 0)
+            out = rast.render(scene, cams[v])
+            last = j == 1
+            rast.render_backward(scene, cams[v], out, dcs[v], grads=got, accumulate=j > 0,
+                                 buckets=buckets, on_bucket=red.start_range if last else None)
+        red.finish()
+        torch.cuda.synchronize()
+        for name in device.DeviceGradientSet.NAMES:
+            assert torch.equal(getattr(ref, name), getattr(got, name)), name
+    finally:
+        dist.destroy_process_group()

@@ -160,3 +160,53 @@ def test_scene_io_header_errors(tmp_path):
                                   b"\0" * 8))
     with pytest.raises(ValueError):
         scene_io.import_3dgs(write("f.ply", "ply\n"), normal_init="bogus")
+
+
+def _bucketed_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2406_02720_b200.device import DeviceGradientSet
+
+    class S:  # the attributes DeviceGradientSet.empty_flat reads
+        pass
+
+    n, k = 700, 9
+
+    class Sc(S):
+        sh_coeffs = torch.zeros((n, k, 3))
+        device, dtype = torch.device("cpu"), torch.float32
+
+        def __len__(self):
+            return n
+
+    g = DeviceGradientSet.empty_flat(Sc())
+    torch.manual_seed(rank)
+    for name in DeviceGradientSet.NAMES[:-1]:
+        getattr(g, name).copy_(torch.randn(getattr(g, name).shape))
+    g.touch_count.copy_(torch.randint(0, 3, (n,), dtype=torch.int32))
+    want = [getattr(g, name).clone() for name in DeviceGradientSet.NAMES]
+    for t in want:
+        dist.all_reduce(t)
+    red = GradientAllReduce(g)
+    for b, e in GradientAllReduce.bucket_ranges(n, buckets=3):
+        red.start_range(b, e)
+    red.finish()
+    ok = all(torch.equal(getattr(g, name), w) for name, w in zip(DeviceGradientSet.NAMES, want))
+    q.put((rank, ok))
+    dist.destroy_process_group()
+
+
+def test_bucketed_allreduce_gloo_world2():
+    """The K7-bucketed exchange (start_range per primitive bucket, then finish) sums
+    exactly what one all-reduce of every group sums, on 2 CPU ranks."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 30500 + os.getpid() % 1000
+    procs = [ctx.Process(target=_bucketed_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok for _, ok in res), res
