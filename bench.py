@@ -562,10 +562,13 @@ def run_e2e(args, sa, cam, dropin, world, barrier, torch, dist):
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms = float(ms_t.item())
-    h2d = sum(getattr(sa, f).nbytes for f in sa.FIELDS) + d_color.nbytes
+    # bytes that cross PCIe: the scene, the cotangent as float32 (converted on the host
+    # into pinned staging), the images, and the gradients with pos_grad_norm (float32)
+    # and touch_count (int64, widened on the device)
+    h2d = sum(getattr(sa, f).nbytes for f in sa.FIELDS) + d_color.size * 4
     d2h = (out.color.size + out.alpha.size + out.depth.size + out.transmittance.size) * 4 + \
         out.per_pixel_terminal_index.nbytes + out.radii.nbytes + \
-        sum(getattr(sa, f).nbytes for f in sa.FIELDS) + len(sa) * 8
+        sum(getattr(sa, f).nbytes for f in sa.FIELDS) + len(sa) * (4 + 8)
     return {"value": world * 1e3 / ms, "unit": "iters/s", "ms_per_step": ms, "steps": n,
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
             "api": "paper_2406_02720_b200.rasterizer.render + render_backward (numpy in/out; "

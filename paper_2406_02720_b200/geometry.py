@@ -83,7 +83,9 @@ def _to_tensor(x, dtype, device):
         t = x.detach()
         if dtype is not None and t.dtype != dtype:
             t = t.to(dtype)
-        return t.to(device).contiguous()
+        # pinned host fields upload asynchronously (one DMA per field, no sync between
+        # them); Scene.__init__ synchronises once after the last one
+        return t.to(device, non_blocking=t.is_pinned()).contiguous()
     a = np.asarray(x)
     if dtype is None:
         dtype = torch.float64 if a.dtype == np.float64 else torch.float32
@@ -113,6 +115,11 @@ class Scene:
         self.raw_opacity_b = _to_tensor(raw_opacity_b, dtype, self.device)
         self.sh_degree = int(sh_degree)
         self.background_color = np.asarray(background_color, dtype=np.float64).reshape(3)
+        srcs = (mu, log_scale, rotation, sh_coeffs, normal, raw_opacity_a, raw_opacity_b)
+        if self.device.type == "cuda" and any(isinstance(x, torch.Tensor) and x.is_pinned()
+                                              for x in srcs):
+            # the caller may reuse its host buffers as soon as the scene exists
+            torch.cuda.current_stream(self.device).synchronize()
         if validate:
             self._validate()
 
