@@ -151,6 +151,11 @@ int hs_blend_bwd(hs_frame* frame, const double* background,
                  const float* d_color, const float* transmittance,
                  const int32_t* terminal, void* stream);
 
+/* Diagnostic: histogram over every (tile, pair) of the blend's strip window
+ * codes (0 none, 1 rows 0-7, 2 rows 8-15, 3 all; hs_blend.cu strip_window).
+ * hist: device array of 4 uint64. */
+int hs_blend_window_stats(hs_frame* frame, unsigned long long* hist, void* stream);
+
 /* K7: merge pair rows per splat and chain to the primitive parameters
  * (GradientSet, rasterizer.py:72-105).  Output pointers are device arrays of
  * the scene dtype (touch_count int32); culled primitives get zeros. */

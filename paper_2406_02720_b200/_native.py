@@ -116,6 +116,7 @@ _SIGNATURES = {
                                c_void_p, c_void_p, c_void_p, c_void_p]),
     "hs_blend_bwd": (c_int32, [ctypes.POINTER(HsFrame), c_double_p, c_void_p, c_void_p,
                                c_void_p, c_void_p]),
+    "hs_blend_window_stats": (c_int32, [ctypes.POINTER(HsFrame), c_void_p, c_void_p]),
     "hs_preprocess_bwd": (c_int32, [ctypes.POINTER(HsFrame), ctypes.POINTER(HsScene),
                                     ctypes.POINTER(HsCamera), ctypes.POINTER(HsGrads), c_void_p]),
     "hs_preprocess_bwd_range": (c_int32, [ctypes.POINTER(HsFrame), ctypes.POINTER(HsScene),

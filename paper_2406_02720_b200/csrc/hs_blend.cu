@@ -18,6 +18,7 @@
 // is exact to ~3e-8 px at any resolution; "steep" splats (see hs_common.cuh)
 // evaluate the erf argument in FP64 from a side record staged with the record.
 #include <cstdint>
+#include <type_traits>
 
 #include <cuda_fp16.h>
 
@@ -45,6 +46,7 @@ __device__ __forceinline__ void cp_async_wait() {
 struct WarpStage {
   float4 rec[2][kBatch][4];
   SteepRec side[2][kBatch];
+  int win[2][kBatch];  // strip window code of each staged splat in the current tile
 };
 
 // Gather the records of `count` (<= 32) pairs, pair j at sorted index
@@ -185,6 +187,76 @@ __device__ __forceinline__ bool fast_flags(uint32_t flags) {
 }
 
 // ---------------------------------------------------------------------------
+// Strip windows.  Strip p of a tile is rows 4p..4p+3, i.e. pixel pair p of every
+// lane.  A splat whose Gaussian is below 2^-27 at every pixel centre of a strip
+// cannot change that strip in FP32: w <= g (u <= max(alpha1, alpha2) < 1), so
+// w T is below half an ulp of T and T (1 - w) rounds to T, every alive pixel
+// still commits (T >= 1e-4 already held), 1 - w rounds to 1 so the backward's
+// T / (1 - w) is T, and the skipped colour, depth and gradient terms are below
+// 2^-27 of their scale per pair.  The fast paths therefore evaluate only the
+// strips the splat reaches (the forward still counts the commit of the others):
+// about a third of the (splat, strip) work at c3-c4 (small splats straddling
+// tile borders).  The reached strips of a convex superlevel set are contiguous;
+// they are evaluated in one of three windows (code 1: pairs 0-1, code 2: pairs
+// 2-3, code 3: all four; code 0: none), which keeps 22 of the 31 points of
+// skippable work at c3 with two extra pair bodies per path (finer windows cost
+// more in instruction-cache misses than they save).
+// The staging lane of each splat computes its code once per tile.  The FP32
+// bound uses 2^-27 against the 2^-25 the argument needs (a factor 4 of margin for
+// its own rounding); NaN keeps every strip.
+constexpr int kWinNone = 0;
+constexpr int kWinAll = 3;
+constexpr float kSkipQ = 37.42994775f;  // q = a dx^2 + 2b dx dy + c dy^2 > 54 ln 2  <=>  g < 2^-27
+
+// min over t in [lo, hi] of a X^2 + 2 b X t + c t^2 (c > 0)
+__device__ __forceinline__ float edge_min_q(float a, float b, float c, float X, float lo,
+                                            float hi) {
+  const float t = fminf(fmaxf(__fdividef(-b * X, c), lo), hi);
+  return fmaf(a * X, X, t * fmaf(2.0f * b, X, c * t));
+}
+
+// min of the conic's quadratic form over the box [xl, xh] x [yl, yh] of offsets:
+// 0 if the centre is inside, else the least of the four edge minima (convexity)
+__device__ __forceinline__ float box_min_q(float a, float b, float c, float xl, float xh,
+                                           float yl, float yh) {
+  if (xl <= 0.f && xh >= 0.f && yl <= 0.f && yh >= 0.f) return 0.f;
+  float m = fminf(edge_min_q(a, b, c, xl, yl, yh), edge_min_q(a, b, c, xh, yl, yh));
+  m = fminf(m, edge_min_q(c, b, a, yl, xl, xh));
+  return fminf(m, edge_min_q(c, b, a, yh, xl, xh));
+}
+
+// window code of a staged record (raw conic, before any prescale) in the tile
+// whose first pixel centre is (x0, y0)
+__device__ __forceinline__ int strip_window(const float4 (&q)[4], float x0, float y0) {
+  const float2 lo = __half22float2(*reinterpret_cast<const __half2*>(&q[3].w));
+  const float xl = (x0 - q[0].x) - lo.x, xh = xl + (float)(kTile - 1);
+  const float a = q[0].z, b = q[0].w, c = q[1].x;
+  int first = 4, last = -1;
+#pragma unroll
+  for (int p = 0; p < kPairs; ++p) {
+    const float yl = (y0 + 4.0f * p - q[0].y) - lo.y;
+    if (!(box_min_q(a, b, c, xl, xh, yl, yl + 3.0f) > kSkipQ)) {
+      first = min(first, p);
+      last = p;
+    }
+  }
+  if (last < 0) return kWinNone;
+  if (last <= 1) return 1;
+  if (first >= 2) return 2;
+  return kWinAll;
+}
+
+// calls f(P0, NP) with the window as compile-time constants
+template <typename F>
+__device__ __forceinline__ void with_window(int win, F&& f) {
+  switch (win) {
+    case 1: f(std::integral_constant<int, 0>{}, std::integral_constant<int, 2>{}); break;
+    case 2: f(std::integral_constant<int, 2>{}, std::integral_constant<int, 2>{}); break;
+    default: f(std::integral_constant<int, 0>{}, std::integral_constant<int, 4>{}); break;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // K5 forward.  Each pixel carries T and a 0/1 float "alive" mask A; a splat
 // commits with m = A * [T (1 - w) >= 1e-4], and every update is an exact
 // multiply by m: nw m is -w or 0, so T <- fma(nw m, T, T) is T (1 - w) or T
@@ -218,7 +290,9 @@ __device__ __forceinline__ void fwd_commit(float nw, float& T, float& A, float& 
 
 // FAST: mode 0 or 2, weight provably below the 0.99 clamp; STEEP takes z from
 // the side-record form.
-template <bool STEEP>
+// Pairs [P0, P0 + NP) are evaluated; the others are outside the splat's strip
+// window and only count the commit of their alive pixels (see strip_window).
+template <bool STEEP, int P0 = 0, int NP = kPairs>
 __device__ __forceinline__ void fwd_splat_fast(const float4 (&q)[4], const SteepRec& side,
                                                float px, float py0, FwdPix& P) {
   const SplatLane s = splat_lane<STEEP, true>(q, side, px, py0);
@@ -226,6 +300,10 @@ __device__ __forceinline__ void fwd_splat_fast(const float4 (&q)[4], const Steep
   const float cr = q[2].y, cg = q[2].z, cb = q[2].w, z = q[3].x;
 #pragma unroll
   for (int p = 0; p < kPairs; ++p) {
+    if (p < P0 || p >= P0 + NP) {
+      P.C[p] = fadd2(P.C[p], P.A[p]);
+      continue;
+    }
     const float2 dy = pair_dy(s.dy0, p);
     const float2 g = ex2x2(ffma2(ffma2(f2(s.C), dy, f2(s.Bx)), dy, f2(s.P0)));
     const float2 e = erf32x2(STEEP ? steep_z2(s, p) : ffma2(f2(s.zb), dy, f2(s.Z0)));
@@ -298,6 +376,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) blend_fwd_kernel(
     const int row0 = ty * kTile + (lane >> 4);
     const float px = (float)col + 0.5f;
     const float py0 = (float)row0 + 0.5f;
+    const float x0 = (float)(tx * kTile) + 0.5f, y0 = (float)(ty * kTile) + 0.5f;
     FwdPix P;
 #pragma unroll
     for (int i = 0; i < kPx; ++i) {
@@ -323,7 +402,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) blend_fwd_kernel(
       cp_async_wait<1>();
       __syncwarp();
       const int s = b & 1;
-      if (lane < nb) prescale_record(st.rec[s][lane]);
+      if (lane < nb) {
+        st.win[s][lane] = strip_window(st.rec[s][lane], x0, y0);
+        prescale_record(st.rec[s][lane]);
+      }
       __syncwarp();
       for (int j = 0; j < nb; ++j) {
         // dead pixels never change again: stop once the whole tile is dead
@@ -332,10 +414,21 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) blend_fwd_kernel(
         const float4 q[4] = {st.rec[s][j][0], st.rec[s][j][1], st.rec[s][j][2], st.rec[s][j][3]};
         const uint32_t flags = __float_as_uint(q[3].y);
         if (fast_flags(flags)) {
-          if (flags & kFlagSteep)
-            fwd_splat_fast<true>(q, st.side[s][j], px, py0, P);
-          else
-            fwd_splat_fast<false>(q, st.side[s][j], px, py0, P);
+          const int win = st.win[s][j];
+          if (win == kWinNone) {
+#pragma unroll
+            for (int p = 0; p < kPairs; ++p) P.C[p] = fadd2(P.C[p], P.A[p]);
+          } else if (flags & kFlagSteep) {
+            with_window(win, [&](auto p0, auto np) {
+              fwd_splat_fast<true, decltype(p0)::value, decltype(np)::value>(
+                  q, st.side[s][j], px, py0, P);
+            });
+          } else {
+            with_window(win, [&](auto p0, auto np) {
+              fwd_splat_fast<false, decltype(p0)::value, decltype(np)::value>(
+                  q, st.side[s][j], px, py0, P);
+            });
+          }
         } else
           fwd_splat_generic(q, st.side[s][j], flags, px, py0, P);
       }
@@ -380,7 +473,9 @@ struct BwdPix {
 // of the warp is active at this position (pos < warp-min of the terminal
 // counts); otherwise inactive pixels are masked with selects and contribute
 // exact zeros (pixels terminated early, as in heavily occluded views).
-template <bool ALL, bool STEEP>
+// Pairs [P0, P0 + NP) are evaluated; the others are outside the splat's strip
+// window and unchanged (see strip_window).
+template <bool ALL, bool STEEP, int P0 = 0, int NP = kPairs>
 __device__ __forceinline__ void bwd_splat_fast(const float4 (&q)[4], const SteepRec& side,
                                                int pos, float px, float py0, BwdPix& P,
                                                BwdAcc& out) {
@@ -396,7 +491,7 @@ __device__ __forceinline__ void bwd_splat_fast(const float4 (&q)[4], const Steep
   float2 s0 = f2(0.f), s1 = f2(0.f), s2 = f2(0.f), q0 = f2(0.f), q1 = f2(0.f), qz = f2(0.f);
   float2 a1 = f2(0.f), a2 = f2(0.f), ar = f2(0.f), ag = f2(0.f), ab = f2(0.f);
 #pragma unroll
-  for (int p = 0; p < kPairs; ++p) {
+  for (int p = P0; p < P0 + NP; ++p) {
     const float2 o = make_float2(4.0f * p, 4.0f * p + 2.0f);
     const float2 o2 = make_float2(16.0f * p * p, (4.0f * p + 2.0f) * (4.0f * p + 2.0f));
     const float2 gg = ex2x2(ffma2(ffma2(f2(s.C), o, f2(Lg)), o, f2(Kg)));
@@ -555,6 +650,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) blend_bwd_kernel(
     const int row0 = ty * kTile + (lane >> 4);
     const float px = (float)col + 0.5f;
     const float py0 = (float)row0 + 0.5f;
+    const float x0 = (float)(tx * kTile) + 0.5f, y0 = (float)(ty * kTile) + 0.5f;
     BwdPix P;
     P.cnt = cnt;
     int maxc = 0, minc = 0x7fffffff;
@@ -608,6 +704,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) blend_bwd_kernel(
       cp_async_wait<1>();
       __syncwarp();
       const int s = b & 1;
+      if (lane < nb) st.win[s][lane] = strip_window(st.rec[s][lane], x0, y0);
+      __syncwarp();
       for (int j = 0; j < nb; ++j) {
         const int pos = hi - j;
         const float4 q[4] = {st.rec[s][j][0], st.rec[s][j][1], st.rec[s][j][2], st.rec[s][j][3]};
@@ -615,13 +713,35 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) blend_bwd_kernel(
         const uint32_t flags = __float_as_uint(q[3].y);
         const int mode = (int)(flags & 3u);
         BwdAcc a;
+        size_t row;
+        if (kRowsBySortedPos) {
+          row = (size_t)(k0 + pos);
+        } else {
+          const int spans_x = (int)(flags >> kFlagSpanShift);
+          row = (size_t)((int)__float_as_uint(q[3].z) + ty * spans_x + tx);
+        }
+        const int vi = lane >> 1;
         if (fast_flags(flags)) {
           const bool steep = flags & kFlagSteep;
+          const int win = st.win[s][j];
+          if (win == kWinNone) {
+            // below 2^-27 on the whole tile: a zero pair row, no reduction
+            if (!(lane & 1) && vi < kCols) rows[row * kStride + vi] = 0.f;
+            continue;
+          }
+          // windows on the all-active path only (the common one); the partial
+          // path evaluates every pair, which FP32 makes equivalent (strip_window)
           if (pos < minc) {
             if (steep)
-              bwd_splat_fast<true, true>(q, side, pos, px, py0, P, a);
+              with_window(win, [&](auto p0, auto np) {
+                bwd_splat_fast<true, true, decltype(p0)::value, decltype(np)::value>(
+                    q, side, pos, px, py0, P, a);
+              });
             else
-              bwd_splat_fast<true, false>(q, side, pos, px, py0, P, a);
+              with_window(win, [&](auto p0, auto np) {
+                bwd_splat_fast<true, false, decltype(p0)::value, decltype(np)::value>(
+                    q, side, pos, px, py0, P, a);
+              });
           } else {
             if (steep)
               bwd_splat_fast<false, true>(q, side, pos, px, py0, P, a);
@@ -653,14 +773,6 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) blend_bwd_kernel(
         v[12] = erf_mode ? a.qz : 0.f;
         v[13] = v[14] = v[15] = 0.f;
         const float total = warp_transpose_reduce16(v, lane);
-        size_t row;
-        if (kRowsBySortedPos) {
-          row = (size_t)(k0 + pos);
-        } else {
-          const int spans_x = (int)(flags >> kFlagSpanShift);
-          row = (size_t)((int)__float_as_uint(q[3].z) + ty * spans_x + tx);
-        }
-        const int vi = lane >> 1;
         if (!(lane & 1) && vi < kCols) rows[row * kStride + vi] = total;
       }
       __syncwarp();
@@ -668,6 +780,31 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) blend_bwd_kernel(
     cp_async_wait<0>();
     __syncwarp();
   }
+}
+
+// Diagnostic: histogram of the strip window codes over every (tile, pair).
+__global__ void window_stats_kernel(BlendGeom g, unsigned long long* __restrict__ hist) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= g.n_work) return;
+  const int tile = g.tile_lo + t;
+  const int ty = tile / g.tiles_x, tx = tile - ty * g.tiles_x;
+  const float x0 = (float)(tx * kTile) + 0.5f, y0 = (float)(ty * kTile) + 0.5f;
+  unsigned long long h[4] = {0, 0, 0, 0};
+  for (int k = g.tile_starts[tile]; k < g.tile_starts[tile + 1]; ++k) {
+    const float4* r = g.rec + 4 * (size_t)(g.pair_src[k] & kIndexMask);
+    const float4 q[4] = {r[0], r[1], r[2], r[3]};
+    ++h[strip_window(q, x0, y0)];
+  }
+  for (int i = 0; i < 4; ++i)
+    if (h[i]) atomicAdd(hist + i, h[i]);
+}
+
+cudaError_t launch_window_stats(const BlendGeom& g, unsigned long long* hist, cudaStream_t stream) {
+  cudaError_t e = cudaMemsetAsync(hist, 0, 4 * sizeof(unsigned long long), stream);
+  if (e != cudaSuccess) return e;
+  window_stats_kernel<<<(g.n_work + 127) / 128, 128, 0, stream>>>(g, hist);
+  note_launch();
+  return cudaGetLastError();
 }
 
 // Seam 1: reference packed (M,13) float64 + mode int8 -> records; steep splats

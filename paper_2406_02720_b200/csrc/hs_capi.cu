@@ -408,6 +408,18 @@ int hs_blend_bwd(hs_frame* frame, const double* bg, const float* d_color,
   return HS_OK;
 }
 
+int hs_blend_window_stats(hs_frame* frame, unsigned long long* hist, void* stream_) {
+  int st = check_frame_ws(frame);
+  if (st) return st;
+  if ((st = check_bin_ws(frame))) return st;
+  if (!hist) return HS_ERR_INVALID_ARG;
+  FrameBufs f = carve_frame(frame->frame_ws, frame->n, frame->n_tiles, nullptr);
+  BinBufs b = carve_bin(frame->bin_ws, frame->num_pairs, frame->tile_bits, nullptr);
+  BlendGeom g = frame_geom(frame, f, b);
+  HS_CUDA(launch_window_stats(g, hist, static_cast<cudaStream_t>(stream_)));
+  return HS_OK;
+}
+
 int hs_preprocess_bwd(hs_frame* frame, const hs_scene* scene, const hs_camera* cam,
                       const hs_grads* grads, void* stream_) {
   return hs_preprocess_bwd_range(frame, scene, cam, grads, 0, INT64_MAX, stream_);

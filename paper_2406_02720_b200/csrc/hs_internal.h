@@ -84,6 +84,8 @@ cudaError_t launch_blend_bwd(const BlendGeom& g, float bg0, float bg1, float bg2
                              const float* d_color, const float* trans, const int32_t* terminal,
                              float* rows, int32_t* last_rank, const uint32_t* rank_of,
                              bool rows_by_sorted_pos, cudaStream_t stream);
+// diagnostic: strip window codes (hs_blend.cu strip_window) over all pairs -> hist[4]
+cudaError_t launch_window_stats(const BlendGeom& g, unsigned long long* hist, cudaStream_t stream);
 // Seam 1: reference packed (M,13) f64 + mode -> records + side records; marks
 // steep splats in bit 31 of pair_splat (in place, device copy).
 cudaError_t launch_pack_records(const double* packed, const int8_t* mode, int64_t m,

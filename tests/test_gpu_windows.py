@@ -1,0 +1,88 @@
+"""Strip windows of the blend kernels (hs_blend.cu strip_window): a splat is not
+evaluated on the 16x4-pixel strips of a tile where its Gaussian is below 2^-27,
+which FP32 makes equivalent to evaluating it (T(1 - w) rounds to T).  These tests
+check that the windows are conservative against the exact per-strip maximum of
+the Gaussian (safety threshold 2^-25), that they do skip work, and that images
+and gradients on a scene full of skipped strips match the FP64 oracle."""
+
+import ctypes
+
+import numpy as np
+import pytest
+import torch
+
+from parity import assert_grads, assert_images, GRAD_GROUPS
+from paper_2406_02720_b200 import _native, device, scenes
+from paper_2406_02720_b200.geometry import CameraModel, Scene
+
+pytestmark = pytest.mark.gpu
+
+
+def _scene():
+    # small anisotropic splats: many straddle tile borders with strips they never reach
+    return scenes.frustum(6000, 1, 256, 192, seed=21, sig_lo=0.3, sig_hi=3.0)
+
+
+def _strip_gmax(packed, pair_splat, tile_starts, tiles_x):
+    """Exact max of the Gaussian over each 16x4 strip for every (tile, pair): (P, 4)."""
+    t = np.repeat(np.arange(len(tile_starts) - 1), np.diff(tile_starts))
+    p = packed[pair_splat].astype(np.float64)
+    off = np.arange(16) + 0.5
+    dx = (t % tiles_x)[:, None] * 16 + off[None, :] - p[:, 0:1]
+    dy = (t // tiles_x)[:, None] * 16 + off[None, :] - p[:, 1:2]
+    a, b, c = (p[:, k, None, None] for k in (2, 3, 4))
+    pw = -0.5 * (a * dx[:, None, :] ** 2 + c * dy[:, :, None] ** 2) - b * dx[:, None, :] * dy[:, :, None]
+    return np.exp(pw).reshape(len(p), 4, 64).max(axis=2)
+
+
+def test_windows_conservative_and_effective(cuda):
+    sa = _scene()
+    cam = CameraModel(**sa.cameras[0])
+    sc = Scene(*(getattr(sa, f) for f in sa.FIELDS), sh_degree=sa.sh_degree,
+               background_color=sa.background_color, device="cuda", dtype=torch.float32)
+    fr = device.prepare(sc, cam)
+    hist = torch.zeros(4, dtype=torch.int64, device="cuda")
+    st = _native.load().hs_blend_window_stats(
+        ctypes.byref(fr.st), ctypes.c_void_p(hist.data_ptr()),
+        ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    _native.check(st, "hs_blend_window_stats")
+    none, lower, upper, full = (int(v) for v in hist.cpu())
+    ex = fr.export()
+    g = _strip_gmax(ex["packed"], ex["pair_splat"], ex["tile_starts"], fr.tiles_x)
+    need = g >= 2.0 ** -25          # strips that must be evaluated
+    may_none = ~need.any(1)
+    may_lower = ~need[:, 2:].any(1)  # nothing needed in strips 2-3
+    may_upper = ~need[:, :2].any(1)
+    assert none + lower + upper + full == len(g)
+    assert none <= may_none.sum()
+    assert none + lower <= may_lower.sum()
+    assert none + upper <= may_upper.sum()
+    # and effective: everything a 2^-30 criterion skips is skipped (the kernel's bound
+    # sits at 2^-27, a factor 8 inside)
+    strict = g >= 2.0 ** -30
+    assert none >= (~strict.any(1)).sum() > 0
+    assert none + lower >= (~strict[:, 2:].any(1)).sum()
+    assert none + upper >= (~strict[:, :2].any(1)).sum()
+    assert lower > 0 and upper > 0
+
+
+def test_windowed_scene_matches_oracle(cuda):
+    from oracle import oracle as O
+    sa = _scene()
+    cam = CameraModel(**sa.cameras[0])
+    d_color = scenes.cotangent(cam.height, cam.width, seed=2)
+    s64 = sa.as_float64()
+    ref = O.render(s64, cam)
+    ref_g = O.render_backward(s64, cam, ref, d_color)
+    sc = Scene(*(getattr(sa, f) for f in sa.FIELDS), sh_degree=sa.sh_degree,
+               background_color=sa.background_color, device="cuda", dtype=torch.float32)
+    out = device.render(sc, cam)
+    got = {"color": out.color.cpu().numpy(), "alpha": out.alpha.cpu().numpy(),
+           "depth": out.depth.cpu().numpy(), "transmittance": out.transmittance.cpu().numpy(),
+           "terminal": out.terminal.cpu().numpy()}
+    assert_images(got, {"color": ref.color, "alpha": ref.alpha, "depth": ref.depth,
+                        "transmittance": ref.transmittance,
+                        "terminal": ref.per_pixel_terminal_index})
+    g = device.render_backward(sc, cam, out, torch.as_tensor(d_color, dtype=torch.float32))
+    assert_grads({k: getattr(g, k).double().cpu().numpy() for k in GRAD_GROUPS},
+                 {k: ref_g[k] for k in GRAD_GROUPS})
