@@ -90,39 +90,93 @@ __device__ __forceinline__ void sh_basis(const double d[3], int deg, double* out
   }
 }
 
-// d basis / d direction, sh.py:64-98; g is (K,3) row-major.
-__device__ __forceinline__ void sh_basis_grad(const double d[3], int deg, double* g) {
-  const double SH_C1 = 0.4886025119029199;
-  const double x = d[0], y = d[1], z = d[2];
-  const int k = (deg + 1) * (deg + 1);
-  for (int i = 0; i < 3 * k; ++i) g[i] = 0.0;
-  if (deg >= 1) {
-    g[1 * 3 + 1] = -SH_C1;
-    g[2 * 3 + 2] = SH_C1;
-    g[3 * 3 + 0] = -SH_C1;
+// K7's SH backward in FP32 (eval_sh_basis / eval_sh_basis_grad, sh.py:32-98):
+// sh holds the primitive's (K,3) coefficients and is overwritten with d_sh =
+// basis (x) dpre; d_dir = sum_k (sum_ch sh[k,ch] dpre[ch]) d basis_k / d dir.
+template <int DEG, typename E>
+__device__ __forceinline__ void sh_bwd_f32(const float d[3], const float dpre[3], E* sh,
+                                           float d_dir[3]) {
+  constexpr int K = (DEG + 1) * (DEG + 1);
+  const float x = d[0], y = d[1], z = d[2];
+  float b[K];
+  b[0] = 0.28209479177387814f;
+  if (DEG >= 1) {
+    b[1] = -0.4886025119029199f * y;
+    b[2] = 0.4886025119029199f * z;
+    b[3] = -0.4886025119029199f * x;
   }
-  if (deg >= 2) {
-    const double c0 = 1.0925484305920792, c1 = -1.0925484305920792, c2 = 0.31539156525252005,
-                 c3 = -1.0925484305920792, c4 = 0.5462742152960396;
-    g[12] = c0 * y; g[13] = c0 * x; g[14] = 0.0;
-    g[15] = 0.0; g[16] = c1 * z; g[17] = c1 * y;
-    g[18] = c2 * (-2 * x); g[19] = c2 * (-2 * y); g[20] = c2 * (4 * z);
-    g[21] = c3 * z; g[22] = 0.0; g[23] = c3 * x;
-    g[24] = c4 * (2 * x); g[25] = c4 * (-2 * y); g[26] = 0.0;
+  const float xx = x * x, yy = y * y, zz = z * z;
+  if (DEG >= 2) {
+    b[4] = 1.0925484305920792f * x * y;
+    b[5] = -1.0925484305920792f * y * z;
+    b[6] = 0.31539156525252005f * (2.0f * zz - xx - yy);
+    b[7] = -1.0925484305920792f * x * z;
+    b[8] = 0.5462742152960396f * (xx - yy);
   }
-  if (deg >= 3) {
-    const double xx = x * x, yy = y * y, zz = z * z;
-    const double e0 = -0.5900435899266435, e1 = 2.890611442640554, e2 = -0.4570457994644658,
-                 e3 = 0.3731763325901154, e4 = -0.4570457994644658, e5 = 1.445305721320277,
-                 e6 = -0.5900435899266435;
-    g[27] = e0 * (6 * x * y); g[28] = e0 * (3 * xx - 3 * yy); g[29] = 0.0;
-    g[30] = e1 * (y * z); g[31] = e1 * (x * z); g[32] = e1 * (x * y);
-    g[33] = e2 * (-2 * x * y); g[34] = e2 * (4 * zz - xx - 3 * yy); g[35] = e2 * (8 * y * z);
-    g[36] = e3 * (-6 * x * z); g[37] = e3 * (-6 * y * z); g[38] = e3 * (6 * zz - 3 * xx - 3 * yy);
-    g[39] = e4 * (4 * zz - 3 * xx - yy); g[40] = e4 * (-2 * x * y); g[41] = e4 * (8 * x * z);
-    g[42] = e5 * (2 * x * z); g[43] = e5 * (-2 * y * z); g[44] = e5 * (xx - yy);
-    g[45] = e6 * (3 * xx - 3 * yy); g[46] = e6 * (-6 * x * y); g[47] = 0.0;
+  if (DEG >= 3) {
+    b[9] = -0.5900435899266435f * y * (3.0f * xx - yy);
+    b[10] = 2.890611442640554f * x * y * z;
+    b[11] = -0.4570457994644658f * y * (4.0f * zz - xx - yy);
+    b[12] = 0.3731763325901154f * z * (2.0f * zz - 3.0f * xx - 3.0f * yy);
+    b[13] = -0.4570457994644658f * x * (4.0f * zz - xx - yy);
+    b[14] = 1.445305721320277f * z * (xx - yy);
+    b[15] = -0.5900435899266435f * x * (xx - 3.0f * yy);
   }
+  float db[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    db[k] = (float)sh[3 * k] * dpre[0] + (float)sh[3 * k + 1] * dpre[1] +
+            (float)sh[3 * k + 2] * dpre[2];
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) sh[3 * k + ch] = E(b[k] * dpre[ch]);
+  }
+  float gx = 0.f, gy = 0.f, gz = 0.f;
+  if (DEG >= 1) {
+    const float c1 = 0.4886025119029199f;
+    gy -= c1 * db[1];
+    gz += c1 * db[2];
+    gx -= c1 * db[3];
+  }
+  if (DEG >= 2) {
+    const float c0 = 1.0925484305920792f, c2 = 0.31539156525252005f, c4 = 0.5462742152960396f;
+    gx += c0 * y * db[4];
+    gy += c0 * x * db[4];
+    gy -= c0 * z * db[5];
+    gz -= c0 * y * db[5];
+    gx += c2 * (-2.0f * x) * db[6];
+    gy += c2 * (-2.0f * y) * db[6];
+    gz += c2 * (4.0f * z) * db[6];
+    gx -= c0 * z * db[7];
+    gz -= c0 * x * db[7];
+    gx += c4 * (2.0f * x) * db[8];
+    gy += c4 * (-2.0f * y) * db[8];
+  }
+  if (DEG >= 3) {
+    const float e0 = -0.5900435899266435f, e1 = 2.890611442640554f, e2 = -0.4570457994644658f,
+                e3 = 0.3731763325901154f, e5 = 1.445305721320277f;
+    gx += e0 * (6.0f * x * y) * db[9];
+    gy += e0 * (3.0f * xx - 3.0f * yy) * db[9];
+    gx += e1 * (y * z) * db[10];
+    gy += e1 * (x * z) * db[10];
+    gz += e1 * (x * y) * db[10];
+    gx += e2 * (-2.0f * x * y) * db[11];
+    gy += e2 * (4.0f * zz - xx - 3.0f * yy) * db[11];
+    gz += e2 * (8.0f * y * z) * db[11];
+    gx += e3 * (-6.0f * x * z) * db[12];
+    gy += e3 * (-6.0f * y * z) * db[12];
+    gz += e3 * (6.0f * zz - 3.0f * xx - 3.0f * yy) * db[12];
+    gx += e2 * (4.0f * zz - 3.0f * xx - yy) * db[13];
+    gy += e2 * (-2.0f * x * y) * db[13];
+    gz += e2 * (8.0f * x * z) * db[13];
+    gx += e5 * (2.0f * x * z) * db[14];
+    gy += e5 * (-2.0f * y * z) * db[14];
+    gz += e5 * (xx - yy) * db[14];
+    gx += e0 * (3.0f * xx - 3.0f * yy) * db[15];
+    gy += e0 * (-6.0f * x * y) * db[15];
+  }
+  d_dir[0] = gx;
+  d_dir[1] = gy;
+  d_dir[2] = gz;
 }
 
 // einsum("ab,nbc,dc->nad") / ("nab,nbc,ndc->nad"): sequential over b then c,
@@ -253,6 +307,9 @@ __device__ __forceinline__ void forward_state(const Src& src, const CamArgs& cam
   st.b = st.cray[1];
   st.c = st.cray[4] + kLowpass;
   st.det = st.a * st.c - st.b * st.b;
+  if (kReplay) {
+    st.visible = true;  // K7 needs neither the radius nor the rect
+  } else {
   const double mid = 0.5 * (st.a + st.c);
   const double lam = mid + sqrt(fmax(mid * mid - st.det, 0.0));
   st.radius = kRadiusSigmas * sqrt(fmax(lam, 0.0));
@@ -261,13 +318,14 @@ __device__ __forceinline__ void forward_state(const Src& src, const CamArgs& cam
   long long y0 = to_i64_numpy(ceil(st.muy - st.radius - 0.5));
   long long y1 = to_i64_numpy(floor(st.muy + st.radius - 0.5));
   const long long W1 = cam.width - 1, H1 = cam.height - 1;
-  st.visible = kReplay || ((x1 >= 0) && (x0 <= W1) && (y1 >= 0) && (y0 <= H1) && (x1 >= x0) &&
+  st.visible = ((x1 >= 0) && (x0 <= W1) && (y1 >= 0) && (y0 <= H1) && (x1 >= x0) &&
                            (y1 >= y0) && (st.det > 0.0));
   if (!st.visible) return;
   st.px0 = x0 < 0 ? 0 : (x0 > W1 ? W1 : x0);  // np.clip, rasterizer.py:225-228
   st.px1 = x1 < 0 ? 0 : (x1 > W1 ? W1 : x1);
   st.py0 = y0 < 0 ? 0 : (y0 > H1 ? H1 : y0);
   st.py1 = y1 < 0 ? 0 : (y1 > H1 ? H1 : y1);
+  }
   // whitening: chol3_batch on the undilated ray covariance (geometry.py:126-160)
   {
     const double* A = st.cray;
@@ -343,13 +401,17 @@ __device__ __forceinline__ void forward_state(const Src& src, const CamArgs& cam
   double vv[3] = {m0 - cam.center[0], m1 - cam.center[1], m2 - cam.center[2]};
   st.vdist = sqrt(vv[0] * vv[0] + vv[1] * vv[1] + vv[2] * vv[2]);
   for (int k = 0; k < 3; ++k) st.vdir[k] = vv[k] / st.vdist;
-  sh_basis(st.vdir, DEG, st.basis);
+  // K7 takes the colour clamp from the record (merge_rows_kernel) and evaluates
+  // the basis in FP32 (sh_bwd_f32)
+  if (!kReplay) {
+    sh_basis(st.vdir, DEG, st.basis);
 #pragma unroll
-  for (int ch = 0; ch < 3; ++ch) {
-    double acc = 0.0;
+    for (int ch = 0; ch < 3; ++ch) {
+      double acc = 0.0;
 #pragma unroll
-    for (int k = 0; k < K; ++k) acc += st.basis[k] * src.sh(k, ch);
-    st.rgbu[ch] = acc + 0.5;
+      for (int k = 0; k < K; ++k) acc += st.basis[k] * src.sh(k, ch);
+      st.rgbu[ch] = acc + 0.5;
+    }
   }
 }
 
@@ -489,7 +551,7 @@ __global__ void __launch_bounds__(256) merge_rows_kernel(
   for (int k = 0; k < 13; ++k) m[k] = 0.0;
   const int4 rc = rect[i];
   const int spans_x = rc.y - rc.x + 1;
-  const float4 r3 = rec[4 * i + 3];
+  const float4 r2 = rec[4 * i + 2], r3 = rec[4 * i + 3];
   const int base = __float_as_int(r3.z) + rc.z * spans_x + rc.x;
   const int r = (int)rank_of[i];
   int lx = 0, ly = 0;
@@ -507,6 +569,12 @@ __global__ void __launch_bounds__(256) merge_rows_kernel(
     m[8] += u2.x; m[9] += u2.y; m[10] += u2.z; m[11] += u2.w;
     m[12] += u3.x;
   }
+  // colour clamp (rasterizer.py:544): the record holds max(rgb, 0), which is > 0
+  // exactly when the unclamped FP64 colour is, so the gradient of a clamped
+  // channel is dropped here and K7 does not re-evaluate the colour
+  if (!(r2.y > 0.f)) m[9] = 0.0;
+  if (!(r2.z > 0.f)) m[10] = 0.0;
+  if (!(r2.w > 0.f)) m[11] = 0.0;
   float4* dst = merged + 4 * i;
   dst[0] = make_float4((float)m[0], (float)m[1], (float)m[2], (float)m[3]);
   dst[1] = make_float4((float)m[4], (float)m[5], (float)m[6], (float)m[7]);
@@ -703,26 +771,21 @@ __device__ __forceinline__ void preprocess_bwd_one(
   }
   double d_mu[3];
   for (int a = 0; a < 3; ++a) d_mu[a] = d_t[0] * Wr[a] + d_t[1] * Wr[3 + a] + d_t[2] * Wr[6 + a];
-  // spherical harmonics colour, clamped at zero (rasterizer.py:543-552)
+  // spherical harmonics colour, clamped at zero (rasterizer.py:543-552): the
+  // clamp is already applied to d_rgb (merge_rows_kernel); well conditioned, so
+  // FP32 (sh_bwd_f32); only the direction's normalisation is chained in FP64
   {
-    double dpre[3];
-    for (int ch = 0; ch < 3; ++ch) dpre[ch] = st.rgbu[ch] > 0.0 ? d_rgb[ch] : 0.0;
+    const float dpre[3] = {(float)d_rgb[0], (float)d_rgb[1], (float)d_rgb[2]};
+    const float dirf[3] = {(float)st.vdir[0], (float)st.vdir[1], (float)st.vdir[2]};
+    float d_dir[3];
+    // d_sh overwrites this thread's staged SH row (read first for d_basis)
+    sh_bwd_f32<DEG>(dirf, dpre, sm.sh + t * St::SHS, d_dir);
     if (DEG > 0) {
-      double g[48];
-      sh_basis_grad(st.vdir, DEG, g);
-      double d_dir[3] = {0.0, 0.0, 0.0};
-      for (int k = 0; k < K; ++k) {
-        double db = 0.0;
-        for (int ch = 0; ch < 3; ++ch) db += (double)sm.sh[t * St::SHS + 3 * k + ch] * dpre[ch];
-        for (int d = 0; d < 3; ++d) d_dir[d] += db * g[3 * k + d];
-      }
-      const double dot = d_dir[0] * st.vdir[0] + d_dir[1] * st.vdir[1] + d_dir[2] * st.vdir[2];
+      const double dd[3] = {d_dir[0], d_dir[1], d_dir[2]};
+      const double dot = dd[0] * st.vdir[0] + dd[1] * st.vdir[1] + dd[2] * st.vdir[2];
       const double rv = 1.0 / st.vdist;
-      for (int d = 0; d < 3; ++d) d_mu[d] += (d_dir[d] - dot * st.vdir[d]) * rv;
+      for (int d = 0; d < 3; ++d) d_mu[d] += (dd[d] - dot * st.vdir[d]) * rv;
     }
-    // d_sh overwrites this thread's staged SH row (read above for d_basis)
-    for (int k = 0; k < K; ++k)
-      for (int ch = 0; ch < 3; ++ch) sm.sh[t * St::SHS + 3 * k + ch] = T(st.basis[k] * dpre[ch]);
   }
   // covariance build: cov = M M^T, M = R diag(s) (rasterizer.py:555-562)
   {
