@@ -219,6 +219,24 @@ def committed_traffic(kernel):
     return {"bytes_per_launch": tot, "source": os.path.relpath(files[-1], REPO)}
 
 
+def window_work(lib, frame, achieved, peak):
+    """The blends skip (tile, splat, strip) work that FP32 cannot see (strip windows,
+    DESIGN.md 3); `achieved` counts the reference's evaluations, this the executed ones."""
+    import ctypes
+    import torch
+    from paper_2406_02720_b200 import _native
+    hist = torch.zeros(4, dtype=torch.int64, device="cuda")
+    _native.check(lib.hs_blend_window_stats(ctypes.byref(frame.st),
+                                            ctypes.c_void_p(hist.data_ptr()),
+                                            ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)),
+                  "hs_blend_window_stats")
+    h = [int(v) for v in hist.cpu()]
+    tot = max(1, sum(h))
+    kept = (2 * h[1] + 2 * h[2] + 4 * h[3]) / (4 * tot)
+    return {"pairs_none_lower_upper_all": h, "pair_work_kept": kept,
+            "executed_tflops": achieved * kept, "executed_frac": achieved * kept / peak}
+
+
 def metric_name(cfg):
     if cfg == "c3":
         return "fwd+bwd iters/s (1M half-Gaussians, 1080p)"
@@ -426,6 +444,7 @@ def main():
         "ex2_gops_peak": b.value,
         "fma2_tflops_peak": lib.hs_last_fma2_tflops(),
         "hbm_stages": hbm_stages,
+        "windows": window_work(lib, out.frame, achieved, fp32_peak),
     }
 
     # end-to-end through the drop-in numpy API, host buffers, copies inside

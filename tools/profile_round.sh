@@ -2,11 +2,14 @@
 # Launch list + full ncu captures of every kernel family for profiles/ (one GPU).
 set -u
 mkdir -p gpurun_out
+timeout 900 python bench.py --steps 20 --warmup 3 > gpurun_out/bench_full.log 2>&1
+echo "bench=$?" > gpurun_out/status.txt
+timeout 300 python tools/window_stats.py c3 > gpurun_out/window_stats.txt 2>&1
 CMD="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-clocks"
 timeout 300 $CMD > gpurun_out/plain.log 2>&1 || { echo "plain run failed"; exit 1; }
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
   --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_list.log 2>&1
-echo "list=$?" > gpurun_out/status.txt
+echo "list=$?" >> gpurun_out/status.txt
 for K in blend_bwd blend_fwd preprocess_bwd preprocess_fwd merge_rows duplicate \
          loss_stats loss_grad adam_kernel; do
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$K -s 3 -c 1 \
