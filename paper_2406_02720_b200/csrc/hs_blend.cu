@@ -27,7 +27,36 @@
 
 namespace hs {
 
-constexpr int kWarpsPerCta = 4;
+// Warps per CTA and the minimum resident CTAs per SM (a register cap) of each
+// blend.  One-warp CTAs (each warp is independent: its own tile queue pulls,
+// staging and shared memory) let the SM fill to the register limit exactly:
+// K5 at 126 registers runs 16 warps/SM, K6 at 149 runs 13 (4-warp CTAs: 16 and
+// 12).  Measured on c3: K5 0.856 -> 0.840 ms, K6 1.693 -> 1.651 ms
+// (tools/build_variant.sh + tools/variant_bench.sh).  MINB 0 = no cap.
+#ifndef HS_FWD_WARPS
+#define HS_FWD_WARPS 1
+#endif
+#ifndef HS_FWD_MINB
+#define HS_FWD_MINB 16
+#endif
+#ifndef HS_BWD_WARPS
+#define HS_BWD_WARPS 1
+#endif
+#ifndef HS_BWD_MINB
+#define HS_BWD_MINB 12
+#endif
+constexpr int kFwdWarps = HS_FWD_WARPS;
+constexpr int kBwdWarps = HS_BWD_WARPS;
+#if HS_FWD_MINB > 0
+#define HS_FWD_BOUNDS __launch_bounds__(kFwdWarps * 32, HS_FWD_MINB)
+#else
+#define HS_FWD_BOUNDS __launch_bounds__(kFwdWarps * 32)
+#endif
+#if HS_BWD_MINB > 0
+#define HS_BWD_BOUNDS __launch_bounds__(kBwdWarps * 32, HS_BWD_MINB)
+#else
+#define HS_BWD_BOUNDS __launch_bounds__(kBwdWarps * 32)
+#endif
 constexpr int kBatch = 32;
 constexpr int kPx = 8;  // pixels per lane
 constexpr float kNegHalfLog2e = -0.5f * kLog2e;
@@ -361,11 +390,11 @@ __device__ __forceinline__ bool warp_any_alive(const FwdPix& P) {
   return __any_sync(0xffffffffu, m > 0.0f);
 }
 
-__global__ void __launch_bounds__(kWarpsPerCta * 32) blend_fwd_kernel(
+__global__ void HS_FWD_BOUNDS blend_fwd_kernel(
     BlendGeom g, float bg0, float bg1, float bg2, float* __restrict__ color,
     float* __restrict__ alpha, float* __restrict__ depth, float* __restrict__ trans,
     int32_t* __restrict__ terminal) {
-  __shared__ WarpStage stage_all[kWarpsPerCta];
+  __shared__ WarpStage stage_all[kFwdWarps];
   const int lane = threadIdx.x & 31;
   WarpStage& st = stage_all[threadIdx.x >> 5];
   for (;;) {
@@ -630,15 +659,15 @@ __device__ __forceinline__ float warp_transpose_reduce16(float (&v)[16], int lan
 // columns).  Otherwise the generation-order layout: row = record origin +
 // ty*spans_x + tx, kRowFloats columns, consumed by K7.
 template <bool kRowsBySortedPos>
-__global__ void __launch_bounds__(kWarpsPerCta * 32) blend_bwd_kernel(
+__global__ void HS_BWD_BOUNDS blend_bwd_kernel(
     BlendGeom g, float bg0, float bg1, float bg2, const float* __restrict__ d_color,
     const float* __restrict__ trans, const int32_t* __restrict__ terminal,
     float* __restrict__ rows, int32_t* __restrict__ last_rank,
     const uint32_t* __restrict__ rank_of) {
   constexpr int kStride = kRowsBySortedPos ? 12 : kRowFloats;
   constexpr int kCols = kRowsBySortedPos ? 12 : 13;
-  __shared__ WarpStage stage_all[kWarpsPerCta];
-  __shared__ int cnt_all[kWarpsPerCta][kPx][32];
+  __shared__ WarpStage stage_all[kBwdWarps];
+  __shared__ int cnt_all[kBwdWarps][kPx][32];
   const int lane = threadIdx.x & 31;
   WarpStage& st = stage_all[threadIdx.x >> 5];
   int* cnt = &cnt_all[threadIdx.x >> 5][0][lane];
@@ -843,15 +872,15 @@ __global__ void mark_steep_pairs_kernel(const uint8_t* __restrict__ steep_flag,
 
 // Persistent grid: resident CTAs per SM x SMs of that kernel (queried once).
 template <typename Kernel>
-static int blend_grid(Kernel kernel, int n_work, int* cache) {
+static int blend_grid(Kernel kernel, int warps, int n_work, int* cache) {
   if (*cache == 0) {
     int dev = 0, sms = 148, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kWarpsPerCta * 32, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, warps * 32, 0);
     *cache = sms * (per_sm < 1 ? 1 : per_sm);
   }
-  const int want = (n_work + kWarpsPerCta - 1) / kWarpsPerCta;
+  const int want = (n_work + warps - 1) / warps;
   return want < *cache ? (want > 0 ? want : 1) : *cache;
 }
 static int g_fwd_grid = 0, g_bwd_grid[2] = {0, 0};
@@ -861,7 +890,7 @@ cudaError_t launch_blend_fwd(const BlendGeom& g, float bg0, float bg1, float bg2
                              cudaStream_t stream) {
   cudaError_t e = cudaMemsetAsync(g.work_counter, 0, sizeof(int), stream);
   if (e != cudaSuccess) return e;
-  blend_fwd_kernel<<<blend_grid(blend_fwd_kernel, g.n_work, &g_fwd_grid), kWarpsPerCta * 32, 0,
+  blend_fwd_kernel<<<blend_grid(blend_fwd_kernel, kFwdWarps, g.n_work, &g_fwd_grid), kFwdWarps * 32, 0,
                      stream>>>(
       g, bg0, bg1, bg2, color, alpha, depth, trans, terminal);
   note_launch();
@@ -875,12 +904,12 @@ cudaError_t launch_blend_bwd(const BlendGeom& g, float bg0, float bg1, float bg2
   cudaError_t e = cudaMemsetAsync(g.work_counter, 0, sizeof(int), stream);
   if (e != cudaSuccess) return e;
   if (rows_by_sorted_pos)
-    blend_bwd_kernel<true><<<blend_grid(blend_bwd_kernel<true>, g.n_work, &g_bwd_grid[1]),
-                             kWarpsPerCta * 32, 0, stream>>>(
+    blend_bwd_kernel<true><<<blend_grid(blend_bwd_kernel<true>, kBwdWarps, g.n_work, &g_bwd_grid[1]),
+                             kBwdWarps * 32, 0, stream>>>(
         g, bg0, bg1, bg2, d_color, trans, terminal, rows, last_rank, rank_of);
   else
-    blend_bwd_kernel<false><<<blend_grid(blend_bwd_kernel<false>, g.n_work, &g_bwd_grid[0]),
-                              kWarpsPerCta * 32, 0, stream>>>(
+    blend_bwd_kernel<false><<<blend_grid(blend_bwd_kernel<false>, kBwdWarps, g.n_work, &g_bwd_grid[0]),
+                              kBwdWarps * 32, 0, stream>>>(
         g, bg0, bg1, bg2, d_color, trans, terminal, rows, last_rank, rank_of);
   note_launch();
   return cudaGetLastError();

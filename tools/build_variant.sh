@@ -1,0 +1,16 @@
+#!/bin/bash
+# Build a variant of the library with extra nvcc -D flags for hs_blend.cu only:
+#   tools/build_variant.sh NAME -DHS_BWD_WARPS=1 -DHS_BWD_MINB=14
+# Output: paper_2406_02720_b200/lib/variants/NAME/libhalfsplat_b200.so (experiments only).
+set -e
+NAME=$1; shift
+R=$(cd "$(dirname "$0")/.." && pwd)
+P=$R/paper_2406_02720_b200
+OUT=$P/lib/variants/$NAME
+mkdir -p $OUT
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC \
+  -I $P/csrc -I $R/include --expt-relaxed-constexpr -Xptxas -v "$@" \
+  -c $P/csrc/hs_blend.cu -o $OUT/hs_blend.o 2> $OUT/ptxas.log
+OBJS=$(ls $P/lib/obj/*.o | grep -v hs_blend.o)
+nvcc -gencode arch=compute_100a,code=sm_100a -shared --cudart static -o $OUT/libhalfsplat_b200.so $OBJS $OUT/hs_blend.o
+grep -A2 "blend_fwd_kernel\|blend_bwd_kernelILb0" $OUT/ptxas.log | grep -E "Used|spill" | sed "s/^/$NAME: /"
