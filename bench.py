@@ -395,6 +395,10 @@ def main():
     end.record()
     barrier()
     fwd_ms = start.elapsed_time(end) / args.steps
+    if world > 1:
+        fwd_t = torch.tensor([fwd_ms], device="cuda")
+        dist.all_reduce(fwd_t, op=dist.ReduceOp.MAX)
+        fwd_ms = float(fwd_t.item())
 
     # algorithmic work of the dominant kernels
     term = out.terminal.to(torch.int64)
