@@ -383,11 +383,13 @@ __device__ __forceinline__ void prescale_record(float4 (&r)[4]) {
   r[2].x = -r[2].x;
 }
 
-__device__ __forceinline__ bool warp_any_alive(const FwdPix& P) {
-  float m = fmaxf(P.A[0].x, P.A[0].y);
-#pragma unroll
-  for (int p = 1; p < kPairs; ++p) m = fmaxf(m, fmaxf(P.A[p].x, P.A[p].y));
-  return __any_sync(0xffffffffu, m > 0.0f);
+// Window mask (strip_window codes are a 2-bit mask: 1 pairs 0-1, 2 pairs 2-3) of
+// the halves of the tile that still have an alive pixel in some lane.  A dead
+// half never changes again, so it joins the windows as skipped work.
+__device__ __forceinline__ int alive_halves(const FwdPix& P) {
+  const float lo = fmaxf(fmaxf(P.A[0].x, P.A[0].y), fmaxf(P.A[1].x, P.A[1].y));
+  const float hi = fmaxf(fmaxf(P.A[2].x, P.A[2].y), fmaxf(P.A[3].x, P.A[3].y));
+  return (__any_sync(0xffffffffu, lo > 0.0f) ? 1 : 0) | (__any_sync(0xffffffffu, hi > 0.0f) ? 2 : 0);
 }
 
 __global__ void HS_FWD_BOUNDS blend_fwd_kernel(
@@ -421,6 +423,7 @@ __global__ void HS_FWD_BOUNDS blend_fwd_kernel(
     auto fwd_pos = [](int j) { return j; };
     if (nk > 0) issue_batch(g, k0, min(kBatch, nk), fwd_pos, st, 0, lane);
     bool any = true;
+    int alive = kWinAll;
     for (int b = 0; b * kBatch < nk && any; ++b) {
       const int nb = min(kBatch, nk - b * kBatch);
       if ((b + 1) * kBatch < nk)
@@ -437,13 +440,17 @@ __global__ void HS_FWD_BOUNDS blend_fwd_kernel(
       }
       __syncwarp();
       for (int j = 0; j < nb; ++j) {
-        // dead pixels never change again: stop once the whole tile is dead
-        // (checked every 8 splats; the reference checks per splat, same result)
-        if ((j & 7) == 0 && !(any = warp_any_alive(P))) break;
+        // dead pixels never change again: stop once the whole tile is dead, skip
+        // a dead half (checked every 8 splats; the reference checks per splat,
+        // same result)
+        if ((j & 7) == 0) {
+          alive = alive_halves(P);
+          if (!(any = alive != 0)) break;
+        }
         const float4 q[4] = {st.rec[s][j][0], st.rec[s][j][1], st.rec[s][j][2], st.rec[s][j][3]};
         const uint32_t flags = __float_as_uint(q[3].y);
         if (fast_flags(flags)) {
-          const int win = st.win[s][j];
+          const int win = st.win[s][j] & alive;
           if (win == kWinNone) {
 #pragma unroll
             for (int p = 0; p < kPairs; ++p) P.C[p] = fadd2(P.C[p], P.A[p]);
@@ -758,8 +765,6 @@ __global__ void HS_BWD_BOUNDS blend_bwd_kernel(
             if (!(lane & 1) && vi < kCols) rows[row * kStride + vi] = 0.f;
             continue;
           }
-          // windows on the all-active path only (the common one); the partial
-          // path evaluates every pair, which FP32 makes equivalent (strip_window)
           if (pos < minc) {
             if (steep)
               with_window(win, [&](auto p0, auto np) {
@@ -772,6 +777,9 @@ __global__ void HS_BWD_BOUNDS blend_bwd_kernel(
                     q, side, pos, px, py0, P, a);
               });
           } else {
+            // partially active warp: every pair.  (Skipping the halves with no active
+            // pixel, or static windows here, won 7% on c4 but lost 2-4% on c3 through
+            // the larger code.)
             if (steep)
               bwd_splat_fast<false, true>(q, side, pos, px, py0, P, a);
             else

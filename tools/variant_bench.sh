@@ -5,7 +5,7 @@ L=paper_2406_02720_b200/lib
 cp $L/libhalfsplat_b200.so /tmp/base.so
 for V in base $VARIANTS; do
   if [ "$V" = base ]; then cp /tmp/base.so $L/libhalfsplat_b200.so; else cp $L/variants/$V/libhalfsplat_b200.so $L/libhalfsplat_b200.so; fi
-  timeout 300 python bench.py --steps 20 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/vb_$V.log 2>&1
+  timeout 600 python bench.py --steps ${STEPS:-20} --warmup 3 --no-e2e --no-cpu-baseline $BENCH_ARGS > gpurun_out/vb_$V.log 2>&1
   echo "== $V" >> gpurun_out/variants.txt
   python tools/show_bench.py gpurun_out/vb_$V.log >> gpurun_out/variants.txt 2>&1
 done
