@@ -132,7 +132,10 @@ size_t hs_binning_workspace_size(int64_t n, int64_t num_pairs, int32_t width,
 int hs_preprocess_fwd(hs_frame* frame, const hs_scene* scene,
                       const hs_camera* cam, int32_t* radii, void* stream);
 
-/* Synchronises `stream` and reads P (the number of (tile, splat) pairs). */
+/* Synchronises `stream` and reads P (the number of (tile, splat) pairs).  The
+ * depth ranks of hs_preprocess_fwd come from a 32-bit sort plus a per-run fixup;
+ * when a depth bucket was too long for the fixup this call redoes them with the
+ * full 64-bit sort before returning, so it must precede every use of the ranks. */
 int hs_frame_read_num_pairs(hs_frame* frame, void* stream);
 
 /* K2 duplicate-with-keys, K3 stable tile sort, K4 tile ranges.  Needs

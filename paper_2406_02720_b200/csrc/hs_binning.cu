@@ -17,10 +17,12 @@
 namespace hs {
 
 size_t depth_sort_temp_bytes(int64_t n) {
-  size_t bytes = 0;
+  size_t bytes = 0, hi = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const uint64_t*)nullptr, (uint64_t*)nullptr,
                                   (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)n, 0, 64);
-  return bytes;
+  cub::DeviceRadixSort::SortPairs(nullptr, hi, (const uint64_t*)nullptr, (uint64_t*)nullptr,
+                                  (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)n, 32, 64);
+  return bytes > hi ? bytes : hi;
 }
 
 size_t scan_temp_bytes(int64_t n) {
@@ -45,6 +47,63 @@ cudaError_t run_depth_sort(void* temp, size_t temp_bytes, const uint64_t* keys_i
                                                   order, (int)n, 0, 64, stream);
   note_launch(9);  // onesweep: histogram + one pass per 8-bit digit
   return e;
+}
+
+// Depth ranks in two steps (the default; run_depth_sort is the fallback).  A
+// stable sort on the upper 32 bits of the f64 depth (4 one-sweep passes instead
+// of 8) leaves splats whose depths share those bits -- a bucket 2^-20 of the
+// depth wide -- in index order; the first thread of each such run then puts the
+// run in full-key order by a stable insertion sort, so equal depths keep index
+// order as np.lexsort's tie-break does.  Runs are short: about one splat per
+// bucket at c3, ~80 in c5's clustered depths.  A run longer than kMaxDepthRun
+// sets *overflow and the host redoes the full 64-bit sort
+// (hs_frame_read_num_pairs).  Culled splats share the key ~0 and are already in
+// index order.
+constexpr int kMaxDepthRun = 512;
+
+__global__ void depth_fixup_kernel(uint64_t* __restrict__ keys, uint32_t* __restrict__ order,
+                                   int64_t n, int* __restrict__ overflow) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const uint32_t hi = (uint32_t)(keys[k] >> 32);
+  if (hi == 0xffffffffu) return;                              // culled
+  if (k > 0 && (uint32_t)(keys[k - 1] >> 32) == hi) return;  // not the first of its run
+  int64_t e = k + 1;
+  while (e < n && (uint32_t)(keys[e] >> 32) == hi) {
+    if (e - k >= kMaxDepthRun) {
+      atomicExch(overflow, 1);
+      return;
+    }
+    ++e;
+  }
+  for (int64_t a = k + 1; a < e; ++a) {
+    const uint64_t ka = keys[a];
+    const uint32_t va = order[a];
+    int64_t b = a - 1;
+    while (b >= k && keys[b] > ka) {
+      keys[b + 1] = keys[b];
+      order[b + 1] = order[b];
+      --b;
+    }
+    keys[b + 1] = ka;
+    order[b + 1] = va;
+  }
+}
+
+cudaError_t run_depth_sort_hi(void* temp, size_t temp_bytes, const uint64_t* keys_in,
+                              uint64_t* keys_out, const uint32_t* vals_in, uint32_t* order,
+                              int64_t n, int* overflow, cudaStream_t stream) {
+  cudaError_t e = cudaMemsetAsync(overflow, 0, sizeof(int), stream);
+  if (e != cudaSuccess) return e;
+  e = cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_in, keys_out, vals_in, order, (int)n,
+                                      32, 64, stream);
+  note_launch(5);
+  if (e != cudaSuccess) return e;
+  const int block = 256;
+  depth_fixup_kernel<<<(unsigned)((n + block - 1) / block), block, 0, stream>>>(keys_out, order, n,
+                                                                               overflow);
+  note_launch();
+  return cudaGetLastError();
 }
 
 __global__ void gather_counts_kernel(const int32_t* __restrict__ count,

@@ -46,6 +46,9 @@ struct Carver {
   }
 };
 
+// counters[]: 0 K5 tile queue, 32 K6 tile queue, 48 depth-fixup overflow flag
+constexpr int kDepthOverflowSlot = 48;
+
 struct FrameBufs {
   float4* rec;
   SteepRec* side;
@@ -320,8 +323,8 @@ int hs_preprocess_fwd(hs_frame* frame, const hs_scene* scene, const hs_camera* c
                                             frame->n, f.rec, f.side, f.rect, f.count, f.dkey_in,
                                             f.dval, radii, stream));
   }
-  HS_CUDA(run_depth_sort(f.temp, f.temp_bytes, f.dkey_in, f.dkey_out, f.dval, f.order, frame->n,
-                         stream));
+  HS_CUDA(run_depth_sort_hi(f.temp, f.temp_bytes, f.dkey_in, f.dkey_out, f.dval, f.order,
+                            frame->n, f.counters + kDepthOverflowSlot, stream));
   HS_CUDA(run_count_scan(f.temp, f.temp_bytes, f.count, f.order, f.cnt_r, f.off_r, f.rank_of,
                          frame->n, stream));
   frame->num_pairs = -1;
@@ -334,9 +337,20 @@ int hs_frame_read_num_pairs(hs_frame* frame, void* stream_) {
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
   FrameBufs f = carve_frame(frame->frame_ws, frame->n, frame->n_tiles, nullptr);
   int32_t p = 0;
+  int overflow = 0;
   HS_CUDA(cudaMemcpyAsync(&p, f.off_r + frame->n, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
+  HS_CUDA(cudaMemcpyAsync(&overflow, f.counters + kDepthOverflowSlot, sizeof(int),
+                          cudaMemcpyDeviceToHost, stream));
   HS_CUDA(cudaStreamSynchronize(stream));
   if (p < 0) return HS_ERR_INVALID_ARG;  // overflowed int32
+  if (overflow) {
+    // a depth bucket held more than the fixup handles (e.g. thousands of equal
+    // depths): redo the ranks with the full 64-bit sort; P is order-independent
+    HS_CUDA(run_depth_sort(f.temp, f.temp_bytes, f.dkey_in, f.dkey_out, f.dval, f.order,
+                           frame->n, stream));
+    HS_CUDA(run_count_scan(f.temp, f.temp_bytes, f.count, f.order, f.cnt_r, f.off_r, f.rank_of,
+                           frame->n, stream));
+  }
   frame->num_pairs = p;
   return HS_OK;
 }
