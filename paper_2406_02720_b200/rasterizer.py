@@ -261,8 +261,18 @@ def _upload_f32(a, device):
     if src.dtype == torch.float32 and src.is_pinned():
         return src.to(device, non_blocking=True)
     stage = torch.empty(src.shape, dtype=torch.float32, pin_memory=True)
-    stage.copy_(src)
-    return stage.to(device, non_blocking=True)
+    dst = torch.empty(src.shape, dtype=torch.float32, device=device)
+    # in row chunks, so the DMA of one chunk overlaps the conversion of the next
+    rows = src.shape[0] if src.dim() else 1
+    step = max(1, -(-rows // UPLOAD_CHUNKS))
+    for r in range(0, rows, step):
+        stage[r:r + step].copy_(src[r:r + step])
+        dst[r:r + step].copy_(stage[r:r + step], non_blocking=True)
+    return dst
+
+
+# row chunks of the host-side conversion + upload in _upload_f32
+UPLOAD_CHUNKS = 4
 
 
 # K7 runs in this many primitive buckets on the drop-in path, so the D2H of each

@@ -26,8 +26,9 @@ for _ in range(2):
     fr = t("prepare", lambda: device.prepare(sc, cam))
     do = t("blend fwd", lambda: device.render(sc, cam, frame=fr))
     host = t("D2H image outputs", lambda: R._to_host([do.color, do.alpha, do.depth, do.transmittance, do.terminal, do.radii]))
-    dcd = t("upload d_color (f64 pageable)", lambda: torch.as_tensor(np.ascontiguousarray(dc)).to("cuda").float())
+    dcd = t("upload d_color (pinned f32 staging)", lambda: R._upload_f32(dc, "cuda"))
     gg = t("backward", lambda: device.render_backward(sc, cam, do, dcd))
     hg = t("D2H grads", lambda: R._to_host([getattr(gg, n) for n in R.GradientSet.NAMES]))
+    t("backward + bucketed D2H", lambda: R._backward_to_host(sc, cam, do, dcd))
     t("full render()", lambda: R.render(hs, cam))
     t("full render+backward", lambda: R.render_backward(hs, cam, R.render(hs, cam), dc))
