@@ -142,6 +142,13 @@ int hs_frame_read_num_pairs(hs_frame* frame, void* stream);
  * frame->bin_ws of hs_binning_workspace_size(...) bytes. */
 int hs_bin_and_sort(hs_frame* frame, void* stream);
 
+/* hs_frame_read_num_pairs followed by hs_bin_and_sort in one call, so the GPU
+ * is not left idle while the caller sizes the binning workspace: with a
+ * frame->bin_ws already large enough (e.g. the previous view's) it bins right
+ * after the sync; otherwise it returns HS_ERR_WORKSPACE with num_pairs set, and
+ * the caller sizes the workspace and calls hs_bin_and_sort. */
+int hs_read_pairs_and_bin(hs_frame* frame, void* stream);
+
 /* K5 forward blend.  Outputs (device, float32 / int32):
  * color (H,W,3), alpha (H,W), depth (H,W), transmittance (H,W), terminal (H,W). */
 int hs_blend_fwd(hs_frame* frame, const double* background, float* color,

@@ -111,6 +111,7 @@ _SIGNATURES = {
     "hs_preprocess_fwd": (c_int32, [ctypes.POINTER(HsFrame), ctypes.POINTER(HsScene),
                                     ctypes.POINTER(HsCamera), c_void_p, c_void_p]),
     "hs_frame_read_num_pairs": (c_int32, [ctypes.POINTER(HsFrame), c_void_p]),
+    "hs_read_pairs_and_bin": (c_int32, [ctypes.POINTER(HsFrame), c_void_p]),
     "hs_bin_and_sort": (c_int32, [ctypes.POINTER(HsFrame), c_void_p]),
     "hs_blend_fwd": (c_int32, [ctypes.POINTER(HsFrame), c_double_p, c_void_p, c_void_p,
                                c_void_p, c_void_p, c_void_p, c_void_p]),

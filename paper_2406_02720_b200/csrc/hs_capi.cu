@@ -355,6 +355,16 @@ int hs_frame_read_num_pairs(hs_frame* frame, void* stream_) {
   return HS_OK;
 }
 
+int hs_read_pairs_and_bin(hs_frame* frame, void* stream_) {
+  int st = hs_frame_read_num_pairs(frame, stream_);
+  if (st) return st;
+  if (!frame->bin_ws ||
+      frame->bin_ws_bytes <
+          hs_binning_workspace_size(frame->n, frame->num_pairs, frame->width, frame->height))
+    return HS_ERR_WORKSPACE;  // P is set: size the workspace, then hs_bin_and_sort
+  return hs_bin_and_sort(frame, stream_);
+}
+
 int hs_bin_and_sort(hs_frame* frame, void* stream_) {
   int st = check_frame_ws(frame);
   if (st) return st;

@@ -5,8 +5,9 @@ reference, but every tensor stays in HBM and every stage is one or more
 sm_100a kernels of libhalfsplat_b200.so:
 
     prepare          hs_preprocess_fwd (K1 + depth-rank sort + count scan),
-                     hs_frame_read_num_pairs (the one host sync: P),
-                     hs_bin_and_sort (K2 duplicate, K3 stable tile sort, K4 ranges)
+                     hs_read_pairs_and_bin (the one host sync: P, then K2 duplicate,
+                     K3 stable tile sort, K4 ranges; hs_bin_and_sort after sizing the
+                     binning workspace when it is too small)
     render           hs_blend_fwd (K5)
     render_backward  hs_blend_bwd (K6) + hs_preprocess_bwd (K7)
 
@@ -130,6 +131,16 @@ class DeviceFrame:
     def tiles_y(self):
         return int(self.st.tiles_y)
 
+    def reuse_binning(self):
+        """Point the frame at whatever binning workspace is already there (the
+        Workspace's, or this frame's) before P is known."""
+        buf = self.ws._bufs.get("bin_ws") if self.ws is not None else self.bin_ws
+        if buf is not None:
+            self.st.bin_ws = buf.data_ptr()
+            self.st.bin_ws_bytes = buf.numel()
+            if self.ws is None:
+                self.bin_ws = buf
+
     def alloc_binning(self):
         lib = self.lib
         nbytes = lib.hs_binning_workspace_size(self.st.n, self.st.num_pairs, self.st.width,
@@ -191,11 +202,15 @@ def prepare(scene, cam, kernel="half", timer=None, ws=None):
         st = lib.hs_preprocess_fwd(ctypes.byref(frame.st), ctypes.byref(sc), ctypes.byref(cs),
                                    _ptr(frame.radii), s)
     _native.check(st, "hs_preprocess_fwd")
-    _native.check(lib.hs_frame_read_num_pairs(ctypes.byref(frame.st), s), "read_num_pairs")
-    frame.alloc_binning()
+    # the one host sync (P).  With the previous view's binning workspace in place the
+    # library bins right after it (no host round trip while the GPU idles).
+    frame.reuse_binning()
     with timer.span("bin_and_sort"):
-        st = lib.hs_bin_and_sort(ctypes.byref(frame.st), s)
-    _native.check(st, "hs_bin_and_sort")
+        st = lib.hs_read_pairs_and_bin(ctypes.byref(frame.st), s)
+        if st == _native.HS_ERR_WORKSPACE:
+            frame.alloc_binning()
+            st = lib.hs_bin_and_sort(ctypes.byref(frame.st), s)
+    _native.check(st, "hs_read_pairs_and_bin")
     return frame
 
 
