@@ -665,7 +665,11 @@ __device__ __forceinline__ float warp_transpose_reduce16(float (&v)[16], int lan
 // kRowsBySortedPos: Seam 1 layout (row k = sorted pair index, 12 reference
 // columns).  Otherwise the generation-order layout: row = record origin +
 // ty*spans_x + tx, kRowFloats columns, consumed by K7.
-template <bool kRowsBySortedPos>
+// kDyn (occluded views, BlendGeom::occluded): the partially-active path also
+// takes windows, masked by the halves that still hold an active pixel (exact:
+// inactive pixels contribute exact zeros).  7% faster on c4, but the extra
+// bodies cost 2-4% on c3, so it is a separate instantiation.
+template <bool kRowsBySortedPos, bool kDyn = false>
 __global__ void HS_BWD_BOUNDS blend_bwd_kernel(
     BlendGeom g, float bg0, float bg1, float bg2, const float* __restrict__ d_color,
     const float* __restrict__ trans, const int32_t* __restrict__ terminal,
@@ -716,6 +720,17 @@ __global__ void HS_BWD_BOUNDS blend_bwd_kernel(
     }
     minc = __reduce_min_sync(0xffffffffu, minc);
     maxc = __reduce_max_sync(0xffffffffu, maxc);
+    // kDyn: per half (pairs 0-1 / 2-3), positions at or past its largest count
+    int hmax_lo = 0, hmax_hi = 0;
+    if (kDyn) {
+#pragma unroll
+      for (int i = 0; i < kPx; ++i) {
+        const int c = cnt[i * 32] == 0x7fffffff ? 0 : cnt[i * 32];
+        if (i < kPx / 2) hmax_lo = max(hmax_lo, c); else hmax_hi = max(hmax_hi, c);
+      }
+      hmax_lo = __reduce_max_sync(0xffffffffu, hmax_lo);
+      hmax_hi = __reduce_max_sync(0xffffffffu, hmax_hi);
+    }
     const int k0 = g.tile_starts[tile];
     if (!kRowsBySortedPos && lane == 0)
       last_rank[tile] =
@@ -776,10 +791,25 @@ __global__ void HS_BWD_BOUNDS blend_bwd_kernel(
                 bwd_splat_fast<true, false, decltype(p0)::value, decltype(np)::value>(
                     q, side, pos, px, py0, P, a);
               });
+          } else if (kDyn) {
+            const int wd = win & ((pos < hmax_lo ? 1 : 0) | (pos < hmax_hi ? 2 : 0));
+            if (wd == kWinNone) {
+              if (!(lane & 1) && vi < kCols) rows[row * kStride + vi] = 0.f;
+              continue;
+            }
+            if (steep)
+              with_window(wd, [&](auto p0, auto np) {
+                bwd_splat_fast<false, true, decltype(p0)::value, decltype(np)::value>(
+                    q, side, pos, px, py0, P, a);
+              });
+            else
+              with_window(wd, [&](auto p0, auto np) {
+                bwd_splat_fast<false, false, decltype(p0)::value, decltype(np)::value>(
+                    q, side, pos, px, py0, P, a);
+              });
           } else {
-            // partially active warp: every pair.  (Skipping the halves with no active
-            // pixel, or static windows here, won 7% on c4 but lost 2-4% on c3 through
-            // the larger code.)
+            // partially active warp: every pair (windows here cost more in code size
+            // than they save unless the view is occluded: kDyn)
             if (steep)
               bwd_splat_fast<false, true>(q, side, pos, px, py0, P, a);
             else
@@ -891,7 +921,7 @@ static int blend_grid(Kernel kernel, int warps, int n_work, int* cache) {
   const int want = (n_work + warps - 1) / warps;
   return want < *cache ? (want > 0 ? want : 1) : *cache;
 }
-static int g_fwd_grid = 0, g_bwd_grid[2] = {0, 0};
+static int g_fwd_grid = 0, g_bwd_grid[3] = {0, 0, 0};
 
 cudaError_t launch_blend_fwd(const BlendGeom& g, float bg0, float bg1, float bg2, float* color,
                              float* alpha, float* depth, float* trans, int32_t* terminal,
@@ -914,6 +944,11 @@ cudaError_t launch_blend_bwd(const BlendGeom& g, float bg0, float bg1, float bg2
   if (rows_by_sorted_pos)
     blend_bwd_kernel<true><<<blend_grid(blend_bwd_kernel<true>, kBwdWarps, g.n_work, &g_bwd_grid[1]),
                              kBwdWarps * 32, 0, stream>>>(
+        g, bg0, bg1, bg2, d_color, trans, terminal, rows, last_rank, rank_of);
+  else if (g.occluded)
+    blend_bwd_kernel<false, true><<<blend_grid(blend_bwd_kernel<false, true>, kBwdWarps, g.n_work,
+                                               &g_bwd_grid[2]),
+                                    kBwdWarps * 32, 0, stream>>>(
         g, bg0, bg1, bg2, d_color, trans, terminal, rows, last_rank, rank_of);
   else
     blend_bwd_kernel<false><<<blend_grid(blend_bwd_kernel<false>, kBwdWarps, g.n_work, &g_bwd_grid[0]),

@@ -86,3 +86,29 @@ def test_windowed_scene_matches_oracle(cuda):
     g = device.render_backward(sc, cam, out, torch.as_tensor(d_color, dtype=torch.float32))
     assert_grads({k: getattr(g, k).double().cpu().numpy() for k in GRAD_GROUPS},
                  {k: ref_g[k] for k in GRAD_GROUPS})
+
+
+def test_occluded_view_matches_oracle(cuda):
+    """Mean tile list above 1000 pairs: K6 takes its occluded instantiation (windows on
+    the partially-active path, masked by the halves that still hold an active pixel)."""
+    from oracle import oracle as O
+    sa = scenes.frustum(6000, 1, 64, 48, seed=8, sig_lo=6.0, sig_hi=24.0)
+    cam = CameraModel(**sa.cameras[0])
+    d_color = scenes.cotangent(cam.height, cam.width, seed=5)
+    s64 = sa.as_float64()
+    ref = O.render(s64, cam)
+    ref_g = O.render_backward(s64, cam, ref, d_color)
+    assert ref.frame.pair_splat.shape[0] > 1000 * (len(ref.frame.tile_starts) - 1)
+    assert (ref.per_pixel_terminal_index < np.diff(ref.frame.tile_starts).max()).mean() > 0.5
+    sc = Scene(*(getattr(sa, f) for f in sa.FIELDS), sh_degree=sa.sh_degree,
+               background_color=sa.background_color, device="cuda", dtype=torch.float32)
+    out = device.render(sc, cam)
+    got = {"color": out.color.cpu().numpy(), "alpha": out.alpha.cpu().numpy(),
+           "depth": out.depth.cpu().numpy(), "transmittance": out.transmittance.cpu().numpy(),
+           "terminal": out.terminal.cpu().numpy()}
+    assert_images(got, {"color": ref.color, "alpha": ref.alpha, "depth": ref.depth,
+                        "transmittance": ref.transmittance,
+                        "terminal": ref.per_pixel_terminal_index})
+    g = device.render_backward(sc, cam, out, torch.as_tensor(d_color, dtype=torch.float32))
+    assert_grads({k: getattr(g, k).double().cpu().numpy() for k in GRAD_GROUPS},
+                 {k: ref_g[k] for k in GRAD_GROUPS})
