@@ -58,6 +58,68 @@ def parse():
     return ap.parse_args()
 
 
+class NvmlClockSampler:
+    """SM clock and clock-event reasons read through NVML every ~2 ms on a thread
+    (nvidia-smi's 50 ms loop sees one or two samples of a short timed region)."""
+
+    REASONS = {"hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
+               "hw_thermal_slowdown": "nvmlClocksEventReasonHwThermalSlowdown",
+               "sw_thermal_slowdown": "nvmlClocksEventReasonSwThermalSlowdown",
+               "sw_power_cap": "nvmlClocksEventReasonSwPowerCap"}
+
+    def __init__(self, cuda_index):
+        import threading
+        import pynvml
+        import torch
+        self.nv = pynvml
+        pynvml.nvmlInit()
+        uuid = str(torch.cuda.get_device_properties(cuda_index).uuid)
+        uuid = uuid if uuid.startswith("GPU-") else "GPU-" + uuid
+        self.h = pynvml.nvmlDeviceGetHandleByUUID(uuid)
+        self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        self.masks = {k: getattr(pynvml, v) for k, v in self.REASONS.items()}
+        self.samples = []
+        self.stop_flag = threading.Event()
+        self.thread = threading.Thread(target=self._run, daemon=True)
+        self.thread.start()
+
+    def _run(self):
+        nv = self.nv
+        while not self.stop_flag.is_set():
+            t = time.time()
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except nv.NVMLError:
+                break
+            self.samples.append((t, sm, r))
+            time.sleep(0.002)
+
+    def mark(self, which):
+        setattr(self, which, time.time())
+
+    def stop(self):
+        self.stop_flag.set()
+        self.thread.join(timeout=5)
+        t0, t1 = getattr(self, "t_start", 0.0), getattr(self, "t_end", 1e30)
+        win = [(sm, r) for t, sm, r in self.samples if t0 <= t <= t1]
+        if not win:
+            return None
+        reasons = sorted(k for k, m in self.masks.items() if any(r & m for _, r in win))
+        return {"sm_mhz": statistics.median(sm for sm, _ in win), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(win), "source": "nvml, 2 ms period"}
+
+
+def clock_sampler(gpu_index, enabled=True):
+    """NVML sampler when available, else the nvidia-smi loop."""
+    if enabled:
+        try:
+            return NvmlClockSampler(gpu_index)
+        except Exception:  # no pynvml / NVML: fall back
+            pass
+    return ClockSampler(gpu_index, enabled)
+
+
 class ClockSampler:
     """nvidia-smi clocks/throttle reasons sampled during the timed region."""
 
@@ -362,7 +424,7 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
-    clocks = ClockSampler(local, enabled=not args.no_clocks)
+    clocks = clock_sampler(local, enabled=not args.no_clocks)
     for _ in range(max(args.warmup, 3)):
         step()
     barrier()
