@@ -555,6 +555,10 @@ def main():
     end.record()
     barrier()
     train_ms = start.elapsed_time(end) / args.steps
+    if world > 1:
+        train_t = torch.tensor([train_ms], device="cuda")
+        dist.all_reduce(train_t, op=dist.ReduceOp.MAX)
+        train_ms = float(train_t.item())
     loss_ms = statistics.mean(loss_timer.totals().get("loss", [float("nan")]))
     adam_ms = statistics.mean(loss_timer.totals().get("adam", [float("nan")]))
     # one density-control event on the accumulated statistics (plan + host sync + apply),
