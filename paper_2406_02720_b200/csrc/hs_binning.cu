@@ -52,47 +52,62 @@ cudaError_t run_depth_sort(void* temp, size_t temp_bytes, const uint64_t* keys_i
 // Depth ranks in two steps (the default; run_depth_sort is the fallback).  A
 // stable sort on the upper 32 bits of the f64 depth (4 one-sweep passes instead
 // of 8) leaves splats whose depths share those bits -- a bucket 2^-20 of the
-// depth wide -- in index order; the first thread of each such run then puts the
-// run in full-key order by a stable insertion sort, so equal depths keep index
-// order as np.lexsort's tie-break does.  Runs are short: about one splat per
-// bucket at c3, ~80 in c5's clustered depths.  A run longer than kMaxDepthRun
-// sets *overflow and the host redoes the full 64-bit sort
+// depth wide -- in index order.  Each such run is then put in full-key order:
+// every element counts the run's elements that precede it in (full key, current
+// position) order -- its rank in the run, a stable order, so equal depths keep
+// index order as np.lexsort's tie-break does -- and a second kernel scatters the
+// run into those ranks.  Runs are about one splat long at c3 and ~200 in c5's
+// clustered depths (O(run) work per element, all in parallel).  A run longer
+// than kMaxDepthRun sets *overflow and the host redoes the full 64-bit sort
 // (hs_frame_read_num_pairs).  Culled splats share the key ~0 and are already in
 // index order.
-constexpr int kMaxDepthRun = 512;
+#ifndef HS_MAX_DEPTH_RUN
+#define HS_MAX_DEPTH_RUN 2048
+#endif
+constexpr int kMaxDepthRun = HS_MAX_DEPTH_RUN;
 
-__global__ void depth_fixup_kernel(uint64_t* __restrict__ keys, uint32_t* __restrict__ order,
-                                   int64_t n, int* __restrict__ overflow) {
+// newpos[k] = position of sorted element k after its run is ordered by the full
+// key; val[k] = its order value (copied, so the scatter does not race)
+__global__ void depth_run_rank_kernel(const uint64_t* __restrict__ keys,
+                                      const uint32_t* __restrict__ order, int64_t n,
+                                      uint32_t* __restrict__ newpos, uint32_t* __restrict__ val,
+                                      int* __restrict__ overflow) {
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
-  const uint32_t hi = (uint32_t)(keys[k] >> 32);
-  if (hi == 0xffffffffu) return;                              // culled
-  if (k > 0 && (uint32_t)(keys[k - 1] >> 32) == hi) return;  // not the first of its run
-  int64_t e = k + 1;
-  while (e < n && (uint32_t)(keys[e] >> 32) == hi) {
-    if (e - k >= kMaxDepthRun) {
-      atomicExch(overflow, 1);
-      return;
-    }
-    ++e;
+  const uint64_t key = keys[k];
+  const uint32_t hi = (uint32_t)(key >> 32);
+  val[k] = order[k];
+  if (hi == 0xffffffffu) {  // culled
+    newpos[k] = (uint32_t)k;
+    return;
   }
-  for (int64_t a = k + 1; a < e; ++a) {
-    const uint64_t ka = keys[a];
-    const uint32_t va = order[a];
-    int64_t b = a - 1;
-    while (b >= k && keys[b] > ka) {
-      keys[b + 1] = keys[b];
-      order[b + 1] = order[b];
-      --b;
-    }
-    keys[b + 1] = ka;
-    order[b + 1] = va;
+  int64_t s = k, e = k + 1;
+  while (s > 0 && (uint32_t)(keys[s - 1] >> 32) == hi && k - s < kMaxDepthRun) --s;
+  while (e < n && (uint32_t)(keys[e] >> 32) == hi && e - s <= kMaxDepthRun) ++e;
+  if (e - s > kMaxDepthRun || k - s >= kMaxDepthRun) {
+    atomicExch(overflow, 1);
+    newpos[k] = (uint32_t)k;
+    return;
   }
+  int64_t r = 0;
+  for (int64_t j = s; j < e; ++j) {
+    const uint64_t kj = keys[j];
+    r += (kj < key || (kj == key && j < k)) ? 1 : 0;
+  }
+  newpos[k] = (uint32_t)(s + r);
+}
+
+__global__ void depth_run_scatter_kernel(const uint32_t* __restrict__ newpos,
+                                         const uint32_t* __restrict__ val, int64_t n,
+                                         uint32_t* __restrict__ order) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) order[newpos[k]] = val[k];
 }
 
 cudaError_t run_depth_sort_hi(void* temp, size_t temp_bytes, const uint64_t* keys_in,
                               uint64_t* keys_out, const uint32_t* vals_in, uint32_t* order,
-                              int64_t n, int* overflow, cudaStream_t stream) {
+                              int64_t n, uint32_t* scratch_pos, uint32_t* scratch_val,
+                              int* overflow, cudaStream_t stream) {
   cudaError_t e = cudaMemsetAsync(overflow, 0, sizeof(int), stream);
   if (e != cudaSuccess) return e;
   e = cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_in, keys_out, vals_in, order, (int)n,
@@ -100,9 +115,11 @@ cudaError_t run_depth_sort_hi(void* temp, size_t temp_bytes, const uint64_t* key
   note_launch(5);
   if (e != cudaSuccess) return e;
   const int block = 256;
-  depth_fixup_kernel<<<(unsigned)((n + block - 1) / block), block, 0, stream>>>(keys_out, order, n,
-                                                                               overflow);
-  note_launch();
+  const unsigned grid = (unsigned)((n + block - 1) / block);
+  depth_run_rank_kernel<<<grid, block, 0, stream>>>(keys_out, order, n, scratch_pos, scratch_val,
+                                                    overflow);
+  depth_run_scatter_kernel<<<grid, block, 0, stream>>>(scratch_pos, scratch_val, n, order);
+  note_launch(2);
   return cudaGetLastError();
 }
 

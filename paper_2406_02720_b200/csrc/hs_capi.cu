@@ -323,8 +323,10 @@ int hs_preprocess_fwd(hs_frame* frame, const hs_scene* scene, const hs_camera* c
                                             frame->n, f.rec, f.side, f.rect, f.count, f.dkey_in,
                                             f.dval, radii, stream));
   }
+  // rank_of and cnt_r are outputs of the count scan below: free as fixup scratch here
   HS_CUDA(run_depth_sort_hi(f.temp, f.temp_bytes, f.dkey_in, f.dkey_out, f.dval, f.order,
-                            frame->n, f.counters + kDepthOverflowSlot, stream));
+                            frame->n, f.rank_of, reinterpret_cast<uint32_t*>(f.cnt_r),
+                            f.counters + kDepthOverflowSlot, stream));
   HS_CUDA(run_count_scan(f.temp, f.temp_bytes, f.count, f.order, f.cnt_r, f.off_r, f.rank_of,
                          frame->n, stream));
   frame->num_pairs = -1;

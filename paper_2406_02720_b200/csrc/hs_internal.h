@@ -103,11 +103,12 @@ size_t pair_sort_temp_bytes(int64_t p, int tile_bits);
 cudaError_t run_depth_sort(void* temp, size_t temp_bytes, const uint64_t* keys_in,
                            uint64_t* keys_out, const uint32_t* vals_in, uint32_t* order,
                            int64_t n, cudaStream_t stream);
-// upper-32-bit sort + per-run fixup; *overflow = 1 when a run was too long (then
-// run_depth_sort must redo the ranks)
+// upper-32-bit sort + per-run fixup (two n-element u32 scratch arrays); *overflow =
+// 1 when a run was too long (then run_depth_sort must redo the ranks)
 cudaError_t run_depth_sort_hi(void* temp, size_t temp_bytes, const uint64_t* keys_in,
                               uint64_t* keys_out, const uint32_t* vals_in, uint32_t* order,
-                              int64_t n, int* overflow, cudaStream_t stream);
+                              int64_t n, uint32_t* scratch_pos, uint32_t* scratch_val,
+                              int* overflow, cudaStream_t stream);
 // cnt_r[r] = count[order[r]], off_r = exclusive scan (n+1 entries), rank_of[order[r]] = r
 cudaError_t run_count_scan(void* temp, size_t temp_bytes, const int32_t* count,
                            const uint32_t* order, int32_t* cnt_r, int32_t* off_r,

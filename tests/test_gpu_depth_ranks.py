@@ -45,9 +45,9 @@ def test_short_runs_in_upper_bits():
 
 def test_runs_just_under_the_fixup_limit():
     rng = np.random.default_rng(2)
-    n = 1500
-    # three buckets of 500 (limit 512), descending low bits against the index order
-    z = 3.0 + (np.arange(n) // 500) * 0.25 + (n - np.arange(n)) * 2.0 ** -44
+    n = 6000
+    # three buckets of 2000 (limit 2048), descending low bits against the index order
+    z = 3.0 + (np.arange(n) // 2000) * 0.25 + (n - np.arange(n)) * 2.0 ** -44
     z = z[rng.permutation(n)]
     _check(_with_depths(n, z))
 
@@ -55,6 +55,7 @@ def test_runs_just_under_the_fixup_limit():
 def test_long_runs_take_the_full_sort():
     rng = np.random.default_rng(3)
     n = 4000
-    # one bucket of 2500 distinct depths plus 1500 exactly equal ones: both overflow
+    # one bucket of 2500 distinct depths (over the limit: the full sort) plus 1500
+    # exactly equal ones (ranked by index)
     z = np.concatenate([4.0 + rng.permutation(2500) * 2.0 ** -42, np.full(1500, 5.0)])
     _check(_with_depths(n, z[rng.permutation(n)]))
