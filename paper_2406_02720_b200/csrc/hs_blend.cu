@@ -435,7 +435,11 @@ __global__ void HS_FWD_BOUNDS blend_fwd_kernel(
       __syncwarp();
       const int s = b & 1;
       if (lane < nb) {
-        st.win[s][lane] = strip_window(st.rec[s][lane], x0, y0);
+        // one dispatch key per staged splat: 4 * kind + window, kind 0 fast, 1 fast
+        // steep, 2 generic (the window mask then only selects among the fast bodies)
+        const uint32_t fl = __float_as_uint(st.rec[s][lane][3].y);
+        const int kind = !fast_flags(fl) ? 2 : ((fl & kFlagSteep) ? 1 : 0);
+        st.win[s][lane] = 4 * kind + (kind == 2 ? kWinAll : strip_window(st.rec[s][lane], x0, y0));
         prescale_record(st.rec[s][lane]);
       }
       __syncwarp();
@@ -449,24 +453,21 @@ __global__ void HS_FWD_BOUNDS blend_fwd_kernel(
         }
         const float4 q[4] = {st.rec[s][j][0], st.rec[s][j][1], st.rec[s][j][2], st.rec[s][j][3]};
         const uint32_t flags = __float_as_uint(q[3].y);
-        if (fast_flags(flags)) {
-          const int win = st.win[s][j] & alive;
-          if (win == kWinNone) {
+        const int key = st.win[s][j] & (~3 | alive);  // generic keeps its window bits: 8+
+        switch (key) {
+          case 1: fwd_splat_fast<false, 0, 2>(q, st.side[s][j], px, py0, P); break;
+          case 2: fwd_splat_fast<false, 2, 2>(q, st.side[s][j], px, py0, P); break;
+          case 3: fwd_splat_fast<false, 0, 4>(q, st.side[s][j], px, py0, P); break;
+          case 5: fwd_splat_fast<true, 0, 2>(q, st.side[s][j], px, py0, P); break;
+          case 6: fwd_splat_fast<true, 2, 2>(q, st.side[s][j], px, py0, P); break;
+          case 7: fwd_splat_fast<true, 0, 4>(q, st.side[s][j], px, py0, P); break;
+          case 0:
+          case 4:
 #pragma unroll
             for (int p = 0; p < kPairs; ++p) P.C[p] = fadd2(P.C[p], P.A[p]);
-          } else if (flags & kFlagSteep) {
-            with_window(win, [&](auto p0, auto np) {
-              fwd_splat_fast<true, decltype(p0)::value, decltype(np)::value>(
-                  q, st.side[s][j], px, py0, P);
-            });
-          } else {
-            with_window(win, [&](auto p0, auto np) {
-              fwd_splat_fast<false, decltype(p0)::value, decltype(np)::value>(
-                  q, st.side[s][j], px, py0, P);
-            });
-          }
-        } else
-          fwd_splat_generic(q, st.side[s][j], flags, px, py0, P);
+            break;
+          default: fwd_splat_generic(q, st.side[s][j], flags, px, py0, P); break;
+        }
       }
       __syncwarp();
     }
