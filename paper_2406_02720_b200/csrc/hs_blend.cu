@@ -756,7 +756,12 @@ __global__ void HS_BWD_BOUNDS blend_bwd_kernel(
       cp_async_wait<1>();
       __syncwarp();
       const int s = b & 1;
-      if (lane < nb) st.win[s][lane] = strip_window(st.rec[s][lane], x0, y0);
+      if (lane < nb) {
+        // dispatch key 4 * kind + window, as in K5 (kind 0 fast, 1 fast steep, 2 generic)
+        const uint32_t fl = __float_as_uint(st.rec[s][lane][3].y);
+        const int kind = !fast_flags(fl) ? 2 : ((fl & kFlagSteep) ? 1 : 0);
+        st.win[s][lane] = 4 * kind + (kind == 2 ? kWinAll : strip_window(st.rec[s][lane], x0, y0));
+      }
       __syncwarp();
       for (int j = 0; j < nb; ++j) {
         const int pos = hi - j;
@@ -773,51 +778,41 @@ __global__ void HS_BWD_BOUNDS blend_bwd_kernel(
           row = (size_t)((int)__float_as_uint(q[3].z) + ty * spans_x + tx);
         }
         const int vi = lane >> 1;
-        if (fast_flags(flags)) {
-          const bool steep = flags & kFlagSteep;
-          const int win = st.win[s][j];
-          if (win == kWinNone) {
-            // below 2^-27 on the whole tile: a zero pair row, no reduction
-            if (!(lane & 1) && vi < kCols) rows[row * kStride + vi] = 0.f;
-            continue;
+        int key = st.win[s][j];
+        if (kDyn && pos >= minc) key &= ~3 | (pos < hmax_lo ? 1 : 0) | (pos < hmax_hi ? 2 : 0);
+        if (key == 0 || key == 4) {
+          // fast splat below 2^-27 on every live strip: a zero pair row, no reduction
+          if (!(lane & 1) && vi < kCols) rows[row * kStride + vi] = 0.f;
+          continue;
+        }
+        if (pos < minc) {
+          switch (key) {
+            case 1: bwd_splat_fast<true, false, 0, 2>(q, side, pos, px, py0, P, a); break;
+            case 2: bwd_splat_fast<true, false, 2, 2>(q, side, pos, px, py0, P, a); break;
+            case 3: bwd_splat_fast<true, false, 0, 4>(q, side, pos, px, py0, P, a); break;
+            case 5: bwd_splat_fast<true, true, 0, 2>(q, side, pos, px, py0, P, a); break;
+            case 6: bwd_splat_fast<true, true, 2, 2>(q, side, pos, px, py0, P, a); break;
+            case 7: bwd_splat_fast<true, true, 0, 4>(q, side, pos, px, py0, P, a); break;
+            default: bwd_splat_generic(q, side, flags, pos, px, py0, P, a); break;
           }
-          if (pos < minc) {
-            if (steep)
-              with_window(win, [&](auto p0, auto np) {
-                bwd_splat_fast<true, true, decltype(p0)::value, decltype(np)::value>(
-                    q, side, pos, px, py0, P, a);
-              });
-            else
-              with_window(win, [&](auto p0, auto np) {
-                bwd_splat_fast<true, false, decltype(p0)::value, decltype(np)::value>(
-                    q, side, pos, px, py0, P, a);
-              });
-          } else if (kDyn) {
-            const int wd = win & ((pos < hmax_lo ? 1 : 0) | (pos < hmax_hi ? 2 : 0));
-            if (wd == kWinNone) {
-              if (!(lane & 1) && vi < kCols) rows[row * kStride + vi] = 0.f;
-              continue;
-            }
-            if (steep)
-              with_window(wd, [&](auto p0, auto np) {
-                bwd_splat_fast<false, true, decltype(p0)::value, decltype(np)::value>(
-                    q, side, pos, px, py0, P, a);
-              });
-            else
-              with_window(wd, [&](auto p0, auto np) {
-                bwd_splat_fast<false, false, decltype(p0)::value, decltype(np)::value>(
-                    q, side, pos, px, py0, P, a);
-              });
-          } else {
-            // partially active warp: every pair (windows here cost more in code size
-            // than they save unless the view is occluded: kDyn)
-            if (steep)
-              bwd_splat_fast<false, true>(q, side, pos, px, py0, P, a);
-            else
-              bwd_splat_fast<false, false>(q, side, pos, px, py0, P, a);
+        } else if (kDyn) {
+          switch (key) {
+            case 1: bwd_splat_fast<false, false, 0, 2>(q, side, pos, px, py0, P, a); break;
+            case 2: bwd_splat_fast<false, false, 2, 2>(q, side, pos, px, py0, P, a); break;
+            case 3: bwd_splat_fast<false, false, 0, 4>(q, side, pos, px, py0, P, a); break;
+            case 5: bwd_splat_fast<false, true, 0, 2>(q, side, pos, px, py0, P, a); break;
+            case 6: bwd_splat_fast<false, true, 2, 2>(q, side, pos, px, py0, P, a); break;
+            case 7: bwd_splat_fast<false, true, 0, 4>(q, side, pos, px, py0, P, a); break;
+            default: bwd_splat_generic(q, side, flags, pos, px, py0, P, a); break;
           }
         } else {
-          bwd_splat_generic(q, side, flags, pos, px, py0, P, a);
+          // partially active warp: every pair (windows here cost more in code size
+          // than they save unless the view is occluded: kDyn)
+          switch (key >> 2) {
+            case 0: bwd_splat_fast<false, false>(q, side, pos, px, py0, P, a); break;
+            case 1: bwd_splat_fast<false, true>(q, side, pos, px, py0, P, a); break;
+            default: bwd_splat_generic(q, side, flags, pos, px, py0, P, a); break;
+          }
         }
         // per-lane partials -> the pair-row columns (_blend_py.py:16-18)
         const float ca = q[0].z, cb = q[0].w, cc = q[1].x, za = q[1].y, zb = q[1].z;
