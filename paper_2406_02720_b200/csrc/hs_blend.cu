@@ -498,6 +498,7 @@ struct BwdAcc {
   float s0, s1, s2;  // sum d_pow, d_pow*dy, d_pow*dy^2 (dx is constant per lane)
   float q0, q1, qz;  // sum d_z, d_z*dy, d_z*z
   float c1, c2, r, g, b;
+  float dx;          // the lane's pixel offset from the splat centre (for the row columns)
 };
 
 struct BwdPix {
@@ -575,6 +576,7 @@ __device__ __forceinline__ void bwd_splat_fast(const float4 (&q)[4], const Steep
   out.q0 = c2k * Q0; out.q1 = c2k * fmaf(s.dy0, Q0, Q1); out.qz = c2k * (qz.x + qz.y);
   out.c1 = a1.x + a1.y; out.c2 = a2.x + a2.y;
   out.r = ar.x + ar.y; out.g = ag.x + ag.y; out.b = ab.x + ab.y;
+  out.dx = s.dx;
 }
 
 // Generic: steep, sign mode, clamped weights, partially active warps.  Scalar;
@@ -590,7 +592,7 @@ __device__ __forceinline__ void bwd_splat_generic(const float4 (&q)[4], const St
   const float cr = q[2].y, cg = q[2].z, cb = q[2].w;
   // d erf/dz = 2/sqrt(pi) exp(-z^2); only the erf mode has a z derivative
   const float c2k = mode == kModeErf ? c2 * (2.0f * kInvSqrtPi) : 0.0f;
-  a = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  a = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, s.dx};
 #pragma unroll
   for (int i = 0; i < kPx; ++i) {
     const int p = i >> 1, h = i & 1;
@@ -761,6 +763,12 @@ __global__ void HS_BWD_BOUNDS blend_bwd_kernel(
         const uint32_t fl = __float_as_uint(st.rec[s][lane][3].y);
         const int kind = !fast_flags(fl) ? 2 : ((fl & kFlagSteep) ? 1 : 0);
         st.win[s][lane] = 4 * kind + (kind == 2 ? kWinAll : strip_window(st.rec[s][lane], x0, y0));
+        // the pair's generation-order row in this tile, once per splat instead of per lane
+        if (!kRowsBySortedPos) {
+          const int spans_x = (int)(fl >> kFlagSpanShift);
+          st.rec[s][lane][3].z =
+              __int_as_float((int)__float_as_uint(st.rec[s][lane][3].z) + ty * spans_x + tx);
+        }
       }
       __syncwarp();
       for (int j = 0; j < nb; ++j) {
@@ -770,13 +778,8 @@ __global__ void HS_BWD_BOUNDS blend_bwd_kernel(
         const uint32_t flags = __float_as_uint(q[3].y);
         const int mode = (int)(flags & 3u);
         BwdAcc a;
-        size_t row;
-        if (kRowsBySortedPos) {
-          row = (size_t)(k0 + pos);
-        } else {
-          const int spans_x = (int)(flags >> kFlagSpanShift);
-          row = (size_t)((int)__float_as_uint(q[3].z) + ty * spans_x + tx);
-        }
+        // kRowsBySortedPos: the sorted position; else the row staged above
+        const size_t row = kRowsBySortedPos ? (size_t)(k0 + pos) : (size_t)__float_as_int(q[3].z);
         const int vi = lane >> 1;
         int key = st.win[s][j];
         if (kDyn && pos >= minc) key &= ~3 | (pos < hmax_lo ? 1 : 0) | (pos < hmax_hi ? 2 : 0);
@@ -816,8 +819,7 @@ __global__ void HS_BWD_BOUNDS blend_bwd_kernel(
         }
         // per-lane partials -> the pair-row columns (_blend_py.py:16-18)
         const float ca = q[0].z, cb = q[0].w, cc = q[1].x, za = q[1].y, zb = q[1].z;
-        const float2 lo = __half22float2(*reinterpret_cast<const __half2*>(&q[3].w));
-        const float dx = (px - q[0].x) - lo.x;
+        const float dx = a.dx;
         float v[16];
         v[0] = fmaf(ca * dx, a.s0, fmaf(cb, a.s1, -za * a.q0));
         v[1] = fmaf(cc, a.s1, fmaf(cb * dx, a.s0, -zb * a.q0));
