@@ -260,19 +260,11 @@ __device__ __forceinline__ int strip_window(const float4 (&q)[4], float x0, floa
   const float2 lo = __half22float2(*reinterpret_cast<const __half2*>(&q[3].w));
   const float xl = (x0 - q[0].x) - lo.x, xh = xl + (float)(kTile - 1);
   const float a = q[0].z, b = q[0].w, c = q[1].x;
-  int first = 4, last = -1;
-#pragma unroll
-  for (int p = 0; p < kPairs; ++p) {
-    const float yl = (y0 + 4.0f * p - q[0].y) - lo.y;
-    if (!(box_min_q(a, b, c, xl, xh, yl, yl + 3.0f) > kSkipQ)) {
-      first = min(first, p);
-      last = p;
-    }
-  }
-  if (last < 0) return kWinNone;
-  if (last <= 1) return 1;
-  if (first >= 2) return 2;
-  return kWinAll;
+  // the windows are halves (strips 0-1, 2-3): one box per half, rows 0-7 and 8-15
+  const float yl = (y0 - q[0].y) - lo.y;
+  const bool low = !(box_min_q(a, b, c, xl, xh, yl, yl + 7.0f) > kSkipQ);
+  const bool high = !(box_min_q(a, b, c, xl, xh, yl + 8.0f, yl + 15.0f) > kSkipQ);
+  return (low ? 1 : 0) | (high ? 2 : 0);
 }
 
 // calls f(P0, NP) with the window as compile-time constants
