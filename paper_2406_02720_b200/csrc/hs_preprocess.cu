@@ -420,7 +420,16 @@ __device__ __forceinline__ void forward_state(const Src& src, const CamArgs& cam
 // K1: preprocess forward.  Writes the 64-B record, tile rect, pair count and
 // the depth-rank sort key of each primitive (culled: count 0, key ~0).
 template <typename T, int DEG, int NT>
-__global__ void __launch_bounds__(NT) preprocess_fwd_kernel(
+#ifndef HS_K1_MINB
+#define HS_K1_MINB 5  // resident CTAs per SM to cap registers for (0: no cap): 96 registers,
+                      // 20 warps/SM; 0.289 -> 0.274 ms with the ranks at c3
+#endif
+#if HS_K1_MINB > 0
+#define HS_K1_BOUNDS __launch_bounds__(NT, HS_K1_MINB)
+#else
+#define HS_K1_BOUNDS __launch_bounds__(NT)
+#endif
+__global__ void HS_K1_BOUNDS preprocess_fwd_kernel(
     SceneArgs<T> sc, CamArgs cam, int kernel, int64_t n, float4* __restrict__ rec,
     SteepRec* __restrict__ side, int4* __restrict__ rect, int32_t* __restrict__ count,
     uint64_t* __restrict__ dkey, uint32_t* __restrict__ dval, int32_t* __restrict__ radii) {
@@ -959,7 +968,10 @@ __device__ __forceinline__ void reduce_block(E* __restrict__ dst, int cnt, const
 }
 
 template <typename T, int DEG, int NT>
-__global__ void __launch_bounds__(NT, 3) preprocess_bwd_kernel(
+#ifndef HS_K7_MINB
+#define HS_K7_MINB 3
+#endif
+__global__ void __launch_bounds__(NT, HS_K7_MINB) preprocess_bwd_kernel(
     SceneArgs<T> sc, CamArgs cam, int kernel, int64_t n, const int32_t* __restrict__ count,
     const float4* __restrict__ merged, GradArgs<T> out) {
   constexpr int K = (DEG + 1) * (DEG + 1);
