@@ -59,3 +59,21 @@ def test_long_runs_take_the_full_sort():
     # exactly equal ones (ranked by index)
     z = np.concatenate([4.0 + rng.permutation(2500) * 2.0 ** -42, np.full(1500, 5.0)])
     _check(_with_depths(n, z[rng.permutation(n)]))
+
+
+def test_workspace_reuse_across_pair_counts():
+    """One Rasterizer (persistent workspace) over scenes whose pair count grows and
+    shrinks: hs_read_pairs_and_bin bins in place when the workspace fits and asks for
+    a larger one otherwise; every render equals a fresh one bit for bit."""
+    rast = device.Rasterizer("cuda", slots=1)
+    for n, seed in ((500, 1), (4000, 2), (800, 3), (6000, 4)):
+        sa = scenes.frustum(n, 1, 96, 64, seed=seed, sig_lo=1.0, sig_hi=6.0)
+        cam = CameraModel(**sa.cameras[0])
+        sc = Scene(*(getattr(sa, f) for f in sa.FIELDS), sh_degree=sa.sh_degree,
+                   background_color=sa.background_color, device="cuda", dtype=torch.float32)
+        a = rast.render(sc, cam)
+        ca, ta = a.color.clone(), a.terminal.clone()
+        pa = a.frame.export()["pair_splat"]
+        b = device.render(sc, cam)
+        assert torch.equal(ca, b.color) and torch.equal(ta, b.terminal)
+        assert np.array_equal(pa, b.frame.export()["pair_splat"])
