@@ -657,6 +657,32 @@ __device__ __forceinline__ float warp_transpose_reduce16(float (&v)[16], int lan
   return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
 }
 
+// Sum 13 per-lane values over the warp through shared memory: every lane writes
+// its values as column `lane` of a 13 x 36 buffer (rows padded to 36 floats: the
+// 16-B reads below hit distinct bank groups), then lane 2m + h sums the 16 values
+// of row m in columns 16h..16h+15 (four LDS.128 and a 4-level add tree) and the
+// two halves are combined with one shuffle: lanes 2m and 2m + 1 both hold the warp
+// total of value m.  ~35 instructions against the 61 of the shuffle transpose.
+#ifndef HS_SMEM_REDUCE
+#define HS_SMEM_REDUCE 1
+#endif
+constexpr int kRedStride = 36;
+__device__ __forceinline__ float warp_reduce13_smem(const float (&v)[16], float* red, int lane) {
+  __syncwarp();  // the previous splat's reads are done
+#pragma unroll
+  for (int k = 0; k < 13; ++k) red[k * kRedStride + lane] = v[k];
+  __syncwarp();
+  const int m = lane >> 1, h = lane & 1;
+  float t = 0.f;
+  if (m < 13) {
+    const float4* row = reinterpret_cast<const float4*>(red + m * kRedStride + 16 * h);
+    const float4 a = row[0], b = row[1], c = row[2], d = row[3];
+    t = ((a.x + a.y) + (a.z + a.w)) + ((b.x + b.y) + (b.z + b.w)) +
+        (((c.x + c.y) + (c.z + c.w)) + ((d.x + d.y) + (d.z + d.w)));
+  }
+  return t + __shfl_xor_sync(0xffffffffu, t, 1);
+}
+
 // kRowsBySortedPos: Seam 1 layout (row k = sorted pair index, 12 reference
 // columns).  Otherwise the generation-order layout: row = record origin +
 // ty*spans_x + tx, kRowFloats columns, consumed by K7.
@@ -674,6 +700,8 @@ __global__ void HS_BWD_BOUNDS blend_bwd_kernel(
   constexpr int kCols = kRowsBySortedPos ? 12 : 13;
   __shared__ WarpStage stage_all[kBwdWarps];
   __shared__ int cnt_all[kBwdWarps][kPx][32];
+  __shared__ __align__(16) float red_all[kBwdWarps][13 * kRedStride];
+  float* red = red_all[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
   WarpStage& st = stage_all[threadIdx.x >> 5];
   int* cnt = &cnt_all[threadIdx.x >> 5][0][lane];
@@ -829,7 +857,8 @@ __global__ void HS_BWD_BOUNDS blend_bwd_kernel(
         v[11] = a.b;
         v[12] = erf_mode ? a.qz : 0.f;
         v[13] = v[14] = v[15] = 0.f;
-        const float total = warp_transpose_reduce16(v, lane);
+        const float total = HS_SMEM_REDUCE ? warp_reduce13_smem(v, red, lane)
+                                           : warp_transpose_reduce16(v, lane);
         if (!(lane & 1) && vi < kCols) rows[row * kStride + vi] = total;
       }
       __syncwarp();
