@@ -1104,7 +1104,10 @@ cudaError_t launch_preprocess_bwd_t(const SceneArgs<T>& sc, const CamArgs& cam, 
   merge_rows_kernel<<<(unsigned)((cnt + 255) / 256), 256, 0, stream>>>(
       end, tiles_x, rec, rect, count, rank_of, last_rank, rows, merged, out.begin);
   note_launch();
-  constexpr int NT = sizeof(T) == 4 ? 128 : 64;
+#ifndef HS_K7_NT_F32
+#define HS_K7_NT_F32 128
+#endif
+  constexpr int NT = sizeof(T) == 4 ? HS_K7_NT_F32 : 64;
   const int64_t grid = (cnt + NT - 1) / NT;
   switch (sc.deg) {
 #define HS_K7(D)                                                                               \
