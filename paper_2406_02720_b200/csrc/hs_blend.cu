@@ -30,9 +30,10 @@ namespace hs {
 // Warps per CTA and the minimum resident CTAs per SM (a register cap) of each
 // blend.  One-warp CTAs (each warp is independent: its own tile queue pulls,
 // staging and shared memory) let the SM fill to the register limit exactly:
-// K5 at 126 registers runs 16 warps/SM, K6 at 149 runs 13 (4-warp CTAs: 16 and
-// 12).  Measured on c3: K5 0.856 -> 0.840 ms, K6 1.693 -> 1.651 ms
-// (tools/build_variant.sh + tools/variant_bench.sh).  MINB 0 = no cap.
+// K5 at 124 registers runs 16 warps/SM, K6 at 153 runs 12.  Measured on c3
+// (tools/build_variant.sh + tools/variant_bench.sh): one-warp CTAs took K5 0.856
+// -> 0.840 ms and K6 1.693 -> 1.651 ms; with the current bodies, capping K6 at 13
+// or 14 warps (MINB 13/14) or K5 at 12/14 is slower.  MINB 0 = no cap.
 #ifndef HS_FWD_WARPS
 #define HS_FWD_WARPS 1
 #endif
