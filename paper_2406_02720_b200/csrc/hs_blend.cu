@@ -258,6 +258,7 @@ __device__ __forceinline__ float box_min_q(float a, float b, float c, float xl, 
 // window code of a staged record (raw conic, before any prescale) in the tile
 // whose first pixel centre is (x0, y0)
 __device__ __forceinline__ int strip_window(const float4 (&q)[4], float x0, float y0) {
+  if (__float_as_uint(q[3].y) & kFlagNoWin) return kWinAll;
   const float2 lo = __half22float2(*reinterpret_cast<const __half2*>(&q[3].w));
   const float xl = (x0 - q[0].x) - lo.x, xh = xl + (float)(kTile - 1);
   const float a = q[0].z, b = q[0].w, c = q[1].x;
@@ -915,7 +916,8 @@ __global__ void pack_records_kernel(const double* __restrict__ packed,
   const bool steep = md != kModePlain && is_steep(p[5], p[6], reach);
   const float mux = (float)p[0], muy = (float)p[1];
   const __half2 lo = __floats2half2_rn((float)(p[0] - (double)mux), (float)(p[1] - (double)muy));
-  r[R_FLAGS] = __uint_as_float(pack_flags(md, steep, may_clamp(p[7], p[8]), 0));
+  r[R_FLAGS] = __uint_as_float(pack_flags(md, steep, may_clamp(p[7], p[8]), 0, false,
+                                          reach - 24.0 > kWinMaxRadius));
   r[R_ROW_ORIGIN] = __int_as_float(0);
   r[R_MU_LO] = __uint_as_float(*reinterpret_cast<const uint32_t*>(&lo));
   if (steep) side[l] = make_steep(p[0], p[1], p[5], p[6]);

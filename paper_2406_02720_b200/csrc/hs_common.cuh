@@ -43,7 +43,7 @@ enum RecordSlot {
   R_MUX = 0, R_MUY, R_CA, R_CB, R_CC, R_ZA, R_ZB, R_C1, R_C2,
   R_RED, R_GREEN, R_BLUE, R_DEPTH,
   R_FLAGS,       // u32: mode (bits 0-1) | steep (bit 2) | may-clamp (bit 3) | bad frame (bit 4)
-                 //      | spans_x << 5
+                 //      | no strip windows (bit 5) | spans_x << 6
   R_ROW_ORIGIN,  // i32: pair_base - ty0*spans_x - tx0; pair (tx,ty) -> row origin + ty*spans_x + tx
   R_MU_LO        // half2: (mux - (float)mux, muy - (float)muy)
 };
@@ -97,7 +97,12 @@ constexpr uint32_t kFlagClamp = 8u;
 // the whitening fell back to the identity (rasterizer.py:233-234, 246-247); K7
 // replays K1's decision from this bit instead of re-deciding it
 constexpr uint32_t kFlagBad = 16u;
-constexpr int kFlagSpanShift = 5;
+// Splats whose 3.5-sigma radius exceeds kWinMaxRadius px take no strip windows
+// (hs_blend.cu strip_window): the FP32 box bound sums terms up to ~a (r + 16)^2,
+// whose rounding stays far inside the bound's margin only for moderate r.
+constexpr uint32_t kFlagNoWin = 32u;
+constexpr double kWinMaxRadius = 256.0;
+constexpr int kFlagSpanShift = 6;
 // Splats whose weight can never reach the 0.99 clamp (c1 + |c2| bounds
 // (c1 + c2 E) g; 0.989 leaves room for FP32 rounding) skip the clamp and the
 // backward's gating test.
@@ -105,9 +110,11 @@ __host__ __device__ __forceinline__ bool may_clamp(double c1, double c2) {
   return c1 + fabs(c2) > 0.989;
 }
 __host__ __device__ __forceinline__ uint32_t pack_flags(int mode, bool steep, bool clamp,
-                                                        int spans_x, bool bad = false) {
+                                                        int spans_x, bool bad = false,
+                                                        bool nowin = false) {
   return (uint32_t)mode | (steep ? kFlagSteep : 0u) | (clamp ? kFlagClamp : 0u) |
-         (bad ? kFlagBad : 0u) | ((uint32_t)spans_x << kFlagSpanShift);
+         (bad ? kFlagBad : 0u) | (nowin ? kFlagNoWin : 0u) |
+         ((uint32_t)spans_x << kFlagSpanShift);
 }
 __host__ __device__ __forceinline__ bool is_steep(double za, double zb, double reach) {
   return (fabs(za) + fabs(zb)) * reach > kSteepLimit;

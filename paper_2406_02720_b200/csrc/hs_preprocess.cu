@@ -468,7 +468,7 @@ __global__ void HS_K1_BOUNDS preprocess_fwd_kernel(
   float4 r1 = make_float4((float)(st.a / st.det), (float)st.za, (float)st.zb, (float)st.c1);
   float4 r2 = make_float4((float)st.c2, (float)fmax(st.rgbu[0], 0.0), (float)fmax(st.rgbu[1], 0.0),
                           (float)fmax(st.rgbu[2], 0.0));
-  float4 r3 = make_float4((float)st.t[2], __uint_as_float(pack_flags(st.mode, steep, may_clamp(st.c1, st.c2), spans_x, st.bad)),
+  float4 r3 = make_float4((float)st.t[2], __uint_as_float(pack_flags(st.mode, steep, may_clamp(st.c1, st.c2), spans_x, st.bad, st.radius > kWinMaxRadius)),
                           __uint_as_float(0u), __uint_as_float(*reinterpret_cast<const uint32_t*>(&lo)));
   float4* dst = rec + 4 * i;
   dst[0] = r0;

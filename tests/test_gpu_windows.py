@@ -112,3 +112,35 @@ def test_occluded_view_matches_oracle(cuda):
     g = device.render_backward(sc, cam, out, torch.as_tensor(d_color, dtype=torch.float32))
     assert_grads({k: getattr(g, k).double().cpu().numpy() for k in GRAD_GROUPS},
                  {k: ref_g[k] for k in GRAD_GROUPS})
+
+
+def test_large_thin_splats_take_no_windows(cuda):
+    """Splats with a radius above 256 px (the FP32 box bound's safe range) are
+    evaluated on every strip; a scene of long, thin, large splats matches the oracle."""
+    from oracle import oracle as O
+    rng = np.random.default_rng(4)
+    sa = scenes.frustum(60, 1, 640, 480, seed=6, sig_lo=1.0, sig_hi=2.0)
+    # stretch every splat along one axis to 30-60x its width: radii of 100-420 px
+    # (longer, thinner splats reach the FP32 exponent's own cancellation limit,
+    # DESIGN.md 4, independent of the windows)
+    ls = sa.log_scale.astype(np.float64)
+    ls[:, 0] += np.log(rng.uniform(30.0, 60.0, len(ls)))
+    sa.log_scale = ls.astype(np.float32)
+    cam = CameraModel(**sa.cameras[0])
+    sc = Scene(*(getattr(sa, f) for f in sa.FIELDS), sh_degree=sa.sh_degree,
+               background_color=sa.background_color, device="cuda", dtype=torch.float32)
+    out = device.render(sc, cam)
+    assert int(out.radii.max()) > 256
+    d_color = scenes.cotangent(cam.height, cam.width, seed=3)
+    s64 = sa.as_float64()
+    ref = O.render(s64, cam)
+    ref_g = O.render_backward(s64, cam, ref, d_color)
+    got = {"color": out.color.cpu().numpy(), "alpha": out.alpha.cpu().numpy(),
+           "depth": out.depth.cpu().numpy(), "transmittance": out.transmittance.cpu().numpy(),
+           "terminal": out.terminal.cpu().numpy()}
+    assert_images(got, {"color": ref.color, "alpha": ref.alpha, "depth": ref.depth,
+                        "transmittance": ref.transmittance,
+                        "terminal": ref.per_pixel_terminal_index})
+    g = device.render_backward(sc, cam, out, torch.as_tensor(d_color, dtype=torch.float32))
+    assert_grads({k: getattr(g, k).double().cpu().numpy() for k in GRAD_GROUPS},
+                 {k: ref_g[k] for k in GRAD_GROUPS})
