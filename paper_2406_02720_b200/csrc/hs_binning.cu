@@ -286,8 +286,12 @@ __global__ void export_splats_kernel(const int32_t* __restrict__ count,
   const int64_t l = local_of[i];
   if (valid) valid[l] = (int32_t)i;
   const float* r = reinterpret_cast<const float*>(rec + 4 * i);
-  if (packed)
+  if (packed) {
     for (int c = 0; c < 13; ++c) packed[l * 13 + c] = r[c];
+    // large splats carry the stable conic form (hs_common.cuh kFlagNoWin)
+    conic_abc(r[R_CA], r[R_CB], r[R_CC], __float_as_uint(r[R_FLAGS]), packed[l * 13 + R_CB],
+              packed[l * 13 + R_CC]);
+  }
   if (mode) mode[l] = (int8_t)(__float_as_uint(r[R_FLAGS]) & 3u);
   if (tile_rect) {
     const int4 rc = rect[i];

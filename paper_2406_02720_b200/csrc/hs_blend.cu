@@ -355,11 +355,14 @@ __device__ __forceinline__ void fwd_splat_generic(const float4 (&q)[4], const St
   const int mode = (int)(flags & 3u);
   const float c1 = -q[1].w, c2 = -q[2].x;  // prescale_record negated them
   const float cr = q[2].y, cg = q[2].z, cb = q[2].w, z = q[3].x;
+  const bool large = flags & kFlagNoWin;  // s.A, s.C = scaled a, D; q[0].w = r
 #pragma unroll
   for (int i = 0; i < kPx; ++i) {
     const int p = i >> 1, h = i & 1;
     const float dy = s.dy0 + 2.0f * i;
-    const float g = ex2_approx(fmaf(fmaf(s.C, dy, s.Bx), dy, s.P0));
+    const float u = fmaf(q[0].w, dy, s.dx);
+    const float g = ex2_approx(large ? fmaf(s.A * u, u, s.C * dy * dy)
+                                     : fmaf(fmaf(s.C, dy, s.Bx), dy, s.P0));
     const float e = mode_factor(mode, erf_arg(s, steep, i));
     const float w = fminf(fmaf(c2, e, c1) * g, kWeightClamp);
     fwd_commit(-w, slot(P.T[p], h), slot(P.A[p], h), slot(P.C[p], h), slot(P.ar[p], h),
@@ -371,7 +374,7 @@ __device__ __forceinline__ void fwd_splat_generic(const float4 (&q)[4], const St
 // log2 scale of the exponent and -c1, -c2 (the forward composites with -w).
 __device__ __forceinline__ void prescale_record(float4 (&r)[4]) {
   r[0].z *= kNegHalfLog2e;
-  r[0].w *= kNegLog2e;
+  if (!(__float_as_uint(r[3].y) & kFlagNoWin)) r[0].w *= kNegLog2e;  // large: r = b/a stays
   r[1].x *= kNegHalfLog2e;
   r[1].w = -r[1].w;
   r[2].x = -r[2].x;
@@ -432,7 +435,7 @@ __global__ void HS_FWD_BOUNDS blend_fwd_kernel(
         // one dispatch key per staged splat: 4 * kind + window, kind 0 fast, 1 fast
         // steep, 2 generic (the window mask then only selects among the fast bodies)
         const uint32_t fl = __float_as_uint(st.rec[s][lane][3].y);
-        const int kind = !fast_flags(fl) ? 2 : ((fl & kFlagSteep) ? 1 : 0);
+        const int kind = (!fast_flags(fl) || (fl & kFlagNoWin)) ? 2 : ((fl & kFlagSteep) ? 1 : 0);
         st.win[s][lane] = 4 * kind + (kind == 2 ? kWinAll : strip_window(st.rec[s][lane], x0, y0));
         prescale_record(st.rec[s][lane]);
       }
@@ -493,6 +496,7 @@ struct BwdAcc {
   float q0, q1, qz;  // sum d_z, d_z*dy, d_z*z
   float c1, c2, r, g, b;
   float dx;          // the lane's pixel offset from the splat centre (for the row columns)
+  float cb, cc;      // the conic's b and c (the generic path rebuilds them for kFlagNoWin)
 };
 
 struct BwdPix {
@@ -571,6 +575,8 @@ __device__ __forceinline__ void bwd_splat_fast(const float4 (&q)[4], const Steep
   out.c1 = a1.x + a1.y; out.c2 = a2.x + a2.y;
   out.r = ar.x + ar.y; out.g = ag.x + ag.y; out.b = ab.x + ab.y;
   out.dx = s.dx;
+  out.cb = q[0].w;
+  out.cc = q[1].x;
 }
 
 // Generic: steep, sign mode, clamped weights, partially active warps.  Scalar;
@@ -586,7 +592,9 @@ __device__ __forceinline__ void bwd_splat_generic(const float4 (&q)[4], const St
   const float cr = q[2].y, cg = q[2].z, cb = q[2].w;
   // d erf/dz = 2/sqrt(pi) exp(-z^2); only the erf mode has a z derivative
   const float c2k = mode == kModeErf ? c2 * (2.0f * kInvSqrtPi) : 0.0f;
-  a = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, s.dx};
+  const bool large = flags & kFlagNoWin;  // s.A, s.C = scaled a, D; q[0].w = r
+  a = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, s.dx, 0.f, 0.f};
+  conic_abc(q[0].z, q[0].w, q[1].x, flags, a.cb, a.cc);
 #pragma unroll
   for (int i = 0; i < kPx; ++i) {
     const int p = i >> 1, h = i & 1;
@@ -595,7 +603,9 @@ __device__ __forceinline__ void bwd_splat_generic(const float4 (&q)[4], const St
     const float dr = slot(P.dr[p], h), dg = slot(P.dg[p], h), db = slot(P.db[p], h);
     const bool active = pos < P.cnt[i * 32];
     const float dy = s.dy0 + 2.0f * i;
-    const float gg = ex2_approx(fmaf(fmaf(s.C, dy, s.Bx), dy, s.P0));
+    const float ul = fmaf(q[0].w, dy, s.dx);
+    const float gg = ex2_approx(large ? fmaf(s.A * ul, ul, s.C * dy * dy)
+                                      : fmaf(fmaf(s.C, dy, s.Bx), dy, s.P0));
     const float zz = erf_arg(s, steep, i);
     const float e = mode_factor(mode, zz);
     const float u = fmaf(c2, e, c1);
@@ -783,7 +793,7 @@ __global__ void HS_BWD_BOUNDS blend_bwd_kernel(
       if (lane < nb) {
         // dispatch key 4 * kind + window, as in K5 (kind 0 fast, 1 fast steep, 2 generic)
         const uint32_t fl = __float_as_uint(st.rec[s][lane][3].y);
-        const int kind = !fast_flags(fl) ? 2 : ((fl & kFlagSteep) ? 1 : 0);
+        const int kind = (!fast_flags(fl) || (fl & kFlagNoWin)) ? 2 : ((fl & kFlagSteep) ? 1 : 0);
         st.win[s][lane] = 4 * kind + (kind == 2 ? kWinAll : strip_window(st.rec[s][lane], x0, y0));
         // the pair's generation-order row in this tile, once per splat instead of per lane
         if (!kRowsBySortedPos) {
@@ -840,7 +850,7 @@ __global__ void HS_BWD_BOUNDS blend_bwd_kernel(
           }
         }
         // per-lane partials -> the pair-row columns (_blend_py.py:16-18)
-        const float ca = q[0].z, cb = q[0].w, cc = q[1].x, za = q[1].y, zb = q[1].z;
+        const float ca = q[0].z, cb = a.cb, cc = a.cc, za = q[1].y, zb = q[1].z;
         const float dx = a.dx;
         float v[16];
         v[0] = fmaf(ca * dx, a.s0, fmaf(cb, a.s1, -za * a.q0));
@@ -916,8 +926,12 @@ __global__ void pack_records_kernel(const double* __restrict__ packed,
   const bool steep = md != kModePlain && is_steep(p[5], p[6], reach);
   const float mux = (float)p[0], muy = (float)p[1];
   const __half2 lo = __floats2half2_rn((float)(p[0] - (double)mux), (float)(p[1] - (double)muy));
-  r[R_FLAGS] = __uint_as_float(pack_flags(md, steep, may_clamp(p[7], p[8]), 0, false,
-                                          reach - 24.0 > kWinMaxRadius));
+  const bool large = reach - 24.0 > kWinMaxRadius;
+  if (large) {  // the stable conic form (hs_common.cuh kFlagNoWin)
+    r[R_CB] = (float)(p[3] / p[2]);
+    r[R_CC] = (float)(p[4] - p[3] * p[3] / p[2]);
+  }
+  r[R_FLAGS] = __uint_as_float(pack_flags(md, steep, may_clamp(p[7], p[8]), 0, false, large));
   r[R_ROW_ORIGIN] = __int_as_float(0);
   r[R_MU_LO] = __uint_as_float(*reinterpret_cast<const uint32_t*>(&lo));
   if (steep) side[l] = make_steep(p[0], p[1], p[5], p[6]);

@@ -97,11 +97,26 @@ constexpr uint32_t kFlagClamp = 8u;
 // the whitening fell back to the identity (rasterizer.py:233-234, 246-247); K7
 // replays K1's decision from this bit instead of re-deciding it
 constexpr uint32_t kFlagBad = 16u;
-// Splats whose 3.5-sigma radius exceeds kWinMaxRadius px take no strip windows
-// (hs_blend.cu strip_window): the FP32 box bound sums terms up to ~a (r + 16)^2,
-// whose rounding stays far inside the bound's margin only for moderate r.
+// Large splats (3.5-sigma radius above kWinMaxRadius px).  Their conic is stored
+// in a cancellation-free form: slot R_CA = a, R_CB = r = b / a, R_CC = D =
+// c - b^2 / a (all from FP64), so the exponent a dx^2 + 2b dx dy + c dy^2 is
+// evaluated as a (dx + r dy)^2 + D dy^2, a sum of two non-negative terms.  With the
+// plain (a, b, c) in FP32, the terms of a long, thin splat far from its centre
+// reach ~a r^2 and cancel; their rounding grew the blend's error past 1e-4.  These
+// splats take the blend's generic path and no strip windows (whose FP32 box bound
+// has the same cancellation); conic_abc() gives back (a, b, c).
 constexpr uint32_t kFlagNoWin = 32u;
 constexpr double kWinMaxRadius = 256.0;
+__host__ __device__ __forceinline__ void conic_abc(float a, float s1, float s2, uint32_t flags,
+                                                   float& b, float& c) {
+  if (flags & kFlagNoWin) {
+    b = s1 * a;
+    c = fmaf(a * s1, s1, s2);
+  } else {
+    b = s1;
+    c = s2;
+  }
+}
 constexpr int kFlagSpanShift = 6;
 // Splats whose weight can never reach the 0.99 clamp (c1 + |c2| bounds
 // (c1 + c2 E) g; 0.989 leaves room for FP32 rounding) skip the clamp and the

@@ -464,11 +464,16 @@ __global__ void HS_K1_BOUNDS preprocess_fwd_kernel(
   if (steep) side[i] = make_steep(st.mux, st.muy, st.za, st.zb);
   const float mux = (float)st.mux, muy = (float)st.muy;
   const __half2 lo = __floats2half2_rn((float)(st.mux - (double)mux), (float)(st.muy - (double)muy));
-  float4 r0 = make_float4(mux, muy, (float)(st.c / st.det), (float)(-st.b / st.det));
-  float4 r1 = make_float4((float)(st.a / st.det), (float)st.za, (float)st.zb, (float)st.c1);
+  // conic = inverse of the dilated covariance [[a, b], [b, c]]; a large splat stores
+  // (c/det, -b/c, 1/c) = (a_c, b_c / a_c, c_c - b_c^2 / a_c) instead (kFlagNoWin)
+  const bool large = st.radius > kWinMaxRadius;
+  float4 r0 = make_float4(mux, muy, (float)(st.c / st.det),
+                          large ? (float)(-st.b / st.c) : (float)(-st.b / st.det));
+  float4 r1 = make_float4(large ? (float)(1.0 / st.c) : (float)(st.a / st.det), (float)st.za,
+                          (float)st.zb, (float)st.c1);
   float4 r2 = make_float4((float)st.c2, (float)fmax(st.rgbu[0], 0.0), (float)fmax(st.rgbu[1], 0.0),
                           (float)fmax(st.rgbu[2], 0.0));
-  float4 r3 = make_float4((float)st.t[2], __uint_as_float(pack_flags(st.mode, steep, may_clamp(st.c1, st.c2), spans_x, st.bad, st.radius > kWinMaxRadius)),
+  float4 r3 = make_float4((float)st.t[2], __uint_as_float(pack_flags(st.mode, steep, may_clamp(st.c1, st.c2), spans_x, st.bad, large)),
                           __uint_as_float(0u), __uint_as_float(*reinterpret_cast<const uint32_t*>(&lo)));
   float4* dst = rec + 4 * i;
   dst[0] = r0;

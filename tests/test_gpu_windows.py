@@ -114,17 +114,17 @@ def test_occluded_view_matches_oracle(cuda):
                  {k: ref_g[k] for k in GRAD_GROUPS})
 
 
-def test_large_thin_splats_take_no_windows(cuda):
-    """Splats with a radius above 256 px (the FP32 box bound's safe range) are
-    evaluated on every strip; a scene of long, thin, large splats matches the oracle."""
+def test_large_thin_splats_stable_conic(cuda):
+    """Splats with a radius above 256 px carry the cancellation-free conic form, take the
+    generic blend path and no strip windows; a scene of long, thin, large splats matches
+    the oracle (images, gradients and the exported packed conic)."""
     from oracle import oracle as O
     rng = np.random.default_rng(4)
     sa = scenes.frustum(60, 1, 640, 480, seed=6, sig_lo=1.0, sig_hi=2.0)
-    # stretch every splat along one axis to 30-60x its width: radii of 100-420 px
-    # (longer, thinner splats reach the FP32 exponent's own cancellation limit,
-    # DESIGN.md 4, independent of the windows)
+    # stretch every splat along one axis to 60-150x its width: radii up to ~1000 px.
+    # Before the stable conic form (hs_common.cuh kFlagNoWin) alpha was 1.7e-4 off here.
     ls = sa.log_scale.astype(np.float64)
-    ls[:, 0] += np.log(rng.uniform(30.0, 60.0, len(ls)))
+    ls[:, 0] += np.log(rng.uniform(60.0, 150.0, len(ls)))
     sa.log_scale = ls.astype(np.float32)
     cam = CameraModel(**sa.cameras[0])
     sc = Scene(*(getattr(sa, f) for f in sa.FIELDS), sh_degree=sa.sh_degree,
@@ -144,3 +144,7 @@ def test_large_thin_splats_take_no_windows(cuda):
     g = device.render_backward(sc, cam, out, torch.as_tensor(d_color, dtype=torch.float32))
     assert_grads({k: getattr(g, k).double().cpu().numpy() for k in GRAD_GROUPS},
                  {k: ref_g[k] for k in GRAD_GROUPS})
+    # the export reconstructs (a, b, c) from the stable form
+    ex = out.frame.export()
+    np.testing.assert_allclose(ex["packed"][:, 2:5], ref.frame.packed[:, 2:5], rtol=2e-6,
+                               atol=1e-30)
