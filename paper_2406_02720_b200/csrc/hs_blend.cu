@@ -698,11 +698,16 @@ __device__ __forceinline__ float warp_reduce13_smem(const float (&v)[16], float*
 // kRowsBySortedPos: Seam 1 layout (row k = sorted pair index, 12 reference
 // columns).  Otherwise the generation-order layout: row = record origin +
 // ty*spans_x + tx, kRowFloats columns, consumed by K7.
-// kDyn (occluded views, BlendGeom::occluded): the partially-active path also
-// takes windows, masked by the halves that still hold an active pixel (exact:
-// inactive pixels contribute exact zeros).  7% faster on c4, but the extra
-// bodies cost 2-4% on c3, so it is a separate instantiation.
-template <bool kRowsBySortedPos, bool kDyn = false>
+// Inert pixels.  A pixel whose terminal count c is below the tile's largest is
+// inactive at the positions >= c that the reverse walk visits first.  Instead of
+// masking it per splat, it starts "inert": T = 0 and D = 0, which makes every
+// body contribute exact zeros for it (T_prev = 0, w T = 0, d_w = inv (0 - 0)) and
+// keeps it inert.  Its real T and D wait in shared memory and are restored at
+// position c - 1, when the warp reaches the next activation level (a warp-uniform
+// check per splat; the restore itself runs once per distinct count).  So every
+// position runs the all-active bodies with their strip windows, masked further by
+// the halves (pairs 0-1, 2-3) in which every pixel is still inert.
+template <bool kRowsBySortedPos>
 __global__ void HS_BWD_BOUNDS blend_bwd_kernel(
     BlendGeom g, float bg0, float bg1, float bg2, const float* __restrict__ d_color,
     const float* __restrict__ trans, const int32_t* __restrict__ terminal,
@@ -712,11 +717,14 @@ __global__ void HS_BWD_BOUNDS blend_bwd_kernel(
   constexpr int kCols = kRowsBySortedPos ? 12 : 13;
   __shared__ WarpStage stage_all[kBwdWarps];
   __shared__ int cnt_all[kBwdWarps][kPx][32];
+  __shared__ float tfin_all[kBwdWarps][kPx][32], dini_all[kBwdWarps][kPx][32];
   __shared__ __align__(16) float red_all[kBwdWarps][13 * kRedStride];
   float* red = red_all[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
   WarpStage& st = stage_all[threadIdx.x >> 5];
   int* cnt = &cnt_all[threadIdx.x >> 5][0][lane];
+  float* tfin = &tfin_all[threadIdx.x >> 5][0][lane];
+  float* dini = &dini_all[threadIdx.x >> 5][0][lane];
   for (;;) {
     const int tile = next_tile(g, lane);
     if (tile < 0) break;
@@ -728,7 +736,7 @@ __global__ void HS_BWD_BOUNDS blend_bwd_kernel(
     const float x0 = (float)(tx * kTile) + 0.5f, y0 = (float)(ty * kTile) + 0.5f;
     BwdPix P;
     P.cnt = cnt;
-    int maxc = 0, minc = 0x7fffffff;
+    int maxc = 0;
 #pragma unroll
     for (int i = 0; i < kPx; ++i) {
       const int p = i >> 1, h = i & 1;
@@ -745,27 +753,34 @@ __global__ void HS_BWD_BOUNDS blend_bwd_kernel(
         // suffix S starts at T_final * background; only dC.S is needed
         slot(P.D[p], h) = t * fmaf(dr, bg0, fmaf(dg, bg1, db * bg2));
         maxc = max(maxc, cnt[i * 32]);
-        minc = min(minc, cnt[i * 32]);
       } else {
-        // outside the image: always "active" with T = 0 and a zero cotangent,
-        // which contributes exact zeros (and keeps T_prev = 0 finite)
+        // outside the image: inert for good (T = 0, zero cotangent; count "infinite"
+        // so no activation level ever picks it)
         slot(P.T[p], h) = 0.f; cnt[i * 32] = 0x7fffffff; slot(P.dr[p], h) = 0.f;
         slot(P.dg[p], h) = 0.f; slot(P.db[p], h) = 0.f; slot(P.D[p], h) = 0.f;
       }
     }
-    minc = __reduce_min_sync(0xffffffffu, minc);
     maxc = __reduce_max_sync(0xffffffffu, maxc);
-    // kDyn: per half (pairs 0-1 / 2-3), positions at or past its largest count
-    int hmax_lo = 0, hmax_hi = 0;
-    if (kDyn) {
+    // park the pixels that start inactive; nxt = the next activation level (the
+    // largest count below maxc), hmax_* = each half's largest count
+    int nxt = -1, hmax_lo = 0, hmax_hi = 0;
 #pragma unroll
-      for (int i = 0; i < kPx; ++i) {
-        const int c = cnt[i * 32] == 0x7fffffff ? 0 : cnt[i * 32];
-        if (i < kPx / 2) hmax_lo = max(hmax_lo, c); else hmax_hi = max(hmax_hi, c);
+    for (int i = 0; i < kPx; ++i) {
+      const int p = i >> 1, h = i & 1;
+      const int c = cnt[i * 32];
+      if (c < maxc) {
+        tfin[i * 32] = slot(P.T[p], h);
+        dini[i * 32] = slot(P.D[p], h);
+        slot(P.T[p], h) = 0.f;
+        slot(P.D[p], h) = 0.f;
+        nxt = max(nxt, c);
       }
-      hmax_lo = __reduce_max_sync(0xffffffffu, hmax_lo);
-      hmax_hi = __reduce_max_sync(0xffffffffu, hmax_hi);
+      const int cm = c == 0x7fffffff ? 0 : c;
+      if (i < kPx / 2) hmax_lo = max(hmax_lo, cm); else hmax_hi = max(hmax_hi, cm);
     }
+    nxt = __reduce_max_sync(0xffffffffu, nxt);
+    hmax_lo = __reduce_max_sync(0xffffffffu, hmax_lo);
+    hmax_hi = __reduce_max_sync(0xffffffffu, hmax_hi);
     const int k0 = g.tile_starts[tile];
     if (!kRowsBySortedPos && lane == 0)
       last_rank[tile] =
@@ -805,49 +820,46 @@ __global__ void HS_BWD_BOUNDS blend_bwd_kernel(
       __syncwarp();
       for (int j = 0; j < nb; ++j) {
         const int pos = hi - j;
+        if (pos < nxt) {
+          // activation level nxt: its pixels are active from this position on
+#pragma unroll
+          for (int i = 0; i < kPx; ++i) {
+            const int p = i >> 1, h = i & 1;
+            if (cnt[i * 32] == nxt) {
+              slot(P.T[p], h) = tfin[i * 32];
+              slot(P.D[p], h) = dini[i * 32];
+            }
+          }
+          int m = -1;
+#pragma unroll
+          for (int i = 0; i < kPx; ++i) {
+            const int c = cnt[i * 32];
+            if (c < nxt) m = max(m, c);
+          }
+          nxt = __reduce_max_sync(0xffffffffu, m);
+        }
         const float4 q[4] = {st.rec[s][j][0], st.rec[s][j][1], st.rec[s][j][2], st.rec[s][j][3]};
         const SteepRec& side = st.side[s][j];
         const uint32_t flags = __float_as_uint(q[3].y);
-        const int mode = (int)(flags & 3u);
         BwdAcc a;
         // kRowsBySortedPos: the sorted position; else the row staged above
         const size_t row = kRowsBySortedPos ? (size_t)(k0 + pos) : (size_t)__float_as_int(q[3].z);
         const int vi = lane >> 1;
-        int key = st.win[s][j];
-        if (kDyn && pos >= minc) key &= ~3 | (pos < hmax_lo ? 1 : 0) | (pos < hmax_hi ? 2 : 0);
+        // halves in which every pixel is still inert contribute nothing: skip them
+        const int key = st.win[s][j] & (~3 | (pos < hmax_lo ? 1 : 0) | (pos < hmax_hi ? 2 : 0));
         if (key == 0 || key == 4) {
           // fast splat below 2^-27 on every live strip: a zero pair row, no reduction
           if (!(lane & 1) && vi < kCols) rows[row * kStride + vi] = 0.f;
           continue;
         }
-        if (pos < minc) {
-          switch (key) {
-            case 1: bwd_splat_fast<true, false, 0, 2>(q, side, pos, px, py0, P, a); break;
-            case 2: bwd_splat_fast<true, false, 2, 2>(q, side, pos, px, py0, P, a); break;
-            case 3: bwd_splat_fast<true, false, 0, 4>(q, side, pos, px, py0, P, a); break;
-            case 5: bwd_splat_fast<true, true, 0, 2>(q, side, pos, px, py0, P, a); break;
-            case 6: bwd_splat_fast<true, true, 2, 2>(q, side, pos, px, py0, P, a); break;
-            case 7: bwd_splat_fast<true, true, 0, 4>(q, side, pos, px, py0, P, a); break;
-            default: bwd_splat_generic(q, side, flags, pos, px, py0, P, a); break;
-          }
-        } else if (kDyn) {
-          switch (key) {
-            case 1: bwd_splat_fast<false, false, 0, 2>(q, side, pos, px, py0, P, a); break;
-            case 2: bwd_splat_fast<false, false, 2, 2>(q, side, pos, px, py0, P, a); break;
-            case 3: bwd_splat_fast<false, false, 0, 4>(q, side, pos, px, py0, P, a); break;
-            case 5: bwd_splat_fast<false, true, 0, 2>(q, side, pos, px, py0, P, a); break;
-            case 6: bwd_splat_fast<false, true, 2, 2>(q, side, pos, px, py0, P, a); break;
-            case 7: bwd_splat_fast<false, true, 0, 4>(q, side, pos, px, py0, P, a); break;
-            default: bwd_splat_generic(q, side, flags, pos, px, py0, P, a); break;
-          }
-        } else {
-          // partially active warp: every pair (windows here cost more in code size
-          // than they save unless the view is occluded: kDyn)
-          switch (key >> 2) {
-            case 0: bwd_splat_fast<false, false>(q, side, pos, px, py0, P, a); break;
-            case 1: bwd_splat_fast<false, true>(q, side, pos, px, py0, P, a); break;
-            default: bwd_splat_generic(q, side, flags, pos, px, py0, P, a); break;
-          }
+        switch (key) {
+          case 1: bwd_splat_fast<true, false, 0, 2>(q, side, pos, px, py0, P, a); break;
+          case 2: bwd_splat_fast<true, false, 2, 2>(q, side, pos, px, py0, P, a); break;
+          case 3: bwd_splat_fast<true, false, 0, 4>(q, side, pos, px, py0, P, a); break;
+          case 5: bwd_splat_fast<true, true, 0, 2>(q, side, pos, px, py0, P, a); break;
+          case 6: bwd_splat_fast<true, true, 2, 2>(q, side, pos, px, py0, P, a); break;
+          case 7: bwd_splat_fast<true, true, 0, 4>(q, side, pos, px, py0, P, a); break;
+          default: bwd_splat_generic(q, side, flags, pos, px, py0, P, a); break;
         }
         // per-lane partials -> the pair-row columns (_blend_py.py:16-18)
         const float ca = q[0].z, cb = a.cb, cc = a.cc, za = q[1].y, zb = q[1].z;
@@ -957,7 +969,7 @@ static int blend_grid(Kernel kernel, int warps, int n_work, int* cache) {
   const int want = (n_work + warps - 1) / warps;
   return want < *cache ? (want > 0 ? want : 1) : *cache;
 }
-static int g_fwd_grid = 0, g_bwd_grid[3] = {0, 0, 0};
+static int g_fwd_grid = 0, g_bwd_grid[2] = {0, 0};
 
 cudaError_t launch_blend_fwd(const BlendGeom& g, float bg0, float bg1, float bg2, float* color,
                              float* alpha, float* depth, float* trans, int32_t* terminal,
@@ -980,11 +992,6 @@ cudaError_t launch_blend_bwd(const BlendGeom& g, float bg0, float bg1, float bg2
   if (rows_by_sorted_pos)
     blend_bwd_kernel<true><<<blend_grid(blend_bwd_kernel<true>, kBwdWarps, g.n_work, &g_bwd_grid[1]),
                              kBwdWarps * 32, 0, stream>>>(
-        g, bg0, bg1, bg2, d_color, trans, terminal, rows, last_rank, rank_of);
-  else if (g.occluded)
-    blend_bwd_kernel<false, true><<<blend_grid(blend_bwd_kernel<false, true>, kBwdWarps, g.n_work,
-                                               &g_bwd_grid[2]),
-                                    kBwdWarps * 32, 0, stream>>>(
         g, bg0, bg1, bg2, d_color, trans, terminal, rows, last_rank, rank_of);
   else
     blend_bwd_kernel<false><<<blend_grid(blend_bwd_kernel<false>, kBwdWarps, g.n_work, &g_bwd_grid[0]),

@@ -401,11 +401,6 @@ static BlendGeom frame_geom(const hs_frame* frame, const FrameBufs& f, const Bin
   g.n_work = frame->n_tiles;
   g.tile_order = nullptr;
   g.work_counter = f.counters;
-  // mean tile list above HS_OCCLUDED_LIST pairs: occluded views (c4 2797, c5 2069; c3 415)
-#ifndef HS_OCCLUDED_LIST
-#define HS_OCCLUDED_LIST 1000
-#endif
-  g.occluded = frame->num_pairs > HS_OCCLUDED_LIST * (int64_t)frame->n_tiles;
   return g;
 }
 

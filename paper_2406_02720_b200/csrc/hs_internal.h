@@ -73,9 +73,6 @@ struct BlendGeom {
   int tile_lo, n_work;         // tiles [tile_lo, tile_lo + n_work)
   const int32_t* tile_order;   // optional work order (nullptr = natural)
   int* work_counter;           // zeroed before launch
-  // long tile lists (heavy occlusion): K6 also windows its partially-active path
-  // by the halves that still hold an active pixel (launch_blend_bwd)
-  int occluded = 0;
 };
 
 cudaError_t launch_blend_fwd(const BlendGeom& g, float bg0, float bg1, float bg2, float* color,
