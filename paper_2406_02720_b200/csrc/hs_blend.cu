@@ -501,17 +501,15 @@ struct BwdAcc {
 
 struct BwdPix {
   float2 T[kPairs], D[kPairs], dr[kPairs], dg[kPairs], db[kPairs];
-  const int* cnt;  // this lane's terminal counts, cnt[i * 32] (shared memory: keeps
-                   // 8 registers free on the ALL path, which never reads them)
+  const int* cnt;  // this lane's terminal counts, cnt[i * 32] (shared memory; read
+                   // by the generic path only)
 };
 
-// FAST: mode 0 or 2, FP32 z, no clamp.  Packed pixel pairs.  ALL: every pixel
-// of the warp is active at this position (pos < warp-min of the terminal
-// counts); otherwise inactive pixels are masked with selects and contribute
-// exact zeros (pixels terminated early, as in heavily occluded views).
-// Pairs [P0, P0 + NP) are evaluated; the others are outside the splat's strip
-// window and unchanged (see strip_window).
-template <bool ALL, bool STEEP, int P0 = 0, int NP = kPairs>
+// FAST: mode 0 or 2, FP32 z, no clamp.  Packed pixel pairs, no per-pixel masks:
+// pixels past their terminal count are inert (T = D = 0, see blend_bwd_kernel)
+// and contribute exact zeros.  Pairs [P0, P0 + NP) are evaluated; the others are
+// outside the splat's strip window and unchanged (see strip_window).
+template <bool STEEP, int P0 = 0, int NP = kPairs>
 __device__ __forceinline__ void bwd_splat_fast(const float4 (&q)[4], const SteepRec& side,
                                                int pos, float px, float py0, BwdPix& P,
                                                BwdAcc& out) {
@@ -538,16 +536,13 @@ __device__ __forceinline__ void bwd_splat_fast(const float4 (&q)[4], const Steep
     const float2 om = fadd2(f2(1.0f), neg2(w));
     const float2 inv = make_float2(rcp_approx(om.x), rcp_approx(om.y));  // 1 - w >= 0.01
     const float2 Tp = fmul2(P.T[p], inv);
-    const bool ax = ALL || pos < P.cnt[(2 * p) * 32], ay = ALL || pos < P.cnt[(2 * p + 1) * 32];
     float2 wt = fmul2(w, Tp);
-    if (!ALL) wt = make_float2(ax ? wt.x : 0.f, ay ? wt.y : 0.f);
     const float2 dcr = ffma2(P.dr[p], f2(cr), ffma2(P.dg[p], f2(cg), fmul2(P.db[p], f2(cb))));
     ar = ffma2(P.dr[p], wt, ar);
     ag = ffma2(P.dg[p], wt, ag);
     ab = ffma2(P.db[p], wt, ab);
     // d_w = T_prev*(dC.rgb) - (dC.S)/(1-w) = inv*(T*dcr - D) (_blend_cy.pyx:310-312)
     float2 d_w = fmul2(inv, ffma2(P.T[p], dcr, neg2(P.D[p])));
-    if (!ALL) d_w = make_float2(ax ? d_w.x : 0.f, ay ? d_w.y : 0.f);
     const float2 dwg = fmul2(d_w, gg);
     const float2 d_pow = fmul2(dwg, u);
     s0 = fadd2(s0, d_pow);
@@ -562,7 +557,7 @@ __device__ __forceinline__ void bwd_splat_fast(const float4 (&q)[4], const Steep
     q1 = ffma2(dz, o, q1);
     qz = ffma2(dz, zz, qz);
     P.D[p] = ffma2(wt, dcr, P.D[p]);
-    P.T[p] = ALL ? Tp : make_float2(ax ? Tp.x : P.T[p].x, ay ? Tp.y : P.T[p].y);
+    P.T[p] = Tp;
   }
   const float c2k = c2 * (2.0f * kInvSqrtPi);
   const float S0 = s0.x + s0.y, S1 = s1.x + s1.y, S2 = s2.x + s2.y;
@@ -853,12 +848,12 @@ __global__ void HS_BWD_BOUNDS blend_bwd_kernel(
           continue;
         }
         switch (key) {
-          case 1: bwd_splat_fast<true, false, 0, 2>(q, side, pos, px, py0, P, a); break;
-          case 2: bwd_splat_fast<true, false, 2, 2>(q, side, pos, px, py0, P, a); break;
-          case 3: bwd_splat_fast<true, false, 0, 4>(q, side, pos, px, py0, P, a); break;
-          case 5: bwd_splat_fast<true, true, 0, 2>(q, side, pos, px, py0, P, a); break;
-          case 6: bwd_splat_fast<true, true, 2, 2>(q, side, pos, px, py0, P, a); break;
-          case 7: bwd_splat_fast<true, true, 0, 4>(q, side, pos, px, py0, P, a); break;
+          case 1: bwd_splat_fast<false, 0, 2>(q, side, pos, px, py0, P, a); break;
+          case 2: bwd_splat_fast<false, 2, 2>(q, side, pos, px, py0, P, a); break;
+          case 3: bwd_splat_fast<false, 0, 4>(q, side, pos, px, py0, P, a); break;
+          case 5: bwd_splat_fast<true, 0, 2>(q, side, pos, px, py0, P, a); break;
+          case 6: bwd_splat_fast<true, 2, 2>(q, side, pos, px, py0, P, a); break;
+          case 7: bwd_splat_fast<true, 0, 4>(q, side, pos, px, py0, P, a); break;
           default: bwd_splat_generic(q, side, flags, pos, px, py0, P, a); break;
         }
         // per-lane partials -> the pair-row columns (_blend_py.py:16-18)
