@@ -574,8 +574,8 @@ __device__ __forceinline__ void bwd_splat_fast(const float4 (&q)[4], const Steep
   out.cc = q[1].x;
 }
 
-// Generic: steep, sign mode, clamped weights, partially active warps.  Scalar;
-// inactive pixels compute and contribute exact zeros.
+// Generic: sign mode, clamped weights, large splats (kFlagNoWin).  Scalar;
+// inert pixels (T = D = 0) compute and contribute exact zeros.
 __device__ __forceinline__ void bwd_splat_generic(const float4 (&q)[4], const SteepRec& side,
                                                   uint32_t flags, int pos, float px, float py0,
                                                   BwdPix& P, BwdAcc& a) {
@@ -596,7 +596,6 @@ __device__ __forceinline__ void bwd_splat_generic(const float4 (&q)[4], const St
     float& T = slot(P.T[p], h);
     float& D = slot(P.D[p], h);
     const float dr = slot(P.dr[p], h), dg = slot(P.dg[p], h), db = slot(P.db[p], h);
-    const bool active = pos < P.cnt[i * 32];
     const float dy = s.dy0 + 2.0f * i;
     const float ul = fmaf(q[0].w, dy, s.dx);
     const float gg = ex2_approx(large ? fmaf(s.A * ul, ul, s.C * dy * dy)
@@ -608,13 +607,13 @@ __device__ __forceinline__ void bwd_splat_generic(const float4 (&q)[4], const St
     const float w = fminf(w_raw, kWeightClamp);
     const float inv = rcp_approx(1.0f - w);
     const float Tp = T * inv;
-    const float wt = active ? w * Tp : 0.0f;
+    const float wt = w * Tp;  // inert pixels (T = D = 0) give exact zeros throughout
     const float dcr = fmaf(dr, cr, fmaf(dg, cg, db * cb));
     a.r = fmaf(dr, wt, a.r);
     a.g = fmaf(dg, wt, a.g);
     a.b = fmaf(db, wt, a.b);
     // gated on the unclamped weight (_blend_cy.pyx:309)
-    const float d_w = (active && w_raw <= kWeightClamp) ? inv * fmaf(T, dcr, -D) : 0.0f;
+    const float d_w = w_raw <= kWeightClamp ? inv * fmaf(T, dcr, -D) : 0.0f;
     const float dwg = d_w * gg;
     const float d_pow = dwg * u;
     a.s0 += d_pow;
@@ -627,7 +626,7 @@ __device__ __forceinline__ void bwd_splat_generic(const float4 (&q)[4], const St
     a.q1 = fmaf(d_z, dy, a.q1);
     a.qz = fmaf(d_z, zz, a.qz);
     D = fmaf(wt, dcr, D);
-    T = active ? Tp : T;
+    T = Tp;
   }
 }
 
