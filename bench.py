@@ -500,7 +500,9 @@ def main():
     roofline = {
         "bound": "fp32", "kernel": "blend_bwd (K6)", "achieved": achieved, "peak": fp32_peak,
         "unit": "TFLOP/s", "frac": achieved / fp32_peak,
-        "traffic": (tr := committed_traffic("blend_bwd")) and tr["bytes_per_launch"],
+        # the committed ncu captures are of c3: other configs report no traffic
+        "traffic": (tr := committed_traffic("blend_bwd") if args.config == "c3" else None)
+        and tr["bytes_per_launch"],
         "traffic_source": tr and tr["source"],
         "traffic_hbm_frac": tr and tr["bytes_per_launch"] / (bwd_ms * 1e-3) / 1e9 / HBM_PEAK_GBS,
         "peak_source": "measured on this GPU by hs_measure_fp32_peaks (FMA probe; "

@@ -569,19 +569,41 @@ __global__ void __launch_bounds__(256) merge_rows_kernel(
   const int base = __float_as_int(r3.z) + rc.z * spans_x + rc.x;
   const int r = (int)rank_of[i];
   int lx = 0, ly = 0;
-  for (int l = 0; l < cnt; ++l) {
+  auto next_tile_of = [&]() {
     const int tile = (rc.z + ly) * tiles_x + rc.x + lx;
     if (++lx == spans_x) {
       lx = 0;
       ++ly;
     }
+    return tile;
+  };
+  auto load_row = [&](int l, float4 (&u)[4]) {
     const float4* row = reinterpret_cast<const float4*>(rows + (size_t)(base + l) * kRowFloats);
-    const float4 u0 = row[0], u1 = row[1], u2 = row[2], u3 = row[3];
-    if (r > last_rank[tile]) continue;
-    m[0] += u0.x; m[1] += u0.y; m[2] += u0.z; m[3] += u0.w;
-    m[4] += u1.x; m[5] += u1.y; m[6] += u1.z; m[7] += u1.w;
-    m[8] += u2.x; m[9] += u2.y; m[10] += u2.z; m[11] += u2.w;
-    m[12] += u3.x;
+    u[0] = row[0]; u[1] = row[1]; u[2] = row[2]; u[3] = row[3];
+  };
+  auto add_row = [&](const float4 (&u)[4]) {
+    m[0] += u[0].x; m[1] += u[0].y; m[2] += u[0].z; m[3] += u[0].w;
+    m[4] += u[1].x; m[5] += u[1].y; m[6] += u[1].z; m[7] += u[1].w;
+    m[8] += u[2].x; m[9] += u[2].y; m[10] += u[2].z; m[11] += u[2].w;
+    m[12] += u[3].x;
+  };
+  // two rows (and their tiles' last ranks) in flight per step: the gathers are
+  // independent, the additions keep the row order (bitwise the same sum)
+  int l = 0;
+  for (; l + 1 < cnt; l += 2) {
+    const int t0 = next_tile_of(), t1 = next_tile_of();
+    float4 u[4], v[4];
+    load_row(l, u);
+    load_row(l + 1, v);
+    const int lr0 = last_rank[t0], lr1 = last_rank[t1];
+    if (r <= lr0) add_row(u);
+    if (r <= lr1) add_row(v);
+  }
+  if (l < cnt) {
+    const int t0 = next_tile_of();
+    float4 u[4];
+    load_row(l, u);
+    if (r <= last_rank[t0]) add_row(u);
   }
   // colour clamp (rasterizer.py:544): the record holds max(rgb, 0), which is > 0
   // exactly when the unclamped FP64 colour is, so the gradient of a clamped
