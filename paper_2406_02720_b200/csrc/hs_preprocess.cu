@@ -587,23 +587,33 @@ __global__ void __launch_bounds__(256) merge_rows_kernel(
     m[8] += u[2].x; m[9] += u[2].y; m[10] += u[2].z; m[11] += u[2].w;
     m[12] += u[3].x;
   };
-  // two rows (and their tiles' last ranks) in flight per step: the gathers are
-  // independent, the additions keep the row order (bitwise the same sum)
+  // HS_K7A_ROWS rows in flight per step: the tiles' last ranks first, then the
+  // gathers of the rows below them only (rows past a tile's last composited
+  // rank were never written, and at c5 they are most of them), additions in
+  // row order (bitwise the same sum)
+#ifndef HS_K7A_ROWS
+#define HS_K7A_ROWS 2
+#endif
+  constexpr int U = HS_K7A_ROWS;
   int l = 0;
-  for (; l + 1 < cnt; l += 2) {
-    const int t0 = next_tile_of(), t1 = next_tile_of();
-    float4 u[4], v[4];
-    load_row(l, u);
-    load_row(l + 1, v);
-    const int lr0 = last_rank[t0], lr1 = last_rank[t1];
-    if (r <= lr0) add_row(u);
-    if (r <= lr1) add_row(v);
+  for (; l + U <= cnt; l += U) {
+    int lr[U];
+    float4 u[U][4];
+#pragma unroll
+    for (int k = 0; k < U; ++k) lr[k] = last_rank[next_tile_of()];
+#pragma unroll
+    for (int k = 0; k < U; ++k)
+      if (r <= lr[k]) load_row(l + k, u[k]);
+#pragma unroll
+    for (int k = 0; k < U; ++k)
+      if (r <= lr[k]) add_row(u[k]);
   }
-  if (l < cnt) {
-    const int t0 = next_tile_of();
+  for (; l < cnt; ++l) {
+    const int tl = next_tile_of();
+    if (r > last_rank[tl]) continue;
     float4 u[4];
     load_row(l, u);
-    if (r <= last_rank[t0]) add_row(u);
+    add_row(u);
   }
   // colour clamp (rasterizer.py:544): the record holds max(rgb, 0), which is > 0
   // exactly when the unclamped FP64 colour is, so the gradient of a clamped
