@@ -235,15 +235,31 @@ cudaError_t run_pair_sort(void* temp, size_t temp_bytes, uint32_t* keys0, uint32
 
 // K4: CSR tile offsets (np.searchsorted(tile_sorted, arange(T+1)),
 // rasterizer.py:324-325).  Every entry is written exactly once.
+// K4: tile_starts[u] = first sorted pair of tile >= u.  Each thread takes four
+// consecutive keys with one 16-B load (the sorted keys come from CUB's 256-B
+// aligned buffers) and writes the starts of the tiles that begin at them.
+__device__ __forceinline__ void tile_starts_at(int64_t k, int t, int& prev,
+                                               int32_t* __restrict__ starts) {
+  for (int u = prev + 1; u <= t; ++u) starts[u] = (int32_t)k;
+  prev = t;
+}
+
 __global__ void tile_ranges_kernel(const uint32_t* __restrict__ keys, int64_t p, int n_tiles,
                                    int32_t* __restrict__ starts) {
-  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= p) return;
-  const int t = (int)keys[k];
-  const int tp = k == 0 ? -1 : (int)keys[k - 1];
-  for (int u = tp + 1; u <= t; ++u) starts[u] = (int32_t)k;
-  if (k == p - 1)
-    for (int u = t + 1; u <= n_tiles; ++u) starts[u] = (int32_t)p;
+  const int64_t k0 = 4 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
+  if (k0 >= p) return;
+  int prev = k0 == 0 ? -1 : (int)keys[k0 - 1];
+  if (k0 + 4 <= p && !((uintptr_t)keys & 15)) {
+    const uint4 v = reinterpret_cast<const uint4*>(keys)[k0 >> 2];
+    tile_starts_at(k0, (int)v.x, prev, starts);
+    tile_starts_at(k0 + 1, (int)v.y, prev, starts);
+    tile_starts_at(k0 + 2, (int)v.z, prev, starts);
+    tile_starts_at(k0 + 3, (int)v.w, prev, starts);
+  } else {
+    for (int64_t k = k0; k < p && k < k0 + 4; ++k) tile_starts_at(k, (int)keys[k], prev, starts);
+  }
+  if (k0 + 4 >= p)  // the thread holding the last pair closes the table
+    for (int u = prev + 1; u <= n_tiles; ++u) starts[u] = (int32_t)p;
 }
 
 __global__ void fill_i32_kernel(int32_t* __restrict__ a, int64_t n, int32_t v) {
@@ -258,7 +274,8 @@ cudaError_t run_tile_ranges(const uint32_t* sorted_keys, int64_t p, int n_tiles,
     fill_i32_kernel<<<(unsigned)((n_tiles + 1 + block - 1) / block), block, 0, stream>>>(
         tile_starts, n_tiles + 1, 0);
   } else {
-    tile_ranges_kernel<<<(unsigned)((p + block - 1) / block), block, 0, stream>>>(
+    const int64_t threads = (p + 3) / 4;
+    tile_ranges_kernel<<<(unsigned)((threads + block - 1) / block), block, 0, stream>>>(
         sorted_keys, p, n_tiles, tile_starts);
   }
   note_launch();
