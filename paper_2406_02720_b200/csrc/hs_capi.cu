@@ -469,11 +469,13 @@ int hs_preprocess_bwd_range(hs_frame* frame, const hs_scene* scene, const hs_cam
   if (scene->dtype == HS_DTYPE_F32) {
     HS_CUDA(launch_preprocess_bwd_t<float>(scene_args<float>(scene), ca, frame->kernel, frame->n,
                                            frame->tiles_x, f.rec, f.rect, f.count, f.rank_of,
-                                           f.last_rank, b.rows, f.merged, ranged(grad_args<float>(grads), begin, end), stream));
+                                           f.last_rank, b.rows, f.merged, frame->num_pairs,
+                                           ranged(grad_args<float>(grads), begin, end), stream));
   } else {
     HS_CUDA(launch_preprocess_bwd_t<double>(scene_args<double>(scene), ca, frame->kernel,
                                             frame->n, frame->tiles_x, f.rec, f.rect, f.count,
                                             f.rank_of, f.last_rank, b.rows, f.merged,
+                                            frame->num_pairs,
                                             ranged(grad_args<double>(grads), begin, end),
                                             stream));
   }

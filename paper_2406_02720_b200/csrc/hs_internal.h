@@ -57,7 +57,8 @@ cudaError_t launch_preprocess_bwd_t(const SceneArgs<T>& sc, const CamArgs& cam, 
                                     int64_t n, int tiles_x, const float4* rec, const int4* rect,
                                     const int32_t* count, const uint32_t* rank_of,
                                     const int32_t* last_rank, const float* rows, float4* merged,
-                                    const GradArgs<T>& out, cudaStream_t stream);
+                                    int64_t num_pairs, const GradArgs<T>& out,
+                                    cudaStream_t stream);
 
 template <typename T>
 cudaError_t launch_screen_splats_t(const SceneArgs<T>& sc, const CamArgs& cam, int kernel,

@@ -551,28 +551,44 @@ template cudaError_t launch_screen_splats_t<double>(const SceneArgs<double>&, co
 // the tiles of its rect in row-major (= sorted k) order, skipping pairs past
 // the tile's last composited position (never written by K6).  A separate,
 // register-light kernel so the dependent gathers are hidden by occupancy.
+// G lanes per splat (a power of two <= 32): lane j of the group takes rows
+// j, j + G, ... and the group's partial sums meet in a fixed xor-shuffle tree,
+// so the result is deterministic (G = 1: plain row-order sums).  The launcher
+// picks G from the frame's mean rows per primitive (HS_K7A_WIDE_ROWS).
+template <int G>
 __global__ void __launch_bounds__(256) merge_rows_kernel(
     int64_t n, int tiles_x, const float4* __restrict__ rec, const int4* __restrict__ rect,
     const int32_t* __restrict__ count, const uint32_t* __restrict__ rank_of,
     const int32_t* __restrict__ last_rank, const float* __restrict__ rows,
     float4* __restrict__ merged, int64_t begin) {
-  const int64_t i = begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int cnt = count[i];
-  if (cnt == 0) return;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t i = begin + tid / G;
+  const int sub = (int)(tid % G);
+  // with G > 1 every lane stays to the shuffles (a group never straddles a warp)
+  const int cnt = i < n ? count[i] : 0;
+  if (G == 1 && cnt == 0) return;
   double m[13];
 #pragma unroll
   for (int k = 0; k < 13; ++k) m[k] = 0.0;
-  const int4 rc = rect[i];
-  const int spans_x = rc.y - rc.x + 1;
-  const float4 r2 = rec[4 * i + 2], r3 = rec[4 * i + 3];
-  const int base = __float_as_int(r3.z) + rc.z * spans_x + rc.x;
-  const int r = (int)rank_of[i];
-  int lx = 0, ly = 0;
+  int4 rc = make_int4(0, 0, 0, 0);
+  int spans_x = 1, base = 0, r = 0;
+  float4 r2 = make_float4(0.f, 0.f, 0.f, 0.f), r3 = r2;
+  if (cnt > 0) {
+    rc = rect[i];
+    spans_x = rc.y - rc.x + 1;
+    r2 = rec[4 * i + 2];
+    r3 = rec[4 * i + 3];
+    base = __float_as_int(r3.z) + rc.z * spans_x + rc.x;
+    r = (int)rank_of[i];
+  }
+  // row l of the splat is tile (rc.z + l / spans_x, rc.x + l % spans_x); the
+  // lane walks l = sub, sub + G, ... keeping (lx, ly) incrementally
+  int ly = sub / spans_x, lx = sub - ly * spans_x;
   auto next_tile_of = [&]() {
     const int tile = (rc.z + ly) * tiles_x + rc.x + lx;
-    if (++lx == spans_x) {
-      lx = 0;
+    lx += G;
+    while (lx >= spans_x) {
+      lx -= spans_x;
       ++ly;
     }
     return tile;
@@ -595,25 +611,32 @@ __global__ void __launch_bounds__(256) merge_rows_kernel(
 #define HS_K7A_ROWS 2
 #endif
   constexpr int U = HS_K7A_ROWS;
-  int l = 0;
-  for (; l + U <= cnt; l += U) {
+  int l = sub;
+  for (; l + (U - 1) * G < cnt; l += U * G) {
     int lr[U];
     float4 u[U][4];
 #pragma unroll
     for (int k = 0; k < U; ++k) lr[k] = last_rank[next_tile_of()];
 #pragma unroll
     for (int k = 0; k < U; ++k)
-      if (r <= lr[k]) load_row(l + k, u[k]);
+      if (r <= lr[k]) load_row(l + k * G, u[k]);
 #pragma unroll
     for (int k = 0; k < U; ++k)
       if (r <= lr[k]) add_row(u[k]);
   }
-  for (; l < cnt; ++l) {
+  for (; l < cnt; l += G) {
     const int tl = next_tile_of();
     if (r > last_rank[tl]) continue;
     float4 u[4];
     load_row(l, u);
     add_row(u);
+  }
+  if (G > 1) {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1)
+#pragma unroll
+      for (int k = 0; k < 13; ++k) m[k] += __shfl_xor_sync(0xffffffffu, m[k], o, G);
+    if (sub != 0 || cnt == 0) return;
   }
   // colour clamp (rasterizer.py:544): the record holds max(rgb, 0), which is > 0
   // exactly when the unclamped FP64 colour is, so the gradient of a clamped
@@ -1133,13 +1156,23 @@ cudaError_t launch_preprocess_bwd_t(const SceneArgs<T>& sc, const CamArgs& cam, 
                                     int64_t n, int tiles_x, const float4* rec, const int4* rect,
                                     const int32_t* count, const uint32_t* rank_of,
                                     const int32_t* last_rank, const float* rows, float4* merged,
-                                    const GradArgs<T>& out, cudaStream_t stream) {
+                                    int64_t num_pairs, const GradArgs<T>& out,
+                                    cudaStream_t stream) {
   // the launch covers primitives [out.begin, out.end): K7a and K7 over that range only
   const int64_t end = out.end < n ? out.end : n;
   if (end <= out.begin) return cudaSuccess;
   const int64_t cnt = end - out.begin;
-  merge_rows_kernel<<<(unsigned)((cnt + 255) / 256), 256, 0, stream>>>(
-      end, tiles_x, rec, rect, count, rank_of, last_rank, rows, merged, out.begin);
+  // wide splats (c5: ~134 rows per primitive) take 8 lanes each; at c1-c4
+  // (3-4 rows) one lane per splat is faster (measured)
+#ifndef HS_K7A_WIDE_ROWS
+#define HS_K7A_WIDE_ROWS 32
+#endif
+  if (num_pairs >= (int64_t)HS_K7A_WIDE_ROWS * n)
+    merge_rows_kernel<8><<<(unsigned)((cnt * 8 + 255) / 256), 256, 0, stream>>>(
+        end, tiles_x, rec, rect, count, rank_of, last_rank, rows, merged, out.begin);
+  else
+    merge_rows_kernel<1><<<(unsigned)((cnt + 255) / 256), 256, 0, stream>>>(
+        end, tiles_x, rec, rect, count, rank_of, last_rank, rows, merged, out.begin);
   note_launch();
 #ifndef HS_K7_NT_F32
 #define HS_K7_NT_F32 128
@@ -1168,13 +1201,14 @@ cudaError_t launch_preprocess_bwd_t(const SceneArgs<T>& sc, const CamArgs& cam, 
 template cudaError_t launch_preprocess_bwd_t<float>(const SceneArgs<float>&, const CamArgs&, int,
                                                     int64_t, int, const float4*, const int4*,
                                                     const int32_t*, const uint32_t*, const int32_t*,
-                                                    const float*, float4*, const GradArgs<float>&,
-                                                    cudaStream_t);
+                                                    const float*, float4*, int64_t,
+                                                    const GradArgs<float>&, cudaStream_t);
 template cudaError_t launch_preprocess_bwd_t<double>(const SceneArgs<double>&, const CamArgs&, int,
                                                      int64_t, int, const float4*, const int4*,
                                                      const int32_t*, const uint32_t*,
                                                      const int32_t*, const float*, float4*,
-                                                     const GradArgs<double>&, cudaStream_t);
+                                                     int64_t, const GradArgs<double>&,
+                                                     cudaStream_t);
 #endif  // HS_GEOMETRY_BWD_TU
 
 }  // namespace hs

@@ -216,3 +216,27 @@ def test_steep_and_sign_mode_splats_oracle(cuda):
                "terminal": ref_out.per_pixel_terminal_index}
         assert_images(got, ref)
         assert_grads(got, ref_g)
+
+
+def test_wide_splat_row_merge_oracle(cuda):
+    """Large splats (c5-like sigma 8-40 px): the frame's mean rows per primitive is
+    >= 32, so K7a merges each splat's rows with 8 lanes and a shuffle tree
+    (HS_K7A_WIDE_ROWS) instead of one lane in row order.  Integers bit-exact,
+    images and gradients within the parity contract against the FP64 oracle."""
+    O = _oracle()
+    sa = scenes.frustum(800, 2, 320, 240, seed=31, sig_lo=8.0, sig_hi=40.0, clustered=True,
+                        dup=0.1)
+    s64 = sa.as_float64()
+    cam = CameraModel(**sa.cameras[0])
+    d_color = scenes.cotangent(cam.height, cam.width, seed=9)
+    ref_out = O.render(s64, cam)
+    ref_g = O.render_backward(s64, cam, ref_out, d_color)
+    f = ref_out.frame
+    assert len(f.pair_splat) >= 32 * len(sa.mu)  # the wide merge path is the one taken
+    got = run_gpu(sa, 0, "half", torch.float32, d_color)
+    assert np.array_equal(got["pair_splat"], f.pair_splat)
+    assert np.array_equal(got["tile_starts"], f.tile_starts)
+    ref = {"color": ref_out.color, "alpha": ref_out.alpha, "depth": ref_out.depth,
+           "transmittance": ref_out.transmittance, "terminal": ref_out.per_pixel_terminal_index}
+    assert_images(got, ref)
+    assert_grads(got, ref_g)
