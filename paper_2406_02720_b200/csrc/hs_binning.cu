@@ -81,9 +81,45 @@ __global__ void depth_run_rank_kernel(const uint64_t* __restrict__ keys,
     newpos[k] = (uint32_t)k;
     return;
   }
-  int64_t s = k, e = k + 1;
-  while (s > 0 && (uint32_t)(keys[s - 1] >> 32) == hi && k - s < kMaxDepthRun) --s;
-  while (e < n && (uint32_t)(keys[e] >> 32) == hi && e - s <= kMaxDepthRun) ++e;
+  // The run's bounds by galloping then bisecting over the sorted upper bits:
+  // O(log run) dependent loads instead of O(run).  s = first index >= lo with
+  // this hi; e = first index in (k, cap) with another hi, else cap -- the same
+  // bounds a linear walk capped at kMaxDepthRun finds.
+  auto same = [&](int64_t j) { return (uint32_t)(keys[j] >> 32) == hi; };
+  const int64_t lo = k - kMaxDepthRun > 0 ? k - kMaxDepthRun : 0;
+  int64_t good = k, bad = lo - 1;
+  for (int64_t step = 1;; step <<= 1) {
+    const int64_t c = good - step;
+    if (c < lo) break;
+    if (same(c)) {
+      good = c;
+    } else {
+      bad = c;
+      break;
+    }
+  }
+  while (good - bad > 1) {
+    const int64_t mid = bad + (good - bad) / 2;
+    if (same(mid)) good = mid; else bad = mid;
+  }
+  const int64_t s = good;
+  const int64_t cap = s + kMaxDepthRun + 1 < n ? s + kMaxDepthRun + 1 : n;
+  int64_t in = k, out = cap;  // same(in); out = cap or an index with another hi
+  for (int64_t step = 1;; step <<= 1) {
+    const int64_t c = in + step;
+    if (c >= cap) break;
+    if (same(c)) {
+      in = c;
+    } else {
+      out = c;
+      break;
+    }
+  }
+  while (out - in > 1) {
+    const int64_t mid = in + (out - in) / 2;
+    if (same(mid)) in = mid; else out = mid;
+  }
+  const int64_t e = out;
   if (e - s > kMaxDepthRun || k - s >= kMaxDepthRun) {
     atomicExch(overflow, 1);
     newpos[k] = (uint32_t)k;
