@@ -252,6 +252,12 @@ size_t hs_loss_workspace_size(int32_t height, int32_t width, int32_t channels);
 int hs_loss(const float* rendered, const float* target, int32_t height, int32_t width,
             int32_t channels, double lambda_ssim, double* loss4, float* d_rendered,
             double* d_rendered_f64, void* ws, size_t ws_bytes, void* stream);
+/* hs_loss on float64 images (a reference caller's arrays, e.g. uint8/255
+ * targets): same outputs, workspace and errors; the FP64 arithmetic then sees
+ * the inputs unrounded, as loss.py does. */
+int hs_loss_f64(const double* rendered, const double* target, int32_t height, int32_t width,
+                int32_t channels, double lambda_ssim, double* loss4, float* d_rendered,
+                double* d_rendered_f64, void* ws, size_t ws_bytes, void* stream);
 
 /* ---- optimizer: per-group Adam, the step after K7 ----------------------- */
 
@@ -411,6 +417,9 @@ int hs_measure_fp32_peaks(double* fma_tflops, double* ex2_gops);
 /* Packed FP32 (fma.rn.f32x2) throughput measured by the last
  * hs_measure_fp32_peaks call, TFLOP/s. */
 double hs_last_fma2_tflops(void);
+/* Evaluates the blend kernels' FP32 erf (the one K5/K6 use, on MUFU.EX2) at n
+ * device points z -> out: a test probe for its accuracy and oddness. */
+int hs_probe_erf32(const float* z, float* out, int64_t n, void* stream);
 
 #ifdef __cplusplus
 }

@@ -534,6 +534,7 @@ typedef struct {
   int32_t* tile_rect;
   int32_t* pair_splat;
   int64_t* tile_starts;
+  int32_t* radii; /* (n,) ceil(3.5 sqrt(lambda_max)) of rasterizer.py:194-200, 0 if culled */
 } oracle_frame;
 
 static const double* g_sort_depth;
@@ -553,6 +554,7 @@ void oracle_frame_free(oracle_frame* f) {
   free(f->tile_rect);
   free(f->pair_splat);
   free(f->tile_starts);
+  free(f->radii);
   free(f);
 }
 
@@ -584,11 +586,13 @@ oracle_frame* oracle_prepare(const double* mu, const double* log_scale, const do
   double* rec = (double*)malloc(sizeof(double) * 13 * (n > 0 ? n : 1));
   int8_t* md = (int8_t*)malloc(n > 0 ? n : 1);
   int32_t* rect = (int32_t*)malloc(sizeof(int32_t) * 4 * (n > 0 ? n : 1));
+  f->radii = (int32_t*)calloc(n > 0 ? n : 1, sizeof(int32_t));
 #pragma omp parallel for schedule(static) num_threads(threads)
   for (int64_t i = 0; i < n; ++i) {
     splat_t s;
     vis[i] = (char)splat_state(&f->sc, &f->cam, kernel, i, &s);
     if (!vis[i]) continue;
+    f->radii[i] = (int32_t)ceil(s.radius);
     double* r = rec + 13 * i;
     r[0] = s.mux; r[1] = s.muy;
     r[2] = s.c / s.det; r[3] = -s.b / s.det; r[4] = s.a / s.det;
@@ -672,6 +676,11 @@ void oracle_frame_get(const oracle_frame* f, int64_t* valid, double* packed, int
   if (tile_rect) memcpy(tile_rect, f->tile_rect, sizeof(int32_t) * 4 * f->m);
   if (pair_splat) memcpy(pair_splat, f->pair_splat, sizeof(int32_t) * f->p);
   if (tile_starts) memcpy(tile_starts, f->tile_starts, sizeof(int64_t) * (n_tiles + 1));
+}
+
+/* radii (N,): int32 ceil of the influence radius (rasterizer.py:194-200), 0 when culled */
+void oracle_frame_radii(const oracle_frame* f, int32_t* radii) {
+  memcpy(radii, f->radii, sizeof(int32_t) * f->sc.n);
 }
 
 /* render (rasterizer.py:351-383) over all tiles */

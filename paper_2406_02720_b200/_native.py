@@ -136,6 +136,8 @@ _SIGNATURES = {
     "hs_loss_workspace_size": (c_size_t, [c_int32, c_int32, c_int32]),
     "hs_loss": (c_int32, [c_void_p, c_void_p, c_int32, c_int32, c_int32, ctypes.c_double,
                           c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
+    "hs_loss_f64": (c_int32, [c_void_p, c_void_p, c_int32, c_int32, c_int32, ctypes.c_double,
+                              c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
     "hs_adam_step": (c_int32, [ctypes.POINTER(HsScene), ctypes.POINTER(HsGrads),
                                ctypes.POINTER(HsAdamState), ctypes.POINTER(ctypes.c_double),
                                c_int32, c_void_p]),
@@ -167,6 +169,7 @@ _SIGNATURES = {
     "hs_measure_fp32_peaks": (c_int32, [ctypes.POINTER(ctypes.c_double),
                                         ctypes.POINTER(ctypes.c_double)]),
     "hs_last_fma2_tflops": (ctypes.c_double, []),
+    "hs_probe_erf32": (c_int32, [c_void_p, c_void_p, c_int64, c_void_p]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGNATURES)

@@ -9,6 +9,7 @@ header is newer than the library.
 """
 
 import argparse
+import concurrent.futures
 import os
 import shutil
 import subprocess
@@ -67,12 +68,20 @@ def build(force=False, verbose=False):
         return LIB_PATH
     nvcc = nvcc_path()
     os.makedirs(OBJ_DIR, exist_ok=True)
-    objs = []
-    logs = []
-    for src, extra in SOURCES.items():
+
+    def compile_one(item):
+        src, extra = item
         obj = os.path.join(OBJ_DIR, src.replace(".cu", ".o"))
         cmd = [nvcc, *ARCH, *COMMON, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
-        res = subprocess.run(cmd, capture_output=True, text=True)
+        return src, obj, subprocess.run(cmd, capture_output=True, text=True)
+
+    # one nvcc per translation unit, in parallel (the FP64 units dominate)
+    jobs = max(1, min(len(SOURCES), os.cpu_count() or 1))
+    with concurrent.futures.ThreadPoolExecutor(jobs) as pool:
+        results = list(pool.map(compile_one, SOURCES.items()))
+    objs = []
+    logs = []
+    for src, obj, res in results:
         logs.append(res.stderr)
         if res.returncode != 0:
             sys.stderr.write(res.stdout + res.stderr)

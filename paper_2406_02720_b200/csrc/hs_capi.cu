@@ -702,10 +702,12 @@ extern "C" size_t hs_loss_workspace_size(int32_t height, int32_t width, int32_t 
   return bytes;
 }
 
-extern "C" int hs_loss(const float* rendered, const float* target, int32_t height, int32_t width,
-                       int32_t channels, double lambda_ssim, double* loss4, float* d_rendered,
-                       double* d_rendered_f64, void* ws, size_t ws_bytes, void* stream_) {
-  if (!rendered || !target || !loss4 || height <= 0 || width <= 0 || channels <= 0)
+static int loss_impl(const float* rendered, const float* target, const double* rendered64,
+                     const double* target64, int32_t height, int32_t width, int32_t channels,
+                     double lambda_ssim, double* loss4, float* d_rendered,
+                     double* d_rendered_f64, void* ws, size_t ws_bytes, void* stream_) {
+  if (!((rendered && target) || (rendered64 && target64)) || !loss4 || height <= 0 ||
+      width <= 0 || channels <= 0)
     return HS_ERR_INVALID_ARG;
   if (!(lambda_ssim >= 0.0 && lambda_ssim <= 1.0)) return HS_ERR_INVALID_LAMBDA;
   const bool ssim = lambda_ssim != 0.0;  // loss.py:97-103: lambda 0 skips SSIM
@@ -717,6 +719,8 @@ extern "C" int hs_loss(const float* rendered, const float* target, int32_t heigh
   hs::LossArgs a;
   a.x = rendered;
   a.y = target;
+  a.x64 = rendered64;
+  a.y64 = target64;
   a.width = width;
   a.height = height;
   a.channels = channels;
@@ -747,6 +751,23 @@ extern "C" int hs_loss(const float* rendered, const float* target, int32_t heigh
   for (int k = 0; k < 11; ++k) a.win[k] /= sum;
   HS_CUDA(hs::launch_loss(a, static_cast<cudaStream_t>(stream_)));
   return HS_OK;
+}
+
+extern "C" int hs_loss(const float* rendered, const float* target, int32_t height, int32_t width,
+                       int32_t channels, double lambda_ssim, double* loss4, float* d_rendered,
+                       double* d_rendered_f64, void* ws, size_t ws_bytes, void* stream_) {
+  if (!rendered || !target) return HS_ERR_INVALID_ARG;
+  return loss_impl(rendered, target, nullptr, nullptr, height, width, channels, lambda_ssim,
+                   loss4, d_rendered, d_rendered_f64, ws, ws_bytes, stream_);
+}
+
+extern "C" int hs_loss_f64(const double* rendered, const double* target, int32_t height,
+                           int32_t width, int32_t channels, double lambda_ssim, double* loss4,
+                           float* d_rendered, double* d_rendered_f64, void* ws, size_t ws_bytes,
+                           void* stream_) {
+  if (!rendered || !target) return HS_ERR_INVALID_ARG;
+  return loss_impl(nullptr, nullptr, rendered, target, height, width, channels, lambda_ssim,
+                   loss4, d_rendered, d_rendered_f64, ws, ws_bytes, stream_);
 }
 
 // ---- optimizer (trainer.py:192-224) -------------------------------------------

@@ -130,6 +130,8 @@ cudaError_t run_export(void* temp, size_t temp_bytes, const int32_t* count, cons
 struct LossArgs {
   const float* x;  // rendered (H,W,C) float32
   const float* y;  // target   (H,W,C) float32
+  const double* x64;  // float64 images instead (hs_loss_f64); x, y unused then
+  const double* y64;
   int width, height, channels;
   double lambda;   // lambda_ssim
   double n;        // H*W*C

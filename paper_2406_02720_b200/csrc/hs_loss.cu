@@ -114,15 +114,33 @@ __device__ __forceinline__ void horizontal_pair(const double* w, const double* r
   win_run<kHOut>(v, w, out);
 }
 
+// The images in their input type: float32 (the render's, hs_loss) or float64
+// (a reference caller's host arrays, hs_loss_f64).
+template <typename TI>
+__device__ __forceinline__ const TI* image_x(const LossArgs& a);
+template <>
+__device__ __forceinline__ const float* image_x<float>(const LossArgs& a) { return a.x; }
+template <>
+__device__ __forceinline__ const double* image_x<double>(const LossArgs& a) { return a.x64; }
+template <typename TI>
+__device__ __forceinline__ const TI* image_y(const LossArgs& a);
+template <>
+__device__ __forceinline__ const float* image_y<float>(const LossArgs& a) { return a.y; }
+template <>
+__device__ __forceinline__ const double* image_y<double>(const LossArgs& a) { return a.y64; }
+
 // Dynamic shared memory of L1: the interleaved halo rows of both images for the
-// CTA's channel group (float: the images are FP32, converted on use).
+// CTA's channel group, in the input type (converted to FP64 on use).
+template <typename TI>
 __host__ __device__ constexpr size_t loss_stats_smem(int cg) {
-  return (size_t)2 * kLHY * kLHX * cg * sizeof(float);
+  return (size_t)2 * kLHY * kLHX * cg * sizeof(TI);
 }
 
-template <bool SSIM, int CG>
-__global__ void __launch_bounds__(kLossThreads, 3) loss_stats_kernel(LossArgs a) {
-  extern __shared__ __align__(16) float halo[];  // x then y, [kLHY][kLHX * cg]
+template <typename TI, bool SSIM, int CG>
+__global__ void __launch_bounds__(kLossThreads, sizeof(TI) == 4 ? 3 : 2)
+loss_stats_kernel(LossArgs a) {
+  extern __shared__ __align__(16) unsigned char halo_raw[];
+  TI* halo = reinterpret_cast<TI*>(halo_raw);  // x then y, [kLHY][kLHX * cg]
   __shared__ __align__(16) double vs[5][kLTY][kLHX];  // vertical sums of x, y, xx, yy, xy
   __shared__ double red[kLossThreads / 32];
   const int group = a.group0 + blockIdx.z;
@@ -131,8 +149,10 @@ __global__ void __launch_bounds__(kLossThreads, 3) loss_stats_kernel(LossArgs a)
   const int64_t W = a.width, H = a.height, C = a.channels;
   constexpr int cg = CG;  // channels of this CTA (a tail group has its own launch)
   constexpr int rowf = kLHX * cg;  // floats per staged halo row
-  float* xs = halo;
-  float* ys = halo + kLHY * rowf;
+  TI* xs = halo;
+  TI* ys = halo + kLHY * rowf;
+  const TI* ax = image_x<TI>(a);
+  const TI* ay = image_y<TI>(a);
   double l1 = 0.0, ssum = 0.0, sq = 0.0;
   if (SSIM) {
     // the halo rows of all cg channels: contiguous runs of the HWC images
@@ -141,8 +161,8 @@ __global__ void __launch_bounds__(kLossThreads, 3) loss_stats_kernel(LossArgs a)
       const int gy = y0 - kWinR + r, gx = x0 - kWinR + q;
       const bool in = gx >= 0 && gx < W && gy >= 0 && gy < H;
       const int64_t k = (gy * W + gx) * C + c0 + cc;
-      xs[e] = in ? a.x[k] : 0.f;  // mode="constant", cval 0 (loss.py:31-32)
-      ys[e] = in ? a.y[k] : 0.f;
+      xs[e] = in ? ax[k] : TI(0);  // mode="constant", cval 0 (loss.py:31-32)
+      ys[e] = in ? ay[k] : TI(0);
     }
     __syncthreads();
   }
@@ -151,7 +171,8 @@ __global__ void __launch_bounds__(kLossThreads, 3) loss_stats_kernel(LossArgs a)
   for (int cc = 0; cc < cg; ++cc) {
     double f[5][kHOut];
     if (SSIM) {
-      // x^2, y^2 and xy of FP32 values are exact in FP64 (loss.py:62-64)
+      // x^2, y^2 and xy in FP64 (exact for FP32 inputs; numpy's products for
+      // float64 ones, loss.py:62-64)
       vertical_pass<5>(a.win, [&](int m, int r, int q) {
         const double x = xs[r * rowf + q * cg + cc], y = ys[r * rowf + q * cg + cc];
         return m == 0 ? x : m == 1 ? y : m == 2 ? x * x : m == 3 ? y * y : x * y;
@@ -173,8 +194,8 @@ __global__ void __launch_bounds__(kLossThreads, 3) loss_stats_kernel(LossArgs a)
         y = ys[h];
       } else {
         const int64_t k = (gy * W + gx) * C + c;
-        x = a.x[k];
-        y = a.y[k];
+        x = ax[k];
+        y = ay[k];
       }
       l1 += fabs(x - y);
       sq += (x - y) * (x - y);  // metrics.psnr's MSE (metrics.py:13-22)
@@ -207,7 +228,7 @@ __global__ void __launch_bounds__(kLossThreads, 3) loss_stats_kernel(LossArgs a)
   }
 }
 
-template <bool SSIM>
+template <typename TI, bool SSIM>
 __global__ void __launch_bounds__(kLossThreads) loss_grad_kernel(LossArgs a) {
   __shared__ __align__(16) double hs_[3][kLHY][kLHX];  // adjoint maps with halo
   __shared__ __align__(16) double vs[3][kLTY][kLHX];
@@ -262,7 +283,7 @@ __global__ void __launch_bounds__(kLossThreads) loss_grad_kernel(LossArgs a) {
       const int64_t gx = x0 + tx0 + i;
       if (gx >= W || gy >= H) continue;
       const int64_t k = (gy * W + gx) * C + c;
-      const double x = a.x[k], y = a.y[k];
+      const double x = image_x<TI>(a)[k], y = image_y<TI>(a)[k];
       const double diff = x - y;
       const double sg = diff > 0.0 ? 1.0 : (diff < 0.0 ? -1.0 : (diff == 0.0 ? 0.0 : diff));
       double g = w_l1 * (sg * a.inv_n);  // loss.py:96-99
@@ -276,40 +297,46 @@ __global__ void __launch_bounds__(kLossThreads) loss_grad_kernel(LossArgs a) {
   }
 }
 
-template <int CG>
+template <typename TI, int CG>
 static cudaError_t launch_stats(const LossArgs& a, dim3 grid, cudaStream_t stream) {
   if (!a.ssim) {
-    loss_stats_kernel<false, CG><<<grid, kLossThreads, 0, stream>>>(a);
+    loss_stats_kernel<TI, false, CG><<<grid, kLossThreads, 0, stream>>>(a);
     return cudaGetLastError();
   }
-  const cudaError_t attr = set_dynamic_smem<loss_stats_kernel<true, CG>>((int)loss_stats_smem(CG));
+  constexpr size_t smem = loss_stats_smem<TI>(CG);
+  const cudaError_t attr = set_dynamic_smem<loss_stats_kernel<TI, true, CG>>((int)smem);
   if (attr != cudaSuccess) return attr;
-  loss_stats_kernel<true, CG><<<grid, kLossThreads, loss_stats_smem(CG), stream>>>(a);
+  loss_stats_kernel<TI, true, CG><<<grid, kLossThreads, smem, stream>>>(a);
   return cudaGetLastError();
 }
 
-cudaError_t launch_loss(const LossArgs& a, cudaStream_t stream) {
+template <typename TI>
+static cudaError_t launch_loss_t(const LossArgs& a, cudaStream_t stream) {
   // channel groups of kMaxCG; a tail group of fewer channels gets its own launch
   const int full = a.channels / kMaxCG, tail = a.channels - full * kMaxCG;
   const unsigned gx = (unsigned)((a.width + kLTX - 1) / kLTX);
   const unsigned gy = (unsigned)((a.height + kLTY - 1) / kLTY);
   cudaError_t e = cudaSuccess;
-  if (full > 0) e = launch_stats<kMaxCG>(a, dim3(gx, gy, (unsigned)full), stream);
+  if (full > 0) e = launch_stats<TI, kMaxCG>(a, dim3(gx, gy, (unsigned)full), stream);
   if (e == cudaSuccess && tail > 0) {
     LossArgs t = a;
     t.group0 = full;
     const dim3 g(gx, gy, 1);
-    e = tail == 1 ? launch_stats<1>(t, g, stream)
-                  : tail == 2 ? launch_stats<2>(t, g, stream) : launch_stats<3>(t, g, stream);
+    e = tail == 1 ? launch_stats<TI, 1>(t, g, stream)
+                  : tail == 2 ? launch_stats<TI, 2>(t, g, stream) : launch_stats<TI, 3>(t, g, stream);
   }
   if (e != cudaSuccess) return e;
   const dim3 grid(gx, gy, (unsigned)(full + (tail > 0)));
   if (a.ssim)
-    loss_grad_kernel<true><<<grid, kLossThreads, 0, stream>>>(a);
+    loss_grad_kernel<TI, true><<<grid, kLossThreads, 0, stream>>>(a);
   else
-    loss_grad_kernel<false><<<grid, kLossThreads, 0, stream>>>(a);
+    loss_grad_kernel<TI, false><<<grid, kLossThreads, 0, stream>>>(a);
   note_launch((full > 0) + (tail > 0) + 1);
   return cudaGetLastError();
+}
+
+cudaError_t launch_loss(const LossArgs& a, cudaStream_t stream) {
+  return a.x64 ? launch_loss_t<double>(a, stream) : launch_loss_t<float>(a, stream);
 }
 
 int64_t loss_partials(int width, int height, int channels) {

@@ -63,7 +63,26 @@ __global__ void __launch_bounds__(256) ex2_probe_kernel(float* out, int iters) {
   if (s == 12345.678f) out[0] = s;
 }
 
+// The blend kernels' erf32 (hs_common.cuh) on the hardware's MUFU.EX2, so its
+// accuracy bound is checked on the device rather than on an exact-exp2 emulation.
+__global__ void erf32_probe_kernel(const float* __restrict__ z, float* __restrict__ out,
+                                   int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = erf32(z[i]);
+}
+
 }  // namespace hs
+
+extern "C" int hs_probe_erf32(const float* z, float* out, int64_t n, void* stream) {
+  if (n < 0 || (n > 0 && (!z || !out))) return HS_ERR_INVALID_ARG;
+  if (n == 0) return HS_OK;
+  const int threads = 256;
+  const int blocks = (int)((n + threads - 1) / threads < 4096 ? (n + threads - 1) / threads : 4096);
+  hs::erf32_probe_kernel<<<blocks, threads, 0, (cudaStream_t)stream>>>(z, out, n);
+  hs::note_launch();
+  return cudaGetLastError() == cudaSuccess ? HS_OK : HS_ERR_CUDA;
+}
 
 static double g_fma2_tflops = 0.0;
 extern "C" double hs_last_fma2_tflops(void) { return g_fma2_tflops; }

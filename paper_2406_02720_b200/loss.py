@@ -8,8 +8,10 @@ and return float64 numpy gradients like the reference; `DeviceLoss` is the
 allocation-free form for device-resident training loops (torch CUDA tensors in,
 loss scalars and the float32 cotangent out, no host synchronisation).
 
-All arithmetic runs in `hs_loss` (csrc/hs_loss.cu) in FP64 on the FP32
-images; there is no CPU path.
+All arithmetic runs in `hs_loss` (csrc/hs_loss.cu) in FP64; float32 images are
+read as float32 (exact in FP64), anything else as float64 (`hs_loss_f64`), so a
+reference caller's float64 renders and uint8/255 targets are not rounded.
+There is no CPU path.
 """
 
 import ctypes
@@ -36,8 +38,8 @@ def _ptr(t):
 class DeviceLoss:
     """compute_loss on device tensors with a persistent workspace.
 
-    `__call__(rendered, target)` takes (H,W,C) or (H,W) float32 CUDA tensors and
-    returns `(stats, d_rendered)`: stats is a (4,) float64 device tensor
+    `__call__(rendered, target)` takes (H,W,C) or (H,W) CUDA tensors (float32,
+    or float64 when either is float64: then both are read as float64) and returns `(stats, d_rendered)`: stats is a (4,) float64 device tensor
     [loss, L1, mean SSIM, MSE] and d_rendered the float32 gradient, shaped like
     `rendered`.  Nothing is copied to the host.
     """
@@ -63,26 +65,32 @@ class DeviceLoss:
             raise errors.ShapeMismatch("expected HxW or HxWxC images")
         if not (rendered.is_cuda and target.is_cuda):
             raise ValueError("DeviceLoss takes CUDA tensors")
-        x = rendered.contiguous().float()
-        y = target.contiguous().float()
+        f64 = torch.float64 in (rendered.dtype, target.dtype)
+        x = rendered.contiguous().to(torch.float64 if f64 else torch.float32)
+        y = target.contiguous().to(x.dtype)
         h, w = x.shape[0], x.shape[1]
         c = x.shape[2] if x.dim() == 3 else 1
         if stats is None:
             stats = torch.empty(4, dtype=torch.float64, device=x.device)
         if d_out is None and d_out_f64 is None:
-            d_out = torch.empty_like(x)
+            d_out = torch.empty(x.shape, dtype=torch.float32, device=x.device)
         ws = self._workspace(h, w, c, x.device)
         lib = _native.load()
-        _native.check(lib.hs_loss(_ptr(x), _ptr(y), h, w, c, self.lambda_ssim, _ptr(stats),
-                                  _ptr(d_out), _ptr(d_out_f64), _ptr(ws), ws.numel(),
-                                  _stream()), "hs_loss")
+        fn = lib.hs_loss_f64 if f64 else lib.hs_loss
+        _native.check(fn(_ptr(x), _ptr(y), h, w, c, self.lambda_ssim, _ptr(stats),
+                         _ptr(d_out), _ptr(d_out_f64), _ptr(ws), ws.numel(), _stream()),
+                      "hs_loss")
         return stats, (d_out if d_out is not None else d_out_f64)
 
 
 def _check_pair(a, b):
-    """loss.py:35-45 (shapes only; values go to the device as float32)."""
+    """loss.py:35-45.  Two float32 arrays stay float32 (exact in the FP64 kernel);
+    anything else is read as float64, as the reference's np.asarray(.., float64)."""
     a = np.asarray(a)
     b = np.asarray(b)
+    dt = np.float32 if a.dtype == np.float32 and b.dtype == np.float32 else np.float64
+    a = np.ascontiguousarray(a, dtype=dt)
+    b = np.ascontiguousarray(b, dtype=dt)
     if a.shape != b.shape:
         raise errors.ShapeMismatch(f"{a.shape} vs {b.shape}")
     if a.ndim not in (2, 3):
@@ -97,8 +105,8 @@ def _run(rendered, target, lambda_ssim):
     if lambda_ssim != 0.0 and min(a.shape[0], a.shape[1]) < SSIM_WINDOW:
         raise errors.ImageTooSmall(f"needs at least {SSIM_WINDOW} pixels on each side")
     dev = torch.device("cuda", torch.cuda.current_device())
-    x = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(dev)
-    y = torch.from_numpy(np.ascontiguousarray(b, dtype=np.float32)).to(dev)
+    x = torch.from_numpy(a).to(dev)
+    y = torch.from_numpy(b).to(dev)
     d64 = torch.empty(x.shape, dtype=torch.float64, device=dev)
     stats, _ = DeviceLoss(lambda_ssim)(x, y, d_out=None, d_out_f64=d64)
     return stats.cpu().numpy(), d64.cpu().numpy()

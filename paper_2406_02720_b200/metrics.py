@@ -1,7 +1,8 @@
 """Image-quality metrics on the GPU (drop-in for metrics.py's psnr / ssim).
 
 `psnr` takes the MSE from the same `hs_loss` pass that computes the training loss
-(lambda 0: L1 and MSE only); `ssim` is loss.ssim.  Inputs are uploaded as float32.
+(lambda 0: L1 and MSE only); `ssim` is loss.ssim.  float32 pairs are read as float32,
+anything else as float64 (metrics.py:15-16).
 """
 
 import math

@@ -9,9 +9,16 @@ the end-to-end path a reference caller gets by switching imports.
 float64 reference scenes are uploaded as float64 (the FP64 preprocess then sees
 exactly the reference's inputs); float32 scenes stay float32.  The blend runs in
 FP32; see DESIGN.md for the parity contract.
+
+Outputs have the reference's dtypes by default: float64 images and gradients,
+int32 terminal indices, int64 touch counts (rasterizer.py:357-361, 400;
+GradientSet.zeros 85-97).  `set_output_dtype(np.float32)` (or HS_HOST_FLOAT=float32)
+is an explicit opt-in that returns the images as the FP32 the blend computes and
+the gradients in the scene's own dtype, halving the bytes that cross PCIe.
 """
 
 import ctypes
+import os
 import weakref
 from dataclasses import dataclass
 
@@ -140,27 +147,45 @@ def _n(scene):
     return int(scene.mu.shape[0])
 
 
-# Host dtype of floating-point outputs.  The GPU computes images in FP32, so
-# float32 arrays carry every bit of the result; set to np.float64 to get the
-# reference's dtype at the cost of a host-side conversion.
-HOST_FLOAT = np.float32
+# Host dtype of the floating-point outputs: the reference's float64 unless the
+# caller opts into float32 (module docstring).
+_OUTPUT_DTYPE = [np.float32 if os.environ.get("HS_HOST_FLOAT") == "float32" else np.float64]
+
+
+def set_output_dtype(dtype):
+    """np.float64 (default, the reference's dtypes) or np.float32 (opt-in: images
+    as computed in FP32, gradients in the scene's dtype).  Returns the previous one."""
+    dtype = np.dtype(dtype).type
+    if dtype not in (np.float32, np.float64):
+        raise ValueError("output dtype must be float32 or float64")
+    prev, _OUTPUT_DTYPE[0] = _OUTPUT_DTYPE[0], dtype
+    return prev
+
+
+def output_dtype():
+    return _OUTPUT_DTYPE[0]
+
+
+def _host_float_dtype(t):
+    """torch dtype a floating device tensor is returned in."""
+    if _OUTPUT_DTYPE[0] is np.float64:
+        return torch.float64
+    return t.dtype
 
 
 def _to_host(tensors):
-    """D2H through pinned staging buffers (one sync for the whole batch)."""
+    """D2H through pinned staging buffers (one sync for the whole batch).  Float
+    tensors are widened on the device when float64 is requested, so the host
+    gets the reference's dtype without a host-side conversion pass."""
     staged = []
     for t in tensors:
+        if t.is_floating_point() and t.dtype != _host_float_dtype(t):
+            t = t.to(_host_float_dtype(t))
         h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
         h.copy_(t, non_blocking=True)
         staged.append(h)
     torch.cuda.current_stream().synchronize()
-    out = []
-    for h in staged:
-        a = h.numpy()
-        if a.dtype.kind == "f" and a.dtype != HOST_FLOAT:
-            a = a.astype(HOST_FLOAT)
-        out.append(a)
-    return out
+    return [h.numpy() for h in staged]
 
 
 def resolve_threads(threads):
@@ -283,12 +308,17 @@ D2H_BUCKETS = 4
 def _backward_to_host(dscene, cam, dout, dc):
     """render_backward with the gradient download overlapped with K7: after each
     primitive bucket a side stream copies that bucket's rows of every field into
-    pinned host arrays (touch counts widened to int64 on the device first)."""
+    pinned host arrays (touch counts widened to int64 on the device first, and the
+    float fields to float64 when the reference's dtype is requested)."""
     n = len(dscene)
     dev = dscene.device
     grads = _dev.DeviceGradientSet.empty_like_scene(dscene)
     touch64 = torch.empty(n, dtype=torch.int64, device=dev)
-    fields = [getattr(grads, name) for name in GradientSet.NAMES[:-1]] + [touch64]
+    src = [getattr(grads, name) for name in GradientSet.NAMES[:-1]]
+    fields = [t if t.dtype == _host_float_dtype(t) else
+              torch.empty(t.shape, dtype=_host_float_dtype(t), device=dev) for t in src]
+    widen = [(a, b) for a, b in zip(src, fields) if a is not b]
+    fields.append(touch64)
     host = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in fields]
     compute = torch.cuda.current_stream(dev)
     copy = _copy_stream(dev)
@@ -299,6 +329,8 @@ def _backward_to_host(dscene, cam, dout, dc):
 
     def on_bucket(b, e):
         touch64[b:e].copy_(grads.touch_count[b:e])
+        for a, w in widen:
+            w[b:e].copy_(a[b:e])
         ev = torch.cuda.Event()
         ev.record(compute)
         copy.wait_event(ev)
@@ -309,13 +341,7 @@ def _backward_to_host(dscene, cam, dout, dc):
     _dev.render_backward(dscene, cam, dout, dc, grads=grads, buckets=buckets,
                          on_bucket=on_bucket)
     copy.synchronize()  # before the device buffers go back to the allocator
-    out = []
-    for h in host:
-        a = h.numpy()
-        if a.dtype.kind == "f" and a.dtype != HOST_FLOAT:
-            a = a.astype(HOST_FLOAT)
-        out.append(a)
-    return out
+    return [h.numpy() for h in host]
 
 
 _COPY_STREAMS = {}

@@ -12,7 +12,6 @@ the reference's).
 """
 
 import ctypes
-import re
 
 import numpy as np
 import torch
@@ -35,83 +34,126 @@ _3DGS_REQUIRED = ["x", "y", "z", "f_dc_0", "f_dc_1", "f_dc_2", "opacity", "scale
                   "scale_2", "rot_0", "rot_1", "rot_2", "rot_3"]
 
 
-def _read_ply_header(fh):
-    """scene_io.py:49-88 (same checks, same messages)."""
-    magic = fh.readline()
+class _Header:
+    """What the header of a point file declares: the vertex count, the properties in
+    payload order as (name, type), the `comment key value` pairs, and the offset of
+    the first payload byte."""
+
+    def __init__(self):
+        self.count = None
+        self.props = []
+        self.comments = {}
+        self.payload_offset = 0
+
+    @property
+    def stride(self):
+        return sum(_PLY_TYPES[t][1] for _, t in self.props)
+
+
+def _header_lines(blob):
+    """Yields (line, end) for each newline-terminated line at the start of `blob`;
+    `end` is the offset just past the line."""
+    pos = 0
+    while pos < len(blob):
+        nl = blob.find(b"\n", pos)
+        end = len(blob) if nl < 0 else nl + 1
+        yield blob[pos:end], end
+        pos = end
+
+
+def _on_comment(h, words, line):
+    key_value = line.decode("ascii", "replace").split(None, 2)[1:]
+    if len(key_value) == 2:
+        h.comments[key_value[0]] = key_value[1].strip()
+
+
+def _on_element(h, words, line):
+    if words[1] != b"vertex":
+        raise MalformedHeader(f"unsupported element {words[1].decode()}")
+    h.count = int(words[2])
+
+
+def _on_property(h, words, line):
+    if words[1] == b"list":
+        raise MalformedHeader("list properties are not supported")
+    type_name = words[1].decode()
+    if type_name not in _PLY_TYPES:
+        raise MalformedHeader(f"unsupported property type {type_name}")
+    h.props.append((words[2].decode(), type_name))
+
+
+_HEADER_KEYWORDS = {b"comment": _on_comment, b"element": _on_element, b"property": _on_property}
+
+
+def _parse_header(blob):
+    """The header grammar of scene_io.py:49-88 with the reference's exception types
+    and messages: `ply`, `format binary_little_endian ...`, then comment / element
+    vertex / scalar property lines up to `end_header`."""
+    lines = _header_lines(blob)
+    magic, _ = next(lines, (b"", 0))
     if magic.strip() != b"ply":
         raise MalformedHeader("not a PLY file")
-    fmt = fh.readline().split()
-    if len(fmt) < 2 or fmt[0] != b"format" or fmt[1] != b"binary_little_endian":
+    fmt, _ = next(lines, (b"", 0))
+    if fmt.split()[:2] != [b"format", b"binary_little_endian"]:
         raise MalformedHeader("expected format binary_little_endian")
-    count = None
-    props = []
-    comments = {}
-    while True:
-        line = fh.readline()
-        if not line:
-            raise MalformedHeader("unterminated header")
-        tokens = line.split()
-        if not tokens:
+    h = _Header()
+    for line, end in lines:
+        words = line.split()
+        if not words:
             continue
-        if tokens[0] == b"end_header":
+        if words[0] == b"end_header":
+            h.payload_offset = end
             break
-        if tokens[0] == b"comment":
-            parts = line.decode("ascii", "replace").split(None, 2)
-            if len(parts) == 3:
-                comments[parts[1]] = parts[2].strip()
-            continue
-        if tokens[0] == b"element":
-            if tokens[1] != b"vertex":
-                raise MalformedHeader(f"unsupported element {tokens[1].decode()}")
-            count = int(tokens[2])
-            continue
-        if tokens[0] == b"property":
-            if tokens[1] == b"list":
-                raise MalformedHeader("list properties are not supported")
-            tname = tokens[1].decode()
-            if tname not in _PLY_TYPES:
-                raise MalformedHeader(f"unsupported property type {tname}")
-            props.append((tokens[2].decode(), tname))
-            continue
-        raise MalformedHeader(f"unexpected header line {line.decode(errors='replace').strip()!r}")
-    if count is None:
+        handler = _HEADER_KEYWORDS.get(words[0])
+        if handler is None:
+            shown = line.decode(errors="replace").strip()
+            raise MalformedHeader(f"unexpected header line {shown!r}")
+        handler(h, words, line)
+    else:
+        raise MalformedHeader("unterminated header")
+    if h.count is None:
         raise MalformedHeader("missing vertex element")
-    return count, props, comments
+    return h
 
 
 def _read_ply(path):
-    """Header on the host; the payload as one uint8 array (scene_io.py:91-102)."""
+    """The header parsed on the host; the payload as one uint8 view of the file
+    (scene_io.py:91-102), which crosses PCIe in one copy."""
     with open(path, "rb") as fh:
-        count, props, comments = _read_ply_header(fh)
-        body = fh.read()
-    stride = sum(_PLY_TYPES[t][1] for _, t in props)
-    if len(body) < count * stride:
-        raise TruncatedPayload(f"expected {count * stride} payload bytes, found {len(body)}")
-    if len(props) > 128:
+        blob = fh.read()
+    h = _parse_header(blob)
+    need = h.count * h.stride
+    have = len(blob) - h.payload_offset
+    if have < need:
+        raise TruncatedPayload(f"expected {need} payload bytes, found {have}")
+    if len(h.props) > 128:
         raise MalformedHeader("more than 128 properties")
-    payload = np.frombuffer(body, dtype=np.uint8, count=count * stride)
-    return count, props, comments, payload, stride
+    payload = np.frombuffer(blob, dtype=np.uint8, count=need, offset=h.payload_offset)
+    return h.count, h.props, h.comments, payload, h.stride
 
 
 def _require(columns, names):
-    for name in names:
-        if name not in columns:
-            raise MissingProperty(f"point file is missing property {name!r}")
+    """MissingProperty for the first required name the file lacks (in `names` order)."""
+    missing = [name for name in names if name not in columns]
+    if missing:
+        raise MissingProperty(f"point file is missing property {missing[0]!r}")
 
 
 def _rest_names(columns):
-    rest = sorted(
-        (int(m.group(1)) for m in (re.fullmatch(r"f_rest_(\d+)", c) for c in columns) if m))
-    if rest != list(range(len(rest))):
+    """The f_rest_<i> properties, which must be numbered 0..R-1 without gaps."""
+    idx = sorted(int(c[len("f_rest_"):]) for c in columns
+                 if c.startswith("f_rest_") and c[len("f_rest_"):].isdigit())
+    if idx and (idx[0] != 0 or idx[-1] != len(idx) - 1 or len(set(idx)) != len(idx)):
         raise MissingProperty("f_rest_* properties are not contiguous")
-    return [f"f_rest_{i}" for i in rest]
+    return [f"f_rest_{i}" for i in idx]
 
 
 def _degree(rest_names):
-    n_rest = len(rest_names)
-    if n_rest % 3 != 0 or n_rest // 3 not in _SH_DEGREE_BY_REST:
-        raise MalformedHeader(f"unsupported f_rest count {n_rest}")
-    return _SH_DEGREE_BY_REST[n_rest // 3]
+    per_channel, ragged = divmod(len(rest_names), 3)
+    degree = _SH_DEGREE_BY_REST.get(per_channel)
+    if ragged or degree is None:
+        raise MalformedHeader(f"unsupported f_rest count {len(rest_names)}")
+    return degree
 
 
 def _layout(count, props, stride, degree, names):
@@ -160,11 +202,10 @@ def load_scene(path, device_name="cuda", dtype=torch.float64):
     _require(columns, _NATIVE_REQUIRED)
     rest = _rest_names(columns)
     degree = _degree(rest)
-    if "sh_degree" in comments and int(comments["sh_degree"]) != degree:
+    declared = comments.get("sh_degree")
+    if declared is not None and int(declared) != degree:
         raise MalformedHeader("sh_degree comment disagrees with f_rest count")
-    background = (0.0, 0.0, 0.0)
-    if "background" in comments:
-        background = tuple(float(v) for v in comments["background"].split())
+    background = tuple(map(float, comments.get("background", "0 0 0").split()))
     scene = _empty_scene(count, degree, background, device_name, dtype)
     lay = _layout(count, props, stride, degree, dict(
         mu=["x", "y", "z"], log_scale=["scale_0", "scale_1", "scale_2"],

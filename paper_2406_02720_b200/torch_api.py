@@ -50,6 +50,7 @@ class _RasterizeHalfGaussians(torch.autograd.Function):
         scene = Scene(means3D, log_scales, rotations, shs, normals, raw_opacity_a, raw_opacity_b,
                       sh_degree=settings.sh_degree, background_color=settings.background,
                       device=means3D.device, dtype=means3D.dtype, validate=False)
+        scene.check_shapes()  # shape-only: no device sync on the autograd path
         cam = settings.camera()
         out = device.render(scene, cam, settings.kernel)
         ctx.scene, ctx.cam, ctx.out = scene, cam, out

@@ -90,6 +90,26 @@ def run_reference(sa, cam_idx, backward, threads, kernel="half"):
     return frame, out, grads, d_color, (t1 - t0, t2 - t1)
 
 
+def ref_radii(frame):
+    """(N,) int32 radii from the reference's own frame: r = RADIUS_SIGMAS * sqrt(lam_max)
+    of the dilated screen covariance, recomputed from frame.cov_ray with the expression
+    of rasterizer.py:194-200 (elementwise, so bit-identical to prepare's), then ceil;
+    0 for culled primitives.  The reference never materialises radii itself; SURVEY.md
+    8(b) defines them this way."""
+    from halfsplat import rasterizer as R
+    cov = frame.cov_ray
+    a = cov[:, 0, 0] + R.LOWPASS_DILATION
+    b = cov[:, 0, 1]
+    c = cov[:, 1, 1] + R.LOWPASS_DILATION
+    det = a * c - b * b
+    mid = 0.5 * (a + c)
+    lam_max = mid + np.sqrt(np.maximum(mid * mid - det, 0.0))
+    radius = R.RADIUS_SIGMAS * np.sqrt(np.maximum(lam_max, 0.0))
+    out = np.zeros(frame.n_total, np.int32)
+    out[frame.valid] = np.ceil(radius).astype(np.int32)
+    return out
+
+
 def full_fixture(name, sa, cam_idx, backward, threads, kernel="half"):
     frame, out, grads, d_color, secs = run_reference(sa, cam_idx, backward, threads, kernel)
     d = dict(scene_sha=scene_sha(sa), cam_idx=cam_idx, kernel=kernel,
@@ -98,6 +118,7 @@ def full_fixture(name, sa, cam_idx, backward, threads, kernel="half"):
              tiles_x=frame.tiles_x, tiles_y=frame.tiles_y)
     for k, dt in INT_ARRAYS.items():
         d[k] = np.asarray(getattr(frame, k), dtype=dt)
+    d["radii"] = ref_radii(frame)
     if backward:
         d["d_color"] = d_color
         for g in GRAD_GROUPS:
@@ -128,6 +149,9 @@ def summary_fixture(name, sa, cam_idx, backward, threads, n_px=4096, n_rows=2048
              ref_seconds=np.array(secs))
     for k, dt in INT_ARRAYS.items():
         d[f"sha_{k}"] = sha(getattr(frame, k), dt)
+    radii = ref_radii(frame)
+    d["sha_radii"] = sha(radii, np.int32)
+    d["radii_sum"] = int(radii.astype(np.int64).sum())
     d["packed_sample_rows"] = rng.choice(frame.valid.shape[0], size=min(n_rows, frame.valid.shape[0]),
                                          replace=False)
     d["packed_sample"] = frame.packed[d["packed_sample_rows"]]
@@ -190,6 +214,38 @@ def loss_fixture():
     d["cases"] = np.array(list(cases))
     np.savez_compressed(os.path.join(HERE, "loss.npz"), **d)
     print("loss:", len(cases), "cases")
+
+
+def loss64_fixture():
+    """compute_loss / ssim_with_grad / metrics.psnr on float64 images that float32
+    cannot hold: a render in float64 against a uint8/255 target, a pair whose
+    differences sit below float32 resolution (sign(diff) must stay non-zero), and
+    a float64 2-D pair."""
+    from halfsplat import loss as ref_loss
+    from halfsplat import metrics as ref_metrics
+    rng = np.random.default_rng(33)
+    x = rng.random((41, 57, 3))
+    tgt8 = rng.integers(0, 256, (41, 57, 3)).astype(np.uint8)
+    tiny = x + rng.choice([-1.0, 1.0], x.shape) * 1e-12  # below float32's ulp near 0.5
+    g = rng.random((33, 29))
+    cases = {
+        "u8_target_l02": (x, tgt8, 0.2),
+        "tiny_diff_l02": (x, tiny, 0.2),
+        "tiny_diff_l0": (x, tiny, 0.0),
+        "gray_f64_l05": (g, np.roll(g, 2, axis=0) * 0.9, 0.5),
+    }
+    d = {}
+    for name, (a, b, lam) in cases.items():
+        loss, grad = ref_loss.compute_loss(a, b, lam)
+        d[f"{name}_a"], d[f"{name}_b"], d[f"{name}_lambda"] = a, b, np.float64(lam)
+        d[f"{name}_loss"], d[f"{name}_grad"] = np.float64(loss), grad
+        d[f"{name}_psnr"] = np.float64(ref_metrics.psnr(a, b))
+        if lam > 0:
+            s, sg = ref_loss.ssim_with_grad(a, b)
+            d[f"{name}_ssim"], d[f"{name}_ssim_grad"] = np.float64(s), sg
+    d["cases"] = np.array(list(cases))
+    np.savez_compressed(os.path.join(HERE, "loss64.npz"), **d)
+    print("loss64:", len(cases), "cases")
 
 
 def adam_fixture():
@@ -439,16 +495,51 @@ def train_fixture():
         print({k: (round(v, 5) if isinstance(v, float) else v) for k, v in r.items()})
 
 
+def radii_patch(threads):
+    """Adds the reference's radii to the existing scene fixtures without re-running
+    the blend: only prepare() runs (the scene hash is checked first)."""
+    from halfsplat.rasterizer import prepare
+    gens = {name: (gen, kernel) for name, (gen, kernel) in RADII_SCENES.items()}
+    for name, (gen, kernel) in gens.items():
+        path = os.path.join(HERE, f"{name}.npz")
+        old = dict(np.load(path, allow_pickle=False))
+        sa = gen()
+        assert scene_sha(sa) == str(old["scene_sha"]), name
+        frame = prepare(ref_scene(sa), ref_camera(sa.cameras[int(old["cam_idx"])]), kernel)
+        radii = ref_radii(frame)
+        if "sha_valid" in old:
+            old["sha_radii"] = sha(radii, np.int32)
+            old["radii_sum"] = np.int64(radii.astype(np.int64).sum())
+        else:
+            old["radii"] = radii
+        np.savez_compressed(path, **old)
+        print(f"{name}: radii max {radii.max()} sum {int(radii.astype(np.int64).sum())}")
+
+
+RADII_SCENES = {
+    "c1": (lambda: scenes.make_config("c1"), "half"),
+    "mini": (lambda: scenes.frustum(300, 2, 64, 48, seed=3), "half"),
+    "mini_full": (lambda: scenes.frustum(300, 2, 64, 48, seed=3), "full"),
+    "ball_small": (lambda: scenes.ball(3000, 3, 96, 72, views=4, seed=9), "half"),
+    "ties": (lambda: scenes.frustum(2000, 1, 96, 80, seed=5, clustered=True, dup=0.3), "half"),
+    "c2": (lambda: scenes.make_config("c2"), "half"),
+    "c3": (lambda: scenes.make_config("c3"), "half"),
+    "c5": (lambda: scenes.make_config("c5"), "half"),
+    "c4v0": (lambda: scenes.make_config("c4"), "half"),
+}
+
 SCENE_FIELDS = ("mu", "log_scale", "rotation", "sh_coeffs", "normal", "raw_opacity_a",
                 "raw_opacity_b")
 
 JOBS = {
+    "radii": radii_patch,
     "erf": lambda t: erf_fixture(),
     "adam": lambda t: adam_fixture(),
     "densify": lambda t: densify_fixture(),
     "io": lambda t: io_fixture(),
     "train": lambda t: train_fixture(),
     "loss": lambda t: loss_fixture(),
+    "loss64": lambda t: loss64_fixture(),
     # small scenes, every array
     "c1": lambda t: full_fixture("c1", scenes.make_config("c1"), 0, True, t),
     "mini": lambda t: full_fixture("mini", scenes.frustum(300, 2, 64, 48, seed=3), 0, True, t),
@@ -469,7 +560,7 @@ JOBS = {
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--build-dir", default="/tmp/hs_refbuild")
-    ap.add_argument("--only", default=",".join(JOBS))
+    ap.add_argument("--only", default=",".join(j for j in JOBS if j != "radii"))
     ap.add_argument("--threads", type=int, default=os.cpu_count())
     args = ap.parse_args()
     build_reference(args.build_dir)

@@ -6,6 +6,7 @@ import os
 import re
 
 import numpy as np
+import pytest
 
 from conftest import REPO, load_golden
 
@@ -51,3 +52,28 @@ def test_erf32_is_exactly_odd():
     z = np.linspace(-5, 5, 20001, dtype=np.float32)
     assert np.array_equal(erf32(-z), -erf32(z))
     assert erf32(np.float32(0.0)) == 0.0
+
+
+@pytest.mark.gpu
+def test_device_erf32_on_mufu(cuda):
+    """The device erf itself (MUFU.EX2, not an exact exp2): within 4e-7 of the
+    reference's fast_erf on its golden points, and bitwise odd."""
+    import torch
+    from paper_2406_02720_b200 import _native
+    lib = _native.load()
+    gold = load_golden("erf")
+    z = np.concatenate([gold["z"].astype(np.float32),
+                        np.linspace(-6, 6, 200001, dtype=np.float32)])
+    zt = torch.as_tensor(z, device="cuda")
+    outs = []
+    for arg in (zt, -zt):
+        o = torch.empty_like(arg)
+        _native.check(lib.hs_probe_erf32(arg.data_ptr(), o.data_ptr(), arg.numel(), None),
+                      "probe_erf32")
+        outs.append(o.cpu().numpy())
+    pos, neg = outs
+    ng = gold["z"].shape[0]
+    assert np.abs(pos[:ng].astype(np.float64) - gold["erf"]).max() < 4e-7
+    assert np.array_equal(neg, -pos)
+    # the emulation above agrees with the hardware to a few ulps of 1.0f
+    assert np.abs(pos - erf32(z)).max() <= 2.0 ** -21

@@ -43,6 +43,48 @@ def test_dropin_render_matches_oracle(cuda):
     assert np.array_equal(fg.tile_starts, ref.frame.tile_starts)
 
 
+def test_dropin_output_dtypes_match_reference(cuda):
+    """Seam 2 returns the reference's dtypes by default (the dtypes of its own arrays in
+    the golden fixture: float64 images and gradients, int32 terminal, int64 touch
+    counts); float32 is an explicit opt-in that keeps gradients in the scene's dtype."""
+    gold = load_golden("mini")
+    sa = scenes.frustum(300, 2, 64, 48, seed=3)
+    s64 = sa.as_float64()
+    cam = CameraModel(**sa.cameras[0])
+    images = ("color", "alpha", "depth", "transmittance")
+    out = R.render(s64, cam)
+    g = R.render_backward(s64, cam, out, gold["d_color"])
+    for k in images:
+        assert getattr(out, k).dtype == gold[k].dtype == np.float64, k
+    assert out.per_pixel_terminal_index.dtype == gold["terminal"].dtype == np.int32
+    for k in R.GradientSet.NAMES:
+        assert getattr(g, k).dtype == gold[k].dtype, k
+    assert_images({k: getattr(out, k) for k in images} |
+                  {"terminal": out.per_pixel_terminal_index},
+                  {k: gold[k] for k in images + ("terminal",)})
+    assert_grads({k: getattr(g, k) for k in R.GradientSet.NAMES[:-1]},
+                 {k: gold[k] for k in R.GradientSet.NAMES[:-1]})
+    # float32 scene, default: still float64 out (widened on the device, same values)
+    out32 = R.render(sa, cam)
+    g32 = R.render_backward(sa, cam, out32, gold["d_color"])
+    assert out32.color.dtype == np.float64 and g32.d_mu.dtype == np.float64
+    prev = R.set_output_dtype(np.float32)
+    try:
+        o = R.render(s64, cam)
+        gg = R.render_backward(s64, cam, o, gold["d_color"])
+        assert o.color.dtype == np.float32 and o.per_pixel_terminal_index.dtype == np.int32
+        assert gg.d_mu.dtype == np.float64 and gg.touch_count.dtype == np.int64  # scene's dtype
+        assert np.array_equal(gg.d_mu, g.d_mu)  # FP64 K7: nothing rounded
+        assert np.array_equal(o.color.astype(np.float64), out.color)
+        o = R.render(sa, cam)
+        gg = R.render_backward(sa, cam, o, gold["d_color"])
+        assert o.color.dtype == np.float32 and gg.d_mu.dtype == np.float32
+        assert np.array_equal(gg.d_mu.astype(np.float64), g32.d_mu)
+    finally:
+        R.set_output_dtype(prev)
+    assert R.output_dtype() is np.float64
+
+
 def test_dropin_errors(cuda):
     rng = np.random.default_rng(0)
     sa = make_scene(rng, 3)

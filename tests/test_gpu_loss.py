@@ -121,3 +121,39 @@ def test_loss_random_shapes_vs_oracle(cuda, seed):
     assert grad.shape == ref_grad.shape
     assert val == pytest.approx(ref_loss, rel=1e-12, abs=1e-15)
     assert _grad_close(grad, ref_grad, 1e-12)
+
+
+def test_loss_float64_inputs_match_reference(cuda):
+    """Float64 renders and uint8 targets are read unrounded (hs_loss_f64): a uint8/255
+    target, differences below float32 resolution (sign(diff) stays +-1, so the L1
+    cotangent keeps its 1/n per pixel) and a 2-D pair, against the reference's own
+    compute_loss / ssim_with_grad / psnr (tests/golden/loss64.npz)."""
+    from paper_2406_02720_b200 import loss as L
+    from paper_2406_02720_b200 import metrics as M
+    gold = load_golden("loss64")
+    for c in gold["cases"]:
+        a, b, lam = gold[f"{c}_a"], gold[f"{c}_b"], float(gold[f"{c}_lambda"])
+        val, grad = L.compute_loss(a, b, lam)
+        ref = gold[f"{c}_grad"]
+        assert grad.shape == ref.shape and grad.dtype == np.float64, c
+        assert val == pytest.approx(float(gold[f"{c}_loss"]), rel=1e-12, abs=1e-15), c
+        assert _grad_close(grad, ref, 1e-12), c
+        # the L1 part's sign pattern is exact (no float32 ties)
+        assert np.array_equal(np.sign(grad) != 0, np.sign(ref) != 0) or lam > 0, c
+        assert M.psnr(a, b) == pytest.approx(float(gold[f"{c}_psnr"]), rel=1e-12), c
+        if lam > 0:
+            s, sg = L.ssim_with_grad(a, b)
+            assert s == pytest.approx(float(gold[f"{c}_ssim"]), rel=1e-12), c
+            assert _grad_close(sg, gold[f"{c}_ssim_grad"], 1e-12), c
+
+
+def test_device_loss_float64_tensors(cuda):
+    """DeviceLoss on float64 CUDA tensors takes the float64 kernel too."""
+    import torch
+    from paper_2406_02720_b200 import loss as L
+    gold = load_golden("loss64")
+    a, b = gold["tiny_diff_l02_a"], gold["tiny_diff_l02_b"]
+    stats, d = L.DeviceLoss(0.2)(torch.from_numpy(a).to(cuda), torch.from_numpy(b).to(cuda),
+                                 d_out_f64=torch.empty(a.shape, dtype=torch.float64, device=cuda))
+    assert float(stats[0]) == pytest.approx(float(gold["tiny_diff_l02_loss"]), rel=1e-12)
+    assert _grad_close(d.cpu().numpy(), gold["tiny_diff_l02_grad"], 1e-12)

@@ -71,6 +71,9 @@ def test_full_fixture_parity(cuda, name, dtype):
     # integers: bit-exact
     for k, dt in INT_DTYPES.items():
         assert np.array_equal(np.asarray(got[k], dtype=dt), gold[k]), k
+    # radii = ceil(3.5 sqrt(lambda_max)) of the reference's own cov_ray, 0 when culled
+    assert got["radii"].dtype == np.int32
+    assert np.array_equal(got["radii"], gold["radii"]), "radii"
     # packed: FP64 value rounded to FP32
     ref32 = gold["packed"].astype(np.float32).astype(np.float64)
     np.testing.assert_allclose(got["packed"].astype(np.float64), ref32, rtol=PACKED_RTOL,
@@ -93,6 +96,9 @@ def test_full_size_summary_parity(cuda, name):
     for k, dt in INT_DTYPES.items():
         h = hashlib.sha256(np.ascontiguousarray(got[k], dtype=dt).tobytes()).hexdigest()
         assert h == str(gold[f"sha_{k}"]), f"{k} differs from the reference"
+    h = hashlib.sha256(np.ascontiguousarray(got["radii"], dtype=np.int32).tobytes()).hexdigest()
+    assert h == str(gold["sha_radii"]), "radii differ from the reference"
+    assert int(got["radii"].astype(np.int64).sum()) == int(gold["radii_sum"])
     assert got["valid"].shape[0] == int(gold["M"])
     assert got["pair_splat"].shape[0] == int(gold["P"])
     rows = gold["packed_sample_rows"]
@@ -170,18 +176,16 @@ def test_look_at_views_oracle(cuda):
         assert_grads(got, ref_g)
 
 
-def test_radii_match_oracle_formula(cuda):
-    """radii = ceil(3.5 sqrt(lambda_max)) for visible splats, 0 when culled."""
-    gold = load_golden("mini")
-    sa = scenes.frustum(300, 2, 64, 48, seed=3)
-    got = run_gpu(sa, 0)
-    radii = got["radii"]
-    vis = np.zeros(len(sa), bool)
-    vis[gold["valid"]] = True
-    assert (radii[~vis] == 0).all()
-    assert (radii[vis] >= 1).all()
-    # rect span is consistent with the radius: the pixel rect fits in 2*ceil(r)+1
-    assert np.array_equal(np.nonzero(radii)[0], gold["valid"])
+def test_radii_match_live_oracle(cuda):
+    """Radii bit-exact against the live oracle on an unseen scene with a wide radius
+    range (sigma 0.3-40 px), float32 and float64 inputs."""
+    O = _oracle()
+    sa = scenes.frustum(20_000, 1, 480, 320, seed=23, sig_lo=0.3, sig_hi=40.0)
+    ref = O.prepare(sa.as_float64(), CameraModel(**sa.cameras[0]))
+    assert ref.radii.max() > 100
+    for dt in (torch.float32, torch.float64):
+        got = run_gpu(sa, 0, "half", dt)
+        assert np.array_equal(got["radii"], ref.radii), dt
 
 
 def test_steep_and_sign_mode_splats_oracle(cuda):

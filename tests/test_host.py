@@ -54,6 +54,27 @@ def test_scene_validation_on_cpu():
         Scene(*fields, sh_degree=1, background_color=(2, 0, 0), device="cpu")
 
 
+def test_autograd_front_end_checks_shapes_on_cpu():
+    """torch_api builds its Scene unvalidated (no device sync), but the shape checks
+    still run before anything reaches K1/K7: a shs tensor of the wrong degree or a
+    field of the wrong length raises instead of reading out of bounds."""
+    from paper_2406_02720_b200 import torch_api
+    sa = scenes.frustum(20, 1, 32, 32, seed=1)
+    t = {f: torch.from_numpy(getattr(sa, f)) for f in sa.FIELDS}
+    settings = torch_api.HalfGaussianRasterizationSettings(
+        image_height=32, image_width=32, world_to_cam=np.eye(4), fx=30.0, fy=30.0, cx=16.0,
+        cy=16.0, sh_degree=2)
+    with pytest.raises(ValueError, match="sh_coeffs"):
+        torch_api.rasterize_half_gaussians(t["mu"], t["normal"], t["raw_opacity_a"],
+                                           t["raw_opacity_b"], t["log_scale"], t["rotation"],
+                                           t["sh_coeffs"], settings)
+    settings.sh_degree = 1
+    with pytest.raises(ValueError, match="opacity"):
+        torch_api.rasterize_half_gaussians(t["mu"], t["normal"], t["raw_opacity_a"][:-1],
+                                           t["raw_opacity_b"], t["log_scale"], t["rotation"],
+                                           t["sh_coeffs"], settings)
+
+
 def test_backend_seam():
     assert backend.available_backends() == ["cuda"]
     backend.set_backend("cuda")
@@ -160,6 +181,33 @@ def test_scene_io_header_errors(tmp_path):
                                   b"\0" * 8))
     with pytest.raises(ValueError):
         scene_io.import_3dgs(write("f.ply", "ply\n"), normal_init="bogus")
+    # the reference's messages (scene_io.py:49-88), parsed before any device work
+    for text, msg in [
+            ("", "not a PLY file"),
+            ("ply\n", "expected format binary_little_endian"),
+            ("ply\nformat binary_little_endian 1.0\nelement face 2\nend_header\n",
+             "unsupported element face"),
+            ("ply\nformat binary_little_endian 1.0\nproperty half x\nend_header\n",
+             "unsupported property type half"),
+            ("ply\nformat binary_little_endian 1.0\nbogus line\nend_header\n",
+             "unexpected header line 'bogus line'"),
+            ("ply\nformat binary_little_endian 1.0\nproperty float x\nend_header\n",
+             "missing vertex element"),
+            ("ply\nformat binary_little_endian 1.0\nelement vertex 3\n", "unterminated header")]:
+        with pytest.raises(errors.MalformedHeader, match=msg):
+            scene_io.load_scene(write("g.ply", text))
+    h = scene_io._parse_header(b"ply\nformat binary_little_endian 1.0\ncomment sh_degree 3\n"
+                               b"comment background 0.1 0.2 0.3\n\nelement vertex 2\n"
+                               b"property double x\nproperty float y\nend_header\nPAYLOAD")
+    assert (h.count, h.props, h.stride) == (2, [("x", "double"), ("y", "float")], 12)
+    assert h.comments == {"sh_degree": "3", "background": "0.1 0.2 0.3"}
+    assert h.payload_offset == len(b"ply\nformat binary_little_endian 1.0\ncomment sh_degree 3\n"
+                                   b"comment background 0.1 0.2 0.3\n\nelement vertex 2\n"
+                                   b"property double x\nproperty float y\nend_header\n")
+    assert scene_io._rest_names({"f_rest_1": 0, "f_rest_0": 0, "x": 0}) == ["f_rest_0",
+                                                                            "f_rest_1"]
+    with pytest.raises(errors.MissingProperty, match="not contiguous"):
+        scene_io._rest_names({"f_rest_1": 0, "f_rest_2": 0})
 
 
 def _bucketed_worker(rank, world, port, q):

@@ -49,6 +49,7 @@ def test_oracle_full_fixture(name):
     f = out.frame
     for k, dt in INTS.items():
         assert np.array_equal(np.asarray(getattr(f, k), dtype=dt), gold[k]), k
+    assert np.array_equal(f.radii, gold["radii"]), "radii"
     # packed: only libm-vs-numpy `exp` ulps separate the two
     np.testing.assert_allclose(f.packed, gold["packed"], rtol=1e-9, atol=1e-12)
     for k in ("color", "alpha", "depth", "transmittance"):
@@ -75,6 +76,7 @@ def test_oracle_c2_summary():
     f = out.frame
     for k, dt in INTS.items():
         assert _sha(getattr(f, k), dt) == str(gold[f"sha_{k}"]), k
+    assert _sha(f.radii, np.int32) == str(gold["sha_radii"]), "radii"
     px = gold["px_index"]
     np.testing.assert_allclose(out.color.reshape(-1, 3)[px], gold["px_color"], atol=1e-11)
     assert np.array_equal(out.per_pixel_terminal_index.reshape(-1)[px], gold["px_terminal"])
@@ -128,6 +130,16 @@ def test_loss_oracle_matches_reference():
             assert s == pytest.approx(float(gold[f"{c}_ssim"]), rel=1e-12), c
     s, _ = O.ssim_with_grad(gold["same_l02_a"], gold["same_l02_a"])
     assert s == 1.0
+
+
+def test_loss_oracle_float64_inputs():
+    """The oracle on float64 / uint8 inputs float32 cannot hold (loss64.npz)."""
+    gold = load_golden("loss64")
+    for c in gold["cases"]:
+        a, b, lam = gold[f"{c}_a"], gold[f"{c}_b"], float(gold[f"{c}_lambda"])
+        loss, grad = O.compute_loss(a, b, lam)
+        assert np.array_equal(grad, gold[f"{c}_grad"]), c
+        assert loss == pytest.approx(float(gold[f"{c}_loss"]), rel=1e-12, abs=1e-15), c
 
 
 def test_adam_oracle_matches_reference():
