@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the per-config records (multiview_c4, c1, c2, c5)")
     return ap.parse_args()
 
 
@@ -332,6 +334,120 @@ def bench_config(cfg, world, views_per_step=None):
             "l2": "inputs larger than L2 (scene 252 MB + 64 MB records per view at c3)"}
 
 
+def view_evals(out, cam, torch):
+    """(forward, backward) pixel-splat evaluations of one rendered view: SURVEY.md
+    8(d)'s counts, sum_px min(terminal + 1, list length) and sum_px terminal."""
+    term = out.terminal.to(torch.int64)
+    starts = torch.as_tensor(out.frame.export()["tile_starts"], device=term.device)
+    lens = (starts[1:] - starts[:-1]).reshape(out.frame.tiles_y, out.frame.tiles_x)
+    lens_px = lens.repeat_interleave(16, 0).repeat_interleave(16, 1)[:cam.height, :cam.width]
+    return int(torch.minimum(term + 1, lens_px).sum().item()), int(term.sum().item())
+
+
+def config_run(cfg, args, world, rank, fp32_peak, torch, dist, barrier):
+    """GPU-only fwd+bwd throughput of one BASELINE config with its blend roofline
+    fractions (the K5/K6 FP32 fractions per config).  c4 is
+    north_star's multi-GPU configuration: its batch of 8 views is sharded over the
+    ranks and the gradient buffer all-reduced (bucketed under K7) every step;
+    `allreduce_exposed_ms` is the time from the last K7 launch to the end of the
+    exchange on the compute stream.  Other configs: one view per rank."""
+    from paper_2406_02720_b200 import device, scenes
+    from paper_2406_02720_b200.geometry import CameraModel, Scene
+    from paper_2406_02720_b200.multiview import GradientAllReduce, shard_views
+    sa = scenes.make_config(cfg)
+    multi = len(sa.cameras) > 1
+    if multi:
+        cams = [CameraModel(**c) for c in sa.cameras]
+        views = shard_views(len(cams), world, rank)
+    else:
+        cams = [CameraModel(**jitter_camera(sa.cameras[0], rank))]
+        views = [0]
+    scene = Scene(*(getattr(sa, f) for f in sa.FIELDS), sh_degree=sa.sh_degree,
+                  background_color=sa.background_color, device="cuda", dtype=torch.float32)
+    del sa
+    d_colors = [torch.as_tensor(scenes.cotangent(c.height, c.width, seed=1 + v),
+                                dtype=torch.float32, device="cuda") for v, c in enumerate(cams)]
+    grads = device.DeviceGradientSet.empty_flat(scene)
+    reducer = GradientAllReduce(grads) if world > 1 else None
+    buckets = GradientAllReduce.bucket_ranges(len(scene)) if reducer is not None else None
+    rast = device.Rasterizer("cuda", slots=1)
+    timer = device.StageTimer()
+    marks = []
+
+    def step(t=None):
+        for j, v in enumerate(views):
+            out = rast.render(scene, cams[v], timer=t)
+            last = j == len(views) - 1 and reducer is not None
+            rast.render_backward(scene, cams[v], out, d_colors[v], grads=grads, timer=t,
+                                 accumulate=j > 0, buckets=buckets if last else None,
+                                 on_bucket=reducer.start_range if last else None)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        if reducer is not None:
+            reducer.finish()
+        e1 = torch.cuda.Event(enable_timing=True)
+        e1.record()
+        if t is not None:
+            marks.append((e0, e1))
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    steps = max(3, min(args.steps, 10))
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    start.record()
+    for _ in range(steps):
+        step(timer)
+    end.record()
+    barrier()
+    ms = start.elapsed_time(end) / steps
+    exposed = statistics.mean(a.elapsed_time(b) for a, b in marks) if marks else 0.0
+    t = torch.tensor([ms, exposed], device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms, exposed = float(t[0]), float(t[1])
+    tot = timer.totals()
+    per_view = {k: sum(v) / steps / max(1, len(views)) for k, v in tot.items()}
+    fwd_e = bwd_e = 0
+    for v in views:
+        out = rast.render(scene, cams[v])
+        fe, be = view_evals(out, cams[v], torch)
+        fwd_e += fe
+        bwd_e += be
+    k5 = sum(tot.get("blend_fwd", [0.0])) / steps
+    k6 = sum(tot.get("blend_bwd", [0.0])) / steps
+    n_views = len(cams) if multi else world
+    rec = {"value": n_views * 1e3 / ms, "unit": "views/s" if multi else "iters/s",
+           "ms_per_step": ms, "steps": steps, "views_per_step": n_views,
+           "views_this_rank": len(views), "stage_ms_per_view": per_view,
+           "blend_fwd_frac": fwd_e * FWD_FLOPS_PER_EVAL / (k5 * 1e-3) / 1e12 / fp32_peak
+           if k5 else None,
+           "blend_bwd_frac": bwd_e * BWD_FLOPS_PER_EVAL / (k6 * 1e-3) / 1e12 / fp32_peak
+           if k6 else None,
+           "evals_this_rank": {"fwd": fwd_e, "bwd": bwd_e}, "n_gaussians": len(scene),
+           "resolution": [cams[0].width, cams[0].height]}
+    if multi:
+        rec["allreduce_exposed_ms"] = exposed
+        rec["k7_ms_per_view"] = per_view.get("preprocess_bwd")
+        rec["what"] = (f"{cfg}: batch of {len(cams)} views sharded over {world} rank(s), K1-K7 per "
+                       "view, gradients summed over the batch" +
+                       (" and all-reduced (NCCL via hs_grad_allreduce, 4 buckets under K7)"
+                        if world > 1 else ""))
+    del scene, grads, rast
+    torch.cuda.empty_cache()
+    return rec
+
+
+def nccl_info(torch, dist, world):
+    """The communicator the exchange uses, as NCCL reports it (ranks, version)."""
+    if world <= 1:
+        return None
+    from paper_2406_02720_b200.multiview import NcclComm
+    ranks, rank, version = NcclComm.for_group(None).info()
+    return {"ranks": ranks, "rank": rank, "nccl_version": version,
+            "debug": os.environ.get("NCCL_DEBUG")}
+
+
 # --------------------------------------------------------------------------
 def main():
     args = parse()
@@ -349,6 +465,9 @@ def main():
     world, rank, local = rank_info()
     torch.cuda.set_device(local)
     if world > 1:
+        # the communicators' INIT lines (ranks, NVLS / channels) go to stderr
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     lib = _native.load()
 
@@ -587,10 +706,20 @@ def main():
     # Adam moves param, m, v (read+write) and reads grad: 28 B per float32 element
     adam_bytes = sum(getattr(scene, f).numel() for f in scene.FIELDS) * 7 * scene.mu.element_size()
 
+    # north_star's multi-GPU configuration at this N, and every other BASELINE config's
+    # GPU-only throughput with its blend roofline fractions (value stays on --config)
+    configs = {}
+    if not args.no_configs:
+        for cfg in ("c4", "c1", "c2", "c5"):
+            if cfg != args.config:
+                configs["multiview_c4" if cfg == "c4" else cfg] = config_run(
+                    cfg, args, world, rank, peak_a.value, torch, dist, barrier)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args.config)
 
+    comm_info = nccl_info(torch, dist, world)
     views_per_step = len(cams) if multi else world
     value = views_per_step * 1e3 / ms
     if rank == 0:
@@ -614,6 +743,7 @@ def main():
                                    "(hs_adam_step), synthetic targets",
                            "densify": densify},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "configs": configs, "nccl": comm_info,
             "gpu_launches": launches, "clocks": clock_info,
             "counts": {"P": out.frame.num_pairs, "fwd_evals": fwd_evals, "bwd_evals": bwd_evals},
         }

@@ -404,6 +404,30 @@ int32_t hs_ply_row_bytes(int32_t sh_degree, int32_t kind);
  * HS_PLY_3DGS_MEAN writes logit(clip((a1 + a2) / 2, 1e-6, 1 - 1e-6)). */
 int hs_ply_pack(const hs_scene* scene, void* payload, int32_t kind, void* stream);
 
+/* ---- multi-GPU: the gradient exchange ------------------
+ * View-sharded training: every rank renders its views against a replica of
+ * the Gaussians and accumulates their gradients (hs_grads.accumulate = 1);
+ * the batch gradient is the sum over ranks (GradientSet.add,
+ * rasterizer.py:100-105).  A communicator is an NCCL communicator (NCCL is
+ * loaded at run time; these return HS_ERR_CUDA without it).  Rank 0 calls
+ * hs_comm_unique_id, the host hands the HS_COMM_ID_BYTES bytes to every rank
+ * (any channel), and every rank calls hs_comm_init on its own device. */
+#define HS_COMM_ID_BYTES 128
+int hs_comm_unique_id(void* id);
+int hs_comm_init(void** comm, int32_t world, int32_t rank, const void* id);
+int hs_comm_destroy(void* comm);
+/* Ranks in / this rank of `comm`, and the NCCL version loaded (comm may be
+ * NULL for the version only). */
+int hs_comm_info(void* comm, int32_t* world, int32_t* rank, int32_t* nccl_version);
+/* Sums primitive rows [begin, end) of every gradient field of `grads` (n
+ * primitives, SH degree, dtype HS_DTYPE_F32/F64) over the ranks of `comm`, in
+ * place, as one NCCL group on `stream`; with_touch also sums the int32 touch
+ * counts.  Issued on a side stream after each K7 bucket
+ * (hs_preprocess_bwd_range), bucket b's exchange overlaps bucket b+1's K7. */
+int hs_grad_allreduce(void* comm, const hs_grads* grads, int64_t n, int32_t sh_degree,
+                      int32_t dtype, int64_t begin, int64_t end, int32_t with_touch,
+                      void* stream);
+
 /* ---- misc --------------------------------------------------------------- */
 const char* hs_status_string(int status);
 const char* hs_last_cuda_error(void);

@@ -25,6 +25,7 @@ HS_ERR_INVALID_LAMBDA = 9
 
 HS_DTYPE_F32 = 0
 HS_DTYPE_F64 = 1
+HS_COMM_ID_BYTES = 128
 HS_KERNEL_HALF = 0
 HS_KERNEL_FULL = 1
 
@@ -162,6 +163,13 @@ _SIGNATURES = {
     "hs_opacity_disparity_workspace_size": (c_size_t, [c_int64]),
     "hs_opacity_disparity": (c_int32, [ctypes.POINTER(HsScene), c_void_p, c_void_p, c_size_t,
                                        c_void_p]),
+    "hs_comm_unique_id": (c_int32, [c_void_p]),
+    "hs_comm_init": (c_int32, [ctypes.POINTER(c_void_p), c_int32, c_int32, c_void_p]),
+    "hs_comm_destroy": (c_int32, [c_void_p]),
+    "hs_comm_info": (c_int32, [c_void_p, ctypes.POINTER(c_int32), ctypes.POINTER(c_int32),
+                               ctypes.POINTER(c_int32)]),
+    "hs_grad_allreduce": (c_int32, [c_void_p, ctypes.POINTER(HsGrads), c_int64, c_int32, c_int32,
+                                    c_int64, c_int64, c_int32, c_void_p]),
     "hs_status_string": (ctypes.c_char_p, [c_int32]),
     "hs_last_cuda_error": (ctypes.c_char_p, []),
     "hs_kernel_launch_count": (c_int64, []),

@@ -38,6 +38,7 @@ SOURCES = {
     "hs_blend.cu": [],
     "hs_capi.cu": [],
     "hs_microbench.cu": [],
+    "hs_comm.cu": [],
 }
 
 
@@ -88,7 +89,7 @@ def build(force=False, verbose=False):
             raise RuntimeError(f"nvcc failed on {src}")
         objs.append(obj)
     tmp = LIB_PATH + ".tmp"
-    cmd = [nvcc, *ARCH, "-shared", "--cudart", "static", "-o", tmp, *objs]
+    cmd = [nvcc, *ARCH, "-shared", "--cudart", "static", "-o", tmp, *objs, "-ldl"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)

@@ -1091,6 +1091,10 @@ __global__ void __launch_bounds__(NT, HS_K7_MINB) preprocess_bwd_kernel(
       const int tt = e / (3 * K);
       return sm.sh[tt * St::SHS + (e - tt * 3 * K)];
     });
+    // multimem.red is relaxed: release this thread's reductions at system scope
+    // before the kernel ends, so the host-side cross-rank barrier that closes the
+    // batch (FusedGradientReduce.end) orders them before any rank reads its copy
+    if (mc) asm volatile("fence.acq_rel.sys;\n" ::: "memory");
     return;
   }
   store_block<NT, 3>(out.d_mu + base * 3, ncta, acc ? g->mu : nullptr, touch_s,

@@ -368,6 +368,15 @@ class DeviceGradientSet:
         return [getattr(self, name) for name in self.NAMES]
 
 
+def grads_struct(grads, accumulate=0):
+    """hs_grads over a DeviceGradientSet's buffers."""
+    g = _native.HsGrads()
+    for name in DeviceGradientSet.NAMES:
+        setattr(g, name, getattr(grads, name).data_ptr())
+    g.accumulate = accumulate
+    return g
+
+
 class Rasterizer:
     """Allocation-free rendering loop: `slots` persistent workspaces used round
     robin.  An output stays valid until its slot is reused `slots` renders later
@@ -419,10 +428,7 @@ def render_backward(scene, cam, out, d_color, grads=None, timer=None, accumulate
     _native.check(st, "hs_blend_bwd")
     if grads is None:
         grads = DeviceGradientSet.empty_like_scene(scene)
-    g = _native.HsGrads()
-    for name in DeviceGradientSet.NAMES:
-        setattr(g, name, getattr(grads, name).data_ptr())
-    g.accumulate = 1 if accumulate else 0
+    g = grads_struct(grads, 1 if accumulate else 0)
     if reduce_ptrs is not None:
         # reduction stores: {name: address} (NVLS multicast addresses -> mode 3, or the
         # buffers' own addresses with reduce_ptrs["mode"] == 2 for device atomics)

@@ -21,15 +21,61 @@ def shard_views(n_views, world, rank):
     return list(range(lo, min(lo + per, n_views)))
 
 
+class NcclComm:
+    """An NCCL communicator of the library (hs_comm_*), one per process group: rank 0
+    creates the unique id, the group broadcasts it, every rank joins on its current
+    device.  hs_grad_allreduce then sums gradient ranges as single NCCL groups."""
+
+    _cache = {}
+
+    def __init__(self, group=None):
+        import ctypes
+        from . import _native
+        lib = _native.load()
+        world = dist.get_world_size(group)
+        rank = dist.get_rank(group)
+        uid = torch.zeros(_native.HS_COMM_ID_BYTES, dtype=torch.uint8)
+        if rank == 0:
+            _native.check(lib.hs_comm_unique_id(ctypes.c_void_p(uid.data_ptr())),
+                          "hs_comm_unique_id")
+        on_gpu = dist.get_backend(group) == "nccl"
+        buf = uid.cuda() if on_gpu else uid
+        dist.broadcast(buf, src=dist.get_global_rank(group, 0) if group is not None else 0,
+                       group=group)
+        uid = buf.cpu()
+        self.handle = ctypes.c_void_p()
+        _native.check(lib.hs_comm_init(ctypes.byref(self.handle), world, rank,
+                                       ctypes.c_void_p(uid.data_ptr())), "hs_comm_init")
+        self.world, self.rank = world, rank
+
+    @classmethod
+    def for_group(cls, group=None):
+        key = id(group) if group is not None else None
+        if key not in cls._cache:
+            cls._cache[key] = cls(group)
+        return cls._cache[key]
+
+    def info(self):
+        """(ranks, rank, NCCL version) as the communicator reports them."""
+        import ctypes
+        from . import _native
+        w, r, v = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+        _native.check(_native.load().hs_comm_info(self.handle, ctypes.byref(w), ctypes.byref(r),
+                                                  ctypes.byref(v)), "hs_comm_info")
+        return w.value, r.value, v.value
+
+
 class GradientAllReduce:
     """Sums a flat gradient buffer (+ int touch counts) over the default group.
 
     allreduce() sums everything after the last K7.  The bucketed form overlaps the
     exchange with K7: K7 runs over primitive buckets
-    (`bucket_ranges`), start_range(b, e) issues the bucket's all-reduce
-    asynchronously right after its K7 launch (NCCL orders it after that launch on
-    its own stream, so it runs under the next bucket's K7), and finish() waits
-    for all of them and sums the touch counts."""
+    (`bucket_ranges`), start_range(b, e) issues the bucket's exchange right after
+    its K7 launch on a side stream that waits for that launch, so it runs under the
+    next bucket's K7, and finish() makes the compute stream wait for all of them.
+    On CUDA tensors over NCCL each exchange is one grouped hs_grad_allreduce (every
+    field slice and the touch counts of the range); with gloo (CPU tests) it is a
+    public dist.all_reduce per slice."""
 
     def __init__(self, grads, group=None):
         if not hasattr(grads, "flat"):
@@ -37,13 +83,34 @@ class GradientAllReduce:
         self.grads = grads
         self.group = group
         self._pending = []
+        self._comm = None
+        self._stream = None
+        self._touch_done = False
+        if self._active() and grads.flat.is_cuda and dist.get_backend(group) == "nccl":
+            self._comm = NcclComm.for_group(group)
+            self._stream = torch.cuda.Stream(device=grads.flat.device)
 
     @staticmethod
     def _active():
         return dist.is_available() and dist.is_initialized()
 
+    def _native_range(self, b, e, stream):
+        import ctypes
+        from . import _native, device
+        g = self.grads
+        dtype = _native.HS_DTYPE_F64 if g.d_mu.dtype == torch.float64 else _native.HS_DTYPE_F32
+        k = g.d_sh.shape[1]
+        deg = {1: 0, 4: 1, 9: 2, 16: 3}[k]
+        st = device.grads_struct(g, 0)
+        _native.check(_native.load().hs_grad_allreduce(
+            self._comm.handle, ctypes.byref(st), g.d_mu.shape[0], deg, dtype, b, e, 1,
+            ctypes.c_void_p(stream.cuda_stream)), "hs_grad_allreduce")
+
     def allreduce(self):
         if not self._active():
+            return self.grads
+        if self._comm is not None:
+            self._native_range(0, self.grads.d_mu.shape[0], torch.cuda.current_stream())
             return self.grads
         dist.all_reduce(self.grads.flat, op=dist.ReduceOp.SUM, group=self.group)
         dist.all_reduce(self.grads.touch_count, op=dist.ReduceOp.SUM, group=self.group)
@@ -65,26 +132,27 @@ class GradientAllReduce:
     def start_range(self, b, e):
         if not self._active():
             return
-        tensors = self.slices(b, e)
-        if tensors[0].is_cuda and dist.get_backend(self.group) == "nccl":
-            from torch.distributed.distributed_c10d import _coalescing_manager
-            # one grouped NCCL launch for the bucket's eight field slices
-            with _coalescing_manager(group=self.group, device=tensors[0].device,
-                                     async_ops=True) as cm:
-                for t in tensors:
-                    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
-            self._pending.append(cm)
-        else:
-            self._pending.extend(dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group,
-                                                 async_op=True) for t in tensors)
+        if self._comm is not None:
+            ev = torch.cuda.Event()
+            ev.record(torch.cuda.current_stream())
+            self._stream.wait_event(ev)
+            self._native_range(b, e, self._stream)
+            self._pending.append(True)
+            return
+        tensors = self.slices(b, e) + [self.grads.touch_count[b:e]]
+        self._pending.extend(dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group,
+                                             async_op=True) for t in tensors)
 
     def finish(self):
         if not self._active():
             return self.grads
-        for w in self._pending:
-            w.wait()
+        if self._comm is not None:
+            if self._pending:
+                torch.cuda.current_stream().wait_stream(self._stream)
+        else:
+            for w in self._pending:
+                w.wait()
         self._pending = []
-        dist.all_reduce(self.grads.touch_count, op=dist.ReduceOp.SUM, group=self.group)
         return self.grads
 
 
