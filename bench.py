@@ -587,7 +587,9 @@ def main():
         dist.all_reduce(fwd_t, op=dist.ReduceOp.MAX)
         fwd_ms = float(fwd_t.item())
 
-    # algorithmic work of the dominant kernels
+    # algorithmic work of the dominant kernels, from a fresh render of
+    # the timed view (the forward-only loop above reused the workspace)
+    out = rast.render(scene, cam)
     term = out.terminal.to(torch.int64)
     starts = torch.as_tensor(out.frame.export()["tile_starts"], device="cuda")
     lens = (starts[1:] - starts[:-1]).reshape(out.frame.tiles_y, out.frame.tiles_x)
@@ -745,7 +747,7 @@ def main():
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "configs": configs, "nccl": comm_info,
             "gpu_launches": launches, "clocks": clock_info,
-            "counts": {"P": out.frame.num_pairs, "fwd_evals": fwd_evals, "bwd_evals": bwd_evals},
+            "counts": {"P": p_pairs, "fwd_evals": fwd_evals, "bwd_evals": bwd_evals},
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -109,11 +109,16 @@ typedef struct hs_frame {
   int32_t kernel;       /* HS_KERNEL_HALF / HS_KERNEL_FULL */
   int32_t tile_bits;    /* significant bits of the pair sort key */
   int32_t sort_selector;/* internal: which pair double-buffer holds the result */
-  int64_t num_pairs;    /* P, valid after hs_frame_read_num_pairs */
+  int64_t num_pairs;    /* P once read (hs_frame_read_num_pairs / hs_frame_status),
+                           else -1 */
   void* frame_ws;       /* size hs_frame_workspace_size(n, width, height) */
   size_t frame_ws_bytes;
-  void* bin_ws;         /* size hs_binning_workspace_size(num_pairs, ...) */
+  void* bin_ws;         /* size hs_binning_workspace_size(n, pair_capacity, ...) */
   size_t bin_ws_bytes;
+  int64_t pair_capacity;/* pairs bin_ws is laid out for (0: num_pairs) */
+  int32_t depth_sort_full;/* in: 1 ranks depths with the full 64-bit sort (no
+                           run fixup, so no depth fallback can be pending); out:
+                           hs_frame_read_num_pairs sets it when it had to */
 } hs_frame;
 
 /* ---- Seam 2: staged device pipeline ----------------------------------- */
@@ -138,9 +143,36 @@ int hs_preprocess_fwd(hs_frame* frame, const hs_scene* scene,
  * full 64-bit sort before returning, so it must precede every use of the ranks. */
 int hs_frame_read_num_pairs(hs_frame* frame, void* stream);
 
-/* K2 duplicate-with-keys, K3 stable tile sort, K4 tile ranges.  Needs
- * frame->bin_ws of hs_binning_workspace_size(...) bytes. */
+/* K2 duplicate-with-keys, K3 stable tile sort, K4 tile ranges, once P is known.
+ * Needs frame->bin_ws of hs_binning_workspace_size(n, max(P, pair_capacity), ...)
+ * bytes. */
 int hs_bin_and_sort(hs_frame* frame, void* stream);
+
+/* The same binning with no host round trip: P stays on the device and the
+ * workspace is laid out for frame->pair_capacity pairs (set by the caller, e.g.
+ * from an earlier view's P with headroom).  K2 writes every pair straight into
+ * a row bucket and a stable counting sort by tile column finishes the order;
+ * tile_starts come out of the same scans.  If P exceeds the capacity nothing is
+ * binned (every tile list is empty, so the blends and K7 do no work) and the
+ * status says so: check it with hs_frame_status at the caller's next sync point
+ * and re-bin with a larger workspace.  Images wider than 2048 or taller than
+ * 1024 tiles take the synchronous path inside this call. */
+int hs_bin_async(hs_frame* frame, void* stream);
+
+/* Binning status flags (hs_frame_status) */
+#define HS_FRAME_PAIR_OVERFLOW 1 /* P > pair_capacity: re-bin (hs_bin_and_sort) */
+#define HS_FRAME_DEPTH_FALLBACK 2 /* a depth run was too long for the fixup:
+                                    hs_frame_read_num_pairs redoes the ranks */
+/* Synchronises `stream` and reads P (int64: more pairs than int32 offsets hold
+ * is reported, not wrapped) and the flags; with no flag set, frame->num_pairs
+ * becomes P. */
+int hs_frame_status(hs_frame* frame, int64_t* num_pairs, int32_t* flags, void* stream);
+/* The same status without waiting: enqueues on `stream` a copy of it into
+ * host_status (24 bytes of host memory, pinned for an asynchronous copy):
+ * int64 P at byte 0, int32 binning flags at byte 8 (bit 0: HS_FRAME_PAIR_OVERFLOW),
+ * int32 depth-fallback flag at byte 16 (non-zero: HS_FRAME_DEPTH_FALLBACK).
+ * Valid once the stream has passed this point (e.g. an event recorded after it). */
+int hs_frame_status_async(const hs_frame* frame, void* host_status, void* stream);
 
 /* hs_frame_read_num_pairs followed by hs_bin_and_sort in one call, so the GPU
  * is not left idle while the caller sizes the binning workspace: with a

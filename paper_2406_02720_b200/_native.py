@@ -26,6 +26,8 @@ HS_ERR_INVALID_LAMBDA = 9
 HS_DTYPE_F32 = 0
 HS_DTYPE_F64 = 1
 HS_COMM_ID_BYTES = 128
+HS_FRAME_PAIR_OVERFLOW = 1
+HS_FRAME_DEPTH_FALLBACK = 2
 HS_KERNEL_HALF = 0
 HS_KERNEL_FULL = 1
 
@@ -65,6 +67,7 @@ class HsFrame(ctypes.Structure):
         ("num_pairs", c_int64),
         ("frame_ws", c_void_p), ("frame_ws_bytes", c_size_t),
         ("bin_ws", c_void_p), ("bin_ws_bytes", c_size_t),
+        ("pair_capacity", c_int64), ("depth_sort_full", c_int32),
     ]
 
 
@@ -170,6 +173,10 @@ _SIGNATURES = {
                                ctypes.POINTER(c_int32)]),
     "hs_grad_allreduce": (c_int32, [c_void_p, ctypes.POINTER(HsGrads), c_int64, c_int32, c_int32,
                                     c_int64, c_int64, c_int32, c_void_p]),
+    "hs_bin_async": (c_int32, [ctypes.POINTER(HsFrame), c_void_p]),
+    "hs_frame_status": (c_int32, [ctypes.POINTER(HsFrame), ctypes.POINTER(c_int64),
+                                  ctypes.POINTER(c_int32), c_void_p]),
+    "hs_frame_status_async": (c_int32, [ctypes.POINTER(HsFrame), c_void_p, c_void_p]),
     "hs_status_string": (ctypes.c_char_p, [c_int32]),
     "hs_last_cuda_error": (ctypes.c_char_p, []),
     "hs_kernel_launch_count": (c_int64, []),

@@ -1,13 +1,16 @@
-// hs_binning.cu -- depth-rank sort (K3a), pair counts and their scan,
-// duplicate-with-keys (K2), the stable tile sort (K3b) and tile ranges (K4);
+// hs_binning.cu -- depth-rank sort (K3a), pair counts and their scan, and the
+// tile binning: duplicate-with-keys (K2) fused with a stable two-level counting
+// sort by tile (row buckets, then columns) that also yields the tile ranges (K4);
 // plus the FrameGeometry export used by the parity tests.
 //
 // The reference orders pairs with np.lexsort((prim index, depth f64, tile))
 // (rasterizer.py:318-323).  Here the primitives are first ranked once by
-// (depth f64 bits, index) with a stable 64-bit radix sort, pairs are emitted in
-// that rank order, and a stable radix sort on the tile id alone (tile_bits =
-// ceil(log2 n_tiles) bits, two 8-bit passes at 1080p) yields exactly the
-// lexsort order without ever materialising a 64-bit (tile|depth) key.
+// (depth f64 bits, index), pairs are generated in that rank order, and a STABLE
+// sort on the tile id alone yields exactly the lexsort order without ever
+// materialising a 64-bit (tile|depth) key.  The stable tile sort is the
+// row-bucket counting sort below (no host round trip: P stays on the device);
+// images wider than kBinMaxCols or taller than kBinMaxRows tiles use a CUB radix
+// sort on the tile id after a host read of P instead.
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
@@ -25,10 +28,10 @@ size_t depth_sort_temp_bytes(int64_t n) {
   return bytes > hi ? bytes : hi;
 }
 
-size_t scan_temp_bytes(int64_t n) {
+size_t scan_temp_bytes(int64_t n) {  // n scan entries
   size_t bytes = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, bytes, (const int32_t*)nullptr, (int32_t*)nullptr,
-                                (int)(n + 1));
+                                (int)n);
   return bytes;
 }
 
@@ -159,32 +162,373 @@ cudaError_t run_depth_sort_hi(void* temp, size_t temp_bytes, const uint64_t* key
   return cudaGetLastError();
 }
 
-__global__ void gather_counts_kernel(const int32_t* __restrict__ count,
-                                     const uint32_t* __restrict__ order, int32_t* __restrict__ cnt_r,
-                                     uint32_t* __restrict__ rank_of, int64_t n) {
-  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r > n) return;
-  if (r == n) {
-    cnt_r[n] = 0;
-    return;
+// cnt_r[r] = count[order[r]] and rank_of; P accumulates as int64 next to the
+// int32 scan (which may wrap).  With the row path (ROWS) each CTA -- one block of
+// kBinRanks ranks -- also histograms its pairs by tile row (a splat adds spans_x
+// to each row of its rect) into cnt_r[n + 1 + ty * nb + block].
+template <bool ROWS>
+__global__ void __launch_bounds__(kBinRanks) gather_counts_kernel(
+    const int32_t* __restrict__ count, const uint32_t* __restrict__ order,
+    const int4* __restrict__ rect, int32_t* __restrict__ cnt_r, uint32_t* __restrict__ rank_of,
+    int64_t n, int tiles_y, BinStatusDev* __restrict__ status) {
+  extern __shared__ int rows_s[];
+  __shared__ long long csum[kBinRanks / 32];
+  const int64_t r = (int64_t)blockIdx.x * kBinRanks + threadIdx.x;
+  if (ROWS) {
+    for (int ty = threadIdx.x; ty < tiles_y; ty += kBinRanks) rows_s[ty] = 0;
+    __syncthreads();
   }
-  const uint32_t i = order[r] & kIndexMask;
-  cnt_r[r] = count[i];
-  rank_of[i] = (uint32_t)r;
+  int c = 0;
+  if (r < n) {
+    const uint32_t i = order[r] & kIndexMask;
+    c = count[i];
+    cnt_r[r] = c;
+    rank_of[i] = (uint32_t)r;
+    if (ROWS && c > 0) {
+      const int4 rc = rect[i];
+      const int sx = rc.y - rc.x + 1;
+      for (int ty = rc.z; ty <= rc.w; ++ty) atomicAdd(&rows_s[ty], sx);
+    }
+  }
+  if (r == 0) cnt_r[n] = 0;
+  long long v = c;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) csum[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long t = 0;
+    for (int w = 0; w < kBinRanks / 32; ++w) t += csum[w];
+    if (t) atomicAdd(reinterpret_cast<unsigned long long*>(&status->pairs),
+                     (unsigned long long)t);
+  }
+  if (!ROWS) return;
+  const int64_t nb = gridDim.x;
+  for (int ty = threadIdx.x; ty < tiles_y; ty += kBinRanks)
+    cnt_r[n + 1 + ty * nb + blockIdx.x] = rows_s[ty];
 }
 
 cudaError_t run_count_scan(void* temp, size_t temp_bytes, const int32_t* count,
-                           const uint32_t* order, int32_t* cnt_r, int32_t* off_r,
-                           uint32_t* rank_of, int64_t n, cudaStream_t stream) {
-  const int block = 256;
-  gather_counts_kernel<<<(unsigned)((n + 1 + block - 1) / block), block, 0, stream>>>(
-      count, order, cnt_r, rank_of, n);
-  note_launch();
-  cudaError_t e = cudaGetLastError();
+                           const uint32_t* order, const int4* rect, int32_t* cnt_r,
+                           int32_t* off_r, uint32_t* rank_of, int64_t n, int tiles_y,
+                           BinStatusDev* status, cudaStream_t stream) {
+  const bool rows = tiles_y > 0;
+  const unsigned nb = (unsigned)bin_row_blocks(n);
+  cudaError_t e = cudaMemsetAsync(status, 0, sizeof(BinStatusDev), stream);
   if (e != cudaSuccess) return e;
-  e = cub::DeviceScan::ExclusiveSum(temp, temp_bytes, cnt_r, off_r, (int)(n + 1), stream);
+  if (rows) {
+    gather_counts_kernel<true><<<nb, kBinRanks, tiles_y * sizeof(int), stream>>>(
+        count, order, rect, cnt_r, rank_of, n, tiles_y, status);
+  } else {
+    gather_counts_kernel<false><<<nb, kBinRanks, 0, stream>>>(count, order, rect, cnt_r,
+                                                              rank_of, n, 0, status);
+  }
+  note_launch();
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  e = cub::DeviceScan::ExclusiveSum(temp, temp_bytes, cnt_r, off_r,
+                                    (int)count_scan_len(n, tiles_y, rows), stream);
   note_launch(2);
   return e;
+}
+
+// ---- row-bucket binning (no host round trip) --------------------------------
+// 256-thread exclusive scan of one int per thread; returns the CTA total.
+__device__ __forceinline__ int block_exclusive_scan(int v, int* excl, int* warp_tot) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += t;
+  }
+  if (lane == 31) warp_tot[w] = x;
+  __syncthreads();
+  int before = 0, total = 0;
+  for (int k = 0; k < (int)(blockDim.x >> 5); ++k) {
+    const int t = warp_tot[k];
+    before += k < w ? t : 0;
+    total += t;
+  }
+  *excl = before + x - v;
+  __syncthreads();
+  return total;
+}
+
+__device__ __forceinline__ bool bin_overflowed(const RowBinArgs& a, long long* p_out) {
+  const long long p = *reinterpret_cast<volatile long long*>(&a.status->pairs);
+  *p_out = p;
+  return p > a.capacity || p > 0x7fffffffll;
+}
+
+// start of row ty's bucket (the row histograms' scan entries are offset by P)
+__device__ __forceinline__ int row_start(const RowBinArgs& a, int ty, int p) {
+  return ty < a.tiles_y ? a.off_r[a.n + 1 + (int64_t)ty * a.nb] - p : p;
+}
+
+// Emit: one CTA per block of kBinRanks depth ranks (8 warps x 32 ranks, the
+// count pass's blocks).  Warp w's pairs are one contiguous run of the
+// generation order; in each tile row they go to
+//   row bucket base (the scan) + the earlier warps' pairs in that row + the
+//   warp's earlier pairs in that row (match_any on the row, in pair order),
+// so every row bucket holds its pairs in generation (depth rank) order.
+// CTA 0 also lays out the column passes' chunks (kBinChunk pairs, row-aligned).
+__global__ void __launch_bounds__(kBinRanks) row_emit_kernel(RowBinArgs a) {
+  extern __shared__ int wrow[];  // [8][tiles_y]
+  __shared__ int scan_tot[kBinRanks / 32];
+  long long p64;
+  if (bin_overflowed(a, &p64)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.status->flags |= kBinFlagOverflow;
+    return;
+  }
+  const int p = (int)p64;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int T = a.tiles_y;
+  if (blockIdx.x == 0) {
+    // chunk layout: row ty's bucket is split into ceil(len / kBinChunk) chunks
+    constexpr int kPer = kBinMaxRows / kBinRanks;
+    int nch[kPer], tot = 0;
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int ty = threadIdx.x * kPer + k;
+      nch[k] = ty < T ? (row_start(a, ty + 1, p) - row_start(a, ty, p) + kBinChunk - 1) /
+                            kBinChunk
+                      : 0;
+      tot += nch[k];
+    }
+    int excl;
+    const int all = block_exclusive_scan(tot, &excl, scan_tot);
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int ty = threadIdx.x * kPer + k;
+      if (ty < T) a.chunk_first[ty] = excl;
+      excl += nch[k];
+    }
+    if (threadIdx.x == 0) a.chunk_first[T] = all;
+  }
+  for (int e = threadIdx.x; e < 8 * T; e += kBinRanks) wrow[e] = 0;
+  __syncthreads();
+  const int64_t r = (int64_t)blockIdx.x * kBinRanks + threadIdx.x;
+  const int c = r < a.n ? a.cnt_r[r] : 0;
+  uint32_t v = 0;
+  int4 rc = make_int4(0, 0, 0, 0);
+  int spans_x = 1;
+  if (c > 0) {
+    v = a.order[r];
+    const uint32_t i = v & kIndexMask;
+    rc = a.rect[i];
+    spans_x = rc.y - rc.x + 1;
+    // pair (tx, ty) of this splat has generation index origin + ty * spans_x + tx
+    reinterpret_cast<float*>(a.rec)[(size_t)i * kRecordFloats + R_ROW_ORIGIN] =
+        __int_as_float(a.off_r[r] - rc.z * spans_x - rc.x);
+    for (int ty = rc.z; ty <= rc.w; ++ty) atomicAdd(&wrow[w * T + ty], spans_x);
+  }
+  __syncthreads();
+  for (int ty = threadIdx.x; ty < T; ty += kBinRanks) {
+    int base = a.off_r[a.n + 1 + (int64_t)ty * a.nb + blockIdx.x] - p;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int t = wrow[k * T + ty];
+      wrow[k * T + ty] = base;
+      base += t;
+    }
+  }
+  __syncthreads();
+  int* cur = wrow + w * T;
+  // the warp's pairs, consecutive lanes on consecutive pairs (splat-major, then
+  // row-major over the splat's rect)
+  int incl = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  const int excl = incl - c;
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  const unsigned lt = (1u << lane) - 1u;
+  for (int j0 = 0; j0 < total; j0 += 32) {
+    const int j = j0 + lane;
+    int sidx = 0;
+#pragma unroll
+    for (int step = 16; step > 0; step >>= 1) {
+      const int cand = sidx + step;
+      const int e = __shfl_sync(0xffffffffu, excl, cand & 31);
+      if (cand < 32 && e <= j) sidx = cand;
+    }
+    const int es = __shfl_sync(0xffffffffu, excl, sidx);
+    const int sx = __shfl_sync(0xffffffffu, spans_x, sidx);
+    const int x0 = __shfl_sync(0xffffffffu, rc.x, sidx);
+    const int y0 = __shfl_sync(0xffffffffu, rc.z, sidx);
+    const uint32_t vs = __shfl_sync(0xffffffffu, v, sidx);
+    const bool live = j < total;
+    const int l = j - es, ly = l / sx, lx = l - ly * sx;
+    const int ty = live ? y0 + ly : -1;
+    const unsigned peers = __match_any_sync(0xffffffffu, ty);
+    const int pos = live ? cur[ty] + __popc(peers & lt) : 0;
+    __syncwarp();
+    if (live && lane == __ffs(peers) - 1) cur[ty] += __popc(peers);
+    __syncwarp();
+    if (live) {
+      a.tx_row[pos] = (uint16_t)(x0 + lx);
+      a.val_row[pos] = vs;
+    }
+  }
+}
+
+// The chunk a column-pass CTA owns: its row and [begin, end) in the row buckets.
+__device__ __forceinline__ bool chunk_of(const RowBinArgs& a, int p, int c, int* ty, int* begin,
+                                         int* end) {
+  const int T = a.tiles_y;
+  if (c >= a.chunk_first[T]) return false;
+  int lo = 0, hi = T;  // last row with chunk_first[row] <= c
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (a.chunk_first[mid] <= c) lo = mid; else hi = mid;
+  }
+  *ty = lo;
+  const int rs = row_start(a, lo, p), re = row_start(a, lo + 1, p);
+  *begin = rs + (c - a.chunk_first[lo]) * kBinChunk;
+  *end = min(*begin + kBinChunk, re);
+  return true;
+}
+
+// Column pass 1: per chunk, pairs per tile column -> hist[chunk][tx].
+__global__ void __launch_bounds__(256) tile_hist_kernel(RowBinArgs a) {
+  extern __shared__ int hs_[];  // [tiles_x]
+  long long p64;
+  if (bin_overflowed(a, &p64)) return;
+  int ty, begin, end;
+  if (!chunk_of(a, (int)p64, blockIdx.x, &ty, &begin, &end)) return;
+  for (int t = threadIdx.x; t < a.tiles_x; t += 256) hs_[t] = 0;
+  __syncthreads();
+  for (int k = begin + threadIdx.x; k < end; k += 256) atomicAdd(&hs_[a.tx_row[k]], 1);
+  __syncthreads();
+  int32_t* h = a.hist + (int64_t)blockIdx.x * a.tiles_x;
+  for (int t = threadIdx.x; t < a.tiles_x; t += 256) h[t] = hs_[t];
+}
+
+// Column pass 2: one CTA per tile row.  Each column's chunk counts become
+// exclusive prefixes over the row's chunks (in place); the columns' totals,
+// scanned along the row from the row's bucket start, are the row's tile_starts
+// (np.searchsorted's CSR, rasterizer.py:324-325).  On overflow every tile list
+// is left empty, so the blends and K7 see no pairs.
+__global__ void __launch_bounds__(256) tile_scan_kernel(RowBinArgs a) {
+  __shared__ int tot_s[kBinMaxCols];
+  __shared__ int scan_tot[8];
+  long long p64;
+  const int ty = blockIdx.x, X = a.tiles_x;
+  if (bin_overflowed(a, &p64)) {
+    for (int t = threadIdx.x; t < X; t += 256) a.tile_starts[ty * X + t] = 0;
+    if (ty == a.tiles_y - 1 && threadIdx.x == 0) a.tile_starts[a.tiles_y * X] = 0;
+    return;
+  }
+  const int p = (int)p64;
+  const int c0 = a.chunk_first[ty], c1 = a.chunk_first[ty + 1];
+  for (int t = threadIdx.x; t < X; t += 256) {
+    int run = 0;
+    int32_t* h = a.hist + (int64_t)c0 * X + t;
+    for (int c = c0; c < c1; ++c, h += X) {
+      const int v = *h;
+      *h = run;
+      run += v;
+    }
+    tot_s[t] = run;
+  }
+  __syncthreads();
+  // exclusive scan of tot_s[0..X) with 256 threads, kPer columns each
+  constexpr int kPer = kBinMaxCols / 256;
+  int loc = 0;
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    const int t = threadIdx.x * kPer + k;
+    loc += t < X ? tot_s[t] : 0;
+  }
+  int excl;
+  block_exclusive_scan(loc, &excl, scan_tot);
+  int base = row_start(a, ty, p) + excl;
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    const int t = threadIdx.x * kPer + k;
+    if (t < X) {
+      a.tile_starts[ty * X + t] = base;
+      base += tot_s[t];
+    }
+  }
+  if (ty == a.tiles_y - 1 && threadIdx.x == 0) a.tile_starts[a.tiles_y * X] = p;
+}
+
+// Column pass 3: per chunk, every pair to tile_starts[tile] + the chunk's
+// prefix for its column + its rank among the chunk's earlier pairs of that
+// column (warp sub-ranges in order, match_any within a warp): a stable
+// counting sort, so each tile list keeps generation (depth rank) order and
+// equals np.lexsort((index, depth, tile)) (rasterizer.py:318-323).
+constexpr int kScatterItems = kBinChunk / 256;  // 16 pairs per lane
+__global__ void __launch_bounds__(256) tile_scatter_kernel(RowBinArgs a) {
+  extern __shared__ int wcnt[];  // [8][tiles_x]
+  long long p64;
+  if (bin_overflowed(a, &p64)) return;
+  int ty, begin, end;
+  if (!chunk_of(a, (int)p64, blockIdx.x, &ty, &begin, &end)) return;
+  const int X = a.tiles_x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  const int sub = begin + w * (kBinChunk / 8);
+  int tx[kScatterItems];
+  uint32_t val[kScatterItems];
+#pragma unroll
+  for (int k = 0; k < kScatterItems; ++k) {
+    const int idx = sub + k * 32 + lane;
+    const bool in = idx < end;
+    tx[k] = in ? (int)a.tx_row[idx] : -1;
+    val[k] = in ? a.val_row[idx] : 0u;
+  }
+  for (int e = threadIdx.x; e < 8 * X; e += 256) wcnt[e] = 0;
+  __syncthreads();
+  int* cur = wcnt + w * X;
+#pragma unroll
+  for (int k = 0; k < kScatterItems; ++k) {
+    const unsigned peers = __match_any_sync(0xffffffffu, tx[k]);
+    if (tx[k] >= 0 && lane == __ffs(peers) - 1) cur[tx[k]] += __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  const int32_t* hrow = a.hist + (int64_t)blockIdx.x * X;
+  const int32_t* ts = a.tile_starts + ty * X;
+  for (int t = threadIdx.x; t < X; t += 256) {
+    int base = ts[t] + hrow[t];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int v = wcnt[q * X + t];
+      wcnt[q * X + t] = base;
+      base += v;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kScatterItems; ++k) {
+    const unsigned peers = __match_any_sync(0xffffffffu, tx[k]);
+    const bool live = tx[k] >= 0;
+    const int pos = live ? cur[tx[k]] + __popc(peers & lt) : 0;
+    __syncwarp();
+    if (live && lane == __ffs(peers) - 1) cur[tx[k]] += __popc(peers);
+    __syncwarp();
+    if (live) a.pair_src[pos] = val[k];
+  }
+}
+
+cudaError_t run_row_binning(const RowBinArgs& a, cudaStream_t stream) {
+  const unsigned chunks = (unsigned)bin_chunk_capacity(a.capacity, a.tiles_y);
+  // the attribute is set once per device: set it for the largest image the path takes
+  cudaError_t e = set_dynamic_smem<row_emit_kernel>(8 * kBinMaxRows * (int)sizeof(int));
+  if (e != cudaSuccess) return e;
+  e = set_dynamic_smem<tile_scatter_kernel>(8 * kBinMaxCols * (int)sizeof(int));
+  if (e != cudaSuccess) return e;
+  row_emit_kernel<<<(unsigned)a.nb, kBinRanks, 8 * a.tiles_y * sizeof(int), stream>>>(a);
+  tile_hist_kernel<<<chunks, 256, a.tiles_x * sizeof(int), stream>>>(a);
+  tile_scan_kernel<<<(unsigned)a.tiles_y, 256, 0, stream>>>(a);
+  tile_scatter_kernel<<<chunks, 256, 8 * a.tiles_x * sizeof(int), stream>>>(a);
+  note_launch(4);
+  return cudaGetLastError();
 }
 
 // K2: one thread per depth rank; a splat's pairs are contiguous, row-major over

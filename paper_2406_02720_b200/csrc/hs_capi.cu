@@ -46,8 +46,10 @@ struct Carver {
   }
 };
 
-// counters[]: 0 K5 tile queue, 32 K6 tile queue, 48 depth-fixup overflow flag
+// counters[]: 0 K5 tile queue, 32 K6 tile queue, 48 depth-fixup overflow flag,
+// 52-55 the binning status (BinStatusDev: P as int64, flags)
 constexpr int kDepthOverflowSlot = 48;
+constexpr int kBinStatusSlot = 52;
 
 struct FrameBufs {
   float4* rec;
@@ -67,6 +69,8 @@ struct FrameBufs {
   int32_t* xflags;
   int32_t* xlocal;
   float4* merged;
+  int32_t* chunk_first;
+  BinStatusDev* status;
   void* temp;
   size_t temp_bytes;
 };
@@ -85,13 +89,15 @@ static std::mutex g_size_mu;
 static std::map<int64_t, size_t> g_frame_temp;
 static std::map<std::pair<int64_t, int>, size_t> g_pair_temp;
 
-static size_t frame_temp_bytes(int64_t n) {
-  const int64_t b = pow2_bucket(n);
+static size_t frame_temp_bytes(int64_t n, int64_t scan_len) {
+  const int64_t b = pow2_bucket(n), bs = pow2_bucket(scan_len);
   std::lock_guard<std::mutex> lock(g_size_mu);
-  auto it = g_frame_temp.find(b);
+  const int64_t key = b * 4096 + (bs / 1024 > 4095 ? 4095 : bs / 1024);
+  auto it = g_frame_temp.find(key);
   if (it != g_frame_temp.end()) return it->second;
-  const size_t x = depth_sort_temp_bytes(b), y = scan_temp_bytes(b);
-  return g_frame_temp[b] = x > y ? x : y;
+  const size_t x = depth_sort_temp_bytes(b), y = scan_temp_bytes(bs), z = scan_temp_bytes(b + 1);
+  size_t m = x > y ? x : y;
+  return g_frame_temp[key] = m > z ? m : z;
 }
 
 static size_t pair_temp_bytes(int64_t p, int tile_bits) {
@@ -102,9 +108,12 @@ static size_t pair_temp_bytes(int64_t p, int tile_bits) {
   return g_pair_temp[key] = pair_sort_temp_bytes(key.first, tile_bits);
 }
 
-static FrameBufs carve_frame(void* ws, int64_t n, int n_tiles, size_t* total) {
+static FrameBufs carve_frame(void* ws, int64_t n, int tiles_x, int tiles_y, size_t* total) {
   Carver c(ws);
   FrameBufs f;
+  const int n_tiles = tiles_x * tiles_y;
+  const bool rows = row_binning_ok(tiles_x, tiles_y);
+  const int64_t scan_len = count_scan_len(n, tiles_y, rows);
   f.rec = c.take<float4>(4 * (size_t)n);
   f.side = c.take<SteepRec>(n);
   f.rect = c.take<int4>(n);
@@ -113,8 +122,8 @@ static FrameBufs carve_frame(void* ws, int64_t n, int n_tiles, size_t* total) {
   f.dkey_out = c.take<uint64_t>(n);
   f.dval = c.take<uint32_t>(n);
   f.order = c.take<uint32_t>(n);
-  f.cnt_r = c.take<int32_t>(n + 1);
-  f.off_r = c.take<int32_t>(n + 1);
+  f.cnt_r = c.take<int32_t>(scan_len);
+  f.off_r = c.take<int32_t>(scan_len);
   f.rank_of = c.take<uint32_t>(n);
   f.tile_starts = c.take<int32_t>(n_tiles + 1);
   f.last_rank = c.take<int32_t>(n_tiles);
@@ -122,33 +131,64 @@ static FrameBufs carve_frame(void* ws, int64_t n, int n_tiles, size_t* total) {
   f.xflags = c.take<int32_t>(n + 1);
   f.xlocal = c.take<int32_t>(n + 1);
   f.merged = c.take<float4>(4 * (size_t)n);
-  f.temp_bytes = frame_temp_bytes(n);
+  f.chunk_first = c.take<int32_t>(tiles_y + 1);
+  f.status = reinterpret_cast<BinStatusDev*>(f.counters ? f.counters + kBinStatusSlot : nullptr);
+  f.temp_bytes = frame_temp_bytes(n, scan_len);
   f.temp = c.take<char>(f.temp_bytes);
   if (total) *total = c.off;
   return f;
 }
 
+// The binning workspace for a pair capacity p.  Row-bucket path: the row buckets
+// (tile column u16 + value), the final pair order, the column histograms and K6's
+// pair rows; CUB path (very large images): keys/values double buffers + temp.
 struct BinBufs {
   uint32_t* keys[2];
   uint32_t* vals[2];
+  uint16_t* tx_row;
+  uint32_t* val_row;
+  uint32_t* pair_src;
+  int32_t* hist;
   float* rows;
   void* temp;
   size_t temp_bytes;
 };
 
-static BinBufs carve_bin(void* ws, int64_t p, int tile_bits, size_t* total) {
+static BinBufs carve_bin(void* ws, int64_t p, int tiles_x, int tiles_y, size_t* total) {
   Carver c(ws);
-  BinBufs b;
+  BinBufs b{};
   const size_t pp = p > 0 ? (size_t)p : 1;
-  b.keys[0] = c.take<uint32_t>(pp);
-  b.keys[1] = c.take<uint32_t>(pp);
-  b.vals[0] = c.take<uint32_t>(pp);
-  b.vals[1] = c.take<uint32_t>(pp);
+  if (row_binning_ok(tiles_x, tiles_y)) {
+    b.tx_row = c.take<uint16_t>(pp);
+    b.val_row = c.take<uint32_t>(pp);
+    b.pair_src = c.take<uint32_t>(pp);
+    b.hist = c.take<int32_t>((size_t)bin_chunk_capacity(p, tiles_y) * tiles_x);
+  } else {
+    int bits = 0;
+    while ((1ll << bits) < (long long)tiles_x * tiles_y) ++bits;
+    b.keys[0] = c.take<uint32_t>(pp);
+    b.keys[1] = c.take<uint32_t>(pp);
+    b.vals[0] = c.take<uint32_t>(pp);
+    b.vals[1] = c.take<uint32_t>(pp);
+    b.temp_bytes = pair_temp_bytes(p, bits);
+    b.temp = c.take<char>(b.temp_bytes);
+  }
   b.rows = c.take<float>(pp * kRowFloats);
-  b.temp_bytes = pair_temp_bytes(p, tile_bits);
-  b.temp = c.take<char>(b.temp_bytes);
   if (total) *total = c.off;
   return b;
+}
+
+// pair capacity the binning workspace is laid out for
+static int64_t bin_capacity(const hs_frame* f) {
+  return f->pair_capacity > 0 ? f->pair_capacity : (f->num_pairs > 0 ? f->num_pairs : 0);
+}
+
+static BinBufs frame_bin(const hs_frame* f) {
+  return carve_bin(f->bin_ws, bin_capacity(f), f->tiles_x, f->tiles_y, nullptr);
+}
+
+static FrameBufs frame_bufs(const hs_frame* f) {
+  return carve_frame(f->frame_ws, f->n, f->tiles_x, f->tiles_y, nullptr);
 }
 
 static int tiles_of(int32_t px) { return (px + kTile - 1) / kTile; }
@@ -226,7 +266,7 @@ static int check_frame_ws(const hs_frame* f) {
 
 static int check_bin_ws(const hs_frame* f) {
   if (!f->bin_ws) return HS_ERR_WORKSPACE;
-  if (f->bin_ws_bytes < hs_binning_workspace_size(f->n, f->num_pairs, f->width, f->height))
+  if (f->bin_ws_bytes < hs_binning_workspace_size(f->n, bin_capacity(f), f->width, f->height))
     return HS_ERR_WORKSPACE;
   return HS_OK;
 }
@@ -247,7 +287,7 @@ using namespace hs;
 
 extern "C" {
 
-int32_t hs_abi_version(void) { return 1; }
+int32_t hs_abi_version(void) { return 2; }
 
 int64_t hs_kernel_launch_count(void) { return g_launches.load(); }
 
@@ -294,15 +334,21 @@ int hs_frame_init(hs_frame* frame, int64_t n, int32_t width, int32_t height, int
 
 size_t hs_frame_workspace_size(int64_t n, int32_t width, int32_t height) {
   size_t total = 0;
-  carve_frame(nullptr, n, tiles_of(width) * tiles_of(height), &total);
+  carve_frame(nullptr, n, tiles_of(width), tiles_of(height), &total);
   return total;
 }
 
 size_t hs_binning_workspace_size(int64_t n, int64_t num_pairs, int32_t width, int32_t height) {
   (void)n;
   size_t total = 0;
-  carve_bin(nullptr, num_pairs, bits_for(tiles_of(width) * tiles_of(height)), &total);
+  carve_bin(nullptr, num_pairs, tiles_of(width), tiles_of(height), &total);
   return total;
+}
+
+static cudaError_t count_scan(const hs_frame* frame, const FrameBufs& f, cudaStream_t stream) {
+  const bool rows = row_binning_ok(frame->tiles_x, frame->tiles_y);
+  return run_count_scan(f.temp, f.temp_bytes, f.count, f.order, f.rect, f.cnt_r, f.off_r,
+                        f.rank_of, frame->n, rows ? frame->tiles_y : 0, f.status, stream);
 }
 
 int hs_preprocess_fwd(hs_frame* frame, const hs_scene* scene, const hs_camera* cam,
@@ -312,7 +358,7 @@ int hs_preprocess_fwd(hs_frame* frame, const hs_scene* scene, const hs_camera* c
   if ((st = check_scene(scene, frame))) return st;
   if (!cam || cam->width != frame->width || cam->height != frame->height) return HS_ERR_INVALID_ARG;
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
-  FrameBufs f = carve_frame(frame->frame_ws, frame->n, frame->n_tiles, nullptr);
+  FrameBufs f = frame_bufs(frame);
   const CamArgs ca = cam_args(cam);
   if (scene->dtype == HS_DTYPE_F32) {
     HS_CUDA(launch_preprocess_fwd_t<float>(scene_args<float>(scene), ca, frame->kernel, frame->n,
@@ -323,13 +369,32 @@ int hs_preprocess_fwd(hs_frame* frame, const hs_scene* scene, const hs_camera* c
                                             frame->n, f.rec, f.side, f.rect, f.count, f.dkey_in,
                                             f.dval, radii, stream));
   }
-  // rank_of and cnt_r are outputs of the count scan below: free as fixup scratch here
-  HS_CUDA(run_depth_sort_hi(f.temp, f.temp_bytes, f.dkey_in, f.dkey_out, f.dval, f.order,
-                            frame->n, f.rank_of, reinterpret_cast<uint32_t*>(f.cnt_r),
-                            f.counters + kDepthOverflowSlot, stream));
-  HS_CUDA(run_count_scan(f.temp, f.temp_bytes, f.count, f.order, f.cnt_r, f.off_r, f.rank_of,
-                         frame->n, stream));
+  if (frame->depth_sort_full) {
+    HS_CUDA(cudaMemsetAsync(f.counters + kDepthOverflowSlot, 0, sizeof(int), stream));
+    HS_CUDA(run_depth_sort(f.temp, f.temp_bytes, f.dkey_in, f.dkey_out, f.dval, f.order,
+                           frame->n, stream));
+  } else {
+    // rank_of and cnt_r are outputs of the count scan below: free as fixup scratch here
+    HS_CUDA(run_depth_sort_hi(f.temp, f.temp_bytes, f.dkey_in, f.dkey_out, f.dval, f.order,
+                              frame->n, f.rank_of, reinterpret_cast<uint32_t*>(f.cnt_r),
+                              f.counters + kDepthOverflowSlot, stream));
+  }
+  HS_CUDA(count_scan(frame, f, stream));
   frame->num_pairs = -1;
+  return HS_OK;
+}
+
+// P (int64, it cannot wrap) and the flags, with a host synchronisation.
+static int read_status(hs_frame* frame, const FrameBufs& f, int64_t* p, int32_t* flags,
+                       cudaStream_t stream) {
+  BinStatusDev bs;
+  int depth = 0;
+  HS_CUDA(cudaMemcpyAsync(&bs, f.status, sizeof(bs), cudaMemcpyDeviceToHost, stream));
+  HS_CUDA(cudaMemcpyAsync(&depth, f.counters + kDepthOverflowSlot, sizeof(int),
+                          cudaMemcpyDeviceToHost, stream));
+  HS_CUDA(cudaStreamSynchronize(stream));
+  *p = bs.pairs;
+  *flags = bs.flags | (depth ? kBinFlagDepth : 0);
   return HS_OK;
 }
 
@@ -337,44 +402,92 @@ int hs_frame_read_num_pairs(hs_frame* frame, void* stream_) {
   int st = check_frame_ws(frame);
   if (st) return st;
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
-  FrameBufs f = carve_frame(frame->frame_ws, frame->n, frame->n_tiles, nullptr);
-  int32_t p = 0;
-  int overflow = 0;
-  HS_CUDA(cudaMemcpyAsync(&p, f.off_r + frame->n, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
-  HS_CUDA(cudaMemcpyAsync(&overflow, f.counters + kDepthOverflowSlot, sizeof(int),
-                          cudaMemcpyDeviceToHost, stream));
-  HS_CUDA(cudaStreamSynchronize(stream));
-  if (p < 0) return HS_ERR_INVALID_ARG;  // overflowed int32
-  if (overflow) {
+  FrameBufs f = frame_bufs(frame);
+  int64_t p = 0;
+  int32_t flags = 0;
+  if ((st = read_status(frame, f, &p, &flags, stream))) return st;
+  if (p > 0x7fffffffll) return HS_ERR_INVALID_ARG;  // more pairs than int32 offsets hold
+  if (flags & kBinFlagDepth) {
     // a depth bucket held more than the fixup handles (e.g. thousands of equal
     // depths): redo the ranks with the full 64-bit sort; P is order-independent
+    HS_CUDA(cudaMemsetAsync(f.counters + kDepthOverflowSlot, 0, sizeof(int), stream));
     HS_CUDA(run_depth_sort(f.temp, f.temp_bytes, f.dkey_in, f.dkey_out, f.dval, f.order,
                            frame->n, stream));
-    HS_CUDA(run_count_scan(f.temp, f.temp_bytes, f.count, f.order, f.cnt_r, f.off_r, f.rank_of,
-                           frame->n, stream));
+    HS_CUDA(count_scan(frame, f, stream));
+    frame->depth_sort_full = 1;
   }
   frame->num_pairs = p;
+  return HS_OK;
+}
+
+int hs_frame_status(hs_frame* frame, int64_t* num_pairs, int32_t* flags, void* stream_) {
+  int st = check_frame_ws(frame);
+  if (st) return st;
+  if (!num_pairs || !flags) return HS_ERR_INVALID_ARG;
+  FrameBufs f = frame_bufs(frame);
+  if ((st = read_status(frame, f, num_pairs, flags, static_cast<cudaStream_t>(stream_))))
+    return st;
+  if (!*flags) frame->num_pairs = *num_pairs;
+  return HS_OK;
+}
+
+int hs_frame_status_async(const hs_frame* frame, void* host_status, void* stream_) {
+  int st = check_frame_ws(frame);
+  if (st) return st;
+  if (!host_status) return HS_ERR_INVALID_ARG;
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  FrameBufs f = frame_bufs(frame);
+  char* h = static_cast<char*>(host_status);
+  HS_CUDA(cudaMemcpyAsync(h, f.status, sizeof(BinStatusDev), cudaMemcpyDeviceToHost, stream));
+  HS_CUDA(cudaMemcpyAsync(h + sizeof(BinStatusDev), f.counters + kDepthOverflowSlot, sizeof(int),
+                          cudaMemcpyDeviceToHost, stream));
   return HS_OK;
 }
 
 int hs_read_pairs_and_bin(hs_frame* frame, void* stream_) {
   int st = hs_frame_read_num_pairs(frame, stream_);
   if (st) return st;
+  const int64_t cap = frame->pair_capacity > frame->num_pairs ? frame->pair_capacity
+                                                              : frame->num_pairs;
   if (!frame->bin_ws ||
-      frame->bin_ws_bytes <
-          hs_binning_workspace_size(frame->n, frame->num_pairs, frame->width, frame->height))
+      frame->bin_ws_bytes < hs_binning_workspace_size(frame->n, cap, frame->width, frame->height))
     return HS_ERR_WORKSPACE;  // P is set: size the workspace, then hs_bin_and_sort
   return hs_bin_and_sort(frame, stream_);
+}
+
+static int row_bin(hs_frame* frame, const FrameBufs& f, const BinBufs& b, cudaStream_t stream) {
+  RowBinArgs a;
+  a.order = f.order;
+  a.rect = f.rect;
+  a.rec = f.rec;
+  a.cnt_r = f.cnt_r;
+  a.off_r = f.off_r;
+  a.status = f.status;
+  a.n = frame->n;
+  a.nb = (int)bin_row_blocks(frame->n);
+  a.tiles_x = frame->tiles_x;
+  a.tiles_y = frame->tiles_y;
+  a.capacity = bin_capacity(frame);
+  a.tx_row = b.tx_row;
+  a.val_row = b.val_row;
+  a.chunk_first = f.chunk_first;
+  a.hist = b.hist;
+  a.tile_starts = f.tile_starts;
+  a.pair_src = b.pair_src;
+  HS_CUDA(run_row_binning(a, stream));
+  return HS_OK;
 }
 
 int hs_bin_and_sort(hs_frame* frame, void* stream_) {
   int st = check_frame_ws(frame);
   if (st) return st;
   if (frame->num_pairs < 0) return HS_ERR_INVALID_ARG;
+  if (frame->pair_capacity < frame->num_pairs) frame->pair_capacity = frame->num_pairs;
   if ((st = check_bin_ws(frame))) return st;
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
-  FrameBufs f = carve_frame(frame->frame_ws, frame->n, frame->n_tiles, nullptr);
-  BinBufs b = carve_bin(frame->bin_ws, frame->num_pairs, frame->tile_bits, nullptr);
+  FrameBufs f = frame_bufs(frame);
+  BinBufs b = frame_bin(frame);
+  if (row_binning_ok(frame->tiles_x, frame->tiles_y)) return row_bin(frame, f, b, stream);
   const int64_t p = frame->num_pairs;
   int sel = 0;
   if (p > 0) {
@@ -388,10 +501,35 @@ int hs_bin_and_sort(hs_frame* frame, void* stream_) {
   return HS_OK;
 }
 
+int hs_bin_async(hs_frame* frame, void* stream_) {
+  int st = check_frame_ws(frame);
+  if (st) return st;
+  if (!row_binning_ok(frame->tiles_x, frame->tiles_y)) {
+    // the CUB path sizes its passes from P: read it (a host sync), then bin
+    if ((st = hs_frame_read_num_pairs(frame, stream_))) return st;
+    if (frame->pair_capacity < frame->num_pairs) return HS_ERR_WORKSPACE;
+    return hs_bin_and_sort(frame, stream_);
+  }
+  if (frame->pair_capacity <= 0) return HS_ERR_INVALID_ARG;
+  if ((st = check_bin_ws(frame))) return st;
+  frame->num_pairs = -1;  // on the device until hs_frame_status
+  return row_bin(frame, frame_bufs(frame), frame_bin(frame), static_cast<cudaStream_t>(stream_));
+}
+
+static const uint32_t* sorted_pairs(const hs_frame* frame, const BinBufs& b) {
+  return row_binning_ok(frame->tiles_x, frame->tiles_y) ? b.pair_src
+                                                        : b.vals[frame->sort_selector];
+}
+
+// P for launch heuristics (K7a's lanes per splat): exact once read, else the capacity
+static int64_t pairs_hint(const hs_frame* frame) {
+  return frame->num_pairs >= 0 ? frame->num_pairs : bin_capacity(frame) * 4 / 5;
+}
+
 static BlendGeom frame_geom(const hs_frame* frame, const FrameBufs& f, const BinBufs& b) {
   BlendGeom g;
   g.tile_starts = f.tile_starts;
-  g.pair_src = b.vals[frame->sort_selector];
+  g.pair_src = sorted_pairs(frame, b);
   g.rec = f.rec;
   g.side = f.side;
   g.width = frame->width;
@@ -410,8 +548,8 @@ int hs_blend_fwd(hs_frame* frame, const double* bg, float* color, float* alpha, 
   if (st) return st;
   if ((st = check_bin_ws(frame))) return st;
   if (!bg || !color || !alpha || !depth || !transmittance || !terminal) return HS_ERR_INVALID_ARG;
-  FrameBufs f = carve_frame(frame->frame_ws, frame->n, frame->n_tiles, nullptr);
-  BinBufs b = carve_bin(frame->bin_ws, frame->num_pairs, frame->tile_bits, nullptr);
+  FrameBufs f = frame_bufs(frame);
+  BinBufs b = frame_bin(frame);
   BlendGeom g = frame_geom(frame, f, b);
   HS_CUDA(launch_blend_fwd(g, (float)bg[0], (float)bg[1], (float)bg[2], color, alpha, depth,
                            transmittance, terminal, static_cast<cudaStream_t>(stream_)));
@@ -424,8 +562,8 @@ int hs_blend_bwd(hs_frame* frame, const double* bg, const float* d_color,
   if (st) return st;
   if ((st = check_bin_ws(frame))) return st;
   if (!bg || !d_color || !transmittance || !terminal) return HS_ERR_INVALID_ARG;
-  FrameBufs f = carve_frame(frame->frame_ws, frame->n, frame->n_tiles, nullptr);
-  BinBufs b = carve_bin(frame->bin_ws, frame->num_pairs, frame->tile_bits, nullptr);
+  FrameBufs f = frame_bufs(frame);
+  BinBufs b = frame_bin(frame);
   BlendGeom g = frame_geom(frame, f, b);
   g.work_counter = f.counters + 32;
   HS_CUDA(launch_blend_bwd(g, (float)bg[0], (float)bg[1], (float)bg[2], d_color, transmittance,
@@ -439,8 +577,8 @@ int hs_blend_window_stats(hs_frame* frame, unsigned long long* hist, void* strea
   if (st) return st;
   if ((st = check_bin_ws(frame))) return st;
   if (!hist) return HS_ERR_INVALID_ARG;
-  FrameBufs f = carve_frame(frame->frame_ws, frame->n, frame->n_tiles, nullptr);
-  BinBufs b = carve_bin(frame->bin_ws, frame->num_pairs, frame->tile_bits, nullptr);
+  FrameBufs f = frame_bufs(frame);
+  BinBufs b = frame_bin(frame);
   BlendGeom g = frame_geom(frame, f, b);
   HS_CUDA(launch_window_stats(g, hist, static_cast<cudaStream_t>(stream_)));
   return HS_OK;
@@ -463,19 +601,19 @@ int hs_preprocess_bwd_range(hs_frame* frame, const hs_scene* scene, const hs_cam
       grads->accumulate > 3 || begin < 0 || begin % 128 != 0 || end < begin)
     return HS_ERR_INVALID_ARG;
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
-  FrameBufs f = carve_frame(frame->frame_ws, frame->n, frame->n_tiles, nullptr);
-  BinBufs b = carve_bin(frame->bin_ws, frame->num_pairs, frame->tile_bits, nullptr);
+  FrameBufs f = frame_bufs(frame);
+  BinBufs b = frame_bin(frame);
   const CamArgs ca = cam_args(cam);
   if (scene->dtype == HS_DTYPE_F32) {
     HS_CUDA(launch_preprocess_bwd_t<float>(scene_args<float>(scene), ca, frame->kernel, frame->n,
                                            frame->tiles_x, f.rec, f.rect, f.count, f.rank_of,
-                                           f.last_rank, b.rows, f.merged, frame->num_pairs,
+                                           f.last_rank, b.rows, f.merged, pairs_hint(frame),
                                            ranged(grad_args<float>(grads), begin, end), stream));
   } else {
     HS_CUDA(launch_preprocess_bwd_t<double>(scene_args<double>(scene), ca, frame->kernel,
                                             frame->n, frame->tiles_x, f.rec, f.rect, f.count,
                                             f.rank_of, f.last_rank, b.rows, f.merged,
-                                            frame->num_pairs,
+                                            pairs_hint(frame),
                                             ranged(grad_args<double>(grads), begin, end),
                                             stream));
   }
@@ -490,11 +628,11 @@ int hs_frame_export(const hs_frame* frame, int32_t* valid, int64_t* m_out, float
   if (!m_out) return HS_ERR_INVALID_ARG;
   const bool binned = frame->bin_ws && frame->num_pairs >= 0;
   if ((pair_splat || tile_starts) && !binned) return HS_ERR_INVALID_ARG;
-  FrameBufs f = carve_frame(frame->frame_ws, frame->n, frame->n_tiles, nullptr);
+  FrameBufs f = frame_bufs(frame);
   const uint32_t* pair_src = nullptr;
   if (binned) {
-    BinBufs b = carve_bin(frame->bin_ws, frame->num_pairs, frame->tile_bits, nullptr);
-    pair_src = b.vals[frame->sort_selector];
+    BinBufs b = frame_bin(frame);
+    pair_src = sorted_pairs(frame, b);
   }
   HS_CUDA(run_export(f.temp, f.temp_bytes, f.count, f.rec, f.rect, pair_src, f.tile_starts,
                      frame->n, binned ? frame->num_pairs : 0, frame->n_tiles, f.xlocal, f.xflags,

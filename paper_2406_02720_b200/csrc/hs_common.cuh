@@ -3,23 +3,29 @@
 #pragma once
 
 #include <atomic>
+#include <mutex>
 #include <cstdint>
 #include <cuda_runtime.h>
 
 namespace hs {
 
-// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel and device
-// (a bit per device; the attribute is per-device state).
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) per kernel and device, raised
+// whenever a launch needs more than was set before (the attribute is per-device
+// state and a launch above it fails; never lowered, so concurrent callers with
+// different sizes stay valid).
 template <auto Kernel>
 inline cudaError_t set_dynamic_smem(int bytes) {
-  static std::atomic<uint64_t> done{0};
+  static std::mutex mu;
+  static int set_bytes[64] = {};
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
-  const uint64_t bit = dev < 64 ? (1ull << dev) : 0ull;
-  if (bit && (done.load(std::memory_order_acquire) & bit)) return cudaSuccess;
+  if (dev < 0 || dev >= 64)
+    return cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  std::lock_guard<std::mutex> lock(mu);
+  if (set_bytes[dev] >= bytes && set_bytes[dev] > 0) return cudaSuccess;
   e = cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  if (e == cudaSuccess && bit) done.fetch_or(bit, std::memory_order_acq_rel);
+  if (e == cudaSuccess) set_bytes[dev] = bytes;
   return e;
 }
 

@@ -107,10 +107,64 @@ cudaError_t run_depth_sort_hi(void* temp, size_t temp_bytes, const uint64_t* key
                               uint64_t* keys_out, const uint32_t* vals_in, uint32_t* order,
                               int64_t n, uint32_t* scratch_pos, uint32_t* scratch_val,
                               int* overflow, cudaStream_t stream);
-// cnt_r[r] = count[order[r]], off_r = exclusive scan (n+1 entries), rank_of[order[r]] = r
+// ---- tile binning without a host round trip -------------------
+// The count pass also histograms every block of kBinRanks depth ranks' pairs by
+// tile row; the emit pass writes each pair straight into its row bucket (rank
+// order within the row, so stable); the column passes counting-sort every row
+// bucket by tile column in chunks of kBinChunk pairs.  P stays on the device: the
+// caller sizes the binning workspace for a pair capacity, and a frame whose P
+// exceeds it is flagged (kBinFlagOverflow) with every tile list left empty.
+constexpr int kBinRanks = 256;
+constexpr int kBinMaxRows = 1024;  // tiles_y limit of the row-bucket path
+constexpr int kBinMaxCols = 2048;  // tiles_x limit (larger images: CUB pair sort)
+constexpr int kBinChunk = 4096;    // 256 threads x 16 pairs
+constexpr int kBinFlagOverflow = 1;
+constexpr int kBinFlagDepth = 2;   // the depth-run fixup overflowed: ranks need the full sort
+inline bool row_binning_ok(int tiles_x, int tiles_y) {
+  return tiles_x <= kBinMaxCols && tiles_y <= kBinMaxRows;
+}
+inline int64_t bin_row_blocks(int64_t n) { return (n + kBinRanks - 1) / kBinRanks; }
+inline int64_t bin_chunk_capacity(int64_t capacity, int tiles_y) {
+  return capacity / kBinChunk + tiles_y + 1;
+}
+// scan entries of the count pass: pair counts by rank (n + 1), then, with the row
+// path, the row histograms [tiles_y][row blocks]
+inline int64_t count_scan_len(int64_t n, int tiles_y, bool rows) {
+  return n + 1 + (rows ? (int64_t)tiles_y * bin_row_blocks(n) : 0);
+}
+struct BinStatusDev {   // in the frame's counters
+  long long pairs;      // P as int64 (the int32 scan may wrap)
+  int flags;
+  int pad;
+};
+
+// cnt_r[r] = count[order[r]], off_r = exclusive scan (count_scan_len entries),
+// rank_of[order[r]] = r; with tiles_y > 0 also the row histograms and P as int64
+// in *status (zeroed here).
 cudaError_t run_count_scan(void* temp, size_t temp_bytes, const int32_t* count,
-                           const uint32_t* order, int32_t* cnt_r, int32_t* off_r,
-                           uint32_t* rank_of, int64_t n, cudaStream_t stream);
+                           const uint32_t* order, const int4* rect, int32_t* cnt_r,
+                           int32_t* off_r, uint32_t* rank_of, int64_t n, int tiles_y,
+                           BinStatusDev* status, cudaStream_t stream);
+struct RowBinArgs {
+  const uint32_t* order;
+  const int4* rect;
+  float4* rec;
+  const int32_t* cnt_r;
+  const int32_t* off_r;
+  BinStatusDev* status;
+  int64_t n;
+  int nb;  // row blocks
+  int tiles_x, tiles_y;
+  int64_t capacity;
+  uint16_t* tx_row;      // [capacity] row buckets: tile column
+  uint32_t* val_row;     // [capacity] row buckets: index | steep
+  int32_t* chunk_first;  // [tiles_y + 1]
+  int32_t* hist;         // [chunk capacity][tiles_x]
+  int32_t* tile_starts;  // [n_tiles + 1]
+  uint32_t* pair_src;    // [capacity] final order
+};
+// emit + column passes (4 launches); no host synchronisation
+cudaError_t run_row_binning(const RowBinArgs& a, cudaStream_t stream);
 cudaError_t run_duplicate(const uint32_t* order, const int32_t* cnt_r, const int32_t* off_r,
                           const int4* rect, float4* rec, int tiles_x, uint32_t* keys,
                           uint32_t* vals, int64_t n, cudaStream_t stream);

@@ -21,7 +21,7 @@ import numpy as np
 import torch
 
 from . import _native
-from .errors import EmptyScene, ImageTooLarge, MismatchedForward
+from .errors import EmptyScene, ImageTooLarge, MismatchedForward, WorkspaceError
 from .geometry import CameraModel, Scene
 
 MAX_PIXELS = 2**31  # rasterizer.py:40
@@ -76,6 +76,40 @@ class Workspace:
     def __init__(self, device="cuda"):
         self.device = torch.device(device)
         self._bufs = {}
+        # asynchronous binning (hs_bin_async): the pair capacity the binning
+        # workspace is laid out for, the last P read back, and the status copy of
+        # the frame binned last (checked by the next prepare into this workspace)
+        self.pair_capacity = 0
+        self.last_pairs = -1
+        self.pending = None
+        self.generation = 0
+        self._status_host = None
+        self.depth_sort_full = 0  # sticky once a view needed the full depth sort
+
+    def status_buffer(self):
+        """Pinned host memory for hs_frame_status_async (3 int64 words)."""
+        if self._status_host is None:
+            self._status_host = torch.zeros(3, dtype=torch.int64, pin_memory=True)
+        return self._status_host
+
+    def check_previous(self):
+        """Status of the frame this workspace binned asynchronously last: waits
+        for that frame's binning (the GPU is normally still busy with its blends,
+        so this does not idle it) and raises BinningOverflow if its P exceeded the
+        capacity -- its outputs were then empty.  The capacity grows either way
+        when P comes near it."""
+        pend, self.pending = self.pending, None
+        if pend is None:
+            return
+        event, host, frame = pend
+        event.synchronize()
+        p, flags, depth = int(host[0]), int(host[1]) & 0xffffffff, int(host[2]) & 0xffffffff
+        frame._status_seen(p, flags, depth)
+        if flags or depth:
+            raise BinningOverflow(
+                f"an asynchronously binned view had P={p} pairs for a capacity of "
+                f"{frame.capacity} (flags {flags}, depth fallback {depth}); its outputs were "
+                "incomplete -- the capacity has grown, re-run that view")
 
     def tensor(self, name, shape, dtype):
         t = self._bufs.get(name)
@@ -87,6 +121,17 @@ class Workspace:
 
     def bytes(self, name, nbytes):
         return self.tensor(name, (nbytes,), torch.uint8)
+
+
+class BinningOverflow(RuntimeError):
+    """An asynchronously binned view needed more pair capacity than its workspace
+    had (see Workspace.check_previous)."""
+
+
+# Capacity headroom of a binning workspace: P * 5/4 + 64K pairs, grown again once a
+# view's P passes 90% of it.
+def _capacity_for(p):
+    return int(p) * 5 // 4 + 65536
 
 
 class DeviceFrame:
@@ -114,6 +159,12 @@ class DeviceFrame:
         self.st.frame_ws_bytes = nbytes
         self.bin_ws = None
         self.device = dev
+        self.pending = False   # binned asynchronously, P not read back yet
+        self.capacity = 0
+        if ws is not None:
+            ws.generation += 1
+            self.generation = ws.generation
+            self.st.depth_sort_full = ws.depth_sort_full
 
     @property
     def n_total(self):
@@ -121,7 +172,52 @@ class DeviceFrame:
 
     @property
     def num_pairs(self):
+        self.resolve()
+        if self.st.num_pairs < 0 and self.stale():
+            raise WorkspaceError("this frame's workspace was reused by a later view")
         return int(self.st.num_pairs)
+
+    def _status_seen(self, p, flags, depth):
+        if self.ws is not None and depth:
+            self.ws.depth_sort_full = 1
+        if self.ws is not None:
+            self.ws.last_pairs = max(self.ws.last_pairs, p) if flags or depth else p
+            if p > 0.9 * self.ws.pair_capacity:
+                self.ws.pair_capacity = 0  # re-lay the workspace out at the next prepare
+                self.ws.last_pairs = p
+
+    def resolve(self):
+        """For an asynchronously binned frame: read P and the status (a host sync);
+        if the frame overflowed its capacity (or its depth ranks needed the full
+        sort) grow the workspace and bin it again synchronously.  Returns True when
+        it re-binned, i.e. any blend already run on this frame must be redone."""
+        if not self.pending:
+            return False
+        if self.ws is not None and self.ws.generation != self.generation:
+            # the workspace was reused since: this frame's buffers (and its status)
+            # belong to a later view, whose prepare checked this one's status
+            self.pending = False
+            return False
+        self.pending = False
+        if self.ws is not None and self.ws.pending is not None and self.ws.pending[2] is self:
+            self.ws.pending = None
+        p, flags = ctypes.c_int64(), ctypes.c_int32()
+        _native.check(self.lib.hs_frame_status(ctypes.byref(self.st), ctypes.byref(p),
+                                               ctypes.byref(flags), _stream()), "hs_frame_status")
+        self._status_seen(p.value, flags.value & _native.HS_FRAME_PAIR_OVERFLOW,
+                          flags.value & _native.HS_FRAME_DEPTH_FALLBACK)
+        if flags.value == 0:
+            return False
+        if flags.value & _native.HS_FRAME_DEPTH_FALLBACK:
+            # redoes the ranks with the full sort and re-reads P
+            _native.check(self.lib.hs_frame_read_num_pairs(ctypes.byref(self.st), _stream()),
+                          "hs_frame_read_num_pairs")
+        else:
+            self.st.num_pairs = p.value
+        self.alloc_binning()
+        _native.check(self.lib.hs_bin_and_sort(ctypes.byref(self.st), _stream()),
+                      "hs_bin_and_sort")
+        return True
 
     @property
     def tiles_x(self):
@@ -132,28 +228,53 @@ class DeviceFrame:
         return int(self.st.tiles_y)
 
     def reuse_binning(self):
-        """Point the frame at whatever binning workspace is already there (the
-        Workspace's, or this frame's) before P is known."""
-        buf = self.ws._bufs.get("bin_ws") if self.ws is not None else self.bin_ws
-        if buf is not None:
-            self.st.bin_ws = buf.data_ptr()
-            self.st.bin_ws_bytes = buf.numel()
-            if self.ws is None:
-                self.bin_ws = buf
+        """Point the frame at the workspace's binning buffer and pair capacity (set
+        by an earlier view), so it can bin without reading P first.  Returns the
+        capacity (0: none yet, read P)."""
+        if self.ws is None:
+            return 0
+        buf = self.ws._bufs.get("bin_ws")
+        cap = self.ws.pair_capacity
+        if buf is None or cap <= 0:
+            return 0
+        if buf.numel() < self.lib.hs_binning_workspace_size(self.st.n, cap, self.st.width,
+                                                            self.st.height):
+            return 0
+        self.bin_ws = buf
+        self.st.bin_ws = buf.data_ptr()
+        self.st.bin_ws_bytes = buf.numel()
+        self.st.pair_capacity = cap
+        self.capacity = cap
+        return cap
 
     def alloc_binning(self):
+        """A binning workspace for the known P, with headroom for later views."""
         lib = self.lib
-        nbytes = lib.hs_binning_workspace_size(self.st.n, self.st.num_pairs, self.st.width,
-                                               self.st.height)
+        p = int(self.st.num_pairs)
+        cap = max(_capacity_for(p), self.ws.pair_capacity if self.ws is not None else 0)
+        if self.ws is None:
+            cap = p
+        nbytes = lib.hs_binning_workspace_size(self.st.n, cap, self.st.width, self.st.height)
         if self.ws is not None:
             self.bin_ws = self.ws.bytes("bin_ws", nbytes)
+            self.ws.pair_capacity = cap
+            self.ws.last_pairs = p
         elif self.bin_ws is None or self.bin_ws.numel() < nbytes:
             self.bin_ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
         self.st.bin_ws = self.bin_ws.data_ptr()
         self.st.bin_ws_bytes = self.bin_ws.numel()
+        self.st.pair_capacity = cap
+        self.capacity = cap
+
+    def stale(self):
+        """True once a later view was prepared into this frame's workspace."""
+        return self.ws is not None and self.ws.generation != self.generation
 
     def export(self):
         """FrameGeometry integers/packed columns as host numpy arrays (parity)."""
+        if self.stale():
+            raise WorkspaceError("this frame's workspace was reused by a later view")
+        self.resolve()
         n, p, t = self.n_total, self.num_pairs, int(self.st.n_tiles)
         dev = self.device
         valid = torch.empty(n, dtype=torch.int32, device=dev)
@@ -193,6 +314,8 @@ def prepare(scene, cam, kernel="half", timer=None, ws=None):
     scene = Scene.from_any(scene)
     cam = CameraModel.from_any(cam)
     _validate(scene, cam, kernel)
+    if ws is not None:
+        ws.check_previous()
     frame = DeviceFrame(scene, cam, kernel, ws)
     lib = frame.lib
     s = _stream()
@@ -202,15 +325,36 @@ def prepare(scene, cam, kernel="half", timer=None, ws=None):
         st = lib.hs_preprocess_fwd(ctypes.byref(frame.st), ctypes.byref(sc), ctypes.byref(cs),
                                    _ptr(frame.radii), s)
     _native.check(st, "hs_preprocess_fwd")
-    # the one host sync (P).  With the previous view's binning workspace in place the
-    # library bins right after it (no host round trip while the GPU idles).
-    frame.reuse_binning()
+    if frame.reuse_binning() > 0:
+        # the workspace has a pair capacity from an earlier view: bin with P on the
+        # device (no host round trip); the status is copied back behind the binning
+        # and checked by the next prepare into this workspace (or frame.resolve())
+        with timer.span("bin_and_sort"):
+            st = lib.hs_bin_async(ctypes.byref(frame.st), s)
+        if st == _native.HS_ERR_WORKSPACE:  # large-image path: P was read, too big
+            frame.alloc_binning()
+            st = lib.hs_bin_and_sort(ctypes.byref(frame.st), s)
+        _native.check(st, "hs_bin_async")
+        if frame.st.num_pairs < 0:
+            frame.pending = True
+            pinned = ws.status_buffer()
+            _native.check(lib.hs_frame_status_async(ctypes.byref(frame.st),
+                                                    ctypes.c_void_p(pinned.data_ptr()), s),
+                          "hs_frame_status_async")
+            ev = torch.cuda.Event()
+            ev.record()
+            ws.pending = (ev, pinned, frame)
+        return frame
+    # first view of this workspace (or no workspace): read P (a host sync), size the
+    # binning workspace with headroom, then bin
     with timer.span("bin_and_sort"):
         st = lib.hs_read_pairs_and_bin(ctypes.byref(frame.st), s)
         if st == _native.HS_ERR_WORKSPACE:
             frame.alloc_binning()
             st = lib.hs_bin_and_sort(ctypes.byref(frame.st), s)
     _native.check(st, "hs_read_pairs_and_bin")
+    if ws is not None and frame.st.depth_sort_full:
+        ws.depth_sort_full = 1  # the fixup overflowed: rank later views with the full sort
     return frame
 
 

@@ -239,6 +239,12 @@ def render(scene, cam, kernel="half", threads=None, frame=None):
     frame._ws_gen[0] += 1
     color, alpha, depth, trans, term, radii = _to_host(
         [dout.color, dout.alpha, dout.depth, dout.transmittance, dout.terminal, dout.radii])
+    if frame._device.resolve():
+        # the view was binned with P on the device and overflowed its workspace's pair
+        # capacity; resolve() re-binned it with a larger one: blend it again
+        dout = _dev.render(dscene, cam, kernel, frame=frame._device, ws=frame._ws)
+        color, alpha, depth, trans, term, radii = _to_host(
+            [dout.color, dout.alpha, dout.depth, dout.transmittance, dout.terminal, dout.radii])
     out = RenderOutput(color=color, alpha=alpha, depth=depth, per_pixel_terminal_index=term,
                        camera=cam, transmittance=trans, frame=frame, radii=radii)
     out._device_out = dout

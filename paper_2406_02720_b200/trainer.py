@@ -352,12 +352,18 @@ class StepRunner:
             self.grads = device.DeviceGradientSet.empty_flat(scene)
         out = self.rast.render(scene, cam)
         stats, d_color = self.loss(out.color, target)
-        self.last_stats = stats
         loss = stats[0]
         if check_finite:
             loss = float(loss)  # trainer.py:189-190 (one 8-byte read)
+            if out.frame.resolve():
+                # binned with P on the device past the workspace's capacity (e.g. right
+                # after density control grew the scene): re-binned, blend it again
+                out = self.rast.render(scene, cam)
+                stats, d_color = self.loss(out.color, target)
+                loss = float(stats[0])
             if not math.isfinite(loss):
                 raise NonFiniteLoss(iteration, loss)
+        self.last_stats = stats
         self.rast.render_backward(scene, cam, out, d_color, grads=self.grads)
         adam_step(scene, self.grads, self.config, opt_state, iteration, spatial_scale)
         return loss, self.grads, out

@@ -62,7 +62,7 @@ def test_status_mapping(native_lib):
         _native.check(_native.HS_ERR_MISMATCHED_FORWARD)
     with pytest.raises(ValueError):
         _native.check(_native.HS_ERR_INVALID_KERNEL)
-    assert native_lib.hs_abi_version() == 1
+    assert native_lib.hs_abi_version() == 2
     assert b"EmptyScene" in native_lib.hs_status_string(_native.HS_ERR_EMPTY_SCENE)
 
 
