@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="time eager launches, no CUDA graph")
     ap.add_argument("--no-configs", action="store_true",
                     help="skip the per-config records (multiview_c4, c1, c2, c5)")
     return ap.parse_args()
@@ -394,6 +395,21 @@ def config_run(cfg, args, world, rank, fp32_peak, torch, dist, barrier):
         step()
     steps = max(3, min(args.steps, 10))
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    graph_ms = None
+    if world == 1 and not args.no_graph:
+        try:
+            graph = device.CapturedStep(step, rast.slots, warmup=1)
+            barrier()
+            start.record()
+            for _ in range(steps):
+                graph.replay()
+            end.record()
+            barrier()
+            graph.check()
+            graph_ms = start.elapsed_time(end) / steps
+            del graph
+        except Exception:
+            graph_ms = None
     barrier()
     start.record()
     for _ in range(steps):
@@ -401,6 +417,9 @@ def config_run(cfg, args, world, rank, fp32_peak, torch, dist, barrier):
     end.record()
     barrier()
     ms = start.elapsed_time(end) / steps
+    eager_ms = ms
+    if graph_ms is not None:
+        ms = graph_ms
     exposed = statistics.mean(a.elapsed_time(b) for a, b in marks) if marks else 0.0
     t = torch.tensor([ms, exposed], device="cuda")
     if world > 1:
@@ -418,7 +437,9 @@ def config_run(cfg, args, world, rank, fp32_peak, torch, dist, barrier):
     k6 = sum(tot.get("blend_bwd", [0.0])) / steps
     n_views = len(cams) if multi else world
     rec = {"value": n_views * 1e3 / ms, "unit": "views/s" if multi else "iters/s",
-           "ms_per_step": ms, "steps": steps, "views_per_step": n_views,
+           "ms_per_step": ms, "eager_ms_per_step": eager_ms,
+           "launch_mode": "cuda graph" if graph_ms is not None else "eager",
+           "steps": steps, "views_per_step": n_views,
            "views_this_rank": len(views), "stage_ms_per_view": per_view,
            "blend_fwd_frac": fwd_e * FWD_FLOPS_PER_EVAL / (k5 * 1e-3) / 1e12 / fp32_peak
            if k5 else None,
@@ -553,19 +574,46 @@ def main():
     for _ in range(max(args.warmup, 3)):
         step()
     barrier()
+    # one GPU: the step is captured once as a CUDA graph and replayed (binning needs no
+    # host round trip, so the whole step is capturable); N > 1 runs eagerly (the
+    # bucketed NCCL exchange lives on a side stream)
+    graph, graph_note = None, "eager"
+    if world == 1 and fused is None and not args.no_graph:
+        try:
+            graph = device.CapturedStep(step, rast.slots, warmup=1)
+            graph_note = "cuda graph of the whole step, replayed"
+        except Exception as e:  # report and fall back to eager launches
+            graph_note = f"eager (graph capture failed: {e!r})"[:300]
     launches0 = _native.launch_count()
+    step()  # launches of one step (a graph replay does not pass through the library)
+    per_step_launches = _native.launch_count() - launches0
+    barrier()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     clocks.mark("t_start")
     start.record()
     for _ in range(args.steps):
-        out = step(timer)
+        if graph is not None:
+            graph.replay()
+        else:
+            out = step(timer)
     end.record()
     barrier()
     clocks.mark("t_end")
     clock_info = clocks.stop()
-    launches = _native.launch_count() - launches0
+    launches = per_step_launches * args.steps
     ms = start.elapsed_time(end) / args.steps
+    eager_ms = None
+    if graph is not None:
+        graph.check()  # no replayed view outgrew its binning capacity
+        # the per-stage CUDA-event times come from the same steps run eagerly
+        barrier()
+        start.record()
+        for _ in range(args.steps):
+            out = step(timer)
+        end.record()
+        barrier()
+        eager_ms = start.elapsed_time(end) / args.steps
     ms_t = torch.tensor([ms], device="cuda")
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
@@ -733,6 +781,7 @@ def main():
             "vs_baseline": None, "dtype": "f32 blend / f64 geometry", "data": "synthetic",
             "config": bench_config(args.config, world, views_per_step),
             "fwd_fps": views_per_step * 1e3 / fwd_ms, "fwd_ms_per_step": fwd_ms,
+            "launch_mode": graph_note, "eager_ms_per_step": eager_ms,
             "train_step": {"value": views_per_step * 1e3 / train_ms, "unit": metric_unit(multi),
                            "ms_per_step": train_ms, "loss_kernel_ms": loss_ms,
                            "adam_kernel_ms": adam_ms,

@@ -150,13 +150,16 @@ int hs_bin_and_sort(hs_frame* frame, void* stream);
 
 /* The same binning with no host round trip: P stays on the device and the
  * workspace is laid out for frame->pair_capacity pairs (set by the caller, e.g.
- * from an earlier view's P with headroom).  K2 writes every pair straight into
- * a row bucket and a stable counting sort by tile column finishes the order;
- * tile_starts come out of the same scans.  If P exceeds the capacity nothing is
- * binned (every tile list is empty, so the blends and K7 do no work) and the
- * status says so: check it with hs_frame_status at the caller's next sync point
- * and re-bin with a larger workspace.  Images wider than 2048 or taller than
- * 1024 tiles take the synchronous path inside this call. */
+ * from an earlier view's P with headroom).  K2 writes each splat's pairs as
+ * segments (one per tile row and block of 32 tile columns) straight into
+ * per-(row, block) buckets in depth-rank order, and a warp per bucket chunk
+ * appends them to the tile lists (a stable counting sort by tile); tile_starts
+ * come out of the same scans.  If P exceeds the capacity nothing is binned
+ * (every tile list is empty, so the blends and K7 do no work) and the status
+ * says so: check it with hs_frame_status at the caller's next sync point and
+ * re-bin with a larger workspace.  Images wider than 2048 tiles, taller than
+ * 1024 tiles, or with more than 2048 (tile row, 32-column block) pairs (beyond
+ * 4K UHD) take the synchronous path inside this call. */
 int hs_bin_async(hs_frame* frame, void* stream);
 
 /* Binning status flags (hs_frame_status) */
@@ -169,8 +172,9 @@ int hs_bin_async(hs_frame* frame, void* stream);
 int hs_frame_status(hs_frame* frame, int64_t* num_pairs, int32_t* flags, void* stream);
 /* The same status without waiting: enqueues on `stream` a copy of it into
  * host_status (24 bytes of host memory, pinned for an asynchronous copy):
- * int64 P at byte 0, int32 binning flags at byte 8 (bit 0: HS_FRAME_PAIR_OVERFLOW),
- * int32 depth-fallback flag at byte 16 (non-zero: HS_FRAME_DEPTH_FALLBACK).
+ * int64 P at byte 0, int64 segment count at byte 8, int32 binning flags at
+ * byte 16 (bit 0: HS_FRAME_PAIR_OVERFLOW), int32 depth-fallback flag at byte 24
+ * (non-zero: HS_FRAME_DEPTH_FALLBACK); 32 bytes.
  * Valid once the stream has passed this point (e.g. an event recorded after it). */
 int hs_frame_status_async(const hs_frame* frame, void* host_status, void* stream);
 

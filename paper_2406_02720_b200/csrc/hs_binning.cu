@@ -163,76 +163,105 @@ cudaError_t run_depth_sort_hi(void* temp, size_t temp_bytes, const uint64_t* key
 }
 
 // cnt_r[r] = count[order[r]] and rank_of; P accumulates as int64 next to the
-// int32 scan (which may wrap).  With the row path (ROWS) each CTA -- one block of
-// kBinRanks ranks -- also histograms its pairs by tile row (a splat adds spans_x
-// to each row of its rect) into cnt_r[n + 1 + ty * nb + block].
-template <bool ROWS>
+// int32 scan (which may wrap).  With the segment path (SEGS) each CTA -- one
+// block of kBinRanks ranks -- also histograms its segments by (tile row, column
+// block) key into cnt_r[n + 1 + key * nb + block] and adds its pairs per tile row
+// into row_pairs.
+template <bool SEGS>
 __global__ void __launch_bounds__(kBinRanks) gather_counts_kernel(
     const int32_t* __restrict__ count, const uint32_t* __restrict__ order,
     const int4* __restrict__ rect, int32_t* __restrict__ cnt_r, uint32_t* __restrict__ rank_of,
-    int64_t n, int tiles_y, BinStatusDev* __restrict__ status) {
-  extern __shared__ int rows_s[];
-  __shared__ long long csum[kBinRanks / 32];
+    int64_t n, int tiles_y, int nblk, int32_t* __restrict__ row_pairs,
+    BinStatusDev* __restrict__ status) {
+  extern __shared__ int smem_cnt[];  // [keys] segments, then [tiles_y] pairs
+  __shared__ long long csum[kBinRanks / 32][2];
+  const int keys = tiles_y * nblk;
+  int* keys_s = smem_cnt;
+  int* rows_s = smem_cnt + keys;
   const int64_t r = (int64_t)blockIdx.x * kBinRanks + threadIdx.x;
-  if (ROWS) {
-    for (int ty = threadIdx.x; ty < tiles_y; ty += kBinRanks) rows_s[ty] = 0;
+  if (SEGS) {
+    for (int e = threadIdx.x; e < keys + tiles_y; e += kBinRanks) smem_cnt[e] = 0;
     __syncthreads();
   }
-  int c = 0;
+  int c = 0, nseg = 0;
   if (r < n) {
     const uint32_t i = order[r] & kIndexMask;
     c = count[i];
     cnt_r[r] = c;
     rank_of[i] = (uint32_t)r;
-    if (ROWS && c > 0) {
+    if (SEGS && c > 0) {
       const int4 rc = rect[i];
       const int sx = rc.y - rc.x + 1;
-      for (int ty = rc.z; ty <= rc.w; ++ty) atomicAdd(&rows_s[ty], sx);
+      const int b0 = rc.x / kSegCols, b1 = rc.y / kSegCols;
+      nseg = (rc.w - rc.z + 1) * (b1 - b0 + 1);
+      for (int ty = rc.z; ty <= rc.w; ++ty) {
+        atomicAdd(&rows_s[ty], sx);
+        for (int b = b0; b <= b1; ++b) atomicAdd(&keys_s[ty * nblk + b], 1);
+      }
     }
   }
   if (r == 0) cnt_r[n] = 0;
-  long long v = c;
+  long long v = c, vs = nseg;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  if ((threadIdx.x & 31) == 0) csum[threadIdx.x >> 5] = v;
+  for (int o = 16; o > 0; o >>= 1) {
+    v += __shfl_xor_sync(0xffffffffu, v, o);
+    vs += __shfl_xor_sync(0xffffffffu, vs, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    csum[threadIdx.x >> 5][0] = v;
+    csum[threadIdx.x >> 5][1] = vs;
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
-    long long t = 0;
-    for (int w = 0; w < kBinRanks / 32; ++w) t += csum[w];
+    long long t = 0, ts = 0;
+    for (int w = 0; w < kBinRanks / 32; ++w) {
+      t += csum[w][0];
+      ts += csum[w][1];
+    }
     if (t) atomicAdd(reinterpret_cast<unsigned long long*>(&status->pairs),
                      (unsigned long long)t);
+    if (ts) atomicAdd(reinterpret_cast<unsigned long long*>(&status->segs),
+                      (unsigned long long)ts);
   }
-  if (!ROWS) return;
+  if (!SEGS) return;
   const int64_t nb = gridDim.x;
+  for (int k = threadIdx.x; k < keys; k += kBinRanks)
+    cnt_r[n + 1 + k * nb + blockIdx.x] = keys_s[k];
   for (int ty = threadIdx.x; ty < tiles_y; ty += kBinRanks)
-    cnt_r[n + 1 + ty * nb + blockIdx.x] = rows_s[ty];
+    if (rows_s[ty]) atomicAdd(&row_pairs[ty], rows_s[ty]);
 }
 
 cudaError_t run_count_scan(void* temp, size_t temp_bytes, const int32_t* count,
                            const uint32_t* order, const int4* rect, int32_t* cnt_r,
-                           int32_t* off_r, uint32_t* rank_of, int64_t n, int tiles_y,
-                           BinStatusDev* status, cudaStream_t stream) {
-  const bool rows = tiles_y > 0;
+                           int32_t* off_r, uint32_t* rank_of, int64_t n, int tiles_x,
+                           int tiles_y, int32_t* row_pairs, BinStatusDev* status,
+                           cudaStream_t stream) {
+  const bool segs = tiles_x > 0;
+  const int nblk = segs ? seg_blocks(tiles_x) : 0;
+  const int keys = segs ? tiles_y * nblk : 0;
   const unsigned nb = (unsigned)bin_row_blocks(n);
   cudaError_t e = cudaMemsetAsync(status, 0, sizeof(BinStatusDev), stream);
   if (e != cudaSuccess) return e;
-  if (rows) {
-    gather_counts_kernel<true><<<nb, kBinRanks, tiles_y * sizeof(int), stream>>>(
-        count, order, rect, cnt_r, rank_of, n, tiles_y, status);
+  if (segs) {
+    e = cudaMemsetAsync(row_pairs, 0, tiles_y * sizeof(int32_t), stream);
+    if (e != cudaSuccess) return e;
+    gather_counts_kernel<true><<<nb, kBinRanks, (keys + tiles_y) * sizeof(int), stream>>>(
+        count, order, rect, cnt_r, rank_of, n, tiles_y, nblk, row_pairs, status);
   } else {
     gather_counts_kernel<false><<<nb, kBinRanks, 0, stream>>>(count, order, rect, cnt_r,
-                                                              rank_of, n, 0, status);
+                                                              rank_of, n, 0, 0, row_pairs,
+                                                              status);
   }
   note_launch();
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   e = cub::DeviceScan::ExclusiveSum(temp, temp_bytes, cnt_r, off_r,
-                                    (int)count_scan_len(n, tiles_y, rows), stream);
+                                    (int)count_scan_len(n, keys, segs), stream);
   note_launch(2);
   return e;
 }
 
-// ---- row-bucket binning (no host round trip) --------------------------------
+// ---- segment binning (no host round trip) -----------------------------------
 // 256-thread exclusive scan of one int per thread; returns the CTA total.
 __device__ __forceinline__ int block_exclusive_scan(int v, int* excl, int* warp_tot) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -255,26 +284,51 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int* excl, int* warp_
   return total;
 }
 
+// Lanes of the warp holding the same key (0 <= key < 2^nbits), from one ballot per
+// key bit: the multisplit form of __match_any_sync.  MATCH.ANY issues on the ADU
+// pipe, whose throughput capped a per-pair version of these passes at c5 (ncu: ADU
+// 96% busy).
+__device__ __forceinline__ unsigned warp_peers(int key, int nbits) {
+  unsigned peers = 0xffffffffu;
+  for (int b = 0; b < nbits; ++b) {
+    const bool bit = (key >> b) & 1;
+    const unsigned vote = __ballot_sync(0xffffffffu, bit);
+    peers &= bit ? vote : ~vote;
+  }
+  return peers;
+}
+
+__device__ __forceinline__ int bit_width(int v) { return 32 - __clz(v); }
+
 __device__ __forceinline__ bool bin_overflowed(const RowBinArgs& a, long long* p_out) {
   const long long p = *reinterpret_cast<volatile long long*>(&a.status->pairs);
   *p_out = p;
   return p > a.capacity || p > 0x7fffffffll;
 }
 
-// start of row ty's bucket (the row histograms' scan entries are offset by P)
-__device__ __forceinline__ int row_start(const RowBinArgs& a, int ty, int p) {
-  return ty < a.tiles_y ? a.off_r[a.n + 1 + (int64_t)ty * a.nb] - p : p;
+// first segment of key k's bucket (the histograms' scan entries are offset by P)
+__device__ __forceinline__ int key_start(const RowBinArgs& a, int k, int p) {
+  return k < a.keys ? a.off_r[a.n + 1 + (int64_t)k * a.nb] - p
+                    : (int)*reinterpret_cast<volatile long long*>(&a.status->segs);
 }
 
-// Emit: one CTA per block of kBinRanks depth ranks (8 warps x 32 ranks, the
-// count pass's blocks).  Warp w's pairs are one contiguous run of the
-// generation order; in each tile row they go to
-//   row bucket base (the scan) + the earlier warps' pairs in that row + the
-//   warp's earlier pairs in that row (match_any on the row, in pair order),
-// so every row bucket holds its pairs in generation (depth rank) order.
-// CTA 0 also lays out the column passes' chunks (kBinChunk pairs, row-aligned).
-__global__ void __launch_bounds__(kBinRanks) row_emit_kernel(RowBinArgs a) {
-  extern __shared__ int wrow[];  // [8][tiles_y]
+// a / b for 0 <= a < 2^24, 1 <= b: a float estimate corrected by one step (exact)
+__device__ __forceinline__ int div_small(int a, int b, float inv_b) {
+  int q = __float2int_rz((float)a * inv_b);
+  if (q * b > a) --q;
+  if ((q + 1) * b <= a) ++q;
+  return q;
+}
+
+// Emit: one CTA per block of kBinRanks depth ranks (8 warps x 32 ranks, the count
+// pass's blocks).  Warp w's segments, in generation order (splat-major, then tile
+// row, then column block), go to
+//   the key's bucket base (the scan) + the earlier warps' segments of that key +
+//   the warp's earlier segments of that key (ballot peers, in segment order),
+// so every bucket holds its segments in depth-rank order.
+// CTA 0 also lays out the fill passes' chunks (kSegChunk segments, key-aligned).
+__global__ void __launch_bounds__(kBinRanks) seg_emit_kernel(RowBinArgs a) {
+  extern __shared__ int wkey[];  // [8][keys]
   __shared__ int scan_tot[kBinRanks / 32];
   long long p64;
   if (bin_overflowed(a, &p64)) {
@@ -283,69 +337,71 @@ __global__ void __launch_bounds__(kBinRanks) row_emit_kernel(RowBinArgs a) {
   }
   const int p = (int)p64;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int T = a.tiles_y;
+  const int K = a.keys;
   if (blockIdx.x == 0) {
-    // chunk layout: row ty's bucket is split into ceil(len / kBinChunk) chunks
-    constexpr int kPer = kBinMaxRows / kBinRanks;
+    constexpr int kPer = kBinMaxKeys / kBinRanks;
     int nch[kPer], tot = 0;
 #pragma unroll
-    for (int k = 0; k < kPer; ++k) {
-      const int ty = threadIdx.x * kPer + k;
-      nch[k] = ty < T ? (row_start(a, ty + 1, p) - row_start(a, ty, p) + kBinChunk - 1) /
-                            kBinChunk
-                      : 0;
-      tot += nch[k];
+    for (int q = 0; q < kPer; ++q) {
+      const int k = threadIdx.x * kPer + q;
+      nch[q] = k < K ? (key_start(a, k + 1, p) - key_start(a, k, p) + kSegChunk - 1) / kSegChunk
+                     : 0;
+      tot += nch[q];
     }
     int excl;
     const int all = block_exclusive_scan(tot, &excl, scan_tot);
 #pragma unroll
-    for (int k = 0; k < kPer; ++k) {
-      const int ty = threadIdx.x * kPer + k;
-      if (ty < T) a.chunk_first[ty] = excl;
-      excl += nch[k];
+    for (int q = 0; q < kPer; ++q) {
+      const int k = threadIdx.x * kPer + q;
+      if (k < K) a.chunk_first[k] = excl;
+      excl += nch[q];
     }
-    if (threadIdx.x == 0) a.chunk_first[T] = all;
+    if (threadIdx.x == 0) a.chunk_first[K] = all;
   }
-  for (int e = threadIdx.x; e < 8 * T; e += kBinRanks) wrow[e] = 0;
+  for (int e = threadIdx.x; e < 8 * K; e += kBinRanks) wkey[e] = 0;
   __syncthreads();
   const int64_t r = (int64_t)blockIdx.x * kBinRanks + threadIdx.x;
   const int c = r < a.n ? a.cnt_r[r] : 0;
   uint32_t v = 0;
   int4 rc = make_int4(0, 0, 0, 0);
-  int spans_x = 1;
+  int nbl = 1, b0 = 0, ns = 0;
   if (c > 0) {
     v = a.order[r];
     const uint32_t i = v & kIndexMask;
     rc = a.rect[i];
-    spans_x = rc.y - rc.x + 1;
+    const int spans_x = rc.y - rc.x + 1;
     // pair (tx, ty) of this splat has generation index origin + ty * spans_x + tx
     reinterpret_cast<float*>(a.rec)[(size_t)i * kRecordFloats + R_ROW_ORIGIN] =
         __int_as_float(a.off_r[r] - rc.z * spans_x - rc.x);
-    for (int ty = rc.z; ty <= rc.w; ++ty) atomicAdd(&wrow[w * T + ty], spans_x);
+    b0 = rc.x / kSegCols;
+    nbl = rc.y / kSegCols - b0 + 1;
+    ns = (rc.w - rc.z + 1) * nbl;
+    for (int ty = rc.z; ty <= rc.w; ++ty)
+      for (int b = 0; b < nbl; ++b) atomicAdd(&wkey[w * K + ty * a.nblk + b0 + b], 1);
   }
   __syncthreads();
-  for (int ty = threadIdx.x; ty < T; ty += kBinRanks) {
-    int base = a.off_r[a.n + 1 + (int64_t)ty * a.nb + blockIdx.x] - p;
+  for (int k = threadIdx.x; k < K; k += kBinRanks) {
+    int base = a.off_r[a.n + 1 + (int64_t)k * a.nb + blockIdx.x] - p;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int t = wrow[k * T + ty];
-      wrow[k * T + ty] = base;
+    for (int q = 0; q < 8; ++q) {
+      const int t = wkey[q * K + k];
+      wkey[q * K + k] = base;
       base += t;
     }
   }
   __syncthreads();
-  int* cur = wrow + w * T;
-  // the warp's pairs, consecutive lanes on consecutive pairs (splat-major, then
-  // row-major over the splat's rect)
-  int incl = c;
+  int* cur = wkey + w * K;
+  int incl = ns;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const int t = __shfl_up_sync(0xffffffffu, incl, o);
     if (lane >= o) incl += t;
   }
-  const int excl = incl - c;
+  const int excl = incl - ns;
   const int total = __shfl_sync(0xffffffffu, incl, 31);
   const unsigned lt = (1u << lane) - 1u;
+  const int kbits = bit_width(K);  // keys 0..K (K: no segment)
+  const float inv_nbl = 1.0f / (float)nbl;
   for (int j0 = 0; j0 < total; j0 += 32) {
     const int j = j0 + lane;
     int sidx = 0;
@@ -356,62 +412,84 @@ __global__ void __launch_bounds__(kBinRanks) row_emit_kernel(RowBinArgs a) {
       if (cand < 32 && e <= j) sidx = cand;
     }
     const int es = __shfl_sync(0xffffffffu, excl, sidx);
-    const int sx = __shfl_sync(0xffffffffu, spans_x, sidx);
+    const int sn = __shfl_sync(0xffffffffu, nbl, sidx);
+    const float sinv = __shfl_sync(0xffffffffu, inv_nbl, sidx);
+    const int sb0 = __shfl_sync(0xffffffffu, b0, sidx);
     const int x0 = __shfl_sync(0xffffffffu, rc.x, sidx);
+    const int x1 = __shfl_sync(0xffffffffu, rc.y, sidx);
     const int y0 = __shfl_sync(0xffffffffu, rc.z, sidx);
     const uint32_t vs = __shfl_sync(0xffffffffu, v, sidx);
     const bool live = j < total;
-    const int l = j - es, ly = l / sx, lx = l - ly * sx;
-    const int ty = live ? y0 + ly : -1;
-    const unsigned peers = __match_any_sync(0xffffffffu, ty);
-    const int pos = live ? cur[ty] + __popc(peers & lt) : 0;
+    const int l = j - es;
+    const int row = div_small(l, sn, sinv);
+    const int b = sb0 + (l - row * sn);
+    const int key = live ? (y0 + row) * a.nblk + b : K;
+    const unsigned peers = warp_peers(key, kbits);
+    const int pos = live ? cur[key] + __popc(peers & lt) : 0;
     __syncwarp();
-    if (live && lane == __ffs(peers) - 1) cur[ty] += __popc(peers);
+    if (live && lane == __ffs(peers) - 1) cur[key] += __popc(peers);
     __syncwarp();
     if (live) {
-      a.tx_row[pos] = (uint16_t)(x0 + lx);
-      a.val_row[pos] = vs;
+      const int lo = max(x0, b * kSegCols) - b * kSegCols;
+      const int hi = min(x1, b * kSegCols + kSegCols - 1) - b * kSegCols;
+      a.segs[pos] = make_uint2(vs, (uint32_t)(lo | ((hi - lo + 1) << 5)));
     }
   }
 }
 
-// The chunk a column-pass CTA owns: its row and [begin, end) in the row buckets.
-__device__ __forceinline__ bool chunk_of(const RowBinArgs& a, int p, int c, int* ty, int* begin,
-                                         int* end) {
-  const int T = a.tiles_y;
-  if (c >= a.chunk_first[T]) return false;
-  int lo = 0, hi = T;  // last row with chunk_first[row] <= c
+// The chunk a fill warp owns: its key and [begin, end) in the segment buckets.
+__device__ __forceinline__ bool seg_chunk_of(const RowBinArgs& a, int p, int c, int* key,
+                                             int* begin, int* end) {
+  const int K = a.keys;
+  if (c >= a.chunk_first[K]) return false;
+  int lo = 0, hi = K;  // last key with chunk_first[key] <= c
   while (hi - lo > 1) {
     const int mid = (lo + hi) >> 1;
     if (a.chunk_first[mid] <= c) lo = mid; else hi = mid;
   }
-  *ty = lo;
-  const int rs = row_start(a, lo, p), re = row_start(a, lo + 1, p);
-  *begin = rs + (c - a.chunk_first[lo]) * kBinChunk;
-  *end = min(*begin + kBinChunk, re);
+  *key = lo;
+  *begin = key_start(a, lo, p) + (c - a.chunk_first[lo]) * kSegChunk;
+  *end = min(*begin + kSegChunk, key_start(a, lo + 1, p));
   return true;
 }
 
-// Column pass 1: per chunk, pairs per tile column -> hist[chunk][tx].
-__global__ void __launch_bounds__(256) tile_hist_kernel(RowBinArgs a) {
-  extern __shared__ int hs_[];  // [tiles_x]
+// Fill pass 1: per chunk (one warp), lane L counts the chunk's segments covering
+// tile column L of the key's block -> seg_cnt[chunk][L].  Each segment adds +1 at
+// its first column and -1 past its last in a per-warp difference array in shared
+// memory; one 32-wide prefix sum at the end gives the counts.
+__global__ void __launch_bounds__(256) seg_count_kernel(RowBinArgs a) {
+  __shared__ int diff_all[8][33];
   long long p64;
   if (bin_overflowed(a, &p64)) return;
-  int ty, begin, end;
-  if (!chunk_of(a, (int)p64, blockIdx.x, &ty, &begin, &end)) return;
-  for (int t = threadIdx.x; t < a.tiles_x; t += 256) hs_[t] = 0;
-  __syncthreads();
-  for (int k = begin + threadIdx.x; k < end; k += 256) atomicAdd(&hs_[a.tx_row[k]], 1);
-  __syncthreads();
-  int32_t* h = a.hist + (int64_t)blockIdx.x * a.tiles_x;
-  for (int t = threadIdx.x; t < a.tiles_x; t += 256) h[t] = hs_[t];
+  const int lane = threadIdx.x & 31;
+  int* diff = diff_all[threadIdx.x >> 5];
+  const int c = blockIdx.x * 8 + (threadIdx.x >> 5);
+  int key, begin, end;
+  if (!seg_chunk_of(a, (int)p64, c, &key, &begin, &end)) return;
+  diff[lane] = 0;
+  if (lane == 0) diff[32] = 0;
+  __syncwarp();
+  for (int s = begin + lane; s < end; s += 32) {
+    const uint32_t sg = a.segs[s].y;
+    const int lo = (int)(sg & 31u), len = (int)(sg >> 5);
+    atomicAdd(&diff[lo], 1);
+    atomicAdd(&diff[lo + len], -1);
+  }
+  __syncwarp();
+  int cnt = diff[lane];
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, cnt, o);
+    if (lane >= o) cnt += t;
+  }
+  a.seg_cnt[(int64_t)c * 32 + lane] = cnt;
 }
 
-// Column pass 2: one CTA per tile row.  Each column's chunk counts become
-// exclusive prefixes over the row's chunks (in place); the columns' totals,
-// scanned along the row from the row's bucket start, are the row's tile_starts
-// (np.searchsorted's CSR, rasterizer.py:324-325).  On overflow every tile list
-// is left empty, so the blends and K7 see no pairs.
+// Fill pass 2: one CTA per tile row.  Each tile's chunk counts become exclusive
+// prefixes over its key's chunks (in place); the tiles' totals, scanned along the
+// row from the pairs of the rows above, are the row's tile_starts
+// (np.searchsorted's CSR, rasterizer.py:324-325).  On overflow every tile list is
+// left empty, so the blends and K7 see no pairs.
 __global__ void __launch_bounds__(256) tile_scan_kernel(RowBinArgs a) {
   __shared__ int tot_s[kBinMaxCols];
   __shared__ int scan_tot[8];
@@ -423,19 +501,28 @@ __global__ void __launch_bounds__(256) tile_scan_kernel(RowBinArgs a) {
     return;
   }
   const int p = (int)p64;
-  const int c0 = a.chunk_first[ty], c1 = a.chunk_first[ty + 1];
   for (int t = threadIdx.x; t < X; t += 256) {
+    const int key = ty * a.nblk + t / kSegCols, L = t % kSegCols;
+    const int c0 = a.chunk_first[key], c1 = a.chunk_first[key + 1];
     int run = 0;
-    int32_t* h = a.hist + (int64_t)c0 * X + t;
-    for (int c = c0; c < c1; ++c, h += X) {
-      const int v = *h;
-      *h = run;
-      run += v;
+    int32_t* h = a.seg_cnt + (int64_t)c0 * 32 + L;
+    // 16 independent loads in flight per step (a key's chunks are many at c5)
+    for (int c = c0; c < c1; c += 16, h += 16 * 32) {
+      int v[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) v[k] = c + k < c1 ? h[k * 32] : 0;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        if (c + k < c1) h[k * 32] = run;
+        run += v[k];
+      }
     }
     tot_s[t] = run;
   }
+  // pairs of the rows above (up to kBinMaxRows values, summed by every CTA)
+  int above = 0;
+  for (int q = threadIdx.x; q < ty; q += 256) above += a.row_pairs[q];
   __syncthreads();
-  // exclusive scan of tot_s[0..X) with 256 threads, kPer columns each
   constexpr int kPer = kBinMaxCols / 256;
   int loc = 0;
 #pragma unroll
@@ -443,9 +530,10 @@ __global__ void __launch_bounds__(256) tile_scan_kernel(RowBinArgs a) {
     const int t = threadIdx.x * kPer + k;
     loc += t < X ? tot_s[t] : 0;
   }
-  int excl;
+  int excl, excl_above;
   block_exclusive_scan(loc, &excl, scan_tot);
-  int base = row_start(a, ty, p) + excl;
+  const int row_base = block_exclusive_scan(above, &excl_above, scan_tot);
+  int base = row_base + excl;
 #pragma unroll
   for (int k = 0; k < kPer; ++k) {
     const int t = threadIdx.x * kPer + k;
@@ -457,76 +545,64 @@ __global__ void __launch_bounds__(256) tile_scan_kernel(RowBinArgs a) {
   if (ty == a.tiles_y - 1 && threadIdx.x == 0) a.tile_starts[a.tiles_y * X] = p;
 }
 
-// Column pass 3: per chunk, every pair to tile_starts[tile] + the chunk's
-// prefix for its column + its rank among the chunk's earlier pairs of that
-// column (warp sub-ranges in order, match_any within a warp): a stable
-// counting sort, so each tile list keeps generation (depth rank) order and
-// equals np.lexsort((index, depth, tile)) (rasterizer.py:318-323).
-constexpr int kScatterItems = kBinChunk / 256;  // 16 pairs per lane
-__global__ void __launch_bounds__(256) tile_scatter_kernel(RowBinArgs a) {
-  extern __shared__ int wcnt[];  // [8][tiles_x]
+// Fill pass 3: per chunk (one warp), the values of the segments covering each tile
+// column L of the key's block are appended, in segment (= depth rank) order, at
+// tile_starts[tile] + the chunk's prefix: a stable counting sort by tile, so each
+// tile list equals np.lexsort((index, depth, tile)) (rasterizer.py:318-323).  The
+// warp holds 32 segments (one per lane) and walks the block's columns: a ballot
+// says which segments cover column L, and the covering lanes store their values
+// at consecutive positions of tile L's list -- one coalesced store per column
+// instead of one scattered store per pair.
+__global__ void __launch_bounds__(256) seg_fill_kernel(RowBinArgs a) {
   long long p64;
   if (bin_overflowed(a, &p64)) return;
-  int ty, begin, end;
-  if (!chunk_of(a, (int)p64, blockIdx.x, &ty, &begin, &end)) return;
-  const int X = a.tiles_x;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
-  const int sub = begin + w * (kBinChunk / 8);
-  int tx[kScatterItems];
-  uint32_t val[kScatterItems];
-#pragma unroll
-  for (int k = 0; k < kScatterItems; ++k) {
-    const int idx = sub + k * 32 + lane;
-    const bool in = idx < end;
-    tx[k] = in ? (int)a.tx_row[idx] : -1;
-    val[k] = in ? a.val_row[idx] : 0u;
-  }
-  for (int e = threadIdx.x; e < 8 * X; e += 256) wcnt[e] = 0;
-  __syncthreads();
-  int* cur = wcnt + w * X;
-#pragma unroll
-  for (int k = 0; k < kScatterItems; ++k) {
-    const unsigned peers = __match_any_sync(0xffffffffu, tx[k]);
-    if (tx[k] >= 0 && lane == __ffs(peers) - 1) cur[tx[k]] += __popc(peers);
-    __syncwarp();
-  }
-  __syncthreads();
-  const int32_t* hrow = a.hist + (int64_t)blockIdx.x * X;
-  const int32_t* ts = a.tile_starts + ty * X;
-  for (int t = threadIdx.x; t < X; t += 256) {
-    int base = ts[t] + hrow[t];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int v = wcnt[q * X + t];
-      wcnt[q * X + t] = base;
-      base += v;
+  const int c = blockIdx.x * 8 + (threadIdx.x >> 5);
+  int key, begin, end;
+  if (!seg_chunk_of(a, (int)p64, c, &key, &begin, &end)) return;
+  const int ty = key / a.nblk, tx = (key - ty * a.nblk) * kSegCols + lane;
+  int base = tx < a.tiles_x ? a.tile_starts[ty * a.tiles_x + tx] +
+                                  a.seg_cnt[(int64_t)c * 32 + lane]
+                            : 0;
+  for (int s0 = begin; s0 < end; s0 += 32) {
+    const uint2 sg = s0 + lane < end ? a.segs[s0 + lane] : make_uint2(0u, 0u);
+    const int lo = (int)(sg.y & 31u), len = (int)(sg.y >> 5);
+    // columns any of the 32 segments covers
+    const unsigned span = len ? (0xffffffffu >> (32 - len)) << lo : 0u;
+    unsigned cols = __reduce_or_sync(0xffffffffu, span);
+    const int m = min(32, end - s0);
+    if (__popc(cols) > m + (m >> 1)) {
+      // narrow segments (small splats): one pass per segment is shorter, each lane
+      // storing for its own column when the segment covers it
+      for (int k = 0; k < m; ++k) {
+        const unsigned sk = __shfl_sync(0xffffffffu, span, k);
+        const uint32_t vk = __shfl_sync(0xffffffffu, sg.x, k);
+        if ((sk >> lane) & 1u) a.pair_src[base++] = vk;
+      }
+      continue;
     }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int k = 0; k < kScatterItems; ++k) {
-    const unsigned peers = __match_any_sync(0xffffffffu, tx[k]);
-    const bool live = tx[k] >= 0;
-    const int pos = live ? cur[tx[k]] + __popc(peers & lt) : 0;
-    __syncwarp();
-    if (live && lane == __ffs(peers) - 1) cur[tx[k]] += __popc(peers);
-    __syncwarp();
-    if (live) a.pair_src[pos] = val[k];
+    while (cols) {
+      const int L = __ffs(cols) - 1;
+      cols &= cols - 1;
+      const unsigned m = __ballot_sync(0xffffffffu, (span >> L) & 1u);
+      const int b = __shfl_sync(0xffffffffu, base, L);
+      if ((span >> L) & 1u) a.pair_src[b + __popc(m & lt)] = sg.x;
+      if (lane == L) base += __popc(m);
+    }
   }
 }
 
 cudaError_t run_row_binning(const RowBinArgs& a, cudaStream_t stream) {
-  const unsigned chunks = (unsigned)bin_chunk_capacity(a.capacity, a.tiles_y);
-  // the attribute is set once per device: set it for the largest image the path takes
-  cudaError_t e = set_dynamic_smem<row_emit_kernel>(8 * kBinMaxRows * (int)sizeof(int));
+  const int64_t chunks = bin_chunk_capacity(a.capacity, a.keys);
+  const unsigned fill_grid = (unsigned)((chunks + 7) / 8);
+  // the attribute is set once per device: set it for the largest key count
+  cudaError_t e = set_dynamic_smem<seg_emit_kernel>(8 * kBinMaxKeys * (int)sizeof(int));
   if (e != cudaSuccess) return e;
-  e = set_dynamic_smem<tile_scatter_kernel>(8 * kBinMaxCols * (int)sizeof(int));
-  if (e != cudaSuccess) return e;
-  row_emit_kernel<<<(unsigned)a.nb, kBinRanks, 8 * a.tiles_y * sizeof(int), stream>>>(a);
-  tile_hist_kernel<<<chunks, 256, a.tiles_x * sizeof(int), stream>>>(a);
+  seg_emit_kernel<<<(unsigned)a.nb, kBinRanks, 8 * a.keys * sizeof(int), stream>>>(a);
+  seg_count_kernel<<<fill_grid, 256, 0, stream>>>(a);
   tile_scan_kernel<<<(unsigned)a.tiles_y, 256, 0, stream>>>(a);
-  tile_scatter_kernel<<<chunks, 256, 8 * a.tiles_x * sizeof(int), stream>>>(a);
+  seg_fill_kernel<<<fill_grid, 256, 0, stream>>>(a);
   note_launch(4);
   return cudaGetLastError();
 }

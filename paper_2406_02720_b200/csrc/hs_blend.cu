@@ -486,6 +486,15 @@ __global__ void HS_FWD_BOUNDS blend_fwd_kernel(
         terminal[o] = (int32_t)slot(P.C[p], h);
       }
     }
+    if (g.tile_work) {
+      // the backward's work on this tile: its largest terminal count (K6 walks
+      // positions maxc-1 .. 0), for K6's longest-first tile order
+      float mc = 0.f;
+#pragma unroll
+      for (int p = 0; p < kPairs; ++p) mc = fmaxf(mc, fmaxf(P.C[p].x, P.C[p].y));
+      mc = __reduce_max_sync(0xffffffffu, (int)mc);
+      if (lane == 0) g.tile_work[tile] = (int32_t)mc;
+    }
   }
 }
 
@@ -948,6 +957,65 @@ __global__ void mark_steep_pairs_kernel(const uint8_t* __restrict__ steep_flag,
                                         uint32_t* __restrict__ pairs, int64_t p) {
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k < p && steep_flag[pairs[k]]) pairs[k] |= kSteepBit;
+}
+
+// Longest-first tile order for the persistent blends (LPT): one CTA buckets the
+// tiles by their work estimate -- the list length from tile_starts for K5, K5's
+// largest terminal count per tile for K6 -- into 256 buckets, longest first, so
+// the long tiles start first and the queue's tail holds short ones.  Order within
+// a bucket is arbitrary: every tile's result is independent of when it runs.
+__global__ void __launch_bounds__(1024) tile_order_kernel(const int32_t* __restrict__ starts,
+                                                          const int32_t* __restrict__ work,
+                                                          int n_tiles,
+                                                          int32_t* __restrict__ order) {
+  __shared__ int off[256];
+  __shared__ int wmax;
+  // (clamped: a K6 whose frame never ran K5 orders arbitrary values -- still a
+  // permutation, so still correct)
+  auto w_of = [&](int t) {
+    return min(max(starts ? starts[t + 1] - starts[t] : work[t], 0), 1 << 30);
+  };
+  if (threadIdx.x == 0) wmax = 0;
+  if (threadIdx.x < 256) off[threadIdx.x] = 0;
+  __syncthreads();
+  int m = 0;
+  for (int t = threadIdx.x; t < n_tiles; t += 1024) m = max(m, w_of(t));
+  m = __reduce_max_sync(0xffffffffu, m);
+  if ((threadIdx.x & 31) == 0) atomicMax(&wmax, m);
+  __syncthreads();
+  const int shift = max(0, 24 - __clz(wmax));  // (w >> shift) < 256
+  auto bucket = [&](int t) { return 255 - (w_of(t) >> shift); };
+  for (int t = threadIdx.x; t < n_tiles; t += 1024) atomicAdd(&off[bucket(t)], 1);
+  __syncthreads();
+  if (threadIdx.x < 32) {  // exclusive scan of the 256 bucket sizes, 8 per lane
+    int v[8], s = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      v[k] = off[threadIdx.x * 8 + k];
+      s += v[k];
+    }
+    int incl = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int x = __shfl_up_sync(0xffffffffu, incl, o);
+      if (threadIdx.x >= o) incl += x;
+    }
+    int e = incl - s;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      off[threadIdx.x * 8 + k] = e;
+      e += v[k];
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < n_tiles; t += 1024) order[atomicAdd(&off[bucket(t)], 1)] = t;
+}
+
+cudaError_t launch_tile_order(const int32_t* starts, const int32_t* work, int n_tiles,
+                              int32_t* order, cudaStream_t stream) {
+  tile_order_kernel<<<1, 1024, 0, stream>>>(starts, work, n_tiles, order);
+  note_launch();
+  return cudaGetLastError();
 }
 
 // Persistent grid: resident CTAs per SM x SMs of that kernel (queried once).

@@ -5,6 +5,7 @@
 #include <mutex>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -47,7 +48,7 @@ struct Carver {
 };
 
 // counters[]: 0 K5 tile queue, 32 K6 tile queue, 48 depth-fixup overflow flag,
-// 52-55 the binning status (BinStatusDev: P as int64, flags)
+// 52-57 the binning status (BinStatusDev: P and segments as int64, flags)
 constexpr int kDepthOverflowSlot = 48;
 constexpr int kBinStatusSlot = 52;
 
@@ -70,6 +71,10 @@ struct FrameBufs {
   int32_t* xlocal;
   float4* merged;
   int32_t* chunk_first;
+  int32_t* row_pairs;
+  int32_t* order_fwd;   // longest-first tile orders of K5 / K6
+  int32_t* order_bwd;
+  int32_t* tile_work;   // K5 -> K6: per-tile largest terminal count
   BinStatusDev* status;
   void* temp;
   size_t temp_bytes;
@@ -113,7 +118,7 @@ static FrameBufs carve_frame(void* ws, int64_t n, int tiles_x, int tiles_y, size
   FrameBufs f;
   const int n_tiles = tiles_x * tiles_y;
   const bool rows = row_binning_ok(tiles_x, tiles_y);
-  const int64_t scan_len = count_scan_len(n, tiles_y, rows);
+  const int64_t scan_len = count_scan_len(n, seg_keys(tiles_x, tiles_y), rows);
   f.rec = c.take<float4>(4 * (size_t)n);
   f.side = c.take<SteepRec>(n);
   f.rect = c.take<int4>(n);
@@ -131,7 +136,11 @@ static FrameBufs carve_frame(void* ws, int64_t n, int tiles_x, int tiles_y, size
   f.xflags = c.take<int32_t>(n + 1);
   f.xlocal = c.take<int32_t>(n + 1);
   f.merged = c.take<float4>(4 * (size_t)n);
-  f.chunk_first = c.take<int32_t>(tiles_y + 1);
+  f.chunk_first = c.take<int32_t>(seg_keys(tiles_x, tiles_y) + 1);
+  f.row_pairs = c.take<int32_t>(tiles_y);
+  f.order_fwd = c.take<int32_t>(n_tiles);
+  f.order_bwd = c.take<int32_t>(n_tiles);
+  f.tile_work = c.take<int32_t>(n_tiles);
   f.status = reinterpret_cast<BinStatusDev*>(f.counters ? f.counters + kBinStatusSlot : nullptr);
   f.temp_bytes = frame_temp_bytes(n, scan_len);
   f.temp = c.take<char>(f.temp_bytes);
@@ -145,10 +154,9 @@ static FrameBufs carve_frame(void* ws, int64_t n, int tiles_x, int tiles_y, size
 struct BinBufs {
   uint32_t* keys[2];
   uint32_t* vals[2];
-  uint16_t* tx_row;
-  uint32_t* val_row;
+  uint2* segs;
   uint32_t* pair_src;
-  int32_t* hist;
+  int32_t* seg_cnt;
   float* rows;
   void* temp;
   size_t temp_bytes;
@@ -159,10 +167,9 @@ static BinBufs carve_bin(void* ws, int64_t p, int tiles_x, int tiles_y, size_t* 
   BinBufs b{};
   const size_t pp = p > 0 ? (size_t)p : 1;
   if (row_binning_ok(tiles_x, tiles_y)) {
-    b.tx_row = c.take<uint16_t>(pp);
-    b.val_row = c.take<uint32_t>(pp);
+    b.segs = c.take<uint2>(pp);
     b.pair_src = c.take<uint32_t>(pp);
-    b.hist = c.take<int32_t>((size_t)bin_chunk_capacity(p, tiles_y) * tiles_x);
+    b.seg_cnt = c.take<int32_t>((size_t)bin_chunk_capacity(p, seg_keys(tiles_x, tiles_y)) * 32);
   } else {
     int bits = 0;
     while ((1ll << bits) < (long long)tiles_x * tiles_y) ++bits;
@@ -346,9 +353,10 @@ size_t hs_binning_workspace_size(int64_t n, int64_t num_pairs, int32_t width, in
 }
 
 static cudaError_t count_scan(const hs_frame* frame, const FrameBufs& f, cudaStream_t stream) {
-  const bool rows = row_binning_ok(frame->tiles_x, frame->tiles_y);
+  const bool segs = row_binning_ok(frame->tiles_x, frame->tiles_y);
   return run_count_scan(f.temp, f.temp_bytes, f.count, f.order, f.rect, f.cnt_r, f.off_r,
-                        f.rank_of, frame->n, rows ? frame->tiles_y : 0, f.status, stream);
+                        f.rank_of, frame->n, segs ? frame->tiles_x : 0, frame->tiles_y,
+                        f.row_pairs, f.status, stream);
 }
 
 int hs_preprocess_fwd(hs_frame* frame, const hs_scene* scene, const hs_camera* cam,
@@ -463,15 +471,17 @@ static int row_bin(hs_frame* frame, const FrameBufs& f, const BinBufs& b, cudaSt
   a.cnt_r = f.cnt_r;
   a.off_r = f.off_r;
   a.status = f.status;
+  a.row_pairs = f.row_pairs;
   a.n = frame->n;
   a.nb = (int)bin_row_blocks(frame->n);
   a.tiles_x = frame->tiles_x;
   a.tiles_y = frame->tiles_y;
+  a.nblk = seg_blocks(frame->tiles_x);
+  a.keys = seg_keys(frame->tiles_x, frame->tiles_y);
   a.capacity = bin_capacity(frame);
-  a.tx_row = b.tx_row;
-  a.val_row = b.val_row;
+  a.segs = b.segs;
   a.chunk_first = f.chunk_first;
-  a.hist = b.hist;
+  a.seg_cnt = b.seg_cnt;
   a.tile_starts = f.tile_starts;
   a.pair_src = b.pair_src;
   HS_CUDA(run_row_binning(a, stream));
@@ -526,6 +536,15 @@ static int64_t pairs_hint(const hs_frame* frame) {
   return frame->num_pairs >= 0 ? frame->num_pairs : bin_capacity(frame) * 4 / 5;
 }
 
+// Longest-first tile order for the blends (HS_LPT=0 turns it off).
+static bool lpt_order() {
+  static const bool on = [] {
+    const char* e = getenv("HS_LPT");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 static BlendGeom frame_geom(const hs_frame* frame, const FrameBufs& f, const BinBufs& b) {
   BlendGeom g;
   g.tile_starts = f.tile_starts;
@@ -538,6 +557,7 @@ static BlendGeom frame_geom(const hs_frame* frame, const FrameBufs& f, const Bin
   g.tile_lo = 0;
   g.n_work = frame->n_tiles;
   g.tile_order = nullptr;
+  g.tile_work = nullptr;
   g.work_counter = f.counters;
   return g;
 }
@@ -551,8 +571,14 @@ int hs_blend_fwd(hs_frame* frame, const double* bg, float* color, float* alpha, 
   FrameBufs f = frame_bufs(frame);
   BinBufs b = frame_bin(frame);
   BlendGeom g = frame_geom(frame, f, b);
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  g.tile_work = f.tile_work;
+  if (lpt_order()) {
+    HS_CUDA(launch_tile_order(f.tile_starts, nullptr, frame->n_tiles, f.order_fwd, stream));
+    g.tile_order = f.order_fwd;
+  }
   HS_CUDA(launch_blend_fwd(g, (float)bg[0], (float)bg[1], (float)bg[2], color, alpha, depth,
-                           transmittance, terminal, static_cast<cudaStream_t>(stream_)));
+                           transmittance, terminal, stream));
   return HS_OK;
 }
 
@@ -566,9 +592,14 @@ int hs_blend_bwd(hs_frame* frame, const double* bg, const float* d_color,
   BinBufs b = frame_bin(frame);
   BlendGeom g = frame_geom(frame, f, b);
   g.work_counter = f.counters + 32;
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  if (lpt_order()) {
+    // K5 left each tile's largest terminal count: the positions K6 walks
+    HS_CUDA(launch_tile_order(nullptr, f.tile_work, frame->n_tiles, f.order_bwd, stream));
+    g.tile_order = f.order_bwd;
+  }
   HS_CUDA(launch_blend_bwd(g, (float)bg[0], (float)bg[1], (float)bg[2], d_color, transmittance,
-                           terminal, b.rows, f.last_rank, f.rank_of, false,
-                           static_cast<cudaStream_t>(stream_)));
+                           terminal, b.rows, f.last_rank, f.rank_of, false, stream));
   return HS_OK;
 }
 
@@ -722,6 +753,7 @@ int hs_forward_tiles(const double* packed, const int8_t* mode, const int32_t* pa
   g.tile_lo = tile_lo;
   g.n_work = tile_hi - tile_lo;
   g.tile_order = nullptr;
+  g.tile_work = nullptr;
   g.work_counter = (int*)d_ctr.p;
   float* o = (float*)d_out.p;
   HS_CUDA(launch_blend_fwd(g, (float)bg[0], (float)bg[1], (float)bg[2], o, o + 3 * npx,
@@ -795,6 +827,7 @@ int hs_backward_tiles(const double* packed, const int8_t* mode, const int32_t* p
   g.tile_lo = tile_lo;
   g.n_work = tile_hi - tile_lo;
   g.tile_order = nullptr;
+  g.tile_work = nullptr;
   g.work_counter = (int*)d_ctr.p;
   const float* in = (const float*)d_in.p;
   HS_CUDA(launch_blend_bwd(g, (float)bg[0], (float)bg[1], (float)bg[2], in, in + 3 * npx,

@@ -74,7 +74,11 @@ struct BlendGeom {
   int tile_lo, n_work;         // tiles [tile_lo, tile_lo + n_work)
   const int32_t* tile_order;   // optional work order (nullptr = natural)
   int* work_counter;           // zeroed before launch
+  int32_t* tile_work;          // optional (K5): per-tile largest terminal count
 };
+// longest-first tile order: work = list length (starts != nullptr) or work[t]
+cudaError_t launch_tile_order(const int32_t* starts, const int32_t* work, int n_tiles,
+                              int32_t* order, cudaStream_t stream);
 
 cudaError_t launch_blend_fwd(const BlendGeom& g, float bg0, float bg1, float bg2, float* color,
                              float* alpha, float* depth, float* trans, int32_t* terminal,
@@ -108,43 +112,58 @@ cudaError_t run_depth_sort_hi(void* temp, size_t temp_bytes, const uint64_t* key
                               int64_t n, uint32_t* scratch_pos, uint32_t* scratch_val,
                               int* overflow, cudaStream_t stream);
 // ---- tile binning without a host round trip -------------------
-// The count pass also histograms every block of kBinRanks depth ranks' pairs by
-// tile row; the emit pass writes each pair straight into its row bucket (rank
-// order within the row, so stable); the column passes counting-sort every row
-// bucket by tile column in chunks of kBinChunk pairs.  P stays on the device: the
-// caller sizes the binning workspace for a pair capacity, and a frame whose P
-// exceeds it is flagged (kBinFlagOverflow) with every tile list left empty.
+// A splat's pairs in one tile row and one block of 32 tile columns form a
+// SEGMENT (value, first column, length).  The count pass histograms every block
+// of kBinRanks depth ranks' segments by (tile row, column block) key and its pairs
+// by tile row; the emit pass writes each segment straight into its key's bucket
+// (rank order within the key, so stable); the fill passes give each warp a chunk
+// of one bucket, lane L = tile column L of the block, and every lane appends the
+// values of the segments that cover it -- a stable counting sort by tile whose
+// per-pair cost is one predicated store.  P stays on the device: the caller sizes
+// the binning workspace for a pair capacity, and a frame whose P exceeds it is
+// flagged (kBinFlagOverflow) with every tile list left empty.
 constexpr int kBinRanks = 256;
-constexpr int kBinMaxRows = 1024;  // tiles_y limit of the row-bucket path
-constexpr int kBinMaxCols = 2048;  // tiles_x limit (larger images: CUB pair sort)
-constexpr int kBinChunk = 4096;    // 256 threads x 16 pairs
+constexpr int kSegCols = 32;        // tile columns per block (one warp's lanes)
+constexpr int kBinMaxCols = 2048;   // tiles_x limit (larger images: CUB pair sort)
+constexpr int kBinMaxRows = 1024;   // tiles_y limit
+constexpr int kBinMaxKeys = 2048;   // tile rows x column blocks limit
+#ifndef HS_SEG_CHUNK
+#define HS_SEG_CHUNK 256
+#endif
+constexpr int kSegChunk = HS_SEG_CHUNK;  // segments per warp in the fill passes
 constexpr int kBinFlagOverflow = 1;
-constexpr int kBinFlagDepth = 2;   // the depth-run fixup overflowed: ranks need the full sort
+constexpr int kBinFlagDepth = 2;    // the depth-run fixup overflowed: ranks need the full sort
+inline int seg_blocks(int tiles_x) { return (tiles_x + kSegCols - 1) / kSegCols; }
+inline int seg_keys(int tiles_x, int tiles_y) { return tiles_y * seg_blocks(tiles_x); }
 inline bool row_binning_ok(int tiles_x, int tiles_y) {
-  return tiles_x <= kBinMaxCols && tiles_y <= kBinMaxRows;
+  return tiles_x <= kBinMaxCols && tiles_y <= kBinMaxRows &&
+         seg_keys(tiles_x, tiles_y) <= kBinMaxKeys;
 }
 inline int64_t bin_row_blocks(int64_t n) { return (n + kBinRanks - 1) / kBinRanks; }
-inline int64_t bin_chunk_capacity(int64_t capacity, int tiles_y) {
-  return capacity / kBinChunk + tiles_y + 1;
+inline int64_t bin_chunk_capacity(int64_t capacity, int keys) {
+  return capacity / kSegChunk + keys + 1;
 }
-// scan entries of the count pass: pair counts by rank (n + 1), then, with the row
-// path, the row histograms [tiles_y][row blocks]
-inline int64_t count_scan_len(int64_t n, int tiles_y, bool rows) {
-  return n + 1 + (rows ? (int64_t)tiles_y * bin_row_blocks(n) : 0);
+// scan entries of the count pass: pair counts by rank (n + 1), then, with the
+// segment path, the segment histograms [key][rank block]
+inline int64_t count_scan_len(int64_t n, int keys, bool rows) {
+  return n + 1 + (rows ? (int64_t)keys * bin_row_blocks(n) : 0);
 }
 struct BinStatusDev {   // in the frame's counters
   long long pairs;      // P as int64 (the int32 scan may wrap)
+  long long segs;       // segments
   int flags;
   int pad;
 };
 
 // cnt_r[r] = count[order[r]], off_r = exclusive scan (count_scan_len entries),
-// rank_of[order[r]] = r; with tiles_y > 0 also the row histograms and P as int64
-// in *status (zeroed here).
+// rank_of[order[r]] = r, P as int64 in *status (zeroed here); with the segment
+// path (tiles_x > 0) also the segment histograms and row_pairs[tiles_y] (pairs per
+// tile row, zeroed here).
 cudaError_t run_count_scan(void* temp, size_t temp_bytes, const int32_t* count,
                            const uint32_t* order, const int4* rect, int32_t* cnt_r,
-                           int32_t* off_r, uint32_t* rank_of, int64_t n, int tiles_y,
-                           BinStatusDev* status, cudaStream_t stream);
+                           int32_t* off_r, uint32_t* rank_of, int64_t n, int tiles_x,
+                           int tiles_y, int32_t* row_pairs, BinStatusDev* status,
+                           cudaStream_t stream);
 struct RowBinArgs {
   const uint32_t* order;
   const int4* rect;
@@ -152,14 +171,14 @@ struct RowBinArgs {
   const int32_t* cnt_r;
   const int32_t* off_r;
   BinStatusDev* status;
+  const int32_t* row_pairs;  // [tiles_y]
   int64_t n;
-  int nb;  // row blocks
-  int tiles_x, tiles_y;
+  int nb;  // rank blocks
+  int tiles_x, tiles_y, nblk, keys;
   int64_t capacity;
-  uint16_t* tx_row;      // [capacity] row buckets: tile column
-  uint32_t* val_row;     // [capacity] row buckets: index | steep
-  int32_t* chunk_first;  // [tiles_y + 1]
-  int32_t* hist;         // [chunk capacity][tiles_x]
+  uint2* segs;           // [capacity] buckets: (index | steep, first column | length << 5)
+  int32_t* chunk_first;  // [keys + 1]
+  int32_t* seg_cnt;      // [chunk capacity][32]
   int32_t* tile_starts;  // [n_tiles + 1]
   uint32_t* pair_src;    // [capacity] final order
 };

@@ -85,11 +85,12 @@ class Workspace:
         self.generation = 0
         self._status_host = None
         self.depth_sort_full = 0  # sticky once a view needed the full depth sort
+        self.capturing = False    # inside a CUDA-graph capture (CapturedStep)
 
     def status_buffer(self):
-        """Pinned host memory for hs_frame_status_async (3 int64 words)."""
+        """Pinned host memory for hs_frame_status_async (4 int64 words)."""
         if self._status_host is None:
-            self._status_host = torch.zeros(3, dtype=torch.int64, pin_memory=True)
+            self._status_host = torch.zeros(4, dtype=torch.int64, pin_memory=True)
         return self._status_host
 
     def check_previous(self):
@@ -103,7 +104,7 @@ class Workspace:
             return
         event, host, frame = pend
         event.synchronize()
-        p, flags, depth = int(host[0]), int(host[1]) & 0xffffffff, int(host[2]) & 0xffffffff
+        p, flags, depth = int(host[0]), int(host[2]) & 0xffffffff, int(host[3]) & 0xffffffff
         frame._status_seen(p, flags, depth)
         if flags or depth:
             raise BinningOverflow(
@@ -314,7 +315,7 @@ def prepare(scene, cam, kernel="half", timer=None, ws=None):
     scene = Scene.from_any(scene)
     cam = CameraModel.from_any(cam)
     _validate(scene, cam, kernel)
-    if ws is not None:
+    if ws is not None and not ws.capturing:
         ws.check_previous()
     frame = DeviceFrame(scene, cam, kernel, ws)
     lib = frame.lib
@@ -341,9 +342,10 @@ def prepare(scene, cam, kernel="half", timer=None, ws=None):
             _native.check(lib.hs_frame_status_async(ctypes.byref(frame.st),
                                                     ctypes.c_void_p(pinned.data_ptr()), s),
                           "hs_frame_status_async")
-            ev = torch.cuda.Event()
-            ev.record()
-            ws.pending = (ev, pinned, frame)
+            if not ws.capturing:  # a graph replays the copy; CapturedStep.check reads it
+                ev = torch.cuda.Event()
+                ev.record()
+                ws.pending = (ev, pinned, frame)
         return frame
     # first view of this workspace (or no workspace): read P (a host sync), size the
     # binning workspace with headroom, then bin
@@ -519,6 +521,48 @@ def grads_struct(grads, accumulate=0):
         setattr(g, name, getattr(grads, name).data_ptr())
     g.accumulate = accumulate
     return g
+
+
+class CapturedStep:
+    """A steady-state step (e.g. Rasterizer render + render_backward of fixed views)
+    captured once as a CUDA graph and replayed: one launch for the whole step, no
+    per-kernel host work.  Possible because binning needs no host round trip
+    (hs_bin_async): `fn` runs eagerly `warmup` times first, which sizes every
+    workspace (pair capacities, cached attributes), then once under capture.
+    The binning status of each replay lands in the workspaces' pinned status words;
+    check() (after a synchronisation) raises BinningOverflow if a replayed view ever
+    outgrew its capacity.  The captured buffers must not be reallocated afterwards:
+    replay only while the scene and views keep their sizes."""
+
+    def __init__(self, fn, workspaces, warmup=2):
+        self.workspaces = list(workspaces)
+        for _ in range(max(1, warmup)):
+            fn()
+        torch.cuda.synchronize()
+        for ws in self.workspaces:
+            ws.check_previous()
+            ws.status_buffer().zero_()
+        self.graph = torch.cuda.CUDAGraph()
+        for ws in self.workspaces:
+            ws.capturing = True
+        try:
+            with torch.cuda.graph(self.graph):
+                fn()
+        finally:
+            for ws in self.workspaces:
+                ws.capturing = False
+
+    def replay(self):
+        self.graph.replay()
+
+    def check(self):
+        """Call after synchronising: the status of the last replay of every view."""
+        for ws in self.workspaces:
+            host = ws.status_buffer()
+            flags, depth = int(host[2]) & 0xffffffff, int(host[3]) & 0xffffffff
+            if flags or depth:
+                raise BinningOverflow(f"a replayed view overflowed its binning workspace "
+                                      f"(P={int(host[0])}, capacity {ws.pair_capacity})")
 
 
 class Rasterizer:
