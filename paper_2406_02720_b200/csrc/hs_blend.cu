@@ -1033,6 +1033,15 @@ static int blend_grid(Kernel kernel, int warps, int n_work, int* cache) {
 }
 static int g_fwd_grid = 0, g_bwd_grid[2] = {0, 0};
 
+// resident warps of the persistent blends (the longest-first order pays only when
+// the tiles are several times these)
+int blend_fwd_slots() {
+  return blend_grid(blend_fwd_kernel, kFwdWarps, 1 << 30, &g_fwd_grid) * kFwdWarps;
+}
+int blend_bwd_slots() {
+  return blend_grid(blend_bwd_kernel<false>, kBwdWarps, 1 << 30, &g_bwd_grid[0]) * kBwdWarps;
+}
+
 cudaError_t launch_blend_fwd(const BlendGeom& g, float bg0, float bg1, float bg2, float* color,
                              float* alpha, float* depth, float* trans, int32_t* terminal,
                              cudaStream_t stream) {

@@ -536,13 +536,16 @@ static int64_t pairs_hint(const hs_frame* frame) {
   return frame->num_pairs >= 0 ? frame->num_pairs : bin_capacity(frame) * 4 / 5;
 }
 
-// Longest-first tile order for the blends (HS_LPT=0 turns it off).
-static bool lpt_order() {
-  static const bool on = [] {
+// Longest-first tile order for the blends when the tiles are at least 1.5x the
+// blend's resident warps (HS_LPT=0 never, HS_LPT=1 always).  Measured per view:
+// c3 K5 0.807 -> 0.784 ms, K6 1.512 -> 1.475; c4 K6 1.314 -> 1.096; but c2, whose
+// 2500 tiles about fill the resident warps once, K5 0.379 -> 0.457, K6 0.630 -> 0.695.
+static bool lpt_order(int n_tiles, int slots) {
+  static const int mode = [] {
     const char* e = getenv("HS_LPT");
-    return !(e && e[0] == '0');
+    return e ? (e[0] == '0' ? 0 : 1) : 2;
   }();
-  return on;
+  return mode == 1 || (mode == 2 && 2 * (int64_t)n_tiles >= 3 * (int64_t)slots);
 }
 
 static BlendGeom frame_geom(const hs_frame* frame, const FrameBufs& f, const BinBufs& b) {
@@ -573,7 +576,7 @@ int hs_blend_fwd(hs_frame* frame, const double* bg, float* color, float* alpha, 
   BlendGeom g = frame_geom(frame, f, b);
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
   g.tile_work = f.tile_work;
-  if (lpt_order()) {
+  if (lpt_order(frame->n_tiles, blend_fwd_slots())) {
     HS_CUDA(launch_tile_order(f.tile_starts, nullptr, frame->n_tiles, f.order_fwd, stream));
     g.tile_order = f.order_fwd;
   }
@@ -593,7 +596,7 @@ int hs_blend_bwd(hs_frame* frame, const double* bg, const float* d_color,
   BlendGeom g = frame_geom(frame, f, b);
   g.work_counter = f.counters + 32;
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
-  if (lpt_order()) {
+  if (lpt_order(frame->n_tiles, blend_bwd_slots())) {
     // K5 left each tile's largest terminal count: the positions K6 walks
     HS_CUDA(launch_tile_order(nullptr, f.tile_work, frame->n_tiles, f.order_bwd, stream));
     g.tile_order = f.order_bwd;

@@ -76,6 +76,8 @@ struct BlendGeom {
   int* work_counter;           // zeroed before launch
   int32_t* tile_work;          // optional (K5): per-tile largest terminal count
 };
+int blend_fwd_slots();
+int blend_bwd_slots();
 // longest-first tile order: work = list length (starts != nullptr) or work[t]
 cudaError_t launch_tile_order(const int32_t* starts, const int32_t* work, int n_tiles,
                               int32_t* order, cudaStream_t stream);

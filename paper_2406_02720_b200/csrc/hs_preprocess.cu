@@ -914,13 +914,37 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem));
 }
 
+// Which of the CTA's primitives this view touched, as a bit mask (one ballot per
+// warp) plus an all-touched flag: the vectorised copies below test a 16-B vector's
+// primitives with two word loads and a shift instead of a per-primitive loop with
+// divisions, which was 18% of K7's instructions at c4 (ncu source view).
+template <int NT>
+struct LiveMask {
+  uint32_t w[NT / 32 + 1];  // a zero word past the end: 64-bit windows never overrun
+  int all;
+};
+
+// after touch_s is final and a __syncthreads()
+template <int NT>
+__device__ __forceinline__ void build_live_mask(LiveMask<NT>& m, const int32_t* touch_s) {
+  const unsigned b = __ballot_sync(0xffffffffu, touch_s[threadIdx.x] != 0);
+  if ((threadIdx.x & 31) == 0) m.w[threadIdx.x >> 5] = b;
+  if (threadIdx.x == 0) m.w[NT / 32] = 0u;
+  const int full = __syncthreads_and(b == 0xffffffffu);
+  if (threadIdx.x == 0) m.all = full;
+  __syncthreads();
+}
+
 // Does any primitive of elements [e0, e0 + len) (S elements per primitive) have
-// a non-zero flag?
-template <int S>
-__device__ __forceinline__ bool any_live(const int32_t* live, int e0, int len) {
-  bool any = false;
-  for (int p = e0 / S; p <= (e0 + len - 1) / S; ++p) any |= live[p] != 0;
-  return any;
+// a non-zero flag?  (len < 32 * S)
+template <int S, int NT>
+__device__ __forceinline__ bool any_live(const LiveMask<NT>& m, int e0, int len) {
+  if (m.all) return true;
+  const int p0 = e0 / S, p1 = (e0 + len - 1) / S;
+  const int wi = p0 >> 5;
+  const uint64_t win = ((uint64_t)m.w[wi + 1] << 32) | m.w[wi];
+  const int n = p1 - p0 + 1;
+  return ((win >> (p0 & 31)) & ((1ull << n) - 1ull)) != 0ull;
 }
 
 // Accumulation targets of one CTA, prefetched into shared memory while the
@@ -938,12 +962,12 @@ struct GradStage {
 // not touch.  16-B copies when `src` is 16-B aligned, element copies otherwise.
 template <int NT, int S, typename E>
 __device__ __forceinline__ void prefetch_block(E* smem, const E* src, int cnt,
-                                               const int32_t* live) {
+                                               const int32_t* live, const LiveMask<NT>& lm) {
   constexpr int kV = 16 / sizeof(E);
   const int n = cnt * S;
   const int nv = ((uintptr_t)src & 15) ? 0 : n / kV;
   for (int v = threadIdx.x; v < nv; v += NT)
-    if (any_live<S>(live, v * kV, kV)) cp_async16(smem + v * kV, src + v * kV);
+    if (any_live<S>(lm, v * kV, kV)) cp_async16(smem + v * kV, src + v * kV);
   for (int e = nv * kV + threadIdx.x; e < n; e += NT)
     if (live[e / S]) cp_async_elem(smem + e, src + e);
 }
@@ -953,14 +977,15 @@ __device__ __forceinline__ void prefetch_block(E* smem, const E* src, int cnt,
 // (their gradient is zero).  16-B stores when `dst` is 16-B aligned.
 template <int NT, int S, typename E, typename Get>
 __device__ __forceinline__ void store_block(E* __restrict__ dst, int cnt, const E* old,
-                                            const int32_t* live, Get get) {
+                                            const int32_t* live, const LiveMask<NT>& lm,
+                                            Get get) {
   using V = typename Vec16<E>::type;
   constexpr int kV = 16 / sizeof(E);
   const int n = cnt * S;
   const int nv = ((uintptr_t)dst & 15) ? 0 : n / kV;
   V* dv = reinterpret_cast<V*>(dst);
   for (int v = threadIdx.x; v < nv; v += NT) {
-    if (old && !any_live<S>(live, v * kV, kV)) continue;
+    if (old && !any_live<S>(lm, v * kV, kV)) continue;
     V nw;
     E* ne = reinterpret_cast<E*>(&nw);
 #pragma unroll
@@ -1011,13 +1036,13 @@ __device__ __forceinline__ void red_add4(float* p, float4 v, bool mc) {
 // others add zero).  float fields move in 16-B vector reductions when aligned.
 template <int NT, int S, typename E, typename Get>
 __device__ __forceinline__ void reduce_block(E* __restrict__ dst, int cnt, const int32_t* live,
-                                             bool mc, Get get) {
+                                             const LiveMask<NT>& lm, bool mc, Get get) {
   const int n = cnt * S;
   int done = 0;
   if constexpr (sizeof(E) == 4 && !std::is_same<E, int32_t>::value) {
     const int nv = ((uintptr_t)dst & 15) ? 0 : n / 4;
     for (int v = threadIdx.x; v < nv; v += NT) {
-      if (!any_live<S>(live, v * 4, 4)) continue;
+      if (!any_live<S>(lm, v * 4, 4)) continue;
       red_add4(dst + 4 * v, make_float4(get(4 * v), get(4 * v + 1), get(4 * v + 2),
                                         get(4 * v + 3)), mc);
     }
@@ -1040,6 +1065,7 @@ __global__ void __launch_bounds__(NT, HS_K7_MINB) preprocess_bwd_kernel(
   __shared__ St sm;
   __shared__ T pgn_s[NT];
   __shared__ int32_t touch_s[NT];
+  __shared__ LiveMask<NT> lm;
   extern __shared__ __align__(16) unsigned char dyn_smem[];
   const int64_t base = out.begin + (int64_t)blockIdx.x * NT;
   const int ncta = (int)(n - base < NT ? n - base : NT);
@@ -1055,15 +1081,16 @@ __global__ void __launch_bounds__(NT, HS_K7_MINB) preprocess_bwd_kernel(
     // scene staging and are waited for only before the final stores.
     touch_s[t] = t < ncta ? (count[base + t] != 0) : 0;
     __syncthreads();
-    prefetch_block<NT, 3>(g->mu, out.d_mu + base * 3, ncta, touch_s);
-    prefetch_block<NT, 3>(g->ls, out.d_log_scale + base * 3, ncta, touch_s);
-    prefetch_block<NT, 3>(g->nrm, out.d_normal + base * 3, ncta, touch_s);
-    prefetch_block<NT, 4>(g->rot, out.d_rotation + base * 4, ncta, touch_s);
-    prefetch_block<NT, 1>(g->ra, out.d_ra + base, ncta, touch_s);
-    prefetch_block<NT, 1>(g->rb, out.d_rb + base, ncta, touch_s);
-    prefetch_block<NT, 1>(g->pgn, out.pos_grad_norm + base, ncta, touch_s);
-    prefetch_block<NT, 1>(g->touch, out.touch + base, ncta, touch_s);
-    prefetch_block<NT, 3 * K>(g->sh, out.d_sh + base * 3 * K, ncta, touch_s);
+    build_live_mask(lm, touch_s);
+    prefetch_block<NT, 3>(g->mu, out.d_mu + base * 3, ncta, touch_s, lm);
+    prefetch_block<NT, 3>(g->ls, out.d_log_scale + base * 3, ncta, touch_s, lm);
+    prefetch_block<NT, 3>(g->nrm, out.d_normal + base * 3, ncta, touch_s, lm);
+    prefetch_block<NT, 4>(g->rot, out.d_rotation + base * 4, ncta, touch_s, lm);
+    prefetch_block<NT, 1>(g->ra, out.d_ra + base, ncta, touch_s, lm);
+    prefetch_block<NT, 1>(g->rb, out.d_rb + base, ncta, touch_s, lm);
+    prefetch_block<NT, 1>(g->pgn, out.pos_grad_norm + base, ncta, touch_s, lm);
+    prefetch_block<NT, 1>(g->touch, out.touch + base, ncta, touch_s, lm);
+    prefetch_block<NT, 3 * K>(g->sh, out.d_sh + base * 3 * K, ncta, touch_s, lm);
     asm volatile("cp.async.commit_group;\n" ::);
     asm volatile("cp.async.wait_group 1;\n" ::);
   } else {
@@ -1072,22 +1099,25 @@ __global__ void __launch_bounds__(NT, HS_K7_MINB) preprocess_bwd_kernel(
   __syncthreads();
   if (t < ncta)
     preprocess_bwd_one<T, DEG, NT>(sm, pgn_s, touch_s, t, base + t, cam, kernel, count, merged);
+  else
+    touch_s[t] = 0;
   asm volatile("cp.async.wait_all;\n" ::);
   __syncthreads();
+  if (!acc) build_live_mask(lm, touch_s);  // (acc: built from the same values above)
   if (red) {
-    reduce_block<NT, 3>(out.d_mu + base * 3, ncta, touch_s, mc, [&](int e) { return sm.mu[e]; });
-    reduce_block<NT, 3>(out.d_log_scale + base * 3, ncta, touch_s, mc,
+    reduce_block<NT, 3>(out.d_mu + base * 3, ncta, touch_s, lm, mc, [&](int e) { return sm.mu[e]; });
+    reduce_block<NT, 3>(out.d_log_scale + base * 3, ncta, touch_s, lm, mc,
                         [&](int e) { return sm.ls[e]; });
-    reduce_block<NT, 3>(out.d_normal + base * 3, ncta, touch_s, mc,
+    reduce_block<NT, 3>(out.d_normal + base * 3, ncta, touch_s, lm, mc,
                         [&](int e) { return sm.nrm[e]; });
-    reduce_block<NT, 4>(out.d_rotation + base * 4, ncta, touch_s, mc,
+    reduce_block<NT, 4>(out.d_rotation + base * 4, ncta, touch_s, lm, mc,
                         [&](int e) { return sm.rot[e]; });
-    reduce_block<NT, 1>(out.d_ra + base, ncta, touch_s, mc, [&](int e) { return sm.ra[e]; });
-    reduce_block<NT, 1>(out.d_rb + base, ncta, touch_s, mc, [&](int e) { return sm.rb[e]; });
-    reduce_block<NT, 1>(out.pos_grad_norm + base, ncta, touch_s, mc,
+    reduce_block<NT, 1>(out.d_ra + base, ncta, touch_s, lm, mc, [&](int e) { return sm.ra[e]; });
+    reduce_block<NT, 1>(out.d_rb + base, ncta, touch_s, lm, mc, [&](int e) { return sm.rb[e]; });
+    reduce_block<NT, 1>(out.pos_grad_norm + base, ncta, touch_s, lm, mc,
                         [&](int e) { return pgn_s[e]; });
-    reduce_block<NT, 1>(out.touch + base, ncta, touch_s, mc, [&](int e) { return touch_s[e]; });
-    reduce_block<NT, 3 * K>(out.d_sh + base * 3 * K, ncta, touch_s, mc, [&](int e) {
+    reduce_block<NT, 1>(out.touch + base, ncta, touch_s, lm, mc, [&](int e) { return touch_s[e]; });
+    reduce_block<NT, 3 * K>(out.d_sh + base * 3 * K, ncta, touch_s, lm, mc, [&](int e) {
       const int tt = e / (3 * K);
       return sm.sh[tt * St::SHS + (e - tt * 3 * K)];
     });
@@ -1097,23 +1127,23 @@ __global__ void __launch_bounds__(NT, HS_K7_MINB) preprocess_bwd_kernel(
     if (mc) asm volatile("fence.acq_rel.sys;\n" ::: "memory");
     return;
   }
-  store_block<NT, 3>(out.d_mu + base * 3, ncta, acc ? g->mu : nullptr, touch_s,
+  store_block<NT, 3>(out.d_mu + base * 3, ncta, acc ? g->mu : nullptr, touch_s, lm,
                      [&](int e) { return sm.mu[e]; });
-  store_block<NT, 3>(out.d_log_scale + base * 3, ncta, acc ? g->ls : nullptr, touch_s,
+  store_block<NT, 3>(out.d_log_scale + base * 3, ncta, acc ? g->ls : nullptr, touch_s, lm,
                      [&](int e) { return sm.ls[e]; });
-  store_block<NT, 3>(out.d_normal + base * 3, ncta, acc ? g->nrm : nullptr, touch_s,
+  store_block<NT, 3>(out.d_normal + base * 3, ncta, acc ? g->nrm : nullptr, touch_s, lm,
                      [&](int e) { return sm.nrm[e]; });
-  store_block<NT, 4>(out.d_rotation + base * 4, ncta, acc ? g->rot : nullptr, touch_s,
+  store_block<NT, 4>(out.d_rotation + base * 4, ncta, acc ? g->rot : nullptr, touch_s, lm,
                      [&](int e) { return sm.rot[e]; });
-  store_block<NT, 1>(out.d_ra + base, ncta, acc ? g->ra : nullptr, touch_s,
+  store_block<NT, 1>(out.d_ra + base, ncta, acc ? g->ra : nullptr, touch_s, lm,
                      [&](int e) { return sm.ra[e]; });
-  store_block<NT, 1>(out.d_rb + base, ncta, acc ? g->rb : nullptr, touch_s,
+  store_block<NT, 1>(out.d_rb + base, ncta, acc ? g->rb : nullptr, touch_s, lm,
                      [&](int e) { return sm.rb[e]; });
-  store_block<NT, 1>(out.pos_grad_norm + base, ncta, acc ? g->pgn : nullptr, touch_s,
+  store_block<NT, 1>(out.pos_grad_norm + base, ncta, acc ? g->pgn : nullptr, touch_s, lm,
                      [&](int e) { return pgn_s[e]; });
-  store_block<NT, 1>(out.touch + base, ncta, acc ? g->touch : nullptr, touch_s,
+  store_block<NT, 1>(out.touch + base, ncta, acc ? g->touch : nullptr, touch_s, lm,
                      [&](int e) { return touch_s[e]; });
-  store_block<NT, 3 * K>(out.d_sh + base * 3 * K, ncta, acc ? g->sh : nullptr, touch_s,
+  store_block<NT, 3 * K>(out.d_sh + base * 3 * K, ncta, acc ? g->sh : nullptr, touch_s, lm,
                          [&](int e) {
                            const int tt = e / (3 * K);
                            return sm.sh[tt * St::SHS + (e - tt * 3 * K)];
