@@ -207,16 +207,25 @@ def jitter_camera(cam_kw, rank):
 
 
 # --------------------------------------------------------------------------
-def run_reference_arm(args):
-    """The reference's CPU path (oracle port, all host threads) on the same config."""
-    world, rank, _ = rank_info()
-    if rank != 0:
-        return
-    from oracle import oracle as O
+def reference_step(cfg, threads):
+    """One iteration of the reference's CPU path on config `cfg`: the reference itself
+    (halfsplat with its Cython core, pip-installed into oracle/_ref by
+    oracle/build_ref.py) when present, else the C oracle port.  Returns
+    (step() -> seconds, kind, description)."""
+    from oracle import reference_arm as RA
     from paper_2406_02720_b200 import scenes
-    sa = scenes.make_config(args.config).as_float64()
-    cam = sa.cameras[0]
-    threads = os.cpu_count() or 1
+    sa = scenes.make_config(cfg)
+    cam = dict(sa.cameras[0])
+    d_color = scenes.cotangent(cam["height"], cam["width"])
+    backward = scenes.CONFIGS[cfg]["backward"]
+    what = f"prepare+render{'+render_backward' if backward else ''}"
+    if RA.available():
+        def step():
+            return RA.iteration(sa, cam, d_color, backward, threads)
+        return step, "reference", (f"the reference's own {what} (halfsplat from oracle/_ref, "
+                                   f"Cython blend core, HALFSPLAT threads {threads})")
+    from oracle import oracle as O
+    s64 = sa.as_float64()
 
     class Cam:
         pass
@@ -225,27 +234,32 @@ def run_reference_arm(args):
     for k, v in cam.items():
         setattr(c, k, v)
     c.near_clip = 0.01
-    d_color = scenes.cotangent(cam["height"], cam["width"])
-    backward = scenes.CONFIGS[args.config]["backward"]
 
     def step():
-        out = O.render(sa, c, threads=threads)
+        t0 = time.perf_counter()
+        out = O.render(s64, c, threads=threads)
         if backward:
-            O.render_backward(sa, c, out, d_color, threads=threads)
+            O.render_backward(s64, c, out, d_color, threads=threads)
+        return time.perf_counter() - t0
+    return step, "port", f"the C oracle port's {what}, {threads} OpenMP threads"
 
-    t0 = time.perf_counter()
-    step()
-    first = time.perf_counter() - t0
+
+def run_reference_arm(args):
+    """The reference's CPU path (all host threads) on the same config, rank 0 only."""
+    world, rank, _ = rank_info()
+    if rank != 0:
+        return
+    from paper_2406_02720_b200 import scenes
+    threads = os.cpu_count() or 1
+    step, kind, what = reference_step(args.config, threads)
+    backward = scenes.CONFIGS[args.config]["backward"]
+    first = step()
     budget = 150.0
     warm = min(args.warmup, max(0, int(budget * 0.2 / max(first, 1e-3))))
     for _ in range(warm):
         step()
     n_run = max(1, min(args.steps, int(budget / max(first, 1e-3))))
-    times = []
-    for _ in range(n_run):
-        t0 = time.perf_counter()
-        step()
-        times.append(time.perf_counter() - t0)
+    times = [step() for _ in range(n_run)]
     ms = 1e3 * statistics.mean(times)
     value = 1e3 / ms
     unit = "iters/s" if backward else "frames/s"
@@ -254,10 +268,9 @@ def run_reference_arm(args):
         "n_gpus": world, "steps": n_run, "warmup": warm, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": bench_config(args.config, world),
-        "cpu_baseline": {"value": value, "unit": unit, "cores": threads, "kind": "port",
-                         "sample": f"{n_run} full {args.config} iterations (prepare+render"
-                                   f"{'+render_backward' if backward else ''}) of the C oracle "
-                                   f"port, {threads} OpenMP threads; requested steps {args.steps}"},
+        "cpu_baseline": {"value": value, "unit": unit, "cores": threads, "kind": kind,
+                         "sample": f"{n_run} full {args.config} iterations of {what}; "
+                                   f"requested steps {args.steps}"},
         "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -877,28 +890,13 @@ def run_e2e(args, sa, cam, dropin, world, barrier, torch, dist):
 
 
 def cpu_baseline(cfg):
-    """Oracle port (C, all host threads) on one full iteration of the same config."""
-    from oracle import oracle as O
-    from paper_2406_02720_b200 import scenes
-    sa = scenes.make_config(cfg).as_float64()
-    cam = dict(sa.cameras[0])
-
-    class Cam:
-        pass
-
-    c = Cam()
-    for k, v in cam.items():
-        setattr(c, k, v)
-    c.near_clip = 0.01
+    """The reference's CPU path (see reference_step), one full iteration of the same
+    config on all host threads."""
     threads = os.cpu_count() or 1
-    d_color = scenes.cotangent(cam["height"], cam["width"])
-    t0 = time.perf_counter()
-    out = O.render(sa, c, threads=threads)
-    O.render_backward(sa, c, out, d_color, threads=threads)
-    sec = time.perf_counter() - t0
-    return {"value": 1.0 / sec, "unit": "iters/s", "cores": threads, "kind": "port",
-            "sample": f"1 full {cfg} iteration (prepare+render+render_backward) of the C oracle "
-                      f"port, {threads} OpenMP threads, {sec:.2f} s"}
+    step, kind, what = reference_step(cfg, threads)
+    sec = step()
+    return {"value": 1.0 / sec, "unit": "iters/s", "cores": threads, "kind": kind,
+            "sample": f"1 full {cfg} iteration of {what}: {sec:.2f} s"}
 
 
 if __name__ == "__main__":

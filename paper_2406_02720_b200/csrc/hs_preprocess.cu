@@ -35,6 +35,11 @@ __device__ __forceinline__ long long to_i64_numpy(double x) {
 template <typename T>
 __device__ __forceinline__ double ld(const T* p, int64_t i) { return (double)p[i]; }
 
+// 1 / (1 + e^-x) in FP32 (MUFU ex2 + rcp), saturating cleanly at both ends
+__device__ __forceinline__ double sigmoid_f32(float x) {
+  return (double)__frcp_rn(1.0f + exp2f(-1.4426950408889634f * x));
+}
+
 // Forward state of one primitive for one view: the subset of FrameGeometry
 // (rasterizer.py:108-147) that K1 emits and K7 needs.  Recomputed by K7 rather
 // than stored (about 1 KB per splat in the reference).
@@ -191,6 +196,23 @@ __device__ __forceinline__ void sandwich(const double A[9], const double C[9], d
     }
 }
 
+// K7's replay (no numpy-exact rounding needed): the same product as two 3x3
+// multiplications, out = (A C) A^T, with C symmetric (6 unique outputs).
+__device__ __forceinline__ void sandwich_fast(const double A[9], const double C[9],
+                                              double out[9]) {
+  double AC[9];
+  for (int a = 0; a < 3; ++a)
+    for (int c = 0; c < 3; ++c)
+      AC[3 * a + c] = A[3 * a] * C[c] + A[3 * a + 1] * C[3 + c] + A[3 * a + 2] * C[6 + c];
+  for (int a = 0; a < 3; ++a)
+    for (int d = a; d < 3; ++d) {
+      const double v = AC[3 * a] * A[3 * d] + AC[3 * a + 1] * A[3 * d + 1] +
+                       AC[3 * a + 2] * A[3 * d + 2];
+      out[3 * a + d] = v;
+      out[3 * d + a] = v;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Shared-memory staging of one CTA's primitives.  The scene is array-of-structs
 // per field ((N,3), (N,K,3), ...); a thread reading its own primitive would issue
@@ -228,9 +250,20 @@ __device__ __forceinline__ void stage_in(Staged<T, K, NT>& s, const SceneArgs<T>
     cp_async_elem(&s.ra[e], &sc.ra[base + e]);
     cp_async_elem(&s.rb[e], &sc.rb[base + e]);
   }
-  for (int e = tid; e < cnt * 3 * K; e += NT) {
-    const int t = e / (3 * K), c = e - t * (3 * K);
-    cp_async_elem(&s.sh[t * Staged<T, K, NT>::SHS + c], &sc.sh[base * 3 * K + e]);
+  {
+    // consecutive threads on consecutive floats; the padded row (t, c) of element e
+    // advances incrementally (NT = qt * R + qc) instead of one division per element
+    constexpr int R = 3 * K, qt = NT / R, qc = NT % R;
+    int t = tid / R, c = tid - t * R;
+    for (int e = tid; e < cnt * R; e += NT) {
+      cp_async_elem(&s.sh[t * Staged<T, K, NT>::SHS + c], &sc.sh[base * R + e]);
+      t += qt;
+      c += qc;
+      if (c >= R) {
+        c -= R;
+        ++t;
+      }
+    }
   }
   asm volatile("cp.async.commit_group;\n" ::);
   if (wait) {
@@ -279,8 +312,25 @@ __device__ __forceinline__ void forward_state(const Src& src, const CamArgs& cam
     for (int k = 0; k < 4; ++k) ss += q[k] * q[k];
     st.qnorm = sqrt(ss);
   }
-  for (int k = 0; k < 4; ++k) st.qu[k] = q[k] / st.qnorm;
-  quat_to_rot_ref(st.qu, st.R);
+  if constexpr (kReplay) {
+    // K7: reciprocals instead of divisions; the rotation straight from the unit
+    // quaternion (quat_to_rot's second normalisation is a no-op up to rounding)
+    const double rq = 1.0 / st.qnorm;
+    for (int k = 0; k < 4; ++k) st.qu[k] = q[k] * rq;
+    const double w = st.qu[0], x = st.qu[1], y = st.qu[2], z = st.qu[3];
+    st.R[0] = 1 - 2 * (y * y + z * z);
+    st.R[1] = 2 * (x * y - w * z);
+    st.R[2] = 2 * (x * z + w * y);
+    st.R[3] = 2 * (x * y + w * z);
+    st.R[4] = 1 - 2 * (x * x + z * z);
+    st.R[5] = 2 * (y * z - w * x);
+    st.R[6] = 2 * (x * z - w * y);
+    st.R[7] = 2 * (y * z + w * x);
+    st.R[8] = 1 - 2 * (x * x + y * y);
+  } else {
+    for (int k = 0; k < 4; ++k) st.qu[k] = q[k] / st.qnorm;
+    quat_to_rot_ref(st.qu, st.R);
+  }
   for (int k = 0; k < 3; ++k) st.s[k] = exp(src.ls(k));
   double M[9];
   for (int r = 0; r < 3; ++r)
@@ -292,14 +342,21 @@ __device__ __forceinline__ void forward_state(const Src& src, const CamArgs& cam
   st.visible = false;
   if (!kReplay && !st.in_front) return;
   // cov_cam, Jacobian, ray covariance (rasterizer.py:183-185; geometry.py:189-207)
-  sandwich(cam.R, st.cov, st.ccam);
+  if constexpr (kReplay) sandwich_fast(cam.R, st.cov, st.ccam);
+  else sandwich(cam.R, st.cov, st.ccam);
   const double tx = st.t[0], ty = st.t[1], tz = st.t[2];
   const double invz = 1.0 / tz;
   const double ell = sqrt(tx * tx + ty * ty + tz * tz);
   st.J[0] = cam.fx * invz; st.J[1] = 0.0; st.J[2] = -cam.fx * tx * invz * invz;
   st.J[3] = 0.0; st.J[4] = cam.fy * invz; st.J[5] = -cam.fy * ty * invz * invz;
-  st.J[6] = tx / ell; st.J[7] = ty / ell; st.J[8] = tz / ell;
-  sandwich(st.J, st.ccam, st.cray);
+  if constexpr (kReplay) {
+    const double rl = 1.0 / ell;
+    st.J[6] = tx * rl; st.J[7] = ty * rl; st.J[8] = tz * rl;
+    sandwich_fast(st.J, st.ccam, st.cray);
+  } else {
+    st.J[6] = tx / ell; st.J[7] = ty / ell; st.J[8] = tz / ell;
+    sandwich(st.J, st.ccam, st.cray);
+  }
   st.mux = cam.fx * tx * invz + cam.cx;  // rasterizer.py:188-191
   st.muy = cam.fy * ty * invz + cam.cy;
   // dilated conic, radius, pixel rect, on-screen test (rasterizer.py:194-210)
@@ -358,7 +415,12 @@ __device__ __forceinline__ void forward_state(const Src& src, const CamArgs& cam
   double nrm[3];
   for (int k = 0; k < 3; ++k) nrm[k] = src.nrm(k);
   st.nnorm = sqrt(nrm[0] * nrm[0] + nrm[1] * nrm[1] + nrm[2] * nrm[2]);
-  for (int k = 0; k < 3; ++k) st.nu[k] = nrm[k] / st.nnorm;
+  if constexpr (kReplay) {
+    const double rn = 1.0 / st.nnorm;
+    for (int k = 0; k < 3; ++k) st.nu[k] = nrm[k] * rn;
+  } else {
+    for (int k = 0; k < 3; ++k) st.nu[k] = nrm[k] / st.nnorm;
+  }
   double hw[3];
   matvec_einsum(st.cov, st.nu, hw);
   matvec_blas(cam.R, hw, st.hc);
@@ -371,12 +433,21 @@ __device__ __forceinline__ void forward_state(const Src& src, const CamArgs& cam
   st.ynorm = st.bad ? 1.0 : yn;
   if (st.bad) {
     st.nray[0] = 0.0; st.nray[1] = 0.0; st.nray[2] = 1.0;
+  } else if constexpr (kReplay) {
+    const double ry = 1.0 / st.ynorm;
+    for (int k = 0; k < 3; ++k) st.nray[k] = st.y[k] * ry;
   } else {
     for (int k = 0; k < 3; ++k) st.nray[k] = st.y[k] / st.ynorm;
   }
   // opacities, blend mode, erf coefficients (rasterizer.py:256-277)
-  st.a1 = sigmoid_ref(src.ra());
-  st.a2 = sigmoid_ref(src.rb());
+  if constexpr (kReplay) {
+    // K7 only needs alpha (1 - alpha) for the logits' gradients: FP32 is ample
+    st.a1 = sigmoid_f32((float)src.ra());
+    st.a2 = sigmoid_f32((float)src.rb());
+  } else {
+    st.a1 = sigmoid_ref(src.ra());
+    st.a2 = sigmoid_ref(src.rb());
+  }
   st.c1 = 0.5 * (st.a1 + st.a2);
   if (kernel == 1) {
     st.c2 = 0.0;
@@ -400,7 +471,12 @@ __device__ __forceinline__ void forward_state(const Src& src, const CamArgs& cam
   // view-dependent colour (rasterizer.py:280-285)
   double vv[3] = {m0 - cam.center[0], m1 - cam.center[1], m2 - cam.center[2]};
   st.vdist = sqrt(vv[0] * vv[0] + vv[1] * vv[1] + vv[2] * vv[2]);
-  for (int k = 0; k < 3; ++k) st.vdir[k] = vv[k] / st.vdist;
+  if constexpr (kReplay) {
+    const double rv = 1.0 / st.vdist;
+    for (int k = 0; k < 3; ++k) st.vdir[k] = vv[k] * rv;
+  } else {
+    for (int k = 0; k < 3; ++k) st.vdir[k] = vv[k] / st.vdist;
+  }
   // K7 takes the colour clamp from the record (merge_rows_kernel) and evaluates
   // the basis in FP32 (sh_bwd_f32)
   if (!kReplay) {
@@ -938,8 +1014,8 @@ __device__ __forceinline__ void build_live_mask(LiveMask<NT>& m, const int32_t* 
 // Does any primitive of elements [e0, e0 + len) (S elements per primitive) have
 // a non-zero flag?  (len < 32 * S)
 template <int S, int NT>
-__device__ __forceinline__ bool any_live(const LiveMask<NT>& m, int e0, int len) {
-  if (m.all) return true;
+__device__ __forceinline__ bool any_live(bool all, const LiveMask<NT>& m, int e0, int len) {
+  if (all) return true;
   const int p0 = e0 / S, p1 = (e0 + len - 1) / S;
   const int wi = p0 >> 5;
   const uint64_t win = ((uint64_t)m.w[wi + 1] << 32) | m.w[wi];
@@ -966,8 +1042,9 @@ __device__ __forceinline__ void prefetch_block(E* smem, const E* src, int cnt,
   constexpr int kV = 16 / sizeof(E);
   const int n = cnt * S;
   const int nv = ((uintptr_t)src & 15) ? 0 : n / kV;
+  const bool all = lm.all;
   for (int v = threadIdx.x; v < nv; v += NT)
-    if (any_live<S>(lm, v * kV, kV)) cp_async16(smem + v * kV, src + v * kV);
+    if (any_live<S>(all, lm, v * kV, kV)) cp_async16(smem + v * kV, src + v * kV);
   for (int e = nv * kV + threadIdx.x; e < n; e += NT)
     if (live[e / S]) cp_async_elem(smem + e, src + e);
 }
@@ -984,8 +1061,9 @@ __device__ __forceinline__ void store_block(E* __restrict__ dst, int cnt, const 
   const int n = cnt * S;
   const int nv = ((uintptr_t)dst & 15) ? 0 : n / kV;
   V* dv = reinterpret_cast<V*>(dst);
+  const bool all = lm.all;
   for (int v = threadIdx.x; v < nv; v += NT) {
-    if (old && !any_live<S>(lm, v * kV, kV)) continue;
+    if (old && !any_live<S>(all, lm, v * kV, kV)) continue;
     V nw;
     E* ne = reinterpret_cast<E*>(&nw);
 #pragma unroll
@@ -1032,6 +1110,37 @@ __device__ __forceinline__ void red_add4(float* p, float4 v, bool mc) {
                  "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
 }
 
+// store_block for a field staged in padded shared-memory rows (row r of R elements
+// at rows + r * STRIDE) whose rows are whole 16-B vectors: each vector's row and
+// column come from one division instead of one per element.
+template <int NT, int R, int STRIDE, typename E>
+__device__ __forceinline__ void store_rows(E* __restrict__ dst, int cnt, const E* old,
+                                           const int32_t* live, const LiveMask<NT>& lm,
+                                           const E* rows) {
+  using V = typename Vec16<E>::type;
+  constexpr int kV = 16 / sizeof(E);
+  static_assert(R % kV == 0, "rows must be whole vectors");
+  const int n = cnt * R;
+  if ((uintptr_t)dst & 15) {
+    for (int e = threadIdx.x; e < n; e += NT) {
+      const int r = e / R;
+      if (old && !live[r]) continue;
+      dst[e] = rows[r * STRIDE + (e - r * R)] + (old ? old[e] : E(0));
+    }
+    return;
+  }
+  V* dv = reinterpret_cast<V*>(dst);
+  for (int v = threadIdx.x; v < n / kV; v += NT) {
+    const int r = (v * kV) / R, c = v * kV - r * R;
+    if (old && !live[r]) continue;
+    V nw;
+    E* ne = reinterpret_cast<E*>(&nw);
+#pragma unroll
+    for (int j = 0; j < kV; ++j) ne[j] = rows[r * STRIDE + c + j] + (old ? old[v * kV + j] : E(0));
+    dv[v] = nw;
+  }
+}
+
 // One field of the CTA's primitives reduced into `dst` (only touched ones: the
 // others add zero).  float fields move in 16-B vector reductions when aligned.
 template <int NT, int S, typename E, typename Get>
@@ -1041,8 +1150,9 @@ __device__ __forceinline__ void reduce_block(E* __restrict__ dst, int cnt, const
   int done = 0;
   if constexpr (sizeof(E) == 4 && !std::is_same<E, int32_t>::value) {
     const int nv = ((uintptr_t)dst & 15) ? 0 : n / 4;
+    const bool all = lm.all;
     for (int v = threadIdx.x; v < nv; v += NT) {
-      if (!any_live<S>(lm, v * 4, 4)) continue;
+      if (!any_live<S>(all, lm, v * 4, 4)) continue;
       red_add4(dst + 4 * v, make_float4(get(4 * v), get(4 * v + 1), get(4 * v + 2),
                                         get(4 * v + 3)), mc);
     }
@@ -1143,11 +1253,16 @@ __global__ void __launch_bounds__(NT, HS_K7_MINB) preprocess_bwd_kernel(
                      [&](int e) { return pgn_s[e]; });
   store_block<NT, 1>(out.touch + base, ncta, acc ? g->touch : nullptr, touch_s, lm,
                      [&](int e) { return touch_s[e]; });
-  store_block<NT, 3 * K>(out.d_sh + base * 3 * K, ncta, acc ? g->sh : nullptr, touch_s, lm,
-                         [&](int e) {
-                           const int tt = e / (3 * K);
-                           return sm.sh[tt * St::SHS + (e - tt * 3 * K)];
-                         });
+  if constexpr ((3 * K) % (16 / sizeof(T)) == 0) {
+    store_rows<NT, 3 * K, St::SHS>(out.d_sh + base * 3 * K, ncta, acc ? g->sh : nullptr,
+                                   touch_s, lm, sm.sh);
+  } else {
+    store_block<NT, 3 * K>(out.d_sh + base * 3 * K, ncta, acc ? g->sh : nullptr, touch_s, lm,
+                           [&](int e) {
+                             const int tt = e / (3 * K);
+                             return sm.sh[tt * St::SHS + (e - tt * 3 * K)];
+                           });
+  }
 }
 
 
