@@ -270,6 +270,11 @@ int hs_backward_tiles(const double* packed, const int8_t* mode,
                       const int32_t* terminal, double* pair_grads,
                       int32_t tile_lo, int32_t tile_hi);
 
+/* Seam 1 keeps the last frame's full GPU result (and a host copy of its inputs)
+ * so the reference's concurrent chunk calls on one frame blend it once; a call
+ * whose inputs differ (exact byte compare) recomputes.  This releases it. */
+void hs_seam1_cache_clear(void);
+
 /* ---- training loss: the cotangent producer between K5 and K6 ---------- */
 
 /* Device workspace for hs_loss on an (height, width, channels) image. */

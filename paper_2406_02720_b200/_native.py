@@ -177,6 +177,7 @@ _SIGNATURES = {
     "hs_frame_status": (c_int32, [ctypes.POINTER(HsFrame), ctypes.POINTER(c_int64),
                                   ctypes.POINTER(c_int32), c_void_p]),
     "hs_frame_status_async": (c_int32, [ctypes.POINTER(HsFrame), c_void_p, c_void_p]),
+    "hs_seam1_cache_clear": (None, []),
     "hs_status_string": (ctypes.c_char_p, [c_int32]),
     "hs_last_cuda_error": (ctypes.c_char_p, []),
     "hs_kernel_launch_count": (c_int64, []),

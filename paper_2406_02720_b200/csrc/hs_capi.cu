@@ -3,6 +3,7 @@
 #include <atomic>
 #include <map>
 #include <mutex>
+#include <shared_mutex>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -712,6 +713,117 @@ int seam1_validate(const int64_t* tile_starts, int64_t num_pairs, int32_t height
 }
 }  // namespace
 
+}  // extern "C"
+
+// Seam 1 under the reference's threaded chunk dispatch (rasterizer.py:373-378):
+// every chunk call of one frame passes the same packed / mode / pair_splat /
+// tile_starts (and, backward, the same cotangent and forward outputs).  The
+// first call of a frame blends ALL tiles on the GPU and keeps the full result on
+// the host; every later call whose inputs compare equal (memcmp against the kept
+// copies, exact) only copies its tiles out.  Concurrent calls read the cache
+// under a shared lock; a miss recomputes under the exclusive lock.
+namespace {
+
+struct HostCopy {
+  std::vector<char> b;
+  void set(const void* p, size_t n) {
+    b.resize(n);
+    if (n) memcpy(b.data(), p, n);
+  }
+  bool same(const void* p, size_t n) const {
+    return b.size() == n && (n == 0 || memcmp(b.data(), p, n) == 0);
+  }
+};
+
+struct Seam1Key {
+  HostCopy packed, mode, pairs, starts;
+  int32_t h = -1, w = -1, tx = -1;
+  double bg[3] = {0, 0, 0};
+  void set(const double* pk, const int8_t* md, const int32_t* ps, const int64_t* ts, int64_t m,
+           int64_t p, int32_t hh, int32_t ww, int32_t t, const double* b, int n_tiles) {
+    packed.set(pk, (size_t)m * 13 * sizeof(double));
+    mode.set(md, (size_t)m);
+    pairs.set(ps, (size_t)p * sizeof(int32_t));
+    starts.set(ts, (size_t)(n_tiles + 1) * sizeof(int64_t));
+    h = hh; w = ww; tx = t;
+    for (int k = 0; k < 3; ++k) bg[k] = b[k];
+  }
+  bool same(const double* pk, const int8_t* md, const int32_t* ps, const int64_t* ts, int64_t m,
+            int64_t p, int32_t hh, int32_t ww, int32_t t, const double* b, int n_tiles) const {
+    return h == hh && w == ww && tx == t && bg[0] == b[0] && bg[1] == b[1] && bg[2] == b[2] &&
+           starts.same(ts, (size_t)(n_tiles + 1) * sizeof(int64_t)) &&
+           pairs.same(ps, (size_t)p * sizeof(int32_t)) && mode.same(md, (size_t)m) &&
+           packed.same(pk, (size_t)m * 13 * sizeof(double));
+  }
+};
+
+struct FwdCache {
+  bool valid = false;
+  Seam1Key key;
+  std::vector<float> out;  // color (3 npx), alpha, depth, transmittance
+  std::vector<int32_t> term;
+};
+struct BwdCache {
+  bool valid = false;
+  Seam1Key key;
+  HostCopy d_color, trans, term;
+  std::vector<float> rows;  // (P, 12), every pair of the frame
+};
+std::shared_mutex g_fwd_mu, g_bwd_mu;
+FwdCache g_fwd;
+BwdCache g_bwd;
+
+struct Seam1Dev {
+  cudaStream_t s = nullptr;
+  DevBuf packed, mode, rec, side, pairs, ts, ctr;
+  ~Seam1Dev() {
+    if (s) cudaStreamDestroy(s);
+  }
+};
+
+// upload + pack the reference's frame (shared by both directions)
+int seam1_upload(Seam1Dev& d, const double* packed, const int8_t* mode,
+                 const int32_t* pair_splat, const int64_t* tile_starts, int64_t m, int64_t p,
+                 int n_tiles, BlendGeom& g, int32_t height, int32_t width, int32_t tiles_x) {
+  std::vector<int32_t> ts32(n_tiles + 1);
+  for (int t = 0; t <= n_tiles; ++t) ts32[t] = (int32_t)tile_starts[t];
+  HS_CUDA(cudaStreamCreateWithFlags(&d.s, cudaStreamNonBlocking));
+  HS_CUDA(d.packed.alloc(m * 13 * sizeof(double)));
+  HS_CUDA(d.mode.alloc(m));
+  HS_CUDA(d.rec.alloc(m * 64));
+  HS_CUDA(d.side.alloc(m * sizeof(SteepRec)));
+  HS_CUDA(d.pairs.alloc(p * 4));
+  HS_CUDA(d.ts.alloc((n_tiles + 1) * 4));
+  HS_CUDA(d.ctr.alloc(256));
+  if (m > 0) {
+    HS_CUDA(cudaMemcpyAsync(d.packed.p, packed, m * 13 * sizeof(double), cudaMemcpyHostToDevice,
+                            d.s));
+    HS_CUDA(cudaMemcpyAsync(d.mode.p, mode, m, cudaMemcpyHostToDevice, d.s));
+  }
+  if (p > 0) HS_CUDA(cudaMemcpyAsync(d.pairs.p, pair_splat, p * 4, cudaMemcpyHostToDevice, d.s));
+  HS_CUDA(cudaMemcpyAsync(d.ts.p, ts32.data(), (n_tiles + 1) * 4, cudaMemcpyHostToDevice, d.s));
+  HS_CUDA(launch_pack_records((const double*)d.packed.p, (const int8_t*)d.mode.p, m,
+                              (float4*)d.rec.p, (SteepRec*)d.side.p, (uint32_t*)d.pairs.p, p, d.s));
+  HS_CUDA(cudaStreamSynchronize(d.s));  // ts32 goes out of scope
+  g.tile_starts = (const int32_t*)d.ts.p;
+  g.pair_src = (const uint32_t*)d.pairs.p;
+  g.rec = (const float4*)d.rec.p;
+  g.side = (const SteepRec*)d.side.p;
+  g.width = width;
+  g.height = height;
+  g.tiles_x = tiles_x;
+  g.tile_lo = 0;
+  g.n_work = n_tiles;
+  g.tile_order = nullptr;
+  g.tile_work = nullptr;
+  g.work_counter = (int*)d.ctr.p;
+  return HS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
 int hs_forward_tiles(const double* packed, const int8_t* mode, const int32_t* pair_splat,
                      const int64_t* tile_starts, int64_t m, int64_t p, int32_t height,
                      int32_t width, int32_t tiles_x, const double* bg, double* color, double* alpha,
@@ -722,62 +834,55 @@ int hs_forward_tiles(const double* packed, const int8_t* mode, const int32_t* pa
   if (tile_hi == tile_lo) return HS_OK;
   const int n_tiles = tiles_x * tiles_of(height);
   const size_t npx = (size_t)height * width;
-  std::vector<int32_t> ts32(n_tiles + 1);
-  for (int t = 0; t <= n_tiles; ++t) ts32[t] = (int32_t)tile_starts[t];
-  cudaStream_t s;
-  HS_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-  struct StreamGuard { cudaStream_t s; ~StreamGuard() { cudaStreamDestroy(s); } } sg{s};
-  DevBuf d_packed, d_mode, d_rec, d_side, d_pairs, d_ts, d_out, d_term, d_ctr;
-  HS_CUDA(d_packed.alloc(m * 13 * sizeof(double)));
-  HS_CUDA(d_mode.alloc(m));
-  HS_CUDA(d_rec.alloc(m * 64));
-  HS_CUDA(d_side.alloc(m * sizeof(SteepRec)));
-  HS_CUDA(d_pairs.alloc(p * 4));
-  HS_CUDA(d_ts.alloc((n_tiles + 1) * 4));
-  HS_CUDA(d_out.alloc(npx * 6 * sizeof(float)));
-  HS_CUDA(d_term.alloc(npx * 4));
-  HS_CUDA(d_ctr.alloc(256));
-  if (m > 0) {
-    HS_CUDA(cudaMemcpyAsync(d_packed.p, packed, m * 13 * sizeof(double), cudaMemcpyHostToDevice, s));
-    HS_CUDA(cudaMemcpyAsync(d_mode.p, mode, m, cudaMemcpyHostToDevice, s));
+  auto copy_out = [&](const FwdCache& c) {
+    const float* h = c.out.data();
+    for (int t = tile_lo; t < tile_hi; ++t) {
+      const int ty = t / tiles_x, tx = t - ty * tiles_x;
+      for (int r = ty * kTile; r < ty * kTile + kTile && r < height; ++r)
+        for (int col = tx * kTile; col < tx * kTile + kTile && col < width; ++col) {
+          const size_t q = (size_t)r * width + col;
+          for (int ch = 0; ch < 3; ++ch) color[3 * q + ch] = h[3 * q + ch];
+          alpha[q] = h[3 * npx + q];
+          depth[q] = h[4 * npx + q];
+          transmittance[q] = h[5 * npx + q];
+          terminal[q] = c.term[q];
+        }
+    }
+  };
+  {
+    std::shared_lock<std::shared_mutex> lock(g_fwd_mu);
+    if (g_fwd.valid && g_fwd.key.same(packed, mode, pair_splat, tile_starts, m, p, height, width,
+                                      tiles_x, bg, n_tiles)) {
+      copy_out(g_fwd);
+      return HS_OK;
+    }
   }
-  if (p > 0) HS_CUDA(cudaMemcpyAsync(d_pairs.p, pair_splat, p * 4, cudaMemcpyHostToDevice, s));
-  HS_CUDA(cudaMemcpyAsync(d_ts.p, ts32.data(), (n_tiles + 1) * 4, cudaMemcpyHostToDevice, s));
-  HS_CUDA(launch_pack_records((const double*)d_packed.p, (const int8_t*)d_mode.p, m,
-                              (float4*)d_rec.p, (SteepRec*)d_side.p, (uint32_t*)d_pairs.p, p, s));
-  BlendGeom g;
-  g.tile_starts = (const int32_t*)d_ts.p;
-  g.pair_src = (const uint32_t*)d_pairs.p;
-  g.rec = (const float4*)d_rec.p;
-  g.side = (const SteepRec*)d_side.p;
-  g.width = width;
-  g.height = height;
-  g.tiles_x = tiles_x;
-  g.tile_lo = tile_lo;
-  g.n_work = tile_hi - tile_lo;
-  g.tile_order = nullptr;
-  g.tile_work = nullptr;
-  g.work_counter = (int*)d_ctr.p;
-  float* o = (float*)d_out.p;
-  HS_CUDA(launch_blend_fwd(g, (float)bg[0], (float)bg[1], (float)bg[2], o, o + 3 * npx,
-                           o + 4 * npx, o + 5 * npx, (int32_t*)d_term.p, s));
-  std::vector<float> h(npx * 6);
-  std::vector<int32_t> ht(npx);
-  HS_CUDA(cudaMemcpyAsync(h.data(), o, npx * 6 * sizeof(float), cudaMemcpyDeviceToHost, s));
-  HS_CUDA(cudaMemcpyAsync(ht.data(), d_term.p, npx * 4, cudaMemcpyDeviceToHost, s));
-  HS_CUDA(cudaStreamSynchronize(s));
-  for (int t = tile_lo; t < tile_hi; ++t) {
-    const int ty = t / tiles_x, tx = t - ty * tiles_x;
-    for (int r = ty * kTile; r < ty * kTile + kTile && r < height; ++r)
-      for (int c = tx * kTile; c < tx * kTile + kTile && c < width; ++c) {
-        const size_t q = (size_t)r * width + c;
-        for (int ch = 0; ch < 3; ++ch) color[3 * q + ch] = h[3 * q + ch];
-        alpha[q] = h[3 * npx + q];
-        depth[q] = h[4 * npx + q];
-        transmittance[q] = h[5 * npx + q];
-        terminal[q] = ht[q];
-      }
+  std::unique_lock<std::shared_mutex> lock(g_fwd_mu);
+  if (!(g_fwd.valid && g_fwd.key.same(packed, mode, pair_splat, tile_starts, m, p, height, width,
+                                      tiles_x, bg, n_tiles))) {
+    g_fwd.valid = false;
+    Seam1Dev d;
+    BlendGeom g;
+    if ((st = seam1_upload(d, packed, mode, pair_splat, tile_starts, m, p, n_tiles, g, height,
+                           width, tiles_x)))
+      return st;
+    DevBuf d_out, d_term;
+    HS_CUDA(d_out.alloc(npx * 6 * sizeof(float)));
+    HS_CUDA(d_term.alloc(npx * 4));
+    float* o = (float*)d_out.p;
+    HS_CUDA(launch_blend_fwd(g, (float)bg[0], (float)bg[1], (float)bg[2], o, o + 3 * npx,
+                             o + 4 * npx, o + 5 * npx, (int32_t*)d_term.p, d.s));
+    g_fwd.out.resize(npx * 6);
+    g_fwd.term.resize(npx);
+    HS_CUDA(cudaMemcpyAsync(g_fwd.out.data(), o, npx * 6 * sizeof(float), cudaMemcpyDeviceToHost,
+                            d.s));
+    HS_CUDA(cudaMemcpyAsync(g_fwd.term.data(), d_term.p, npx * 4, cudaMemcpyDeviceToHost, d.s));
+    HS_CUDA(cudaStreamSynchronize(d.s));
+    g_fwd.key.set(packed, mode, pair_splat, tile_starts, m, p, height, width, tiles_x, bg,
+                  n_tiles);
+    g_fwd.valid = true;
   }
+  copy_out(g_fwd);
   return HS_OK;
 }
 
@@ -791,59 +896,69 @@ int hs_backward_tiles(const double* packed, const int8_t* mode, const int32_t* p
   if (tile_hi == tile_lo || p == 0) return HS_OK;
   const int n_tiles = tiles_x * tiles_of(height);
   const size_t npx = (size_t)height * width;
-  std::vector<int32_t> ts32(n_tiles + 1);
-  for (int t = 0; t <= n_tiles; ++t) ts32[t] = (int32_t)tile_starts[t];
-  std::vector<float> hin(npx * 4);
-  for (size_t q = 0; q < npx * 3; ++q) hin[q] = (float)d_color[q];
-  for (size_t q = 0; q < npx; ++q) hin[3 * npx + q] = (float)transmittance[q];
-  cudaStream_t s;
-  HS_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-  struct StreamGuard { cudaStream_t s; ~StreamGuard() { cudaStreamDestroy(s); } } sg{s};
-  DevBuf d_packed, d_mode, d_rec, d_side, d_pairs, d_ts, d_in, d_term, d_rows, d_ctr;
-  HS_CUDA(d_packed.alloc(m * 13 * sizeof(double)));
-  HS_CUDA(d_mode.alloc(m));
-  HS_CUDA(d_rec.alloc(m * 64));
-  HS_CUDA(d_side.alloc(m * sizeof(SteepRec)));
-  HS_CUDA(d_pairs.alloc(p * 4));
-  HS_CUDA(d_ts.alloc((n_tiles + 1) * 4));
-  HS_CUDA(d_in.alloc(npx * 4 * sizeof(float)));
-  HS_CUDA(d_term.alloc(npx * 4));
-  HS_CUDA(d_rows.alloc(p * 12 * sizeof(float)));
-  HS_CUDA(d_ctr.alloc(256));
-  HS_CUDA(cudaMemcpyAsync(d_packed.p, packed, m * 13 * sizeof(double), cudaMemcpyHostToDevice, s));
-  HS_CUDA(cudaMemcpyAsync(d_mode.p, mode, m, cudaMemcpyHostToDevice, s));
-  HS_CUDA(cudaMemcpyAsync(d_pairs.p, pair_splat, p * 4, cudaMemcpyHostToDevice, s));
-  HS_CUDA(cudaMemcpyAsync(d_ts.p, ts32.data(), (n_tiles + 1) * 4, cudaMemcpyHostToDevice, s));
-  HS_CUDA(cudaMemcpyAsync(d_in.p, hin.data(), npx * 4 * sizeof(float), cudaMemcpyHostToDevice, s));
-  HS_CUDA(cudaMemcpyAsync(d_term.p, terminal, npx * 4, cudaMemcpyHostToDevice, s));
-  HS_CUDA(cudaMemsetAsync(d_rows.p, 0, p * 12 * sizeof(float), s));
-  HS_CUDA(launch_pack_records((const double*)d_packed.p, (const int8_t*)d_mode.p, m,
-                              (float4*)d_rec.p, (SteepRec*)d_side.p, (uint32_t*)d_pairs.p, p, s));
-  BlendGeom g;
-  g.tile_starts = (const int32_t*)d_ts.p;
-  g.pair_src = (const uint32_t*)d_pairs.p;
-  g.rec = (const float4*)d_rec.p;
-  g.side = (const SteepRec*)d_side.p;
-  g.width = width;
-  g.height = height;
-  g.tiles_x = tiles_x;
-  g.tile_lo = tile_lo;
-  g.n_work = tile_hi - tile_lo;
-  g.tile_order = nullptr;
-  g.tile_work = nullptr;
-  g.work_counter = (int*)d_ctr.p;
-  const float* in = (const float*)d_in.p;
-  HS_CUDA(launch_blend_bwd(g, (float)bg[0], (float)bg[1], (float)bg[2], in, in + 3 * npx,
-                           (const int32_t*)d_term.p, (float*)d_rows.p, nullptr, nullptr, true, s));
-  const int64_t r0 = tile_starts[tile_lo], r1 = tile_starts[tile_hi];
-  std::vector<float> rows((size_t)(r1 - r0) * 12);
-  if (r1 > r0)
-    HS_CUDA(cudaMemcpyAsync(rows.data(), (float*)d_rows.p + r0 * 12, (r1 - r0) * 12 * sizeof(float),
-                            cudaMemcpyDeviceToHost, s));
-  HS_CUDA(cudaStreamSynchronize(s));
-  for (int64_t k = r0; k < r1; ++k)
-    for (int c = 0; c < 12; ++c) pair_grads[k * 12 + c] += rows[(k - r0) * 12 + c];
+  auto same = [&](const BwdCache& c) {
+    return c.valid && c.term.same(terminal, npx * 4) &&
+           c.trans.same(transmittance, npx * sizeof(double)) &&
+           c.d_color.same(d_color, npx * 3 * sizeof(double)) &&
+           c.key.same(packed, mode, pair_splat, tile_starts, m, p, height, width, tiles_x, bg,
+                      n_tiles);
+  };
+  auto add_rows = [&](const BwdCache& c) {  // pair rows of this chunk's tiles, +=
+    const int64_t r0 = tile_starts[tile_lo], r1 = tile_starts[tile_hi];
+    for (int64_t k = r0; k < r1; ++k)
+      for (int col = 0; col < 12; ++col) pair_grads[k * 12 + col] += c.rows[k * 12 + col];
+  };
+  {
+    std::shared_lock<std::shared_mutex> lock(g_bwd_mu);
+    if (same(g_bwd)) {
+      add_rows(g_bwd);
+      return HS_OK;
+    }
+  }
+  std::unique_lock<std::shared_mutex> lock(g_bwd_mu);
+  if (!same(g_bwd)) {
+    g_bwd.valid = false;
+    std::vector<float> hin(npx * 4);
+    for (size_t q = 0; q < npx * 3; ++q) hin[q] = (float)d_color[q];
+    for (size_t q = 0; q < npx; ++q) hin[3 * npx + q] = (float)transmittance[q];
+    Seam1Dev d;
+    BlendGeom g;
+    if ((st = seam1_upload(d, packed, mode, pair_splat, tile_starts, m, p, n_tiles, g, height,
+                           width, tiles_x)))
+      return st;
+    DevBuf d_in, d_term, d_rows;
+    HS_CUDA(d_in.alloc(npx * 4 * sizeof(float)));
+    HS_CUDA(d_term.alloc(npx * 4));
+    HS_CUDA(d_rows.alloc(p * 12 * sizeof(float)));
+    HS_CUDA(cudaMemcpyAsync(d_in.p, hin.data(), npx * 4 * sizeof(float), cudaMemcpyHostToDevice,
+                            d.s));
+    HS_CUDA(cudaMemcpyAsync(d_term.p, terminal, npx * 4, cudaMemcpyHostToDevice, d.s));
+    HS_CUDA(cudaMemsetAsync(d_rows.p, 0, p * 12 * sizeof(float), d.s));
+    const float* in = (const float*)d_in.p;
+    HS_CUDA(launch_blend_bwd(g, (float)bg[0], (float)bg[1], (float)bg[2], in, in + 3 * npx,
+                             (const int32_t*)d_term.p, (float*)d_rows.p, nullptr, nullptr, true,
+                             d.s));
+    g_bwd.rows.resize((size_t)p * 12);
+    HS_CUDA(cudaMemcpyAsync(g_bwd.rows.data(), d_rows.p, p * 12 * sizeof(float),
+                            cudaMemcpyDeviceToHost, d.s));
+    HS_CUDA(cudaStreamSynchronize(d.s));
+    g_bwd.key.set(packed, mode, pair_splat, tile_starts, m, p, height, width, tiles_x, bg, n_tiles);
+    g_bwd.d_color.set(d_color, npx * 3 * sizeof(double));
+    g_bwd.trans.set(transmittance, npx * sizeof(double));
+    g_bwd.term.set(terminal, npx * 4);
+    g_bwd.valid = true;
+  }
+  add_rows(g_bwd);
   return HS_OK;
+}
+
+void hs_seam1_cache_clear(void) {
+  {
+    std::unique_lock<std::shared_mutex> lock(g_fwd_mu);
+    g_fwd = FwdCache();
+  }
+  std::unique_lock<std::shared_mutex> lock(g_bwd_mu);
+  g_bwd = BwdCache();
 }
 
 }  // extern "C"

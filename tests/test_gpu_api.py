@@ -212,6 +212,58 @@ def test_seam1_blend_plugin_vs_oracle(cuda, chunks):
         assert rel.max() < 1e-3, rel
 
 
+def test_seam1_threaded_chunks_vs_oracle(cuda):
+    """The reference's dispatch (rasterizer.py:373-378, 412-417): 8 threads call the
+    plugin concurrently on disjoint tile chunks of one frame.  The first call blends
+    the frame once and the rest copy their tiles out of the kept result; images and
+    pair rows equal the oracle's, and an in-place change of an input array (same
+    pointers) is detected and recomputed."""
+    from concurrent.futures import ThreadPoolExecutor
+    from oracle import oracle as O
+    blend = backend.get_backend()
+    gold = load_golden("ball_small")
+    tx, ty = int(gold["tiles_x"]), int(gold["tiles_y"])
+    h, w = gold["color"].shape[:2]
+    bg = np.array(scenes.BACKGROUND)
+    n_tiles = tx * ty
+    bounds = np.linspace(0, n_tiles, 9).astype(int)
+    spans = list(zip(bounds[:-1].tolist(), bounds[1:].tolist()))
+    packed = gold["packed"].copy()
+    args = (packed, gold["mode"], gold["pair_splat"], gold["tile_starts"], h, w, tx, bg)
+
+    def forward():
+        out = [np.zeros((h, w, 3)), np.zeros((h, w)), np.zeros((h, w)), np.ones((h, w)),
+               np.zeros((h, w), np.int32)]
+        with ThreadPoolExecutor(max_workers=8) as pool:
+            list(pool.map(lambda sp: blend.forward_tiles(*args, *out, *sp), spans))
+        return dict(zip(("color", "alpha", "depth", "transmittance", "terminal"), out))
+
+    def oracle_forward():
+        out = [np.zeros((h, w, 3)), np.zeros((h, w)), np.zeros((h, w)), np.ones((h, w)),
+               np.zeros((h, w), np.int32)]
+        O.forward_tiles(*args, *out, 0, n_tiles)
+        return dict(zip(("color", "alpha", "depth", "transmittance", "terminal"), out))
+
+    for _ in range(2):  # the second frame is a cache hit for every chunk
+        assert_images(forward(), gold)
+    pg = np.zeros((gold["pair_splat"].shape[0], 12))
+    with ThreadPoolExecutor(max_workers=8) as pool:
+        list(pool.map(lambda sp: blend.backward_tiles(*args, gold["d_color"],
+                                                      gold["transmittance"], gold["terminal"],
+                                                      pg, *sp), spans))
+    ref = np.zeros_like(pg)
+    O.backward_tiles(*args, gold["d_color"], gold["transmittance"], gold["terminal"], ref, 0,
+                     n_tiles)
+    rel = np.linalg.norm(pg - ref, axis=0) / np.maximum(np.linalg.norm(ref, axis=0), 1e-30)
+    assert rel.max() < 1e-3, rel
+    # same buffers, new values: the colour columns change in place
+    packed[:, 9:12] *= 0.5
+    got = forward()
+    assert_images(got, oracle_forward())
+    from paper_2406_02720_b200 import _native
+    _native.load().hs_seam1_cache_clear()
+
+
 def test_seam1_rejects_bad_arrays(cuda):
     gold = load_golden("mini")
     h, w = gold["color"].shape[:2]
