@@ -164,44 +164,47 @@ cudaError_t run_depth_sort_hi(void* temp, size_t temp_bytes, const uint64_t* key
 
 // cnt_r[r] = count[order[r]] and rank_of; P accumulates as int64 next to the
 // int32 scan (which may wrap).  With the segment path (SEGS) each CTA -- one
-// block of kBinRanks ranks -- also histograms its segments by (tile row, column
-// block) key into cnt_r[n + 1 + key * nb + block] and adds its pairs per tile row
-// into row_pairs.
+// block of kBinRanks ranks, 4 per thread -- also histograms its segments by
+// (tile row, column block) key into cnt_r[n + 1 + key * nb + block] and adds its
+// pairs per key into key_pairs.
 template <bool SEGS>
-__global__ void __launch_bounds__(kBinRanks) gather_counts_kernel(
+__global__ void __launch_bounds__(kBinThreads) gather_counts_kernel(
     const int32_t* __restrict__ count, const uint32_t* __restrict__ order,
     const int4* __restrict__ rect, int32_t* __restrict__ cnt_r, uint32_t* __restrict__ rank_of,
-    int64_t n, int tiles_y, int nblk, int32_t* __restrict__ row_pairs,
+    int64_t n, int tiles_y, int nblk, int32_t* __restrict__ key_pairs,
     BinStatusDev* __restrict__ status) {
-  extern __shared__ int smem_cnt[];  // [keys] segments, then [tiles_y] pairs
-  __shared__ long long csum[kBinRanks / 32][2];
+  extern __shared__ int smem_cnt[];  // [keys] segments, then [keys] pairs
+  __shared__ long long csum[kBinThreads / 32][2];
   const int keys = tiles_y * nblk;
   int* keys_s = smem_cnt;
-  int* rows_s = smem_cnt + keys;
-  const int64_t r = (int64_t)blockIdx.x * kBinRanks + threadIdx.x;
+  int* pairs_s = smem_cnt + keys;
   if (SEGS) {
-    for (int e = threadIdx.x; e < keys + tiles_y; e += kBinRanks) smem_cnt[e] = 0;
+    for (int e = threadIdx.x; e < 2 * keys; e += kBinThreads) smem_cnt[e] = 0;
     __syncthreads();
   }
-  int c = 0, nseg = 0;
-  if (r < n) {
+  long long v = 0, vs = 0;
+#pragma unroll
+  for (int q = 0; q < kBinRanks / kBinThreads; ++q) {
+    const int64_t r = (int64_t)blockIdx.x * kBinRanks + q * kBinThreads + threadIdx.x;
+    if (r >= n) continue;
     const uint32_t i = order[r] & kIndexMask;
-    c = count[i];
+    const int c = count[i];
     cnt_r[r] = c;
     rank_of[i] = (uint32_t)r;
+    v += c;
     if (SEGS && c > 0) {
       const int4 rc = rect[i];
-      const int sx = rc.y - rc.x + 1;
       const int b0 = rc.x / kSegCols, b1 = rc.y / kSegCols;
-      nseg = (rc.w - rc.z + 1) * (b1 - b0 + 1);
-      for (int ty = rc.z; ty <= rc.w; ++ty) {
-        atomicAdd(&rows_s[ty], sx);
-        for (int b = b0; b <= b1; ++b) atomicAdd(&keys_s[ty * nblk + b], 1);
-      }
+      vs += (rc.w - rc.z + 1) * (b1 - b0 + 1);
+      for (int ty = rc.z; ty <= rc.w; ++ty)
+        for (int b = b0; b <= b1; ++b) {
+          const int lo = max(rc.x, b * kSegCols), hi = min(rc.y, b * kSegCols + kSegCols - 1);
+          atomicAdd(&keys_s[ty * nblk + b], 1);
+          atomicAdd(&pairs_s[ty * nblk + b], hi - lo + 1);
+        }
     }
   }
-  if (r == 0) cnt_r[n] = 0;
-  long long v = c, vs = nseg;
+  if (blockIdx.x == 0 && threadIdx.x == 0) cnt_r[n] = 0;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -214,7 +217,7 @@ __global__ void __launch_bounds__(kBinRanks) gather_counts_kernel(
   __syncthreads();
   if (threadIdx.x == 0) {
     long long t = 0, ts = 0;
-    for (int w = 0; w < kBinRanks / 32; ++w) {
+    for (int w = 0; w < kBinThreads / 32; ++w) {
       t += csum[w][0];
       ts += csum[w][1];
     }
@@ -225,16 +228,16 @@ __global__ void __launch_bounds__(kBinRanks) gather_counts_kernel(
   }
   if (!SEGS) return;
   const int64_t nb = gridDim.x;
-  for (int k = threadIdx.x; k < keys; k += kBinRanks)
+  for (int k = threadIdx.x; k < keys; k += kBinThreads) {
     cnt_r[n + 1 + k * nb + blockIdx.x] = keys_s[k];
-  for (int ty = threadIdx.x; ty < tiles_y; ty += kBinRanks)
-    if (rows_s[ty]) atomicAdd(&row_pairs[ty], rows_s[ty]);
+    if (pairs_s[k]) atomicAdd(&key_pairs[k], pairs_s[k]);
+  }
 }
 
 cudaError_t run_count_scan(void* temp, size_t temp_bytes, const int32_t* count,
                            const uint32_t* order, const int4* rect, int32_t* cnt_r,
                            int32_t* off_r, uint32_t* rank_of, int64_t n, int tiles_x,
-                           int tiles_y, int32_t* row_pairs, BinStatusDev* status,
+                           int tiles_y, int32_t* key_pairs, BinStatusDev* status,
                            cudaStream_t stream) {
   const bool segs = tiles_x > 0;
   const int nblk = segs ? seg_blocks(tiles_x) : 0;
@@ -243,14 +246,14 @@ cudaError_t run_count_scan(void* temp, size_t temp_bytes, const int32_t* count,
   cudaError_t e = cudaMemsetAsync(status, 0, sizeof(BinStatusDev), stream);
   if (e != cudaSuccess) return e;
   if (segs) {
-    e = cudaMemsetAsync(row_pairs, 0, tiles_y * sizeof(int32_t), stream);
+    e = cudaMemsetAsync(key_pairs, 0, keys * sizeof(int32_t), stream);
     if (e != cudaSuccess) return e;
-    gather_counts_kernel<true><<<nb, kBinRanks, (keys + tiles_y) * sizeof(int), stream>>>(
-        count, order, rect, cnt_r, rank_of, n, tiles_y, nblk, row_pairs, status);
+    gather_counts_kernel<true><<<nb, kBinThreads, 2 * keys * sizeof(int), stream>>>(
+        count, order, rect, cnt_r, rank_of, n, tiles_y, nblk, key_pairs, status);
   } else {
-    gather_counts_kernel<false><<<nb, kBinRanks, 0, stream>>>(count, order, rect, cnt_r,
-                                                              rank_of, n, 0, 0, row_pairs,
-                                                              status);
+    gather_counts_kernel<false><<<nb, kBinThreads, 0, stream>>>(count, order, rect, cnt_r,
+                                                                rank_of, n, 0, 0, key_pairs,
+                                                                status);
   }
   note_launch();
   e = cudaGetLastError();
@@ -320,16 +323,17 @@ __device__ __forceinline__ int div_small(int a, int b, float inv_b) {
   return q;
 }
 
-// Emit: one CTA per block of kBinRanks depth ranks (8 warps x 32 ranks, the count
-// pass's blocks).  Warp w's segments, in generation order (splat-major, then tile
-// row, then column block), go to
+// Emit: one CTA per block of kBinRanks depth ranks, 8 warps x 128 ranks (4
+// sub-blocks of 32), the count pass's blocks.  Warp w's segments, in generation
+// order (splat-major, then tile row, then column block), go to
 //   the key's bucket base (the scan) + the earlier warps' segments of that key +
 //   the warp's earlier segments of that key (ballot peers, in segment order),
 // so every bucket holds its segments in depth-rank order.
 // CTA 0 also lays out the fill passes' chunks (kSegChunk segments, key-aligned).
-__global__ void __launch_bounds__(kBinRanks) seg_emit_kernel(RowBinArgs a) {
+__global__ void __launch_bounds__(kBinThreads) seg_emit_kernel(RowBinArgs a) {
   extern __shared__ int wkey[];  // [8][keys]
-  __shared__ int scan_tot[kBinRanks / 32];
+  __shared__ int scan_tot[kBinThreads / 32];
+  constexpr int kSub = kBinRanks / kBinThreads;  // sub-blocks of 32 ranks per warp
   long long p64;
   if (bin_overflowed(a, &p64)) {
     if (blockIdx.x == 0 && threadIdx.x == 0) a.status->flags |= kBinFlagOverflow;
@@ -339,7 +343,7 @@ __global__ void __launch_bounds__(kBinRanks) seg_emit_kernel(RowBinArgs a) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int K = a.keys;
   if (blockIdx.x == 0) {
-    constexpr int kPer = kBinMaxKeys / kBinRanks;
+    constexpr int kPer = kBinMaxKeys / kBinThreads;
     int nch[kPer], tot = 0;
 #pragma unroll
     for (int q = 0; q < kPer; ++q) {
@@ -358,29 +362,39 @@ __global__ void __launch_bounds__(kBinRanks) seg_emit_kernel(RowBinArgs a) {
     }
     if (threadIdx.x == 0) a.chunk_first[K] = all;
   }
-  for (int e = threadIdx.x; e < 8 * K; e += kBinRanks) wkey[e] = 0;
+  for (int e = threadIdx.x; e < 8 * K; e += kBinThreads) wkey[e] = 0;
   __syncthreads();
-  const int64_t r = (int64_t)blockIdx.x * kBinRanks + threadIdx.x;
-  const int c = r < a.n ? a.cnt_r[r] : 0;
-  uint32_t v = 0;
-  int4 rc = make_int4(0, 0, 0, 0);
-  int nbl = 1, b0 = 0, ns = 0;
-  if (c > 0) {
-    v = a.order[r];
-    const uint32_t i = v & kIndexMask;
-    rc = a.rect[i];
-    const int spans_x = rc.y - rc.x + 1;
-    // pair (tx, ty) of this splat has generation index origin + ty * spans_x + tx
-    reinterpret_cast<float*>(a.rec)[(size_t)i * kRecordFloats + R_ROW_ORIGIN] =
-        __int_as_float(a.off_r[r] - rc.z * spans_x - rc.x);
-    b0 = rc.x / kSegCols;
-    nbl = rc.y / kSegCols - b0 + 1;
-    ns = (rc.w - rc.z + 1) * nbl;
-    for (int ty = rc.z; ty <= rc.w; ++ty)
-      for (int b = 0; b < nbl; ++b) atomicAdd(&wkey[w * K + ty * a.nblk + b0 + b], 1);
+  // this lane's splat of each sub-block: rank base + w * 128 + sub * 32 + lane
+  const int64_t r0 = (int64_t)blockIdx.x * kBinRanks + w * (32 * kSub) + lane;
+  uint32_t v[kSub];
+  int4 rc[kSub];
+  int nbl[kSub], b0[kSub], ns[kSub];
+#pragma unroll
+  for (int q = 0; q < kSub; ++q) {
+    const int64_t r = r0 + 32 * q;
+    const int c = r < a.n ? a.cnt_r[r] : 0;
+    v[q] = 0;
+    rc[q] = make_int4(0, 0, 0, 0);
+    nbl[q] = 1;
+    b0[q] = 0;
+    ns[q] = 0;
+    if (c > 0) {
+      v[q] = a.order[r];
+      const uint32_t i = v[q] & kIndexMask;
+      rc[q] = a.rect[i];
+      const int spans_x = rc[q].y - rc[q].x + 1;
+      // pair (tx, ty) of this splat has generation index origin + ty * spans_x + tx
+      reinterpret_cast<float*>(a.rec)[(size_t)i * kRecordFloats + R_ROW_ORIGIN] =
+          __int_as_float(a.off_r[r] - rc[q].z * spans_x - rc[q].x);
+      b0[q] = rc[q].x / kSegCols;
+      nbl[q] = rc[q].y / kSegCols - b0[q] + 1;
+      ns[q] = (rc[q].w - rc[q].z + 1) * nbl[q];
+      for (int ty = rc[q].z; ty <= rc[q].w; ++ty)
+        for (int b = 0; b < nbl[q]; ++b) atomicAdd(&wkey[w * K + ty * a.nblk + b0[q] + b], 1);
+    }
   }
   __syncthreads();
-  for (int k = threadIdx.x; k < K; k += kBinRanks) {
+  for (int k = threadIdx.x; k < K; k += kBinThreads) {
     int base = a.off_r[a.n + 1 + (int64_t)k * a.nb + blockIdx.x] - p;
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
@@ -391,48 +405,51 @@ __global__ void __launch_bounds__(kBinRanks) seg_emit_kernel(RowBinArgs a) {
   }
   __syncthreads();
   int* cur = wkey + w * K;
-  int incl = ns;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int t = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += t;
-  }
-  const int excl = incl - ns;
-  const int total = __shfl_sync(0xffffffffu, incl, 31);
   const unsigned lt = (1u << lane) - 1u;
   const int kbits = bit_width(K);  // keys 0..K (K: no segment)
-  const float inv_nbl = 1.0f / (float)nbl;
-  for (int j0 = 0; j0 < total; j0 += 32) {
-    const int j = j0 + lane;
-    int sidx = 0;
 #pragma unroll
-    for (int step = 16; step > 0; step >>= 1) {
-      const int cand = sidx + step;
-      const int e = __shfl_sync(0xffffffffu, excl, cand & 31);
-      if (cand < 32 && e <= j) sidx = cand;
+  for (int q = 0; q < kSub; ++q) {
+    int incl = ns[q];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
     }
-    const int es = __shfl_sync(0xffffffffu, excl, sidx);
-    const int sn = __shfl_sync(0xffffffffu, nbl, sidx);
-    const float sinv = __shfl_sync(0xffffffffu, inv_nbl, sidx);
-    const int sb0 = __shfl_sync(0xffffffffu, b0, sidx);
-    const int x0 = __shfl_sync(0xffffffffu, rc.x, sidx);
-    const int x1 = __shfl_sync(0xffffffffu, rc.y, sidx);
-    const int y0 = __shfl_sync(0xffffffffu, rc.z, sidx);
-    const uint32_t vs = __shfl_sync(0xffffffffu, v, sidx);
-    const bool live = j < total;
-    const int l = j - es;
-    const int row = div_small(l, sn, sinv);
-    const int b = sb0 + (l - row * sn);
-    const int key = live ? (y0 + row) * a.nblk + b : K;
-    const unsigned peers = warp_peers(key, kbits);
-    const int pos = live ? cur[key] + __popc(peers & lt) : 0;
-    __syncwarp();
-    if (live && lane == __ffs(peers) - 1) cur[key] += __popc(peers);
-    __syncwarp();
-    if (live) {
-      const int lo = max(x0, b * kSegCols) - b * kSegCols;
-      const int hi = min(x1, b * kSegCols + kSegCols - 1) - b * kSegCols;
-      a.segs[pos] = make_uint2(vs, (uint32_t)(lo | ((hi - lo + 1) << 5)));
+    const int excl = incl - ns[q];
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    const float inv_nbl = 1.0f / (float)nbl[q];
+    for (int j0 = 0; j0 < total; j0 += 32) {
+      const int j = j0 + lane;
+      int sidx = 0;
+#pragma unroll
+      for (int step = 16; step > 0; step >>= 1) {
+        const int cand = sidx + step;
+        const int e = __shfl_sync(0xffffffffu, excl, cand & 31);
+        if (cand < 32 && e <= j) sidx = cand;
+      }
+      const int es = __shfl_sync(0xffffffffu, excl, sidx);
+      const int sn = __shfl_sync(0xffffffffu, nbl[q], sidx);
+      const float sinv = __shfl_sync(0xffffffffu, inv_nbl, sidx);
+      const int sb0 = __shfl_sync(0xffffffffu, b0[q], sidx);
+      const int x0 = __shfl_sync(0xffffffffu, rc[q].x, sidx);
+      const int x1 = __shfl_sync(0xffffffffu, rc[q].y, sidx);
+      const int y0 = __shfl_sync(0xffffffffu, rc[q].z, sidx);
+      const uint32_t vs = __shfl_sync(0xffffffffu, v[q], sidx);
+      const bool live = j < total;
+      const int l = j - es;
+      const int row = div_small(l, sn, sinv);
+      const int b = sb0 + (l - row * sn);
+      const int key = live ? (y0 + row) * a.nblk + b : K;
+      const unsigned peers = warp_peers(key, kbits);
+      const int pos = live ? cur[key] + __popc(peers & lt) : 0;
+      __syncwarp();
+      if (live && lane == __ffs(peers) - 1) cur[key] += __popc(peers);
+      __syncwarp();
+      if (live) {
+        const int lo = max(x0, b * kSegCols) - b * kSegCols;
+        const int hi = min(x1, b * kSegCols + kSegCols - 1) - b * kSegCols;
+        a.segs[pos] = make_uint2(vs, (uint32_t)(lo | ((hi - lo + 1) << 5)));
+      }
     }
   }
 }
@@ -485,64 +502,69 @@ __global__ void __launch_bounds__(256) seg_count_kernel(RowBinArgs a) {
   a.seg_cnt[(int64_t)c * 32 + lane] = cnt;
 }
 
-// Fill pass 2: one CTA per tile row.  Each tile's chunk counts become exclusive
-// prefixes over its key's chunks (in place); the tiles' totals, scanned along the
-// row from the pairs of the rows above, are the row's tile_starts
+// Fill pass 2: one CTA per key (tile row, column block); lane L of each warp is
+// tile column L of the block.  Each tile's chunk counts become exclusive prefixes
+// over the key's chunks (in place; the 8 warps take consecutive chunk ranges);
+// the tile totals, scanned across the block from the pairs of every earlier key
+// (row-major, the count pass's per-key pair totals), are the block's tile_starts
 // (np.searchsorted's CSR, rasterizer.py:324-325).  On overflow every tile list is
 // left empty, so the blends and K7 see no pairs.
 __global__ void __launch_bounds__(256) tile_scan_kernel(RowBinArgs a) {
-  __shared__ int tot_s[kBinMaxCols];
-  __shared__ int scan_tot[8];
+  __shared__ int part[8][32];
+  __shared__ int red[8];
   long long p64;
-  const int ty = blockIdx.x, X = a.tiles_x;
+  const int key = blockIdx.x, X = a.tiles_x;
+  const int ty = key / a.nblk, b = key - ty * a.nblk;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int tx = b * kSegCols + lane;
   if (bin_overflowed(a, &p64)) {
-    for (int t = threadIdx.x; t < X; t += 256) a.tile_starts[ty * X + t] = 0;
-    if (ty == a.tiles_y - 1 && threadIdx.x == 0) a.tile_starts[a.tiles_y * X] = 0;
+    if (w == 0 && tx < X) a.tile_starts[ty * X + tx] = 0;
+    if (key == a.keys - 1 && threadIdx.x == 0) a.tile_starts[a.tiles_y * X] = 0;
     return;
   }
   const int p = (int)p64;
-  for (int t = threadIdx.x; t < X; t += 256) {
-    const int key = ty * a.nblk + t / kSegCols, L = t % kSegCols;
-    const int c0 = a.chunk_first[key], c1 = a.chunk_first[key + 1];
-    int run = 0;
-    int32_t* h = a.seg_cnt + (int64_t)c0 * 32 + L;
-    // 16 independent loads in flight per step (a key's chunks are many at c5)
-    for (int c = c0; c < c1; c += 16, h += 16 * 32) {
-      int v[16];
-#pragma unroll
-      for (int k = 0; k < 16; ++k) v[k] = c + k < c1 ? h[k * 32] : 0;
-#pragma unroll
-      for (int k = 0; k < 16; ++k) {
-        if (c + k < c1) h[k * 32] = run;
-        run += v[k];
-      }
-    }
-    tot_s[t] = run;
-  }
-  // pairs of the rows above (up to kBinMaxRows values, summed by every CTA)
+  const int c0 = a.chunk_first[key], c1 = a.chunk_first[key + 1];
+  const int per = (c1 - c0 + 7) / 8;
+  const int w0 = c0 + min(c1 - c0, w * per), w1 = c0 + min(c1 - c0, (w + 1) * per);
+  int32_t* h = a.seg_cnt + (int64_t)w0 * 32 + lane;
+  int run = 0;
+  for (int c = w0; c < w1; ++c, h += 32) run += *h;
+  part[w][lane] = run;
+  // pairs of every earlier key: the rows above and this row's earlier blocks
   int above = 0;
-  for (int q = threadIdx.x; q < ty; q += 256) above += a.row_pairs[q];
+  for (int k = threadIdx.x; k < key; k += 256) above += a.key_pairs[k];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) above += __shfl_xor_sync(0xffffffffu, above, o);
+  if (lane == 0) red[w] = above;
   __syncthreads();
-  constexpr int kPer = kBinMaxCols / 256;
-  int loc = 0;
+  int before = 0, total = 0;
 #pragma unroll
-  for (int k = 0; k < kPer; ++k) {
-    const int t = threadIdx.x * kPer + k;
-    loc += t < X ? tot_s[t] : 0;
+  for (int q = 0; q < 8; ++q) {
+    const int t = part[q][lane];
+    before += q < w ? t : 0;
+    total += t;
   }
-  int excl, excl_above;
-  block_exclusive_scan(loc, &excl, scan_tot);
-  const int row_base = block_exclusive_scan(above, &excl_above, scan_tot);
-  int base = row_base + excl;
+  // second pass: exclusive prefixes in place
+  run = before;
+  h = a.seg_cnt + (int64_t)w0 * 32 + lane;
+  for (int c = w0; c < w1; ++c, h += 32) {
+    const int t = *h;
+    *h = run;
+    run += t;
+  }
+  if (w == 0) {
+    int base = 0;
 #pragma unroll
-  for (int k = 0; k < kPer; ++k) {
-    const int t = threadIdx.x * kPer + k;
-    if (t < X) {
-      a.tile_starts[ty * X + t] = base;
-      base += tot_s[t];
+    for (int q = 0; q < 8; ++q) base += red[q];
+    int incl = total;  // tile totals scanned across the block's 32 columns
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
     }
+    if (tx < X) a.tile_starts[ty * X + tx] = base + incl - total;
+    if (key == a.keys - 1 && lane == 0) a.tile_starts[a.tiles_y * X] = p;
   }
-  if (ty == a.tiles_y - 1 && threadIdx.x == 0) a.tile_starts[a.tiles_y * X] = p;
 }
 
 // Fill pass 3: per chunk (one warp), the values of the segments covering each tile
@@ -599,9 +621,9 @@ cudaError_t run_row_binning(const RowBinArgs& a, cudaStream_t stream) {
   // the attribute is set once per device: set it for the largest key count
   cudaError_t e = set_dynamic_smem<seg_emit_kernel>(8 * kBinMaxKeys * (int)sizeof(int));
   if (e != cudaSuccess) return e;
-  seg_emit_kernel<<<(unsigned)a.nb, kBinRanks, 8 * a.keys * sizeof(int), stream>>>(a);
+  seg_emit_kernel<<<(unsigned)a.nb, kBinThreads, 8 * a.keys * sizeof(int), stream>>>(a);
   seg_count_kernel<<<fill_grid, 256, 0, stream>>>(a);
-  tile_scan_kernel<<<(unsigned)a.tiles_y, 256, 0, stream>>>(a);
+  tile_scan_kernel<<<(unsigned)a.keys, 256, 0, stream>>>(a);
   seg_fill_kernel<<<fill_grid, 256, 0, stream>>>(a);
   note_launch(4);
   return cudaGetLastError();

@@ -72,7 +72,7 @@ struct FrameBufs {
   int32_t* xlocal;
   float4* merged;
   int32_t* chunk_first;
-  int32_t* row_pairs;
+  int32_t* key_pairs;
   int32_t* order_fwd;   // longest-first tile orders of K5 / K6
   int32_t* order_bwd;
   int32_t* tile_work;   // K5 -> K6: per-tile largest terminal count
@@ -138,7 +138,7 @@ static FrameBufs carve_frame(void* ws, int64_t n, int tiles_x, int tiles_y, size
   f.xlocal = c.take<int32_t>(n + 1);
   f.merged = c.take<float4>(4 * (size_t)n);
   f.chunk_first = c.take<int32_t>(seg_keys(tiles_x, tiles_y) + 1);
-  f.row_pairs = c.take<int32_t>(tiles_y);
+  f.key_pairs = c.take<int32_t>(seg_keys(tiles_x, tiles_y));
   f.order_fwd = c.take<int32_t>(n_tiles);
   f.order_bwd = c.take<int32_t>(n_tiles);
   f.tile_work = c.take<int32_t>(n_tiles);
@@ -357,7 +357,7 @@ static cudaError_t count_scan(const hs_frame* frame, const FrameBufs& f, cudaStr
   const bool segs = row_binning_ok(frame->tiles_x, frame->tiles_y);
   return run_count_scan(f.temp, f.temp_bytes, f.count, f.order, f.rect, f.cnt_r, f.off_r,
                         f.rank_of, frame->n, segs ? frame->tiles_x : 0, frame->tiles_y,
-                        f.row_pairs, f.status, stream);
+                        f.key_pairs, f.status, stream);
 }
 
 int hs_preprocess_fwd(hs_frame* frame, const hs_scene* scene, const hs_camera* cam,
@@ -472,7 +472,7 @@ static int row_bin(hs_frame* frame, const FrameBufs& f, const BinBufs& b, cudaSt
   a.cnt_r = f.cnt_r;
   a.off_r = f.off_r;
   a.status = f.status;
-  a.row_pairs = f.row_pairs;
+  a.key_pairs = f.key_pairs;
   a.n = frame->n;
   a.nb = (int)bin_row_blocks(frame->n);
   a.tiles_x = frame->tiles_x;

@@ -124,7 +124,11 @@ cudaError_t run_depth_sort_hi(void* temp, size_t temp_bytes, const uint64_t* key
 // per-pair cost is one predicated store.  P stays on the device: the caller sizes
 // the binning workspace for a pair capacity, and a frame whose P exceeds it is
 // flagged (kBinFlagOverflow) with every tile list left empty.
-constexpr int kBinRanks = 256;
+#ifndef HS_BIN_RANKS
+#define HS_BIN_RANKS 256
+#endif
+constexpr int kBinRanks = HS_BIN_RANKS;  // depth ranks per CTA of the count and emit passes
+constexpr int kBinThreads = 256;  // 8 warps, each kBinRanks / 8 ranks (sub-blocks of 32)
 constexpr int kSegCols = 32;        // tile columns per block (one warp's lanes)
 constexpr int kBinMaxCols = 2048;   // tiles_x limit (larger images: CUB pair sort)
 constexpr int kBinMaxRows = 1024;   // tiles_y limit
@@ -159,12 +163,12 @@ struct BinStatusDev {   // in the frame's counters
 
 // cnt_r[r] = count[order[r]], off_r = exclusive scan (count_scan_len entries),
 // rank_of[order[r]] = r, P as int64 in *status (zeroed here); with the segment
-// path (tiles_x > 0) also the segment histograms and row_pairs[tiles_y] (pairs per
-// tile row, zeroed here).
+// path (tiles_x > 0) also the segment histograms and key_pairs[keys] (pairs per
+// (tile row, column block) key, zeroed here).
 cudaError_t run_count_scan(void* temp, size_t temp_bytes, const int32_t* count,
                            const uint32_t* order, const int4* rect, int32_t* cnt_r,
                            int32_t* off_r, uint32_t* rank_of, int64_t n, int tiles_x,
-                           int tiles_y, int32_t* row_pairs, BinStatusDev* status,
+                           int tiles_y, int32_t* key_pairs, BinStatusDev* status,
                            cudaStream_t stream);
 struct RowBinArgs {
   const uint32_t* order;
@@ -173,7 +177,7 @@ struct RowBinArgs {
   const int32_t* cnt_r;
   const int32_t* off_r;
   BinStatusDev* status;
-  const int32_t* row_pairs;  // [tiles_y]
+  const int32_t* key_pairs;  // [keys] pairs per (tile row, column block)
   int64_t n;
   int nb;  // rank blocks
   int tiles_x, tiles_y, nblk, keys;
