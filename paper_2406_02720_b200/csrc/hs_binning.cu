@@ -567,14 +567,22 @@ __global__ void __launch_bounds__(256) tile_scan_kernel(RowBinArgs a) {
   }
 }
 
-// Fill pass 3: per chunk (one warp), the values of the segments covering each tile
-// column L of the key's block are appended, in segment (= depth rank) order, at
-// tile_starts[tile] + the chunk's prefix: a stable counting sort by tile, so each
-// tile list equals np.lexsort((index, depth, tile)) (rasterizer.py:318-323).  The
-// warp holds 32 segments (one per lane) and walks the block's columns: a ballot
-// says which segments cover column L, and the covering lanes store their values
-// at consecutive positions of tile L's list -- one coalesced store per column
-// instead of one scattered store per pair.
+// Fill pass 3: per chunk (one warp), lane L owns tile column L of the key's block;
+// the values of the segments covering it are appended, in segment (= depth rank)
+// order, at tile_starts[tile] + the chunk's prefix: a stable counting sort by
+// tile, so each tile list equals np.lexsort((index, depth, tile))
+// (rasterizer.py:318-323).  The warp loads 32 segments at a time (one per lane).
+// Two ways to write them, chosen per key by its mean segment length:
+// * narrow segments (small splats, c3/c4): the segments are broadcast in order and
+//   each lane stores for its own column -- a few instructions per segment;
+// * wide segments (c5): the columns are walked, a ballot names the segments that
+//   cover a column and they store at consecutive positions of its list -- one
+//   coalesced store per column, but two population counts per lane (XU pipe).
+// Measured per view: narrow c3 0.110 / c4 0.330 / c5 0.81 ms; wide 0.139 / 0.37 /
+// 0.52 ms (binning stage).
+#ifndef HS_FILL_WIDE
+#define HS_FILL_WIDE 6  // mean pairs per segment from which the column walk is used
+#endif
 __global__ void __launch_bounds__(256) seg_fill_kernel(RowBinArgs a) {
   long long p64;
   if (bin_overflowed(a, &p64)) return;
@@ -584,33 +592,32 @@ __global__ void __launch_bounds__(256) seg_fill_kernel(RowBinArgs a) {
   int key, begin, end;
   if (!seg_chunk_of(a, (int)p64, c, &key, &begin, &end)) return;
   const int ty = key / a.nblk, tx = (key - ty * a.nblk) * kSegCols + lane;
-  int base = tx < a.tiles_x ? a.tile_starts[ty * a.tiles_x + tx] +
-                                  a.seg_cnt[(int64_t)c * 32 + lane]
-                            : 0;
+  int pos = tx < a.tiles_x ? a.tile_starts[ty * a.tiles_x + tx] +
+                                 a.seg_cnt[(int64_t)c * 32 + lane]
+                           : 0;
+  const int key_segs = key_start(a, key + 1, (int)p64) - key_start(a, key, (int)p64);
+  const bool wide = a.key_pairs[key] >= HS_FILL_WIDE * key_segs;
   for (int s0 = begin; s0 < end; s0 += 32) {
     const uint2 sg = s0 + lane < end ? a.segs[s0 + lane] : make_uint2(0u, 0u);
-    const int lo = (int)(sg.y & 31u), len = (int)(sg.y >> 5);
-    // columns any of the 32 segments covers
-    const unsigned span = len ? (0xffffffffu >> (32 - len)) << lo : 0u;
-    unsigned cols = __reduce_or_sync(0xffffffffu, span);
-    const int m = min(32, end - s0);
-    if (__popc(cols) > m + (m >> 1)) {
-      // narrow segments (small splats): one pass per segment is shorter, each lane
-      // storing for its own column when the segment covers it
-      for (int k = 0; k < m; ++k) {
-        const unsigned sk = __shfl_sync(0xffffffffu, span, k);
-        const uint32_t vk = __shfl_sync(0xffffffffu, sg.x, k);
-        if ((sk >> lane) & 1u) a.pair_src[base++] = vk;
+    const uint32_t len = sg.y >> 5;
+    const uint32_t span = len ? (0xffffffffu >> (32 - len)) << (sg.y & 31u) : 0u;
+    if (wide) {
+      unsigned cols = __reduce_or_sync(0xffffffffu, span);
+      while (cols) {
+        const int L = __ffs(cols) - 1;
+        cols &= cols - 1;
+        const unsigned m = __ballot_sync(0xffffffffu, (span >> L) & 1u);
+        const int b = __shfl_sync(0xffffffffu, pos, L);
+        if ((span >> L) & 1u) a.pair_src[b + __popc(m & lt)] = sg.x;
+        if (lane == L) pos += __popc(m);
       }
-      continue;
-    }
-    while (cols) {
-      const int L = __ffs(cols) - 1;
-      cols &= cols - 1;
-      const unsigned m = __ballot_sync(0xffffffffu, (span >> L) & 1u);
-      const int b = __shfl_sync(0xffffffffu, base, L);
-      if ((span >> L) & 1u) a.pair_src[b + __popc(m & lt)] = sg.x;
-      if (lane == L) base += __popc(m);
+    } else {
+      const int m = min(32, end - s0);
+      for (int k = 0; k < m; ++k) {
+        const uint32_t sk = __shfl_sync(0xffffffffu, span, k);
+        const uint32_t vk = __shfl_sync(0xffffffffu, sg.x, k);
+        if ((sk >> lane) & 1u) a.pair_src[pos++] = vk;
+      }
     }
   }
 }

@@ -1,0 +1,29 @@
+#!/bin/bash
+# profiles/round2 evidence on one GPU: the full bench line, launch lists of one c3 / c4 /
+# c5 step, and ncu --set full captures (summaries + per-line tables) of the step's
+# kernels at c3.  Every ncu command profiles a program that first ran plainly and
+# exited 0.  Output: gpurun_out/r2/ (copy the summaries into profiles/round2/).
+set -u
+O=gpurun_out/r2
+mkdir -p $O
+timeout 1200 python bench.py --steps 20 --warmup 3 > $O/bench_full.log 2>&1
+echo "bench=$?" > $O/status.txt
+for CFG in c3 c4 c5; do
+  CMD="python bench.py --config $CFG --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-clocks --no-configs --no-graph"
+  timeout 600 $CMD > $O/plain_$CFG.log 2>&1 || { echo "plain $CFG failed" >> $O/status.txt; continue; }
+  N=150; W=3
+  if [ $CFG = c4 ]; then N=700; W=20; fi
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c $N --csv \
+    --log-file $O/launches_$CFG.csv $CMD > $O/ncu_list_$CFG.log 2>&1
+  python tools/launch_list.py $O/launches_$CFG.csv $W > $O/launch_list_$CFG.txt 2>&1
+  echo "list_$CFG=$?" >> $O/status.txt
+done
+CMD="python bench.py --config c3 --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-clocks --no-configs --no-graph"
+for K in blend_bwd blend_fwd preprocess_bwd_kernel preprocess_fwd_kernel merge_rows seg_emit \
+         seg_fill gather_counts; do
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$K -s 3 -c 1 \
+    -o $O/prof_$K -f $CMD > $O/ncu_$K.log 2>&1
+  echo "$K=$?" >> $O/status.txt
+  python tools/ncu_summary.py $O/prof_$K.ncu-rep > $O/ncu_$K.txt 2>&1
+  python tools/ncu_lines.py $O/prof_$K.ncu-rep 30 > $O/lines_$K.txt 2>&1
+done
