@@ -256,16 +256,18 @@ __device__ __forceinline__ float box_min_q(float a, float b, float c, float xl, 
 }
 
 // window code of a staged record (raw conic, before any prescale) in the tile
-// whose first pixel centre is (x0, y0)
+// (or sub-tile of 2 H rows: H = pixels per lane) whose first pixel centre is (x0, y0)
+template <int H = kPx>
 __device__ __forceinline__ int strip_window(const float4 (&q)[4], float x0, float y0) {
   if (__float_as_uint(q[3].y) & kFlagNoWin) return kWinAll;
   const float2 lo = __half22float2(*reinterpret_cast<const __half2*>(&q[3].w));
   const float xl = (x0 - q[0].x) - lo.x, xh = xl + (float)(kTile - 1);
   const float a = q[0].z, b = q[0].w, c = q[1].x;
-  // the windows are halves (strips 0-1, 2-3): one box per half, rows 0-7 and 8-15
+  // the windows are halves: one box per half, rows 0..H-1 and H..2H-1
   const float yl = (y0 - q[0].y) - lo.y;
-  const bool low = !(box_min_q(a, b, c, xl, xh, yl, yl + 7.0f) > kSkipQ);
-  const bool high = !(box_min_q(a, b, c, xl, xh, yl + 8.0f, yl + 15.0f) > kSkipQ);
+  const bool low = !(box_min_q(a, b, c, xl, xh, yl, yl + (float)(H - 1)) > kSkipQ);
+  const bool high = !(box_min_q(a, b, c, xl, xh, yl + (float)H, yl + (float)(2 * H - 1)) > kSkipQ);
+  if (H <= 2) return (low || high) ? kWinAll : 0;  // one pixel pair: no half windows
   return (low ? 1 : 0) | (high ? 2 : 0);
 }
 
@@ -288,8 +290,10 @@ __device__ __forceinline__ void with_window(int win, F&& f) {
 // pixels outside the image start dead.  The colour/depth accumulators hold the
 // NEGATED sums (T - w T = fma(-w, T, T) needs -w; the sign is restored at the
 // store).  Dead pixels compute and discard.
+template <int NPX = kPx>
 struct FwdPix {
-  float2 T[kPairs], A[kPairs], C[kPairs], ar[kPairs], ag[kPairs], ab[kPairs], ad[kPairs];
+  static constexpr int NP = NPX / 2;
+  float2 T[NP], A[NP], C[NP], ar[NP], ag[NP], ab[NP], ad[NP];
 };
 
 __device__ __forceinline__ float ge_mask(float v) { return v >= kTerminationT ? 1.0f : 0.0f; }
@@ -315,14 +319,14 @@ __device__ __forceinline__ void fwd_commit(float nw, float& T, float& A, float& 
 // the side-record form.
 // Pairs [P0, P0 + NP) are evaluated; the others are outside the splat's strip
 // window and only count the commit of their alive pixels (see strip_window).
-template <bool STEEP, int P0 = 0, int NP = kPairs>
+template <bool STEEP, int P0, int NP, int NPX>
 __device__ __forceinline__ void fwd_splat_fast(const float4 (&q)[4], const SteepRec& side,
-                                               float px, float py0, FwdPix& P) {
+                                               float px, float py0, FwdPix<NPX>& P) {
   const SplatLane s = splat_lane<STEEP, true>(q, side, px, py0);
   const float nc1 = q[1].w, nc2 = q[2].x;  // negated by prescale_record
   const float cr = q[2].y, cg = q[2].z, cb = q[2].w, z = q[3].x;
 #pragma unroll
-  for (int p = 0; p < kPairs; ++p) {
+  for (int p = 0; p < NPX / 2; ++p) {
     if (p < P0 || p >= P0 + NP) {
       P.C[p] = fadd2(P.C[p], P.A[p]);
       continue;
@@ -346,9 +350,10 @@ __device__ __forceinline__ void fwd_splat_fast(const float4 (&q)[4], const Steep
 }
 
 // Generic: steep (FP64 z), sign mode, clamped weights; scalar per pixel.
+template <int NPX>
 __device__ __forceinline__ void fwd_splat_generic(const float4 (&q)[4], const SteepRec& side,
                                                   uint32_t flags, float px, float py0,
-                                                  FwdPix& P) {
+                                                  FwdPix<NPX>& P) {
   const bool steep = flags & kFlagSteep;
   const SplatLane s = steep ? splat_lane<true, true>(q, side, px, py0)
                             : splat_lane<false, true>(q, side, px, py0);
@@ -357,7 +362,7 @@ __device__ __forceinline__ void fwd_splat_generic(const float4 (&q)[4], const St
   const float cr = q[2].y, cg = q[2].z, cb = q[2].w, z = q[3].x;
   const bool large = flags & kFlagNoWin;  // s.A, s.C = scaled a, D; q[0].w = r
 #pragma unroll
-  for (int i = 0; i < kPx; ++i) {
+  for (int i = 0; i < NPX; ++i) {
     const int p = i >> 1, h = i & 1;
     const float dy = s.dy0 + 2.0f * i;
     const float u = fmaf(q[0].w, dy, s.dx);
@@ -380,34 +385,54 @@ __device__ __forceinline__ void prescale_record(float4 (&r)[4]) {
   r[2].x = -r[2].x;
 }
 
-// Window mask (strip_window codes are a 2-bit mask: 1 pairs 0-1, 2 pairs 2-3) of
-// the halves of the tile that still have an alive pixel in some lane.  A dead
-// half never changes again, so it joins the windows as skipped work.
-__device__ __forceinline__ int alive_halves(const FwdPix& P) {
-  const float lo = fmaxf(fmaxf(P.A[0].x, P.A[0].y), fmaxf(P.A[1].x, P.A[1].y));
-  const float hi = fmaxf(fmaxf(P.A[2].x, P.A[2].y), fmaxf(P.A[3].x, P.A[3].y));
+// Window mask (strip_window codes are a 2-bit mask: 1 first half of the pairs, 2
+// second half) of the halves of the (sub-)tile that still have an alive pixel in
+// some lane.  A dead half never changes again, so it joins the windows as skipped
+// work.  With one pixel pair per lane there are no halves: 3 or 0.
+template <int NPX>
+__device__ __forceinline__ int alive_halves(const FwdPix<NPX>& P) {
+  constexpr int NP = NPX / 2;
+  float lo = 0.f, hi = 0.f;
+#pragma unroll
+  for (int p = 0; p < NP; ++p) {
+    const float a = fmaxf(P.A[p].x, P.A[p].y);
+    if (NP == 1 || p < NP / 2) lo = fmaxf(lo, a); else hi = fmaxf(hi, a);
+  }
+  if (NP == 1) return __any_sync(0xffffffffu, lo > 0.0f) ? kWinAll : 0;
   return (__any_sync(0xffffffffu, lo > 0.0f) ? 1 : 0) | (__any_sync(0xffffffffu, hi > 0.0f) ? 2 : 0);
 }
 
+// A forward work unit: a 16-column by 2 * NPX-row sub-tile (the whole 16 x 16 tile
+// at NPX = 8).  Small frames (c1's 64 tiles, c2's 2500 against 2368 resident warps)
+// split their tiles into 2 or 4 sub-tiles, so more warps share the work and each
+// stops when its own pixels are done.
+template <int NPX>
 __global__ void HS_FWD_BOUNDS blend_fwd_kernel(
     BlendGeom g, float bg0, float bg1, float bg2, float* __restrict__ color,
     float* __restrict__ alpha, float* __restrict__ depth, float* __restrict__ trans,
     int32_t* __restrict__ terminal) {
+  constexpr int NP = NPX / 2;
+  constexpr int SUB = kPx / NPX;  // sub-tiles per tile
   __shared__ WarpStage stage_all[kFwdWarps];
   const int lane = threadIdx.x & 31;
   WarpStage& st = stage_all[threadIdx.x >> 5];
   for (;;) {
-    const int tile = next_tile(g, lane);
-    if (tile < 0) break;
+    int t = 0;
+    if (lane == 0) t = atomicAdd(g.work_counter, 1);
+    t = __shfl_sync(0xffffffffu, t, 0);
+    if (t >= g.n_work * SUB) break;
+    const int tr = t / SUB, sub = t - tr * SUB;
+    const int tile = g.tile_order ? g.tile_order[tr] : g.tile_lo + tr;
     const int ty = tile / g.tiles_x, tx = tile - ty * g.tiles_x;
     const int col = tx * kTile + (lane & 15);
-    const int row0 = ty * kTile + (lane >> 4);
+    const int sy0 = ty * kTile + sub * 2 * NPX;  // first row of the sub-tile
+    const int row0 = sy0 + (lane >> 4);
     const float px = (float)col + 0.5f;
     const float py0 = (float)row0 + 0.5f;
-    const float x0 = (float)(tx * kTile) + 0.5f, y0 = (float)(ty * kTile) + 0.5f;
-    FwdPix P;
+    const float x0 = (float)(tx * kTile) + 0.5f, y0 = (float)sy0 + 0.5f;
+    FwdPix<NPX> P;
 #pragma unroll
-    for (int i = 0; i < kPx; ++i) {
+    for (int i = 0; i < NPX; ++i) {
       const int p = i >> 1, h = i & 1;
       slot(P.T[p], h) = 1.f;
       slot(P.A[p], h) = (col < g.width && row0 + 2 * i < g.height) ? 1.f : 0.f;
@@ -436,14 +461,15 @@ __global__ void HS_FWD_BOUNDS blend_fwd_kernel(
         // steep, 2 generic (the window mask then only selects among the fast bodies)
         const uint32_t fl = __float_as_uint(st.rec[s][lane][3].y);
         const int kind = (!fast_flags(fl) || (fl & kFlagNoWin)) ? 2 : ((fl & kFlagSteep) ? 1 : 0);
-        st.win[s][lane] = 4 * kind + (kind == 2 ? kWinAll : strip_window(st.rec[s][lane], x0, y0));
+        st.win[s][lane] =
+            4 * kind + (kind == 2 ? kWinAll : strip_window<NPX>(st.rec[s][lane], x0, y0));
         prescale_record(st.rec[s][lane]);
       }
       __syncwarp();
       for (int j = 0; j < nb; ++j) {
-        // dead pixels never change again: stop once the whole tile is dead, skip
-        // a dead half (checked every 8 splats; the reference checks per splat,
-        // same result)
+        // dead pixels never change again: stop once the whole (sub-)tile is dead,
+        // skip a dead half (checked every 8 splats; the reference checks per
+        // splat, same result)
         if ((j & 7) == 0) {
           alive = alive_halves(P);
           if (!(any = alive != 0)) break;
@@ -451,17 +477,18 @@ __global__ void HS_FWD_BOUNDS blend_fwd_kernel(
         const float4 q[4] = {st.rec[s][j][0], st.rec[s][j][1], st.rec[s][j][2], st.rec[s][j][3]};
         const uint32_t flags = __float_as_uint(q[3].y);
         const int key = st.win[s][j] & (~3 | alive);  // generic keeps its window bits: 8+
+        constexpr int H = NP > 1 ? NP / 2 : NP;  // pairs per half window
         switch (key) {
-          case 1: fwd_splat_fast<false, 0, 2>(q, st.side[s][j], px, py0, P); break;
-          case 2: fwd_splat_fast<false, 2, 2>(q, st.side[s][j], px, py0, P); break;
-          case 3: fwd_splat_fast<false, 0, 4>(q, st.side[s][j], px, py0, P); break;
-          case 5: fwd_splat_fast<true, 0, 2>(q, st.side[s][j], px, py0, P); break;
-          case 6: fwd_splat_fast<true, 2, 2>(q, st.side[s][j], px, py0, P); break;
-          case 7: fwd_splat_fast<true, 0, 4>(q, st.side[s][j], px, py0, P); break;
+          case 1: fwd_splat_fast<false, 0, H>(q, st.side[s][j], px, py0, P); break;
+          case 2: fwd_splat_fast<false, NP - H, H>(q, st.side[s][j], px, py0, P); break;
+          case 3: fwd_splat_fast<false, 0, NP>(q, st.side[s][j], px, py0, P); break;
+          case 5: fwd_splat_fast<true, 0, H>(q, st.side[s][j], px, py0, P); break;
+          case 6: fwd_splat_fast<true, NP - H, H>(q, st.side[s][j], px, py0, P); break;
+          case 7: fwd_splat_fast<true, 0, NP>(q, st.side[s][j], px, py0, P); break;
           case 0:
           case 4:
 #pragma unroll
-            for (int p = 0; p < kPairs; ++p) P.C[p] = fadd2(P.C[p], P.A[p]);
+            for (int p = 0; p < NP; ++p) P.C[p] = fadd2(P.C[p], P.A[p]);
             break;
           default: fwd_splat_generic(q, st.side[s][j], flags, px, py0, P); break;
         }
@@ -471,7 +498,7 @@ __global__ void HS_FWD_BOUNDS blend_fwd_kernel(
     cp_async_wait<0>();
     __syncwarp();
 #pragma unroll
-    for (int i = 0; i < kPx; ++i) {
+    for (int i = 0; i < NPX; ++i) {
       const int p = i >> 1, h = i & 1;
       const int row = row0 + 2 * i;
       if (col < g.width && row < g.height) {
@@ -491,9 +518,12 @@ __global__ void HS_FWD_BOUNDS blend_fwd_kernel(
       // positions maxc-1 .. 0), for K6's longest-first tile order
       float mc = 0.f;
 #pragma unroll
-      for (int p = 0; p < kPairs; ++p) mc = fmaxf(mc, fmaxf(P.C[p].x, P.C[p].y));
-      mc = __reduce_max_sync(0xffffffffu, (int)mc);
-      if (lane == 0) g.tile_work[tile] = (int32_t)mc;
+      for (int p = 0; p < NP; ++p) mc = fmaxf(mc, fmaxf(P.C[p].x, P.C[p].y));
+      const int m = __reduce_max_sync(0xffffffffu, (int)mc);
+      if (lane == 0) {
+        if (SUB == 1) g.tile_work[tile] = m;
+        else atomicMax(g.tile_work + tile, m);
+      }
     }
   }
 }
@@ -637,6 +667,20 @@ __device__ __forceinline__ void bwd_splat_generic(const float4 (&q)[4], const St
     D = fmaf(wt, dcr, D);
     T = Tp;
   }
+}
+
+// Pair rows are written once and read once, by K7a after the whole blend: a
+// streaming (evict-first) store keeps them from evicting the splat records the
+// blend gathers again for neighbouring tiles (HS_ROWS_STREAM=0: plain stores).
+#ifndef HS_ROWS_STREAM
+#define HS_ROWS_STREAM 1
+#endif
+__device__ __forceinline__ void row_store(float* p, float v) {
+#if HS_ROWS_STREAM
+  __stcs(p, v);
+#else
+  *p = v;
+#endif
 }
 
 // Sum 16 per-lane values over the warp with 16 shuffles (recursive halving):
@@ -852,7 +896,7 @@ __global__ void HS_BWD_BOUNDS blend_bwd_kernel(
         const int key = st.win[s][j] & (~3 | (pos < hmax_lo ? 1 : 0) | (pos < hmax_hi ? 2 : 0));
         if (key == 0 || key == 4) {
           // fast splat below 2^-27 on every live strip: a zero pair row, no reduction
-          if (!(lane & 1) && vi < kCols) rows[row * kStride + vi] = 0.f;
+          if (!(lane & 1) && vi < kCols) row_store(rows + row * kStride + vi, 0.f);
           continue;
         }
         switch (key) {
@@ -886,7 +930,7 @@ __global__ void HS_BWD_BOUNDS blend_bwd_kernel(
         v[13] = v[14] = v[15] = 0.f;
         const float total = HS_SMEM_REDUCE ? warp_reduce13_smem(v, red, lane)
                                            : warp_transpose_reduce16(v, lane);
-        if (!(lane & 1) && vi < kCols) rows[row * kStride + vi] = total;
+        if (!(lane & 1) && vi < kCols) row_store(rows + row * kStride + vi, total);
       }
       __syncwarp();
     }
@@ -1031,12 +1075,12 @@ static int blend_grid(Kernel kernel, int warps, int n_work, int* cache) {
   const int want = (n_work + warps - 1) / warps;
   return want < *cache ? (want > 0 ? want : 1) : *cache;
 }
-static int g_fwd_grid = 0, g_bwd_grid[2] = {0, 0};
+static int g_fwd_grid = 0, g_fwd_grid2 = 0, g_fwd_grid4 = 0, g_bwd_grid[2] = {0, 0};
 
 // resident warps of the persistent blends (the longest-first order pays only when
 // the tiles are several times these)
 int blend_fwd_slots() {
-  return blend_grid(blend_fwd_kernel, kFwdWarps, 1 << 30, &g_fwd_grid) * kFwdWarps;
+  return blend_grid(blend_fwd_kernel<kPx>, kFwdWarps, 1 << 30, &g_fwd_grid) * kFwdWarps;
 }
 int blend_bwd_slots() {
   return blend_grid(blend_bwd_kernel<false>, kBwdWarps, 1 << 30, &g_bwd_grid[0]) * kBwdWarps;
@@ -1047,9 +1091,28 @@ cudaError_t launch_blend_fwd(const BlendGeom& g, float bg0, float bg1, float bg2
                              cudaStream_t stream) {
   cudaError_t e = cudaMemsetAsync(g.work_counter, 0, sizeof(int), stream);
   if (e != cudaSuccess) return e;
-  blend_fwd_kernel<<<blend_grid(blend_fwd_kernel, kFwdWarps, g.n_work, &g_fwd_grid), kFwdWarps * 32, 0,
-                     stream>>>(
-      g, bg0, bg1, bg2, color, alpha, depth, trans, terminal);
+  const int sub = g.sub_tiles == 2 || g.sub_tiles == 4 ? g.sub_tiles : 1;
+  if (sub > 1 && g.tile_work) {  // max-reduced by the sub-tiles
+    e = cudaMemsetAsync(g.tile_work, 0, (size_t)g.n_work * sizeof(int32_t), stream);
+    if (e != cudaSuccess) return e;
+  }
+  const int units = g.n_work * sub;
+  switch (sub) {
+    case 4:
+      blend_fwd_kernel<2><<<blend_grid(blend_fwd_kernel<2>, kFwdWarps, units, &g_fwd_grid4),
+                             kFwdWarps * 32, 0, stream>>>(g, bg0, bg1, bg2, color, alpha, depth,
+                                                          trans, terminal);
+      break;
+    case 2:
+      blend_fwd_kernel<4><<<blend_grid(blend_fwd_kernel<4>, kFwdWarps, units, &g_fwd_grid2),
+                             kFwdWarps * 32, 0, stream>>>(g, bg0, bg1, bg2, color, alpha, depth,
+                                                          trans, terminal);
+      break;
+    default:
+      blend_fwd_kernel<kPx><<<blend_grid(blend_fwd_kernel<kPx>, kFwdWarps, units, &g_fwd_grid),
+                               kFwdWarps * 32, 0, stream>>>(g, bg0, bg1, bg2, color, alpha, depth,
+                                                            trans, terminal);
+  }
   note_launch();
   return cudaGetLastError();
 }

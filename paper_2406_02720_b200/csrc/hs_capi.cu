@@ -549,6 +549,18 @@ static bool lpt_order(int n_tiles, int slots) {
   return mode == 1 || (mode == 2 && 2 * (int64_t)n_tiles >= 3 * (int64_t)slots);
 }
 
+// K5 work units per tile: tiles split into 2 (16x8) or 4 (16x4) sub-tiles when the
+// frame has too few tiles to fill the resident warps 1.5 times (HS_SUBTILE=1/2/4
+// forces a split).
+static int fwd_sub_tiles(int n_tiles, int slots) {
+  const char* env = getenv("HS_SUBTILE");  // read per call: tests switch it
+  const int forced = env ? atoi(env) : 0;
+  if (forced == 1 || forced == 2 || forced == 4) return forced;
+  for (int sub = 1; sub < 4; sub *= 2)
+    if (2 * (int64_t)n_tiles * sub >= 3 * (int64_t)slots) return sub;
+  return 4;
+}
+
 static BlendGeom frame_geom(const hs_frame* frame, const FrameBufs& f, const BinBufs& b) {
   BlendGeom g;
   g.tile_starts = f.tile_starts;
@@ -562,6 +574,7 @@ static BlendGeom frame_geom(const hs_frame* frame, const FrameBufs& f, const Bin
   g.n_work = frame->n_tiles;
   g.tile_order = nullptr;
   g.tile_work = nullptr;
+  g.sub_tiles = 1;
   g.work_counter = f.counters;
   return g;
 }
@@ -577,7 +590,8 @@ int hs_blend_fwd(hs_frame* frame, const double* bg, float* color, float* alpha, 
   BlendGeom g = frame_geom(frame, f, b);
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
   g.tile_work = f.tile_work;
-  if (lpt_order(frame->n_tiles, blend_fwd_slots())) {
+  g.sub_tiles = fwd_sub_tiles(frame->n_tiles, blend_fwd_slots());
+  if (lpt_order(frame->n_tiles * g.sub_tiles, blend_fwd_slots())) {
     HS_CUDA(launch_tile_order(f.tile_starts, nullptr, frame->n_tiles, f.order_fwd, stream));
     g.tile_order = f.order_fwd;
   }
@@ -816,6 +830,7 @@ int seam1_upload(Seam1Dev& d, const double* packed, const int8_t* mode,
   g.n_work = n_tiles;
   g.tile_order = nullptr;
   g.tile_work = nullptr;
+  g.sub_tiles = 1;
   g.work_counter = (int*)d.ctr.p;
   return HS_OK;
 }

@@ -75,6 +75,7 @@ struct BlendGeom {
   const int32_t* tile_order;   // optional work order (nullptr = natural)
   int* work_counter;           // zeroed before launch
   int32_t* tile_work;          // optional (K5): per-tile largest terminal count
+  int sub_tiles;               // K5 work units per tile: 1 (16x16), 2 (16x8) or 4 (16x4)
 };
 int blend_fwd_slots();
 int blend_bwd_slots();
