@@ -7,9 +7,12 @@
 
 namespace hs {
 
-// sigmoid, geometry.py:349-352
+// sigmoid, geometry.py:349-352: x >= 0 ? 1 / (1 + exp(-x)) : exp(x) / (1 + exp(x)).
+// Both branches need exp(-|x|) once: computed branch-free with one exp and one
+// division, bit for bit the reference's value (same operations, same rounding).
 __device__ __forceinline__ double sigmoid_ref(double x) {
-  return x >= 0.0 ? 1.0 / (1.0 + exp(-x)) : exp(x) / (1.0 + exp(x));
+  const double e = exp(-fabs(x));
+  return (x >= 0.0 ? 1.0 : e) / (1.0 + e);
 }
 
 // quat_to_rot, geometry.py:27-49 (normalises its input again, as the reference

@@ -95,9 +95,27 @@ __device__ __forceinline__ void sh_basis(const double d[3], int deg, double* out
   }
 }
 
+// One primitive's R staged values from its dense shared-memory row (16-B loads for
+// float rows: the row start is 16-B aligned when 3K is a multiple of 4).
+template <int R, typename T, bool VEC = std::is_same<T, float>::value && R % 4 == 0>
+__device__ __forceinline__ void load_row(const T* p, float (&out)[R]) {
+  if constexpr (VEC) {
+    const float4* q = reinterpret_cast<const float4*>(p);
+#pragma unroll
+    for (int j = 0; j < R / 4; ++j) {
+      const float4 v = q[j];
+      out[4 * j] = v.x; out[4 * j + 1] = v.y; out[4 * j + 2] = v.z; out[4 * j + 3] = v.w;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < R; ++j) out[j] = (float)p[j];
+  }
+}
+
 // K7's SH backward in FP32 (eval_sh_basis / eval_sh_basis_grad, sh.py:32-98):
-// sh holds the primitive's (K,3) coefficients and is overwritten with d_sh =
-// basis (x) dpre; d_dir = sum_k (sum_ch sh[k,ch] dpre[ch]) d basis_k / d dir.
+// sh holds the primitive's (K,3) coefficients (a dense shared-memory row) and is
+// overwritten with d_sh = basis (x) dpre; d_dir = sum_k (sum_ch sh[k,ch] dpre[ch])
+// d basis_k / d dir.
 template <int DEG, typename E>
 __device__ __forceinline__ void sh_bwd_f32(const float d[3], const float dpre[3], E* sh,
                                            float d_dir[3]) {
@@ -127,11 +145,12 @@ __device__ __forceinline__ void sh_bwd_f32(const float d[3], const float dpre[3]
     b[14] = 1.445305721320277f * z * (xx - yy);
     b[15] = -0.5900435899266435f * x * (xx - 3.0f * yy);
   }
+  float cf[3 * K];
+  load_row<3 * K>(sh, cf);
   float db[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) {
-    db[k] = (float)sh[3 * k] * dpre[0] + (float)sh[3 * k + 1] * dpre[1] +
-            (float)sh[3 * k + 2] * dpre[2];
+    db[k] = cf[3 * k] * dpre[0] + cf[3 * k + 1] * dpre[1] + cf[3 * k + 2] * dpre[2];
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch) sh[3 * k + ch] = E(b[k] * dpre[ch]);
   }
@@ -223,7 +242,12 @@ __device__ __forceinline__ void sandwich_fast(const double A[9], const double C[
 // K7 reuses the same slots to stage its gradient outputs for coalesced stores.
 template <typename T, int K, int NT>
 struct Staged {
-  static constexpr int SHS = 3 * K + 1;
+  // float scenes with whole 16-B SH rows (deg 1, 3) stage them dense (the global
+  // layout, 16-B cp.async of one contiguous block) and read them back as 16-B
+  // vectors; otherwise rows are padded to an odd stride so per-thread scalar reads
+  // are conflict-free
+  static constexpr bool DENSE = std::is_same<T, float>::value && (3 * K) % 4 == 0;
+  static constexpr int SHS = DENSE ? 3 * K : 3 * K + 1;
   T mu[NT * 3], ls[NT * 3], rot[NT * 4], nrm[NT * 3], ra[NT], rb[NT];
   T sh[NT * SHS];
 };
@@ -250,20 +274,22 @@ __device__ __forceinline__ void stage_in(Staged<T, K, NT>& s, const SceneArgs<T>
     cp_async_elem(&s.ra[e], &sc.ra[base + e]);
     cp_async_elem(&s.rb[e], &sc.rb[base + e]);
   }
-  {
-    // consecutive threads on consecutive floats; the padded row (t, c) of element e
-    // advances incrementally (NT = qt * R + qc) instead of one division per element
-    constexpr int R = 3 * K, qt = NT / R, qc = NT % R;
-    int t = tid / R, c = tid - t * R;
+  if constexpr (!Staged<T, K, NT>::DENSE) {
+    constexpr int R = 3 * K;
     for (int e = tid; e < cnt * R; e += NT) {
+      const int t = e / R, c = e - t * R;
       cp_async_elem(&s.sh[t * Staged<T, K, NT>::SHS + c], &sc.sh[base * R + e]);
-      t += qt;
-      c += qc;
-      if (c >= R) {
-        c -= R;
-        ++t;
-      }
     }
+  } else {
+    constexpr int R = 3 * K, kV = 16 / sizeof(T);
+    const T* src = sc.sh + base * R;
+    const int n = cnt * R;
+    const int nv = ((uintptr_t)src & 15) ? 0 : n / kV;
+    for (int v = tid; v < nv; v += NT) {
+      const unsigned d = (unsigned)__cvta_generic_to_shared(&s.sh[v * kV]);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src + v * kV));
+    }
+    for (int e = nv * kV + tid; e < n; e += NT) cp_async_elem(&s.sh[e], &src[e]);
   }
   asm volatile("cp.async.commit_group;\n" ::);
   if (wait) {
@@ -285,6 +311,26 @@ struct StagedView {
   __device__ __forceinline__ double rb() const { return (double)s.rb[t]; }
   __device__ __forceinline__ double sh(int k, int ch) const {
     return (double)s.sh[t * Staged<T, K, NT>::SHS + 3 * k + ch];
+  }
+  // f(flat index 3k + ch, value) for every coefficient in index order: 16-B reads
+  // of a dense row (a per-element read of a dense row would conflict 16 ways)
+  template <typename F>
+  __device__ __forceinline__ void for_each_sh(F&& f) const {
+    const T* row = s.sh + t * Staged<T, K, NT>::SHS;
+    if constexpr (Staged<T, K, NT>::DENSE) {
+      const float4* q = reinterpret_cast<const float4*>(row);
+#pragma unroll
+      for (int j = 0; j < 3 * K / 4; ++j) {
+        const float4 v = q[j];
+        f(4 * j, (double)v.x);
+        f(4 * j + 1, (double)v.y);
+        f(4 * j + 2, (double)v.z);
+        f(4 * j + 3, (double)v.w);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 3 * K; ++j) f(j, (double)row[j]);
+    }
   }
 };
 
@@ -481,13 +527,12 @@ __device__ __forceinline__ void forward_state(const Src& src, const CamArgs& cam
   // the basis in FP32 (sh_bwd_f32)
   if (!kReplay) {
     sh_basis(st.vdir, DEG, st.basis);
+    // each channel sums basis[k] * sh[k, ch] over k in order (the coefficients are
+    // read in index order; the three sums interleave but do not mix)
+    double acc[3] = {0.0, 0.0, 0.0};
+    src.for_each_sh([&](int j, double v) { acc[j % 3] += st.basis[j / 3] * v; });
 #pragma unroll
-    for (int ch = 0; ch < 3; ++ch) {
-      double acc = 0.0;
-#pragma unroll
-      for (int k = 0; k < K; ++k) acc += st.basis[k] * src.sh(k, ch);
-      st.rgbu[ch] = acc + 0.5;
-    }
+    for (int ch = 0; ch < 3; ++ch) st.rgbu[ch] = acc[ch] + 0.5;
   }
 }
 
@@ -573,6 +618,11 @@ struct GlobalView {
   __device__ __forceinline__ double rb() const { return (double)sc.rb[i]; }
   __device__ __forceinline__ double sh(int k, int ch) const {
     return (double)sc.sh[(i * K + k) * 3 + ch];
+  }
+  template <typename F>
+  __device__ __forceinline__ void for_each_sh(F&& f) const {
+#pragma unroll
+    for (int j = 0; j < 3 * K; ++j) f(j, (double)sc.sh[i * K * 3 + j]);
   }
 };
 
