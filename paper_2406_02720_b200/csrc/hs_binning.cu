@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(kBinThreads) gather_counts_kernel(
     const int32_t* __restrict__ count, const uint32_t* __restrict__ order,
     const int4* __restrict__ rect, int32_t* __restrict__ cnt_r, uint32_t* __restrict__ rank_of,
     int64_t n, int tiles_y, int nblk, int32_t* __restrict__ key_pairs,
-    BinStatusDev* __restrict__ status) {
+    BinStatusDev* __restrict__ status, int4* __restrict__ rect_r) {
   extern __shared__ int smem_cnt[];  // [keys] segments, then [keys] pairs
   __shared__ long long csum[kBinThreads / 32][2];
   const int keys = tiles_y * nblk;
@@ -194,6 +194,7 @@ __global__ void __launch_bounds__(kBinThreads) gather_counts_kernel(
     v += c;
     if (SEGS && c > 0) {
       const int4 rc = rect[i];
+      rect_r[r] = rc;  // in rank order: the emit pass reads it coalesced
       const int b0 = rc.x / kSegCols, b1 = rc.y / kSegCols;
       vs += (rc.w - rc.z + 1) * (b1 - b0 + 1);
       for (int ty = rc.z; ty <= rc.w; ++ty)
@@ -238,7 +239,7 @@ cudaError_t run_count_scan(void* temp, size_t temp_bytes, const int32_t* count,
                            const uint32_t* order, const int4* rect, int32_t* cnt_r,
                            int32_t* off_r, uint32_t* rank_of, int64_t n, int tiles_x,
                            int tiles_y, int32_t* key_pairs, BinStatusDev* status,
-                           cudaStream_t stream) {
+                           int4* rect_r, cudaStream_t stream) {
   const bool segs = tiles_x > 0;
   const int nblk = segs ? seg_blocks(tiles_x) : 0;
   const int keys = segs ? tiles_y * nblk : 0;
@@ -249,11 +250,11 @@ cudaError_t run_count_scan(void* temp, size_t temp_bytes, const int32_t* count,
     e = cudaMemsetAsync(key_pairs, 0, keys * sizeof(int32_t), stream);
     if (e != cudaSuccess) return e;
     gather_counts_kernel<true><<<nb, kBinThreads, 2 * keys * sizeof(int), stream>>>(
-        count, order, rect, cnt_r, rank_of, n, tiles_y, nblk, key_pairs, status);
+        count, order, rect, cnt_r, rank_of, n, tiles_y, nblk, key_pairs, status, rect_r);
   } else {
     gather_counts_kernel<false><<<nb, kBinThreads, 0, stream>>>(count, order, rect, cnt_r,
                                                                 rank_of, n, 0, 0, key_pairs,
-                                                                status);
+                                                                status, rect_r);
   }
   note_launch();
   e = cudaGetLastError();
@@ -381,7 +382,7 @@ __global__ void __launch_bounds__(kBinThreads) seg_emit_kernel(RowBinArgs a) {
     if (c > 0) {
       v[q] = a.order[r];
       const uint32_t i = v[q] & kIndexMask;
-      rc[q] = a.rect[i];
+      rc[q] = a.rect_r[r];
       const int spans_x = rc[q].y - rc[q].x + 1;
       // pair (tx, ty) of this splat has generation index origin + ty * spans_x + tx
       reinterpret_cast<float*>(a.rec)[(size_t)i * kRecordFloats + R_ROW_ORIGIN] =

@@ -73,6 +73,7 @@ struct FrameBufs {
   float4* merged;
   int32_t* chunk_first;
   int32_t* key_pairs;
+  int4* rect_r;
   int32_t* order_fwd;   // longest-first tile orders of K5 / K6
   int32_t* order_bwd;
   int32_t* tile_work;   // K5 -> K6: per-tile largest terminal count
@@ -139,6 +140,7 @@ static FrameBufs carve_frame(void* ws, int64_t n, int tiles_x, int tiles_y, size
   f.merged = c.take<float4>(4 * (size_t)n);
   f.chunk_first = c.take<int32_t>(seg_keys(tiles_x, tiles_y) + 1);
   f.key_pairs = c.take<int32_t>(seg_keys(tiles_x, tiles_y));
+  f.rect_r = c.take<int4>(rows ? n : 1);
   f.order_fwd = c.take<int32_t>(n_tiles);
   f.order_bwd = c.take<int32_t>(n_tiles);
   f.tile_work = c.take<int32_t>(n_tiles);
@@ -357,7 +359,7 @@ static cudaError_t count_scan(const hs_frame* frame, const FrameBufs& f, cudaStr
   const bool segs = row_binning_ok(frame->tiles_x, frame->tiles_y);
   return run_count_scan(f.temp, f.temp_bytes, f.count, f.order, f.rect, f.cnt_r, f.off_r,
                         f.rank_of, frame->n, segs ? frame->tiles_x : 0, frame->tiles_y,
-                        f.key_pairs, f.status, stream);
+                        f.key_pairs, f.status, f.rect_r, stream);
 }
 
 int hs_preprocess_fwd(hs_frame* frame, const hs_scene* scene, const hs_camera* cam,
@@ -468,6 +470,7 @@ static int row_bin(hs_frame* frame, const FrameBufs& f, const BinBufs& b, cudaSt
   RowBinArgs a;
   a.order = f.order;
   a.rect = f.rect;
+  a.rect_r = f.rect_r;
   a.rec = f.rec;
   a.cnt_r = f.cnt_r;
   a.off_r = f.off_r;

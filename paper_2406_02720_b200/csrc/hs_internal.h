@@ -170,10 +170,11 @@ cudaError_t run_count_scan(void* temp, size_t temp_bytes, const int32_t* count,
                            const uint32_t* order, const int4* rect, int32_t* cnt_r,
                            int32_t* off_r, uint32_t* rank_of, int64_t n, int tiles_x,
                            int tiles_y, int32_t* key_pairs, BinStatusDev* status,
-                           cudaStream_t stream);
+                           int4* rect_r, cudaStream_t stream);
 struct RowBinArgs {
   const uint32_t* order;
   const int4* rect;
+  const int4* rect_r;    // rects in depth-rank order (the count pass writes them)
   float4* rec;
   const int32_t* cnt_r;
   const int32_t* off_r;
