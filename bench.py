@@ -367,7 +367,7 @@ def config_run(cfg, args, world, rank, fp32_peak, torch, dist, barrier):
     exchange on the compute stream.  Other configs: one view per rank."""
     from paper_2406_02720_b200 import device, scenes
     from paper_2406_02720_b200.geometry import CameraModel, Scene
-    from paper_2406_02720_b200.multiview import GradientAllReduce, shard_views
+    from paper_2406_02720_b200.multiview import GradientAllReduce, ViewBatch, shard_views
     sa = scenes.make_config(cfg)
     multi = len(sa.cameras) > 1
     if multi:
@@ -388,8 +388,14 @@ def config_run(cfg, args, world, rank, fp32_peak, torch, dist, barrier):
     timer = device.StageTimer()
     marks = []
 
+    vbatch = (ViewBatch(scene, len(views), rast) if multi and len(views) > 1 and
+              os.environ.get("HS_VIEW_BATCH", "1") == "1" else None)
+
     def step(t=None):
-        for j, v in enumerate(views):
+        if vbatch is not None:
+            vbatch.run(scene, cams, d_colors, views, grads, timer=t, buckets=buckets,
+                       on_bucket=reducer.start_range if reducer is not None else None)
+        for j, v in enumerate(views if vbatch is None else []):
             out = rast.render(scene, cams[v], timer=t)
             last = j == len(views) - 1 and reducer is not None
             rast.render_backward(scene, cams[v], out, d_colors[v], grads=grads, timer=t,
@@ -462,12 +468,16 @@ def config_run(cfg, args, world, rank, fp32_peak, torch, dist, barrier):
            "resolution": [cams[0].width, cams[0].height]}
     if multi:
         rec["allreduce_exposed_ms"] = exposed
-        rec["k7_ms_per_view"] = per_view.get("preprocess_bwd")
+        rec["k7_ms_per_view"] = (per_view.get("preprocess_bwd") or 0.0) + (
+            per_view.get("merge_rows") or 0.0)
+        rec["geometry_backward"] = ("one hs_preprocess_bwd_views pass per batch "
+                                    "(merged rows per view via hs_merge_rows)"
+                                    if vbatch is not None else "K7 per view, accumulating")
         rec["what"] = (f"{cfg}: batch of {len(cams)} views sharded over {world} rank(s), K1-K7 per "
                        "view, gradients summed over the batch" +
                        (" and all-reduced (NCCL via hs_grad_allreduce, 4 buckets under K7)"
                         if world > 1 else ""))
-    del scene, grads, rast
+    del scene, grads, rast, vbatch
     torch.cuda.empty_cache()
     return rec
 
@@ -494,7 +504,7 @@ def main():
     from paper_2406_02720_b200 import _native, device, scenes
     from paper_2406_02720_b200 import rasterizer as dropin
     from paper_2406_02720_b200.geometry import CameraModel, Scene
-    from paper_2406_02720_b200.multiview import GradientAllReduce, shard_views
+    from paper_2406_02720_b200.multiview import GradientAllReduce, ViewBatch, shard_views
 
     world, rank, local = rank_info()
     torch.cuda.set_device(local)
@@ -537,13 +547,31 @@ def main():
     timer = device.StageTimer()
     rast = device.Rasterizer("cuda", slots=1)
 
+    # a batch of views (c4): K5/K6 per view, then one geometry backward for the whole
+    # batch (multiview.ViewBatch); HS_VIEW_BATCH=0 runs K7 per view instead
+    vbatch = (ViewBatch(scene, len(views), rast) if multi and len(views) > 1 and
+              os.environ.get("HS_VIEW_BATCH", "1") == "1" else None)
+
     def backward_views(renderer, t=None):
         """Every owned view: render, cotangent, backward; the batch gradient summed
         over views and ranks.  Returns the last view's output."""
         out = None
         if fused is not None:
             fused.begin()
-        for j, v in enumerate(views):
+        if vbatch is not None:
+            for j, v in enumerate(views):
+                out, d = renderer(v, t)
+                device.blend_backward_rows(scene, cams[v], out, d, vbatch.merged[j], timer=t)
+            device.geometry_backward_views(
+                scene, [cams[v] for v in views], vbatch.merged[:len(views)], grads=grads,
+                kernel=rast.kernel, timer=t,
+                reduce_ptrs=fused.ptrs if fused is not None else None,
+                buckets=buckets if bucketed else None,
+                on_bucket=reducer.start_range if bucketed else None)
+            views_done = []
+        else:
+            views_done = views
+        for j, v in enumerate(views_done):
             out, d = renderer(v, t)
             if fused is not None:
                 rast.render_backward(scene, cams[v], out, d, grads=grads, timer=t,

@@ -236,6 +236,22 @@ int hs_preprocess_bwd(hs_frame* frame, const hs_scene* scene,
 int hs_preprocess_bwd_range(hs_frame* frame, const hs_scene* scene, const hs_camera* cam,
                             const hs_grads* grads, int64_t begin, int64_t end, void* stream);
 
+/* Multi-view geometry backward (a batch of views of one scene, the reference's
+ * per-view K7 loop of train.py / GradientSet.add, rasterizer.py:100-105, fused):
+ *   hs_merge_rows      -- after hs_blend_bwd of a view: that view's per-primitive
+ *                         merged blend gradients into merged_out ((n,16) float32,
+ *                         16-B aligned; culled primitives marked), so the frame's
+ *                         workspace can be reused by the next view;
+ *   hs_preprocess_bwd_views -- one pass over the scene for all the views: each
+ *                         primitive's parameters are read once, the gradients of
+ *                         every view it is visible in are summed on chip (in view
+ *                         order) and stored once.  grads->accumulate as for
+ *                         hs_preprocess_bwd; begin a multiple of 128. */
+int hs_merge_rows(hs_frame* frame, float* merged_out, void* stream);
+int hs_preprocess_bwd_views(const hs_scene* scene, int32_t n_views, const hs_camera* cams,
+                            const float* const* merged, int32_t kernel, const hs_grads* grads,
+                            int64_t begin, int64_t end, void* stream);
+
 /* Introspection for parity: the reference's FrameGeometry integers and packed
  * columns (rasterizer.py:108-147).  Device outputs:
  *   valid (n,) int32 -- original indices of surviving primitives, first M used

@@ -127,6 +127,10 @@ _SIGNATURES = {
     "hs_preprocess_bwd_range": (c_int32, [ctypes.POINTER(HsFrame), ctypes.POINTER(HsScene),
                                           ctypes.POINTER(HsCamera), ctypes.POINTER(HsGrads),
                                           c_int64, c_int64, c_void_p]),
+    "hs_merge_rows": (c_int32, [ctypes.POINTER(HsFrame), c_void_p, c_void_p]),
+    "hs_preprocess_bwd_views": (c_int32, [ctypes.POINTER(HsScene), c_int32,
+                                          ctypes.POINTER(HsCamera), c_void_p, c_int32,
+                                          ctypes.POINTER(HsGrads), c_int64, c_int64, c_void_p]),
     "hs_frame_export": (c_int32, [ctypes.POINTER(HsFrame), c_void_p, c_void_p, c_void_p,
                                   c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "hs_screen_splats": (c_int32, [ctypes.POINTER(HsScene), ctypes.POINTER(HsCamera), c_int32,

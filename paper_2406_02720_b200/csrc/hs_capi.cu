@@ -672,6 +672,53 @@ int hs_preprocess_bwd_range(hs_frame* frame, const hs_scene* scene, const hs_cam
   return HS_OK;
 }
 
+int hs_merge_rows(hs_frame* frame, float* merged_out, void* stream_) {
+  int st = check_frame_ws(frame);
+  if (st) return st;
+  if ((st = check_bin_ws(frame))) return st;
+  if (!merged_out || ((uintptr_t)merged_out & 15)) return HS_ERR_INVALID_ARG;
+  FrameBufs f = frame_bufs(frame);
+  BinBufs b = frame_bin(frame);
+  HS_CUDA(launch_merge_rows(frame->n, frame->tiles_x, f.rec, f.rect, f.count, f.rank_of,
+                            f.last_rank, b.rows, reinterpret_cast<float4*>(merged_out),
+                            pairs_hint(frame), static_cast<cudaStream_t>(stream_)));
+  return HS_OK;
+}
+
+int hs_preprocess_bwd_views(const hs_scene* scene, int32_t n_views, const hs_camera* cams,
+                            const float* const* merged, int32_t kernel, const hs_grads* grads,
+                            int64_t begin, int64_t end, void* stream_) {
+  if (!scene || n_views <= 0 || !cams || !merged || kernel < 0 || kernel > 1)
+    return HS_ERR_INVALID_ARG;
+  hs_frame shape{};
+  shape.n = scene->n;
+  if (int st = check_scene(scene, &shape)) return st;
+  if (!grads || !grads->d_mu || !grads->d_log_scale || !grads->d_rotation || !grads->d_sh ||
+      !grads->d_normal || !grads->d_raw_opacity_a || !grads->d_raw_opacity_b ||
+      !grads->pos_grad_norm || !grads->touch_count || grads->accumulate < 0 ||
+      grads->accumulate > 3 || begin < 0 || begin % 128 != 0 || end < begin)
+    return HS_ERR_INVALID_ARG;
+  std::vector<CamArgs> ca((size_t)n_views);
+  std::vector<const float4*> mg((size_t)n_views);
+  for (int v = 0; v < n_views; ++v) {
+    if (!merged[v] || ((uintptr_t)merged[v] & 15)) return HS_ERR_INVALID_ARG;
+    ca[(size_t)v] = cam_args(&cams[v]);
+    mg[(size_t)v] = reinterpret_cast<const float4*>(merged[v]);
+  }
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  if (scene->dtype == HS_DTYPE_F32)
+    HS_CUDA(launch_preprocess_bwd_views_t<float>(scene_args<float>(scene), ca.data(), mg.data(),
+                                                 n_views, kernel, scene->n,
+                                                 ranged(grad_args<float>(grads), begin, end),
+                                                 stream));
+  else
+    HS_CUDA(launch_preprocess_bwd_views_t<double>(scene_args<double>(scene), ca.data(), mg.data(),
+                                                  n_views, kernel, scene->n,
+                                                  ranged(grad_args<double>(grads), begin, end),
+                                                  stream));
+  return HS_OK;
+}
+
 int hs_frame_export(const hs_frame* frame, int32_t* valid, int64_t* m_out, float* packed,
                     int8_t* mode, int32_t* tile_rect, int32_t* pair_splat, int64_t* tile_starts,
                     void* stream_) {

@@ -59,6 +59,21 @@ cudaError_t launch_preprocess_bwd_t(const SceneArgs<T>& sc, const CamArgs& cam, 
                                     const int32_t* last_rank, const float* rows, float4* merged,
                                     int64_t num_pairs, const GradArgs<T>& out,
                                     cudaStream_t stream);
+// the multi-view K7: views in groups of kMaxViews per launch
+constexpr int kMaxViews = 8;
+struct ViewsArgs {
+  CamArgs cam[kMaxViews];
+  const float4* merged[kMaxViews];
+  int n_views;
+};
+template <typename T>
+cudaError_t launch_preprocess_bwd_views_t(const SceneArgs<T>& sc, const CamArgs* cams,
+                                          const float4* const* merged, int n_views, int kernel,
+                                          int64_t n, const GradArgs<T>& out, cudaStream_t stream);
+cudaError_t launch_merge_rows(int64_t n, int tiles_x, const float4* rec, const int4* rect,
+                              const int32_t* count, const uint32_t* rank_of,
+                              const int32_t* last_rank, const float* rows, float4* merged,
+                              int64_t num_pairs, cudaStream_t stream);
 
 template <typename T>
 cudaError_t launch_screen_splats_t(const SceneArgs<T>& sc, const CamArgs& cam, int kernel,

@@ -116,9 +116,14 @@ __device__ __forceinline__ void load_row(const T* p, float (&out)[R]) {
 // sh holds the primitive's (K,3) coefficients (a dense shared-memory row) and is
 // overwritten with d_sh = basis (x) dpre; d_dir = sum_k (sum_ch sh[k,ch] dpre[ch])
 // d basis_k / d dir.
-template <int DEG, typename E>
+// a + b rounded on its own (never contracted into an FMA with the product that
+// made b): the multi-view K7's sums match K7's per-view accumulation bit for bit
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+
+template <int DEG, bool ACC = false, typename E>
 __device__ __forceinline__ void sh_bwd_f32(const float d[3], const float dpre[3], E* sh,
-                                           float d_dir[3]) {
+                                           float d_dir[3], E* out = nullptr) {
   constexpr int K = (DEG + 1) * (DEG + 1);
   const float x = d[0], y = d[1], z = d[2];
   float b[K];
@@ -147,12 +152,17 @@ __device__ __forceinline__ void sh_bwd_f32(const float d[3], const float dpre[3]
   }
   float cf[3 * K];
   load_row<3 * K>(sh, cf);
+  // ACC: the coefficients stay, d_sh adds into `out` (the multi-view K7)
+  E* dst = ACC ? out : sh;
   float db[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) {
     db[k] = cf[3 * k] * dpre[0] + cf[3 * k + 1] * dpre[1] + cf[3 * k + 2] * dpre[2];
 #pragma unroll
-    for (int ch = 0; ch < 3; ++ch) sh[3 * k + ch] = E(b[k] * dpre[ch]);
+    for (int ch = 0; ch < 3; ++ch) {
+      if constexpr (ACC) dst[3 * k + ch] = add_rn(dst[3 * k + ch], E(__fmul_rn(b[k], dpre[ch])));
+      else dst[3 * k + ch] = E(b[k] * dpre[ch]);
+    }
   }
   float gx = 0.f, gy = 0.f, gz = 0.f;
   if (DEG >= 1) {
@@ -686,12 +696,18 @@ __global__ void __launch_bounds__(256) merge_rows_kernel(
     int64_t n, int tiles_x, const float4* __restrict__ rec, const int4* __restrict__ rect,
     const int32_t* __restrict__ count, const uint32_t* __restrict__ rank_of,
     const int32_t* __restrict__ last_rank, const float* __restrict__ rows,
-    float4* __restrict__ merged, int64_t begin) {
+    float4* __restrict__ merged, int64_t begin, int mark) {
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t i = begin + tid / G;
   const int sub = (int)(tid % G);
   // with G > 1 every lane stays to the shuffles (a group never straddles a warp)
   const int cnt = i < n ? count[i] : 0;
+  // mark: rows for a multi-view K7 (hs_merge_rows): a splat this view culled gets an
+  // explicit empty row (visibility .z = 0), the buffer outliving the frame's counts
+  if (mark && cnt == 0 && i < n && sub == 0) {
+    float4* dst = merged + 4 * i;
+    dst[0] = dst[1] = dst[2] = dst[3] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
   if (G == 1 && cnt == 0) return;
   double m[13];
 #pragma unroll
@@ -774,17 +790,35 @@ __global__ void __launch_bounds__(256) merge_rows_kernel(
   dst[0] = make_float4((float)m[0], (float)m[1], (float)m[2], (float)m[3]);
   dst[1] = make_float4((float)m[4], (float)m[5], (float)m[6], (float)m[7]);
   dst[2] = make_float4((float)m[8], (float)m[9], (float)m[10], (float)m[11]);
-  dst[3] = make_float4((float)m[12], r3.y, 0.f, 0.f);  // .y: K1's record flags for K7
+  // .y: K1's record flags for K7; .z: visible in this view (the multi-view K7)
+  dst[3] = make_float4((float)m[12], r3.y, 1.f, 0.f);
 }
 
-template <typename T, int DEG, int NT>
+// The multi-view K7's per-primitive gradient accumulators (the staged inputs stay
+// untouched across the views).
+template <typename T, int K, int NT>
+struct AccStage {
+  T mu[NT * 3], ls[NT * 3], nrm[NT * 3], rot[NT * 4], ra[NT], rb[NT], pgn[NT];
+  T sh[NT * Staged<T, K, NT>::SHS];
+};
+
+// One primitive's geometry backward for one view.  ACC = false (K7): the gradients
+// overwrite the thread's staged inputs (read before), visibility from count.  ACC =
+// true (the multi-view K7): they add into `acc`, visibility from the row's marker.
+template <typename T, int DEG, int NT, bool ACC = false>
 __device__ __forceinline__ void preprocess_bwd_one(
     Staged<T, (DEG + 1) * (DEG + 1), NT>& sm, T* pgn_s, int32_t* touch_s, int t, int64_t i,
     const CamArgs& cam, int kernel, const int32_t* __restrict__ count,
-    const float4* __restrict__ merged) {
+    const float4* __restrict__ merged,
+    AccStage<T, (DEG + 1) * (DEG + 1), NT>* acc = nullptr) {
   constexpr int K = (DEG + 1) * (DEG + 1);
   using St = Staged<T, K, NT>;
-  const int cnt = count[i];
+#define K7_PUT(field, idx, val)                                        \
+  do {                                                                 \
+    if constexpr (ACC) acc->field[idx] = add_rn(acc->field[idx], T(val));      \
+    else sm.field[idx] = T(val);                                               \
+  } while (0)
+  const int cnt = ACC ? 1 : count[i];
   if (cnt == 0) {
     for (int k = 0; k < 3; ++k) sm.mu[3 * t + k] = sm.ls[3 * t + k] = sm.nrm[3 * t + k] = T(0);
     for (int k = 0; k < 4; ++k) sm.rot[4 * t + k] = T(0);
@@ -804,6 +838,7 @@ __device__ __forceinline__ void preprocess_bwd_one(
     m[8] = u2.x; m[9] = u2.y; m[10] = u2.z; m[11] = u2.w;
     m[12] = u3.x;
     flags = __float_as_uint(u3.y);
+    if (ACC && u3.z == 0.f) return;  // culled in this view
   }
   FwdState st;
   forward_state<DEG, true>(StagedView<T, K, NT>{sm, t}, cam, kernel, st, flags);
@@ -816,8 +851,8 @@ __device__ __forceinline__ void preprocess_bwd_one(
   // opacities (rasterizer.py:446-450)
   {
     const double d_a1 = 0.5 * (d_c1 + d_c2), d_a2 = 0.5 * (d_c1 - d_c2);
-    sm.ra[t] = T(d_a1 * st.a1 * (1.0 - st.a1));
-    sm.rb[t] = T(d_a2 * st.a2 * (1.0 - st.a2));
+    K7_PUT(ra, t, d_a1 * st.a1 * (1.0 - st.a1));
+    K7_PUT(rb, t, d_a2 * st.a2 * (1.0 - st.a2));
   }
   // erf coefficients -> n_ray and whitening (rasterizer.py:452-466)
   const bool mode0 = st.mode == kModeErf;
@@ -974,7 +1009,8 @@ __device__ __forceinline__ void preprocess_bwd_one(
     const float dirf[3] = {(float)st.vdir[0], (float)st.vdir[1], (float)st.vdir[2]};
     float d_dir[3];
     // d_sh overwrites this thread's staged SH row (read first for d_basis)
-    sh_bwd_f32<DEG>(dirf, dpre, sm.sh + t * St::SHS, d_dir);
+    sh_bwd_f32<DEG, ACC>(dirf, dpre, sm.sh + t * St::SHS, d_dir,
+                         ACC ? acc->sh + t * St::SHS : nullptr);
     if (DEG > 0) {
       const double dd[3] = {d_dir[0], d_dir[1], d_dir[2]};
       const double dot = dd[0] * st.vdir[0] + dd[1] * st.vdir[1] + dd[2] * st.vdir[2];
@@ -1001,7 +1037,7 @@ __device__ __forceinline__ void preprocess_bwd_one(
         dR[3 * r + k] = dM[3 * r + k] * st.s[k];
         d_s[k] += dM[3 * r + k] * st.R[3 * r + k];
       }
-    for (int k = 0; k < 3; ++k) sm.ls[3 * t + k] = T(d_s[k] * st.s[k]);
+    for (int k = 0; k < 3; ++k) K7_PUT(ls, 3 * t + k, d_s[k] * st.s[k]);
     // quat_rot_vjp (geometry.py:76-107) at the unit quaternion
     const double w = st.qu[0], x = st.qu[1], y = st.qu[2], z = st.qu[3];
     const double Dw[9] = {0, -z, y, z, 0, -x, -y, x, 0};
@@ -1017,17 +1053,23 @@ __device__ __forceinline__ void preprocess_bwd_one(
     }
     const double dot = dq[0] * w + dq[1] * x + dq[2] * y + dq[3] * z;
     const double rq = 1.0 / st.qnorm;
-    for (int k = 0; k < 4; ++k) sm.rot[4 * t + k] = T((dq[k] - dot * st.qu[k]) * rq);
+    for (int k = 0; k < 4; ++k) K7_PUT(rot, 4 * t + k, (dq[k] - dot * st.qu[k]) * rq);
   }
   // splitting normal through its normalisation (rasterizer.py:565-566)
   {
     const double dot = d_nu[0] * st.nu[0] + d_nu[1] * st.nu[1] + d_nu[2] * st.nu[2];
     const double rnn = 1.0 / st.nnorm;
-    for (int k = 0; k < 3; ++k) sm.nrm[3 * t + k] = T((d_nu[k] - dot * st.nu[k]) * rnn);
+    for (int k = 0; k < 3; ++k) K7_PUT(nrm, 3 * t + k, (d_nu[k] - dot * st.nu[k]) * rnn);
   }
-  for (int k = 0; k < 3; ++k) sm.mu[3 * t + k] = T(d_mu[k]);
-  pgn_s[t] = T(sqrt(d_mux * d_mux + d_muy * d_muy));
-  touch_s[t] = 1;
+  for (int k = 0; k < 3; ++k) K7_PUT(mu, 3 * t + k, d_mu[k]);
+  if constexpr (ACC) {
+    acc->pgn[t] = add_rn(acc->pgn[t], T(sqrt(d_mux * d_mux + d_muy * d_muy)));
+    touch_s[t] += 1;
+  } else {
+    pgn_s[t] = T(sqrt(d_mux * d_mux + d_muy * d_muy));
+    touch_s[t] = 1;
+  }
+#undef K7_PUT
 }
 
 template <typename E> struct Vec16;
@@ -1368,10 +1410,10 @@ cudaError_t launch_preprocess_bwd_t(const SceneArgs<T>& sc, const CamArgs& cam, 
 #endif
   if (num_pairs >= (int64_t)HS_K7A_WIDE_ROWS * n)
     merge_rows_kernel<8><<<(unsigned)((cnt * 8 + 255) / 256), 256, 0, stream>>>(
-        end, tiles_x, rec, rect, count, rank_of, last_rank, rows, merged, out.begin);
+        end, tiles_x, rec, rect, count, rank_of, last_rank, rows, merged, out.begin, 0);
   else
     merge_rows_kernel<1><<<(unsigned)((cnt + 255) / 256), 256, 0, stream>>>(
-        end, tiles_x, rec, rect, count, rank_of, last_rank, rows, merged, out.begin);
+        end, tiles_x, rec, rect, count, rank_of, last_rank, rows, merged, out.begin, 0);
   note_launch();
 #ifndef HS_K7_NT_F32
 #define HS_K7_NT_F32 128
@@ -1393,6 +1435,174 @@ cudaError_t launch_preprocess_bwd_t(const SceneArgs<T>& sc, const CamArgs& cam, 
 #undef HS_K7
     default: return cudaErrorInvalidValue;
   }
+  note_launch();
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// The multi-view K7 (a batch of views of one scene): the CTA stages
+// its primitives' parameters once, walks every view's merged rows (hs_merge_rows,
+// one 64-B row per primitive and view), runs the geometry backward of each view the
+// primitive is visible in and adds the gradients into shared-memory accumulators,
+// then stores once.  Against one K7 per view this reads the scene once instead of
+// per view and writes the gradient buffer once instead of a read-modify-write per
+// view (about 1.5 GB per c4 view).  The sum runs in view order, as GradientSet.add
+// (rasterizer.py:100-105) does.
+template <typename T, int DEG, int NT>
+__global__ void __launch_bounds__(NT, HS_K7_MINB) preprocess_bwd_views_kernel(
+    SceneArgs<T> sc, ViewsArgs va, int kernel, int64_t n, GradArgs<T> out) {
+  constexpr int K = (DEG + 1) * (DEG + 1);
+  using St = Staged<T, K, NT>;
+  using Ac = AccStage<T, K, NT>;
+  __shared__ St sm;
+  __shared__ int32_t touch_s[NT];
+  __shared__ LiveMask<NT> lm;
+  extern __shared__ __align__(16) unsigned char dyn_smem[];
+  Ac* acc = reinterpret_cast<Ac*>(dyn_smem);
+  const int64_t base = out.begin + (int64_t)blockIdx.x * NT;
+  const int ncta = (int)(n - base < NT ? n - base : NT);
+  const int t = threadIdx.x;
+  stage_in(sm, sc, base, ncta, /*wait=*/false);
+  // the accumulators start at zero, or (accumulate == 1: an earlier batch or group of
+  // views already wrote) at the stored sums, so every view adds onto the running sum
+  // in view order exactly as K7 per view does
+  if (out.accumulate == 1) {
+    for (int e = t; e < ncta * 3; e += NT) {
+      acc->mu[e] = out.d_mu[base * 3 + e];
+      acc->ls[e] = out.d_log_scale[base * 3 + e];
+      acc->nrm[e] = out.d_normal[base * 3 + e];
+    }
+    for (int e = t; e < ncta * 4; e += NT) acc->rot[e] = out.d_rotation[base * 4 + e];
+    for (int e = t; e < ncta * 3 * K; e += NT) {
+      const int tt = e / (3 * K);
+      acc->sh[tt * St::SHS + (e - tt * 3 * K)] = out.d_sh[base * 3 * K + e];
+    }
+    if (t < ncta) {
+      acc->ra[t] = out.d_ra[base + t];
+      acc->rb[t] = out.d_rb[base + t];
+      acc->pgn[t] = out.pos_grad_norm[base + t];
+    }
+    touch_s[t] = t < ncta ? out.touch[base + t] : 0;
+  } else {
+    T* z = reinterpret_cast<T*>(acc);
+    for (int e = t; e < (int)(sizeof(Ac) / sizeof(T)); e += NT) z[e] = T(0);
+    touch_s[t] = 0;
+  }
+  asm volatile("cp.async.wait_all;\n" ::);
+  __syncthreads();
+  if (t < ncta)
+    for (int v = 0; v < va.n_views; ++v)
+      preprocess_bwd_one<T, DEG, NT, true>(sm, nullptr, touch_s, t, base + t, va.cam[v], kernel,
+                                           nullptr, va.merged[v], acc);
+  __syncthreads();
+  build_live_mask(lm, touch_s);
+  const bool red = out.accumulate >= 2, mc = out.accumulate == 3;
+  if (red) {
+    reduce_block<NT, 3>(out.d_mu + base * 3, ncta, touch_s, lm, mc, [&](int e) { return acc->mu[e]; });
+    reduce_block<NT, 3>(out.d_log_scale + base * 3, ncta, touch_s, lm, mc,
+                        [&](int e) { return acc->ls[e]; });
+    reduce_block<NT, 3>(out.d_normal + base * 3, ncta, touch_s, lm, mc,
+                        [&](int e) { return acc->nrm[e]; });
+    reduce_block<NT, 4>(out.d_rotation + base * 4, ncta, touch_s, lm, mc,
+                        [&](int e) { return acc->rot[e]; });
+    reduce_block<NT, 1>(out.d_ra + base, ncta, touch_s, lm, mc, [&](int e) { return acc->ra[e]; });
+    reduce_block<NT, 1>(out.d_rb + base, ncta, touch_s, lm, mc, [&](int e) { return acc->rb[e]; });
+    reduce_block<NT, 1>(out.pos_grad_norm + base, ncta, touch_s, lm, mc,
+                        [&](int e) { return acc->pgn[e]; });
+    reduce_block<NT, 1>(out.touch + base, ncta, touch_s, lm, mc, [&](int e) { return touch_s[e]; });
+    reduce_block<NT, 3 * K>(out.d_sh + base * 3 * K, ncta, touch_s, lm, mc, [&](int e) {
+      const int tt = e / (3 * K);
+      return acc->sh[tt * St::SHS + (e - tt * 3 * K)];
+    });
+    if (mc) asm volatile("fence.acq_rel.sys;\n" ::: "memory");
+    return;
+  }
+  // accumulate 0 / 1: the accumulators hold the final values of every primitive
+  const T* none = nullptr;
+  store_block<NT, 3>(out.d_mu + base * 3, ncta, none, touch_s, lm,
+                     [&](int e) { return acc->mu[e]; });
+  store_block<NT, 3>(out.d_log_scale + base * 3, ncta, none, touch_s, lm,
+                     [&](int e) { return acc->ls[e]; });
+  store_block<NT, 3>(out.d_normal + base * 3, ncta, none, touch_s, lm,
+                     [&](int e) { return acc->nrm[e]; });
+  store_block<NT, 4>(out.d_rotation + base * 4, ncta, none, touch_s, lm,
+                     [&](int e) { return acc->rot[e]; });
+  store_block<NT, 1>(out.d_ra + base, ncta, none, touch_s, lm,
+                     [&](int e) { return acc->ra[e]; });
+  store_block<NT, 1>(out.d_rb + base, ncta, none, touch_s, lm,
+                     [&](int e) { return acc->rb[e]; });
+  store_block<NT, 1>(out.pos_grad_norm + base, ncta, none, touch_s, lm,
+                     [&](int e) { return acc->pgn[e]; });
+  store_block<NT, 1>(out.touch + base, ncta, (const int32_t*)nullptr, touch_s, lm,
+                     [&](int e) { return touch_s[e]; });
+  if constexpr ((3 * K) % (16 / sizeof(T)) == 0) {
+    store_rows<NT, 3 * K, St::SHS>(out.d_sh + base * 3 * K, ncta, none, touch_s, lm, acc->sh);
+  } else {
+    store_block<NT, 3 * K>(out.d_sh + base * 3 * K, ncta, none, touch_s, lm, [&](int e) {
+      const int tt = e / (3 * K);
+      return acc->sh[tt * St::SHS + (e - tt * 3 * K)];
+    });
+  }
+}
+
+template <typename T>
+cudaError_t launch_preprocess_bwd_views_t(const SceneArgs<T>& sc, const CamArgs* cams,
+                                          const float4* const* merged, int n_views, int kernel,
+                                          int64_t n, const GradArgs<T>& out_in,
+                                          cudaStream_t stream) {
+  const int64_t end = out_in.end < n ? out_in.end : n;
+  if (end <= out_in.begin || n_views <= 0) return cudaSuccess;
+  const int64_t cnt = end - out_in.begin;
+  constexpr int NT = sizeof(T) == 4 ? HS_K7_NT_F32 : 64;
+  const int64_t grid = (cnt + NT - 1) / NT;
+  for (int v0 = 0; v0 < n_views; v0 += kMaxViews) {
+    ViewsArgs va;
+    va.n_views = n_views - v0 < kMaxViews ? n_views - v0 : kMaxViews;
+    for (int v = 0; v < va.n_views; ++v) {
+      va.cam[v] = cams[v0 + v];
+      va.merged[v] = merged[v0 + v];
+    }
+    GradArgs<T> out = out_in;
+    if (v0 > 0 && out.accumulate == 0) out.accumulate = 1;  // later groups add
+    switch (sc.deg) {
+#define HS_K7V(D)                                                                              \
+  case D: {                                                                                    \
+    constexpr size_t dyn = sizeof(AccStage<T, (D + 1) * (D + 1), NT>);                          \
+    const cudaError_t attr = set_dynamic_smem<preprocess_bwd_views_kernel<T, D, NT>>((int)dyn); \
+    if (attr != cudaSuccess) return attr;                                                      \
+    preprocess_bwd_views_kernel<T, D, NT><<<(unsigned)grid, NT, dyn, stream>>>(sc, va, kernel, \
+                                                                              end, out);       \
+    break;                                                                                     \
+  }
+      HS_K7V(0) HS_K7V(1) HS_K7V(2) HS_K7V(3)
+#undef HS_K7V
+      default: return cudaErrorInvalidValue;
+    }
+    note_launch();
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+template cudaError_t launch_preprocess_bwd_views_t<float>(const SceneArgs<float>&, const CamArgs*,
+                                                          const float4* const*, int, int, int64_t,
+                                                          const GradArgs<float>&, cudaStream_t);
+template cudaError_t launch_preprocess_bwd_views_t<double>(const SceneArgs<double>&,
+                                                           const CamArgs*, const float4* const*,
+                                                           int, int, int64_t,
+                                                           const GradArgs<double>&, cudaStream_t);
+
+// K7a alone into a caller buffer with culled markers (hs_merge_rows)
+cudaError_t launch_merge_rows(int64_t n, int tiles_x, const float4* rec, const int4* rect,
+                              const int32_t* count, const uint32_t* rank_of,
+                              const int32_t* last_rank, const float* rows, float4* merged,
+                              int64_t num_pairs, cudaStream_t stream) {
+  if (num_pairs >= (int64_t)HS_K7A_WIDE_ROWS * n)
+    merge_rows_kernel<8><<<(unsigned)((n * 8 + 255) / 256), 256, 0, stream>>>(
+        n, tiles_x, rec, rect, count, rank_of, last_rank, rows, merged, 0, 1);
+  else
+    merge_rows_kernel<1><<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(
+        n, tiles_x, rec, rect, count, rank_of, last_rank, rows, merged, 0, 1);
   note_launch();
   return cudaGetLastError();
 }

@@ -595,34 +595,12 @@ def render_backward(scene, cam, out, d_color, grads=None, timer=None, accumulate
     rasterizer.py:100-105) inside the K7 kernel instead of overwriting them."""
     scene = Scene.from_any(scene)
     cam = CameraModel.from_any(cam)
-    frame = out.frame
-    if frame is None or frame.n_total != len(scene):
-        raise MismatchedForward("forward bookkeeping does not match the scene")
-    if tuple(d_color.shape) != (cam.height, cam.width, 3):
-        raise MismatchedForward(
-            f"cotangent shape {tuple(d_color.shape)} != {(cam.height, cam.width, 3)}")
-    if tuple(out.terminal.shape) != (cam.height, cam.width):
-        raise MismatchedForward("terminal-index shape mismatch")
-    if not isinstance(d_color, torch.Tensor):
-        d_color = torch.as_tensor(np.asarray(d_color))
-    d_color = d_color.to(device=scene.device, dtype=torch.float32).contiguous()
     timer = timer or _NO_TIMER
-    lib = frame.lib
-    s = _stream()
-    bg = (ctypes.c_double * 3)(*scene.background_color.tolist())
-    with timer.span("blend_bwd"):
-        st = lib.hs_blend_bwd(ctypes.byref(frame.st), bg, _ptr(d_color),
-                              _ptr(out.transmittance), _ptr(out.terminal), s)
-    _native.check(st, "hs_blend_bwd")
+    frame, lib, s = _blend_backward(scene, cam, out, d_color, timer)
     if grads is None:
         grads = DeviceGradientSet.empty_like_scene(scene)
     g = grads_struct(grads, 1 if accumulate else 0)
-    if reduce_ptrs is not None:
-        # reduction stores: {name: address} (NVLS multicast addresses -> mode 3, or the
-        # buffers' own addresses with reduce_ptrs["mode"] == 2 for device atomics)
-        for name in DeviceGradientSet.NAMES:
-            setattr(g, name, reduce_ptrs[name])
-        g.accumulate = reduce_ptrs.get("mode", 3)
+    _reduction_targets(g, reduce_ptrs)
     sc = scene_struct(scene)
     cs = camera_struct(cam)
     with timer.span("preprocess_bwd"):
@@ -639,4 +617,99 @@ def render_backward(scene, cam, out, d_color, grads=None, timer=None, accumulate
                 _native.check(st, "hs_preprocess_bwd_range")
                 if on_bucket is not None:
                     on_bucket(b, e)
+    return grads
+
+
+def _reduction_targets(g, reduce_ptrs):
+    if reduce_ptrs is not None:
+        # reduction stores: {name: address} (NVLS multicast addresses -> mode 3, or the
+        # buffers' own addresses with reduce_ptrs["mode"] == 2 for device atomics)
+        for name in DeviceGradientSet.NAMES:
+            setattr(g, name, reduce_ptrs[name])
+        g.accumulate = reduce_ptrs.get("mode", 3)
+
+
+def _blend_backward(scene, cam, out, d_color, timer):
+    """K6 of one rendered view (hs_blend_bwd); returns (frame, lib, stream)."""
+    frame = out.frame
+    if frame is None or frame.n_total != len(scene):
+        raise MismatchedForward("forward bookkeeping does not match the scene")
+    if tuple(d_color.shape) != (cam.height, cam.width, 3):
+        raise MismatchedForward(
+            f"cotangent shape {tuple(d_color.shape)} != {(cam.height, cam.width, 3)}")
+    if tuple(out.terminal.shape) != (cam.height, cam.width):
+        raise MismatchedForward("terminal-index shape mismatch")
+    if not isinstance(d_color, torch.Tensor):
+        d_color = torch.as_tensor(np.asarray(d_color))
+    d_color = d_color.to(device=scene.device, dtype=torch.float32).contiguous()
+    lib = frame.lib
+    s = _stream()
+    bg = (ctypes.c_double * 3)(*scene.background_color.tolist())
+    with timer.span("blend_bwd"):
+        st = lib.hs_blend_bwd(ctypes.byref(frame.st), bg, _ptr(d_color),
+                              _ptr(out.transmittance), _ptr(out.terminal), s)
+    _native.check(st, "hs_blend_bwd")
+    return frame, lib, s
+
+
+MERGED_ROW_FLOATS = 16  # one 64-B merged blend-gradient row per primitive (hs_merge_rows)
+
+
+def blend_backward_rows(scene, cam, out, d_color, merged=None, timer=None):
+    """The first half of render_backward for the multi-view geometry backward: K6 of
+    one view, then that view's per-primitive merged blend gradients (K7a) copied
+    into `merged` ((n, 16) float32, allocated if None), so the view's workspace can
+    be reused by the next view.  Pass the rows of a batch of views to
+    geometry_backward_views."""
+    scene = Scene.from_any(scene)
+    cam = CameraModel.from_any(cam)
+    timer = timer or _NO_TIMER
+    frame, lib, s = _blend_backward(scene, cam, out, d_color, timer)
+    if merged is None:
+        merged = torch.empty((len(scene), MERGED_ROW_FLOATS), dtype=torch.float32,
+                             device=scene.device)
+    if (tuple(merged.shape) != (len(scene), MERGED_ROW_FLOATS) or
+            merged.dtype != torch.float32 or not merged.is_contiguous()):
+        raise ValueError(f"merged rows must be a contiguous float32 ({len(scene)}, 16) tensor")
+    with timer.span("merge_rows"):
+        _native.check(lib.hs_merge_rows(ctypes.byref(frame.st), _ptr(merged), s),
+                      "hs_merge_rows")
+    return merged
+
+
+def geometry_backward_views(scene, cams, merged, grads=None, kernel="half", timer=None,
+                            accumulate=False, reduce_ptrs=None, buckets=None, on_bucket=None):
+    """Sum over views of the geometry backward (K7) in ONE pass over the scene
+    (hs_preprocess_bwd_views): merged[v] is view v's blend_backward_rows output.
+    Equal to render_backward over the views with accumulate=True after the first
+    (GradientSet.add, rasterizer.py:100-105), the sum taken in view order."""
+    scene = Scene.from_any(scene)
+    cams = [CameraModel.from_any(c) for c in cams]
+    if len(cams) != len(merged) or not cams:
+        raise ValueError("one merged-row buffer per camera is required")
+    if kernel not in ("half", "full"):
+        raise ValueError("kernel must be 'half' or 'full'")
+    for m in merged:
+        if (tuple(m.shape) != (len(scene), MERGED_ROW_FLOATS) or m.dtype != torch.float32
+                or m.device != scene.mu.device):
+            raise MismatchedForward("merged rows do not match the scene")
+    timer = timer or _NO_TIMER
+    lib = _native.load()
+    s = _stream()
+    if grads is None:
+        grads = DeviceGradientSet.empty_like_scene(scene)
+    g = grads_struct(grads, 1 if accumulate else 0)
+    _reduction_targets(g, reduce_ptrs)
+    sc = scene_struct(scene)
+    cs = (_native.HsCamera * len(cams))(*[camera_struct(c) for c in cams])
+    rows = (ctypes.c_void_p * len(cams))(*[m.data_ptr() for m in merged])
+    kcode = {"half": _native.HS_KERNEL_HALF, "full": _native.HS_KERNEL_FULL}[kernel]
+    ranges = buckets if buckets is not None else [(0, len(scene))]
+    with timer.span("preprocess_bwd"):
+        for b, e in ranges:
+            st = lib.hs_preprocess_bwd_views(ctypes.byref(sc), len(cams), cs, rows, kcode,
+                                             ctypes.byref(g), b, e, s)
+            _native.check(st, "hs_preprocess_bwd_views")
+            if on_bucket is not None:
+                on_bucket(b, e)
     return grads

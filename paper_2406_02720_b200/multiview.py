@@ -217,14 +217,51 @@ class FusedGradientReduce:
         return self.grads
 
 
+class ViewBatch:
+    """The multi-view backward of a batch of views: per view K5, K6
+    and the merged blend-gradient rows (device.blend_backward_rows) into a persistent
+    per-view buffer, then ONE geometry backward over the scene for all of them
+    (device.geometry_backward_views, hs_preprocess_bwd_views).  Against render_backward
+    per view (K7 per view, accumulating) the scene is read once and the gradient
+    buffer written once per batch instead of read-modify-written per view; the sum
+    is the same, in the same order."""
+
+    def __init__(self, scene, n_views, rast=None):
+        from . import device
+        self.rast = rast if rast is not None else device.Rasterizer(scene.device)
+        self.merged = [torch.empty((len(scene), device.MERGED_ROW_FLOATS),
+                                   dtype=torch.float32, device=scene.device)
+                       for _ in range(n_views)]
+
+    def run(self, scene, cams, d_colors, view_ids, grads, timer=None, reduce_ptrs=None,
+            buckets=None, on_bucket=None):
+        from . import device
+        if len(view_ids) > len(self.merged):
+            raise ValueError(f"{len(view_ids)} views for a batch of {len(self.merged)}")
+        for j, v in enumerate(view_ids):
+            r = self.rast.render(scene, cams[v], timer=timer)
+            device.blend_backward_rows(scene, cams[v], r, d_colors[v], self.merged[j],
+                                       timer=timer)
+        return device.geometry_backward_views(
+            scene, [cams[v] for v in view_ids], self.merged[:len(view_ids)], grads=grads,
+            kernel=self.rast.kernel, timer=timer, reduce_ptrs=reduce_ptrs, buckets=buckets,
+            on_bucket=on_bucket)
+
+
 def batch_gradients(scene, cams, d_colors, view_ids, out=None, rast=None, timer=None,
-                    fused=None):
+                    fused=None, batch=None):
     """Sum render_backward over this rank's views into `out` (flat buffer).
 
-    The first view overwrites, later ones accumulate inside the K7 kernel, so a
-    batch costs no extra gradient-sized passes.  With `fused` (a
-    FusedGradientReduce) every view's K7 adds into the shared buffer instead and
-    the result is already summed over all ranks."""
+    With `batch` (a ViewBatch) the geometry backward of all the views runs as one
+    pass over the scene.  Otherwise the first view overwrites and later ones
+    accumulate inside the K7 kernel, so a batch costs no extra gradient-sized
+    passes.  With `fused` (a FusedGradientReduce) every view's K7 adds into the
+    shared buffer instead and the result is already summed over all ranks."""
+    if fused is not None and batch is not None and view_ids:
+        fused.begin()
+        batch.run(scene, cams, d_colors, view_ids, fused.grads, timer=timer,
+                  reduce_ptrs=fused.ptrs)
+        return fused.end()
     if fused is not None:
         from . import device
         if rast is None:
@@ -243,6 +280,9 @@ def batch_gradients(scene, cams, d_colors, view_ids, out=None, rast=None, timer=
     if not view_ids:
         out.flat.zero_()
         out.touch_count.zero_()
+        return out
+    if batch is not None:
+        return batch.run(scene, cams, d_colors, view_ids, out, timer=timer)
     for j, v in enumerate(view_ids):
         r = rast.render(scene, cams[v], timer=timer)
         rast.render_backward(scene, cams[v], r, d_colors[v], grads=out, timer=timer,
@@ -250,11 +290,11 @@ def batch_gradients(scene, cams, d_colors, view_ids, out=None, rast=None, timer=
     return out
 
 
-def multiview_step(scene, cams, d_colors, grads=None, rast=None):
+def multiview_step(scene, cams, d_colors, grads=None, rast=None, batch=None):
     """One data-parallel step: local views, then the all-reduce. Returns the batch gradient."""
     world = dist.get_world_size() if dist.is_available() and dist.is_initialized() else 1
     rank = dist.get_rank() if world > 1 else 0
     views = shard_views(len(cams), world, rank)
-    grads = batch_gradients(scene, cams, d_colors, views, grads, rast)
+    grads = batch_gradients(scene, cams, d_colors, views, grads, rast, batch=batch)
     GradientAllReduce(grads).allreduce()
     return grads
