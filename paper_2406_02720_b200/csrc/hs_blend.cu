@@ -81,12 +81,18 @@ struct WarpStage {
 
 // Gather the records of `count` (<= 32) pairs, pair j at sorted index
 // k0 + pos(j), into stage slot j (one lane per record); steep splats also get
-// their FP64 side record.
+// their FP64 side record.  In two halves, so a batch's sorted indices can be
+// loaded one batch ahead (a register prefetch) and the gather of its records
+// issued without waiting on them: a warp alone on its SM (a frame's longest
+// tiles) otherwise stalls a full global round trip per batch.
 template <typename PosFn>
-__device__ __forceinline__ void issue_batch(const BlendGeom& g, int k0, int count, PosFn pos,
-                                            WarpStage& st, int stage, int lane) {
+__device__ __forceinline__ uint32_t batch_index(const BlendGeom& g, int k0, int count,
+                                                PosFn pos, int lane) {
+  return lane < count ? g.pair_src[k0 + pos(lane)] : 0u;
+}
+__device__ __forceinline__ void issue_records(const BlendGeom& g, uint32_t v, int count,
+                                              WarpStage& st, int stage, int lane) {
   if (lane < count) {
-    const uint32_t v = g.pair_src[k0 + pos(lane)];
     const uint32_t idx = v & kIndexMask;
     const float4* src = g.rec + 4 * (size_t)idx;
 #pragma unroll
@@ -101,11 +107,51 @@ __device__ __forceinline__ void issue_batch(const BlendGeom& g, int k0, int coun
   cp_async_commit();
 }
 
-__device__ __forceinline__ int next_tile(const BlendGeom& g, int lane) {
-  int t = 0;
-  if (lane == 0) t = atomicAdd(g.work_counter, 1);
-  t = __shfl_sync(0xffffffffu, t, 0);
-  if (t >= g.n_work) return -1;
+// The persistent blends' work queue.  Units come in longest-first order, and the
+// warps of one SM share its issue slots, so what has to balance is the work per
+// SM: a plain counter hands the first (longest) units to consecutive warps, i.e. to
+// the same few SMs (c2: 16 of the longest tiles on SM 0, the kernel 2.3x its
+// balanced time).  So the first wave is spread: the k-th warp to start on SM s
+// takes unit k * n_sm + s (snake order over k), claimed with a flag; later units
+// come from a dynamic counter over [n_first, n_units); a first-wave unit nobody
+// claimed (an SM that hosts fewer warps than planned) is picked up by a final
+// sweep over the flags, so every unit runs exactly once whatever the placement.
+// Returns -1 when the queue is empty; `phase` is per warp, starting at 0.
+__device__ __forceinline__ int next_unit(const BlendGeom& g, int n_units, int& phase, int lane) {
+  int t = -1;
+  if (lane == 0) {
+    int* q = g.work_counter;
+    const int n_first = g.spread ? min(g.n_first, n_units) : 0;
+    if (phase == 0) {
+      phase = 1;
+      if (n_first > 0) {
+        int s;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(s));
+        if (s < g.n_sm && s < kQueueMaxSms) {
+          const int k = atomicAdd(q + 2 + s, 1);
+          const int r = k * g.n_sm + ((k & 1) ? g.n_sm - 1 - s : s);
+          if (k < g.per_sm && r < n_first && atomicExch(q + 2 + kQueueMaxSms + r, 1) == 0) t = r;
+        }
+      }
+    }
+    if (t < 0 && phase == 1) {
+      const int d = n_first + atomicAdd(q, 1);
+      if (d < n_units) t = d;
+      else phase = n_first > 0 ? 2 : 3;
+    }
+    while (t < 0 && phase == 2) {
+      const int i = atomicAdd(q + 1, 1);
+      if (i >= n_first) phase = 3;
+      else if (atomicExch(q + 2 + kQueueMaxSms + i, 1) == 0) t = i;
+    }
+  }
+  phase = __shfl_sync(0xffffffffu, phase, 0);
+  return __shfl_sync(0xffffffffu, t, 0);
+}
+
+__device__ __forceinline__ int next_tile(const BlendGeom& g, int& phase, int lane) {
+  const int t = next_unit(g, g.n_work, phase, lane);
+  if (t < 0) return -1;
   return g.tile_order ? g.tile_order[t] : g.tile_lo + t;
 }
 
@@ -402,6 +448,27 @@ __device__ __forceinline__ int alive_halves(const FwdPix<NPX>& P) {
   return (__any_sync(0xffffffffu, lo > 0.0f) ? 1 : 0) | (__any_sync(0xffffffffu, hi > 0.0f) ? 2 : 0);
 }
 
+#ifdef HS_K5_PROBE
+// experiments only (tools/k5_probe.py): per work unit {start ns, end ns, splats
+// evaluated, SM id}
+__device__ long long g_k5_probe[65536 * 4];
+__device__ __forceinline__ long long global_ns() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ int sm_id() {
+  int s;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(s));
+  return s;
+}
+extern "C" int hs_k5_probe_read(long long* out, int n_units) {
+  if (cudaDeviceSynchronize() != cudaSuccess) return 1;
+  return cudaMemcpyFromSymbol(out, g_k5_probe, sizeof(long long) * 4 * (size_t)n_units) !=
+         cudaSuccess;
+}
+#endif
+
 // A forward work unit: a 16-column by 2 * NPX-row sub-tile (the whole 16 x 16 tile
 // at NPX = 8).  Small frames (c1's 64 tiles, c2's 2500 against 2368 resident warps)
 // split their tiles into 2 or 4 sub-tiles, so more warps share the work and each
@@ -416,14 +483,17 @@ __global__ void HS_FWD_BOUNDS blend_fwd_kernel(
   __shared__ WarpStage stage_all[kFwdWarps];
   const int lane = threadIdx.x & 31;
   WarpStage& st = stage_all[threadIdx.x >> 5];
+  int phase = 0;
   for (;;) {
-    int t = 0;
-    if (lane == 0) t = atomicAdd(g.work_counter, 1);
-    t = __shfl_sync(0xffffffffu, t, 0);
-    if (t >= g.n_work * SUB) break;
+    const int t = next_unit(g, g.n_work * SUB, phase, lane);
+    if (t < 0) break;
     const int tr = t / SUB, sub = t - tr * SUB;
     const int tile = g.tile_order ? g.tile_order[tr] : g.tile_lo + tr;
     const int ty = tile / g.tiles_x, tx = tile - ty * g.tiles_x;
+#ifdef HS_K5_PROBE
+    const long long probe_t0 = global_ns();
+    int probe_splats = 0;
+#endif
     const int col = tx * kTile + (lane & 15);
     const int sy0 = ty * kTile + sub * 2 * NPX;  // first row of the sub-tile
     const int row0 = sy0 + (lane >> 4);
@@ -443,16 +513,21 @@ __global__ void HS_FWD_BOUNDS blend_fwd_kernel(
     const int k0 = g.tile_starts[tile];
     const int nk = g.tile_starts[tile + 1] - k0;
     auto fwd_pos = [](int j) { return j; };
-    if (nk > 0) issue_batch(g, k0, min(kBatch, nk), fwd_pos, st, 0, lane);
+    auto count_of = [&](int b) { return min(kBatch, nk - b * kBatch); };
+    if (nk > 0)
+      issue_records(g, batch_index(g, k0, count_of(0), fwd_pos, lane), count_of(0), st, 0, lane);
+    uint32_t vnext = nk > kBatch ? batch_index(g, k0 + kBatch, count_of(1), fwd_pos, lane) : 0u;
     bool any = true;
     int alive = kWinAll;
     for (int b = 0; b * kBatch < nk && any; ++b) {
       const int nb = min(kBatch, nk - b * kBatch);
-      if ((b + 1) * kBatch < nk)
-        issue_batch(g, k0 + (b + 1) * kBatch, min(kBatch, nk - (b + 1) * kBatch), fwd_pos, st,
-                    (b + 1) & 1, lane);
-      else
+      if ((b + 1) * kBatch < nk) {
+        issue_records(g, vnext, count_of(b + 1), st, (b + 1) & 1, lane);
+        if ((b + 2) * kBatch < nk)
+          vnext = batch_index(g, k0 + (b + 2) * kBatch, count_of(b + 2), fwd_pos, lane);
+      } else {
         cp_async_commit();
+      }
       cp_async_wait<1>();
       __syncwarp();
       const int s = b & 1;
@@ -474,6 +549,9 @@ __global__ void HS_FWD_BOUNDS blend_fwd_kernel(
           alive = alive_halves(P);
           if (!(any = alive != 0)) break;
         }
+#ifdef HS_K5_PROBE
+        ++probe_splats;
+#endif
         const float4 q[4] = {st.rec[s][j][0], st.rec[s][j][1], st.rec[s][j][2], st.rec[s][j][3]};
         const uint32_t flags = __float_as_uint(q[3].y);
         const int key = st.win[s][j] & (~3 | alive);  // generic keeps its window bits: 8+
@@ -513,6 +591,15 @@ __global__ void HS_FWD_BOUNDS blend_fwd_kernel(
         terminal[o] = (int32_t)slot(P.C[p], h);
       }
     }
+#ifdef HS_K5_PROBE
+    if (lane == 0 && t < 65536) {
+      long long* pr = g_k5_probe + 4 * (size_t)t;
+      pr[0] = probe_t0;
+      pr[1] = global_ns();
+      pr[2] = probe_splats;
+      pr[3] = sm_id() | ((long long)tile << 16);
+    }
+#endif
     if (g.tile_work) {
       // the backward's work on this tile: its largest terminal count (K6 walks
       // positions maxc-1 .. 0), for K6's longest-first tile order
@@ -772,8 +859,9 @@ __global__ void HS_BWD_BOUNDS blend_bwd_kernel(
   int* cnt = &cnt_all[threadIdx.x >> 5][0][lane];
   float* tfin = &tfin_all[threadIdx.x >> 5][0][lane];
   float* dini = &dini_all[threadIdx.x >> 5][0][lane];
+  int phase = 0;
   for (;;) {
-    const int tile = next_tile(g, lane);
+    const int tile = next_tile(g, phase, lane);
     if (tile < 0) break;
     const int ty = tile / g.tiles_x, tx = tile - ty * g.tiles_x;
     const int col = tx * kTile + (lane & 15);
@@ -835,17 +923,18 @@ __global__ void HS_BWD_BOUNDS blend_bwd_kernel(
     if (maxc == 0) continue;
     // positions maxc-1 .. 0; batch b holds positions hi_b - j for j < nb
     auto batch_hi = [&](int b) { return maxc - 1 - b * kBatch; };
-    {
-      const int hi = batch_hi(0);
-      issue_batch(g, k0, min(kBatch, hi + 1), [hi](int j) { return hi - j; }, st, 0, lane);
-    }
+    auto bwd_index = [&](int b) {
+      const int hi = batch_hi(b);
+      return batch_index(g, k0, min(kBatch, hi + 1), [hi](int j) { return hi - j; }, lane);
+    };
+    issue_records(g, bwd_index(0), min(kBatch, batch_hi(0) + 1), st, 0, lane);
+    uint32_t vnext = kBatch < maxc ? bwd_index(1) : 0u;
     for (int b = 0; b * kBatch < maxc; ++b) {
       const int hi = batch_hi(b);
       const int nb = min(kBatch, hi + 1);
       if ((b + 1) * kBatch < maxc) {
-        const int hi2 = batch_hi(b + 1);
-        issue_batch(g, k0, min(kBatch, hi2 + 1), [hi2](int j) { return hi2 - j; }, st,
-                    (b + 1) & 1, lane);
+        issue_records(g, vnext, min(kBatch, batch_hi(b + 1) + 1), st, (b + 1) & 1, lane);
+        if ((b + 2) * kBatch < maxc) vnext = bwd_index(b + 2);
       } else {
         cp_async_commit();
       }
@@ -1086,51 +1175,83 @@ int blend_bwd_slots() {
   return blend_grid(blend_bwd_kernel<false>, kBwdWarps, 1 << 30, &g_bwd_grid[0]) * kBwdWarps;
 }
 
-cudaError_t launch_blend_fwd(const BlendGeom& g, float bg0, float bg1, float bg2, float* color,
+static int sm_count() {
+  static const int n = [] {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms;
+  }();
+  return n;
+}
+
+// the unit queue of a launch of `grid` CTAs of `warps` warps (see next_unit)
+static cudaError_t reset_queue(BlendGeom& g, int grid, int warps, cudaStream_t stream) {
+  int ints = 1;
+  if (g.spread) {
+    const int slots = grid * warps;
+    g.n_sm = sm_count();
+    g.per_sm = (slots + g.n_sm - 1) / g.n_sm;
+    g.n_first = slots < kQueueMaxFirst ? slots : kQueueMaxFirst;
+    ints = 2 + kQueueMaxSms + g.n_first;
+  }
+  return cudaMemsetAsync(g.work_counter, 0, sizeof(int) * (size_t)ints, stream);
+}
+
+cudaError_t launch_blend_fwd(const BlendGeom& g_in, float bg0, float bg1, float bg2, float* color,
                              float* alpha, float* depth, float* trans, int32_t* terminal,
                              cudaStream_t stream) {
-  cudaError_t e = cudaMemsetAsync(g.work_counter, 0, sizeof(int), stream);
-  if (e != cudaSuccess) return e;
+  BlendGeom g = g_in;
   const int sub = g.sub_tiles == 2 || g.sub_tiles == 4 ? g.sub_tiles : 1;
+  cudaError_t e;
   if (sub > 1 && g.tile_work) {  // max-reduced by the sub-tiles
     e = cudaMemsetAsync(g.tile_work, 0, (size_t)g.n_work * sizeof(int32_t), stream);
     if (e != cudaSuccess) return e;
   }
   const int units = g.n_work * sub;
   switch (sub) {
-    case 4:
-      blend_fwd_kernel<2><<<blend_grid(blend_fwd_kernel<2>, kFwdWarps, units, &g_fwd_grid4),
-                             kFwdWarps * 32, 0, stream>>>(g, bg0, bg1, bg2, color, alpha, depth,
-                                                          trans, terminal);
+    case 4: {
+      const int grid = blend_grid(blend_fwd_kernel<2>, kFwdWarps, units, &g_fwd_grid4);
+      if ((e = reset_queue(g, grid, kFwdWarps, stream)) != cudaSuccess) return e;
+      blend_fwd_kernel<2><<<grid, kFwdWarps * 32, 0, stream>>>(g, bg0, bg1, bg2, color, alpha,
+                                                               depth, trans, terminal);
       break;
-    case 2:
-      blend_fwd_kernel<4><<<blend_grid(blend_fwd_kernel<4>, kFwdWarps, units, &g_fwd_grid2),
-                             kFwdWarps * 32, 0, stream>>>(g, bg0, bg1, bg2, color, alpha, depth,
-                                                          trans, terminal);
+    }
+    case 2: {
+      const int grid = blend_grid(blend_fwd_kernel<4>, kFwdWarps, units, &g_fwd_grid2);
+      if ((e = reset_queue(g, grid, kFwdWarps, stream)) != cudaSuccess) return e;
+      blend_fwd_kernel<4><<<grid, kFwdWarps * 32, 0, stream>>>(g, bg0, bg1, bg2, color, alpha,
+                                                               depth, trans, terminal);
       break;
-    default:
-      blend_fwd_kernel<kPx><<<blend_grid(blend_fwd_kernel<kPx>, kFwdWarps, units, &g_fwd_grid),
-                               kFwdWarps * 32, 0, stream>>>(g, bg0, bg1, bg2, color, alpha, depth,
-                                                            trans, terminal);
+    }
+    default: {
+      const int grid = blend_grid(blend_fwd_kernel<kPx>, kFwdWarps, units, &g_fwd_grid);
+      if ((e = reset_queue(g, grid, kFwdWarps, stream)) != cudaSuccess) return e;
+      blend_fwd_kernel<kPx><<<grid, kFwdWarps * 32, 0, stream>>>(g, bg0, bg1, bg2, color, alpha,
+                                                                 depth, trans, terminal);
+    }
   }
   note_launch();
   return cudaGetLastError();
 }
 
-cudaError_t launch_blend_bwd(const BlendGeom& g, float bg0, float bg1, float bg2,
+cudaError_t launch_blend_bwd(const BlendGeom& g_in, float bg0, float bg1, float bg2,
                              const float* d_color, const float* trans, const int32_t* terminal,
                              float* rows, int32_t* last_rank, const uint32_t* rank_of,
                              bool rows_by_sorted_pos, cudaStream_t stream) {
-  cudaError_t e = cudaMemsetAsync(g.work_counter, 0, sizeof(int), stream);
-  if (e != cudaSuccess) return e;
-  if (rows_by_sorted_pos)
-    blend_bwd_kernel<true><<<blend_grid(blend_bwd_kernel<true>, kBwdWarps, g.n_work, &g_bwd_grid[1]),
-                             kBwdWarps * 32, 0, stream>>>(
+  BlendGeom g = g_in;
+  cudaError_t e;
+  if (rows_by_sorted_pos) {
+    const int grid = blend_grid(blend_bwd_kernel<true>, kBwdWarps, g.n_work, &g_bwd_grid[1]);
+    if ((e = reset_queue(g, grid, kBwdWarps, stream)) != cudaSuccess) return e;
+    blend_bwd_kernel<true><<<grid, kBwdWarps * 32, 0, stream>>>(
         g, bg0, bg1, bg2, d_color, trans, terminal, rows, last_rank, rank_of);
-  else
-    blend_bwd_kernel<false><<<blend_grid(blend_bwd_kernel<false>, kBwdWarps, g.n_work, &g_bwd_grid[0]),
-                              kBwdWarps * 32, 0, stream>>>(
+  } else {
+    const int grid = blend_grid(blend_bwd_kernel<false>, kBwdWarps, g.n_work, &g_bwd_grid[0]);
+    if ((e = reset_queue(g, grid, kBwdWarps, stream)) != cudaSuccess) return e;
+    blend_bwd_kernel<false><<<grid, kBwdWarps * 32, 0, stream>>>(
         g, bg0, bg1, bg2, d_color, trans, terminal, rows, last_rank, rank_of);
+  }
   note_launch();
   return cudaGetLastError();
 }

@@ -48,7 +48,7 @@ struct Carver {
   }
 };
 
-// counters[]: 0 K5 tile queue, 32 K6 tile queue, 48 depth-fixup overflow flag,
+// counters[]: 48 depth-fixup overflow flag,
 // 52-57 the binning status (BinStatusDev: P and segments as int64, flags)
 constexpr int kDepthOverflowSlot = 48;
 constexpr int kBinStatusSlot = 52;
@@ -77,6 +77,8 @@ struct FrameBufs {
   int32_t* order_fwd;   // longest-first tile orders of K5 / K6
   int32_t* order_bwd;
   int32_t* tile_work;   // K5 -> K6: per-tile largest terminal count
+  int* queue_fwd;       // the blends' unit queues (kQueueInts each)
+  int* queue_bwd;
   BinStatusDev* status;
   void* temp;
   size_t temp_bytes;
@@ -144,6 +146,8 @@ static FrameBufs carve_frame(void* ws, int64_t n, int tiles_x, int tiles_y, size
   f.order_fwd = c.take<int32_t>(n_tiles);
   f.order_bwd = c.take<int32_t>(n_tiles);
   f.tile_work = c.take<int32_t>(n_tiles);
+  f.queue_fwd = c.take<int>(kQueueInts);
+  f.queue_bwd = c.take<int>(kQueueInts);
   f.status = reinterpret_cast<BinStatusDev*>(f.counters ? f.counters + kBinStatusSlot : nullptr);
   f.temp_bytes = frame_temp_bytes(n, scan_len);
   f.temp = c.take<char>(f.temp_bytes);
@@ -564,6 +568,15 @@ static int fwd_sub_tiles(int n_tiles, int slots) {
   return 4;
 }
 
+// K5/K6 queues with an SM-spread first wave (HS_SPREAD=0: a plain counter)
+static int spread_queue() {
+  static const int on = [] {
+    const char* e = getenv("HS_SPREAD");
+    return e && e[0] == '0' ? 0 : 1;
+  }();
+  return on;
+}
+
 static BlendGeom frame_geom(const hs_frame* frame, const FrameBufs& f, const BinBufs& b) {
   BlendGeom g;
   g.tile_starts = f.tile_starts;
@@ -578,7 +591,8 @@ static BlendGeom frame_geom(const hs_frame* frame, const FrameBufs& f, const Bin
   g.tile_order = nullptr;
   g.tile_work = nullptr;
   g.sub_tiles = 1;
-  g.work_counter = f.counters;
+  g.work_counter = f.queue_fwd;
+  g.spread = spread_queue();
   return g;
 }
 
@@ -612,7 +626,7 @@ int hs_blend_bwd(hs_frame* frame, const double* bg, const float* d_color,
   FrameBufs f = frame_bufs(frame);
   BinBufs b = frame_bin(frame);
   BlendGeom g = frame_geom(frame, f, b);
-  g.work_counter = f.counters + 32;
+  g.work_counter = f.queue_bwd;
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
   if (lpt_order(frame->n_tiles, blend_bwd_slots())) {
     // K5 left each tile's largest terminal count: the positions K6 walks
@@ -882,6 +896,7 @@ int seam1_upload(Seam1Dev& d, const double* packed, const int8_t* mode,
   g.tile_work = nullptr;
   g.sub_tiles = 1;
   g.work_counter = (int*)d.ctr.p;
+  g.spread = 0;
   return HS_OK;
 }
 

@@ -88,10 +88,19 @@ struct BlendGeom {
   int width, height, tiles_x;
   int tile_lo, n_work;         // tiles [tile_lo, tile_lo + n_work)
   const int32_t* tile_order;   // optional work order (nullptr = natural)
-  int* work_counter;           // zeroed before launch
+  int* work_counter;           // the unit queue (UnitQueue below); zeroed by the launcher
   int32_t* tile_work;          // optional (K5): per-tile largest terminal count
   int sub_tiles;               // K5 work units per tile: 1 (16x16), 2 (16x8) or 4 (16x4)
+  int spread;                  // 1: first wave spread over the SMs (work_counter holds
+                               // kQueueInts ints), 0: plain dynamic queue (1 int)
+  int n_sm, per_sm, n_first;   // set by the launcher
 };
+// The blends' unit queue with an SM-spread first wave: [0] dynamic counter, [1]
+// sweep counter, [2, 2 + kQueueMaxSms) per-SM slot counters, then one claim flag per
+// first-wave unit.
+constexpr int kQueueMaxSms = 256;
+constexpr int kQueueMaxFirst = 4096;
+constexpr int kQueueInts = 2 + kQueueMaxSms + kQueueMaxFirst;
 int blend_fwd_slots();
 int blend_bwd_slots();
 // longest-first tile order: work = list length (starts != nullptr) or work[t]
