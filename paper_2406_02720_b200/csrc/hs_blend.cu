@@ -59,6 +59,7 @@ constexpr int kBwdWarps = HS_BWD_WARPS;
 #define HS_BWD_BOUNDS __launch_bounds__(kBwdWarps * 32)
 #endif
 constexpr int kBatch = 32;
+
 constexpr int kPx = 8;  // pixels per lane
 constexpr float kNegHalfLog2e = -0.5f * kLog2e;
 constexpr float kNegLog2e = -kLog2e;
@@ -448,7 +449,7 @@ __device__ __forceinline__ int alive_halves(const FwdPix<NPX>& P) {
   return (__any_sync(0xffffffffu, lo > 0.0f) ? 1 : 0) | (__any_sync(0xffffffffu, hi > 0.0f) ? 2 : 0);
 }
 
-#ifdef HS_K5_PROBE
+#if defined(HS_K5_PROBE) || defined(HS_K6_PROBE)
 // experiments only (tools/k5_probe.py): per work unit {start ns, end ns, splats
 // evaluated, SM id}
 __device__ long long g_k5_probe[65536 * 4];
@@ -473,7 +474,7 @@ extern "C" int hs_k5_probe_read(long long* out, int n_units) {
 // at NPX = 8).  Small frames (c1's 64 tiles, c2's 2500 against 2368 resident warps)
 // split their tiles into 2 or 4 sub-tiles, so more warps share the work and each
 // stops when its own pixels are done.
-template <int NPX>
+template <int NPX, bool CKPT>
 __global__ void HS_FWD_BOUNDS blend_fwd_kernel(
     BlendGeom g, float bg0, float bg1, float bg2, float* __restrict__ color,
     float* __restrict__ alpha, float* __restrict__ depth, float* __restrict__ trans,
@@ -519,6 +520,9 @@ __global__ void HS_FWD_BOUNDS blend_fwd_kernel(
     uint32_t vnext = nk > kBatch ? batch_index(g, k0 + kBatch, count_of(1), fwd_pos, lane) : 0u;
     bool any = true;
     int alive = kWinAll;
+    // pixel id within the tile (checkpoint layout: row * 16 + column) of pixel 0;
+    // pixel i is 32 i further
+    const int ck_pid0 = CKPT ? (sy0 - ty * kTile + (lane >> 4)) * kTile + (lane & 15) : 0;
     for (int b = 0; b * kBatch < nk && any; ++b) {
       const int nb = min(kBatch, nk - b * kBatch);
       if ((b + 1) * kBatch < nk) {
@@ -548,6 +552,25 @@ __global__ void HS_FWD_BOUNDS blend_fwd_kernel(
         if ((j & 7) == 0) {
           alive = alive_halves(P);
           if (!(any = alive != 0)) break;
+          if (CKPT && j == 0 && b > 0 && (b & (kCkpt / kBatch - 1)) == 0) {
+            // K6 segment checkpoint at list position m = b * kBatch: the state of
+            // every pixel still alive before splat m (T, negated colour sums so far)
+            // (scalar stores: a 16-B store would want the four values in an aligned
+            // register quad, which reshuffles the packed pixel pairs all over the loop)
+            float* ck = reinterpret_cast<float*>(
+                g.ckpt + ((size_t)((k0 + b * kBatch) >> kCkptShift) << kCkptShift));
+#pragma unroll
+            for (int i = 0; i < NPX; ++i) {
+              const int p = i >> 1, h = i & 1;
+              if (slot(P.A[p], h) > 0.f) {
+                float* e = ck + 4 * (ck_pid0 + 32 * i);
+                e[0] = slot(P.T[p], h);
+                e[1] = slot(P.ar[p], h);
+                e[2] = slot(P.ag[p], h);
+                e[3] = slot(P.ab[p], h);
+              }
+            }
+          }
         }
 #ifdef HS_K5_PROBE
         ++probe_splats;
@@ -589,6 +612,30 @@ __global__ void HS_FWD_BOUNDS blend_fwd_kernel(
         depth[o] = -slot(P.ad[p], h);
         trans[o] = t;
         terminal[o] = (int32_t)slot(P.C[p], h);
+      }
+    }
+    if (CKPT) {
+      // the checkpoints become (T_m, S_m): S_m = the pixel's final colour minus its
+      // colour before position m = background term + everything from m on, which K6
+      // needs there (its dC . S).  Written for count >= m (the pixel was alive
+      // before splat m), m < the list length.
+#pragma unroll
+      for (int i = 0; i < NPX; ++i) {
+        const int p = i >> 1, h = i & 1;
+        const int c = (int)slot(P.C[p], h);
+        if (c < kCkpt || col >= g.width || row0 + 2 * i >= g.height) continue;
+        const float t = slot(P.T[p], h);
+        const float fr = fmaf(t, bg0, -slot(P.ar[p], h)), fg = fmaf(t, bg1, -slot(P.ag[p], h)),
+                    fb = fmaf(t, bg2, -slot(P.ab[p], h));
+        for (int m = kCkpt; m <= c && m < nk; m += kCkpt) {
+          float4* ck =
+              g.ckpt + ((size_t)((k0 + m) >> kCkptShift) << kCkptShift) + ck_pid0 + 32 * i;
+          float4 v = *ck;
+          v.y = fr + v.y;
+          v.z = fg + v.z;
+          v.w = fb + v.w;
+          *ck = v;
+        }
       }
     }
 #ifdef HS_K5_PROBE
@@ -841,7 +888,7 @@ __device__ __forceinline__ float warp_reduce13_smem(const float (&v)[16], float*
 // check per splat; the restore itself runs once per distinct count).  So every
 // position runs the all-active bodies with their strip windows, masked further by
 // the halves (pairs 0-1, 2-3) in which every pixel is still inert.
-template <bool kRowsBySortedPos>
+template <bool kRowsBySortedPos, bool SPLIT>
 __global__ void HS_BWD_BOUNDS blend_bwd_kernel(
     BlendGeom g, float bg0, float bg1, float bg2, const float* __restrict__ d_color,
     const float* __restrict__ trans, const int32_t* __restrict__ terminal,
@@ -860,9 +907,21 @@ __global__ void HS_BWD_BOUNDS blend_bwd_kernel(
   float* tfin = &tfin_all[threadIdx.x >> 5][0][lane];
   float* dini = &dini_all[threadIdx.x >> 5][0][lane];
   int phase = 0;
+  const int n_units = SPLIT ? *g.n_units : g.n_work;
   for (;;) {
-    const int tile = next_tile(g, phase, lane);
-    if (tile < 0) break;
+    const int u = next_unit(g, n_units, phase, lane);
+    if (u < 0) break;
+    int tile, seg = -1;
+    if (SPLIT) {
+      const int2 un = g.units[u];
+      tile = un.x;
+      seg = un.y;
+    } else {
+      tile = g.tile_order ? g.tile_order[u] : g.tile_lo + u;
+    }
+#ifdef HS_K6_PROBE
+    const long long probe_t0 = global_ns();
+#endif
     const int ty = tile / g.tiles_x, tx = tile - ty * g.tiles_x;
     const int col = tx * kTile + (lane & 15);
     const int row0 = ty * kTile + (lane >> 4);
@@ -896,14 +955,35 @@ __global__ void HS_BWD_BOUNDS blend_bwd_kernel(
       }
     }
     maxc = __reduce_max_sync(0xffffffffu, maxc);
+    const int k0 = g.tile_starts[tile];
+    // K6 segments: this unit walks positions top-1 .. lo.  Below the tile's top
+    // segment, the pixels alive at `top` start from K5's checkpoint there (T before
+    // position top, S = everything blended from top on).
+    const int lo = SPLIT ? seg << kCkptShift : 0;
+    const int top = SPLIT ? min((seg + 1) << kCkptShift, maxc) : maxc;
+    if (SPLIT && top < maxc) {
+      const float4* ck = g.ckpt + ((size_t)((k0 + top) >> kCkptShift) << kCkptShift);
+#pragma unroll
+      for (int i = 0; i < kPx; ++i) {
+        const int p = i >> 1, h = i & 1;
+        const int c = cnt[i * 32];
+        if (c >= top && c != 0x7fffffff) {
+          const float4 v = ck[((lane >> 4) + 2 * i) * kTile + (lane & 15)];
+          // parked values first: a pixel is restored from them only below its count
+          slot(P.T[p], h) = v.x;
+          slot(P.D[p], h) = fmaf(slot(P.dr[p], h), v.y,
+                                 fmaf(slot(P.dg[p], h), v.z, slot(P.db[p], h) * v.w));
+        }
+      }
+    }
     // park the pixels that start inactive; nxt = the next activation level (the
-    // largest count below maxc), hmax_* = each half's largest count
+    // largest count below top), hmax_* = each half's largest count
     int nxt = -1, hmax_lo = 0, hmax_hi = 0;
 #pragma unroll
     for (int i = 0; i < kPx; ++i) {
       const int p = i >> 1, h = i & 1;
       const int c = cnt[i * 32];
-      if (c < maxc) {
+      if (c < top) {
         tfin[i * 32] = slot(P.T[p], h);
         dini[i * 32] = slot(P.D[p], h);
         slot(P.T[p], h) = 0.f;
@@ -916,25 +996,25 @@ __global__ void HS_BWD_BOUNDS blend_bwd_kernel(
     nxt = __reduce_max_sync(0xffffffffu, nxt);
     hmax_lo = __reduce_max_sync(0xffffffffu, hmax_lo);
     hmax_hi = __reduce_max_sync(0xffffffffu, hmax_hi);
-    const int k0 = g.tile_starts[tile];
-    if (!kRowsBySortedPos && lane == 0)
+    if (!kRowsBySortedPos && lane == 0 && top == maxc)
       last_rank[tile] =
           maxc > 0 ? (int32_t)rank_of[g.pair_src[k0 + maxc - 1] & kIndexMask] : -1;
-    if (maxc == 0) continue;
-    // positions maxc-1 .. 0; batch b holds positions hi_b - j for j < nb
-    auto batch_hi = [&](int b) { return maxc - 1 - b * kBatch; };
+    if (maxc == 0 || top <= lo) continue;
+    // positions top-1 .. lo; batch b holds positions hi_b - j for j < nb
+    const int len = top - lo;
+    auto batch_hi = [&](int b) { return top - 1 - b * kBatch; };
     auto bwd_index = [&](int b) {
       const int hi = batch_hi(b);
-      return batch_index(g, k0, min(kBatch, hi + 1), [hi](int j) { return hi - j; }, lane);
+      return batch_index(g, k0, min(kBatch, hi - lo + 1), [hi](int j) { return hi - j; }, lane);
     };
-    issue_records(g, bwd_index(0), min(kBatch, batch_hi(0) + 1), st, 0, lane);
-    uint32_t vnext = kBatch < maxc ? bwd_index(1) : 0u;
-    for (int b = 0; b * kBatch < maxc; ++b) {
+    issue_records(g, bwd_index(0), min(kBatch, len), st, 0, lane);
+    uint32_t vnext = kBatch < len ? bwd_index(1) : 0u;
+    for (int b = 0; b * kBatch < len; ++b) {
       const int hi = batch_hi(b);
-      const int nb = min(kBatch, hi + 1);
-      if ((b + 1) * kBatch < maxc) {
-        issue_records(g, vnext, min(kBatch, batch_hi(b + 1) + 1), st, (b + 1) & 1, lane);
-        if ((b + 2) * kBatch < maxc) vnext = bwd_index(b + 2);
+      const int nb = min(kBatch, hi - lo + 1);
+      if ((b + 1) * kBatch < len) {
+        issue_records(g, vnext, min(kBatch, batch_hi(b + 1) - lo + 1), st, (b + 1) & 1, lane);
+        if ((b + 2) * kBatch < len) vnext = bwd_index(b + 2);
       } else {
         cp_async_commit();
       }
@@ -1025,6 +1105,15 @@ __global__ void HS_BWD_BOUNDS blend_bwd_kernel(
     }
     cp_async_wait<0>();
     __syncwarp();
+#ifdef HS_K6_PROBE
+    if (lane == 0 && tile < 65536) {
+      long long* pr = g_k5_probe + 4 * (size_t)tile;
+      pr[0] = probe_t0;
+      pr[1] = global_ns();
+      pr[2] = maxc;
+      pr[3] = sm_id() | ((long long)tile << 16);
+    }
+#endif
   }
 }
 
@@ -1090,6 +1179,61 @@ __global__ void mark_steep_pairs_kernel(const uint8_t* __restrict__ steep_flag,
                                         uint32_t* __restrict__ pairs, int64_t p) {
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k < p && steep_flag[pairs[k]]) pairs[k] |= kSteepBit;
+}
+
+// K6 segments: the (tile, segment) units of a split backward, segments of kCkpt
+// list positions below each tile's largest terminal count (one unit for a tile
+// with nothing to walk, which still writes its last_rank), tiles in `order` (K6's
+// longest-first order) or natural order.  One CTA: a block scan per 1024 tiles.
+__global__ void __launch_bounds__(1024) bwd_units_kernel(const int32_t* __restrict__ work,
+                                                         const int32_t* __restrict__ order,
+                                                         int n_tiles, int2* __restrict__ units,
+                                                         int* __restrict__ n_units) {
+  __shared__ int warp_tot[32];
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int base = 0; base < n_tiles; base += 1024) {
+    const int i = base + threadIdx.x;
+    int t = 0, ns = 0;
+    if (i < n_tiles) {
+      t = order ? order[i] : i;
+      const int mc = work[t];
+      ns = mc > kCkpt ? (mc + kCkpt - 1) >> kCkptShift : 1;
+    }
+    int x = ns;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += v;
+    }
+    if (lane == 31) warp_tot[w] = x;
+    __syncthreads();
+    if (w == 0) {
+      int y = warp_tot[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, y, o);
+        if (lane >= o) y += v;
+      }
+      warp_tot[lane] = y;  // inclusive over warps
+    }
+    __syncthreads();
+    const int excl = carry + (w > 0 ? warp_tot[w - 1] : 0) + x - ns;
+    for (int k = 0; k < ns; ++k) units[excl + k] = make_int2(t, k);
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = excl + ns;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *n_units = carry;
+}
+
+cudaError_t launch_bwd_units(const int32_t* tile_work, const int32_t* order, int n_tiles,
+                             int2* units, int* n_units, cudaStream_t stream) {
+  bwd_units_kernel<<<1, 1024, 0, stream>>>(tile_work, order, n_tiles, units, n_units);
+  note_launch();
+  return cudaGetLastError();
 }
 
 // Longest-first tile order for the persistent blends (LPT): one CTA buckets the
@@ -1164,15 +1308,17 @@ static int blend_grid(Kernel kernel, int warps, int n_work, int* cache) {
   const int want = (n_work + warps - 1) / warps;
   return want < *cache ? (want > 0 ? want : 1) : *cache;
 }
-static int g_fwd_grid = 0, g_fwd_grid2 = 0, g_fwd_grid4 = 0, g_bwd_grid[2] = {0, 0};
+static int g_fwd_grid[3][2] = {{0, 0}, {0, 0}, {0, 0}}, g_bwd_grid[2][2] = {{0, 0}, {0, 0}};
 
 // resident warps of the persistent blends (the longest-first order pays only when
 // the tiles are several times these)
 int blend_fwd_slots() {
-  return blend_grid(blend_fwd_kernel<kPx>, kFwdWarps, 1 << 30, &g_fwd_grid) * kFwdWarps;
+  return blend_grid(blend_fwd_kernel<kPx, false>, kFwdWarps, 1 << 30, &g_fwd_grid[0][0]) *
+         kFwdWarps;
 }
 int blend_bwd_slots() {
-  return blend_grid(blend_bwd_kernel<false>, kBwdWarps, 1 << 30, &g_bwd_grid[0]) * kBwdWarps;
+  return blend_grid(blend_bwd_kernel<false, false>, kBwdWarps, 1 << 30, &g_bwd_grid[0][0]) *
+         kBwdWarps;
 }
 
 static int sm_count() {
@@ -1198,6 +1344,18 @@ static cudaError_t reset_queue(BlendGeom& g, int grid, int warps, cudaStream_t s
   return cudaMemsetAsync(g.work_counter, 0, sizeof(int) * (size_t)ints, stream);
 }
 
+template <int NPX, bool CKPT>
+static cudaError_t launch_fwd_variant(BlendGeom& g, int units, int* cache, float bg0, float bg1,
+                                      float bg2, float* color, float* alpha, float* depth,
+                                      float* trans, int32_t* terminal, cudaStream_t stream) {
+  const int grid = blend_grid(blend_fwd_kernel<NPX, CKPT>, kFwdWarps, units, cache);
+  const cudaError_t e = reset_queue(g, grid, kFwdWarps, stream);
+  if (e != cudaSuccess) return e;
+  blend_fwd_kernel<NPX, CKPT><<<grid, kFwdWarps * 32, 0, stream>>>(g, bg0, bg1, bg2, color, alpha,
+                                                                   depth, trans, terminal);
+  return cudaSuccess;
+}
+
 cudaError_t launch_blend_fwd(const BlendGeom& g_in, float bg0, float bg1, float bg2, float* color,
                              float* alpha, float* depth, float* trans, int32_t* terminal,
                              cudaStream_t stream) {
@@ -1209,30 +1367,36 @@ cudaError_t launch_blend_fwd(const BlendGeom& g_in, float bg0, float bg1, float 
     if (e != cudaSuccess) return e;
   }
   const int units = g.n_work * sub;
+  const bool ck = g.ckpt != nullptr;
+#define HS_FWD_LAUNCH(NPX, SLOT)                                                               \
+  (ck ? launch_fwd_variant<NPX, true>(g, units, &g_fwd_grid[SLOT][1], bg0, bg1, bg2, color,   \
+                                      alpha, depth, trans, terminal, stream)                  \
+      : launch_fwd_variant<NPX, false>(g, units, &g_fwd_grid[SLOT][0], bg0, bg1, bg2, color,  \
+                                       alpha, depth, trans, terminal, stream))
   switch (sub) {
-    case 4: {
-      const int grid = blend_grid(blend_fwd_kernel<2>, kFwdWarps, units, &g_fwd_grid4);
-      if ((e = reset_queue(g, grid, kFwdWarps, stream)) != cudaSuccess) return e;
-      blend_fwd_kernel<2><<<grid, kFwdWarps * 32, 0, stream>>>(g, bg0, bg1, bg2, color, alpha,
-                                                               depth, trans, terminal);
-      break;
-    }
-    case 2: {
-      const int grid = blend_grid(blend_fwd_kernel<4>, kFwdWarps, units, &g_fwd_grid2);
-      if ((e = reset_queue(g, grid, kFwdWarps, stream)) != cudaSuccess) return e;
-      blend_fwd_kernel<4><<<grid, kFwdWarps * 32, 0, stream>>>(g, bg0, bg1, bg2, color, alpha,
-                                                               depth, trans, terminal);
-      break;
-    }
-    default: {
-      const int grid = blend_grid(blend_fwd_kernel<kPx>, kFwdWarps, units, &g_fwd_grid);
-      if ((e = reset_queue(g, grid, kFwdWarps, stream)) != cudaSuccess) return e;
-      blend_fwd_kernel<kPx><<<grid, kFwdWarps * 32, 0, stream>>>(g, bg0, bg1, bg2, color, alpha,
-                                                                 depth, trans, terminal);
-    }
+    case 4: e = HS_FWD_LAUNCH(2, 2); break;
+    case 2: e = HS_FWD_LAUNCH(4, 1); break;
+    default: e = HS_FWD_LAUNCH(kPx, 0); break;
   }
+#undef HS_FWD_LAUNCH
+  if (e != cudaSuccess) return e;
   note_launch();
   return cudaGetLastError();
+}
+
+template <bool SORTED, bool SPLIT>
+static cudaError_t launch_bwd_variant(BlendGeom& g, int* cache, float bg0, float bg1, float bg2,
+                                      const float* d_color, const float* trans,
+                                      const int32_t* terminal, float* rows, int32_t* last_rank,
+                                      const uint32_t* rank_of, cudaStream_t stream) {
+  // a split backward's unit count is only known on the device: the persistent grid
+  const int grid = blend_grid(blend_bwd_kernel<SORTED, SPLIT>, kBwdWarps,
+                              SPLIT ? (1 << 30) : g.n_work, cache);
+  const cudaError_t e = reset_queue(g, grid, kBwdWarps, stream);
+  if (e != cudaSuccess) return e;
+  blend_bwd_kernel<SORTED, SPLIT><<<grid, kBwdWarps * 32, 0, stream>>>(
+      g, bg0, bg1, bg2, d_color, trans, terminal, rows, last_rank, rank_of);
+  return cudaSuccess;
 }
 
 cudaError_t launch_blend_bwd(const BlendGeom& g_in, float bg0, float bg1, float bg2,
@@ -1240,18 +1404,22 @@ cudaError_t launch_blend_bwd(const BlendGeom& g_in, float bg0, float bg1, float 
                              float* rows, int32_t* last_rank, const uint32_t* rank_of,
                              bool rows_by_sorted_pos, cudaStream_t stream) {
   BlendGeom g = g_in;
+  const bool split = g.units != nullptr;
   cudaError_t e;
-  if (rows_by_sorted_pos) {
-    const int grid = blend_grid(blend_bwd_kernel<true>, kBwdWarps, g.n_work, &g_bwd_grid[1]);
-    if ((e = reset_queue(g, grid, kBwdWarps, stream)) != cudaSuccess) return e;
-    blend_bwd_kernel<true><<<grid, kBwdWarps * 32, 0, stream>>>(
-        g, bg0, bg1, bg2, d_color, trans, terminal, rows, last_rank, rank_of);
-  } else {
-    const int grid = blend_grid(blend_bwd_kernel<false>, kBwdWarps, g.n_work, &g_bwd_grid[0]);
-    if ((e = reset_queue(g, grid, kBwdWarps, stream)) != cudaSuccess) return e;
-    blend_bwd_kernel<false><<<grid, kBwdWarps * 32, 0, stream>>>(
-        g, bg0, bg1, bg2, d_color, trans, terminal, rows, last_rank, rank_of);
-  }
+  if (rows_by_sorted_pos)
+    e = split ? launch_bwd_variant<true, true>(g, &g_bwd_grid[1][1], bg0, bg1, bg2, d_color,
+                                                trans, terminal, rows, last_rank, rank_of, stream)
+              : launch_bwd_variant<true, false>(g, &g_bwd_grid[1][0], bg0, bg1, bg2, d_color,
+                                                 trans, terminal, rows, last_rank, rank_of,
+                                                 stream);
+  else
+    e = split ? launch_bwd_variant<false, true>(g, &g_bwd_grid[0][1], bg0, bg1, bg2, d_color,
+                                                 trans, terminal, rows, last_rank, rank_of,
+                                                 stream)
+              : launch_bwd_variant<false, false>(g, &g_bwd_grid[0][0], bg0, bg1, bg2, d_color,
+                                                  trans, terminal, rows, last_rank, rank_of,
+                                                  stream);
+  if (e != cudaSuccess) return e;
   note_launch();
   return cudaGetLastError();
 }

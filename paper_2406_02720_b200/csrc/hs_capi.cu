@@ -165,9 +165,24 @@ struct BinBufs {
   uint32_t* pair_src;
   int32_t* seg_cnt;
   float* rows;
+  float4* ckpt;  // split backward only: K5's per-pixel checkpoints, K6's units
+  int2* units;
+  int* n_units;
   void* temp;
   size_t temp_bytes;
 };
+
+// Split backward (K6 segments, hs_blend.cu): frames of at most this many tiles --
+// c1, c2, c4; c3 has 8160 tiles -- where a few long tiles, not the total work, set
+// K6's time.  HS_K6_SPLIT=0 / 1 forces it off / on.
+constexpr int kSplitMaxTiles = 6144;
+static bool bwd_split(int64_t n_tiles) {
+  static const int mode = [] {
+    const char* e = getenv("HS_K6_SPLIT");
+    return e ? (e[0] == '0' ? 0 : 1) : 2;
+  }();
+  return mode == 1 || (mode == 2 && n_tiles <= kSplitMaxTiles);
+}
 
 static BinBufs carve_bin(void* ws, int64_t p, int tiles_x, int tiles_y, size_t* total) {
   Carver c(ws);
@@ -188,6 +203,13 @@ static BinBufs carve_bin(void* ws, int64_t p, int tiles_x, int tiles_y, size_t* 
     b.temp = c.take<char>(b.temp_bytes);
   }
   b.rows = c.take<float>(pp * kRowFloats);
+  const int64_t n_tiles = (int64_t)tiles_x * tiles_y;
+  if (bwd_split(n_tiles)) {
+    // one checkpoint slot (kCkpt pixels) per kCkpt pairs; one unit per tile + per segment
+    b.ckpt = c.take<float4>(((pp >> kCkptShift) + 2) << kCkptShift);
+    b.units = c.take<int2>((size_t)n_tiles + (pp >> kCkptShift) + 1);
+    b.n_units = c.take<int>(1);
+  }
   if (total) *total = c.off;
   return b;
 }
@@ -593,6 +615,9 @@ static BlendGeom frame_geom(const hs_frame* frame, const FrameBufs& f, const Bin
   g.sub_tiles = 1;
   g.work_counter = f.queue_fwd;
   g.spread = spread_queue();
+  g.ckpt = nullptr;
+  g.units = nullptr;
+  g.n_units = nullptr;
   return g;
 }
 
@@ -608,6 +633,7 @@ int hs_blend_fwd(hs_frame* frame, const double* bg, float* color, float* alpha, 
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
   g.tile_work = f.tile_work;
   g.sub_tiles = fwd_sub_tiles(frame->n_tiles, blend_fwd_slots());
+  if (bwd_split(frame->n_tiles)) g.ckpt = b.ckpt;
   if (lpt_order(frame->n_tiles * g.sub_tiles, blend_fwd_slots())) {
     HS_CUDA(launch_tile_order(f.tile_starts, nullptr, frame->n_tiles, f.order_fwd, stream));
     g.tile_order = f.order_fwd;
@@ -632,6 +658,14 @@ int hs_blend_bwd(hs_frame* frame, const double* bg, const float* d_color,
     // K5 left each tile's largest terminal count: the positions K6 walks
     HS_CUDA(launch_tile_order(nullptr, f.tile_work, frame->n_tiles, f.order_bwd, stream));
     g.tile_order = f.order_bwd;
+  }
+  if (bwd_split(frame->n_tiles)) {
+    // (tile, segment) units from K5's checkpoints, tiles in the order above
+    HS_CUDA(launch_bwd_units(f.tile_work, g.tile_order, frame->n_tiles, b.units, b.n_units,
+                             stream));
+    g.ckpt = b.ckpt;
+    g.units = b.units;
+    g.n_units = b.n_units;
   }
   HS_CUDA(launch_blend_bwd(g, (float)bg[0], (float)bg[1], (float)bg[2], d_color, transmittance,
                            terminal, b.rows, f.last_rank, f.rank_of, false, stream));
@@ -897,6 +931,9 @@ int seam1_upload(Seam1Dev& d, const double* packed, const int8_t* mode,
   g.sub_tiles = 1;
   g.work_counter = (int*)d.ctr.p;
   g.spread = 0;
+  g.ckpt = nullptr;
+  g.units = nullptr;
+  g.n_units = nullptr;
   return HS_OK;
 }
 

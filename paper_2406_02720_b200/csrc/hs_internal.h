@@ -94,7 +94,16 @@ struct BlendGeom {
   int spread;                  // 1: first wave spread over the SMs (work_counter holds
                                // kQueueInts ints), 0: plain dynamic queue (1 int)
   int n_sm, per_sm, n_first;   // set by the launcher
+  // Split backward (small frames, see hs_blend.cu "K6 segments"): K5 leaves per-pixel
+  // checkpoints every kCkpt list positions, K6 runs (tile, segment) units
+  float4* ckpt;                // nullptr: off
+  const int2* units;           // K6: (tile, segment) units, *n_units of them
+  const int* n_units;
 };
+constexpr int kCkptShift = 8;
+constexpr int kCkpt = 1 << kCkptShift;  // list positions per K6 segment / checkpoint
+cudaError_t launch_bwd_units(const int32_t* tile_work, const int32_t* order, int n_tiles,
+                             int2* units, int* n_units, cudaStream_t stream);
 // The blends' unit queue with an SM-spread first wave: [0] dynamic counter, [1]
 // sweep counter, [2, 2 + kQueueMaxSms) per-SM slot counters, then one claim flag per
 // first-wave unit.

@@ -244,3 +244,28 @@ def test_wide_splat_row_merge_oracle(cuda):
            "transmittance": ref_out.transmittance, "terminal": ref_out.per_pixel_terminal_index}
     assert_images(got, ref)
     assert_grads(got, ref_g)
+
+
+@pytest.mark.parametrize("kernel", ["half", "full"])
+def test_split_backward_long_lists_oracle(cuda, kernel):
+    """Small frames run K6 as (tile, segment) units of 256 list positions, each below
+    the top starting from K5's checkpoint (hs_blend.cu "K6 segments"): a ball whose
+    tile lists run to thousands of splats, pixels alive through several segments,
+    against the oracle's gradients; K5's images and the integers are unchanged."""
+    O = _oracle()
+    sa = scenes.ball(30_000, 2, 128, 96, views=2, seed=31)
+    s64 = sa.as_float64()
+    cam = CameraModel(**sa.cameras[1])
+    d_color = scenes.cotangent(cam.height, cam.width, seed=7)
+    ref_out = O.render(s64, cam, kernel=kernel)
+    ref_g = O.render_backward(s64, cam, ref_out, d_color)
+    got = run_gpu(sa, 1, kernel, torch.float32, d_color)
+    lens = np.diff(np.asarray(got["tile_starts"]))
+    assert lens.max() > 4 * 256  # several segments per tile
+    assert (got["terminal"] > 2 * 256).mean() > 0.05  # pixels alive past two checkpoints
+    assert np.array_equal(got["tile_starts"], ref_out.frame.tile_starts)
+    ref = {"color": ref_out.color, "alpha": ref_out.alpha, "depth": ref_out.depth,
+           "transmittance": ref_out.transmittance, "terminal": ref_out.per_pixel_terminal_index}
+    assert_images(got, ref)
+    assert_grads(got, ref_g)
+    assert np.array_equal(got["touch_count"], ref_g["touch_count"])

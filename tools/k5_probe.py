@@ -1,9 +1,9 @@
-"""K5's work units on one view, from a library built with -DHS_K5_PROBE
-(tools/build_variant.sh probe -DHS_K5_PROBE, copied over the in-tree library):
-when each unit started and ended, how many splats it evaluated, and the
-critical units' nanoseconds per splat.
+"""K5's (or K6's) work units on one view, from a library built with -DHS_K5_PROBE
+(or -DHS_K6_PROBE; tools/build_variant.sh probe -DHS_K5_PROBE, copied over the
+in-tree library): when each unit started and ended, how many splats it evaluated,
+and the critical units' nanoseconds per splat.
 
-    python tools/k5_probe.py c2 [view]   (on a GPU box)
+    python tools/k5_probe.py c2 [view] [bwd]   (on a GPU box)
 """
 import ctypes
 import sys
@@ -22,8 +22,13 @@ cam = CameraModel(**sa.cameras[view])
 sc = Scene(*(getattr(sa, f) for f in sa.FIELDS), sh_degree=sa.sh_degree,
            background_color=sa.background_color, device="cuda", dtype=torch.float32)
 rast = device.Rasterizer("cuda")
+bwd = len(sys.argv) > 3
+d_color = torch.as_tensor(scenes.cotangent(cam.height, cam.width), dtype=torch.float32,
+                          device="cuda")
 for _ in range(3):
     out = rast.render(sc, cam)
+    if bwd:
+        rast.render_backward(sc, cam, out, d_color)
 torch.cuda.synchronize()
 lib = _native.load()
 n = 65536
