@@ -43,7 +43,18 @@ def _worker(rank, world, port, dtype_name, bucketed, q):
         cams = [CameraModel(**c) for c in sa.cameras]
         dcs = [torch.as_tensor(scenes.cotangent(c.height, c.width, seed=10 + i),
                                dtype=torch.float32, device="cuda") for i, c in enumerate(cams)]
-        if bucketed:
+        if bucketed == "views":
+            # the multi-view backward (one K7 pass for the rank's views) in buckets,
+            # each bucket's exchange issued right after its launch
+            views = multiview.shard_views(len(cams), world, rank)
+            grads = device.DeviceGradientSet.empty_flat(scene)
+            red = multiview.GradientAllReduce(grads)
+            batch = multiview.ViewBatch(scene, len(views))
+            batch.run(scene, cams, dcs, views, grads,
+                      buckets=multiview.GradientAllReduce.bucket_ranges(len(scene), buckets=3),
+                      on_bucket=red.start_range)
+            red.finish()
+        elif bucketed:
             views = multiview.shard_views(len(cams), world, rank)
             grads = device.DeviceGradientSet.empty_flat(scene)
             red = multiview.GradientAllReduce(grads)
@@ -104,7 +115,8 @@ def _oracle_batch():
 
 
 @pytest.mark.parametrize("dtype_name,bucketed,port", [("float32", False, 29611),
-                                                      ("float64", True, 29613)])
+                                                      ("float64", True, 29613),
+                                                      ("float32", "views", 29615)])
 def test_two_rank_batch_gradient_equals_oracle_sum(cuda, dtype_name, bucketed, port):
     res = _run(dtype_name, bucketed, port)
     ref = _oracle_batch()
