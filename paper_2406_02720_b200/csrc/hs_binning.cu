@@ -25,6 +25,11 @@ size_t depth_sort_temp_bytes(int64_t n) {
                                   (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)n, 0, 64);
   cub::DeviceRadixSort::SortPairs(nullptr, hi, (const uint64_t*)nullptr, (uint64_t*)nullptr,
                                   (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)n, 32, 64);
+  size_t k24 = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, k24, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                  (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)n, 0,
+                                  kDepthKeyBits);
+  if (k24 > bytes) bytes = k24;
   return bytes > hi ? bytes : hi;
 }
 
@@ -70,25 +75,28 @@ cudaError_t run_depth_sort(void* temp, size_t temp_bytes, const uint64_t* keys_i
 constexpr int kMaxDepthRun = HS_MAX_DEPTH_RUN;
 
 // newpos[k] = position of sorted element k after its run is ordered by the full
-// key; val[k] = its order value (copied, so the scatter does not race)
-__global__ void depth_run_rank_kernel(const uint64_t* __restrict__ keys,
+// key; val[k] = its order value (copied, so the scatter does not race).  The runs
+// are runs of equal 24-bit keys (= equal upper 32 bits of the depth, see
+// depth_key24_kernel); the full keys are read from the unsorted array by index.
+__global__ void depth_run_rank_kernel(const uint32_t* __restrict__ key24,
+                                      const uint64_t* __restrict__ full,
                                       const uint32_t* __restrict__ order, int64_t n,
                                       uint32_t* __restrict__ newpos, uint32_t* __restrict__ val,
                                       int* __restrict__ overflow) {
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
-  const uint64_t key = keys[k];
-  const uint32_t hi = (uint32_t)(key >> 32);
-  val[k] = order[k];
-  if (hi == 0xffffffffu) {  // culled
+  const uint32_t hk = key24[k];
+  const uint32_t vk = order[k];
+  val[k] = vk;
+  if (hk == kDepthKeyCulled) {  // culled: one run, already in index order
     newpos[k] = (uint32_t)k;
     return;
   }
-  // The run's bounds by galloping then bisecting over the sorted upper bits:
-  // O(log run) dependent loads instead of O(run).  s = first index >= lo with
-  // this hi; e = first index in (k, cap) with another hi, else cap -- the same
-  // bounds a linear walk capped at kMaxDepthRun finds.
-  auto same = [&](int64_t j) { return (uint32_t)(keys[j] >> 32) == hi; };
+  // The run's bounds by galloping then bisecting over the sorted keys: O(log run)
+  // dependent loads instead of O(run).  s = first index >= lo with this key; e =
+  // first index in (k, cap) with another key, else cap -- the same bounds a linear
+  // walk capped at kMaxDepthRun finds.
+  auto same = [&](int64_t j) { return key24[j] == hk; };
   const int64_t lo = k - kMaxDepthRun > 0 ? k - kMaxDepthRun : 0;
   int64_t good = k, bad = lo - 1;
   for (int64_t step = 1;; step <<= 1) {
@@ -107,7 +115,7 @@ __global__ void depth_run_rank_kernel(const uint64_t* __restrict__ keys,
   }
   const int64_t s = good;
   const int64_t cap = s + kMaxDepthRun + 1 < n ? s + kMaxDepthRun + 1 : n;
-  int64_t in = k, out = cap;  // same(in); out = cap or an index with another hi
+  int64_t in = k, out = cap;  // same(in); out = cap or an index with another key
   for (int64_t step = 1;; step <<= 1) {
     const int64_t c = in + step;
     if (c >= cap) break;
@@ -128,12 +136,40 @@ __global__ void depth_run_rank_kernel(const uint64_t* __restrict__ keys,
     newpos[k] = (uint32_t)k;
     return;
   }
+  if (e - s == 1) {  // the usual case: a run of one
+    newpos[k] = (uint32_t)k;
+    return;
+  }
+  const uint64_t key = full[vk & kIndexMask];
   int64_t r = 0;
+  // (independent iterations: unrolled so several gathers are in flight)
+#pragma unroll 8
   for (int64_t j = s; j < e; ++j) {
-    const uint64_t kj = keys[j];
+    const uint64_t kj = full[order[j] & kIndexMask];
     r += (kj < key || (kj == key && j < k)) ? 1 : 0;
   }
   newpos[k] = (uint32_t)(s + r);
+}
+
+// The sort key: the upper 32 bits of a visible splat's f64 depth minus the
+// frame's smallest (K1 reduces the range), which fits 24 bits unless the depths
+// span a factor ~2^16 -- then the overflow flag sends the frame to the full
+// 64-bit sort.  Culled splats take the largest key.  3 radix passes of 8 bits on
+// 4-byte keys instead of 4 passes on 8-byte ones.
+__global__ void depth_key24_kernel(const uint64_t* __restrict__ keys, int64_t n,
+                                   const uint32_t* __restrict__ range, uint32_t* __restrict__ out,
+                                   int* __restrict__ overflow) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const uint32_t lo = range[0], hi_max = range[1];
+  const uint32_t hi = (uint32_t)(keys[k] >> 32);
+  if (hi == 0xffffffffu) {
+    out[k] = kDepthKeyCulled;
+    return;
+  }
+  if (k == 0 && hi_max - lo >= kDepthKeyCulled) atomicExch(overflow, 1);
+  const uint32_t d = hi - lo;
+  out[k] = d < kDepthKeyCulled ? d : kDepthKeyCulled - 1;
 }
 
 __global__ void depth_run_scatter_kernel(const uint32_t* __restrict__ newpos,
@@ -146,19 +182,23 @@ __global__ void depth_run_scatter_kernel(const uint32_t* __restrict__ newpos,
 cudaError_t run_depth_sort_hi(void* temp, size_t temp_bytes, const uint64_t* keys_in,
                               uint64_t* keys_out, const uint32_t* vals_in, uint32_t* order,
                               int64_t n, uint32_t* scratch_pos, uint32_t* scratch_val,
-                              int* overflow, cudaStream_t stream) {
+                              int* overflow, const uint32_t* range, cudaStream_t stream) {
   cudaError_t e = cudaMemsetAsync(overflow, 0, sizeof(int), stream);
-  if (e != cudaSuccess) return e;
-  e = cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_in, keys_out, vals_in, order, (int)n,
-                                      32, 64, stream);
-  note_launch(5);
   if (e != cudaSuccess) return e;
   const int block = 256;
   const unsigned grid = (unsigned)((n + block - 1) / block);
-  depth_run_rank_kernel<<<grid, block, 0, stream>>>(keys_out, order, n, scratch_pos, scratch_val,
-                                                    overflow);
+  // keys_out (8 bytes per splat) holds the 24-bit keys, unsorted then sorted
+  uint32_t* k24_in = reinterpret_cast<uint32_t*>(keys_out);
+  uint32_t* k24_out = k24_in + n;
+  depth_key24_kernel<<<grid, block, 0, stream>>>(keys_in, n, range, k24_in, overflow);
+  e = cub::DeviceRadixSort::SortPairs(temp, temp_bytes, k24_in, k24_out, vals_in, order, (int)n, 0,
+                                      kDepthKeyBits, stream);
+  note_launch(5);
+  if (e != cudaSuccess) return e;
+  depth_run_rank_kernel<<<grid, block, 0, stream>>>(k24_out, keys_in, order, n, scratch_pos,
+                                                    scratch_val, overflow);
   depth_run_scatter_kernel<<<grid, block, 0, stream>>>(scratch_pos, scratch_val, n, order);
-  note_launch(2);
+  note_launch(3);
   return cudaGetLastError();
 }
 

@@ -48,9 +48,10 @@ struct Carver {
   }
 };
 
-// counters[]: 48 depth-fixup overflow flag,
+// counters[]: 48 depth-fixup overflow flag, 60-61 depth range (K1 -> rank sort),
 // 52-57 the binning status (BinStatusDev: P and segments as int64, flags)
 constexpr int kDepthOverflowSlot = 48;
+constexpr int kDepthRangeSlot = 60;  // 60-61: the visible depths' upper-word range
 constexpr int kBinStatusSlot = 52;
 
 struct FrameBufs {
@@ -397,14 +398,22 @@ int hs_preprocess_fwd(hs_frame* frame, const hs_scene* scene, const hs_camera* c
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
   FrameBufs f = frame_bufs(frame);
   const CamArgs ca = cam_args(cam);
+  // the 24-bit rank sort's depth range: [min, max] of the visible upper words
+  uint32_t* range = frame->depth_sort_full
+                        ? nullptr
+                        : reinterpret_cast<uint32_t*>(f.counters + kDepthRangeSlot);
+  if (range) {
+    HS_CUDA(cudaMemsetAsync(range, 0xff, sizeof(uint32_t), stream));
+    HS_CUDA(cudaMemsetAsync(range + 1, 0, sizeof(uint32_t), stream));
+  }
   if (scene->dtype == HS_DTYPE_F32) {
     HS_CUDA(launch_preprocess_fwd_t<float>(scene_args<float>(scene), ca, frame->kernel, frame->n,
                                            f.rec, f.side, f.rect, f.count, f.dkey_in, f.dval,
-                                           radii, stream));
+                                           radii, range, stream));
   } else {
     HS_CUDA(launch_preprocess_fwd_t<double>(scene_args<double>(scene), ca, frame->kernel,
                                             frame->n, f.rec, f.side, f.rect, f.count, f.dkey_in,
-                                            f.dval, radii, stream));
+                                            f.dval, radii, range, stream));
   }
   if (frame->depth_sort_full) {
     HS_CUDA(cudaMemsetAsync(f.counters + kDepthOverflowSlot, 0, sizeof(int), stream));
@@ -414,7 +423,7 @@ int hs_preprocess_fwd(hs_frame* frame, const hs_scene* scene, const hs_camera* c
     // rank_of and cnt_r are outputs of the count scan below: free as fixup scratch here
     HS_CUDA(run_depth_sort_hi(f.temp, f.temp_bytes, f.dkey_in, f.dkey_out, f.dval, f.order,
                               frame->n, f.rank_of, reinterpret_cast<uint32_t*>(f.cnt_r),
-                              f.counters + kDepthOverflowSlot, stream));
+                              f.counters + kDepthOverflowSlot, range, stream));
   }
   HS_CUDA(count_scan(frame, f, stream));
   frame->num_pairs = -1;

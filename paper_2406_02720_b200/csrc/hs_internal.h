@@ -51,7 +51,7 @@ template <typename T>
 cudaError_t launch_preprocess_fwd_t(const SceneArgs<T>& sc, const CamArgs& cam, int kernel,
                                     int64_t n, float4* rec, SteepRec* side, int4* rect,
                                     int32_t* count, uint64_t* dkey, uint32_t* dval,
-                                    int32_t* radii, cudaStream_t stream);
+                                    int32_t* radii, uint32_t* depth_range, cudaStream_t stream);
 template <typename T>
 cudaError_t launch_preprocess_bwd_t(const SceneArgs<T>& sc, const CamArgs& cam, int kernel,
                                     int64_t n, int tiles_x, const float4* rec, const int4* rect,
@@ -143,10 +143,13 @@ cudaError_t run_depth_sort(void* temp, size_t temp_bytes, const uint64_t* keys_i
                            int64_t n, cudaStream_t stream);
 // upper-32-bit sort + per-run fixup (two n-element u32 scratch arrays); *overflow =
 // 1 when a run was too long (then run_depth_sort must redo the ranks)
+// range: the visible splats' smallest and largest upper depth word (K1)
 cudaError_t run_depth_sort_hi(void* temp, size_t temp_bytes, const uint64_t* keys_in,
                               uint64_t* keys_out, const uint32_t* vals_in, uint32_t* order,
                               int64_t n, uint32_t* scratch_pos, uint32_t* scratch_val,
-                              int* overflow, cudaStream_t stream);
+                              int* overflow, const uint32_t* range, cudaStream_t stream);
+constexpr int kDepthKeyBits = 24;
+constexpr uint32_t kDepthKeyCulled = (1u << kDepthKeyBits) - 1u;
 // ---- tile binning without a host round trip -------------------
 // A splat's pairs in one tile row and one block of 32 tile columns form a
 // SEGMENT (value, first column, length).  The count pass histograms every block

@@ -563,7 +563,8 @@ template <typename T, int DEG, int NT>
 __global__ void HS_K1_BOUNDS preprocess_fwd_kernel(
     SceneArgs<T> sc, CamArgs cam, int kernel, int64_t n, float4* __restrict__ rec,
     SteepRec* __restrict__ side, int4* __restrict__ rect, int32_t* __restrict__ count,
-    uint64_t* __restrict__ dkey, uint32_t* __restrict__ dval, int32_t* __restrict__ radii) {
+    uint64_t* __restrict__ dkey, uint32_t* __restrict__ dval, int32_t* __restrict__ radii,
+    uint32_t* __restrict__ depth_range) {
   constexpr int K = (DEG + 1) * (DEG + 1);
   __shared__ Staged<T, K, NT> sm;
   const int64_t base = (int64_t)blockIdx.x * NT;
@@ -589,6 +590,17 @@ __global__ void HS_K1_BOUNDS preprocess_fwd_kernel(
   // positive depths order like their IEEE bit patterns; the stable radix sort
   // then breaks exact ties by primitive index, as np.lexsort does.
   dkey[i] = (uint64_t)__double_as_longlong(st.t[2]);
+  if (depth_range) {
+    // the visible depths' range of upper words, for the 24-bit rank sort: one
+    // atomic pair per group of converged lanes
+    const uint32_t hi = (uint32_t)((uint64_t)__double_as_longlong(st.t[2]) >> 32);
+    const unsigned am = __activemask();
+    const uint32_t mn = __reduce_min_sync(am, hi), mx = __reduce_max_sync(am, hi);
+    if ((threadIdx.x & 31) == __ffs(am) - 1) {
+      atomicMin(depth_range, mn);
+      atomicMax(depth_range + 1, mx);
+    }
+  }
   if (radii) radii[i] = (int32_t)ceil(st.radius);
   const bool steep = st.mode != kModePlain && is_steep(st.za, st.zb, st.radius + 24.0);
   dval[i] = (uint32_t)i | (steep ? kSteepBit : 0u);
@@ -1373,7 +1385,7 @@ template <typename T>
 cudaError_t launch_preprocess_fwd_t(const SceneArgs<T>& sc, const CamArgs& cam, int kernel,
                                     int64_t n, float4* rec, SteepRec* side, int4* rect,
                                     int32_t* count, uint64_t* dkey, uint32_t* dval,
-                                    int32_t* radii, cudaStream_t stream) {
+                                    int32_t* radii, uint32_t* depth_range, cudaStream_t stream) {
   // staging holds NT primitives in shared memory: 128 float or 64 double ones
   constexpr int NT = sizeof(T) == 4 ? 128 : 64;
   const int64_t grid = (n + NT - 1) / NT;
@@ -1382,7 +1394,8 @@ cudaError_t launch_preprocess_fwd_t(const SceneArgs<T>& sc, const CamArgs& cam, 
   case D:                                                                                      \
     preprocess_fwd_kernel<T, D, NT><<<(unsigned)grid, NT, 0, stream>>>(sc, cam, kernel, n, rec, \
                                                                        side, rect, count, dkey, \
-                                                                       dval, radii);           \
+                                                                       dval, radii,            \
+                                                                       depth_range);           \
     break;
     HS_K1(0) HS_K1(1) HS_K1(2) HS_K1(3)
 #undef HS_K1
@@ -1394,10 +1407,12 @@ cudaError_t launch_preprocess_fwd_t(const SceneArgs<T>& sc, const CamArgs& cam, 
 
 template cudaError_t launch_preprocess_fwd_t<float>(const SceneArgs<float>&, const CamArgs&, int,
                                                     int64_t, float4*, SteepRec*, int4*, int32_t*,
-                                                    uint64_t*, uint32_t*, int32_t*, cudaStream_t);
+                                                    uint64_t*, uint32_t*, int32_t*, uint32_t*,
+                                                    cudaStream_t);
 template cudaError_t launch_preprocess_fwd_t<double>(const SceneArgs<double>&, const CamArgs&, int,
                                                      int64_t, float4*, SteepRec*, int4*, int32_t*,
-                                                     uint64_t*, uint32_t*, int32_t*, cudaStream_t);
+                                                     uint64_t*, uint32_t*, int32_t*, uint32_t*,
+                                                     cudaStream_t);
 #else
 template <typename T>
 cudaError_t launch_preprocess_bwd_t(const SceneArgs<T>& sc, const CamArgs& cam, int kernel,
