@@ -154,7 +154,8 @@ __global__ void depth_run_rank_kernel(const uint32_t* __restrict__ key24,
 // The sort key: the upper 32 bits of a visible splat's f64 depth minus the
 // frame's smallest (K1 reduces the range), which fits 24 bits unless the depths
 // span a factor ~2^16 -- then the overflow flag sends the frame to the full
-// 64-bit sort.  Culled splats take the largest key.  3 radix passes of 8 bits on
+// 64-bit sort (the clamped keys would still rank right while the farthest run
+// fits the fixup).  Culled splats take the largest key.  3 radix passes of 8 bits on
 // 4-byte keys instead of 4 passes on 8-byte ones.
 __global__ void depth_key24_kernel(const uint64_t* __restrict__ keys, int64_t n,
                                    const uint32_t* __restrict__ range, uint32_t* __restrict__ out,
@@ -162,12 +163,12 @@ __global__ void depth_key24_kernel(const uint64_t* __restrict__ keys, int64_t n,
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
   const uint32_t lo = range[0], hi_max = range[1];
+  if (k == 0 && lo <= hi_max && hi_max - lo >= kDepthKeyCulled) atomicExch(overflow, 1);
   const uint32_t hi = (uint32_t)(keys[k] >> 32);
   if (hi == 0xffffffffu) {
     out[k] = kDepthKeyCulled;
     return;
   }
-  if (k == 0 && hi_max - lo >= kDepthKeyCulled) atomicExch(overflow, 1);
   const uint32_t d = hi - lo;
   out[k] = d < kDepthKeyCulled ? d : kDepthKeyCulled - 1;
 }

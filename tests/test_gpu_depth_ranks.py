@@ -1,6 +1,7 @@
 """Depth ranks (hs_binning.cu run_depth_sort_hi): a stable sort on the upper 32
-bits of the f64 depth plus a per-run fixup, with a full 64-bit re-sort when a
-run is too long for the fixup.  The pair order must stay exactly np.lexsort's
+bits of the f64 depth (as 24-bit offsets from the frame's smallest) plus a
+per-run fixup, with a full 64-bit re-sort when a run is too long for the fixup
+or the depths span too wide a range for 24 bits.  The pair order must stay exactly np.lexsort's
 (tile, depth, index) order in all three regimes: short runs, runs just under
 the fixup limit, and runs far over it (the fallback)."""
 
@@ -29,10 +30,12 @@ def _check(sa):
     cam = CameraModel(**sa.cameras[0])
     sc = Scene(*(getattr(sa, f) for f in sa.FIELDS), sh_degree=sa.sh_degree,
                background_color=sa.background_color, device="cuda", dtype=torch.float64)
-    ex = device.prepare(sc, cam).export()
+    frame = device.prepare(sc, cam)
+    ex = frame.export()
     ref = O.prepare(sa, cam)
     assert np.array_equal(ex["tile_starts"], ref.tile_starts)
     assert np.array_equal(ex["pair_splat"], ref.pair_splat)
+    return frame
 
 
 def test_short_runs_in_upper_bits():
@@ -59,6 +62,25 @@ def test_long_runs_take_the_full_sort():
     # exactly equal ones (ranked by index)
     z = np.concatenate([4.0 + rng.permutation(2500) * 2.0 ** -42, np.full(1500, 5.0)])
     _check(_with_depths(n, z[rng.permutation(n)]))
+
+
+def test_depth_range_wider_than_24_bits_takes_the_full_sort():
+    # visible depths from 0.02 to 5000: the upper words span more than 2^24, so the
+    # 24-bit key overflows and the ranks come from the 64-bit sort
+    rng = np.random.default_rng(4)
+    n = 3000
+    z = np.exp(rng.uniform(np.log(0.02), np.log(5000.0), n))
+    sa = _with_depths(n, z)
+    sa.cameras[0]["near_clip"] = 0.01
+    assert _check(sa).st.depth_sort_full == 1
+
+
+def test_depth_range_just_inside_24_bits():
+    # upper words from 2.0 to just under 2^(2+16): the widest range the 24-bit keys hold
+    rng = np.random.default_rng(5)
+    n = 3000
+    z = 2.0 * 2.0 ** rng.uniform(0.0, 15.99, n)
+    assert _check(_with_depths(n, z)).st.depth_sort_full == 0
 
 
 def test_workspace_reuse_across_pair_counts():
