@@ -4,7 +4,7 @@ import csv
 import sys
 
 
-def main(path, which=3):
+def main(path, which=3, label="c3"):
     rows = []
     with open(path) as fh:
         lines = [ln for ln in fh if ln.startswith('"')]
@@ -16,7 +16,7 @@ def main(path, which=3):
     i1 = next(i for i in range(i0, len(rows)) if "preprocess_bwd_kernel" in rows[i][0])
     step = rows[i0:i1 + 1]
     tot = sum(t for _, t in step)
-    print("# ncu launch list, one c3 fwd+bwd step (bench.py --steps 2 --warmup 3), B200")
+    print(f"# ncu launch list, one {label} fwd+bwd step (bench.py --steps 2 --warmup 3), B200")
     print("# gpu__time_duration.sum per launch, --clock-control none; ncu serialises launches and")
     print("# runs them cold-cache, so compare SHARES with bench.py's event times, not absolutes.")
     print(f"{'kernel':75s} {'us':>8s} {'share':>7s}")
@@ -26,4 +26,5 @@ def main(path, which=3):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 3)
+    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 3,
+         sys.argv[3] if len(sys.argv) > 3 else "c3")

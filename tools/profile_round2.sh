@@ -12,18 +12,29 @@ for CFG in c3 c4 c5; do
   CMD="python bench.py --config $CFG --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-clocks --no-configs --no-graph"
   timeout 600 $CMD > $O/plain_$CFG.log 2>&1 || { echo "plain $CFG failed" >> $O/status.txt; continue; }
   N=150; W=3
-  if [ $CFG = c4 ]; then N=700; W=20; fi
+  # c4: a step is 8 views (K1-K7a each) and one multi-view K7
+  if [ $CFG = c4 ]; then N=900; W=24; fi
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c $N --csv \
     --log-file $O/launches_$CFG.csv $CMD > $O/ncu_list_$CFG.log 2>&1
-  python tools/launch_list.py $O/launches_$CFG.csv $W > $O/launch_list_$CFG.txt 2>&1
+  python tools/launch_list.py $O/launches_$CFG.csv $W $CFG > $O/launch_list_$CFG.txt 2>&1
   echo "list_$CFG=$?" >> $O/status.txt
 done
 CMD="python bench.py --config c3 --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-clocks --no-configs --no-graph"
 for K in blend_bwd blend_fwd preprocess_bwd_kernel preprocess_fwd_kernel merge_rows seg_emit \
-         seg_fill gather_counts; do
+         seg_fill gather_counts depth_run_rank; do
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$K -s 3 -c 1 \
     -o $O/prof_$K -f $CMD > $O/ncu_$K.log 2>&1
   echo "$K=$?" >> $O/status.txt
   python tools/ncu_summary.py $O/prof_$K.ncu-rep > $O/ncu_$K.txt 2>&1
   python tools/ncu_lines.py $O/prof_$K.ncu-rep 30 > $O/lines_$K.txt 2>&1
+done
+# c4: the split backward and the multi-view K7
+CMD4="python bench.py --config c4 --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-clocks --no-configs --no-graph"
+for K in blend_bwd preprocess_bwd_views blend_fwd; do
+  S=24; [ $K = preprocess_bwd_views ] && S=3  # one multi-view K7 per step
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$K -s $S -c 1 \
+    -o $O/prof_c4_$K -f $CMD4 > $O/ncu_c4_$K.log 2>&1
+  echo "c4_$K=$?" >> $O/status.txt
+  python tools/ncu_summary.py $O/prof_c4_$K.ncu-rep > $O/ncu_c4_$K.txt 2>&1
+  python tools/ncu_lines.py $O/prof_c4_$K.ncu-rep 30 > $O/lines_c4_$K.txt 2>&1
 done
