@@ -881,7 +881,7 @@ def run_e2e(args, sa, cam, dropin, world, barrier, torch, dist):
                 out, g = step()
             barrier()
             t0 = time.perf_counter()
-            n = max(2, min(args.steps, 5))
+            n = max(2, min(args.steps, 10))
             for _ in range(n):
                 out, g = step()
             barrier()

@@ -13,7 +13,7 @@ def main(path, which=3, label="c3"):
             rows.append((r["Kernel Name"], float(r["Metric Value"]) / 1e3))
     starts = [i for i, (k, _) in enumerate(rows) if "preprocess_fwd_kernel" in k]
     i0 = starts[which]
-    i1 = next(i for i in range(i0, len(rows)) if "preprocess_bwd_kernel" in rows[i][0])
+    i1 = next(i for i in range(i0, len(rows)) if "preprocess_bwd" in rows[i][0])
     step = rows[i0:i1 + 1]
     tot = sum(t for _, t in step)
     print(f"# ncu launch list, one {label} fwd+bwd step (bench.py --steps 2 --warmup 3), B200")

@@ -13,7 +13,7 @@ for CFG in c3 c4 c5; do
   timeout 600 $CMD > $O/plain_$CFG.log 2>&1 || { echo "plain $CFG failed" >> $O/status.txt; continue; }
   N=150; W=3
   # c4: a step is 8 views (K1-K7a each) and one multi-view K7
-  if [ $CFG = c4 ]; then N=900; W=24; fi
+  if [ $CFG = c4 ]; then N=1500; W=24; fi
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c $N --csv \
     --log-file $O/launches_$CFG.csv $CMD > $O/ncu_list_$CFG.log 2>&1
   python tools/launch_list.py $O/launches_$CFG.csv $W $CFG > $O/launch_list_$CFG.txt 2>&1
@@ -38,3 +38,5 @@ for K in blend_bwd preprocess_bwd_views blend_fwd; do
   python tools/ncu_summary.py $O/prof_c4_$K.ncu-rep > $O/ncu_c4_$K.txt 2>&1
   python tools/ncu_lines.py $O/prof_c4_$K.ncu-rep 30 > $O/lines_c4_$K.txt 2>&1
 done
+# the reports are large (gpurun copies back at most 64 MiB): keep the summaries only
+rm -f $O/*.ncu-rep $O/launches_*.csv
