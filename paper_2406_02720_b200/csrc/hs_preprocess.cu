@@ -56,7 +56,7 @@ struct FwdState {
   bool bad;
   double v00, v10, v11;
   double nnorm, nu[3];
-  double hc[3], hr[3];
+  double hw[3], hc[3], hr[3];
   double y[3], ynorm;
   double nray[3];
   double a1, a2, c1, c2, za, zb;
@@ -347,19 +347,12 @@ struct StagedView {
 // kReplay (K7): the primitive is known visible and K1's discrete decisions --
 // the identity-whitening fallback and the blend mode -- are taken from its
 // record flags, so a K7 build with different rounding cannot branch otherwise.
-template <int DEG, bool kReplay = false, typename Src>
-__device__ __forceinline__ void forward_state(const Src& src, const CamArgs& cam, int kernel,
-                                              FwdState& st, uint32_t flags = 0) {
-  constexpr int K = (DEG + 1) * (DEG + 1);
-  const double m0 = src.mu(0), m1 = src.mu(1), m2 = src.mu(2);
-  // t_all = mu @ rot.T + translation (rasterizer.py:170)
-  {
-    const double mv[3] = {m0, m1, m2};
-    double tt[3];
-    matvec_blas(cam.R, mv, tt);
-    for (int a = 0; a < 3; ++a) st.t[a] = tt[a] + cam.tr[a];
-  }
-  st.in_front = st.t[2] > cam.near_clip;
+// The camera-independent part of the forward state (rasterizer.py:174-179, 241-244,
+// 256-258): quaternion, rotation, scales, covariance, unit normal, cov . n, the two
+// opacities.  A batch of views computes it once per primitive
+// (preprocess_fwd_views_kernel); the arithmetic is the same either way.
+template <bool kReplay = false, typename Src>
+__device__ __forceinline__ void indep_state(const Src& src, FwdState& st) {
   // covariance build (rasterizer.py:174-179)
   double q[4];
   for (int k = 0; k < 4; ++k) q[k] = src.rot(k);
@@ -395,6 +388,41 @@ __device__ __forceinline__ void forward_state(const Src& src, const CamArgs& cam
     for (int d = 0; d < 3; ++d)
       st.cov[3 * a + d] = fma(M[3 * a + 2], M[3 * d + 2],
                               fma(M[3 * a + 1], M[3 * d + 1], M[3 * a] * M[3 * d]));
+  double nrm[3];
+  for (int k = 0; k < 3; ++k) nrm[k] = src.nrm(k);
+  st.nnorm = sqrt(nrm[0] * nrm[0] + nrm[1] * nrm[1] + nrm[2] * nrm[2]);
+  if constexpr (kReplay) {
+    const double rn = 1.0 / st.nnorm;
+    for (int k = 0; k < 3; ++k) st.nu[k] = nrm[k] * rn;
+  } else {
+    for (int k = 0; k < 3; ++k) st.nu[k] = nrm[k] / st.nnorm;
+  }
+  matvec_einsum(st.cov, st.nu, st.hw);
+  if constexpr (kReplay) {
+    // K7 only needs alpha (1 - alpha) for the logits' gradients: FP32 is ample
+    st.a1 = sigmoid_f32((float)src.ra());
+    st.a2 = sigmoid_f32((float)src.rb());
+  } else {
+    st.a1 = sigmoid_ref(src.ra());
+    st.a2 = sigmoid_ref(src.rb());
+  }
+}
+
+// The per-view part: camera-space mean, projection, conic, radius, rect, whitening,
+// ray-space normal, mode, erf coefficients, SH colour (rasterizer.py:170, 183-285).
+// Needs indep_state's fields.
+template <int DEG, bool kReplay = false, typename Src>
+__device__ __forceinline__ void view_state(const Src& src, const CamArgs& cam, int kernel,
+                                           FwdState& st, uint32_t flags = 0) {
+  constexpr int K = (DEG + 1) * (DEG + 1);
+  // t_all = mu @ rot.T + translation (rasterizer.py:170)
+  {
+    const double mv[3] = {src.mu(0), src.mu(1), src.mu(2)};
+    double tt[3];
+    matvec_blas(cam.R, mv, tt);
+    for (int a = 0; a < 3; ++a) st.t[a] = tt[a] + cam.tr[a];
+  }
+  st.in_front = st.t[2] > cam.near_clip;
   st.visible = false;
   if (!kReplay && !st.in_front) return;
   // cov_cam, Jacobian, ray covariance (rasterizer.py:183-185; geometry.py:189-207)
@@ -467,19 +495,8 @@ __device__ __forceinline__ void forward_state(const Src& src, const CamArgs& cam
   st.v00 = 1.0 / st.L[0];  // rasterizer.py:236-238
   st.v11 = 1.0 / st.L[4];
   st.v10 = -st.L[3] * st.v00 * st.v11;
-  // ray-space splitting normal (rasterizer.py:241-254)
-  double nrm[3];
-  for (int k = 0; k < 3; ++k) nrm[k] = src.nrm(k);
-  st.nnorm = sqrt(nrm[0] * nrm[0] + nrm[1] * nrm[1] + nrm[2] * nrm[2]);
-  if constexpr (kReplay) {
-    const double rn = 1.0 / st.nnorm;
-    for (int k = 0; k < 3; ++k) st.nu[k] = nrm[k] * rn;
-  } else {
-    for (int k = 0; k < 3; ++k) st.nu[k] = nrm[k] / st.nnorm;
-  }
-  double hw[3];
-  matvec_einsum(st.cov, st.nu, hw);
-  matvec_blas(cam.R, hw, st.hc);
+  // ray-space splitting normal (rasterizer.py:241-254); hw = cov nu from indep_state
+  matvec_blas(cam.R, st.hw, st.hc);
   matvec_einsum(st.J, st.hc, st.hr);
   st.y[0] = st.hr[0] * st.v00;
   st.y[1] = (st.hr[1] - st.L[3] * st.y[0]) / st.L[4];
@@ -495,15 +512,7 @@ __device__ __forceinline__ void forward_state(const Src& src, const CamArgs& cam
   } else {
     for (int k = 0; k < 3; ++k) st.nray[k] = st.y[k] / st.ynorm;
   }
-  // opacities, blend mode, erf coefficients (rasterizer.py:256-277)
-  if constexpr (kReplay) {
-    // K7 only needs alpha (1 - alpha) for the logits' gradients: FP32 is ample
-    st.a1 = sigmoid_f32((float)src.ra());
-    st.a2 = sigmoid_f32((float)src.rb());
-  } else {
-    st.a1 = sigmoid_ref(src.ra());
-    st.a2 = sigmoid_ref(src.rb());
-  }
+  // blend mode, erf coefficients (rasterizer.py:256-277; the opacities from indep_state)
   st.c1 = 0.5 * (st.a1 + st.a2);
   if (kernel == 1) {
     st.c2 = 0.0;
@@ -525,7 +534,8 @@ __device__ __forceinline__ void forward_state(const Src& src, const CamArgs& cam
     st.zb = st.nray[1] * st.v11;
   }
   // view-dependent colour (rasterizer.py:280-285)
-  double vv[3] = {m0 - cam.center[0], m1 - cam.center[1], m2 - cam.center[2]};
+  double vv[3] = {src.mu(0) - cam.center[0], src.mu(1) - cam.center[1],
+                  src.mu(2) - cam.center[2]};
   st.vdist = sqrt(vv[0] * vv[0] + vv[1] * vv[1] + vv[2] * vv[2]);
   if constexpr (kReplay) {
     const double rv = 1.0 / st.vdist;
@@ -544,6 +554,13 @@ __device__ __forceinline__ void forward_state(const Src& src, const CamArgs& cam
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch) st.rgbu[ch] = acc[ch] + 0.5;
   }
+}
+
+template <int DEG, bool kReplay = false, typename Src>
+__device__ __forceinline__ void forward_state(const Src& src, const CamArgs& cam, int kernel,
+                                              FwdState& st, uint32_t flags = 0) {
+  indep_state<kReplay>(src, st);
+  view_state<DEG, kReplay>(src, cam, kernel, st, flags);
 }
 
 #ifndef HS_GEOMETRY_BWD_TU
