@@ -388,8 +388,11 @@ def config_run(cfg, args, world, rank, fp32_peak, torch, dist, barrier):
     timer = device.StageTimer()
     marks = []
 
-    vbatch = (ViewBatch(scene, len(views), rast) if multi and len(views) > 1 and
-              os.environ.get("HS_VIEW_BATCH", "1") == "1" else None)
+    # HS_VIEWS_K1=0: K1 view by view inside the batch (one shared workspace)
+    vbatch = (ViewBatch(scene, len(views), rast,
+                        shared_k1=os.environ.get("HS_VIEWS_K1", "1") == "1")
+              if multi and len(views) > 1 and os.environ.get("HS_VIEW_BATCH", "1") == "1"
+              else None)
 
     def step(t=None):
         if vbatch is not None:
@@ -417,7 +420,9 @@ def config_run(cfg, args, world, rank, fp32_peak, torch, dist, barrier):
     graph_ms = None
     if world == 1 and not args.no_graph:
         try:
-            graph = device.CapturedStep(step, rast.slots, warmup=1)
+            graph = device.CapturedStep(
+                step, list(rast.slots) + (vbatch.workspaces if vbatch is not None else []),
+                warmup=1)
             barrier()
             start.record()
             for _ in range(steps):
@@ -549,8 +554,9 @@ def main():
 
     # a batch of views (c4): K5/K6 per view, then one geometry backward for the whole
     # batch (multiview.ViewBatch); HS_VIEW_BATCH=0 runs K7 per view instead
-    vbatch = (ViewBatch(scene, len(views), rast) if multi and len(views) > 1 and
-              os.environ.get("HS_VIEW_BATCH", "1") == "1" else None)
+    vbatch = (ViewBatch(scene, len(views), rast, shared_k1=False)
+              if multi and len(views) > 1 and os.environ.get("HS_VIEW_BATCH", "1") == "1"
+              else None)
 
     def backward_views(renderer, t=None):
         """Every owned view: render, cotangent, backward; the batch gradient summed

@@ -137,6 +137,15 @@ size_t hs_binning_workspace_size(int64_t n, int64_t num_pairs, int32_t width,
 int hs_preprocess_fwd(hs_frame* frame, const hs_scene* scene,
                       const hs_camera* cam, int32_t* radii, void* stream);
 
+/* hs_preprocess_fwd for a batch of views of one scene (rasterizer.py:159-298 per
+ * camera): frames[v] (each with its own workspaces) gets view cams[v].  One K1
+ * pass stages each Gaussian once and computes its camera-independent state
+ * (rotation, covariance, normal, opacities) once for all the views; every output
+ * is bit-identical to hs_preprocess_fwd's.  radii may be NULL, or hold NULL
+ * entries. */
+int hs_preprocess_fwd_views(hs_frame* const* frames, int32_t n_views, const hs_scene* scene,
+                            const hs_camera* cams, int32_t* const* radii, void* stream);
+
 /* Synchronises `stream` and reads P (the number of (tile, splat) pairs).  The
  * depth ranks of hs_preprocess_fwd come from a 32-bit sort plus a per-run fixup;
  * when a depth bucket was too long for the fixup this call redoes them with the

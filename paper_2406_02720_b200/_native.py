@@ -114,6 +114,8 @@ _SIGNATURES = {
     "hs_binning_workspace_size": (c_size_t, [c_int64, c_int64, c_int32, c_int32]),
     "hs_preprocess_fwd": (c_int32, [ctypes.POINTER(HsFrame), ctypes.POINTER(HsScene),
                                     ctypes.POINTER(HsCamera), c_void_p, c_void_p]),
+    "hs_preprocess_fwd_views": (c_int32, [c_void_p, c_int32, ctypes.POINTER(HsScene),
+                                          ctypes.POINTER(HsCamera), c_void_p, c_void_p]),
     "hs_frame_read_num_pairs": (c_int32, [ctypes.POINTER(HsFrame), c_void_p]),
     "hs_read_pairs_and_bin": (c_int32, [ctypes.POINTER(HsFrame), c_void_p]),
     "hs_bin_and_sort": (c_int32, [ctypes.POINTER(HsFrame), c_void_p]),

@@ -322,6 +322,11 @@ static int check_scene(const hs_scene* s, const hs_frame* f) {
 
 using namespace hs;
 
+static int reset_depth_range(const hs_frame* frame, const FrameBufs& f, uint32_t** range,
+                             cudaStream_t stream);
+static int rank_and_count(hs_frame* frame, const FrameBufs& f, const uint32_t* range,
+                          cudaStream_t stream);
+
 extern "C" {
 
 int32_t hs_abi_version(void) { return 2; }
@@ -398,14 +403,8 @@ int hs_preprocess_fwd(hs_frame* frame, const hs_scene* scene, const hs_camera* c
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
   FrameBufs f = frame_bufs(frame);
   const CamArgs ca = cam_args(cam);
-  // the 24-bit rank sort's depth range: [min, max] of the visible upper words
-  uint32_t* range = frame->depth_sort_full
-                        ? nullptr
-                        : reinterpret_cast<uint32_t*>(f.counters + kDepthRangeSlot);
-  if (range) {
-    HS_CUDA(cudaMemsetAsync(range, 0xff, sizeof(uint32_t), stream));
-    HS_CUDA(cudaMemsetAsync(range + 1, 0, sizeof(uint32_t), stream));
-  }
+  uint32_t* range = nullptr;
+  if ((st = reset_depth_range(frame, f, &range, stream))) return st;
   if (scene->dtype == HS_DTYPE_F32) {
     HS_CUDA(launch_preprocess_fwd_t<float>(scene_args<float>(scene), ca, frame->kernel, frame->n,
                                            f.rec, f.side, f.rect, f.count, f.dkey_in, f.dval,
@@ -415,6 +414,67 @@ int hs_preprocess_fwd(hs_frame* frame, const hs_scene* scene, const hs_camera* c
                                             frame->n, f.rec, f.side, f.rect, f.count, f.dkey_in,
                                             f.dval, radii, range, stream));
   }
+  return rank_and_count(frame, f, range, stream);
+}
+
+int hs_preprocess_fwd_views(hs_frame* const* frames, int32_t n_views, const hs_scene* scene,
+                            const hs_camera* cams, int32_t* const* radii, void* stream_) {
+  if (!frames || n_views <= 0 || !cams) return HS_ERR_INVALID_ARG;
+  for (int v = 0; v < n_views; ++v) {
+    hs_frame* fr = frames[v];
+    int st = check_frame_ws(fr);
+    if (st) return st;
+    if ((st = check_scene(scene, fr))) return st;
+    if (cams[v].width != fr->width || cams[v].height != fr->height ||
+        fr->kernel != frames[0]->kernel)
+      return HS_ERR_INVALID_ARG;
+  }
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  std::vector<uint32_t*> ranges((size_t)n_views, nullptr);
+  for (int v0 = 0; v0 < n_views; v0 += kMaxViews) {
+    FwdViewsArgs va;
+    va.n_views = n_views - v0 < kMaxViews ? n_views - v0 : kMaxViews;
+    for (int k = 0; k < va.n_views; ++k) {
+      hs_frame* fr = frames[v0 + k];
+      FrameBufs f = frame_bufs(fr);
+      int st = reset_depth_range(fr, f, &ranges[(size_t)(v0 + k)], stream);
+      if (st) return st;
+      va.cam[k] = cam_args(&cams[v0 + k]);
+      va.out[k] = FwdOut{f.rec, f.side, f.rect, f.count, f.dkey_in, f.dval,
+                         radii ? radii[v0 + k] : nullptr, ranges[(size_t)(v0 + k)]};
+    }
+    if (scene->dtype == HS_DTYPE_F32)
+      HS_CUDA(launch_preprocess_fwd_views_t<float>(scene_args<float>(scene), va,
+                                                   frames[0]->kernel, scene->n, stream));
+    else
+      HS_CUDA(launch_preprocess_fwd_views_t<double>(scene_args<double>(scene), va,
+                                                    frames[0]->kernel, scene->n, stream));
+  }
+  for (int v = 0; v < n_views; ++v) {
+    const int st = rank_and_count(frames[v], frame_bufs(frames[v]), ranges[(size_t)v], stream);
+    if (st) return st;
+  }
+  return HS_OK;
+}
+
+}  // extern "C"
+
+// the 24-bit rank sort's depth range: [min, max] of the visible upper words (none
+// when the frame ranks with the full 64-bit sort)
+static int reset_depth_range(const hs_frame* frame, const FrameBufs& f, uint32_t** range,
+                             cudaStream_t stream) {
+  *range = frame->depth_sort_full ? nullptr
+                                  : reinterpret_cast<uint32_t*>(f.counters + kDepthRangeSlot);
+  if (*range) {
+    HS_CUDA(cudaMemsetAsync(*range, 0xff, sizeof(uint32_t), stream));
+    HS_CUDA(cudaMemsetAsync(*range + 1, 0, sizeof(uint32_t), stream));
+  }
+  return HS_OK;
+}
+
+// after K1: the depth ranks and the count scan
+static int rank_and_count(hs_frame* frame, const FrameBufs& f, const uint32_t* range,
+                          cudaStream_t stream) {
   if (frame->depth_sort_full) {
     HS_CUDA(cudaMemsetAsync(f.counters + kDepthOverflowSlot, 0, sizeof(int), stream));
     HS_CUDA(run_depth_sort(f.temp, f.temp_bytes, f.dkey_in, f.dkey_out, f.dval, f.order,
@@ -429,6 +489,8 @@ int hs_preprocess_fwd(hs_frame* frame, const hs_scene* scene, const hs_camera* c
   frame->num_pairs = -1;
   return HS_OK;
 }
+
+extern "C" {
 
 // P (int64, it cannot wrap) and the flags, with a host synchronisation.
 static int read_status(hs_frame* frame, const FrameBufs& f, int64_t* p, int32_t* flags,

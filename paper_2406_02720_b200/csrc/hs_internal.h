@@ -59,8 +59,27 @@ cudaError_t launch_preprocess_bwd_t(const SceneArgs<T>& sc, const CamArgs& cam, 
                                     const int32_t* last_rank, const float* rows, float4* merged,
                                     int64_t num_pairs, const GradArgs<T>& out,
                                     cudaStream_t stream);
-// the multi-view K7: views in groups of kMaxViews per launch
+// the multi-view K7 (and K1): views in groups of kMaxViews per launch
 constexpr int kMaxViews = 8;
+// K1's per-view outputs
+struct FwdOut {
+  float4* rec;
+  SteepRec* side;
+  int4* rect;
+  int32_t* count;
+  uint64_t* dkey;
+  uint32_t* dval;
+  int32_t* radii;
+  uint32_t* range;  // the visible depths' upper-word range, or nullptr
+};
+struct FwdViewsArgs {
+  CamArgs cam[kMaxViews];
+  FwdOut out[kMaxViews];
+  int n_views;
+};
+template <typename T>
+cudaError_t launch_preprocess_fwd_views_t(const SceneArgs<T>& sc, const FwdViewsArgs& va,
+                                          int kernel, int64_t n, cudaStream_t stream);
 struct ViewsArgs {
   CamArgs cam[kMaxViews];
   const float4* merged[kMaxViews];

@@ -564,34 +564,18 @@ __device__ __forceinline__ void forward_state(const Src& src, const CamArgs& cam
 }
 
 #ifndef HS_GEOMETRY_BWD_TU
-// ---------------------------------------------------------------------------
-// K1: preprocess forward.  Writes the 64-B record, tile rect, pair count and
-// the depth-rank sort key of each primitive (culled: count 0, key ~0).
-template <typename T, int DEG, int NT>
-#ifndef HS_K1_MINB
-#define HS_K1_MINB 5  // resident CTAs per SM to cap registers for (0: no cap): 96 registers,
-                      // 20 warps/SM; 0.289 -> 0.274 ms with the ranks at c3
-#endif
-#if HS_K1_MINB > 0
-#define HS_K1_BOUNDS __launch_bounds__(NT, HS_K1_MINB)
-#else
-#define HS_K1_BOUNDS __launch_bounds__(NT)
-#endif
-__global__ void HS_K1_BOUNDS preprocess_fwd_kernel(
-    SceneArgs<T> sc, CamArgs cam, int kernel, int64_t n, float4* __restrict__ rec,
-    SteepRec* __restrict__ side, int4* __restrict__ rect, int32_t* __restrict__ count,
-    uint64_t* __restrict__ dkey, uint32_t* __restrict__ dval, int32_t* __restrict__ radii,
-    uint32_t* __restrict__ depth_range) {
-  constexpr int K = (DEG + 1) * (DEG + 1);
-  __shared__ Staged<T, K, NT> sm;
-  const int64_t base = (int64_t)blockIdx.x * NT;
-  const int cnt = (int)(n - base < NT ? n - base : NT);
-  stage_in(sm, sc, base, cnt);
-  const int t = threadIdx.x;
-  if (t >= cnt) return;
-  const int64_t i = base + t;
-  FwdState st;
-  forward_state<DEG>(StagedView<T, K, NT>{sm, t}, cam, kernel, st);
+// K1's outputs for one primitive of one view: the 64-B record, side record, tile
+// rect, pair count, depth-rank sort key and value, radius; culled: count 0, key ~0.
+__device__ __forceinline__ void write_fwd_outputs(const FwdState& st, int64_t i,
+                                                  const FwdOut& o) {
+  float4* __restrict__ rec = o.rec;
+  SteepRec* __restrict__ side = o.side;
+  int4* __restrict__ rect = o.rect;
+  int32_t* __restrict__ count = o.count;
+  uint64_t* __restrict__ dkey = o.dkey;
+  uint32_t* __restrict__ dval = o.dval;
+  int32_t* __restrict__ radii = o.radii;
+  uint32_t* __restrict__ depth_range = o.range;
   if (!st.visible) {
     dval[i] = (uint32_t)i;
     count[i] = 0;
@@ -640,6 +624,86 @@ __global__ void HS_K1_BOUNDS preprocess_fwd_kernel(
   dst[1] = r1;
   dst[2] = r2;
   dst[3] = r3;
+}
+
+// ---------------------------------------------------------------------------
+// K1: preprocess forward.  Writes the 64-B record, tile rect, pair count and
+// the depth-rank sort key of each primitive (culled: count 0, key ~0).
+template <typename T, int DEG, int NT>
+#ifndef HS_K1_MINB
+#define HS_K1_MINB 5  // resident CTAs per SM to cap registers for (0: no cap): 96 registers,
+                      // 20 warps/SM; 0.289 -> 0.274 ms with the ranks at c3
+#endif
+#if HS_K1_MINB > 0
+#define HS_K1_BOUNDS __launch_bounds__(NT, HS_K1_MINB)
+#else
+#define HS_K1_BOUNDS __launch_bounds__(NT)
+#endif
+__global__ void HS_K1_BOUNDS preprocess_fwd_kernel(
+    SceneArgs<T> sc, CamArgs cam, int kernel, int64_t n, float4* __restrict__ rec,
+    SteepRec* __restrict__ side, int4* __restrict__ rect, int32_t* __restrict__ count,
+    uint64_t* __restrict__ dkey, uint32_t* __restrict__ dval, int32_t* __restrict__ radii,
+    uint32_t* __restrict__ depth_range) {
+  constexpr int K = (DEG + 1) * (DEG + 1);
+  __shared__ Staged<T, K, NT> sm;
+  const int64_t base = (int64_t)blockIdx.x * NT;
+  const int cnt = (int)(n - base < NT ? n - base : NT);
+  stage_in(sm, sc, base, cnt);
+  const int t = threadIdx.x;
+  if (t >= cnt) return;
+  const int64_t i = base + t;
+  FwdState st;
+  forward_state<DEG>(StagedView<T, K, NT>{sm, t}, cam, kernel, st);
+  write_fwd_outputs(st, i, FwdOut{rec, side, rect, count, dkey, dval, radii, depth_range});
+}
+
+// K1 for a batch of views of one scene (multiview.ViewBatch): a CTA stages its
+// primitives once and computes their camera-independent state once (indep_state:
+// quaternion, rotation, scales, covariance, unit normal, cov . n, opacities, ~30%
+// of K1's FP64 work), keeps it in shared memory, then runs every view's projection
+// (view_state) and writes each view's outputs.  Same arithmetic as K1, so the
+// outputs are bit-identical.
+template <typename T, int NT>
+struct IndepStage {
+  double cov[9][NT], hw[3][NT], a1[NT], a2[NT];
+};
+#ifndef HS_K1V_MINB
+#define HS_K1V_MINB 4
+#endif
+template <typename T, int DEG, int NT>
+__global__ void __launch_bounds__(NT, HS_K1V_MINB) preprocess_fwd_views_kernel(
+    SceneArgs<T> sc, FwdViewsArgs va, int kernel, int64_t n) {
+  constexpr int K = (DEG + 1) * (DEG + 1);
+  __shared__ Staged<T, K, NT> sm;
+  __shared__ IndepStage<T, NT> ind;
+  const int64_t base = (int64_t)blockIdx.x * NT;
+  const int cnt = (int)(n - base < NT ? n - base : NT);
+  stage_in(sm, sc, base, cnt);
+  const int t = threadIdx.x;
+  if (t >= cnt) return;
+  const int64_t i = base + t;
+  const StagedView<T, K, NT> src{sm, t};
+  {
+    FwdState st;
+    indep_state(src, st);
+#pragma unroll
+    for (int k = 0; k < 9; ++k) ind.cov[k][t] = st.cov[k];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) ind.hw[k][t] = st.hw[k];
+    ind.a1[t] = st.a1;
+    ind.a2[t] = st.a2;
+  }
+  for (int v = 0; v < va.n_views; ++v) {
+    FwdState st;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) st.cov[k] = ind.cov[k][t];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) st.hw[k] = ind.hw[k][t];
+    st.a1 = ind.a1[t];
+    st.a2 = ind.a2[t];
+    view_state<DEG>(src, va.cam[v], kernel, st);
+    write_fwd_outputs(st, i, va.out[v]);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1421,6 +1485,30 @@ cudaError_t launch_preprocess_fwd_t(const SceneArgs<T>& sc, const CamArgs& cam, 
   note_launch();
   return cudaGetLastError();
 }
+
+template <typename T>
+cudaError_t launch_preprocess_fwd_views_t(const SceneArgs<T>& sc, const FwdViewsArgs& va,
+                                          int kernel, int64_t n, cudaStream_t stream) {
+  constexpr int NT = sizeof(T) == 4 ? 128 : 64;
+  const int64_t grid = (n + NT - 1) / NT;
+  switch (sc.deg) {
+#define HS_K1V(D)                                                                              \
+  case D:                                                                                      \
+    preprocess_fwd_views_kernel<T, D, NT><<<(unsigned)grid, NT, 0, stream>>>(sc, va, kernel, n); \
+    break;
+    HS_K1V(0) HS_K1V(1) HS_K1V(2) HS_K1V(3)
+#undef HS_K1V
+    default: return cudaErrorInvalidValue;
+  }
+  note_launch();
+  return cudaGetLastError();
+}
+template cudaError_t launch_preprocess_fwd_views_t<float>(const SceneArgs<float>&,
+                                                          const FwdViewsArgs&, int, int64_t,
+                                                          cudaStream_t);
+template cudaError_t launch_preprocess_fwd_views_t<double>(const SceneArgs<double>&,
+                                                           const FwdViewsArgs&, int, int64_t,
+                                                           cudaStream_t);
 
 template cudaError_t launch_preprocess_fwd_t<float>(const SceneArgs<float>&, const CamArgs&, int,
                                                     int64_t, float4*, SteepRec*, int4*, int32_t*,

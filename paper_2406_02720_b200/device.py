@@ -326,6 +326,47 @@ def prepare(scene, cam, kernel="half", timer=None, ws=None):
         st = lib.hs_preprocess_fwd(ctypes.byref(frame.st), ctypes.byref(sc), ctypes.byref(cs),
                                    _ptr(frame.radii), s)
     _native.check(st, "hs_preprocess_fwd")
+    return _bin(frame, ws, timer)
+
+
+def prepare_views(scene, cams, kernel="half", timer=None, workspaces=None):
+    """prepare() for a batch of views of one scene with ONE K1 pass
+    (hs_preprocess_fwd_views): each Gaussian is staged once and its
+    camera-independent state (rotation, covariance, normal, opacities) computed once
+    for all the views.  `workspaces`: one Workspace per view (distinct, since the
+    frames live together).  Returns the binned frames, as prepare() does per view."""
+    timer = timer or _NO_TIMER
+    scene = Scene.from_any(scene)
+    cams = [CameraModel.from_any(c) for c in cams]
+    if workspaces is None:
+        workspaces = [None] * len(cams)
+    if len(workspaces) != len(cams) or not cams:
+        raise ValueError("one workspace per view is required")
+    real = [ws for ws in workspaces if ws is not None]
+    if len({id(ws) for ws in real}) != len(real):
+        raise ValueError("the views of one batch need distinct workspaces")
+    for cam in cams:
+        _validate(scene, cam, kernel)
+    for ws in real:
+        if not ws.capturing:
+            ws.check_previous()
+    frames = [DeviceFrame(scene, cam, kernel, ws) for cam, ws in zip(cams, workspaces)]
+    lib = frames[0].lib
+    n = len(frames)
+    ptrs = (ctypes.c_void_p * n)(*[ctypes.addressof(f.st) for f in frames])
+    radii = (ctypes.c_void_p * n)(*[f.radii.data_ptr() for f in frames])
+    cs = (_native.HsCamera * n)(*[camera_struct(c) for c in cams])
+    sc = scene_struct(scene)
+    with timer.span("preprocess_fwd"):
+        st = lib.hs_preprocess_fwd_views(ptrs, n, ctypes.byref(sc), cs, radii, _stream())
+    _native.check(st, "hs_preprocess_fwd_views")
+    return [_bin(f, ws, timer) for f, ws in zip(frames, workspaces)]
+
+
+def _bin(frame, ws, timer):
+    """The binning of a preprocessed frame (prepare's second half)."""
+    lib = frame.lib
+    s = _stream()
     if frame.reuse_binning() > 0:
         # the workspace has a pair capacity from an earlier view: bin with P on the
         # device (no host round trip); the status is copied back behind the binning

@@ -226,22 +226,36 @@ class ViewBatch:
     buffer written once per batch instead of read-modify-written per view; the sum
     is the same, in the same order."""
 
-    def __init__(self, scene, n_views, rast=None):
+    def __init__(self, scene, n_views, rast=None, shared_k1=True):
         from . import device
         self.rast = rast if rast is not None else device.Rasterizer(scene.device)
         self.merged = [torch.empty((len(scene), device.MERGED_ROW_FLOATS),
                                    dtype=torch.float32, device=scene.device)
                        for _ in range(n_views)]
+        # shared_k1: the views' K1 as one pass (device.prepare_views), each view in
+        # its own workspace; else view by view through `rast`
+        self.workspaces = ([device.Workspace(scene.device) for _ in range(n_views)]
+                           if shared_k1 else [])
 
     def run(self, scene, cams, d_colors, view_ids, grads, timer=None, reduce_ptrs=None,
             buckets=None, on_bucket=None):
         from . import device
         if len(view_ids) > len(self.merged):
             raise ValueError(f"{len(view_ids)} views for a batch of {len(self.merged)}")
-        for j, v in enumerate(view_ids):
-            r = self.rast.render(scene, cams[v], timer=timer)
-            device.blend_backward_rows(scene, cams[v], r, d_colors[v], self.merged[j],
-                                       timer=timer)
+        if self.workspaces:
+            wss = self.workspaces[:len(view_ids)]
+            frames = device.prepare_views(scene, [cams[v] for v in view_ids], self.rast.kernel,
+                                          timer=timer, workspaces=wss)
+            for j, v in enumerate(view_ids):
+                r = device.render(scene, cams[v], self.rast.kernel, frame=frames[j], timer=timer,
+                                  ws=wss[j])
+                device.blend_backward_rows(scene, cams[v], r, d_colors[v], self.merged[j],
+                                           timer=timer)
+        else:
+            for j, v in enumerate(view_ids):
+                r = self.rast.render(scene, cams[v], timer=timer)
+                device.blend_backward_rows(scene, cams[v], r, d_colors[v], self.merged[j],
+                                           timer=timer)
         return device.geometry_backward_views(
             scene, [cams[v] for v in view_ids], self.merged[:len(view_ids)], grads=grads,
             kernel=self.rast.kernel, timer=timer, reduce_ptrs=reduce_ptrs, buckets=buckets,

@@ -3,6 +3,7 @@ multiview.ViewBatch): one pass over the scene for a batch of views must give the
 same gradients, bit for bit, as K7 per view accumulating in view order
 (GradientSet.add, rasterizer.py:100-105)."""
 
+import numpy as np
 import pytest
 import torch
 
@@ -20,6 +21,22 @@ def _setup(n, deg, views, dtype, seed=5, w=96, h=80):
     dcs = [torch.as_tensor(scenes.cotangent(h, w, seed=10 + v), dtype=torch.float32,
                            device="cuda") for v in range(views)]
     return sc, cams, dcs
+
+
+def test_prepare_views_equals_prepare(cuda):
+    """One K1 pass for several views (hs_preprocess_fwd_views): every frame's
+    integers, packed columns and radii equal prepare()'s, bit for bit."""
+    sc, cams, _ = _setup(4000, 3, 5, torch.float32, seed=12)
+    wss = [device.Workspace("cuda") for _ in range(5)]
+    frames = device.prepare_views(sc, cams, workspaces=wss)
+    for v, fr in enumerate(frames):
+        ref = device.prepare(sc, cams[v])
+        got, exp = fr.export(), ref.export()
+        for k in exp:
+            assert np.array_equal(np.asarray(got[k]), np.asarray(exp[k])), (v, k)
+        assert torch.equal(fr.radii, ref.radii), v
+    with pytest.raises(ValueError):
+        device.prepare_views(sc, cams[:2], workspaces=[wss[0], wss[0]])
 
 
 def _per_view(sc, cams, dcs, ids, kernel="half"):
@@ -66,11 +83,13 @@ def test_view_batch_more_views_than_one_launch(cuda):
         assert _same(getattr(ref, name), getattr(got, name)), name
 
 
-def test_view_batch_full_kernel_and_subset(cuda):
+@pytest.mark.parametrize("shared_k1", [True, False])
+def test_view_batch_full_kernel_and_subset(cuda, shared_k1):
     sc, cams, dcs = _setup(3000, 1, 5, torch.float32, seed=7)
     ids = [4, 1, 3]
     ref = _per_view(sc, cams, dcs, ids, kernel="full")
-    vb = multiview.ViewBatch(sc, 5, rast=device.Rasterizer("cuda", kernel="full"))
+    vb = multiview.ViewBatch(sc, 5, rast=device.Rasterizer("cuda", kernel="full"),
+                             shared_k1=shared_k1)
     got = multiview.batch_gradients(sc, cams, dcs, ids, batch=vb)
     for name in device.DeviceGradientSet.NAMES:
         assert _same(getattr(ref, name), getattr(got, name)), name
