@@ -78,6 +78,7 @@ struct WarpStage {
   float4 rec[2][kBatch][4];
   SteepRec side[2][kBatch];
   int win[2][kBatch];  // strip window code of each staged splat in the current tile
+  int org[2][kBatch];  // K6: each staged splat's pair-row origin
 };
 
 // Gather the records of `count` (<= 32) pairs, pair j at sorted index
@@ -91,6 +92,13 @@ __device__ __forceinline__ uint32_t batch_index(const BlendGeom& g, int k0, int 
                                                 PosFn pos, int lane) {
   return lane < count ? g.pair_src[k0 + pos(lane)] : 0u;
 }
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem));
+}
+
+// ORG (K6): also the splat's pair-row origin
+template <bool ORG = false>
 __device__ __forceinline__ void issue_records(const BlendGeom& g, uint32_t v, int count,
                                               WarpStage& st, int stage, int lane) {
   if (lane < count) {
@@ -98,6 +106,7 @@ __device__ __forceinline__ void issue_records(const BlendGeom& g, uint32_t v, in
     const float4* src = g.rec + 4 * (size_t)idx;
 #pragma unroll
     for (int c = 0; c < 4; ++c) cp_async16(&st.rec[stage][lane][c], src + c);
+    if (ORG) cp_async4(&st.org[stage][lane], g.row_origin + idx);
     if (v & kSteepBit) {
       const char* s = reinterpret_cast<const char*>(g.side + idx);
       char* d = reinterpret_cast<char*>(&st.side[stage][lane]);
@@ -1007,13 +1016,14 @@ __global__ void HS_BWD_BOUNDS blend_bwd_kernel(
       const int hi = batch_hi(b);
       return batch_index(g, k0, min(kBatch, hi - lo + 1), [hi](int j) { return hi - j; }, lane);
     };
-    issue_records(g, bwd_index(0), min(kBatch, len), st, 0, lane);
+    issue_records<!kRowsBySortedPos>(g, bwd_index(0), min(kBatch, len), st, 0, lane);
     uint32_t vnext = kBatch < len ? bwd_index(1) : 0u;
     for (int b = 0; b * kBatch < len; ++b) {
       const int hi = batch_hi(b);
       const int nb = min(kBatch, hi - lo + 1);
       if ((b + 1) * kBatch < len) {
-        issue_records(g, vnext, min(kBatch, batch_hi(b + 1) - lo + 1), st, (b + 1) & 1, lane);
+        issue_records<!kRowsBySortedPos>(g, vnext, min(kBatch, batch_hi(b + 1) - lo + 1), st,
+                                         (b + 1) & 1, lane);
         if ((b + 2) * kBatch < len) vnext = bwd_index(b + 2);
       } else {
         cp_async_commit();
@@ -1029,8 +1039,7 @@ __global__ void HS_BWD_BOUNDS blend_bwd_kernel(
         // the pair's generation-order row in this tile, once per splat instead of per lane
         if (!kRowsBySortedPos) {
           const int spans_x = (int)(fl >> kFlagSpanShift);
-          st.rec[s][lane][3].z =
-              __int_as_float((int)__float_as_uint(st.rec[s][lane][3].z) + ty * spans_x + tx);
+          st.rec[s][lane][3].z = __int_as_float(st.org[s][lane] + ty * spans_x + tx);
         }
       }
       __syncwarp();

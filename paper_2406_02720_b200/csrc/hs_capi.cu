@@ -78,6 +78,7 @@ struct FrameBufs {
   int32_t* order_fwd;   // longest-first tile orders of K5 / K6
   int32_t* order_bwd;
   int32_t* tile_work;   // K5 -> K6: per-tile largest terminal count
+  int32_t* row_origin;  // binning -> K6 / K7a: each splat's pair-row origin
   int* queue_fwd;       // the blends' unit queues (kQueueInts each)
   int* queue_bwd;
   BinStatusDev* status;
@@ -147,6 +148,7 @@ static FrameBufs carve_frame(void* ws, int64_t n, int tiles_x, int tiles_y, size
   f.order_fwd = c.take<int32_t>(n_tiles);
   f.order_bwd = c.take<int32_t>(n_tiles);
   f.tile_work = c.take<int32_t>(n_tiles);
+  f.row_origin = c.take<int32_t>(n);
   f.queue_fwd = c.take<int>(kQueueInts);
   f.queue_bwd = c.take<int>(kQueueInts);
   f.status = reinterpret_cast<BinStatusDev*>(f.counters ? f.counters + kBinStatusSlot : nullptr);
@@ -568,7 +570,7 @@ static int row_bin(hs_frame* frame, const FrameBufs& f, const BinBufs& b, cudaSt
   a.order = f.order;
   a.rect = f.rect;
   a.rect_r = f.rect_r;
-  a.rec = f.rec;
+  a.row_origin = f.row_origin;
   a.cnt_r = f.cnt_r;
   a.off_r = f.off_r;
   a.status = f.status;
@@ -602,7 +604,8 @@ int hs_bin_and_sort(hs_frame* frame, void* stream_) {
   const int64_t p = frame->num_pairs;
   int sel = 0;
   if (p > 0) {
-    HS_CUDA(run_duplicate(f.order, f.cnt_r, f.off_r, f.rect, f.rec, frame->tiles_x, b.keys[0],
+    HS_CUDA(run_duplicate(f.order, f.cnt_r, f.off_r, f.rect, f.row_origin, frame->tiles_x,
+                          b.keys[0],
                           b.vals[0], frame->n, stream));
     HS_CUDA(run_pair_sort(b.temp, b.temp_bytes, b.keys[0], b.keys[1], b.vals[0], b.vals[1], p,
                           frame->tile_bits, &sel, stream));
@@ -674,6 +677,7 @@ static BlendGeom frame_geom(const hs_frame* frame, const FrameBufs& f, const Bin
   g.tile_starts = f.tile_starts;
   g.pair_src = sorted_pairs(frame, b);
   g.rec = f.rec;
+  g.row_origin = f.row_origin;
   g.side = f.side;
   g.width = frame->width;
   g.height = frame->height;
@@ -776,12 +780,14 @@ int hs_preprocess_bwd_range(hs_frame* frame, const hs_scene* scene, const hs_cam
   const CamArgs ca = cam_args(cam);
   if (scene->dtype == HS_DTYPE_F32) {
     HS_CUDA(launch_preprocess_bwd_t<float>(scene_args<float>(scene), ca, frame->kernel, frame->n,
-                                           frame->tiles_x, f.rec, f.rect, f.count, f.rank_of,
+                                           frame->tiles_x, f.rec, f.row_origin, f.rect, f.count,
+                                           f.rank_of,
                                            f.last_rank, b.rows, f.merged, pairs_hint(frame),
                                            ranged(grad_args<float>(grads), begin, end), stream));
   } else {
     HS_CUDA(launch_preprocess_bwd_t<double>(scene_args<double>(scene), ca, frame->kernel,
-                                            frame->n, frame->tiles_x, f.rec, f.rect, f.count,
+                                            frame->n, frame->tiles_x, f.rec, f.row_origin, f.rect,
+                                            f.count,
                                             f.rank_of, f.last_rank, b.rows, f.merged,
                                             pairs_hint(frame),
                                             ranged(grad_args<double>(grads), begin, end),
@@ -797,7 +803,8 @@ int hs_merge_rows(hs_frame* frame, float* merged_out, void* stream_) {
   if (!merged_out || ((uintptr_t)merged_out & 15)) return HS_ERR_INVALID_ARG;
   FrameBufs f = frame_bufs(frame);
   BinBufs b = frame_bin(frame);
-  HS_CUDA(launch_merge_rows(frame->n, frame->tiles_x, f.rec, f.rect, f.count, f.rank_of,
+  HS_CUDA(launch_merge_rows(frame->n, frame->tiles_x, f.rec, f.row_origin, f.rect, f.count,
+                            f.rank_of,
                             f.last_rank, b.rows, reinterpret_cast<float4*>(merged_out),
                             pairs_hint(frame), static_cast<cudaStream_t>(stream_)));
   return HS_OK;
@@ -990,6 +997,7 @@ int seam1_upload(Seam1Dev& d, const double* packed, const int8_t* mode,
   g.tile_starts = (const int32_t*)d.ts.p;
   g.pair_src = (const uint32_t*)d.pairs.p;
   g.rec = (const float4*)d.rec.p;
+  g.row_origin = nullptr;
   g.side = (const SteepRec*)d.side.p;
   g.width = width;
   g.height = height;

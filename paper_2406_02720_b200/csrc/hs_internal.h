@@ -54,7 +54,8 @@ cudaError_t launch_preprocess_fwd_t(const SceneArgs<T>& sc, const CamArgs& cam, 
                                     int32_t* radii, uint32_t* depth_range, cudaStream_t stream);
 template <typename T>
 cudaError_t launch_preprocess_bwd_t(const SceneArgs<T>& sc, const CamArgs& cam, int kernel,
-                                    int64_t n, int tiles_x, const float4* rec, const int4* rect,
+                                    int64_t n, int tiles_x, const float4* rec,
+                                    const int32_t* row_origin, const int4* rect,
                                     const int32_t* count, const uint32_t* rank_of,
                                     const int32_t* last_rank, const float* rows, float4* merged,
                                     int64_t num_pairs, const GradArgs<T>& out,
@@ -89,7 +90,8 @@ template <typename T>
 cudaError_t launch_preprocess_bwd_views_t(const SceneArgs<T>& sc, const CamArgs* cams,
                                           const float4* const* merged, int n_views, int kernel,
                                           int64_t n, const GradArgs<T>& out, cudaStream_t stream);
-cudaError_t launch_merge_rows(int64_t n, int tiles_x, const float4* rec, const int4* rect,
+cudaError_t launch_merge_rows(int64_t n, int tiles_x, const float4* rec,
+                              const int32_t* row_origin, const int4* rect,
                               const int32_t* count, const uint32_t* rank_of,
                               const int32_t* last_rank, const float* rows, float4* merged,
                               int64_t num_pairs, cudaStream_t stream);
@@ -103,6 +105,7 @@ struct BlendGeom {
   const int32_t* tile_starts;  // (n_tiles+1) CSR offsets into pair_src
   const uint32_t* pair_src;    // sorted pair -> record index
   const float4* rec;           // 4 float4 per record
+  const int32_t* row_origin;   // K6: each splat's pair-row origin (nullptr: Seam 1 rows)
   const SteepRec* side;        // FP64 side records of steep splats (flag: bit 31 of pair_src)
   int width, height, tiles_x;
   int tile_lo, n_work;         // tiles [tile_lo, tile_lo + n_work)
@@ -230,7 +233,7 @@ struct RowBinArgs {
   const uint32_t* order;
   const int4* rect;
   const int4* rect_r;    // rects in depth-rank order (the count pass writes them)
-  float4* rec;
+  int32_t* row_origin;   // [n] each splat's pair-row origin (K6, K7a)
   const int32_t* cnt_r;
   const int32_t* off_r;
   BinStatusDev* status;
@@ -248,7 +251,7 @@ struct RowBinArgs {
 // emit + column passes (4 launches); no host synchronisation
 cudaError_t run_row_binning(const RowBinArgs& a, cudaStream_t stream);
 cudaError_t run_duplicate(const uint32_t* order, const int32_t* cnt_r, const int32_t* off_r,
-                          const int4* rect, float4* rec, int tiles_x, uint32_t* keys,
+                          const int4* rect, int32_t* row_origin, int tiles_x, uint32_t* keys,
                           uint32_t* vals, int64_t n, cudaStream_t stream);
 // returns selector (0/1) of the buffer holding the sorted result
 cudaError_t run_pair_sort(void* temp, size_t temp_bytes, uint32_t* keys0, uint32_t* keys1,

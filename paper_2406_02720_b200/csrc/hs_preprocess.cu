@@ -786,7 +786,8 @@ template cudaError_t launch_screen_splats_t<double>(const SceneArgs<double>&, co
 // picks G from the frame's mean rows per primitive (HS_K7A_WIDE_ROWS).
 template <int G>
 __global__ void __launch_bounds__(256) merge_rows_kernel(
-    int64_t n, int tiles_x, const float4* __restrict__ rec, const int4* __restrict__ rect,
+    int64_t n, int tiles_x, const float4* __restrict__ rec,
+    const int32_t* __restrict__ row_origin, const int4* __restrict__ rect,
     const int32_t* __restrict__ count, const uint32_t* __restrict__ rank_of,
     const int32_t* __restrict__ last_rank, const float* __restrict__ rows,
     float4* __restrict__ merged, int64_t begin, int mark) {
@@ -820,7 +821,7 @@ __global__ void __launch_bounds__(256) merge_rows_kernel(
     spans_x = rc.y - rc.x + 1;
     r2 = rec[4 * i + 2];
     r3 = rec[4 * i + 3];
-    base = __float_as_int(r3.z) + rc.z * spans_x + rc.x;
+    base = row_origin[i] + rc.z * spans_x + rc.x;
     r = (int)rank_of[i];
   }
   // row l of the splat is tile (rc.z + l / spans_x, rc.x + l % spans_x); the
@@ -1521,7 +1522,8 @@ template cudaError_t launch_preprocess_fwd_t<double>(const SceneArgs<double>&, c
 #else
 template <typename T>
 cudaError_t launch_preprocess_bwd_t(const SceneArgs<T>& sc, const CamArgs& cam, int kernel,
-                                    int64_t n, int tiles_x, const float4* rec, const int4* rect,
+                                    int64_t n, int tiles_x, const float4* rec,
+                                    const int32_t* row_origin, const int4* rect,
                                     const int32_t* count, const uint32_t* rank_of,
                                     const int32_t* last_rank, const float* rows, float4* merged,
                                     int64_t num_pairs, const GradArgs<T>& out,
@@ -1537,10 +1539,12 @@ cudaError_t launch_preprocess_bwd_t(const SceneArgs<T>& sc, const CamArgs& cam, 
 #endif
   if (num_pairs >= (int64_t)HS_K7A_WIDE_ROWS * n)
     merge_rows_kernel<8><<<(unsigned)((cnt * 8 + 255) / 256), 256, 0, stream>>>(
-        end, tiles_x, rec, rect, count, rank_of, last_rank, rows, merged, out.begin, 0);
+        end, tiles_x, rec, row_origin, rect, count, rank_of, last_rank, rows, merged, out.begin,
+        0);
   else
     merge_rows_kernel<1><<<(unsigned)((cnt + 255) / 256), 256, 0, stream>>>(
-        end, tiles_x, rec, rect, count, rank_of, last_rank, rows, merged, out.begin, 0);
+        end, tiles_x, rec, row_origin, rect, count, rank_of, last_rank, rows, merged, out.begin,
+        0);
   note_launch();
 #ifndef HS_K7_NT_F32
 #define HS_K7_NT_F32 128
@@ -1720,27 +1724,30 @@ template cudaError_t launch_preprocess_bwd_views_t<double>(const SceneArgs<doubl
                                                            const GradArgs<double>&, cudaStream_t);
 
 // K7a alone into a caller buffer with culled markers (hs_merge_rows)
-cudaError_t launch_merge_rows(int64_t n, int tiles_x, const float4* rec, const int4* rect,
+cudaError_t launch_merge_rows(int64_t n, int tiles_x, const float4* rec,
+                              const int32_t* row_origin, const int4* rect,
                               const int32_t* count, const uint32_t* rank_of,
                               const int32_t* last_rank, const float* rows, float4* merged,
                               int64_t num_pairs, cudaStream_t stream) {
   if (num_pairs >= (int64_t)HS_K7A_WIDE_ROWS * n)
     merge_rows_kernel<8><<<(unsigned)((n * 8 + 255) / 256), 256, 0, stream>>>(
-        n, tiles_x, rec, rect, count, rank_of, last_rank, rows, merged, 0, 1);
+        n, tiles_x, rec, row_origin, rect, count, rank_of, last_rank, rows, merged, 0, 1);
   else
     merge_rows_kernel<1><<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(
-        n, tiles_x, rec, rect, count, rank_of, last_rank, rows, merged, 0, 1);
+        n, tiles_x, rec, row_origin, rect, count, rank_of, last_rank, rows, merged, 0, 1);
   note_launch();
   return cudaGetLastError();
 }
 
 template cudaError_t launch_preprocess_bwd_t<float>(const SceneArgs<float>&, const CamArgs&, int,
-                                                    int64_t, int, const float4*, const int4*,
+                                                    int64_t, int, const float4*, const int32_t*,
+                                                    const int4*,
                                                     const int32_t*, const uint32_t*, const int32_t*,
                                                     const float*, float4*, int64_t,
                                                     const GradArgs<float>&, cudaStream_t);
 template cudaError_t launch_preprocess_bwd_t<double>(const SceneArgs<double>&, const CamArgs&, int,
-                                                     int64_t, int, const float4*, const int4*,
+                                                     int64_t, int, const float4*, const int32_t*,
+                                                     const int4*,
                                                      const int32_t*, const uint32_t*,
                                                      const int32_t*, const float*, float4*,
                                                      int64_t, const GradArgs<double>&,
