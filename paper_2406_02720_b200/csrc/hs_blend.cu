@@ -905,6 +905,9 @@ __global__ void HS_BWD_BOUNDS blend_bwd_kernel(
     const uint32_t* __restrict__ rank_of) {
   constexpr int kStride = kRowsBySortedPos ? 12 : kRowFloats;
   constexpr int kCols = kRowsBySortedPos ? 12 : 13;
+  // generation-order rows are stored whole (columns 13-15 zero): a row's second
+  // 32-B sector written in part would cost a read-modify-write in DRAM
+  constexpr int kStoreCols = kRowsBySortedPos ? kCols : kStride;
   __shared__ WarpStage stage_all[kBwdWarps];
   __shared__ int cnt_all[kBwdWarps][kPx][32];
   __shared__ float tfin_all[kBwdWarps][kPx][32], dini_all[kBwdWarps][kPx][32];
@@ -1074,7 +1077,7 @@ __global__ void HS_BWD_BOUNDS blend_bwd_kernel(
         const int key = st.win[s][j] & (~3 | (pos < hmax_lo ? 1 : 0) | (pos < hmax_hi ? 2 : 0));
         if (key == 0 || key == 4) {
           // fast splat below 2^-27 on every live strip: a zero pair row, no reduction
-          if (!(lane & 1) && vi < kCols) row_store(rows + row * kStride + vi, 0.f);
+          if (!(lane & 1) && vi < kStoreCols) row_store(rows + row * kStride + vi, 0.f);
           continue;
         }
         switch (key) {
@@ -1108,7 +1111,7 @@ __global__ void HS_BWD_BOUNDS blend_bwd_kernel(
         v[13] = v[14] = v[15] = 0.f;
         const float total = HS_SMEM_REDUCE ? warp_reduce13_smem(v, red, lane)
                                            : warp_transpose_reduce16(v, lane);
-        if (!(lane & 1) && vi < kCols) row_store(rows + row * kStride + vi, total);
+        if (!(lane & 1) && vi < kStoreCols) row_store(rows + row * kStride + vi, total);
       }
       __syncwarp();
     }
