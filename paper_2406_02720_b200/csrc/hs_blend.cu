@@ -159,11 +159,6 @@ __device__ __forceinline__ int next_unit(const BlendGeom& g, int n_units, int& p
   return __shfl_sync(0xffffffffu, t, 0);
 }
 
-__device__ __forceinline__ int next_tile(const BlendGeom& g, int& phase, int lane) {
-  const int t = next_unit(g, g.n_work, phase, lane);
-  if (t < 0) return -1;
-  return g.tile_order ? g.tile_order[t] : g.tile_lo + t;
-}
 
 // Per-(splat, lane) constants shared by the forward and backward pixel loops.
 struct SplatLane {
