@@ -554,19 +554,34 @@ def main():
 
     # a batch of views (c4): K5/K6 per view, then one geometry backward for the whole
     # batch (multiview.ViewBatch); HS_VIEW_BATCH=0 runs K7 per view instead
-    vbatch = (ViewBatch(scene, len(views), rast, shared_k1=False)
+    # (HS_VIEWS_K1=0: K1 view by view inside the batch)
+    vbatch = (ViewBatch(scene, len(views), rast,
+                        shared_k1=os.environ.get("HS_VIEWS_K1", "1") == "1")
               if multi and len(views) > 1 and os.environ.get("HS_VIEW_BATCH", "1") == "1"
               else None)
 
+    def render_view(v, t, frame=None, ws=None):
+        if frame is None:
+            return rast.render(scene, cams[v], timer=t)
+        return device.render(scene, cams[v], rast.kernel, frame=frame, timer=t, ws=ws)
+
     def backward_views(renderer, t=None):
         """Every owned view: render, cotangent, backward; the batch gradient summed
-        over views and ranks.  Returns the last view's output."""
+        over views and ranks.  Returns the last view's output.  renderer(v, t, frame,
+        ws) -> (output, cotangent); with a ViewBatch the frames come from one
+        multi-view K1."""
         out = None
         if fused is not None:
             fused.begin()
         if vbatch is not None:
+            if vbatch.workspaces:
+                wss = vbatch.workspaces[:len(views)]
+                frames = device.prepare_views(scene, [cams[v] for v in views], rast.kernel,
+                                              timer=t, workspaces=wss)
+            else:
+                wss = frames = [None] * len(views)
             for j, v in enumerate(views):
-                out, d = renderer(v, t)
+                out, d = renderer(v, t, frames[j], wss[j])
                 device.blend_backward_rows(scene, cams[v], out, d, vbatch.merged[j], timer=t)
             device.geometry_backward_views(
                 scene, [cams[v] for v in views], vbatch.merged[:len(views)], grads=grads,
@@ -578,7 +593,7 @@ def main():
         else:
             views_done = views
         for j, v in enumerate(views_done):
-            out, d = renderer(v, t)
+            out, d = renderer(v, t, None, None)
             if fused is not None:
                 rast.render_backward(scene, cams[v], out, d, grads=grads, timer=t,
                                      reduce_ptrs=fused.ptrs)
@@ -599,8 +614,7 @@ def main():
         return out
 
     def step(t=None):
-        return backward_views(lambda v, tt: (rast.render(scene, cams[v], timer=tt), d_colors[v]),
-                              t)
+        return backward_views(lambda v, tt, fr, ws: (render_view(v, tt, fr, ws), d_colors[v]), t)
 
     def fwd_step():
         for v in views:
@@ -627,7 +641,9 @@ def main():
     graph, graph_note = None, "eager"
     if world == 1 and fused is None and not args.no_graph:
         try:
-            graph = device.CapturedStep(step, rast.slots, warmup=1)
+            graph = device.CapturedStep(
+                step, list(rast.slots) + (vbatch.workspaces if vbatch is not None else []),
+                warmup=1)
             graph_note = "cuda graph of the whole step, replayed"
         except Exception as e:  # report and fall back to eager launches
             graph_note = f"eager (graph capture failed: {e!r})"[:300]
@@ -665,7 +681,9 @@ def main():
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms = float(ms_t.item())
-    stage_ms = {k: statistics.mean(v) for k, v in timer.totals().items()}
+    # per view (a batch's multi-view K1 / K7 is one span for all its views)
+    stage_ms = {k: sum(v) / (args.steps * max(1, len(views)))
+                for k, v in timer.totals().items()}
 
     # forward-only frames/s (prepare + render), same timing discipline
     for _ in range(3):
@@ -756,8 +774,8 @@ def main():
     dstats = T.DensifyStats.zeros(len(scene))
 
     def train_step(t=None):
-        def render_and_loss(v, _):
-            o = rast.render(scene, cams[v])
+        def render_and_loss(v, _, fr, ws):
+            o = render_view(v, None, fr, ws)
             with (t.span("loss") if t is not None else contextlib.nullcontext()):
                 _, d = dloss(o.color, targets[v])
             return o, d
