@@ -11,7 +11,7 @@ def main(path, which=3, label="c3"):
     for r in csv.DictReader(lines):
         if r.get("Metric Name") == "gpu__time_duration.sum":
             rows.append((r["Kernel Name"], float(r["Metric Value"]) / 1e3))
-    starts = [i for i, (k, _) in enumerate(rows) if "preprocess_fwd_kernel" in k]
+    starts = [i for i, (k, _) in enumerate(rows) if "preprocess_fwd" in k]
     i0 = starts[which]
     i1 = next(i for i in range(i0, len(rows)) if "preprocess_bwd" in rows[i][0])
     step = rows[i0:i1 + 1]

@@ -14,7 +14,7 @@ d = collections.OrderedDict()
 for r in csv.DictReader(rows):
     d.setdefault((r["ID"], r["Kernel Name"][:60]), {})[r["Metric Name"]] = r["Metric Value"]
 items = list(d.items())
-starts = [i for i, (k, _) in enumerate(items) if "preprocess_fwd_kernel" in k[1]]
+starts = [i for i, (k, _) in enumerate(items) if "preprocess_fwd" in k[1]]
 for (_, name), m in items[starts[which]:starts[which] + count]:
     t = float(m.get("gpu__time_duration.sum", 0)) / 1e3
     rd = float(m.get("dram__bytes_read.sum", 0)) / 1e6

@@ -13,7 +13,7 @@ for CFG in c3 c4 c5; do
   timeout 600 $CMD > $O/plain_$CFG.log 2>&1 || { echo "plain $CFG failed" >> $O/status.txt; continue; }
   N=150; W=3
   # c4: a step is 8 views (K1-K7a each) and one multi-view K7
-  if [ $CFG = c4 ]; then N=1500; W=24; fi
+  if [ $CFG = c4 ]; then N=1500; W=3; fi
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c $N --csv \
     --log-file $O/launches_$CFG.csv $CMD > $O/ncu_list_$CFG.log 2>&1
   python tools/launch_list.py $O/launches_$CFG.csv $W $CFG > $O/launch_list_$CFG.txt 2>&1
