@@ -437,13 +437,24 @@ def config_run(cfg, args, world, rank, fp32_peak, torch, dist, barrier):
     barrier()
     start.record()
     for _ in range(steps):
-        step(timer)
+        step()
     end.record()
     barrier()
     ms = start.elapsed_time(end) / steps
     eager_ms = ms
     if graph_ms is not None:
         ms = graph_ms
+    # per-stage times from the same steps with the views serialised (a batch's views
+    # run on two streams, and concurrent views would overlap the stage brackets)
+    overlap = bool(vbatch is not None and vbatch.streams)
+    saved_streams = vbatch.streams if vbatch is not None else None
+    if vbatch is not None:
+        vbatch.streams = []
+    for _ in range(steps):
+        step(timer)
+    barrier()
+    if vbatch is not None:
+        vbatch.streams = saved_streams
     exposed = statistics.mean(a.elapsed_time(b) for a, b in marks) if marks else 0.0
     t = torch.tensor([ms, exposed], device="cuda")
     if world > 1:
@@ -463,6 +474,9 @@ def config_run(cfg, args, world, rank, fp32_peak, torch, dist, barrier):
     rec = {"value": n_views * 1e3 / ms, "unit": "views/s" if multi else "iters/s",
            "ms_per_step": ms, "eager_ms_per_step": eager_ms,
            "launch_mode": "cuda graph" if graph_ms is not None else "eager",
+           "views_overlapped": ("K5-K7a of consecutive views on two streams; stage times "
+                                "and fractions from the same steps serialised"
+                                if overlap else None),
            "steps": steps, "views_per_step": n_views,
            "views_this_rank": len(views), "stage_ms_per_view": per_view,
            "blend_fwd_frac": fwd_e * FWD_FLOPS_PER_EVAL / (k5 * 1e-3) / 1e12 / fp32_peak
@@ -574,15 +588,28 @@ def main():
         if fused is not None:
             fused.begin()
         if vbatch is not None:
+            streams = vbatch.streams
             if vbatch.workspaces:
                 wss = vbatch.workspaces[:len(views)]
                 frames = device.prepare_views(scene, [cams[v] for v in views], rast.kernel,
-                                              timer=t, workspaces=wss)
+                                              timer=t, workspaces=wss, bin=not streams)
             else:
                 wss = frames = [None] * len(views)
+            main_stream = torch.cuda.current_stream()
+            if streams:  # consecutive views on alternating streams (multiview.ViewBatch)
+                ready = torch.cuda.Event()
+                ready.record(main_stream)
+                for st in streams:
+                    st.wait_event(ready)
             for j, v in enumerate(views):
-                out, d = renderer(v, t, frames[j], wss[j])
-                device.blend_backward_rows(scene, cams[v], out, d, vbatch.merged[j], timer=t)
+                with (torch.cuda.stream(streams[j % len(streams)]) if streams
+                      else contextlib.nullcontext()):
+                    fr = device.bin_frame(frames[j], wss[j], t) if streams else frames[j]
+                    out, d = renderer(v, t, fr, wss[j])
+                    device.blend_backward_rows(scene, cams[v], out, d, vbatch.merged[j],
+                                               timer=t)
+            for st in streams:
+                main_stream.wait_stream(st)
             device.geometry_backward_views(
                 scene, [cams[v] for v in views], vbatch.merged[:len(views)], grads=grads,
                 kernel=rast.kernel, timer=t,
@@ -669,14 +696,23 @@ def main():
     eager_ms = None
     if graph is not None:
         graph.check()  # no replayed view outgrew its binning capacity
-        # the per-stage CUDA-event times come from the same steps run eagerly
+        # the per-stage CUDA-event times come from the same steps run eagerly (a
+        # batch's views serialised: concurrent views would overlap the brackets)
         barrier()
         start.record()
         for _ in range(args.steps):
-            out = step(timer)
+            out = step()
         end.record()
         barrier()
         eager_ms = start.elapsed_time(end) / args.steps
+        saved_streams = vbatch.streams if vbatch is not None else None
+        if vbatch is not None:
+            vbatch.streams = []
+        for _ in range(args.steps):
+            out = step(timer)
+        barrier()
+        if vbatch is not None:
+            vbatch.streams = saved_streams
     ms_t = torch.tensor([ms], device="cuda")
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)

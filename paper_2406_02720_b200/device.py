@@ -329,12 +329,13 @@ def prepare(scene, cam, kernel="half", timer=None, ws=None):
     return _bin(frame, ws, timer)
 
 
-def prepare_views(scene, cams, kernel="half", timer=None, workspaces=None):
+def prepare_views(scene, cams, kernel="half", timer=None, workspaces=None, bin=True):
     """prepare() for a batch of views of one scene with ONE K1 pass
     (hs_preprocess_fwd_views): each Gaussian is staged once and its
     camera-independent state (rotation, covariance, normal, opacities) computed once
     for all the views.  `workspaces`: one Workspace per view (distinct, since the
-    frames live together).  Returns the binned frames, as prepare() does per view."""
+    frames live together).  Returns the binned frames, as prepare() does per view;
+    with bin=False the frames are only preprocessed (bin each with bin_frame)."""
     timer = timer or _NO_TIMER
     scene = Scene.from_any(scene)
     cams = [CameraModel.from_any(c) for c in cams]
@@ -360,7 +361,15 @@ def prepare_views(scene, cams, kernel="half", timer=None, workspaces=None):
     with timer.span("preprocess_fwd"):
         st = lib.hs_preprocess_fwd_views(ptrs, n, ctypes.byref(sc), cs, radii, _stream())
     _native.check(st, "hs_preprocess_fwd_views")
+    if not bin:
+        return frames
     return [_bin(f, ws, timer) for f, ws in zip(frames, workspaces)]
+
+
+def bin_frame(frame, ws=None, timer=None):
+    """The binning of a frame preprocessed by prepare_views(bin=False), on the
+    current stream."""
+    return _bin(frame, ws, timer or _NO_TIMER)
 
 
 def _bin(frame, ws, timer):

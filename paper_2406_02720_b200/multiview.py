@@ -10,6 +10,8 @@ with a single NCCL all-reduce over NVLink (gloo on CPU for tests).  The sum is
 the batch gradient, Sum_v render_backward(view v).
 """
 
+import contextlib
+
 import torch
 import torch.distributed as dist
 
@@ -226,7 +228,7 @@ class ViewBatch:
     buffer written once per batch instead of read-modify-written per view; the sum
     is the same, in the same order."""
 
-    def __init__(self, scene, n_views, rast=None, shared_k1=True):
+    def __init__(self, scene, n_views, rast=None, shared_k1=True, streams=2):
         from . import device
         self.rast = rast if rast is not None else device.Rasterizer(scene.device)
         self.merged = [torch.empty((len(scene), device.MERGED_ROW_FLOATS),
@@ -236,6 +238,12 @@ class ViewBatch:
         # its own workspace; else view by view through `rast`
         self.workspaces = ([device.Workspace(scene.device) for _ in range(n_views)]
                            if shared_k1 else [])
+        # with own workspaces the views are independent after K1: binning, K5, K6 and
+        # K7a of consecutive views run on alternating streams, so one view's kernels
+        # fill the tail of the other's persistent blends
+        self.streams = ([torch.cuda.Stream(device=scene.device) for _ in range(streams)]
+                        if shared_k1 and streams > 1 and torch.device(scene.device).type == "cuda"
+                        else [])
 
     def run(self, scene, cams, d_colors, view_ids, grads, timer=None, reduce_ptrs=None,
             buckets=None, on_bucket=None):
@@ -245,12 +253,27 @@ class ViewBatch:
         if self.workspaces:
             wss = self.workspaces[:len(view_ids)]
             frames = device.prepare_views(scene, [cams[v] for v in view_ids], self.rast.kernel,
-                                          timer=timer, workspaces=wss)
+                                          timer=timer, workspaces=wss,
+                                          bin=not self.streams)
+            main = torch.cuda.current_stream() if self.streams else None
+            if main is not None:
+                ready = torch.cuda.Event()
+                ready.record(main)
+                for st in self.streams:
+                    st.wait_event(ready)
             for j, v in enumerate(view_ids):
-                r = device.render(scene, cams[v], self.rast.kernel, frame=frames[j], timer=timer,
-                                  ws=wss[j])
-                device.blend_backward_rows(scene, cams[v], r, d_colors[v], self.merged[j],
-                                           timer=timer)
+                ctx = (torch.cuda.stream(self.streams[j % len(self.streams)]) if self.streams
+                       else contextlib.nullcontext())
+                with ctx:
+                    frame = (device.bin_frame(frames[j], wss[j], timer) if self.streams
+                             else frames[j])
+                    r = device.render(scene, cams[v], self.rast.kernel, frame=frame,
+                                      timer=timer, ws=wss[j])
+                    device.blend_backward_rows(scene, cams[v], r, d_colors[v], self.merged[j],
+                                               timer=timer)
+            if main is not None:
+                for st in self.streams:
+                    main.wait_stream(st)
         else:
             for j, v in enumerate(view_ids):
                 r = self.rast.render(scene, cams[v], timer=timer)
