@@ -142,9 +142,13 @@ int hs_preprocess_fwd(hs_frame* frame, const hs_scene* scene,
  * pass stages each Gaussian once and computes its camera-independent state
  * (rotation, covariance, normal, opacities) once for all the views; every output
  * is bit-identical to hs_preprocess_fwd's.  radii may be NULL, or hold NULL
- * entries. */
+ * entries.  rank = 1: each frame's depth ranks and pair counts follow on
+ * `stream`; rank = 0: the caller runs hs_frame_rank per frame (after this call's
+ * work, e.g. on one stream per view) before binning it. */
 int hs_preprocess_fwd_views(hs_frame* const* frames, int32_t n_views, const hs_scene* scene,
-                            const hs_camera* cams, int32_t* const* radii, void* stream);
+                            const hs_camera* cams, int32_t* const* radii, int32_t rank,
+                            void* stream);
+int hs_frame_rank(hs_frame* frame, void* stream);
 
 /* Synchronises `stream` and reads P (the number of (tile, splat) pairs).  The
  * depth ranks of hs_preprocess_fwd come from a 32-bit sort plus a per-run fixup;

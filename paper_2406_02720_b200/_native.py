@@ -115,7 +115,9 @@ _SIGNATURES = {
     "hs_preprocess_fwd": (c_int32, [ctypes.POINTER(HsFrame), ctypes.POINTER(HsScene),
                                     ctypes.POINTER(HsCamera), c_void_p, c_void_p]),
     "hs_preprocess_fwd_views": (c_int32, [c_void_p, c_int32, ctypes.POINTER(HsScene),
-                                          ctypes.POINTER(HsCamera), c_void_p, c_void_p]),
+                                          ctypes.POINTER(HsCamera), c_void_p, c_int32,
+                                          c_void_p]),
+    "hs_frame_rank": (c_int32, [ctypes.POINTER(HsFrame), c_void_p]),
     "hs_frame_read_num_pairs": (c_int32, [ctypes.POINTER(HsFrame), c_void_p]),
     "hs_read_pairs_and_bin": (c_int32, [ctypes.POINTER(HsFrame), c_void_p]),
     "hs_bin_and_sort": (c_int32, [ctypes.POINTER(HsFrame), c_void_p]),

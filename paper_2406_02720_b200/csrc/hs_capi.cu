@@ -420,7 +420,8 @@ int hs_preprocess_fwd(hs_frame* frame, const hs_scene* scene, const hs_camera* c
 }
 
 int hs_preprocess_fwd_views(hs_frame* const* frames, int32_t n_views, const hs_scene* scene,
-                            const hs_camera* cams, int32_t* const* radii, void* stream_) {
+                            const hs_camera* cams, int32_t* const* radii, int32_t rank,
+                            void* stream_) {
   if (!frames || n_views <= 0 || !cams) return HS_ERR_INVALID_ARG;
   for (int v = 0; v < n_views; ++v) {
     hs_frame* fr = frames[v];
@@ -452,11 +453,23 @@ int hs_preprocess_fwd_views(hs_frame* const* frames, int32_t n_views, const hs_s
       HS_CUDA(launch_preprocess_fwd_views_t<double>(scene_args<double>(scene), va,
                                                     frames[0]->kernel, scene->n, stream));
   }
+  if (!rank) return HS_OK;  // the caller ranks each frame (hs_frame_rank), e.g. per stream
   for (int v = 0; v < n_views; ++v) {
     const int st = rank_and_count(frames[v], frame_bufs(frames[v]), ranges[(size_t)v], stream);
     if (st) return st;
   }
   return HS_OK;
+}
+
+int hs_frame_rank(hs_frame* frame, void* stream_) {
+  const int st = check_frame_ws(frame);
+  if (st) return st;
+  FrameBufs f = frame_bufs(frame);
+  return rank_and_count(
+      frame, f,
+      frame->depth_sort_full ? nullptr
+                             : reinterpret_cast<uint32_t*>(f.counters + kDepthRangeSlot),
+      static_cast<cudaStream_t>(stream_));
 }
 
 }  // extern "C"

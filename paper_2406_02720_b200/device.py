@@ -359,7 +359,8 @@ def prepare_views(scene, cams, kernel="half", timer=None, workspaces=None, bin=T
     cs = (_native.HsCamera * n)(*[camera_struct(c) for c in cams])
     sc = scene_struct(scene)
     with timer.span("preprocess_fwd"):
-        st = lib.hs_preprocess_fwd_views(ptrs, n, ctypes.byref(sc), cs, radii, _stream())
+        st = lib.hs_preprocess_fwd_views(ptrs, n, ctypes.byref(sc), cs, radii, 1 if bin else 0,
+                                         _stream())
     _native.check(st, "hs_preprocess_fwd_views")
     if not bin:
         return frames
@@ -367,9 +368,14 @@ def prepare_views(scene, cams, kernel="half", timer=None, workspaces=None, bin=T
 
 
 def bin_frame(frame, ws=None, timer=None):
-    """The binning of a frame preprocessed by prepare_views(bin=False), on the
-    current stream."""
-    return _bin(frame, ws, timer or _NO_TIMER)
+    """The depth ranks, pair counts and binning of a frame K1 left with
+    prepare_views(bin=False), on the current stream (e.g. one stream per view, after
+    an event on the K1 stream)."""
+    timer = timer or _NO_TIMER
+    with timer.span("preprocess_fwd"):
+        st = frame.lib.hs_frame_rank(ctypes.byref(frame.st), _stream())
+    _native.check(st, "hs_frame_rank")
+    return _bin(frame, ws, timer)
 
 
 def _bin(frame, ws, timer):

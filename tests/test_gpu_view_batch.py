@@ -35,6 +35,22 @@ def test_prepare_views_equals_prepare(cuda):
         for k in exp:
             assert np.array_equal(np.asarray(got[k]), np.asarray(exp[k])), (v, k)
         assert torch.equal(fr.radii, ref.radii), v
+    # K1 alone, then each frame ranked and binned on its own stream
+    streams = [torch.cuda.Stream() for _ in range(5)]
+    frames = device.prepare_views(sc, cams, workspaces=wss, bin=False)
+    ready = torch.cuda.Event()
+    ready.record()
+    binned = []
+    for v, fr in enumerate(frames):
+        streams[v].wait_event(ready)
+        with torch.cuda.stream(streams[v]):
+            binned.append(device.bin_frame(fr, wss[v]))
+    for st in streams:
+        torch.cuda.current_stream().wait_stream(st)
+    for v, fr in enumerate(binned):
+        got, exp = fr.export(), device.prepare(sc, cams[v]).export()
+        for k in exp:
+            assert np.array_equal(np.asarray(got[k]), np.asarray(exp[k])), (v, k)
     with pytest.raises(ValueError):
         device.prepare_views(sc, cams[:2], workspaces=[wss[0], wss[0]])
 
