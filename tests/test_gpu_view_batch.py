@@ -144,3 +144,30 @@ def test_view_batch_rejects_bad_rows(cuda):
         device.geometry_backward_views(sc, cams, bad)
     with pytest.raises(ValueError):
         device.geometry_backward_views(sc, cams, bad[:1])
+
+
+def test_view_batch_repeated_steps_on_streams(cuda):
+    """Steady state: the same ViewBatch run step after step (the views' workspaces
+    then bin asynchronously, each on its stream) keeps giving the per-view result,
+    also for a different subset of views and after the scene changes."""
+    sc, cams, dcs = _setup(4000, 2, 6, torch.float32, seed=14)
+    vb = multiview.ViewBatch(sc, 6)
+    assert len(vb.streams) == 6
+    ids = [0, 2, 3, 5]
+    ref = _per_view(sc, cams, dcs, ids)
+    for _ in range(3):
+        got = multiview.batch_gradients(sc, cams, dcs, ids, batch=vb)
+        torch.cuda.synchronize()
+        for name in device.DeviceGradientSet.NAMES:
+            assert _same(getattr(ref, name), getattr(got, name)), name
+    ids2 = [5, 1, 4]
+    ref2 = _per_view(sc, cams, dcs, ids2)
+    got2 = multiview.batch_gradients(sc, cams, dcs, ids2, batch=vb)
+    for name in device.DeviceGradientSet.NAMES:
+        assert _same(getattr(ref2, name), getattr(got2, name)), name
+    with torch.no_grad():
+        sc.mu.mul_(1.01)  # a new scene state: the pair counts change
+    ref3 = _per_view(sc, cams, dcs, ids)
+    got3 = multiview.batch_gradients(sc, cams, dcs, ids, batch=vb)
+    for name in device.DeviceGradientSet.NAMES:
+        assert _same(getattr(ref3, name), getattr(got3, name)), name
