@@ -22,6 +22,8 @@
 
 #include <cuda_fp16.h>
 
+#include <mutex>
+
 #include "hs_common.cuh"
 #include "hs_internal.h"
 
@@ -1305,6 +1307,9 @@ cudaError_t launch_tile_order(const int32_t* starts, const int32_t* work, int n_
 // Persistent grid: resident CTAs per SM x SMs of that kernel (queried once).
 template <typename Kernel>
 static int blend_grid(Kernel kernel, int warps, int n_work, int* cache) {
+  // (filled once per kernel; Seam 1 calls arrive from several host threads)
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
   if (*cache == 0) {
     int dev = 0, sms = 148, per_sm = 0;
     cudaGetDevice(&dev);
