@@ -384,6 +384,12 @@ def test_fused_gradient_reduce_single_rank(cuda):
         torch.cuda.synchronize()
         for name in device.DeviceGradientSet.NAMES:
             assert _same_up_to_subnormals(getattr(ref, name), getattr(got, name)), name
+        # the same reduction stores from the multi-view K7 (views on their streams)
+        got = multiview.batch_gradients(scene, cams, dcs, [0, 1, 2], fused=fused,
+                                        batch=multiview.ViewBatch(scene, 3))
+        torch.cuda.synchronize()
+        for name in device.DeviceGradientSet.NAMES:
+            assert _same_up_to_subnormals(getattr(ref, name), getattr(got, name)), name
     finally:
         dist.destroy_process_group()
 
