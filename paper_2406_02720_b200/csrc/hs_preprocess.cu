@@ -849,9 +849,10 @@ __global__ void __launch_bounds__(256) merge_rows_kernel(
   // HS_K7A_ROWS rows in flight per step: the tiles' last ranks first, then the
   // gathers of the rows below them only (rows past a tile's last composited
   // rank were never written, and at c5 they are most of them), additions in
-  // row order (bitwise the same sum)
+  // row order (the same sum).  With FP32 sums the occupancy carries the latency:
+  // one row per step (c4 0.159 -> 0.145 ms per view; 3 or 4 rows are slower)
 #ifndef HS_K7A_ROWS
-#define HS_K7A_ROWS 2
+#define HS_K7A_ROWS 1
 #endif
   constexpr int U = HS_K7A_ROWS;
   int l = sub;
