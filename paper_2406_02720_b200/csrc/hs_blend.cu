@@ -558,13 +558,13 @@ __global__ void HS_FWD_BOUNDS blend_fwd_kernel(
         if ((j & 7) == 0) {
           alive = alive_halves(P);
           if (!(any = alive != 0)) break;
-          if (CKPT && j == 0 && b > 0 && (b & (kCkpt / kBatch - 1)) == 0) {
+          if (CKPT && j == 0 && b > 0 && ((b * kBatch) & ((1 << g.ckpt_shift) - 1)) == 0) {
             // K6 segment checkpoint at list position m = b * kBatch: the state of
             // every pixel still alive before splat m (T, negated colour sums so far)
             // (scalar stores: a 16-B store would want the four values in an aligned
             // register quad, which reshuffles the packed pixel pairs all over the loop)
             float* ck = reinterpret_cast<float*>(
-                g.ckpt + ((size_t)((k0 + b * kBatch) >> kCkptShift) << kCkptShift));
+                g.ckpt + (size_t)((k0 + b * kBatch) >> g.ckpt_shift) * kCkptSlot);
 #pragma unroll
             for (int i = 0; i < NPX; ++i) {
               const int p = i >> 1, h = i & 1;
@@ -629,13 +629,14 @@ __global__ void HS_FWD_BOUNDS blend_fwd_kernel(
       for (int i = 0; i < NPX; ++i) {
         const int p = i >> 1, h = i & 1;
         const int c = (int)slot(P.C[p], h);
-        if (c < kCkpt || col >= g.width || row0 + 2 * i >= g.height) continue;
+        const int ck_len = 1 << g.ckpt_shift;
+        if (c < ck_len || col >= g.width || row0 + 2 * i >= g.height) continue;
         const float t = slot(P.T[p], h);
         const float fr = fmaf(t, bg0, -slot(P.ar[p], h)), fg = fmaf(t, bg1, -slot(P.ag[p], h)),
                     fb = fmaf(t, bg2, -slot(P.ab[p], h));
-        for (int m = kCkpt; m <= c && m < nk; m += kCkpt) {
+        for (int m = ck_len; m <= c && m < nk; m += ck_len) {
           float4* ck =
-              g.ckpt + ((size_t)((k0 + m) >> kCkptShift) << kCkptShift) + ck_pid0 + 32 * i;
+              g.ckpt + (size_t)((k0 + m) >> g.ckpt_shift) * kCkptSlot + ck_pid0 + 32 * i;
           float4 v = *ck;
           v.y = fr + v.y;
           v.z = fg + v.z;
@@ -968,10 +969,10 @@ __global__ void HS_BWD_BOUNDS blend_bwd_kernel(
     // K6 segments: this unit walks positions top-1 .. lo.  Below the tile's top
     // segment, the pixels alive at `top` start from K5's checkpoint there (T before
     // position top, S = everything blended from top on).
-    const int lo = SPLIT ? seg << kCkptShift : 0;
-    const int top = SPLIT ? min((seg + 1) << kCkptShift, maxc) : maxc;
+    const int lo = SPLIT ? seg << g.ckpt_shift : 0;
+    const int top = SPLIT ? min((seg + 1) << g.ckpt_shift, maxc) : maxc;
     if (SPLIT && top < maxc) {
-      const float4* ck = g.ckpt + ((size_t)((k0 + top) >> kCkptShift) << kCkptShift);
+      const float4* ck = g.ckpt + (size_t)((k0 + top) >> g.ckpt_shift) * kCkptSlot;
 #pragma unroll
       for (int i = 0; i < kPx; ++i) {
         const int p = i >> 1, h = i & 1;
@@ -1196,7 +1197,8 @@ __global__ void mark_steep_pairs_kernel(const uint8_t* __restrict__ steep_flag,
 // longest-first order) or natural order.  One CTA: a block scan per 1024 tiles.
 __global__ void __launch_bounds__(1024) bwd_units_kernel(const int32_t* __restrict__ work,
                                                          const int32_t* __restrict__ order,
-                                                         int n_tiles, int2* __restrict__ units,
+                                                         int n_tiles, int shift,
+                                                         int2* __restrict__ units,
                                                          int* __restrict__ n_units) {
   __shared__ int warp_tot[32];
   __shared__ int carry;
@@ -1209,7 +1211,7 @@ __global__ void __launch_bounds__(1024) bwd_units_kernel(const int32_t* __restri
     if (i < n_tiles) {
       t = order ? order[i] : i;
       const int mc = work[t];
-      ns = mc > kCkpt ? (mc + kCkpt - 1) >> kCkptShift : 1;
+      ns = mc > (1 << shift) ? (mc + (1 << shift) - 1) >> shift : 1;
     }
     int x = ns;
 #pragma unroll
@@ -1239,8 +1241,9 @@ __global__ void __launch_bounds__(1024) bwd_units_kernel(const int32_t* __restri
 }
 
 cudaError_t launch_bwd_units(const int32_t* tile_work, const int32_t* order, int n_tiles,
-                             int2* units, int* n_units, cudaStream_t stream) {
-  bwd_units_kernel<<<1, 1024, 0, stream>>>(tile_work, order, n_tiles, units, n_units);
+                             int ckpt_shift, int2* units, int* n_units, cudaStream_t stream) {
+  bwd_units_kernel<<<1, 1024, 0, stream>>>(tile_work, order, n_tiles, ckpt_shift, units,
+                                           n_units);
   note_launch();
   return cudaGetLastError();
 }

@@ -179,12 +179,28 @@ struct BinBufs {
 // c1, c2, c4; c3 has 8160 tiles -- where a few long tiles, not the total work, set
 // K6's time.  HS_K6_SPLIT=0 / 1 forces it off / on.
 constexpr int kSplitMaxTiles = 6144;
+#ifndef HS_CKPT_SMALL_TILES
+#define HS_CKPT_SMALL_TILES 1024
+#endif
 static bool bwd_split(int64_t n_tiles) {
   static const int mode = [] {
     const char* e = getenv("HS_K6_SPLIT");
     return e ? (e[0] == '0' ? 0 : 1) : 2;
   }();
   return mode == 1 || (mode == 2 && n_tiles <= kSplitMaxTiles);
+}
+
+// list positions per K6 segment (a power of two, 64 .. 256): the fewer the tiles, the
+// shorter the segments, so a frame still has several units per resident warp slot
+// (HS_CKPT_SHIFT forces the log2)
+static int ckpt_shift(int64_t n_tiles) {
+  static const int forced = [] {
+    const char* e = getenv("HS_CKPT_SHIFT");
+    const int v = e ? atoi(e) : 0;
+    return v >= kCkptMinShift && v <= 8 ? v : 0;
+  }();
+  if (forced) return forced;
+  return n_tiles <= HS_CKPT_SMALL_TILES ? kCkptMinShift : 8;
 }
 
 static BinBufs carve_bin(void* ws, int64_t p, int tiles_x, int tiles_y, size_t* total) {
@@ -208,9 +224,11 @@ static BinBufs carve_bin(void* ws, int64_t p, int tiles_x, int tiles_y, size_t* 
   b.rows = c.take<float>(pp * kRowFloats);
   const int64_t n_tiles = (int64_t)tiles_x * tiles_y;
   if (bwd_split(n_tiles)) {
-    // one checkpoint slot (kCkpt pixels) per kCkpt pairs; one unit per tile + per segment
-    b.ckpt = c.take<float4>(((pp >> kCkptShift) + 2) << kCkptShift);
-    b.units = c.take<int2>((size_t)n_tiles + (pp >> kCkptShift) + 1);
+    // one checkpoint slot (a tile's 256 pixels) per segment of pairs; one unit per
+    // tile + per segment
+    const int sh = ckpt_shift(n_tiles);
+    b.ckpt = c.take<float4>(((pp >> sh) + 2) * (size_t)kCkptSlot);
+    b.units = c.take<int2>((size_t)n_tiles + (pp >> sh) + 1);
     b.n_units = c.take<int>(1);
   }
   if (total) *total = c.off;
@@ -705,6 +723,7 @@ static BlendGeom frame_geom(const hs_frame* frame, const FrameBufs& f, const Bin
   g.ckpt = nullptr;
   g.units = nullptr;
   g.n_units = nullptr;
+  g.ckpt_shift = ckpt_shift(frame->n_tiles);
   return g;
 }
 
@@ -748,8 +767,8 @@ int hs_blend_bwd(hs_frame* frame, const double* bg, const float* d_color,
   }
   if (bwd_split(frame->n_tiles)) {
     // (tile, segment) units from K5's checkpoints, tiles in the order above
-    HS_CUDA(launch_bwd_units(f.tile_work, g.tile_order, frame->n_tiles, b.units, b.n_units,
-                             stream));
+    HS_CUDA(launch_bwd_units(f.tile_work, g.tile_order, frame->n_tiles, g.ckpt_shift, b.units,
+                             b.n_units, stream));
     g.ckpt = b.ckpt;
     g.units = b.units;
     g.n_units = b.n_units;
@@ -1025,6 +1044,7 @@ int seam1_upload(Seam1Dev& d, const double* packed, const int8_t* mode,
   g.ckpt = nullptr;
   g.units = nullptr;
   g.n_units = nullptr;
+  g.ckpt_shift = 8;
   return HS_OK;
 }
 

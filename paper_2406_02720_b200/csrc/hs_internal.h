@@ -121,11 +121,14 @@ struct BlendGeom {
   float4* ckpt;                // nullptr: off
   const int2* units;           // K6: (tile, segment) units, *n_units of them
   const int* n_units;
+  int ckpt_shift;              // log2 of the list positions per segment / checkpoint
 };
-constexpr int kCkptShift = 8;
-constexpr int kCkpt = 1 << kCkptShift;  // list positions per K6 segment / checkpoint
+// checkpoint slots hold a tile's 256 pixels; segments of 2^shift list positions,
+// shift in [kCkptMinShift, 8]
+constexpr int kCkptMinShift = 6;
+constexpr int kCkptSlot = 256;
 cudaError_t launch_bwd_units(const int32_t* tile_work, const int32_t* order, int n_tiles,
-                             int2* units, int* n_units, cudaStream_t stream);
+                             int ckpt_shift, int2* units, int* n_units, cudaStream_t stream);
 // The blends' unit queue with an SM-spread first wave: [0] dynamic counter, [1]
 // sweep counter, [2, 2 + kQueueMaxSms) per-SM slot counters, then one claim flag per
 // first-wave unit.
