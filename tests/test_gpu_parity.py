@@ -246,14 +246,17 @@ def test_wide_splat_row_merge_oracle(cuda):
     assert_grads(got, ref_g)
 
 
-@pytest.mark.parametrize("kernel", ["half", "full"])
-def test_split_backward_long_lists_oracle(cuda, kernel):
-    """Small frames run K6 as (tile, segment) units of 256 list positions, each below
-    the top starting from K5's checkpoint (hs_blend.cu "K6 segments"): a ball whose
-    tile lists run to thousands of splats, pixels alive through several segments,
-    against the oracle's gradients; K5's images and the integers are unchanged."""
+@pytest.mark.parametrize("kernel,size", [("half", (128, 96)), ("full", (128, 96)),
+                                         ("half", (528, 512))])
+def test_split_backward_long_lists_oracle(cuda, kernel, size):
+    """Small frames run K6 as (tile, segment) units, each below the top starting from
+    K5's checkpoint (hs_blend.cu "K6 segments"; segments of 64 positions at 48 tiles,
+    256 at 1056): balls whose tile lists run to thousands of splats, pixels alive
+    through several segments, against the oracle's gradients; K5's images and the
+    integers are unchanged."""
     O = _oracle()
-    sa = scenes.ball(30_000, 2, 128, 96, views=2, seed=31)
+    w, h = size
+    sa = scenes.ball(30_000 if w == 128 else 60_000, 2, w, h, views=2, seed=31)
     s64 = sa.as_float64()
     cam = CameraModel(**sa.cameras[1])
     d_color = scenes.cotangent(cam.height, cam.width, seed=7)
