@@ -258,8 +258,14 @@ struct Staged {
   // are conflict-free
   static constexpr bool DENSE = std::is_same<T, float>::value && (3 * K) % 4 == 0;
   static constexpr int SHS = DENSE ? 3 * K : 3 * K + 1;
-  T mu[NT * 3], ls[NT * 3], rot[NT * 4], nrm[NT * 3], ra[NT], rb[NT];
-  T sh[NT * SHS];
+  alignas(16) T mu[NT * 3];
+  alignas(16) T ls[NT * 3];
+  alignas(16) T rot[NT * 4];
+  alignas(16) T nrm[NT * 3];
+  alignas(16) T ra[NT];
+  alignas(16) T rb[NT];
+  alignas(16) T sh[NT * SHS];
+  uint64_t bar;  // the bulk-copy path's transaction barrier
 };
 
 // One element global -> shared without a register round trip (LDGSTS), so a
@@ -270,10 +276,70 @@ __device__ __forceinline__ void cp_async_elem(T* smem, const T* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(d), "l"(gmem), "n"(sizeof(T)));
 }
 
+// Bulk-copy staging (cp.async.bulk, the TMA engine's 1-D form): with dense SH rows
+// every field of a CTA's primitives is ONE contiguous block in global memory and in
+// shared memory, so one thread issues seven bulk copies that complete on a
+// transaction-count mbarrier, instead of every thread issuing ~30 LDGSTS.  Needs
+// 16-B aligned sources and block sizes that are multiples of 16 B (a full CTA of a
+// torch-allocated scene); other CTAs take the LDGSTS path below.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+template <typename T>
+__device__ __forceinline__ bool bulk_ok(const T* src, int64_t elems) {
+  return ((uintptr_t)src & 15) == 0 && ((elems * (int64_t)sizeof(T)) & 15) == 0;
+}
+
+__device__ __forceinline__ void bulk_wait(uint64_t* bar) {
+  asm volatile(
+      "{\n.reg .pred p;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
+      "@!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Returns whether the CTA staged with bulk copies (uniform over the CTA).  With
+// wait = false the caller completes the staging with stage_wait (then syncs).
 template <typename T, int K, int NT>
-__device__ __forceinline__ void stage_in(Staged<T, K, NT>& s, const SceneArgs<T>& sc,
+__device__ __forceinline__ bool stage_in(Staged<T, K, NT>& s, const SceneArgs<T>& sc,
                                          int64_t base, int cnt, bool wait = true) {
   const int tid = threadIdx.x;
+  if constexpr (Staged<T, K, NT>::DENSE) {
+    constexpr int R = 3 * K;
+    const bool bulk = bulk_ok(sc.mu + base * 3, cnt * 3) && bulk_ok(sc.ls + base * 3, cnt * 3) &&
+                      bulk_ok(sc.nrm + base * 3, cnt * 3) && bulk_ok(sc.rot + base * 4, cnt * 4) &&
+                      bulk_ok(sc.ra + base, cnt) && bulk_ok(sc.rb + base, cnt) &&
+                      bulk_ok(sc.sh + base * R, (int64_t)cnt * R);  // uniform over the CTA
+    if (bulk) {
+      if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&s.bar)));
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        const unsigned b3 = cnt * 3 * sizeof(T), b1 = cnt * sizeof(T);
+        const unsigned total = 3 * b3 + 4 * b1 + 2 * b1 + cnt * R * sizeof(T);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n"
+                     ::"r"(smem_u32(&s.bar)), "r"(total) : "memory");
+        bulk_g2s(s.mu, sc.mu + base * 3, b3, &s.bar);
+        bulk_g2s(s.ls, sc.ls + base * 3, b3, &s.bar);
+        bulk_g2s(s.nrm, sc.nrm + base * 3, b3, &s.bar);
+        bulk_g2s(s.rot, sc.rot + base * 4, 4 * b1, &s.bar);
+        bulk_g2s(s.ra, sc.ra + base, b1, &s.bar);
+        bulk_g2s(s.rb, sc.rb + base, b1, &s.bar);
+        bulk_g2s(s.sh, sc.sh + base * R, cnt * R * sizeof(T), &s.bar);
+      }
+      // (the barrier's init is visible to the waiting threads after this sync)
+      __syncthreads();
+      if (wait) {
+        bulk_wait(&s.bar);
+        __syncthreads();
+      }
+      return true;
+    }
+  }
   for (int e = tid; e < cnt * 3; e += NT) {
     cp_async_elem(&s.mu[e], &sc.mu[base * 3 + e]);
     cp_async_elem(&s.ls[e], &sc.ls[base * 3 + e]);
@@ -306,6 +372,16 @@ __device__ __forceinline__ void stage_in(Staged<T, K, NT>& s, const SceneArgs<T>
     asm volatile("cp.async.wait_all;\n" ::);
     __syncthreads();
   }
+  return false;
+}
+
+// Completes a stage_in(wait = false) of this thread's share (the caller syncs).
+template <typename T, int K, int NT>
+__device__ __forceinline__ void stage_wait(Staged<T, K, NT>& s, bool bulk) {
+  if (bulk)
+    bulk_wait(&s.bar);
+  else
+    asm volatile("cp.async.wait_all;\n" ::);
 }
 
 // One thread's view of its staged primitive (the inputs of forward_state).
@@ -1380,7 +1456,7 @@ __global__ void __launch_bounds__(NT, HS_K7_MINB) preprocess_bwd_kernel(
   constexpr bool acc = MODE == 1;
   constexpr bool red = MODE == 2;
   const bool mc = red && out.accumulate == 3;
-  stage_in(sm, sc, base, ncta, /*wait=*/false);
+  const bool bulk = stage_in(sm, sc, base, ncta, /*wait=*/false);
   Gs* g = acc ? reinterpret_cast<Gs*>(dyn_smem) : nullptr;
   if (acc) {
     // touch_s = visible in this view (count > 0); preprocess_bwd_one rewrites
@@ -1399,9 +1475,13 @@ __global__ void __launch_bounds__(NT, HS_K7_MINB) preprocess_bwd_kernel(
     prefetch_block<NT, 1>(g->touch, out.touch + base, ncta, touch_s, lm);
     prefetch_block<NT, 3 * K>(g->sh, out.d_sh + base * 3 * K, ncta, touch_s, lm);
     asm volatile("cp.async.commit_group;\n" ::);
-    asm volatile("cp.async.wait_group 1;\n" ::);
+    // the scene: its bulk copies, or every cp.async group but the targets'
+    if (bulk)
+      bulk_wait(&sm.bar);
+    else
+      asm volatile("cp.async.wait_group 1;\n" ::);
   } else {
-    asm volatile("cp.async.wait_all;\n" ::);
+    stage_wait(sm, bulk);
   }
   __syncthreads();
   if (t < ncta)
@@ -1604,7 +1684,7 @@ __global__ void __launch_bounds__(NT, HS_K7_MINB) preprocess_bwd_views_kernel(
   const int64_t base = out.begin + (int64_t)blockIdx.x * NT;
   const int ncta = (int)(n - base < NT ? n - base : NT);
   const int t = threadIdx.x;
-  stage_in(sm, sc, base, ncta, /*wait=*/false);
+  const bool bulk = stage_in(sm, sc, base, ncta, /*wait=*/false);
   // the accumulators start at zero, or (accumulate == 1: an earlier batch or group of
   // views already wrote) at the stored sums, so every view adds onto the running sum
   // in view order exactly as K7 per view does
@@ -1630,7 +1710,7 @@ __global__ void __launch_bounds__(NT, HS_K7_MINB) preprocess_bwd_views_kernel(
     for (int e = t; e < (int)(sizeof(Ac) / sizeof(T)); e += NT) z[e] = T(0);
     touch_s[t] = 0;
   }
-  asm volatile("cp.async.wait_all;\n" ::);
+  stage_wait(sm, bulk);
   __syncthreads();
   if (t < ncta)
     for (int v = 0; v < va.n_views; ++v)
