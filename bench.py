@@ -445,7 +445,7 @@ def config_run(cfg, args, world, rank, fp32_peak, torch, dist, barrier):
     if graph_ms is not None:
         ms = graph_ms
     # per-stage times from the same steps with the views serialised (a batch's views
-    # run on two streams, and concurrent views would overlap the stage brackets)
+    # run on concurrent streams, which would overlap the stage brackets)
     overlap = bool(vbatch is not None and vbatch.streams)
     saved_streams = vbatch.streams if vbatch is not None else None
     if vbatch is not None:
@@ -474,7 +474,7 @@ def config_run(cfg, args, world, rank, fp32_peak, torch, dist, barrier):
     rec = {"value": n_views * 1e3 / ms, "unit": "views/s" if multi else "iters/s",
            "ms_per_step": ms, "eager_ms_per_step": eager_ms,
            "launch_mode": "cuda graph" if graph_ms is not None else "eager",
-           "views_overlapped": ("K5-K7a of consecutive views on two streams; stage times "
+           "views_overlapped": ("ranks-K7a of the views on concurrent streams; stage times "
                                 "and fractions from the same steps serialised"
                                 if overlap else None),
            "steps": steps, "views_per_step": n_views,
