@@ -30,8 +30,8 @@ for K in blend_bwd blend_fwd preprocess_bwd_kernel preprocess_fwd_kernel merge_r
 done
 # c4: the split backward and the multi-view K7
 CMD4="python bench.py --config c4 --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-clocks --no-configs --no-graph"
-for K in blend_bwd preprocess_bwd_views blend_fwd; do
-  S=24; [ $K = preprocess_bwd_views ] && S=3  # one multi-view K7 per step
+for K in blend_bwd preprocess_bwd_views preprocess_fwd_views blend_fwd; do
+  S=24; case $K in preprocess_*_views) S=3;; esac  # one multi-view K1 and K7 per step
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$K -s $S -c 1 \
     -o $O/prof_c4_$K -f $CMD4 > $O/ncu_c4_$K.log 2>&1
   echo "c4_$K=$?" >> $O/status.txt
