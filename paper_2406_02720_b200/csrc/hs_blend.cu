@@ -372,33 +372,79 @@ __device__ __forceinline__ void fwd_commit(float nw, float& T, float& A, float& 
 // the side-record form.
 // Pairs [P0, P0 + NP) are evaluated; the others are outside the splat's strip
 // window and only count the commit of their alive pixels (see strip_window).
+// -w of pixel pair p (independent of the pixels' state)
+template <bool STEEP>
+__device__ __forceinline__ float2 fwd_pair_nw(const SplatLane& s, const float4 (&q)[4], int p) {
+  const float nc1 = q[1].w, nc2 = q[2].x;  // negated by prescale_record
+  const float2 dy = pair_dy(s.dy0, p);
+  const float2 g = ex2x2(ffma2(ffma2(f2(s.C), dy, f2(s.Bx)), dy, f2(s.P0)));
+  const float2 e = erf32x2(STEEP ? steep_z2(s, p) : ffma2(f2(s.zb), dy, f2(s.Z0)));
+  return fmul2(ffma2(f2(nc2), e, f2(nc1)), g);
+}
+
+// the termination test and compositing of pair p given its -w
+template <int NPX>
+__device__ __forceinline__ void fwd_pair_commit(FwdPix<NPX>& P, int p, float2 nw,
+                                                const float4 (&q)[4]) {
+  const float cr = q[2].y, cg = q[2].z, cb = q[2].w, z = q[3].x;
+  const float2 tn = ffma2(nw, P.T[p], P.T[p]);  // T * (1 - w)
+  const float2 m = fmul2(P.A[p], make_float2(ge_mask(tn.x), ge_mask(tn.y)));
+  const float2 nwm = fmul2(nw, m);
+  const float2 nwt = fmul2(nwm, P.T[p]);
+  P.ar[p] = ffma2(nwt, f2(cr), P.ar[p]);
+  P.ag[p] = ffma2(nwt, f2(cg), P.ag[p]);
+  P.ab[p] = ffma2(nwt, f2(cb), P.ab[p]);
+  P.ad[p] = ffma2(nwt, f2(z), P.ad[p]);
+  P.C[p] = fadd2(P.C[p], m);
+  P.A[p] = m;
+  P.T[p] = ffma2(nwm, P.T[p], P.T[p]);
+}
+
 template <bool STEEP, int P0, int NP, int NPX>
 __device__ __forceinline__ void fwd_splat_fast(const float4 (&q)[4], const SteepRec& side,
                                                float px, float py0, FwdPix<NPX>& P) {
   const SplatLane s = splat_lane<STEEP, true>(q, side, px, py0);
-  const float nc1 = q[1].w, nc2 = q[2].x;  // negated by prescale_record
-  const float cr = q[2].y, cg = q[2].z, cb = q[2].w, z = q[3].x;
 #pragma unroll
   for (int p = 0; p < NPX / 2; ++p) {
     if (p < P0 || p >= P0 + NP) {
       P.C[p] = fadd2(P.C[p], P.A[p]);
       continue;
     }
-    const float2 dy = pair_dy(s.dy0, p);
-    const float2 g = ex2x2(ffma2(ffma2(f2(s.C), dy, f2(s.Bx)), dy, f2(s.P0)));
-    const float2 e = erf32x2(STEEP ? steep_z2(s, p) : ffma2(f2(s.zb), dy, f2(s.Z0)));
-    const float2 nw = fmul2(ffma2(f2(nc2), e, f2(nc1)), g);  // -w
-    const float2 tn = ffma2(nw, P.T[p], P.T[p]);              // T * (1 - w)
-    const float2 m = fmul2(P.A[p], make_float2(ge_mask(tn.x), ge_mask(tn.y)));
-    const float2 nwm = fmul2(nw, m);
-    const float2 nwt = fmul2(nwm, P.T[p]);
-    P.ar[p] = ffma2(nwt, f2(cr), P.ar[p]);
-    P.ag[p] = ffma2(nwt, f2(cg), P.ag[p]);
-    P.ab[p] = ffma2(nwt, f2(cb), P.ab[p]);
-    P.ad[p] = ffma2(nwt, f2(z), P.ad[p]);
-    P.C[p] = fadd2(P.C[p], m);
-    P.A[p] = m;
-    P.T[p] = ffma2(nwm, P.T[p], P.T[p]);
+    fwd_pair_commit(P, p, fwd_pair_nw<STEEP>(s, q, p), q);
+  }
+}
+
+// N consecutive plain fast splats with the same window (pairs [P0, P0 + NPR)): every
+// weight first, then the commits in list order.  The same operations as N
+// fwd_splat_fast calls, but in one block, so the later splats' weight chains
+// (record, exponent, erf) overlap the earlier ones' -- a warp alone on its scheduler
+// (small frames, the long tails of a frame) waits out every splat's latency otherwise.
+// (Pairs outside the window only count their alive pixels; those counts are exact
+// small integers, so their order does not matter.)
+template <int N, int P0, int NPR, int NPX>
+__device__ __forceinline__ void fwd_splats_ilp(const WarpStage& st, int s, int j,
+                                               float px, float py0, FwdPix<NPX>& P) {
+  constexpr int NP = NPX / 2;
+  float2 nw[N][NPR];
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    const float4 q[4] = {st.rec[s][j + k][0], st.rec[s][j + k][1], st.rec[s][j + k][2],
+                         st.rec[s][j + k][3]};
+    const SplatLane sl = splat_lane<false, true>(q, st.side[s][j], px, py0);
+#pragma unroll
+    for (int p = 0; p < NPR; ++p) nw[k][p] = fwd_pair_nw<false>(sl, q, P0 + p);
+  }
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    const float4 q[4] = {st.rec[s][j + k][0], st.rec[s][j + k][1], st.rec[s][j + k][2],
+                         st.rec[s][j + k][3]};
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      if (p >= P0 && p < P0 + NPR)
+        fwd_pair_commit(P, p, nw[k][p - P0], q);
+      else
+        P.C[p] = fadd2(P.C[p], P.A[p]);
+    }
   }
 }
 
@@ -581,10 +627,36 @@ __global__ void HS_FWD_BOUNDS blend_fwd_kernel(
 #ifdef HS_K5_PROBE
         ++probe_splats;
 #endif
+        const int key = st.win[s][j] & (~3 | alive);  // generic keeps its window bits: 8+
+#ifndef HS_K5_TWO
+#define HS_K5_TWO 2
+#endif
+// (HS_K5_TWO8: the same on full 16x16 tiles, off: c5 K5 -3%, c3 +1.2%, c4 -0.5%)
+#ifndef HS_K5_TWO8
+#define HS_K5_TWO8 0
+#endif
+        constexpr int H = NP > 1 ? NP / 2 : NP;  // pairs per half window
+        if constexpr (HS_K5_TWO > 1 && (NPX == 2 || HS_K5_TWO8)) {
+          // two plain fast splats with the same window inside one group of 8 (same
+          // alive mask)
+          if (key >= 1 && key <= 3 && (j & 7) != 7 && j + 1 < nb &&
+              (st.win[s][j + 1] & (~3 | alive)) == key) {
+            if constexpr (NP == 1) {
+              fwd_splats_ilp<2, 0, 1>(st, s, j, px, py0, P);
+            } else {
+              if (key == 1) fwd_splats_ilp<2, 0, H>(st, s, j, px, py0, P);
+              else if (key == 2) fwd_splats_ilp<2, NP - H, H>(st, s, j, px, py0, P);
+              else fwd_splats_ilp<2, 0, NP>(st, s, j, px, py0, P);
+            }
+            ++j;
+#ifdef HS_K5_PROBE
+            ++probe_splats;
+#endif
+            continue;
+          }
+        }
         const float4 q[4] = {st.rec[s][j][0], st.rec[s][j][1], st.rec[s][j][2], st.rec[s][j][3]};
         const uint32_t flags = __float_as_uint(q[3].y);
-        const int key = st.win[s][j] & (~3 | alive);  // generic keeps its window bits: 8+
-        constexpr int H = NP > 1 ? NP / 2 : NP;  // pairs per half window
         switch (key) {
           case 1: fwd_splat_fast<false, 0, H>(q, st.side[s][j], px, py0, P); break;
           case 2: fwd_splat_fast<false, NP - H, H>(q, st.side[s][j], px, py0, P); break;
