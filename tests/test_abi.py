@@ -40,6 +40,30 @@ def test_library_is_sm100a(native_lib):
     assert "sm_100a" in res.stdout
 
 
+def _kernel_sass(native_lib, symbol_re, _dump={}):
+    """SASS of the library's functions whose mangled names match symbol_re."""
+    if "text" not in _dump:
+        _dump["text"] = subprocess.run(["cuobjdump", "-sass", _native.library_path()],
+                                       capture_output=True, text=True, check=True).stdout
+    out, keep = [], False
+    for line in _dump["text"].splitlines():
+        m = re.match(r"\s+Function : (\S+)", line)
+        if m:
+            keep = re.search(symbol_re, m.group(1)) is not None
+        elif keep:
+            out.append(line)
+    return "\n".join(out)
+
+
+def test_sass_uses_sm100_features(native_lib):
+    """The hot kernels use what DESIGN.md says they use: packed FP32 pipe
+    instructions in the blends, bulk copies on an mbarrier in K1/K7's scene staging."""
+    blends = _kernel_sass(native_lib, r"blend_(fwd|bwd)_kernel")
+    assert "FFMA2" in blends and "FMUL2" in blends
+    geom = _kernel_sass(native_lib, r"preprocess_(fwd|bwd)_kernelIfLi3E")
+    assert "UBLKCP" in geom and "SYNCS.PHASECHK" in geom
+
+
 def test_frame_init_error_codes(native_lib):
     f = _native.HsFrame()
     assert native_lib.hs_frame_init(ctypes.byref(f), 0, 64, 64, 0) == _native.HS_ERR_EMPTY_SCENE
