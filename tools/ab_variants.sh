@@ -1,3 +1,7 @@
+#!/bin/bash
+# On the GPU box: the main library against variants built with tools/build_variant.sh,
+# twice each, on some configs (plus a parity subset first).
+#   VARS="name1 name2" CFGS="c3 c4" bash tools/ab_variants.sh
 L=paper_2406_02720_b200/lib
 python -m pytest tests -q -m gpu -x -k "parity or golden or split or windows or multiview or view_batch" 2>&1 | tail -2
 cp $L/libhalfsplat_b200.so $L/main.so
